@@ -1,0 +1,854 @@
+// SPDX-License-Identifier: MIT
+// CP-ALS kernels (solve.hpp:62-262) and Kruskal-model kernels
+// (kruskal.hpp:52-220). The MTTKRP itself is a streamed `sketch` pass over
+// the tensor against a materialized Khatri-Rao panel (kr_panel); the R x R
+// algebra of one mode update (Gram Hadamard, pinv_psd, normalization, Gram,
+// fit, stopping test) runs in one CTA so a whole ALS iteration is a handful
+// of launches with no host round trip; each launch first checks the
+// device-side `done` flag so the host can enqueue iterations ahead.
+#include <cfloat>
+
+#include "als.cuh"
+#include "rng.cuh"
+#include "runtime.cuh"
+
+namespace rcpg {
+
+namespace {
+
+constexpr int kSmallThreads = 1024;
+
+struct ShapeArg {
+  i64 e[kMaxOrder];
+  int n;
+};
+
+ShapeArg make_shape(const i64* shape, int order) {
+  ShapeArg s{};
+  s.n = order;
+  for (int m = 0; m < order; ++m) s.e[m] = shape[m];
+  return s;
+}
+
+// ------------------------------------------------------------ KR panel
+template <typename T>
+__global__ void kr_panel_kernel(FactorSet<T> fs, ShapeArg sh, int mode, i64 J, i64 Rr, T* out, const int* skip) {
+  if (skip != nullptr && *skip) return;
+  const int rank = fs.rank;
+  for (i64 s = blockIdx.x * i64(blockDim.x) + threadIdx.x; s < J; s += i64(gridDim.x) * blockDim.x) {
+    i64 a = s / Rr, b = s - a * Rr;
+    i64 idx[kMaxOrder];
+    for (int k = sh.n - 1; k > mode; --k) {
+      idx[k] = b % sh.e[k];
+      b /= sh.e[k];
+    }
+    for (int k = mode - 1; k >= 0; --k) {
+      idx[k] = a % sh.e[k];
+      a /= sh.e[k];
+    }
+    const i64 a0 = s / Rr, b0 = s - a0 * Rr;
+    for (int r = 0; r < rank; ++r) {
+      T v = T(1);
+      for (int k = sh.n - 1; k >= 0; --k) {  // highest mode first (kruskal.hpp:58-62)
+        if (k == mode) continue;
+        v *= fs.f[k][idx[k] + i64(r) * fs.extent[k]];
+      }
+      out[(a0 * rank + r) * Rr + b0] = v;
+    }
+  }
+}
+
+// --------------------------------------------------------- block helpers
+__device__ double block_reduce_sum(double v) {
+  __shared__ double scratch[33];
+  return block_sum(v, scratch);
+}
+
+// Parallel cyclic Jacobi (round-robin pairs) on a symmetric n x n matrix in
+// global memory A (destroyed; diagonal -> eigenvalues), V <- eigenvectors.
+// On exit evals[0..n) ascending, order[0..n) the column of V for each.
+__device__ void jacobi_eig(double* A, double* V, int n, double* evals, int* order) {
+  __shared__ double cs_c[kMaxRank * 8], cs_s[kMaxRank * 8];
+  __shared__ int pp[kMaxRank * 8], pq[kMaxRank * 8];
+  __shared__ int s_stop;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < n * n; e += nt) V[e] = (e % n == e / n) ? 1.0 : 0.0;
+  __syncthreads();
+  const int m = n + (n & 1);  // players (one dummy when n is odd)
+  const int npairs = m / 2;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0, dg = 0.0;
+    for (int e = tid; e < n * n; e += nt) {
+      const double x = A[e];
+      if (e % n == e / n)
+        dg += x * x;
+      else
+        off += x * x;
+    }
+    off = block_reduce_sum(off);
+    dg = block_reduce_sum(dg);
+    if (tid == 0) s_stop = (off <= 1e-30 * dg) || off == 0.0;
+    __syncthreads();
+    if (s_stop) break;
+    for (int round = 0; round < m - 1; ++round) {
+      for (int q = tid; q < npairs; q += nt) {
+        int i, j;
+        if (q == 0) {
+          i = m - 1;
+          j = round % (m - 1);
+        } else {
+          i = (round + q) % (m - 1);
+          j = (round + m - 1 - q) % (m - 1);
+        }
+        if (i > j) {
+          const int t = i;
+          i = j;
+          j = t;
+        }
+        double c = 1.0, s = 0.0;
+        if (j < n) {
+          const double apq = A[i + j * n];
+          if (apq != 0.0) {
+            const double app = A[i + i * n], aqq = A[j + j * n];
+            const double theta = (aqq - app) / (2.0 * apq);
+            const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+            c = 1.0 / sqrt(t * t + 1.0);
+            s = t * c;
+          }
+        }
+        pp[q] = i;
+        pq[q] = j;
+        cs_c[q] = c;
+        cs_s[q] = s;
+      }
+      __syncthreads();
+      // columns: A <- A J
+      for (int w = tid; w < npairs * n; w += nt) {
+        const int q = w / n, k = w % n;
+        const int i = pp[q], j = pq[q];
+        if (j >= n) continue;
+        const double c = cs_c[q], s = cs_s[q];
+        const double akp = A[k + i * n], akq = A[k + j * n];
+        A[k + i * n] = c * akp - s * akq;
+        A[k + j * n] = s * akp + c * akq;
+      }
+      __syncthreads();
+      // rows: A <- J^T A
+      for (int w = tid; w < npairs * n; w += nt) {
+        const int q = w / n, k = w % n;
+        const int i = pp[q], j = pq[q];
+        if (j >= n) continue;
+        const double c = cs_c[q], s = cs_s[q];
+        const double apk = A[i + k * n], aqk = A[j + k * n];
+        A[i + k * n] = c * apk - s * aqk;
+        A[j + k * n] = s * apk + c * aqk;
+      }
+      // V <- V J
+      for (int w = tid; w < npairs * n; w += nt) {
+        const int q = w / n, k = w % n;
+        const int i = pp[q], j = pq[q];
+        if (j >= n) continue;
+        const double c = cs_c[q], s = cs_s[q];
+        const double vkp = V[k + i * n], vkq = V[k + j * n];
+        V[k + i * n] = c * vkp - s * vkq;
+        V[k + j * n] = s * vkp + c * vkq;
+      }
+      __syncthreads();
+    }
+  }
+  // ascending, stable by index
+  for (int i = tid; i < n; i += nt) {
+    const double di = A[i + i * n];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const double dj = A[j + j * n];
+      if (dj < di || (dj == di && j < i)) ++rank;
+    }
+    evals[rank] = di;
+    order[rank] = i;
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------- init
+template <typename T>
+__global__ void __launch_bounds__(kSmallThreads) init_from_gram_kernel(const T* G, int n, int R, int mode,
+                                                                       u64 seed, int method, T* F, T* gram,
+                                                                       double* work) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double* A = work;
+  double* V = work + i64(n) * n;
+  double* ev = work + 2 * i64(n) * n;
+  int* ord = reinterpret_cast<int*>(ev + n);
+  double* col = ev + 2 * n;  // [n] padding scratch
+  __shared__ int s_filled;
+  for (i64 e = tid; e < i64(n) * R; e += nt) F[e] = T(0);
+  __syncthreads();
+  int filled = 0;
+  if (method == 0) {
+    for (i64 e = tid; e < i64(n) * n; e += nt) A[e] = double(G[e]);
+    __syncthreads();
+    jacobi_eig(A, V, n, ev, ord);
+    filled = R < n ? R : n;
+    for (i64 e = tid; e < i64(n) * filled; e += nt) {
+      const int i = int(e % n), j = int(e / n);
+      F[i + i64(j) * n] = T(V[i + i64(ord[n - 1 - j]) * n]);
+    }
+    __syncthreads();
+    // canonicalize_column_signs (solve.hpp:77-84): first max |entry| >= 0
+    for (int j = tid; j < R; j += nt) {
+      int at = 0;
+      T best = fabs(F[i64(j) * n]);
+      for (int i = 1; i < n; ++i) {
+        const T x = fabs(F[i + i64(j) * n]);
+        if (x > best) {
+          best = x;
+          at = i;
+        }
+      }
+      if (F[at + i64(j) * n] < T(0))
+        for (int i = 0; i < n; ++i) F[i + i64(j) * n] = -F[i + i64(j) * n];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) s_filled = filled;
+  __syncthreads();
+  // padding columns from stream (seed, init << 32 | mode), solve.hpp:117-127
+  if (tid == 0 && filled < R) {
+    const u64 s0 = derive_seed(seed, stream_id(kDomainInit, u64(mode)));
+    u64 e = 0;
+    for (int j = filled; j < R; ++j) {
+      double nr = 0.0;
+      for (int i = 0; i < n; ++i) {
+        const T x = T(normal_at(s0, e++));
+        col[i] = double(x);
+        nr += double(x) * double(x);
+      }
+      nr = sqrt(nr);
+      if (filled > 0 && filled < n) {
+        // col -= F(:, :j) (F(:, :j)^T col)
+        double proj[kMaxRank];
+        for (int c = 0; c < j; ++c) {
+          double s = 0.0;
+          for (int i = 0; i < n; ++i) s += double(F[i + i64(c) * n]) * col[i];
+          proj[c] = s;
+        }
+        double raw_nr = nr;
+        double nrm2 = 0.0;
+        double newc[1];  // placeholder to keep scope
+        (void)newc;
+        for (int i = 0; i < n; ++i) {
+          double s = 0.0;
+          for (int c = 0; c < j; ++c) s += double(F[i + i64(c) * n]) * proj[c];
+          const T v = T(col[i] - s);
+          nrm2 += double(v) * double(v);
+          // stash the projected value in A (scratch) to keep `col` (raw) intact
+          A[i] = double(v);
+        }
+        const double nrm = sqrt(nrm2);
+        for (int i = 0; i < n; ++i)
+          F[i + i64(j) * n] = (T(nrm) > T(1e-8)) ? T(A[i] / nrm) : (raw_nr > 0 ? T(col[i] / raw_nr) : T(col[i]));
+      } else {
+        for (int i = 0; i < n; ++i) F[i + i64(j) * n] = nr > 0 ? T(col[i] / nr) : T(col[i]);
+      }
+    }
+  }
+  __syncthreads();
+  // Gram F^T F
+  for (int e = tid; e < R * R; e += nt) {
+    const int a = e % R, b = e / R;
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += double(F[i + i64(a) * n]) * double(F[i + i64(b) * n]);
+    gram[e] = T(s);
+  }
+}
+
+template <typename T>
+__global__ void zero_factor_kernel(T* F, i64 n, int R, T* gram) {
+  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < n * R; e += i64(gridDim.x) * blockDim.x) F[e] = T(0);
+  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < i64(R) * R; e += i64(gridDim.x) * blockDim.x)
+    gram[e] = T(0);
+}
+
+// --------------------------------------------------------------- ALS
+template <typename T>
+__global__ void __launch_bounds__(kSmallThreads)
+    als_update_kernel(FactorSet<T> fs, int mode, const T* W, T* weights, double tol, int max_iter,
+                      double* trace_fit, double* trace_sec, AlsState* st, double* work) {
+  if (st->done) return;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int R = fs.rank, N = fs.order;
+  const i64 I = fs.extent[mode];
+  T* F = fs.f[mode];
+  double* V = work;             // R x R
+  double* Lm = V + R * R;       // R x R
+  double* Li = Lm + R * R;      // R x R
+  double* Vi = Li + R * R;      // R x R
+  double* ev = Vi + R * R;      // R
+  int* ord = reinterpret_cast<int*>(ev + R);
+  double* EA = ev + 2 * R;      // R x R eigen scratch
+  __shared__ int s_ok;
+  __shared__ double s_piv;
+
+  // 1. V = Hadamard of the other modes' Grams (solve.hpp:209-211)
+  for (int e = tid; e < R * R; e += nt) {
+    double v = 1.0;
+    for (int k = 0; k < N; ++k)
+      if (k != mode) v *= double(fs.gram[k][e]);
+    V[e] = double(T(v));
+  }
+  __syncthreads();
+  double fro = 0.0;
+  for (int e = tid; e < R * R; e += nt) fro += V[e] * V[e];
+  fro = sqrt(block_reduce_sum(fro));
+  // 2. pinv_psd (solve.hpp:62-73). Fast path: when V - tau_up I is positive
+  //    definite with tau_up = R eps ||V||_F >= R eps lambda_max, every
+  //    eigenvalue exceeds the reference's cutoff and pinv(V) = V^{-1}.
+  const double tau_up = double(R) * double(Traits<T>::eps) * fro;
+  for (int pass = 0; pass < 2; ++pass) {
+    const double shift = pass == 0 ? tau_up : 0.0;
+    if (tid == 0) s_ok = 1;
+    __syncthreads();
+    for (int j = 0; j < R; ++j) {
+      if (tid == 0) {
+        double d = V[j + j * R] - shift;
+        for (int k = 0; k < j; ++k) d -= Lm[j + k * R] * Lm[j + k * R];
+        if (!(d > 0.0)) s_ok = 0;
+        s_piv = d > 0.0 ? sqrt(d) : 1.0;
+        Lm[j + j * R] = s_piv;
+      }
+      __syncthreads();
+      if (!s_ok) break;
+      const double dj = s_piv;
+      for (int i = j + 1 + tid; i < R; i += nt) {
+        double s = V[i + j * R];
+        for (int k = 0; k < j; ++k) s -= Lm[i + k * R] * Lm[j + k * R];
+        Lm[i + j * R] = s / dj;
+      }
+      __syncthreads();
+    }
+    if (!s_ok) break;
+  }
+  const bool chol = s_ok != 0;
+  if (chol) {
+    // Li = L^{-1} (column-parallel), Vi = Li^T Li
+    for (int j = tid; j < R; j += nt) {
+      for (int i = 0; i < j; ++i) Li[i + j * R] = 0.0;
+      Li[j + j * R] = 1.0 / Lm[j + j * R];
+      for (int i = j + 1; i < R; ++i) {
+        double s = 0.0;
+        for (int k = j; k < i; ++k) s += Lm[i + k * R] * Li[k + j * R];
+        Li[i + j * R] = -s / Lm[i + i * R];
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < R * R; e += nt) {
+      const int a = e % R, b = e / R;
+      const int k0 = a > b ? a : b;
+      double s = 0.0;
+      for (int k = k0; k < R; ++k) s += Li[k + a * R] * Li[k + b * R];
+      Vi[e] = s;
+    }
+  } else {
+    for (int e = tid; e < R * R; e += nt) EA[e] = V[e];
+    __syncthreads();
+    jacobi_eig(EA, Li, R, ev, ord);
+    T lmax = T(0);
+    for (int k = 0; k < R; ++k) lmax = T(ev[k]) > lmax ? T(ev[k]) : lmax;
+    const T tau = T(R) * Traits<T>::eps * lmax;
+    for (int e = tid; e < R * R; e += nt) {
+      const int a = e % R, b = e / R;
+      double s = 0.0;
+      for (int k = 0; k < R; ++k) {
+        const T lk = T(ev[k]);
+        if (lk > tau) {
+          const int c = ord[k];
+          s += Li[a + c * R] * (1.0 / double(lk)) * Li[b + c * R];
+        }
+      }
+      Vi[e] = s;
+    }
+    if (tid == 0) st->pivots_fallback += 1;
+  }
+  __syncthreads();
+  // 3. F = W pinv(V)
+  for (i64 e = tid; e < I * R; e += nt) {
+    const i64 i = e % I;
+    const int r = int(e / I);
+    double s = 0.0;
+    for (int k = 0; k < R; ++k) s += double(W[i + k * I]) * Vi[k + r * R];
+    F[i + r * I] = T(s);
+  }
+  __syncthreads();
+  // 4. column normalization; weights from the last mode (solve.hpp:215-229)
+  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  for (int r = wid; r < R; r += nw) {
+    double s = 0.0;
+    for (i64 i = lane; i < I; i += 32) s += double(F[i + r * I]) * double(F[i + r * I]);
+    s = warp_sum(s);
+    const T nrm = T(sqrt(s));
+    if (mode == N - 1 && lane == 0) weights[r] = nrm;
+    if (nrm > T(0))
+      for (i64 i = lane; i < I; i += 32) F[i + r * I] = F[i + r * I] / nrm;
+  }
+  __syncthreads();
+  // 5. Gram of the new factor
+  for (int e = tid; e < R * R; e += nt) {
+    const int a = e % R, b = e / R;
+    double s = 0.0;
+    for (i64 i = 0; i < I; ++i) s += double(F[i + a * I]) * double(F[i + b * I]);
+    fs.gram[mode][e] = T(s);
+  }
+  __syncthreads();
+  if (mode != N - 1) return;
+  // 6. fit (solve.hpp:232-254), double accumulation
+  double m2 = 0.0;
+  for (int e = tid; e < R * R; e += nt) {
+    const int a = e % R, b = e / R;
+    double g = 1.0;
+    for (int k = 0; k < N; ++k) g *= double(fs.gram[k][e]);
+    m2 += double(weights[a]) * double(T(g)) * double(weights[b]);
+  }
+  m2 = block_reduce_sum(m2);
+  double xi = 0.0;
+  for (i64 e = tid; e < I * R; e += nt) {
+    const int r = int(e / I);
+    xi += double(W[e]) * double(F[e]) * double(weights[r]);
+  }
+  xi = block_reduce_sum(xi);
+  if (tid == 0) {
+    const double model2 = m2 > 0.0 ? m2 : 0.0;
+    const double nx2 = st->nx2;
+    const double fit_now = 1.0 - (nx2 + model2 - 2.0 * xi) / nx2;
+    const int it = st->it;
+    if (!isfinite(fit_now)) {
+      st->error_it = it;
+      st->done = 1;
+      return;
+    }
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    trace_fit[it - 1] = fit_now;
+    trace_sec[it - 1] = double(now - st->t0) * 1e-9;
+    if (it >= 2 && fabs(fit_now - st->prev_fit) < tol) {
+      st->converged = 1;
+      st->done = 1;
+    }
+    st->prev_fit = fit_now;
+    if (it >= max_iter) st->done = 1;
+    st->it = it + 1;
+  }
+}
+
+__global__ void als_start_kernel(AlsState* st, const double* nx2) {
+  unsigned long long now;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+  st->it = 1;
+  st->done = 0;
+  st->converged = 0;
+  st->error_it = -1;
+  st->pivots_fallback = 0;
+  st->prev_fit = 0.0;
+  st->nx2 = nx2[0];
+  st->t0 = now;
+}
+
+// ----------------------------------------------------------- normalize
+// kruskal.hpp:117-176 on device (one CTA).
+template <typename T>
+__global__ void __launch_bounds__(kSmallThreads) normalize_kernel(FactorSet<T> fs, T* weights, T* tmp) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int R = fs.rank, N = fs.order;
+  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  const T skip = T(32) * Traits<T>::eps;
+  __shared__ int s_order[kMaxRank];
+  for (int j = wid; j < R; j += nw) {
+    for (int m = 0; m < N; ++m) {
+      T* f = fs.f[m] + i64(j) * fs.extent[m];
+      const i64 n = fs.extent[m];
+      double s = 0.0;
+      for (i64 i = lane; i < n; i += 32) s += double(f[i]) * double(f[i]);
+      s = warp_sum(s);
+      const T nrm = T(sqrt(s));
+      __syncwarp();
+      if (nrm == T(0)) {
+        for (i64 i = lane; i < n; i += 32) f[i] = (i == 0) ? T(1) : T(0);
+        if (lane == 0) weights[j] = T(0);
+      } else if (fabs(nrm - T(1)) > skip) {
+        for (i64 i = lane; i < n; i += 32) f[i] = f[i] / nrm;
+        if (lane == 0) weights[j] = weights[j] * nrm;
+      }
+      __syncwarp();
+    }
+    const bool neg = weights[j] < T(0);
+    __syncwarp();
+    T* f0 = fs.f[0] + i64(j) * fs.extent[0];
+    const i64 n0 = fs.extent[0];
+    if (neg) {
+      if (lane == 0) weights[j] = -weights[j];
+      for (i64 i = lane; i < n0; i += 32) f0[i] = -f0[i];
+    }
+    __syncwarp();
+    if (N >= 2) {
+      // first index of the max |entry| of factor 0's column
+      T best = T(-1);
+      i64 at = 0;
+      for (i64 i = lane; i < n0; i += 32) {
+        const T x = fabs(f0[i]);
+        if (x > best) {
+          best = x;
+          at = i;
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const T ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const i64 oa = __shfl_xor_sync(0xffffffffu, at, o);
+        if (ob > best || (ob == best && oa < at)) {
+          best = ob;
+          at = oa;
+        }
+      }
+      const bool flip = f0[at] < T(0);
+      __syncwarp();
+      if (flip) {
+        for (i64 i = lane; i < n0; i += 32) f0[i] = -f0[i];
+        T* f1 = fs.f[1] + i64(j) * fs.extent[1];
+        for (i64 i = lane; i < fs.extent[1]; i += 32) f1[i] = -f1[i];
+      }
+    }
+  }
+  __syncthreads();
+  // stable sort: weight descending, ties by lexicographic factor-0 column
+  for (int a = tid; a < R; a += nt) {
+    int pos = 0;
+    const T wa = weights[a];
+    const T* ca = fs.f[0] + i64(a) * fs.extent[0];
+    for (int b = 0; b < R; ++b) {
+      if (b == a) continue;
+      const T wb = weights[b];
+      bool before;
+      if (wb != wa) {
+        before = wb > wa;
+      } else {
+        const T* cb = fs.f[0] + i64(b) * fs.extent[0];
+        int cmp = 0;
+        for (i64 i = 0; i < fs.extent[0]; ++i)
+          if (cb[i] != ca[i]) {
+            cmp = cb[i] < ca[i] ? -1 : 1;
+            break;
+          }
+        before = cmp < 0 || (cmp == 0 && b < a);
+      }
+      pos += before ? 1 : 0;
+    }
+    s_order[pos] = a;
+  }
+  __syncthreads();
+  bool ident = true;
+  for (int j = 0; j < R; ++j) ident = ident && (s_order[j] == j);
+  if (ident) return;
+  // permute columns through tmp
+  i64 off = 0;
+  for (int m = 0; m < N; ++m) {
+    const i64 n = fs.extent[m];
+    for (i64 e = tid; e < n * R; e += nt) tmp[off + e] = fs.f[m][e];
+    off += n * R;
+  }
+  for (int j = tid; j < R; j += nt) tmp[off + j] = weights[j];
+  __syncthreads();
+  off = 0;
+  for (int m = 0; m < N; ++m) {
+    const i64 n = fs.extent[m];
+    for (i64 e = tid; e < n * R; e += nt) {
+      const i64 i = e % n;
+      const int j = int(e / n);
+      fs.f[m][e] = tmp[off + i + i64(s_order[j]) * n];
+    }
+    off += n * R;
+  }
+  for (int j = tid; j < R; j += nt) weights[j] = tmp[off + s_order[j]];
+}
+
+template <typename T>
+__global__ void small_gemm_kernel(const T* Q, i64 dim, i64 l, const T* A, int rank, T* out) {
+  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < dim * rank; e += i64(gridDim.x) * blockDim.x) {
+    const i64 i = e % dim, r = e / dim;
+    double s = 0.0;
+    for (i64 c = 0; c < l; ++c) s += double(Q[i + c * dim]) * double(A[c + r * l]);
+    out[e] = T(s);
+  }
+}
+
+// ------------------------------------------------------------ reductions
+template <typename T>
+__global__ void norm_finite_kernel(const T* x, i64 n, double* part) {
+  double s = 0.0, bad = 0.0;
+  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < n; e += i64(gridDim.x) * blockDim.x) {
+    const double v = double(x[e]);
+    if (isfinite(v))
+      s += v * v;
+    else
+      bad += 1.0;
+  }
+  s = block_reduce_sum(s);
+  bad = block_reduce_sum(bad);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = s;
+    part[2 * blockIdx.x + 1] = bad;
+  }
+}
+
+__global__ void sum_pairs_kernel(const double* part, int nblocks, double* out) {
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int q = 0; q < nblocks; ++q) {
+      a += part[2 * q];
+      b += part[2 * q + 1];
+    }
+    out[0] = a;
+    out[1] = b;
+  }
+}
+
+constexpr int kResRows = 8;
+
+template <typename T>
+__global__ void __launch_bounds__(256) residual_kernel(const T* X, ShapeArg sh, FactorSet<T> fs, const T* w,
+                                                       double* part) {
+  __shared__ T coef[kResRows][kMaxRank];
+  const int R = fs.rank, N = sh.n;
+  const i64 last = sh.e[N - 1];
+  i64 prefix = 1;
+  for (int m = 0; m < N - 1; ++m) prefix *= sh.e[m];
+  const T* Al = fs.f[N - 1];
+  double acc_r = 0.0, acc_x = 0.0;
+  for (i64 p0 = i64(blockIdx.x) * kResRows; p0 < prefix; p0 += i64(gridDim.x) * kResRows) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < kResRows * R; e += blockDim.x) {
+      const int q = e / R, r = e % R;
+      const i64 p = p0 + q;
+      T v = T(0);
+      if (p < prefix) {
+        v = w[r];
+        i64 rem = p;
+        for (int m = N - 2; m >= 0; --m) {
+          const i64 im = rem % sh.e[m];
+          rem /= sh.e[m];
+          v *= fs.f[m][im + i64(r) * sh.e[m]];
+        }
+      }
+      coef[q][r] = v;
+    }
+    __syncthreads();
+    const int nrows = int(prefix - p0 < kResRows ? prefix - p0 : kResRows);
+    for (i64 il = threadIdx.x; il < last; il += blockDim.x) {
+      T xh[kResRows];
+#pragma unroll
+      for (int q = 0; q < kResRows; ++q) xh[q] = T(0);
+      for (int r = 0; r < R; ++r) {
+        const T a = Al[il + i64(r) * last];
+#pragma unroll
+        for (int q = 0; q < kResRows; ++q) xh[q] = fma(coef[q][r], a, xh[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < kResRows; ++q)
+        if (q < nrows) {
+          const double x = double(X[(p0 + q) * last + il]);
+          const double d = x - double(xh[q]);
+          acc_r += d * d;
+          acc_x += x * x;
+        }
+    }
+  }
+  acc_r = block_reduce_sum(acc_r);
+  acc_x = block_reduce_sum(acc_x);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = acc_r;
+    part[2 * blockIdx.x + 1] = acc_x;
+  }
+}
+
+// ------------------------------------------------------------ synthetic
+struct DFactors {
+  const double* f[kMaxOrder];
+};
+
+template <typename T>
+__global__ void synth_reconstruct_kernel(ShapeArg sh, int R, const double* w, DFactors fs, T* out, i64 total) {
+  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
+    i64 idx[kMaxOrder];
+    i64 rem = e;
+    for (int m = sh.n - 1; m >= 0; --m) {
+      idx[m] = rem % sh.e[m];
+      rem /= sh.e[m];
+    }
+    double s = 0.0;
+    for (int r = 0; r < R; ++r) {
+      double p = w[r];
+      for (int m = 0; m < sh.n; ++m) p *= fs.f[m][idx[m] + i64(r) * sh.e[m]];
+      s += p;
+    }
+    out[e] = T(s);
+  }
+}
+
+template <typename T>
+__global__ void sum_and_sq_kernel(const T* x, i64 n, double mean, double* part) {
+  double s = 0.0, q = 0.0;
+  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < n; e += i64(gridDim.x) * blockDim.x) {
+    const double v = double(x[e]);
+    s += v;
+    q += (v - mean) * (v - mean);
+  }
+  s = block_reduce_sum(s);
+  q = block_reduce_sum(q);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = s;
+    part[2 * blockIdx.x + 1] = q;
+  }
+}
+
+template <typename T>
+__global__ void add_noise_kernel(T* x, i64 n, T sigma, u64 s0) {
+  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < n; e += i64(gridDim.x) * blockDim.x)
+    x[e] += sigma * T(normal_at(s0, u64(e)));
+}
+
+}  // namespace
+
+// ================================================================ host
+template <typename T>
+void kr_panel(const FactorSet<T>& fs, const i64* shape, int mode, T* out, cudaStream_t st, const int* skip) {
+  const ShapeArg sh = make_shape(shape, fs.order);
+  i64 L = 1, Rr = 1;
+  for (int m = 0; m < mode; ++m) L *= shape[m];
+  for (int m = mode + 1; m < fs.order; ++m) Rr *= shape[m];
+  const i64 J = L * Rr;
+  const int blocks = int(std::max<i64>(1, std::min<i64>(ceil_div(J, 256), 148 * 16)));
+  kr_panel_kernel<T><<<blocks, 256, 0, st>>>(fs, sh, mode, J, Rr, out, skip);
+  count_launch();
+  RCPG_LAUNCHED();
+}
+
+template <typename T>
+void init_factor_from_gram(const T* G, int extent, int rank, int mode, u64 seed, int method, T* factor,
+                           T* gram_out, double* work, cudaStream_t st) {
+  check_arg(rank <= kMaxRank, "init_factors: rank above the supported maximum");
+  init_from_gram_kernel<T><<<1, kSmallThreads, 0, st>>>(G, extent, rank, mode, seed, method, factor, gram_out,
+                                                         work);
+  count_launch();
+  RCPG_LAUNCHED();
+}
+
+template <typename T>
+void zero_factor(T* factor, i64 extent, int rank, T* gram_out, cudaStream_t st) {
+  zero_factor_kernel<T><<<64, 256, 0, st>>>(factor, extent, rank, gram_out);
+  count_launch();
+  RCPG_LAUNCHED();
+}
+
+template <typename T>
+void als_update(const FactorSet<T>& fs, int mode, const T* W, T* weights, double tol, int max_iter,
+                double* trace_fit, double* trace_sec, AlsState* state, double* work, cudaStream_t st) {
+  als_update_kernel<T><<<1, kSmallThreads, 0, st>>>(fs, mode, W, weights, tol, max_iter, trace_fit, trace_sec,
+                                                     state, work);
+  count_launch();
+  RCPG_LAUNCHED();
+}
+
+void als_start(AlsState* state, double* nx2_src, cudaStream_t st) {
+  als_start_kernel<<<1, 1, 0, st>>>(state, nx2_src);
+  count_launch();
+  RCPG_LAUNCHED();
+}
+
+template <typename T>
+void normalize_model(const FactorSet<T>& fs, T* weights, T* tmp, cudaStream_t st) {
+  normalize_kernel<T><<<1, kSmallThreads, 0, st>>>(fs, weights, tmp);
+  count_launch();
+  RCPG_LAUNCHED();
+}
+
+template <typename T>
+void small_gemm(const T* Q, i64 dim, i64 l, const T* A, int rank, T* out, cudaStream_t st) {
+  const int blocks = int(std::max<i64>(1, std::min<i64>(ceil_div(dim * rank, 256), 148 * 8)));
+  small_gemm_kernel<T><<<blocks, 256, 0, st>>>(Q, dim, l, A, rank, out);
+  count_launch();
+  RCPG_LAUNCHED();
+}
+
+template <typename T>
+void norm_and_finite(const T* x, i64 n, double* out2, double* scratch, int num_sms, cudaStream_t st) {
+  const int blocks = int(std::max<i64>(1, std::min<i64>(ceil_div(n, 256), i64(num_sms) * 4)));
+  norm_finite_kernel<T><<<blocks, 256, 0, st>>>(x, n, scratch);
+  sum_pairs_kernel<<<1, 32, 0, st>>>(scratch, blocks, out2);
+  count_launch(2);
+  RCPG_LAUNCHED();
+}
+
+size_t residual_scratch_doubles(int num_sms) { return size_t(num_sms) * 8 * 2 + 16; }
+
+template <typename T>
+void residual_norms(const T* X, const i64* shape, int order, const FactorSet<T>& fs, const T* weights,
+                    double* out2, double* scratch, int num_sms, cudaStream_t st) {
+  check_arg(fs.rank <= kMaxRank, "relative_error: rank above the supported maximum");
+  const ShapeArg sh = make_shape(shape, order);
+  i64 prefix = 1;
+  for (int m = 0; m < order - 1; ++m) prefix *= shape[m];
+  const int blocks = int(std::max<i64>(1, std::min<i64>(ceil_div(prefix, kResRows), i64(num_sms) * 8)));
+  residual_kernel<T><<<blocks, 256, 0, st>>>(X, sh, fs, weights, scratch);
+  sum_pairs_kernel<<<1, 32, 0, st>>>(scratch, blocks, out2);
+  count_launch(2);
+  RCPG_LAUNCHED();
+}
+
+template <typename T>
+void synth_tensor(const i64* shape, int order, int rank, const double* w_dev, const double* const* f_dev, double snr,
+                  u64 noise_seed, T* out, double* scratch, int num_sms, cudaStream_t st) {
+  const ShapeArg sh = make_shape(shape, order);
+  DFactors fs{};
+  for (int m = 0; m < order; ++m) fs.f[m] = f_dev[m];
+  i64 total = 1;
+  for (int m = 0; m < order; ++m) total *= shape[m];
+  const int blocks = int(std::max<i64>(1, std::min<i64>(ceil_div(total, 256), i64(num_sms) * 8)));
+  synth_reconstruct_kernel<T><<<blocks, 256, 0, st>>>(sh, rank, w_dev, fs, out, total);
+  count_launch();
+  RCPG_LAUNCHED();
+  if (!(snr > 0)) return;
+  // add_noise (synthetic.hpp:42-58): sigma = sd / snr, sd the sample std.
+  double h[2];
+  sum_and_sq_kernel<T><<<blocks, 256, 0, st>>>(out, total, 0.0, scratch);
+  sum_pairs_kernel<<<1, 32, 0, st>>>(scratch, blocks, scratch + 2 * blocks);
+  RCPG_CUDA(cudaMemcpyAsync(h, scratch + 2 * blocks, sizeof(h), cudaMemcpyDeviceToHost, st));
+  RCPG_CUDA(cudaStreamSynchronize(st));
+  const double mean = h[0] / double(total);
+  sum_and_sq_kernel<T><<<blocks, 256, 0, st>>>(out, total, mean, scratch);
+  sum_pairs_kernel<<<1, 32, 0, st>>>(scratch, blocks, scratch + 2 * blocks);
+  RCPG_CUDA(cudaMemcpyAsync(h, scratch + 2 * blocks, sizeof(h), cudaMemcpyDeviceToHost, st));
+  RCPG_CUDA(cudaStreamSynchronize(st));
+  const T sd = total > 1 ? T(sqrt(h[1] / double(total - 1))) : T(0);
+  const T sigma = sd / T(snr);
+  const u64 s0 = derive_seed(noise_seed, stream_id(kDomainNoise, 0));
+  add_noise_kernel<T><<<blocks, 256, 0, st>>>(out, total, sigma, s0);
+  count_launch(5);
+  RCPG_LAUNCHED();
+}
+
+#define RCPG_INST(T)                                                                                          \
+  template void kr_panel<T>(const FactorSet<T>&, const i64*, int, T*, cudaStream_t, const int*);                          \
+  template void init_factor_from_gram<T>(const T*, int, int, int, u64, int, T*, T*, double*, cudaStream_t);   \
+  template void zero_factor<T>(T*, i64, int, T*, cudaStream_t);                                               \
+  template void als_update<T>(const FactorSet<T>&, int, const T*, T*, double, int, double*, double*,          \
+                              AlsState*, double*, cudaStream_t);                                              \
+  template void normalize_model<T>(const FactorSet<T>&, T*, T*, cudaStream_t);                                \
+  template void small_gemm<T>(const T*, i64, i64, const T*, int, T*, cudaStream_t);                           \
+  template void norm_and_finite<T>(const T*, i64, double*, double*, int, cudaStream_t);                       \
+  template void residual_norms<T>(const T*, const i64*, int, const FactorSet<T>&, const T*, double*, double*, \
+                                  int, cudaStream_t);                                                         \
+  template void synth_tensor<T>(const i64*, int, int, const double*, const double* const*, double, u64, T*,   \
+                                double*, int, cudaStream_t);
+RCPG_INST(float)
+RCPG_INST(double)
+#undef RCPG_INST
+
+}  // namespace rcpg

@@ -1,0 +1,84 @@
+// SPDX-License-Identifier: MIT
+// CP-ALS on the (compressed) tensor, solve.hpp:62-262, and the Kruskal-model
+// kernels of kruskal.hpp (normalize, recover, relative_error).
+#pragma once
+
+#include "common.cuh"
+
+namespace rcpg {
+
+constexpr int kMaxOrder = 8;
+constexpr int kMaxRank = 128;
+
+// Device-side ALS control block (one per solve).
+struct AlsState {
+  int it;          // next iteration (1-based)
+  int done;
+  int converged;
+  int error_it;    // > 0 (or 0 for input errors): SolverError iteration
+  int pivots_fallback;  // number of pinv_psd calls that needed the eigen path
+  int pad;
+  double prev_fit;
+  double nx2;      // ||B||^2 (double)
+  unsigned long long t0;  // globaltimer at solver start (ns)
+};
+
+template <typename T>
+struct FactorSet {
+  T* f[kMaxOrder];     // factor m: extent[m] x rank, column-major
+  T* gram[kMaxOrder];  // R x R (Scalar-rounded), column-major
+  i64 extent[kMaxOrder];
+  int order;
+  int rank;
+};
+
+// Materializes the Khatri-Rao panel K[a, r, b] = prod_{k != m} A_k[i_k, r]
+// (khatri_rao_all_but, kruskal.hpp:52-64) in the (a, c, b) panel layout of
+// mode m of `shape`, so MTTKRP = sketch(B, view_m, K, rank).
+template <typename T>
+void kr_panel(const FactorSet<T>& fs, const i64* shape, int mode, T* out, cudaStream_t st,
+              const int* skip = nullptr);
+
+// init_factors (solve.hpp:93-131) for mode `mode` >= 1 from the Gram matrix
+// G = B_(m) B_(m)^T (extent x extent, T, column-major). Writes factor and its
+// Gram. `work` >= 3 * extent^2 + 4 * extent doubles.
+template <typename T>
+void init_factor_from_gram(const T* G, int extent, int rank, int mode, u64 seed, int method, T* factor,
+                           T* gram_out, double* work, cudaStream_t st);
+template <typename T>
+void zero_factor(T* factor, i64 extent, int rank, T* gram_out, cudaStream_t st);
+
+// One ALS mode update (solve.hpp:207-230) plus, for the last mode, the fit /
+// stopping test (solve.hpp:232-254). W = MTTKRP result (extent x rank).
+template <typename T>
+void als_update(const FactorSet<T>& fs, int mode, const T* W, T* weights, double tol, int max_iter,
+                double* trace_fit, double* trace_sec, AlsState* state, double* work, cudaStream_t st);
+
+void als_start(AlsState* state, double* nx2_src, cudaStream_t st);
+
+// normalize (kruskal.hpp:117-176) in place; `tmp` >= sum extents * rank + rank elements.
+template <typename T>
+void normalize_model(const FactorSet<T>& fs, T* weights, T* tmp, cudaStream_t st);
+
+// out = Q (dim x l) * A (l x rank), column-major (recover, kruskal.hpp:198-220).
+template <typename T>
+void small_gemm(const T* Q, i64 dim, i64 l, const T* A, int rank, T* out, cudaStream_t st);
+
+// Sum of squares (double) and count of non-finite entries of a device array.
+template <typename T>
+void norm_and_finite(const T* x, i64 n, double* out2 /* [2]: sumsq, nonfinite */, double* scratch,
+                     int num_sms, cudaStream_t st);
+
+// ||X - model||^2 and ||X||^2 (double), streamed over X (relative_error,
+// kruskal.hpp:187-194, accumulated in double). out2 = {resid2, x2}.
+template <typename T>
+void residual_norms(const T* X, const i64* shape, int order, const FactorSet<T>& fs, const T* weights,
+                    double* out2, double* scratch, int num_sms, cudaStream_t st);
+size_t residual_scratch_doubles(int num_sms);
+
+// Dense reconstruction of a model given in double + add_noise (synthetic data).
+template <typename T>
+void synth_tensor(const i64* shape, int order, int rank, const double* w_dev, const double* const* f_dev,
+                  double snr, u64 noise_seed, T* out, double* scratch, int num_sms, cudaStream_t st);
+
+}  // namespace rcpg

@@ -1,0 +1,963 @@
+// SPDX-License-Identifier: MIT
+// Host orchestration of the rCP hot path and the C ABI declared in
+// include/rcpg.h. The control flow restates:
+//   compress   /root/reference/proj/include/rcp/compress.hpp:86-146
+//   als_solve  /root/reference/proj/include/rcp/solve.hpp:183-262
+//   decompose  /root/reference/proj/include/rcp/solve.hpp:381-398
+//   recover    /root/reference/proj/include/rcp/kruskal.hpp:198-220
+// Every numeric step runs on the device (passes.cu, factor.cu, als.cu); the
+// host only sequences launches, validates arguments in the reference's
+// order, and reads back a few scalars (norm checks, the ALS stop flag).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../../include/rcpg.h"
+#include "als.cuh"
+#include "common.cuh"
+#include "factor.cuh"
+#include "passes.cuh"
+#include "runtime.cuh"
+
+using namespace rcpg;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t n) {
+    if (n <= bytes) return;
+    if (p) RCPG_CUDA(cudaFree(p));
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(n, 256));
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      throw CudaFailure(std::string("cudaMalloc(") + std::to_string(n) + "): " + cudaGetErrorString(e), e);
+    }
+    bytes = std::max<size_t>(n, 256);
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+struct PassRecord {
+  std::string name;
+  cudaEvent_t a = nullptr, b = nullptr;
+  double bytes = 0;
+};
+
+}  // namespace
+
+struct rcpg_context {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  std::string err;
+  int err_it = -1;
+  // workspace
+  DevBuf panelA, panelB, work0, work1, Y, Qy, scratch, keys, cands, bar, info, part, tau, diag;
+  DevBuf als_f, als_g, als_w, als_kr, als_work, als_trace, als_state, weights, small_tmp, nrm;
+  std::vector<PassRecord> passes;
+  size_t pass_used = 0;
+  bool timing = true;
+};
+
+struct rcpg_tensor {
+  rcpg_context* ctx = nullptr;
+  int dtype = 0;
+  int order = 0;
+  i64 shape[kMaxOrder] = {};
+  i64 size = 0;
+  void* d = nullptr;
+  bool owned = false;
+};
+
+struct BasisRec {
+  bool identity = true;
+  i64 dim = 0, cols = 0;
+  bool rank_warning = false;
+  DevBuf q;
+};
+
+struct rcpg_compressed {
+  int dtype = 0;
+  int order = 0;
+  i64 shape[kMaxOrder] = {};
+  i64 size = 0;
+  DevBuf data;
+  std::vector<BasisRec> bases;
+  ~rcpg_compressed() {
+    data.release();
+    for (auto& b : bases) b.q.release();
+  }
+};
+
+namespace {
+
+size_t dsize(int dtype) { return dtype == RCPG_F64 ? 8 : 4; }
+
+// --------------------------------------------------------------- timing
+void pass_begin(rcpg_context* c, const char* name, double bytes) {
+  if (!c->timing) return;
+  if (c->pass_used == c->passes.size()) {
+    PassRecord r;
+    RCPG_CUDA(cudaEventCreate(&r.a));
+    RCPG_CUDA(cudaEventCreate(&r.b));
+    c->passes.push_back(r);
+  }
+  PassRecord& r = c->passes[c->pass_used];
+  r.name = name;
+  r.bytes = bytes;
+  RCPG_CUDA(cudaEventRecord(r.a, c->st));
+}
+void pass_end(rcpg_context* c) noexcept {
+  if (!c->timing || c->pass_used >= c->passes.size()) return;
+  if (cudaEventRecord(c->passes[c->pass_used].b, c->st) != cudaSuccess) (void)cudaGetLastError();
+  ++c->pass_used;
+}
+
+struct ScopedPass {
+  rcpg_context* c;
+  ScopedPass(rcpg_context* c_, const char* n, double bytes) : c(c_) { pass_begin(c, n, bytes); }
+  ~ScopedPass() { pass_end(c); }
+};
+
+KoldaMap mode_kolda(const i64* shape, int order, int mode) {
+  KoldaMap km{};
+  km.n_low = mode;
+  km.n_high = order - mode - 1;
+  km.L = 1;
+  for (int m = 0; m < mode; ++m) {
+    km.low_ext[m] = shape[m];
+    km.L *= shape[m];
+  }
+  for (int m = mode + 1; m < order; ++m) km.high_ext[m - mode - 1] = shape[m];
+  return km;
+}
+
+KoldaMap identity_kolda(i64 rows) {
+  KoldaMap km{};
+  km.n_low = 0;
+  km.n_high = 1;
+  km.high_ext[0] = rows;
+  km.L = 1;
+  return km;
+}
+
+ModeView mode_view(const i64* shape, int order, int mode) {
+  ModeView v;
+  for (int m = 0; m < mode; ++m) v.L *= shape[m];
+  v.I = shape[mode];
+  for (int m = mode + 1; m < order; ++m) v.R *= shape[m];
+  return v;
+}
+
+FactorWork factor_work(rcpg_context* c, i64 rows) {
+  const int maxb = 148 * 8 * 2;
+  c->keys.ensure(size_t(rows) * sizeof(i64));
+  c->cands.ensure(2 * size_t(maxb) * factor_cand_bytes());
+  c->bar.ensure(sizeof(GridBarrier));
+  c->info.ensure(16);
+  c->part.ensure(2 * size_t(maxb) * (kMaxPanelCols + 1) * sizeof(double));
+  c->tau.ensure(kMaxPanelCols * sizeof(double));
+  c->diag.ensure(kMaxPanelCols * sizeof(double));
+  FactorWork w;
+  w.keys = c->keys.as<i64>();
+  w.cands = c->cands.p;
+  w.bar = c->bar.as<GridBarrier>();
+  w.info = c->info.as<int>();
+  w.part = c->part.as<double>();
+  w.tau = c->tau.p;
+  w.diag = c->diag.p;
+  w.max_blocks = maxb;
+  return w;
+}
+
+// Host copy of a device scalar pair.
+void read_doubles(rcpg_context* c, const double* d, double* h, int n) {
+  RCPG_CUDA(cudaMemcpyAsync(h, d, sizeof(double) * n, cudaMemcpyDeviceToHost, c->st));
+  RCPG_CUDA(cudaStreamSynchronize(c->st));
+}
+
+struct CompressCfg {
+  i64 target_rank, oversampling;
+  int power_iterations, distribution, stabilizer;
+  bool modes_present;
+  std::vector<i64> modes;
+  u64 seed;
+};
+
+CompressCfg to_cfg(const rcpg_compress_config& c) {
+  CompressCfg r{c.target_rank, c.oversampling, c.power_iterations, c.distribution, c.stabilizer,
+                c.modes_present != 0, {}, c.seed};
+  if (c.modes_present && c.n_modes > 0) r.modes.assign(c.modes, c.modes + c.n_modes);
+  return r;
+}
+
+// Stabilize an I x n sample matrix (column-major, destroyed) into out.
+template <typename T>
+int stabilize_small(rcpg_context* c, int stab, T* Y, i64 I, int n, T* out) {
+  FactorWork w = factor_work(c, I);
+  const KoldaMap km = identity_kolda(I);
+  if (stab == RCPG_STAB_LU) return plu_basis<T>(Y, out, I, I, n, km, w, c->st);
+  return thin_qr<T>(Y, out, I, I, n, km, w, nullptr, c->st);
+}
+
+// compress.hpp:86-146
+template <typename T>
+void run_compress(rcpg_context* c, const rcpg_tensor* t, const CompressCfg& cfg, rcpg_compressed* out) {
+  check_arg(cfg.target_rank >= 1, "compress: target rank must be at least 1");
+  check_arg(cfg.oversampling >= 0, "compress: oversampling must be non-negative");
+  check_arg(cfg.power_iterations >= 0, "compress: power iteration count must be non-negative");
+  const int order = t->order;
+  const int sms = device_caps().num_sms;
+  {
+    ScopedPass sp(c, "check_finite", double(t->size) * sizeof(T));
+    c->nrm.ensure(4096 * sizeof(double));
+    c->scratch.ensure(size_t(sms) * 8 * sizeof(double) + 64);
+    norm_and_finite<T>(static_cast<const T*>(t->d), t->size, c->nrm.as<double>(), c->scratch.as<double>(), sms,
+                       c->st);
+  }
+  double h[2];
+  read_doubles(c, c->nrm.as<double>(), h, 2);
+  check_arg(h[1] == 0.0, "compress: input values must be finite");
+
+  std::set<i64> selected;
+  if (cfg.modes_present) {
+    for (i64 m : cfg.modes) {
+      check_arg(m >= 0 && m < order, "compress: mode index out of range");
+      selected.insert(m);
+    }
+  } else {
+    for (i64 m = 0; m < order; ++m) selected.insert(m);
+  }
+
+  i64 shape[kMaxOrder];
+  for (int m = 0; m < order; ++m) shape[m] = t->shape[m];
+  const T* cur = static_cast<const T*>(t->d);
+  int which = 0;
+  out->bases.clear();
+  out->bases.resize(order);
+
+  for (int n = 0; n < order; ++n) {
+    const i64 extent = shape[n];
+    const i64 l = std::min(cfg.target_rank + cfg.oversampling, extent);
+    BasisRec& basis = out->bases[n];
+    basis.dim = extent;
+    if (selected.count(n) == 0 || l >= extent) {
+      basis.identity = true;
+      continue;
+    }
+    check_arg(l <= kMaxPanelCols, "compress: sketch width k + p above the supported maximum (256)");
+    const ModeView v = mode_view(shape, order, n);
+    const i64 J = v.L * v.R;
+    const i64 S = J * extent;
+    const KoldaMap km = mode_kolda(shape, order, n);
+    const double b = sizeof(T);
+    c->panelA.ensure(size_t(J) * l * sizeof(T));
+    c->panelB.ensure(size_t(J) * l * sizeof(T));
+    c->Y.ensure(size_t(extent) * l * sizeof(T));
+    c->Qy.ensure(size_t(extent) * l * sizeof(T));
+    const i64 scr = sketch_scratch_elems<T>(v, l, sms);
+    c->scratch.ensure(size_t(scr) * sizeof(T));
+    T* P = c->panelA.as<T>();
+    T* Zp = c->panelB.as<T>();
+    T* Y = c->Y.as<T>();
+    T* Qy = c->Qy.as<T>();
+
+    {
+      ScopedPass sp(c, "omega", 0.0);
+      omega_panel<T>(cfg.seed, n, km, v, l, cfg.distribution, P, c->st);
+    }
+    {
+      ScopedPass sp(c, "sketch", (S + extent * l) * b);
+      sketch<T>(cur, v, P, l, Y, c->scratch.as<T>(), scr, sms, c->st);
+    }
+    i64 ycols = l;
+    for (int it = 0; it < cfg.power_iterations; ++it) {
+      int rq;
+      {
+        ScopedPass sp(c, "stab_y", 2.0 * extent * ycols * b);
+        rq = stabilize_small<T>(c, cfg.stabilizer, Y, extent, int(ycols), Qy);
+      }
+      {
+        ScopedPass sp(c, "power_xtq", (S + J * rq) * b);
+        project<T>(cur, v, Qy, extent, rq, P, c->st);
+      }
+      int rz;
+      {
+        ScopedPass sp(c, "stab_w", 2.0 * J * rq * b);
+        FactorWork w = factor_work(c, J);
+        if (cfg.stabilizer == RCPG_STAB_LU)
+          rz = plu_basis<T>(P, Zp, J, v.R, rq, km, w, c->st);
+        else
+          rz = thin_qr<T>(P, Zp, J, v.R, rq, km, w, nullptr, c->st);
+      }
+      {
+        ScopedPass sp(c, "power_xz", (S + J * rz + extent * rz) * b);
+        const i64 scr2 = sketch_scratch_elems<T>(v, rz, sms);
+        c->scratch.ensure(size_t(scr2) * sizeof(T));
+        sketch<T>(cur, v, Zp, rz, Y, c->scratch.as<T>(), scr2, sms, c->st);
+      }
+      ycols = rz;
+    }
+    // final Householder basis + rank warning (compress.hpp:135)
+    c->info.ensure(16);
+    int qcols;
+    {
+      ScopedPass sp(c, "thin_qr", 2.0 * extent * ycols * b);
+      FactorWork w = factor_work(c, extent);
+      basis.q.ensure(size_t(extent) * ycols * sizeof(T));
+      qcols = thin_qr<T>(Y, basis.q.as<T>(), extent, extent, int(ycols), identity_kolda(extent), w,
+                         w.info + 1, c->st);
+    }
+    int rw = 0;
+    RCPG_CUDA(cudaMemcpyAsync(&rw, c->info.as<int>() + 1, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    RCPG_CUDA(cudaStreamSynchronize(c->st));
+    basis.identity = false;
+    basis.cols = qcols;
+    basis.rank_warning = rw != 0;
+    // fold(Q^T B_(n)) must match next_shape (tensor.hpp:193-194)
+    check_arg(qcols == l, "fold: matrix dimensions do not match the target shape");
+    DevBuf& dst = which == 0 ? c->work0 : c->work1;
+    dst.ensure(size_t(v.L) * l * v.R * sizeof(T));
+    {
+      ScopedPass sp(c, "project", (S + l * J) * b);
+      project<T>(cur, v, basis.q.as<T>(), extent, l, dst.as<T>(), c->st);
+    }
+    cur = dst.as<T>();
+    which ^= 1;
+    shape[n] = l;
+  }
+  out->dtype = t->dtype;
+  out->order = order;
+  i64 size = 1;
+  for (int m = 0; m < order; ++m) {
+    out->shape[m] = shape[m];
+    size *= shape[m];
+  }
+  out->size = size;
+  out->data.ensure(size_t(size) * sizeof(T));
+  RCPG_CUDA(cudaMemcpyAsync(out->data.p, cur, size_t(size) * sizeof(T), cudaMemcpyDeviceToDevice, c->st));
+  RCPG_CUDA(cudaStreamSynchronize(c->st));
+}
+
+struct AlsResult {
+  int iterations = 0;
+  bool converged = false;
+  std::vector<double> fit, sec;
+};
+
+// solve.hpp:183-262 on a device tensor. Leaves factors/weights on device in
+// the context's ALS buffers (factor m at fs.f[m]); returns the trace.
+template <typename T>
+AlsResult run_als(rcpg_context* c, const T* B, const i64* shape, int order, const rcpg_decompose_config& cfg,
+                  FactorSet<T>& fs, T*& weights) {
+  check_arg(cfg.rank >= 1, "solve: rank must be at least 1");
+  check_arg(cfg.tol > 0, "solve: tolerance must be positive");
+  check_arg(cfg.max_iter >= 1, "solve: iteration limit must be at least 1");
+  const int R = int(cfg.rank);
+  check_arg(R <= kMaxRank, "solve: rank above the supported maximum (128)");
+  const int sms = device_caps().num_sms;
+  i64 S = 1, sum_ext = 0, max_ext = 0, max_J = 0;
+  for (int m = 0; m < order; ++m) {
+    S *= shape[m];
+    sum_ext += shape[m];
+    max_ext = std::max(max_ext, shape[m]);
+  }
+  for (int m = 0; m < order; ++m) max_J = std::max(max_J, S / shape[m]);
+  c->nrm.ensure(4096 * sizeof(double));
+  c->scratch.ensure(size_t(sms) * 8 * sizeof(double) + 64);
+  {
+    ScopedPass sp(c, "als_norm", double(S) * sizeof(T));
+    norm_and_finite<T>(B, S, c->nrm.as<double>(), c->scratch.as<double>(), sms, c->st);
+  }
+  double h[2];
+  read_doubles(c, c->nrm.as<double>(), h, 2);
+  if (h[1] != 0.0) throw SolverFailure("solve: input values are not finite", 0);
+  check_arg(h[0] > 0.0, "solve: tensor norm must be positive");
+
+  // buffers
+  c->als_f.ensure(size_t(sum_ext) * R * sizeof(T));
+  c->als_g.ensure(size_t(order) * R * R * sizeof(T));
+  c->als_w.ensure(size_t(std::max<i64>(max_ext * std::max<i64>(R, max_ext), 1)) * sizeof(T));
+  c->als_kr.ensure(size_t(max_J) * R * sizeof(T));
+  c->als_work.ensure(size_t(std::max<i64>(3 * max_ext * max_ext + 8 * max_ext, 8 * R * R + 8 * R) + 64) *
+                     sizeof(double));
+  c->als_trace.ensure(size_t(2) * cfg.max_iter * sizeof(double));
+  c->als_state.ensure(sizeof(AlsState));
+  c->weights.ensure(size_t(R) * sizeof(T));
+  fs = FactorSet<T>{};
+  fs.order = order;
+  fs.rank = R;
+  i64 off = 0;
+  for (int m = 0; m < order; ++m) {
+    fs.f[m] = c->als_f.as<T>() + off;
+    fs.gram[m] = c->als_g.as<T>() + i64(m) * R * R;
+    fs.extent[m] = shape[m];
+    off += shape[m] * R;
+  }
+  weights = c->weights.as<T>();
+  AlsState* state = c->als_state.as<AlsState>();
+  double* tfit = c->als_trace.as<double>();
+  double* tsec = tfit + cfg.max_iter;
+
+  als_start(state, c->nrm.as<double>(), c->st);
+  {
+    ScopedPass sp(c, "als_init", 0.0);
+    zero_factor<T>(fs.f[0], shape[0], R, fs.gram[0], c->st);
+    for (int m = 1; m < order; ++m) {
+      const ModeView v = mode_view(shape, order, m);
+      if (cfg.init == RCPG_INIT_EIGENVECTORS) {
+        check_arg(shape[m] <= 2048, "init_factors: eigenvector init supports extents up to 2048");
+        // Gram = B_(m) B_(m)^T as a sketch of B against itself.
+        const i64 scr = sketch_scratch_elems<T>(v, shape[m], sms);
+        c->scratch.ensure(size_t(scr) * sizeof(T));
+        sketch<T>(B, v, B, shape[m], c->als_w.as<T>(), c->scratch.as<T>(), scr, sms, c->st);
+      }
+      init_factor_from_gram<T>(c->als_w.as<T>(), int(shape[m]), R, m, cfg.seed, cfg.init, fs.f[m], fs.gram[m],
+                               c->als_work.as<double>(), c->st);
+    }
+    // weights = ones
+    std::vector<T> ones(size_t(R), T(1));
+    RCPG_CUDA(cudaMemcpyAsync(weights, ones.data(), sizeof(T) * R, cudaMemcpyHostToDevice, c->st));
+    RCPG_CUDA(cudaStreamSynchronize(c->st));
+  }
+
+  AlsState hs{};
+  int enqueued = 0, batch = 2;
+  {
+    ScopedPass sp(c, "als_iterations", 0.0);
+    while (enqueued < cfg.max_iter) {
+      const int nb = std::min(batch, cfg.max_iter - enqueued);
+      for (int q = 0; q < nb; ++q) {
+        for (int m = 0; m < order; ++m) {
+          const ModeView v = mode_view(shape, order, m);
+          const int* skip = &state->done;
+          kr_panel<T>(fs, shape, m, c->als_kr.as<T>(), c->st, skip);
+          const i64 scr = sketch_scratch_elems<T>(v, R, sms);
+          c->scratch.ensure(size_t(scr) * sizeof(T));
+          sketch<T>(B, v, c->als_kr.as<T>(), R, c->als_w.as<T>(), c->scratch.as<T>(), scr, sms, c->st, skip);
+          als_update<T>(fs, m, c->als_w.as<T>(), weights, cfg.tol, cfg.max_iter, tfit, tsec, state,
+                        c->als_work.as<double>(), c->st);
+        }
+      }
+      enqueued += nb;
+      RCPG_CUDA(cudaMemcpyAsync(&hs, state, sizeof(AlsState), cudaMemcpyDeviceToHost, c->st));
+      RCPG_CUDA(cudaStreamSynchronize(c->st));
+      if (hs.done) break;
+      batch = std::min(batch * 2, 32);
+    }
+  }
+  if (hs.error_it > 0) throw SolverFailure("als: fit became non-finite", hs.error_it);
+  AlsResult res;
+  res.iterations = hs.it - 1;
+  res.converged = hs.converged != 0;
+  res.fit.resize(size_t(res.iterations));
+  res.sec.resize(size_t(res.iterations));
+  if (res.iterations > 0) {
+    RCPG_CUDA(cudaMemcpyAsync(res.fit.data(), tfit, sizeof(double) * res.iterations, cudaMemcpyDeviceToHost, c->st));
+    RCPG_CUDA(cudaMemcpyAsync(res.sec.data(), tsec, sizeof(double) * res.iterations, cudaMemcpyDeviceToHost, c->st));
+  }
+  // model = normalize(model) (solve.hpp:259)
+  c->small_tmp.ensure(size_t(sum_ext * R + R) * sizeof(T));
+  normalize_model<T>(fs, weights, c->small_tmp.as<T>(), c->st);
+  RCPG_CUDA(cudaStreamSynchronize(c->st));
+  return res;
+}
+
+template <typename T>
+double run_relerr(rcpg_context* c, const T* X, const i64* shape, int order, const FactorSet<T>& fs, const T* w) {
+  const int sms = device_caps().num_sms;
+  i64 S = 1;
+  for (int m = 0; m < order; ++m) S *= shape[m];
+  c->scratch.ensure(residual_scratch_doubles(sms) * sizeof(double));
+  c->nrm.ensure(4096 * sizeof(double));
+  {
+    ScopedPass sp(c, "relerr", double(S) * sizeof(T));
+    residual_norms<T>(X, shape, order, fs, w, c->nrm.as<double>(), c->scratch.as<double>(), sms, c->st);
+  }
+  double h[2];
+  read_doubles(c, c->nrm.as<double>(), h, 2);
+  check_arg(h[1] > 0.0, "relative_error: tensor norm must be positive");
+  return std::sqrt(h[0]) / std::sqrt(h[1]);
+}
+
+template <typename T>
+void copy_result(rcpg_context* c, const FactorSet<T>& fs, const T* w, const AlsResult& ar, double relerr,
+                 rcpg_result* res) {
+  const int R = fs.rank;
+  if (res->weights) RCPG_CUDA(cudaMemcpyAsync(res->weights, w, sizeof(T) * R, cudaMemcpyDeviceToHost, c->st));
+  if (res->factors) {
+    i64 off = 0;
+    for (int m = 0; m < fs.order; ++m) {
+      RCPG_CUDA(cudaMemcpyAsync(static_cast<T*>(res->factors) + off, fs.f[m], sizeof(T) * fs.extent[m] * R,
+                                cudaMemcpyDeviceToHost, c->st));
+      off += fs.extent[m] * R;
+    }
+  }
+  RCPG_CUDA(cudaStreamSynchronize(c->st));
+  const int n = std::min<int>(ar.iterations, res->trace_capacity);
+  for (int i = 0; i < n; ++i) {
+    if (res->trace_iteration) res->trace_iteration[i] = i + 1;
+    if (res->trace_fit) res->trace_fit[i] = ar.fit[size_t(i)];
+    if (res->trace_seconds) res->trace_seconds[i] = ar.sec[size_t(i)];
+  }
+  res->iterations = ar.iterations;
+  res->converged = ar.converged ? 1 : 0;
+  res->final_relative_error = relerr;
+}
+
+// solve.hpp:381-398
+template <typename T>
+void run_decompose(rcpg_context* c, const rcpg_tensor* t, const rcpg_decompose_config& cfg, rcpg_result* res) {
+  check_arg(cfg.method == RCPG_ALS, "decompose: only the ALS solver is on this path (bcd is out of scope)");
+  FactorSet<T> fs;
+  T* w = nullptr;
+  if (!cfg.randomized) {
+    AlsResult ar = run_als<T>(c, static_cast<const T*>(t->d), t->shape, t->order, cfg, fs, w);
+    const double re = run_relerr<T>(c, static_cast<const T*>(t->d), t->shape, t->order, fs, w);
+    copy_result<T>(c, fs, w, ar, re, res);
+    return;
+  }
+  CompressCfg cc = to_cfg(cfg.compress);
+  if (cc.target_rank == 0) cc.target_rank = cfg.rank;
+  check_arg(cc.target_rank == cfg.rank, "decompose: compression target rank must equal the CP rank");
+  rcpg_compressed comp;
+  run_compress<T>(c, t, cc, &comp);
+  AlsResult ar = run_als<T>(c, comp.data.as<T>(), comp.shape, comp.order, cfg, fs, w);
+  // recover (kruskal.hpp:198-220): A_n = Q_n A~_n, then normalize
+  const int R = int(cfg.rank);
+  i64 sum_ext = 0;
+  for (int m = 0; m < t->order; ++m) sum_ext += t->shape[m];
+  DevBuf full;
+  full.ensure(size_t(sum_ext) * R * sizeof(T));
+  FactorSet<T> big = fs;
+  {
+    ScopedPass sp(c, "recover", 0.0);
+    i64 off = 0;
+    for (int m = 0; m < t->order; ++m) {
+      T* dst = full.as<T>() + off;
+      const BasisRec& b = comp.bases[m];
+      if (b.identity) {
+        check_arg(b.dim == fs.extent[m], "recover: identity basis extent mismatch");
+        RCPG_CUDA(cudaMemcpyAsync(dst, fs.f[m], sizeof(T) * fs.extent[m] * R, cudaMemcpyDeviceToDevice, c->st));
+      } else {
+        check_arg(b.cols == fs.extent[m], "recover: basis columns must match the compressed extent");
+        small_gemm<T>(b.q.as<T>(), b.dim, b.cols, fs.f[m], R, dst, c->st);
+      }
+      big.f[m] = dst;
+      big.extent[m] = t->shape[m];
+      off += t->shape[m] * R;
+    }
+    c->small_tmp.ensure(size_t(sum_ext * R + R) * sizeof(T));
+    normalize_model<T>(big, w, c->small_tmp.as<T>(), c->st);
+  }
+  const double re = run_relerr<T>(c, static_cast<const T*>(t->d), t->shape, t->order, big, w);
+  copy_result<T>(c, big, w, ar, re, res);
+  full.release();
+}
+
+template <typename F>
+rcpg_status guarded(rcpg_context* c, F&& f) {
+  try {
+    if (c) {
+      c->err.clear();
+      c->err_it = -1;
+      RCPG_CUDA(cudaSetDevice(c->device));
+    }
+    f();
+    return RCPG_OK;
+  } catch (const InvalidArgument& e) {
+    if (c) c->err = e.what();
+    return RCPG_INVALID_ARGUMENT;
+  } catch (const SolverFailure& e) {
+    if (c) {
+      c->err = e.what();
+      c->err_it = e.iteration;
+    }
+    return RCPG_SOLVER_ERROR;
+  } catch (const CudaFailure& e) {
+    if (c) c->err = e.what();
+    return e.code == cudaErrorMemoryAllocation ? RCPG_OOM : RCPG_CUDA_ERROR;
+  } catch (const std::exception& e) {
+    if (c) c->err = e.what();
+    return RCPG_CUDA_ERROR;
+  }
+}
+
+void validate_tensor_args(int dtype, int order, const int64_t* shape) {
+  check_arg(dtype == RCPG_F32 || dtype == RCPG_F64, "Tensor: unsupported dtype");
+  check_arg(order >= 1, "Tensor: order must be at least 1");
+  check_arg(order <= kMaxOrder, "Tensor: order above the supported maximum (8)");
+  i64 total = 1;
+  for (int m = 0; m < order; ++m) {
+    check_arg(shape[m] >= 1, "shape: every extent must be at least 1");
+    check_arg(total <= INT64_MAX / shape[m], "shape: element count overflows Index");
+    total *= shape[m];
+  }
+}
+
+}  // namespace
+
+// ===================================================================== ABI
+extern "C" {
+
+const char* rcpg_version(void) { return "rcpg 0.1 (sm_100a)"; }
+
+rcpg_status rcpg_create(int device, rcpg_context** out) {
+  if (!out) return RCPG_INVALID_ARGUMENT;
+  *out = nullptr;
+  auto c = std::make_unique<rcpg_context>();
+  c->device = device;
+  const rcpg_status s = guarded(nullptr, [&] {
+    int n = 0;
+    RCPG_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) throw CudaFailure("rcpg_create: no such CUDA device", cudaErrorInvalidDevice);
+    RCPG_CUDA(cudaSetDevice(device));
+    RCPG_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    c->bar.ensure(sizeof(GridBarrier));
+    RCPG_CUDA(cudaMemset(c->bar.p, 0, sizeof(GridBarrier)));
+    (void)device_caps();
+  });
+  if (s == RCPG_OK) *out = c.release();
+  return s;
+}
+
+void rcpg_destroy(rcpg_context* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->st);
+  for (auto& r : c->passes) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (DevBuf* b : {&c->panelA, &c->panelB, &c->work0, &c->work1, &c->Y, &c->Qy, &c->scratch, &c->keys, &c->cands,
+                    &c->bar, &c->info, &c->part, &c->tau, &c->diag, &c->als_f, &c->als_g, &c->als_w, &c->als_kr,
+                    &c->als_work, &c->als_trace, &c->als_state, &c->weights, &c->small_tmp, &c->nrm})
+    b->release();
+  cudaStreamDestroy(c->st);
+  delete c;
+}
+
+const char* rcpg_last_error(const rcpg_context* c) { return c ? c->err.c_str() : "no context"; }
+int32_t rcpg_last_error_iteration(const rcpg_context* c) { return c ? c->err_it : -1; }
+
+rcpg_status rcpg_tensor_upload(rcpg_context* c, rcpg_dtype dtype, int32_t order, const int64_t* shape,
+                               const void* host, rcpg_tensor** out) {
+  return guarded(c, [&] {
+    validate_tensor_args(dtype, order, shape);
+    auto t = std::make_unique<rcpg_tensor>();
+    t->ctx = c;
+    t->dtype = dtype;
+    t->order = order;
+    t->size = 1;
+    for (int m = 0; m < order; ++m) {
+      t->shape[m] = shape[m];
+      t->size *= shape[m];
+    }
+    const size_t bytes = size_t(t->size) * dsize(dtype);
+    cudaError_t e = cudaMalloc(&t->d, bytes);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      throw CudaFailure("rcpg_tensor_upload: cudaMalloc failed", e);
+    }
+    t->owned = true;
+    RCPG_CUDA(cudaMemcpyAsync(t->d, host, bytes, cudaMemcpyHostToDevice, c->st));
+    RCPG_CUDA(cudaStreamSynchronize(c->st));
+    *out = t.release();
+  });
+}
+
+rcpg_status rcpg_tensor_wrap_device(rcpg_context* c, rcpg_dtype dtype, int32_t order, const int64_t* shape,
+                                    void* device_ptr, rcpg_tensor** out) {
+  return guarded(c, [&] {
+    validate_tensor_args(dtype, order, shape);
+    auto t = std::make_unique<rcpg_tensor>();
+    t->ctx = c;
+    t->dtype = dtype;
+    t->order = order;
+    t->size = 1;
+    for (int m = 0; m < order; ++m) {
+      t->shape[m] = shape[m];
+      t->size *= shape[m];
+    }
+    t->d = device_ptr;
+    t->owned = false;
+    *out = t.release();
+  });
+}
+
+rcpg_status rcpg_tensor_download(rcpg_context* c, const rcpg_tensor* t, void* host) {
+  return guarded(c, [&] {
+    RCPG_CUDA(cudaMemcpyAsync(host, t->d, size_t(t->size) * dsize(t->dtype), cudaMemcpyDeviceToHost, c->st));
+    RCPG_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+
+void* rcpg_tensor_device_ptr(const rcpg_tensor* t) { return t ? t->d : nullptr; }
+
+void rcpg_tensor_free(rcpg_tensor* t) {
+  if (!t) return;
+  if (t->owned && t->d) cudaFree(t->d);
+  delete t;
+}
+
+rcpg_status rcpg_compress(rcpg_context* c, const rcpg_tensor* t, const rcpg_compress_config* cfg,
+                          rcpg_compressed** out) {
+  return guarded(c, [&] {
+    c->pass_used = 0;
+    auto comp = std::make_unique<rcpg_compressed>();
+    const CompressCfg cc = to_cfg(*cfg);
+    if (t->dtype == RCPG_F64)
+      run_compress<double>(c, t, cc, comp.get());
+    else
+      run_compress<float>(c, t, cc, comp.get());
+    *out = comp.release();
+  });
+}
+
+int32_t rcpg_compressed_order(const rcpg_compressed* c) { return c->order; }
+void rcpg_compressed_shape(const rcpg_compressed* c, int64_t* shape) {
+  for (int m = 0; m < c->order; ++m) shape[m] = c->shape[m];
+}
+rcpg_status rcpg_compressed_download(rcpg_context* c, const rcpg_compressed* comp, void* host) {
+  return guarded(c, [&] {
+    RCPG_CUDA(cudaMemcpyAsync(host, comp->data.p, size_t(comp->size) * dsize(comp->dtype), cudaMemcpyDeviceToHost,
+                              c->st));
+    RCPG_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+void rcpg_compressed_basis_info(const rcpg_compressed* c, int32_t mode, int32_t* identity, int64_t* dim,
+                                int64_t* cols, int32_t* rank_warning) {
+  const BasisRec& b = c->bases[size_t(mode)];
+  if (identity) *identity = b.identity ? 1 : 0;
+  if (dim) *dim = b.dim;
+  if (cols) *cols = b.identity ? 0 : b.cols;
+  if (rank_warning) *rank_warning = b.rank_warning ? 1 : 0;
+}
+rcpg_status rcpg_compressed_basis_download(rcpg_context* c, const rcpg_compressed* comp, int32_t mode, void* host) {
+  return guarded(c, [&] {
+    const BasisRec& b = comp->bases[size_t(mode)];
+    check_arg(!b.identity, "basis: identity-tagged mode has no explicit matrix");
+    RCPG_CUDA(cudaMemcpyAsync(host, b.q.p, size_t(b.dim * b.cols) * dsize(comp->dtype), cudaMemcpyDeviceToHost,
+                              c->st));
+    RCPG_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+void rcpg_compressed_free(rcpg_compressed* c) { delete c; }
+
+rcpg_status rcpg_decompose(rcpg_context* c, const rcpg_tensor* t, const rcpg_decompose_config* cfg,
+                           rcpg_result* res) {
+  return guarded(c, [&] {
+    c->pass_used = 0;
+    if (t->dtype == RCPG_F64)
+      run_decompose<double>(c, t, *cfg, res);
+    else
+      run_decompose<float>(c, t, *cfg, res);
+  });
+}
+
+rcpg_status rcpg_decompose_host(rcpg_context* c, rcpg_dtype dtype, int32_t order, const int64_t* shape,
+                                const void* host, const rcpg_decompose_config* cfg, rcpg_result* res) {
+  rcpg_tensor* t = nullptr;
+  rcpg_status s = rcpg_tensor_upload(c, dtype, order, shape, host, &t);
+  if (s != RCPG_OK) return s;
+  s = rcpg_decompose(c, t, cfg, res);
+  rcpg_tensor_free(t);
+  return s;
+}
+
+rcpg_status rcpg_relative_error(rcpg_context* c, const rcpg_tensor* t, int64_t rank, const void* weights,
+                                const void* factors, double* out) {
+  return guarded(c, [&] {
+    check_arg(rank >= 1, "Kruskal: rank must be at least 1");
+    const size_t b = dsize(t->dtype);
+    i64 sum_ext = 0;
+    for (int m = 0; m < t->order; ++m) sum_ext += t->shape[m];
+    DevBuf f, w;
+    f.ensure(size_t(sum_ext) * rank * b);
+    w.ensure(size_t(rank) * b);
+    RCPG_CUDA(cudaMemcpyAsync(f.p, factors, size_t(sum_ext) * rank * b, cudaMemcpyHostToDevice, c->st));
+    RCPG_CUDA(cudaMemcpyAsync(w.p, weights, size_t(rank) * b, cudaMemcpyHostToDevice, c->st));
+    auto run = [&](auto tag) {
+      using T = decltype(tag);
+      FactorSet<T> fs{};
+      fs.order = t->order;
+      fs.rank = int(rank);
+      i64 off = 0;
+      for (int m = 0; m < t->order; ++m) {
+        fs.f[m] = f.as<T>() + off;
+        fs.extent[m] = t->shape[m];
+        off += t->shape[m] * rank;
+      }
+      *out = run_relerr<T>(c, static_cast<const T*>(t->d), t->shape, t->order, fs, w.as<T>());
+    };
+    if (t->dtype == RCPG_F64)
+      run(double{});
+    else
+      run(float{});
+    f.release();
+    w.release();
+  });
+}
+
+rcpg_status rcpg_sketch_matrix(rcpg_context* c, rcpg_dtype dtype, uint64_t seed, int64_t mode, int64_t rows,
+                               int64_t cols, int32_t distribution, void* host) {
+  return guarded(c, [&] {
+    // Omega_n is rows x cols column-major: as a panel with L = 1, R = rows
+    // and an identity Kolda map its layout is exactly column-major.
+    ModeView v;
+    v.L = 1;
+    v.I = 1;
+    v.R = rows;
+    const KoldaMap km = identity_kolda(rows);
+    DevBuf buf;
+    buf.ensure(size_t(rows) * cols * dsize(dtype));
+    if (dtype == RCPG_F64)
+      omega_panel<double>(seed, mode, km, v, cols, distribution, buf.as<double>(), c->st);
+    else
+      omega_panel<float>(seed, mode, km, v, cols, distribution, buf.as<float>(), c->st);
+    RCPG_CUDA(cudaMemcpyAsync(host, buf.p, size_t(rows) * cols * dsize(dtype), cudaMemcpyDeviceToHost, c->st));
+    RCPG_CUDA(cudaStreamSynchronize(c->st));
+    buf.release();
+  });
+}
+
+rcpg_status rcpg_plu_basis(rcpg_context* c, rcpg_dtype dtype, int64_t rows, int64_t cols, const void* in,
+                           void* out) {
+  return guarded(c, [&] {
+    check_arg(cols <= kMaxPanelCols, "plu_basis: too many columns");
+    const size_t b = dsize(dtype);
+    const i64 r = std::min(rows, cols);
+    DevBuf A, Z;
+    A.ensure(size_t(rows) * cols * b);
+    Z.ensure(size_t(rows) * r * b);
+    RCPG_CUDA(cudaMemcpyAsync(A.p, in, size_t(rows) * cols * b, cudaMemcpyHostToDevice, c->st));
+    FactorWork w = factor_work(c, rows);
+    if (dtype == RCPG_F64)
+      plu_basis<double>(A.as<double>(), Z.as<double>(), rows, rows, int(cols), identity_kolda(rows), w, c->st);
+    else
+      plu_basis<float>(A.as<float>(), Z.as<float>(), rows, rows, int(cols), identity_kolda(rows), w, c->st);
+    RCPG_CUDA(cudaMemcpyAsync(out, Z.p, size_t(rows) * r * b, cudaMemcpyDeviceToHost, c->st));
+    RCPG_CUDA(cudaStreamSynchronize(c->st));
+    A.release();
+    Z.release();
+  });
+}
+
+rcpg_status rcpg_thin_qr(rcpg_context* c, rcpg_dtype dtype, int64_t rows, int64_t cols, const void* in, void* out,
+                         int32_t* rank_warning) {
+  return guarded(c, [&] {
+    check_arg(cols <= kMaxPanelCols, "thin_qr: too many columns");
+    const size_t b = dsize(dtype);
+    const i64 r = std::min(rows, cols);
+    DevBuf A, Q;
+    A.ensure(size_t(rows) * cols * b);
+    Q.ensure(size_t(rows) * r * b);
+    RCPG_CUDA(cudaMemcpyAsync(A.p, in, size_t(rows) * cols * b, cudaMemcpyHostToDevice, c->st));
+    FactorWork w = factor_work(c, rows);
+    if (dtype == RCPG_F64)
+      thin_qr<double>(A.as<double>(), Q.as<double>(), rows, rows, int(cols), identity_kolda(rows), w, w.info + 1,
+                      c->st);
+    else
+      thin_qr<float>(A.as<float>(), Q.as<float>(), rows, rows, int(cols), identity_kolda(rows), w, w.info + 1, c->st);
+    int rw = 0;
+    RCPG_CUDA(cudaMemcpyAsync(out, Q.p, size_t(rows) * r * b, cudaMemcpyDeviceToHost, c->st));
+    RCPG_CUDA(cudaMemcpyAsync(&rw, w.info + 1, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    RCPG_CUDA(cudaStreamSynchronize(c->st));
+    if (rank_warning) *rank_warning = rw;
+    A.release();
+    Q.release();
+  });
+}
+
+int32_t rcpg_pass_timings(const rcpg_context* c, char* names, int32_t names_cap, double* ms, double* bytes,
+                          int32_t cap) {
+  if (!c) return 0;
+  int32_t n = 0;
+  size_t pos = 0;
+  for (size_t i = 0; i < c->pass_used && n < cap; ++i) {
+    const PassRecord& r = c->passes[i];
+    float t = 0;
+    if (cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) t = -1;
+    if (ms) ms[n] = t;
+    if (bytes) bytes[n] = r.bytes;
+    if (names && pos + r.name.size() + 1 <= size_t(names_cap)) {
+      std::memcpy(names + pos, r.name.c_str(), r.name.size() + 1);
+      pos += r.name.size() + 1;
+    }
+    ++n;
+  }
+  return n;
+}
+
+int64_t rcpg_kernel_launches(const rcpg_context*) { return launch_counter().load(); }
+
+rcpg_status rcpg_synth(rcpg_context* c, rcpg_dtype dtype, int32_t order, const int64_t* shape, int64_t rank,
+                       const double* weights, const double* factors, double snr, uint64_t noise_seed,
+                       rcpg_tensor** out) {
+  return guarded(c, [&] {
+    validate_tensor_args(dtype, order, shape);
+    i64 sum_ext = 0, total = 1;
+    for (int m = 0; m < order; ++m) {
+      sum_ext += shape[m];
+      total *= shape[m];
+    }
+    DevBuf f, w, scr;
+    f.ensure(size_t(sum_ext) * rank * sizeof(double));
+    w.ensure(size_t(rank) * sizeof(double));
+    const int sms = device_caps().num_sms;
+    scr.ensure(size_t(sms) * 8 * 2 * sizeof(double) + 256);
+    RCPG_CUDA(cudaMemcpyAsync(f.p, factors, size_t(sum_ext) * rank * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    RCPG_CUDA(cudaMemcpyAsync(w.p, weights, size_t(rank) * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    const double* fp[kMaxOrder];
+    i64 off = 0;
+    for (int m = 0; m < order; ++m) {
+      fp[m] = f.as<double>() + off;
+      off += shape[m] * rank;
+    }
+    auto t = std::make_unique<rcpg_tensor>();
+    t->ctx = c;
+    t->dtype = dtype;
+    t->order = order;
+    t->size = total;
+    for (int m = 0; m < order; ++m) t->shape[m] = shape[m];
+    cudaError_t e = cudaMalloc(&t->d, size_t(total) * dsize(dtype));
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      throw CudaFailure("rcpg_synth: cudaMalloc failed", e);
+    }
+    t->owned = true;
+    if (dtype == RCPG_F64)
+      synth_tensor<double>(shape, order, int(rank), w.as<double>(), fp, snr, noise_seed, static_cast<double*>(t->d),
+                           scr.as<double>(), sms, c->st);
+    else
+      synth_tensor<float>(shape, order, int(rank), w.as<double>(), fp, snr, noise_seed, static_cast<float*>(t->d),
+                          scr.as<double>(), sms, c->st);
+    RCPG_CUDA(cudaStreamSynchronize(c->st));
+    f.release();
+    w.release();
+    scr.release();
+    *out = t.release();
+  });
+}
+
+rcpg_status rcpg_synchronize(rcpg_context* c) {
+  return guarded(c, [&] { RCPG_CUDA(cudaStreamSynchronize(c->st)); });
+}
+
+}  // extern "C"

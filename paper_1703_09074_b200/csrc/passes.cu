@@ -1,0 +1,185 @@
+// SPDX-License-Identifier: MIT
+// Host launchers for the streamed tensor passes (see passes.cuh) and the
+// Omega generator (compress.hpp:118-124, random.hpp:75-94).
+#include "passes.cuh"
+#include "rng.cuh"
+#include "runtime.cuh"
+
+namespace rcpg {
+
+namespace {
+
+template <typename T>
+struct TileCfg;
+template <>
+struct TileCfg<float> {
+  static constexpr int BM = 128, BK = 32;
+};
+template <>
+struct TileCfg<double> {
+  static constexpr int BM = 64, BK = 32;
+};
+
+template <typename T, int BM, int BN, int BK, bool TXM, class LD, class EP>
+void launch_tile_gemm(dim3 grid, const LD& ld, const EP& ep, cudaStream_t st) {
+  auto kern = tile_gemm_kernel<T, BM, BN, BK, TXM, LD, EP>;
+  const size_t smem = sizeof(TileSmem<T, BM, BN, BK>);
+  static bool configured = false;  // per instantiation
+  if (!configured) {
+    RCPG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    configured = true;
+  }
+  kern<<<grid, kThreads, smem, st>>>(ld, ep);
+  count_launch();
+  RCPG_LAUNCHED();
+}
+
+int pick_bn(i64 cols) {
+  if (cols <= 16) return 16;
+  if (cols <= 32) return 32;
+  if (cols <= 48) return 48;
+  if (cols <= 64) return 64;
+  return 80;
+}
+
+template <typename T>
+__global__ void reduce_partials_kernel(const T* __restrict__ part, i64 splits, i64 n, T* __restrict__ out,
+                                       const int* skip) {
+  if (skip != nullptr && *skip) return;
+  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < n; e += i64(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (i64 q = 0; q < splits; ++q) s += double(part[q * n + e]);
+    out[e] = T(s);
+  }
+}
+
+template <typename T, int BN>
+void sketch_bn(const T* X, ModeView v, const T* P, i64 cols, T* part, i64 splits, i64 tiles_per_split,
+               i64 total, cudaStream_t st, const int* skip) {
+  constexpr int BM = TileCfg<T>::BM, BK = TileCfg<T>::BK;
+  const i64 mt = ceil_div(v.I, BM), nt = ceil_div(cols, BN);
+  dim3 grid{unsigned(mt), unsigned(splits), unsigned(nt)};
+  SketchEpilogue<T, BM, BN> ep{part, v.I, cols};
+  if (v.R > 1) {
+    SketchLoader<T, BM, BN, BK> ld{X, P, v.L, v.I, v.R, cols, ceil_div(v.R, BK), tiles_per_split, total, skip};
+    launch_tile_gemm<T, BM, BN, BK, false>(grid, ld, ep, st);
+  } else {
+    SketchLastLoader<T, BM, BN, BK> ld{X, P, v.L, v.I, cols, tiles_per_split, total, skip};
+    launch_tile_gemm<T, BM, BN, BK, false>(grid, ld, ep, st);
+  }
+}
+
+template <typename T>
+void sketch_plan(ModeView v, i64 cols, int num_sms, i64& splits, i64& tiles_per_split, i64& total) {
+  constexpr int BM = TileCfg<T>::BM, BK = TileCfg<T>::BK;
+  const int BN = pick_bn(cols);
+  const i64 mt = ceil_div(v.I, BM), nt = ceil_div(cols, BN);
+  total = v.R > 1 ? v.L * ceil_div(v.R, BK) : ceil_div(v.L, BK);
+  i64 want = ceil_div(i64(4) * num_sms, mt * nt);
+  want = std::max<i64>(1, std::min<i64>(want, 65535));
+  tiles_per_split = std::max<i64>(1, ceil_div(total, want));
+  splits = ceil_div(total, tiles_per_split);
+}
+
+}  // namespace
+
+template <typename T>
+i64 sketch_scratch_elems(ModeView v, i64 cols, int num_sms) {
+  i64 splits, tps, total;
+  sketch_plan<T>(v, cols, num_sms, splits, tps, total);
+  return splits * cols * v.I;
+}
+
+template <typename T>
+void sketch(const T* X, ModeView v, const T* P, i64 cols, T* Y, T* scratch, i64 scratch_elems, int num_sms,
+            cudaStream_t st, const int* skip) {
+  i64 splits, tps, total;
+  sketch_plan<T>(v, cols, num_sms, splits, tps, total);
+  if (splits * cols * v.I > scratch_elems) throw std::runtime_error("sketch: scratch too small");
+  switch (pick_bn(cols)) {
+    case 16: sketch_bn<T, 16>(X, v, P, cols, scratch, splits, tps, total, st, skip); break;
+    case 32: sketch_bn<T, 32>(X, v, P, cols, scratch, splits, tps, total, st, skip); break;
+    case 48: sketch_bn<T, 48>(X, v, P, cols, scratch, splits, tps, total, st, skip); break;
+    case 64: sketch_bn<T, 64>(X, v, P, cols, scratch, splits, tps, total, st, skip); break;
+    default: sketch_bn<T, 80>(X, v, P, cols, scratch, splits, tps, total, st, skip); break;
+  }
+  const i64 n = cols * v.I;
+  const int blocks = int(std::min<i64>(ceil_div(n, 256), 4 * num_sms));
+  reduce_partials_kernel<T><<<blocks, 256, 0, st>>>(scratch, splits, n, Y, skip);
+  count_launch();
+  RCPG_LAUNCHED();
+}
+
+namespace {
+template <typename T, int BN>
+void project_bn(const T* X, ModeView v, const T* Q, i64 ldq, i64 cols, T* O, cudaStream_t st) {
+  constexpr int BM = TileCfg<T>::BM, BK = TileCfg<T>::BK;
+  const i64 nt = ceil_div(cols, BN), kt = ceil_div(v.I, BK);
+  if (v.R > 1) {
+    // batch over a in chunks of 65535 (gridDim.y limit)
+    for (i64 a0 = 0; a0 < v.L; a0 += 65535) {
+      const i64 na = std::min<i64>(65535, v.L - a0);
+      dim3 grid{unsigned(ceil_div(v.R, BM)), unsigned(na), unsigned(nt)};
+      const i64 off = a0 * v.I * v.R, ooff = a0 * cols * v.R;
+      ProjectLoader<T, BM, BN, BK> ld{X + off, Q, v.I, v.R, cols, ldq, kt};
+      ProjectEpilogue<T, BM, BN> ep{O + ooff, v.R, cols};
+      launch_tile_gemm<T, BM, BN, BK, true>(grid, ld, ep, st);
+    }
+  } else {
+    dim3 grid{unsigned(ceil_div(v.L, BM)), 1u, unsigned(nt)};
+    ProjectLastLoader<T, BM, BN, BK> ld{X, Q, v.L, v.I, cols, ldq, kt};
+    ProjectLastEpilogue<T, BM, BN> ep{O, v.L, cols};
+    launch_tile_gemm<T, BM, BN, BK, false>(grid, ld, ep, st);
+  }
+}
+}  // namespace
+
+template <typename T>
+void project(const T* X, ModeView v, const T* Q, i64 ldq, i64 cols, T* O, cudaStream_t st) {
+  switch (pick_bn(cols)) {
+    case 16: project_bn<T, 16>(X, v, Q, ldq, cols, O, st); break;
+    case 32: project_bn<T, 32>(X, v, Q, ldq, cols, O, st); break;
+    case 48: project_bn<T, 48>(X, v, Q, ldq, cols, O, st); break;
+    case 64: project_bn<T, 64>(X, v, Q, ldq, cols, O, st); break;
+    default: project_bn<T, 80>(X, v, Q, ldq, cols, O, st); break;
+  }
+}
+
+// ---------------------------------------------------------------- Omega
+namespace {
+template <typename T>
+__global__ void omega_panel_kernel(u64 s0, KoldaMap km, i64 J, i64 R, i64 cols, int distribution, T* P) {
+  for (i64 s = blockIdx.x * i64(blockDim.x) + threadIdx.x; s < J; s += i64(gridDim.x) * blockDim.x) {
+    const i64 a = s / R, b = s - a * R;
+    const i64 j = kolda_index(km, a, b);
+    T* dst = P + a * cols * R + b;
+    for (i64 c = 0; c < cols; ++c) {
+      const u64 e = u64(c) * u64(J) + u64(j);
+      const double v = distribution == 0 ? normal_at(s0, e) : uniform_sym_at(s0, e);
+      dst[c * R] = T(v);
+    }
+  }
+}
+}  // namespace
+
+template <typename T>
+void omega_panel(u64 seed, i64 mode, const KoldaMap& km, ModeView v, i64 cols, int distribution, T* P,
+                 cudaStream_t st) {
+  const u64 s0 = derive_seed(seed, stream_id(kDomainCompress, u64(mode)));
+  const i64 J = v.L * v.R;
+  const int blocks = int(std::max<i64>(1, std::min<i64>(ceil_div(J, 256), 148 * 16)));
+  omega_panel_kernel<T><<<blocks, 256, 0, st>>>(s0, km, J, v.R, cols, distribution, P);
+  count_launch();
+  RCPG_LAUNCHED();
+}
+
+#define RCPG_INST(T)                                                                                     \
+  template i64 sketch_scratch_elems<T>(ModeView, i64, int);                                              \
+  template void sketch<T>(const T*, ModeView, const T*, i64, T*, T*, i64, int, cudaStream_t, const int*);             \
+  template void project<T>(const T*, ModeView, const T*, i64, i64, T*, cudaStream_t);                    \
+  template void omega_panel<T>(u64, i64, const KoldaMap&, ModeView, i64, int, T*, cudaStream_t);
+RCPG_INST(float)
+RCPG_INST(double)
+#undef RCPG_INST
+
+}  // namespace rcpg

@@ -1,0 +1,54 @@
+// SPDX-License-Identifier: MIT
+// Runtime plumbing shared by the launchers: kernel-launch accounting,
+// device properties, cooperative launches.
+#pragma once
+
+#include <atomic>
+
+#include "common.cuh"
+
+namespace rcpg {
+
+// Total kernels this library has launched (exported through
+// rcpg_kernel_launches; bench.py reports it as gpu_launches).
+inline std::atomic<long long>& launch_counter() {
+  static std::atomic<long long> c{0};
+  return c;
+}
+inline void count_launch(long long n = 1) { launch_counter().fetch_add(n, std::memory_order_relaxed); }
+
+struct DeviceCaps {
+  int device = 0;
+  int num_sms = 148;
+  int max_smem_optin = 227 * 1024;
+};
+
+inline const DeviceCaps& device_caps() {
+  static thread_local DeviceCaps caps = [] {
+    DeviceCaps c;
+    RCPG_CUDA(cudaGetDevice(&c.device));
+    RCPG_CUDA(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, c.device));
+    RCPG_CUDA(cudaDeviceGetAttribute(&c.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
+    return c;
+  }();
+  return caps;
+}
+
+// Largest cooperative grid for `kernel` at `threads` threads and `smem` bytes.
+template <typename K>
+int max_coop_blocks(K kernel, int threads, size_t smem) {
+  int per_sm = 0;
+  RCPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+  if (per_sm < 1) throw std::runtime_error("cooperative kernel does not fit on an SM");
+  return per_sm * device_caps().num_sms;
+}
+
+template <typename K, typename... Args>
+void launch_coop(K kernel, int blocks, int threads, size_t smem, cudaStream_t st, Args... args) {
+  void* argv[] = {static_cast<void*>(&args)...};
+  RCPG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kernel), dim3(blocks), dim3(threads),
+                                        argv, smem, st));
+  count_launch();
+}
+
+}  // namespace rcpg
