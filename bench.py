@@ -1,0 +1,304 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native rCP hot path (rcp::decompose, randomized ALS).
+
+One step = one full rcp::decompose (randomized=true, method=als) of the
+BASELINE.json workload (default C2: 400^3 fp64, rank 20, p=10, q=2, tol 1e-8,
+max 200 iterations; synthetic input of that shape and distribution, generated
+on the device). `value` = device time-to-solution per decomposition with the
+tensor already in HBM (CUDA events on the library's stream, max over ranks);
+`e2e` = the same through the C-ABI with the host tensor copied in (pinned)
+and the model copied out inside the timed region.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+
+Multi-GPU (torchrun, one process per GPU): every rank decomposes its own
+tensor (replicas), value = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+STREAMED = ("sketch", "power_xtq", "power_xz", "project")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class Dist:
+    def __init__(self, world, rank, local):
+        self.world, self.rank, self.local = world, rank, local
+        self.pg = None
+        if world > 1:
+            import torch
+            import torch.distributed as td
+            torch.cuda.set_device(local)
+            td.init_process_group("nccl", device_id=torch.device("cuda", local))
+            self.td, self.torch = td, torch
+
+    def barrier(self):
+        if self.world > 1:
+            self.td.barrier()
+
+    def max(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda")
+        self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.td.destroy_process_group()
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu),
+                 "--query-gpu=clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+                self.lines = [l for l in out.splitlines() if l.strip()]
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for l in getattr(self, "lines", []):
+            p = [x.strip() for x in l.split(",")]
+            try:
+                rows.append((float(p[0]), float(p[1]), float(p[2]), p[3:7]))
+            except (ValueError, IndexError):
+                pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        loaded = [r for r in rows if r[2] > 0] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in loaded for i, v in enumerate(r[3]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(loaded)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def profile_traffic(cfg_name):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            d = json.load(f)
+        return d.get(cfg_name, {}).get("traffic_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def configs(cfg, rcp):
+    seed = cfg.seed
+    cs = rcp.derive_seed(seed, rcp.stream_id(rcp.COMPRESS))
+    return dict(rank=cfg.rank, tol=cfg.tol, max_iter=cfg.max_iter, seed=seed,
+                compress=dict(target_rank=cfg.rank, oversampling=cfg.oversampling,
+                              power_iterations=cfg.power_iterations, seed=cs))
+
+
+def run_reference(args, dist, cfg):
+    """--impl reference: the reference's algorithm on the host cores (oracle
+    port; the Eigen reference itself cannot be built here)."""
+    if dist.rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    cores = os.cpu_count() or 1
+    os.environ["RCPO_THREADS"] = str(cores)
+    import pyoracle as oracle
+    import paper_1703_09074_b200 as rcp
+    x, _ = oracle.synth(cfg.kind, cfg.shape, cfg.rank, cfg.seed, cfg.snr, dtype=cfg.dtype) if cfg.kind != 1 else \
+        oracle.random_lowrank(cfg.shape, cfg.rank, cfg.seed, snr=cfg.snr, noise_seed=cfg.seed)
+    c = configs(cfg, rcp)
+    ocfg = oracle.DecomposeConfig(rank=c["rank"], tol=c["tol"], max_iter=c["max_iter"], seed=c["seed"],
+                                  compress=oracle.CompressConfig(**c["compress"]))
+    times, res = [], None
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        res = oracle.decompose(x, ocfg)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt * 1e3)
+    ms = statistics.median(times)
+    line = {
+        "impl": "reference", "metric": "rCP time-to-solution", "value": ms, "unit": "ms",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64" if cfg.dtype == np.float64 else "f32", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {'x'.join(map(str, cfg.shape))} rank {cfg.rank} p={cfg.oversampling} "
+                               f"q={cfg.power_iterations} tol={cfg.tol:g}", "parallelism": "host threads"},
+        "cpu_baseline": {"value": ms, "unit": "ms", "cores": cores, "kind": "port",
+                         "sample": f"full {cfg.name} decompose per step (C++ oracle restatement, "
+                                   f"std::thread x{cores}, -O3)"},
+        "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "relerr": res.final_relative_error, "iterations": res.iterations,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg, x_host, c):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    cores = os.cpu_count() or 1
+    os.environ["RCPO_THREADS"] = str(cores)
+    import pyoracle as oracle
+    ocfg = oracle.DecomposeConfig(rank=c["rank"], tol=c["tol"], max_iter=c["max_iter"], seed=c["seed"],
+                                  compress=oracle.CompressConfig(**c["compress"]))
+    t0 = time.perf_counter()
+    res = oracle.decompose(x_host, ocfg)
+    dt = (time.perf_counter() - t0) * 1e3
+    return {"value": dt, "unit": "ms", "cores": cores, "kind": "port",
+            "sample": f"1 full {cfg.name} decompose on the downloaded input (C++ oracle, std::thread x{cores})",
+            "relerr": res.final_relative_error, "iterations": res.iterations}
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    dist = Dist(world, rank, local)
+    from paper_1703_09074_b200.synthetic import CONFIGS
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, dist, cfg)
+        dist.close()
+        return
+
+    import paper_1703_09074_b200 as rcp
+    from paper_1703_09074_b200 import synthetic
+    ctx = rcp.Context(local)
+    w, facs = synthetic.model(cfg.kind, cfg.shape, cfg.rank, cfg.seed)
+    X = rcp.DeviceTensor.synth(cfg.shape, w, facs, cfg.snr, cfg.seed, dtype=cfg.dtype, ctx=ctx)
+    c = configs(cfg, rcp)
+    dcfg = rcp.DecomposeConfig(rank=c["rank"], tol=c["tol"], max_iter=c["max_iter"], seed=c["seed"],
+                               compress=rcp.CompressConfig(**c["compress"]))
+    for _ in range(args.warmup):
+        model, trace = rcp.decompose(X, dcfg, ctx=ctx)
+    ctx.synchronize()
+    dist.barrier()
+    l0 = ctx.kernel_launches()
+    pass_ms, pass_bytes = {}, {}
+    with ClockSampler(local) as clk:
+        ctx.event_record(0)
+        for _ in range(args.steps):
+            model, trace = rcp.decompose(X, dcfg, ctx=ctx)
+            for name, ms, by in ctx.pass_timings():
+                pass_ms[name] = pass_ms.get(name, 0.0) + ms
+                pass_bytes[name] = pass_bytes.get(name, 0.0) + by
+        ctx.event_record(1)
+        total_ms = ctx.event_elapsed_ms(0, 1)
+    ctx.synchronize()
+    launches = ctx.kernel_launches() - l0
+    dist.barrier()
+    ms_step = dist.max(total_ms / args.steps)
+
+    # e2e through the C ABI with host buffers (pinned), copies inside the timed region
+    e2e = None
+    x_host = None
+    if not args.no_e2e or (rank == 0 and world == 1 and not args.no_cpu_baseline):
+        x_host = X.download()
+    if not args.no_e2e:
+        ctx.host_register(x_host)
+        for _ in range(max(1, args.warmup // 2)):
+            rcp.decompose(x_host, dcfg, ctx=ctx)
+        ctx.synchronize()
+        dist.barrier()
+        ctx.event_record(2)
+        for _ in range(args.steps):
+            m2, t2 = rcp.decompose(x_host, dcfg, ctx=ctx)
+        ctx.event_record(3)
+        e2e_ms = dist.max(ctx.event_elapsed_ms(2, 3) / args.steps)
+        ctx.host_unregister(x_host)
+        d2h = (cfg.rank + sum(cfg.shape) * cfg.rank) * np.dtype(cfg.dtype).itemsize + 2 * 8 * t2.iterations
+        e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": int(x_host.nbytes), "d2h_bytes_per_step": int(d2h)}
+
+    if rank == 0:
+        peak, peak_kind = measured_peaks()
+        sm_ms = sum(pass_ms.get(n, 0.0) for n in STREAMED)
+        sm_by = sum(pass_bytes.get(n, 0.0) for n in STREAMED)
+        achieved = (sm_by / 1e9) / (sm_ms / 1e3) if sm_ms > 0 else 0.0
+        passes = {n: {"ms_per_step": pass_ms[n] / args.steps,
+                      "gbs": (pass_bytes[n] / 1e9) / (pass_ms[n] / 1e3) if pass_ms[n] > 0 and pass_bytes[n] > 0
+                      else None} for n in pass_ms}
+        line = {
+            "metric": "rCP time-to-solution", "value": ms_step, "unit": "ms", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if cfg.dtype == np.float64 else "f32",
+            "data": "synthetic (device-generated Kruskal model + add_noise, BASELINE.json shape/distribution)",
+            "config": {"workload": f"{cfg.name}: {'x'.join(map(str, cfg.shape))} rank {cfg.rank} "
+                                   f"p={cfg.oversampling} q={cfg.power_iterations} tol={cfg.tol:g} "
+                                   f"max_iter={cfg.max_iter}",
+                       "parallelism": "replicas" if world > 1 else "single GPU",
+                       "l2": "tensor larger than L2 (no flush needed)" if cfg.nbytes() > 126e6 else "L2-resident"},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak if peak else None, "traffic": profile_traffic(cfg.name),
+                         "kernel": "streamed mode-n passes (sketch / X^T Q / X Z / projection)",
+                         "peak_source": peak_kind},
+            "clocks": clk.summary(),
+            "relerr": trace.final_relative_error, "iterations": trace.iterations, "converged": trace.converged,
+            "passes": passes,
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(cfg, x_host, c)
+        print(json.dumps(line), flush=True)
+    dist.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -169,6 +169,13 @@ rcpg_status rcpg_synth(rcpg_context* ctx, rcpg_dtype dtype, int32_t order, const
                        const double* weights, const double* factors, double snr, uint64_t noise_seed,
                        rcpg_tensor** out);
 rcpg_status rcpg_synchronize(rcpg_context* ctx);
+/* CUDA events on the library's stream (device timing of whole calls):
+ * record into slot [0, 64); elapsed milliseconds between two recorded slots. */
+rcpg_status rcpg_event_record(rcpg_context* ctx, int32_t slot);
+rcpg_status rcpg_event_elapsed(rcpg_context* ctx, int32_t slot_a, int32_t slot_b, double* ms);
+/* Page-lock / unlock a host buffer for asynchronous H2D/D2H (e2e timing). */
+rcpg_status rcpg_host_register(rcpg_context* ctx, void* ptr, size_t bytes);
+rcpg_status rcpg_host_unregister(rcpg_context* ctx, void* ptr);
 
 #ifdef __cplusplus
 }

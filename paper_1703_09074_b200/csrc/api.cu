@@ -71,6 +71,7 @@ struct rcpg_context {
   DevBuf panelA, panelB, work0, work1, Y, Qy, scratch, keys, cands, bar, info, part, tau, diag;
   DevBuf als_f, als_g, als_w, als_kr, als_work, als_trace, als_state, weights, small_tmp, nrm;
   std::vector<PassRecord> passes;
+  cudaEvent_t user_events[64] = {};
   size_t pass_used = 0;
   bool timing = true;
 };
@@ -641,6 +642,8 @@ void rcpg_destroy(rcpg_context* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->st);
+  for (auto& e : c->user_events)
+    if (e) cudaEventDestroy(e);
   for (auto& r : c->passes) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
@@ -958,6 +961,33 @@ rcpg_status rcpg_synth(rcpg_context* c, rcpg_dtype dtype, int32_t order, const i
 
 rcpg_status rcpg_synchronize(rcpg_context* c) {
   return guarded(c, [&] { RCPG_CUDA(cudaStreamSynchronize(c->st)); });
+}
+
+rcpg_status rcpg_event_record(rcpg_context* c, int32_t slot) {
+  return guarded(c, [&] {
+    check_arg(slot >= 0 && slot < 64, "event slot out of range");
+    if (!c->user_events[slot]) RCPG_CUDA(cudaEventCreate(&c->user_events[slot]));
+    RCPG_CUDA(cudaEventRecord(c->user_events[slot], c->st));
+  });
+}
+
+rcpg_status rcpg_event_elapsed(rcpg_context* c, int32_t a, int32_t b, double* ms) {
+  return guarded(c, [&] {
+    check_arg(a >= 0 && a < 64 && b >= 0 && b < 64 && c->user_events[a] && c->user_events[b],
+              "event slot not recorded");
+    RCPG_CUDA(cudaEventSynchronize(c->user_events[b]));
+    float t = 0;
+    RCPG_CUDA(cudaEventElapsedTime(&t, c->user_events[a], c->user_events[b]));
+    *ms = t;
+  });
+}
+
+rcpg_status rcpg_host_register(rcpg_context* c, void* ptr, size_t bytes) {
+  return guarded(c, [&] { RCPG_CUDA(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault)); });
+}
+
+rcpg_status rcpg_host_unregister(rcpg_context* c, void* ptr) {
+  return guarded(c, [&] { RCPG_CUDA(cudaHostUnregister(ptr)); });
 }
 
 }  // extern "C"

@@ -204,6 +204,20 @@ class Context:
     def synchronize(self):
         self.check(self.lib.rcpg_synchronize(self.h))
 
+    def event_record(self, slot: int):
+        self.check(self.lib.rcpg_event_record(self.h, slot))
+
+    def event_elapsed_ms(self, a: int, b: int) -> float:
+        out = C.c_double()
+        self.check(self.lib.rcpg_event_elapsed(self.h, a, b, C.byref(out)))
+        return out.value
+
+    def host_register(self, arr: np.ndarray):
+        self.check(self.lib.rcpg_host_register(self.h, arr.ctypes.data, arr.nbytes))
+
+    def host_unregister(self, arr: np.ndarray):
+        self.check(self.lib.rcpg_host_unregister(self.h, arr.ctypes.data))
+
 
 _tls = threading.local()
 
