@@ -177,9 +177,9 @@ def sketch_matrix(seed: int, mode: int, rows: int, cols: int, dist: int = 0,
 def unfold(x: np.ndarray, mode: int) -> np.ndarray:
     x = np.ascontiguousarray(x, dtype=np.float64)
     s, sp = _shape(x.shape)
-    rows = x.shape[mode]
     out = np.zeros(x.size, dtype=np.float64)
     _check(lib().ro_unfold_d(x.ndim, sp, _p(x, dp), mode, _p(out, dp)))
+    rows = x.shape[mode]
     return out.reshape((rows, x.size // rows), order="F")
 
 

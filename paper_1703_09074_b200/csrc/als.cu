@@ -17,6 +17,8 @@ namespace rcpg {
 namespace {
 
 constexpr int kSmallThreads = 1024;
+constexpr int kEigSmemMax = 96;   // Jacobi in shared memory up to 96 x 96
+constexpr int kAlsSmemRank = 64;  // ALS R x R algebra in shared memory up to R = 64
 
 struct ShapeArg {
   i64 e[kMaxOrder];
@@ -35,8 +37,12 @@ template <typename T>
 __global__ void kr_panel_kernel(FactorSet<T> fs, ShapeArg sh, int mode, i64 J, i64 Rr, T* out, const int* skip) {
   if (skip != nullptr && *skip) return;
   const int rank = fs.rank;
-  for (i64 s = blockIdx.x * i64(blockDim.x) + threadIdx.x; s < J; s += i64(gridDim.x) * blockDim.x) {
-    i64 a = s / Rr, b = s - a * Rr;
+  const i64 total = J * rank;
+  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
+    const i64 s = e / rank;
+    const int r = int(e - s * rank);
+    const i64 a0 = s / Rr, b0 = s - a0 * Rr;
+    i64 a = a0, b = b0;
     i64 idx[kMaxOrder];
     for (int k = sh.n - 1; k > mode; --k) {
       idx[k] = b % sh.e[k];
@@ -46,15 +52,12 @@ __global__ void kr_panel_kernel(FactorSet<T> fs, ShapeArg sh, int mode, i64 J, i
       idx[k] = a % sh.e[k];
       a /= sh.e[k];
     }
-    const i64 a0 = s / Rr, b0 = s - a0 * Rr;
-    for (int r = 0; r < rank; ++r) {
-      T v = T(1);
-      for (int k = sh.n - 1; k >= 0; --k) {  // highest mode first (kruskal.hpp:58-62)
-        if (k == mode) continue;
-        v *= fs.f[k][idx[k] + i64(r) * fs.extent[k]];
-      }
-      out[(a0 * rank + r) * Rr + b0] = v;
+    T v = T(1);
+    for (int k = sh.n - 1; k >= 0; --k) {  // highest mode first (kruskal.hpp:58-62)
+      if (k == mode) continue;
+      v *= fs.f[k][idx[k] + i64(r) * fs.extent[k]];
     }
+    out[(a0 * rank + r) * Rr + b0] = v;
   }
 }
 
@@ -176,8 +179,10 @@ __global__ void __launch_bounds__(kSmallThreads) init_from_gram_kernel(const T* 
                                                                        u64 seed, int method, T* F, T* gram,
                                                                        double* work) {
   const int tid = threadIdx.x, nt = blockDim.x;
-  double* A = work;
-  double* V = work + i64(n) * n;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const bool in_smem = n <= kEigSmemMax;  // A and V resident in shared memory
+  double* A = in_smem ? reinterpret_cast<double*>(smem_raw) : work;
+  double* V = A + i64(n) * n;
   double* ev = work + 2 * i64(n) * n;
   int* ord = reinterpret_cast<int*>(ev + n);
   double* col = ev + 2 * n;  // [n] padding scratch
@@ -271,22 +276,21 @@ __global__ void zero_factor_kernel(T* F, i64 n, int R, T* gram) {
 }
 
 // --------------------------------------------------------------- ALS
-template <typename T>
-__global__ void __launch_bounds__(kSmallThreads)
-    als_update_kernel(FactorSet<T> fs, int mode, const T* W, T* weights, double tol, int max_iter,
-                      double* trace_fit, double* trace_sec, AlsState* st, double* work) {
-  if (st->done) return;
+// One mode update (solve.hpp:207-230) and, for the last mode, the fit and
+// stopping test (solve.hpp:232-254), executed by one CTA. W (I x R,
+// column-major) is the MTTKRP; `work` holds 3 R^2 + 4 R doubles.
+template <typename T, typename WT>
+__device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T* weights, double tol,
+                                int max_iter, double* trace_fit, double* trace_sec, AlsState* st, double* work) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int R = fs.rank, N = fs.order;
   const i64 I = fs.extent[mode];
   T* F = fs.f[mode];
-  double* V = work;             // R x R
-  double* Lm = V + R * R;       // R x R
-  double* Li = Lm + R * R;      // R x R
-  double* Vi = Li + R * R;      // R x R
-  double* ev = Vi + R * R;      // R
+  double* V = work;          // R x R
+  double* Lm = V + R * R;    // R x R: Cholesky factor, then V^{-1}
+  double* X = Lm + R * R;    // R x R: L^{-1} / eigenvectors
+  double* ev = X + R * R;    // R
   int* ord = reinterpret_cast<int*>(ev + R);
-  double* EA = ev + 2 * R;      // R x R eigen scratch
   __shared__ int s_ok;
   __shared__ double s_piv;
 
@@ -330,15 +334,16 @@ __global__ void __launch_bounds__(kSmallThreads)
     if (!s_ok) break;
   }
   const bool chol = s_ok != 0;
+  double* Pm;
   if (chol) {
-    // Li = L^{-1} (column-parallel), Vi = Li^T Li
+    // X = L^{-1} (column-parallel), then Lm = X^T X = V^{-1}
     for (int j = tid; j < R; j += nt) {
-      for (int i = 0; i < j; ++i) Li[i + j * R] = 0.0;
-      Li[j + j * R] = 1.0 / Lm[j + j * R];
+      for (int i = 0; i < j; ++i) X[i + j * R] = 0.0;
+      X[j + j * R] = 1.0 / Lm[j + j * R];
       for (int i = j + 1; i < R; ++i) {
         double s = 0.0;
-        for (int k = j; k < i; ++k) s += Lm[i + k * R] * Li[k + j * R];
-        Li[i + j * R] = -s / Lm[i + i * R];
+        for (int k = j; k < i; ++k) s += Lm[i + k * R] * X[k + j * R];
+        X[i + j * R] = -s / Lm[i + i * R];
       }
     }
     __syncthreads();
@@ -346,13 +351,14 @@ __global__ void __launch_bounds__(kSmallThreads)
       const int a = e % R, b = e / R;
       const int k0 = a > b ? a : b;
       double s = 0.0;
-      for (int k = k0; k < R; ++k) s += Li[k + a * R] * Li[k + b * R];
-      Vi[e] = s;
+      for (int k = k0; k < R; ++k) s += X[k + a * R] * X[k + b * R];
+      Lm[e] = s;
     }
+    Pm = Lm;
   } else {
-    for (int e = tid; e < R * R; e += nt) EA[e] = V[e];
+    for (int e = tid; e < R * R; e += nt) Lm[e] = V[e];
     __syncthreads();
-    jacobi_eig(EA, Li, R, ev, ord);
+    jacobi_eig(Lm, X, R, ev, ord);
     T lmax = T(0);
     for (int k = 0; k < R; ++k) lmax = T(ev[k]) > lmax ? T(ev[k]) : lmax;
     const T tau = T(R) * Traits<T>::eps * lmax;
@@ -363,11 +369,12 @@ __global__ void __launch_bounds__(kSmallThreads)
         const T lk = T(ev[k]);
         if (lk > tau) {
           const int c = ord[k];
-          s += Li[a + c * R] * (1.0 / double(lk)) * Li[b + c * R];
+          s += X[a + c * R] * (1.0 / double(lk)) * X[b + c * R];
         }
       }
-      Vi[e] = s;
+      V[e] = s;
     }
+    Pm = V;
     if (tid == 0) st->pivots_fallback += 1;
   }
   __syncthreads();
@@ -376,7 +383,7 @@ __global__ void __launch_bounds__(kSmallThreads)
     const i64 i = e % I;
     const int r = int(e / I);
     double s = 0.0;
-    for (int k = 0; k < R; ++k) s += double(W[i + k * I]) * Vi[k + r * R];
+    for (int k = 0; k < R; ++k) s += double(W[i + k * I]) * Pm[k + r * R];
     F[i + r * I] = T(s);
   }
   __syncthreads();
@@ -424,19 +431,153 @@ __global__ void __launch_bounds__(kSmallThreads)
     if (!isfinite(fit_now)) {
       st->error_it = it;
       st->done = 1;
-      return;
+    } else {
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      trace_fit[it - 1] = fit_now;
+      trace_sec[it - 1] = double(now - st->t0) * 1e-9;
+      if (it >= 2 && fabs(fit_now - st->prev_fit) < tol) {
+        st->converged = 1;
+        st->done = 1;
+      }
+      st->prev_fit = fit_now;
+      if (it >= max_iter) st->done = 1;
+      st->it = it + 1;
     }
-    unsigned long long now;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-    trace_fit[it - 1] = fit_now;
-    trace_sec[it - 1] = double(now - st->t0) * 1e-9;
-    if (it >= 2 && fabs(fit_now - st->prev_fit) < tol) {
-      st->converged = 1;
-      st->done = 1;
+  }
+  __syncthreads();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kSmallThreads)
+    als_update_kernel(FactorSet<T> fs, int mode, const T* W, T* weights, double tol, int max_iter,
+                      double* trace_fit, double* trace_sec, AlsState* st, double* work) {
+  if (st->done) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (fs.rank <= kAlsSmemRank) work = reinterpret_cast<double*>(smem_raw);
+  als_mode_update<T, T>(fs, mode, W, weights, tol, max_iter, trace_fit, trace_sec, st, work);
+}
+
+// Whole ALS loop in one cooperative launch (solve.hpp:205-255). Per mode:
+//   A. every CTA: MTTKRP partial over its slice of the mode's (a, b)
+//      positions, Khatri-Rao rows formed on the fly (no panel);
+//   B. CTA 0: fixed-order reduction of the partials, then als_mode_update.
+// Two grid barriers per mode; the stop flag is read after the last mode.
+constexpr int kAlsThreads = 256;
+constexpr int kAlsBatch = 32;   // positions per smem batch
+constexpr int kAlsAcc = 32;     // accumulators per thread: I * R <= kAlsAcc * kAlsThreads
+
+template <typename T>
+struct AlsLoopArgs {
+  const T* B;
+  ShapeArg sh;
+  FactorSet<T> fs;
+  T* weights;
+  double tol;
+  int max_iter;
+  double* trace_fit;
+  double* trace_sec;
+  AlsState* st;
+  double* part;  // [2][G][max I*R]
+  i64 part_stride;
+  GridBarrier* bar;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* sm = reinterpret_cast<double*>(smem_raw);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int G = gridDim.x, g = blockIdx.x;
+  const int N = p.sh.n, R = p.fs.rank;
+  int parity = 0;
+  for (;;) {
+    for (int m = 0; m < N; ++m) {
+      const i64 I = p.sh.e[m];
+      i64 L = 1, Rr = 1;
+      for (int k = 0; k < m; ++k) L *= p.sh.e[k];
+      for (int k = m + 1; k < N; ++k) Rr *= p.sh.e[k];
+      const i64 J = L * Rr;
+      const int nout = int(I) * R;
+      // ---- A: partial MTTKRP over positions [j0, j1)
+      double acc[kAlsAcc];
+#pragma unroll
+      for (int q = 0; q < kAlsAcc; ++q) acc[q] = 0.0;
+      const i64 chunk = ceil_div(J, G);
+      const i64 j0 = g * chunk, j1 = j0 + chunk < J ? j0 + chunk : J;
+      double* fib = sm;                       // [kAlsBatch][I]
+      double* kc = sm + kAlsBatch * I;        // [kAlsBatch][R]
+      for (i64 pb = j0; pb < j1; pb += kAlsBatch) {
+        const int np = int(j1 - pb < kAlsBatch ? j1 - pb : kAlsBatch);
+        for (int e = tid; e < kAlsBatch * int(I); e += nt) {
+          const int pp = e % kAlsBatch, i = e / kAlsBatch;
+          double v = 0.0;
+          if (pp < np) {
+            const i64 s = pb + pp, a = s / Rr, b = s - a * Rr;
+            v = double(p.B[(a * I + i) * Rr + b]);
+          }
+          fib[pp * I + i] = v;
+        }
+        for (int e = tid; e < kAlsBatch * R; e += nt) {
+          const int pp = e / R, r = e % R;
+          double v = 0.0;
+          if (pp < np) {
+            const i64 s = pb + pp;
+            i64 a = s / Rr, b = s - a * Rr;
+            i64 idx[kMaxOrder];
+            for (int k = N - 1; k > m; --k) {
+              idx[k] = b % p.sh.e[k];
+              b /= p.sh.e[k];
+            }
+            for (int k = m - 1; k >= 0; --k) {
+              idx[k] = a % p.sh.e[k];
+              a /= p.sh.e[k];
+            }
+            T prod = T(1);
+            for (int k = N - 1; k >= 0; --k)  // highest mode first (kruskal.hpp:58-62)
+              if (k != m) prod *= p.fs.f[k][idx[k] + i64(r) * p.sh.e[k]];
+            v = double(prod);
+          }
+          kc[pp * R + r] = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kAlsAcc; ++q) {
+          const int o = tid + q * nt;
+          if (o < nout) {
+            const int i = o % int(I), r = o / int(I);
+            double s = acc[q];
+            for (int pp = 0; pp < np; ++pp) s = fma(fib[pp * I + i], kc[pp * R + r], s);
+            acc[q] = s;
+          }
+        }
+        __syncthreads();
+      }
+      double* pt = p.part + (i64(parity) * G + g) * p.part_stride;
+#pragma unroll
+      for (int q = 0; q < kAlsAcc; ++q) {
+        const int o = tid + q * nt;
+        if (o < nout) pt[o] = acc[q];
+      }
+      grid_sync(p.bar);
+      // ---- B: reduce + mode update on CTA 0
+      if (g == 0) {
+        double* W = sm;                   // I x R
+        double* work = sm + nout;         // 3 R^2 + 4 R
+        const double* pp0 = p.part + i64(parity) * G * p.part_stride;
+        for (int o = tid; o < nout; o += nt) {
+          double s = 0.0;
+          for (int q = 0; q < G; ++q) s += ldcg(&pp0[i64(q) * p.part_stride + o]);
+          W[o] = s;
+        }
+        __syncthreads();
+        FactorSet<T> fs = p.fs;
+        als_mode_update<T, double>(fs, m, W, p.weights, p.tol, p.max_iter, p.trace_fit, p.trace_sec, p.st, work);
+      }
+      parity ^= 1;
+      grid_sync(p.bar);
     }
-    st->prev_fit = fit_now;
-    if (it >= max_iter) st->done = 1;
-    st->it = it + 1;
+    if (ldcg(&p.st->done)) break;
   }
 }
 
@@ -598,13 +739,16 @@ __global__ void norm_finite_kernel(const T* x, i64 n, double* part) {
   }
 }
 
+// Fixed-order (deterministic) sum of nblocks (a, b) pairs by one CTA.
 __global__ void sum_pairs_kernel(const double* part, int nblocks, double* out) {
+  double a = 0.0, b = 0.0;
+  for (int q = threadIdx.x; q < nblocks; q += blockDim.x) {
+    a += part[2 * q];
+    b += part[2 * q + 1];
+  }
+  a = block_reduce_sum(a);
+  b = block_reduce_sum(b);
   if (threadIdx.x == 0) {
-    double a = 0.0, b = 0.0;
-    for (int q = 0; q < nblocks; ++q) {
-      a += part[2 * q];
-      b += part[2 * q + 1];
-    }
     out[0] = a;
     out[1] = b;
   }
@@ -724,7 +868,7 @@ void kr_panel(const FactorSet<T>& fs, const i64* shape, int mode, T* out, cudaSt
   for (int m = 0; m < mode; ++m) L *= shape[m];
   for (int m = mode + 1; m < fs.order; ++m) Rr *= shape[m];
   const i64 J = L * Rr;
-  const int blocks = int(std::max<i64>(1, std::min<i64>(ceil_div(J, 256), 148 * 16)));
+  const int blocks = int(std::max<i64>(1, std::min<i64>(ceil_div(J * fs.rank, 256), 148 * 16)));
   kr_panel_kernel<T><<<blocks, 256, 0, st>>>(fs, sh, mode, J, Rr, out, skip);
   count_launch();
   RCPG_LAUNCHED();
@@ -734,8 +878,11 @@ template <typename T>
 void init_factor_from_gram(const T* G, int extent, int rank, int mode, u64 seed, int method, T* factor,
                            T* gram_out, double* work, cudaStream_t st) {
   check_arg(rank <= kMaxRank, "init_factors: rank above the supported maximum");
-  init_from_gram_kernel<T><<<1, kSmallThreads, 0, st>>>(G, extent, rank, mode, seed, method, factor, gram_out,
-                                                         work);
+  const size_t smem = extent <= kEigSmemMax ? 2 * size_t(extent) * extent * sizeof(double) : 0;
+  static const size_t lim = enable_max_dyn_smem(init_from_gram_kernel<T>);
+  (void)lim;
+  init_from_gram_kernel<T><<<1, kSmallThreads, smem, st>>>(G, extent, rank, mode, seed, method, factor, gram_out,
+                                                            work);
   count_launch();
   RCPG_LAUNCHED();
 }
@@ -750,10 +897,51 @@ void zero_factor(T* factor, i64 extent, int rank, T* gram_out, cudaStream_t st) 
 template <typename T>
 void als_update(const FactorSet<T>& fs, int mode, const T* W, T* weights, double tol, int max_iter,
                 double* trace_fit, double* trace_sec, AlsState* state, double* work, cudaStream_t st) {
-  als_update_kernel<T><<<1, kSmallThreads, 0, st>>>(fs, mode, W, weights, tol, max_iter, trace_fit, trace_sec,
-                                                     state, work);
+  const int R = fs.rank;
+  const size_t smem = R <= kAlsSmemRank ? (3 * size_t(R) * R + 4 * size_t(R)) * sizeof(double) : 0;
+  static const size_t lim = enable_max_dyn_smem(als_update_kernel<T>);
+  (void)lim;
+  als_update_kernel<T><<<1, kSmallThreads, smem, st>>>(fs, mode, W, weights, tol, max_iter, trace_fit, trace_sec,
+                                                        state, work);
   count_launch();
   RCPG_LAUNCHED();
+}
+
+template <typename T>
+bool als_loop_supported(const i64* shape, int order, int rank) {
+  if (rank > kAlsSmemRank) return false;
+  for (int m = 0; m < order; ++m) {
+    if (shape[m] * rank > i64(kAlsAcc) * kAlsThreads) return false;
+    const size_t smA = (size_t(kAlsBatch) * shape[m] + size_t(kAlsBatch) * rank) * sizeof(double);
+    const size_t smB = (size_t(shape[m]) * rank + 3 * size_t(rank) * rank + 4 * size_t(rank)) * sizeof(double);
+    if (std::max(smA, smB) > 160 * 1024) return false;
+  }
+  return true;
+}
+
+template <typename T>
+void als_loop(const T* B, const i64* shape, int order, const FactorSet<T>& fs, T* weights, double tol, int max_iter,
+              double* trace_fit, double* trace_sec, AlsState* state, double* part, i64 part_elems, GridBarrier* bar,
+              cudaStream_t st) {
+  const int R = fs.rank;
+  size_t smem = 0;
+  i64 maxJ = 1, S = 1, maxout = 1;
+  for (int m = 0; m < order; ++m) S *= shape[m];
+  for (int m = 0; m < order; ++m) {
+    maxJ = std::max(maxJ, S / shape[m]);
+    maxout = std::max(maxout, shape[m] * R);
+    const size_t smA = (size_t(kAlsBatch) * shape[m] + size_t(kAlsBatch) * R) * sizeof(double);
+    const size_t smB = (size_t(shape[m]) * R + 3 * size_t(R) * R + 4 * size_t(R)) * sizeof(double);
+    smem = std::max(smem, std::max(smA, smB));
+  }
+  static const size_t lim = enable_max_dyn_smem(als_loop_kernel<T>);
+  if (smem > lim) throw std::runtime_error("als_loop: shared memory plan too large");
+  const int maxc = max_coop_blocks(als_loop_kernel<T>, kAlsThreads, smem);
+  int G = int(std::max<i64>(1, std::min<i64>(ceil_div(maxJ, 4 * kAlsBatch), maxc)));
+  G = int(std::min<i64>(G, part_elems / (2 * maxout)));
+  AlsLoopArgs<T> a{B, make_shape(shape, order), fs, weights, tol, max_iter, trace_fit, trace_sec, state, part,
+                   maxout, bar};
+  launch_coop(als_loop_kernel<T>, G, kAlsThreads, smem, st, a);
 }
 
 void als_start(AlsState* state, double* nx2_src, cudaStream_t st) {
@@ -781,7 +969,7 @@ template <typename T>
 void norm_and_finite(const T* x, i64 n, double* out2, double* scratch, int num_sms, cudaStream_t st) {
   const int blocks = int(std::max<i64>(1, std::min<i64>(ceil_div(n, 256), i64(num_sms) * 4)));
   norm_finite_kernel<T><<<blocks, 256, 0, st>>>(x, n, scratch);
-  sum_pairs_kernel<<<1, 32, 0, st>>>(scratch, blocks, out2);
+  sum_pairs_kernel<<<1, 256, 0, st>>>(scratch, blocks, out2);
   count_launch(2);
   RCPG_LAUNCHED();
 }
@@ -797,7 +985,7 @@ void residual_norms(const T* X, const i64* shape, int order, const FactorSet<T>&
   for (int m = 0; m < order - 1; ++m) prefix *= shape[m];
   const int blocks = int(std::max<i64>(1, std::min<i64>(ceil_div(prefix, kResRows), i64(num_sms) * 8)));
   residual_kernel<T><<<blocks, 256, 0, st>>>(X, sh, fs, weights, scratch);
-  sum_pairs_kernel<<<1, 32, 0, st>>>(scratch, blocks, out2);
+  sum_pairs_kernel<<<1, 256, 0, st>>>(scratch, blocks, out2);
   count_launch(2);
   RCPG_LAUNCHED();
 }
@@ -818,12 +1006,12 @@ void synth_tensor(const i64* shape, int order, int rank, const double* w_dev, co
   // add_noise (synthetic.hpp:42-58): sigma = sd / snr, sd the sample std.
   double h[2];
   sum_and_sq_kernel<T><<<blocks, 256, 0, st>>>(out, total, 0.0, scratch);
-  sum_pairs_kernel<<<1, 32, 0, st>>>(scratch, blocks, scratch + 2 * blocks);
+  sum_pairs_kernel<<<1, 256, 0, st>>>(scratch, blocks, scratch + 2 * blocks);
   RCPG_CUDA(cudaMemcpyAsync(h, scratch + 2 * blocks, sizeof(h), cudaMemcpyDeviceToHost, st));
   RCPG_CUDA(cudaStreamSynchronize(st));
   const double mean = h[0] / double(total);
   sum_and_sq_kernel<T><<<blocks, 256, 0, st>>>(out, total, mean, scratch);
-  sum_pairs_kernel<<<1, 32, 0, st>>>(scratch, blocks, scratch + 2 * blocks);
+  sum_pairs_kernel<<<1, 256, 0, st>>>(scratch, blocks, scratch + 2 * blocks);
   RCPG_CUDA(cudaMemcpyAsync(h, scratch + 2 * blocks, sizeof(h), cudaMemcpyDeviceToHost, st));
   RCPG_CUDA(cudaStreamSynchronize(st));
   const T sd = total > 1 ? T(sqrt(h[1] / double(total - 1))) : T(0);
@@ -841,6 +1029,9 @@ void synth_tensor(const i64* shape, int order, int rank, const double* w_dev, co
   template void als_update<T>(const FactorSet<T>&, int, const T*, T*, double, int, double*, double*,          \
                               AlsState*, double*, cudaStream_t);                                              \
   template void normalize_model<T>(const FactorSet<T>&, T*, T*, cudaStream_t);                                \
+  template bool als_loop_supported<T>(const i64*, int, int);                                                  \
+  template void als_loop<T>(const T*, const i64*, int, const FactorSet<T>&, T*, double, int, double*, double*, \
+                            AlsState*, double*, i64, GridBarrier*, cudaStream_t);                                \
   template void small_gemm<T>(const T*, i64, i64, const T*, int, T*, cudaStream_t);                           \
   template void norm_and_finite<T>(const T*, i64, double*, double*, int, cudaStream_t);                       \
   template void residual_norms<T>(const T*, const i64*, int, const FactorSet<T>&, const T*, double*, double*, \

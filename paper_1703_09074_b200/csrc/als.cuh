@@ -56,6 +56,15 @@ void als_update(const FactorSet<T>& fs, int mode, const T* W, T* weights, double
 
 void als_start(AlsState* state, double* nx2_src, cudaStream_t st);
 
+// The whole ALS iteration loop as one cooperative kernel (when the mode
+// extents and rank fit its shared-memory plan; see als_loop_supported).
+template <typename T>
+bool als_loop_supported(const i64* shape, int order, int rank);
+template <typename T>
+void als_loop(const T* B, const i64* shape, int order, const FactorSet<T>& fs, T* weights, double tol, int max_iter,
+              double* trace_fit, double* trace_sec, AlsState* state, double* part, i64 part_elems, GridBarrier* bar,
+              cudaStream_t st);
+
 // normalize (kruskal.hpp:117-176) in place; `tmp` >= sum extents * rank + rank elements.
 template <typename T>
 void normalize_model(const FactorSet<T>& fs, T* weights, T* tmp, cudaStream_t st);

@@ -68,8 +68,8 @@ struct rcpg_context {
   std::string err;
   int err_it = -1;
   // workspace
-  DevBuf panelA, panelB, work0, work1, Y, Qy, scratch, keys, cands, bar, info, part, tau, diag;
-  DevBuf als_f, als_g, als_w, als_kr, als_work, als_trace, als_state, weights, small_tmp, nrm;
+  DevBuf panelA, panelB, work0, work1, Y, Qy, scratch, keys, cands, bar, info, part, tau, diag, cqr;
+  DevBuf als_f, als_g, als_w, als_kr, als_work, als_trace, als_state, weights, small_tmp, nrm, als_part;
   std::vector<PassRecord> passes;
   cudaEvent_t user_events[64] = {};
   size_t pass_used = 0;
@@ -184,6 +184,12 @@ FactorWork factor_work(rcpg_context* c, i64 rows) {
   w.tau = c->tau.p;
   w.diag = c->diag.p;
   w.max_blocks = maxb;
+  const i64 cqr_rows = 16384;
+  if (rows <= cqr_rows) {
+    c->cqr.ensure(2 * size_t(rows) * kMaxPanelCols * sizeof(double));
+    w.cqr_work = c->cqr.as<double>();
+    w.cqr_rows = cqr_rows;
+  }
   return w;
 }
 
@@ -440,6 +446,19 @@ AlsResult run_als(rcpg_context* c, const T* B, const i64* shape, int order, cons
 
   AlsState hs{};
   int enqueued = 0, batch = 2;
+  if (als_loop_supported<T>(shape, order, R)) {
+    ScopedPass sp(c, "als_iterations", 0.0);
+    i64 maxout = 1;
+    for (int m = 0; m < order; ++m) maxout = std::max(maxout, shape[m] * R);
+    const i64 part_elems = 2 * i64(2048) * maxout;
+    c->als_part.ensure(size_t(part_elems) * sizeof(double));
+    c->bar.ensure(sizeof(GridBarrier));
+    als_loop<T>(B, shape, order, fs, weights, cfg.tol, cfg.max_iter, tfit, tsec, state, c->als_part.as<double>(),
+                part_elems, c->bar.as<GridBarrier>(), c->st);
+    RCPG_CUDA(cudaMemcpyAsync(&hs, state, sizeof(AlsState), cudaMemcpyDeviceToHost, c->st));
+    RCPG_CUDA(cudaStreamSynchronize(c->st));
+    enqueued = cfg.max_iter;
+  }
   {
     ScopedPass sp(c, "als_iterations", 0.0);
     while (enqueued < cfg.max_iter) {
@@ -649,8 +668,8 @@ void rcpg_destroy(rcpg_context* c) {
     cudaEventDestroy(r.b);
   }
   for (DevBuf* b : {&c->panelA, &c->panelB, &c->work0, &c->work1, &c->Y, &c->Qy, &c->scratch, &c->keys, &c->cands,
-                    &c->bar, &c->info, &c->part, &c->tau, &c->diag, &c->als_f, &c->als_g, &c->als_w, &c->als_kr,
-                    &c->als_work, &c->als_trace, &c->als_state, &c->weights, &c->small_tmp, &c->nrm})
+                    &c->bar, &c->info, &c->part, &c->tau, &c->diag, &c->cqr, &c->als_f, &c->als_g, &c->als_w, &c->als_kr,
+                    &c->als_work, &c->als_trace, &c->als_state, &c->weights, &c->small_tmp, &c->nrm, &c->als_part})
     b->release();
   cudaStreamDestroy(c->st);
   delete c;

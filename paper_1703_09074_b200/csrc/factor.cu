@@ -5,14 +5,21 @@
 //                                   returns P^{-1} L
 //   thin_qr    compress.hpp:60-73  = Eigen::HouseholderQR (LAPACK sign
 //                                   convention) + householderQ() * I + rank warning
-// Parity needs the reference's *basis*, not only its span,
-// so both are faithful right-looking algorithms, not CholeskyQR / tournament
-// pivoting. They run as one cooperative persistent kernel over the panel in
-// its storage layout (rows s = a*R + b, column c at panel_addr(s, c)); every
-// CTA owns a contiguous block of rows, keeps the row's Kolda (physical)
-// position for the reference's column-major tie-breaking, and the
-// grid-wide pivot / reduction steps use a generation barrier. With one CTA
-// the barrier degenerates to __syncthreads (small I x l sample matrices).
+// Parity needs the reference's *basis*, not only its span.
+//
+//  * plu_smem_kernel: one CTA, panel resident in shared memory, rows and
+//    columns physically swapped exactly like FullPivLU (small I x l sample
+//    matrices Y).
+//  * plu_coop_kernel: cooperative persistent kernel over an HBM/L2 panel
+//    (the big J x l panel W = X_(n)^T Q): every CTA owns a block of rows and
+//    tracks each row's physical (Kolda) position for the column-major
+//    first-maximum tie-breaking; one grid barrier per elimination step.
+//  * cqr2_kernel: CholeskyQR2 in double followed by the Householder sign
+//    reconstruction (the LU of Q_top - S that picks each column's sign the
+//    way beta = -sign(c0)||x|| does), which yields Eigen's Householder Q up
+//    to O(eps * cond(Y)). A device-side status flag hands ill-conditioned
+//    or rank-deficient inputs to householder_kernel, a faithful
+//    right-looking Householder QR (same cooperative structure as the LU).
 #include "factor.cuh"
 #include "runtime.cuh"
 
@@ -21,6 +28,14 @@ namespace rcpg {
 namespace {
 
 constexpr int kFacThreads = 256;
+constexpr int kSmallThreads = 1024;
+
+// Storage offset of panel row s (column stride R): a*cols*R + b.
+__device__ __forceinline__ i64 row_base(i64 s, i64 R, i64 J, i64 cols) {
+  if (R == J) return s;  // first-mode panels and I x l samples: column-major
+  const i64 a = s / R, b = s - a * R;
+  return a * cols * R + b;
+}
 
 // ----------------------------------------------------------- row keys
 __global__ void init_row_keys_kernel(KoldaMap km, i64 J, i64 R, i64* keys) {
@@ -30,7 +45,7 @@ __global__ void init_row_keys_kernel(KoldaMap km, i64 J, i64 R, i64* keys) {
   }
 }
 
-// ---------------------------------------------------------------- LU
+// ------------------------------------------------------------ candidates
 template <typename T>
 struct Cand {
   T v;       // |value|; -1 = none
@@ -58,7 +73,6 @@ __device__ Cand<T> shfl_cand(const Cand<T>& x, int off) {
   return y;
 }
 
-// Block-wide arg-max with deterministic tie-breaking; result broadcast.
 template <typename T>
 __device__ Cand<T> block_best(Cand<T> x, Cand<T>* scratch) {
 #pragma unroll
@@ -71,7 +85,7 @@ __device__ Cand<T> block_best(Cand<T> x, Cand<T>* scratch) {
   if (lane == 0) scratch[wid] = x;
   __syncthreads();
   if (wid == 0) {
-    Cand<T> y = lane < nw ? scratch[lane] : Cand<T>{T(-1), 0x7fffffff, 0, 0, 0};
+    Cand<T> y = lane < nw ? scratch[lane] : Cand<T>{T(-1), 0x7fffffff, 0, 0x7fffffffffffffffll, 0};
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       Cand<T> z = shfl_cand(y, o);
@@ -85,6 +99,79 @@ __device__ Cand<T> block_best(Cand<T> x, Cand<T>* scratch) {
   return r;
 }
 
+// ------------------------------------------------ LU, shared-memory CTA
+// Eigen FullPivLU verbatim on an I x n column-major panel held in shared
+// memory (physical row/column swaps, first maximum in column-major order).
+template <typename T>
+__global__ void __launch_bounds__(kSmallThreads) plu_smem_kernel(const T* __restrict__ A, T* __restrict__ Z, int I,
+                                                                 int n, int* info) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* a = reinterpret_cast<T*>(smem_raw);
+  int* perm = reinterpret_cast<int*>(a + i64(I) * n);  // physical -> original row
+  __shared__ Cand<T> red[33];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int r = I < n ? I : n;
+  for (int e = tid; e < I * n; e += nt) a[e] = A[e];
+  for (int i = tid; i < I; i += nt) perm[i] = i;
+  __syncthreads();
+  const int tx = tid & 31, ty = tid >> 5, ny = nt >> 5;
+  int k0 = r;
+  for (int k = 0; k < r; ++k) {
+    // pivot search over the corner, column-major first maximum (explicit keys)
+    Cand<T> best{T(-1), 0x7fffffff, 0, 0x7fffffffffffffffll, 0};
+    for (int j = k + ty; j < n; j += ny)
+      for (int i = k + tx; i < I; i += 32) {
+        const Cand<T> x{T(fabs(a[i + j * I])), j, j, i, i};
+        if (better(x, best)) best = x;
+      }
+    best = block_best(best, red);
+    if (!(best.v > T(0))) {
+      k0 = k;
+      break;
+    }
+    const int br = int(best.prow), bc = best.pcol;
+    if (br != k) {  // row swap, then column swap (FullPivLU order)
+      for (int j = tid; j < n; j += nt) {
+        const T t = a[k + j * I];
+        a[k + j * I] = a[br + j * I];
+        a[br + j * I] = t;
+      }
+      if (tid == 0) {
+        const int t = perm[k];
+        perm[k] = perm[br];
+        perm[br] = t;
+      }
+      __syncthreads();
+    }
+    if (bc != k) {
+      for (int i = tid; i < I; i += nt) {
+        const T t = a[i + k * I];
+        a[i + k * I] = a[i + bc * I];
+        a[i + bc * I] = t;
+      }
+      __syncthreads();
+    }
+    const T piv = a[k + k * I];
+    for (int i = k + 1 + tid; i < I; i += nt) a[i + k * I] = a[i + k * I] / piv;
+    __syncthreads();
+    if (k < r - 1) {
+      for (int j = k + 1 + ty; j < n; j += ny) {
+        const T u = a[k + j * I];
+        for (int i = k + 1 + tx; i < I; i += 32) a[i + j * I] -= a[i + k * I] * u;
+      }
+      __syncthreads();
+    }
+  }
+  // P^{-1} L: physical row p of L goes to original row perm[p]
+  for (int e = tid; e < I * r; e += nt) {
+    const int p = e % I, j = e / I;
+    const T v = (p == j) ? T(1) : (p > j ? a[p + j * I] : T(0));
+    Z[perm[p] + i64(j) * I] = v;
+  }
+  if (tid == 0) *info = k0;
+}
+
+// -------------------------------------------------- LU, cooperative grid
 template <typename T>
 struct LuArgs {
   T* A;        // panel J x n (in/out, destroyed)
@@ -99,7 +186,7 @@ struct LuArgs {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(kFacThreads) plu_kernel(LuArgs<T> p) {
+__global__ void __launch_bounds__(kFacThreads) plu_coop_kernel(LuArgs<T> p) {
   __shared__ Cand<T> red[33];
   __shared__ int pcol_of[kMaxPanelCols], col_at[kMaxPanelCols];
   __shared__ T U[kMaxPanelCols];
@@ -112,6 +199,8 @@ __global__ void __launch_bounds__(kFacThreads) plu_kernel(LuArgs<T> p) {
   const i64 r0 = blockIdx.x * chunk;
   const i64 r1 = r0 + chunk < p.J ? r0 + chunk : p.J;
   const Cand<T> none{T(-1), 0x7fffffff, 0, 0x7fffffffffffffffll, 0};
+  const i64 R = p.R;
+  const bool unit = (p.R == p.J);
 
   for (int c = threadIdx.x; c < p.n; c += blockDim.x) {
     pcol_of[c] = c;
@@ -119,12 +208,12 @@ __global__ void __launch_bounds__(kFacThreads) plu_kernel(LuArgs<T> p) {
   }
   if (threadIdx.x == 0) n_ov = 0;
 
-  // step-0 candidates
   Cand<T> best = none;
   for (i64 s = r0 + threadIdx.x; s < r1; s += blockDim.x) {
     const i64 ps = p.phys[s];
+    const i64 ba = row_base(s, R, p.J, p.n);
     for (int c = 0; c < p.n; ++c) {
-      const Cand<T> x{T(fabs(p.A[panel_addr(s, c, p.R, p.n)])), c, c, ps, s};
+      const Cand<T> x{T(fabs(p.A[ba + c * R])), c, c, ps, s};
       if (better(x, best)) best = x;
     }
   }
@@ -146,7 +235,7 @@ __global__ void __launch_bounds__(kFacThreads) plu_kernel(LuArgs<T> p) {
       if (better(x, g)) g = x;
     }
     g = block_best(g, red);
-    if (g.v == T(0) || g.v < T(0)) {  // exactly-zero corner (FullPivLU early stop)
+    if (!(g.v > T(0))) {  // exactly-zero corner (FullPivLU early stop)
       k0 = k;
       break;
     }
@@ -154,10 +243,10 @@ __global__ void __launch_bounds__(kFacThreads) plu_kernel(LuArgs<T> p) {
     const int cs = g.c;
     const i64 pr = g.prow;
     const int pc = g.pcol;
-    const T piv = ldcg(&p.A[panel_addr(ss, cs, p.R, p.n)]);
+    const i64 bss = row_base(ss, R, p.J, p.n);
+    const T piv = ldcg(&p.A[bss + cs * R]);
     if (threadIdx.x == 0) {
-      // the row at physical position k before the swap
-      i64 u = -1;
+      i64 u = -1;  // row at physical position k before the swap
       for (int q = n_ov - 1; q >= 0; --q)
         if (ov_pos[q] == k) {
           u = ov_row[q];
@@ -176,10 +265,9 @@ __global__ void __launch_bounds__(kFacThreads) plu_kernel(LuArgs<T> p) {
       col_at[k] = cs;
       col_at[pc] = colk;
     }
-    for (int c = threadIdx.x; c < p.n; c += blockDim.x) U[c] = ldcg(&p.A[panel_addr(ss, c, p.R, p.n)]);
+    for (int c = threadIdx.x; c < p.n; c += blockDim.x) U[c] = ldcg(&p.A[bss + c * R]);
     __syncthreads();
     const i64 u = s_u;
-    // physical-position bookkeeping for rows this CTA owns
     if (threadIdx.x == 0) {
       if (ss >= r0 && ss < r1) p.phys[ss] = k;
       if (u != ss && u >= r0 && u < r1) p.phys[u] = pr;
@@ -188,28 +276,46 @@ __global__ void __launch_bounds__(kFacThreads) plu_kernel(LuArgs<T> p) {
 
     best = none;
     Cand<T>* out = p.cands + ((k + 1) & 1) * G;
+    const bool more = (k + 1 < p.r);
     for (i64 s = r0 + threadIdx.x; s < r1; s += blockDim.x) {
       const i64 ps = p.phys[s];
+      if (ps < k) continue;  // pivoted earlier
+      i64 ba, bz;
+      if (unit) {
+        ba = s;
+        bz = s;
+      } else {
+        const i64 aa = s / R, bb = s - aa * R;
+        ba = aa * p.n * R + bb;
+        bz = aa * p.r * R + bb;
+      }
       if (s == ss) {
-        p.Z[panel_addr(s, k, p.R, p.r)] = T(1);
-        for (int j = k + 1; j < p.r; ++j) p.Z[panel_addr(s, j, p.R, p.r)] = T(0);
+        p.Z[bz + k * R] = T(1);
+        for (int j = k + 1; j < p.r; ++j) p.Z[bz + j * R] = T(0);
         continue;
       }
-      if (ps <= k) continue;  // pivoted earlier
-      const T m = p.A[panel_addr(s, cs, p.R, p.n)] / piv;
-      p.Z[panel_addr(s, k, p.R, p.r)] = m;
-      if (k + 1 < p.r) {
-        for (int q = k + 1; q < p.n; ++q) {
-          const int c = col_at[q];
-          const i64 ad = panel_addr(s, c, p.R, p.n);
-          const T v = p.A[ad] - m * U[c];
-          p.A[ad] = v;
-          const Cand<T> x{T(fabs(v)), q, c, ps, s};
-          if (better(x, best)) best = x;
+      const T m = p.A[ba + cs * R] / piv;
+      p.Z[bz + k * R] = m;
+      if (more) {
+        constexpr int B = 8;  // loads in flight per thread
+        for (int q0 = k + 1; q0 < p.n; q0 += B) {
+          T v[B];
+#pragma unroll
+          for (int u = 0; u < B; ++u)
+            if (q0 + u < p.n) v[u] = p.A[ba + col_at[q0 + u] * R];
+#pragma unroll
+          for (int u = 0; u < B; ++u)
+            if (q0 + u < p.n) {
+              const int c = col_at[q0 + u];
+              const T x = v[u] - m * U[c];
+              p.A[ba + c * R] = x;
+              const Cand<T> cd{T(fabs(x)), q0 + u, c, ps, s};
+              if (better(cd, best)) best = cd;
+            }
         }
       }
     }
-    if (k + 1 < p.r) {
+    if (more) {
       best = block_best(best, red);
       if (threadIdx.x == 0) out[blockIdx.x] = best;
       grid_sync(p.bar);
@@ -217,12 +323,14 @@ __global__ void __launch_bounds__(kFacThreads) plu_kernel(LuArgs<T> p) {
   }
 
   if (k0 < p.r) {
-    // Remaining L columns are unit vectors at the rows sitting at physical
-    // positions k0..r-1 (the corner is exactly zero).
+    // the remaining L columns are unit vectors at the rows sitting at
+    // physical positions k0..r-1 (the corner is exactly zero)
     for (i64 s = r0 + threadIdx.x; s < r1; s += blockDim.x) {
       const i64 ps = p.phys[s];
       if (ps < k0) continue;
-      for (int j = k0; j < p.r; ++j) p.Z[panel_addr(s, j, p.R, p.r)] = (ps == j) ? T(1) : T(0);
+      const i64 aa = s / R, bb = s - aa * R;
+      const i64 bz = unit ? s : aa * p.r * R + bb;
+      for (int j = k0; j < p.r; ++j) p.Z[bz + j * R] = (ps == j) ? T(1) : T(0);
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *p.info = k0;
@@ -242,10 +350,12 @@ struct QrArgs {
   T* diag;          // [r] R_kk = beta_k
   GridBarrier* bar;
   int* rank_warning;
+  const int* skip;  // when non-null and *skip == 0: CholeskyQR2 already produced Q
 };
 
 template <typename T>
 __global__ void __launch_bounds__(kFacThreads) householder_kernel(QrArgs<T> p) {
+  if (p.skip != nullptr && *p.skip == 0) return;
   __shared__ double red[33];
   __shared__ double tmp[kMaxPanelCols];
   const int G = gridDim.x;
@@ -254,16 +364,18 @@ __global__ void __launch_bounds__(kFacThreads) householder_kernel(QrArgs<T> p) {
   const i64 r1 = r0 + chunk < p.J ? r0 + chunk : p.J;
   constexpr int PW = kMaxPanelCols + 1;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const i64 R = p.R;
   int phase = 0;
 
   for (int k = 0; k < p.r; ++k) {
     const i64 sk = kolda_inverse(p.km, k, p.R);
     const bool own_k = (sk >= r0 && sk < r1);
+    const i64 bk = row_base(sk, R, p.J, p.n);
     // 1. tail squared norm of column k
     double acc = 0.0;
     for (i64 s = r0 + threadIdx.x; s < r1; s += blockDim.x)
       if (p.krow[s] > k) {
-        const double x = double(p.A[panel_addr(s, k, p.R, p.n)]);
+        const double x = double(p.A[row_base(s, R, p.J, p.n) + k * R]);
         acc += x * x;
       }
     acc = block_sum(acc, red);
@@ -274,7 +386,7 @@ __global__ void __launch_bounds__(kFacThreads) householder_kernel(QrArgs<T> p) {
     for (int q = 0; q < G; ++q) tsq += ldcg(&pb[q * PW]);
     phase ^= 1;
     const T tail_sq = T(tsq);
-    const T c0 = ldcg(&p.A[panel_addr(sk, k, p.R, p.n)]);
+    const T c0 = ldcg(&p.A[bk + k * R]);
     T beta, t;
     const bool trivial = !(tail_sq > Traits<T>::realmin);
     if (trivial) {
@@ -293,7 +405,7 @@ __global__ void __launch_bounds__(kFacThreads) householder_kernel(QrArgs<T> p) {
     // 2. essential vector (own tail rows) and partial v^T A(:, j)
     for (i64 s = r0 + threadIdx.x; s < r1; s += blockDim.x)
       if (p.krow[s] > k) {
-        const i64 ad = panel_addr(s, k, p.R, p.n);
+        const i64 ad = row_base(s, R, p.J, p.n) + k * R;
         p.A[ad] = trivial ? T(0) : p.A[ad] / denom;
       }
     __syncthreads();
@@ -305,10 +417,12 @@ __global__ void __launch_bounds__(kFacThreads) householder_kernel(QrArgs<T> p) {
       const int j = k + 1 + jj;
       double a2 = 0.0;
       for (i64 s = r0 + lane; s < r1; s += 32)
-        if (p.krow[s] > k)
-          a2 += double(p.A[panel_addr(s, k, p.R, p.n)]) * double(p.A[panel_addr(s, j, p.R, p.n)]);
+        if (p.krow[s] > k) {
+          const i64 b = row_base(s, R, p.J, p.n);
+          a2 += double(p.A[b + k * R]) * double(p.A[b + j * R]);
+        }
       a2 = warp_sum(a2);
-      if (lane == 0) pb[blockIdx.x * PW + jj] = a2 + (own_k ? double(p.A[panel_addr(sk, j, p.R, p.n)]) : 0.0);
+      if (lane == 0) pb[blockIdx.x * PW + jj] = a2 + (own_k ? double(p.A[bk + j * R]) : 0.0);
     }
     grid_sync(p.bar);
     for (int jj = threadIdx.x; jj < ncol; jj += blockDim.x) {
@@ -321,23 +435,16 @@ __global__ void __launch_bounds__(kFacThreads) householder_kernel(QrArgs<T> p) {
     // 3. rank-1 update of own rows
     for (i64 s = r0 + threadIdx.x; s < r1; s += blockDim.x) {
       const i64 kr = p.krow[s];
+      const i64 b = row_base(s, R, p.J, p.n);
       if (kr > k) {
-        const T e = p.A[panel_addr(s, k, p.R, p.n)];
-        for (int jj = 0; jj < ncol; ++jj) {
-          const i64 ad = panel_addr(s, k + 1 + jj, p.R, p.n);
-          p.A[ad] -= t * e * T(tmp[jj]);
-        }
+        const T e = p.A[b + k * R];
+        for (int jj = 0; jj < ncol; ++jj) p.A[b + (k + 1 + jj) * R] -= t * e * T(tmp[jj]);
       } else if (kr == k) {
-        for (int jj = 0; jj < ncol; ++jj) {
-          const i64 ad = panel_addr(s, k + 1 + jj, p.R, p.n);
-          p.A[ad] -= t * T(tmp[jj]);
-        }
+        for (int jj = 0; jj < ncol; ++jj) p.A[b + (k + 1 + jj) * R] -= t * T(tmp[jj]);
       }
     }
   }
-  // every tau/diag write (block 0) visible before the Q sweep
-  grid_sync(p.bar);
-  // rank warning (compress.hpp:64-71)
+  grid_sync(p.bar);  // every tau/diag write (block 0) visible before the Q sweep
   if (blockIdx.x == 0 && threadIdx.x == 0 && p.rank_warning) {
     T dmax = T(0), dmin = T(INFINITY);
     for (int k = 0; k < p.r; ++k) {
@@ -351,7 +458,8 @@ __global__ void __launch_bounds__(kFacThreads) householder_kernel(QrArgs<T> p) {
   // Q = H_0 ... H_{r-1} I(J, r): start from the identity columns.
   for (i64 s = r0 + threadIdx.x; s < r1; s += blockDim.x) {
     const i64 kr = p.krow[s];
-    for (int j = 0; j < p.r; ++j) p.Q[panel_addr(s, j, p.R, p.r)] = (kr == j) ? T(1) : T(0);
+    const i64 b = row_base(s, R, p.J, p.r);
+    for (int j = 0; j < p.r; ++j) p.Q[b + j * R] = (kr == j) ? T(1) : T(0);
   }
   __syncthreads();  // rows are written thread-per-row, read warp-per-column below
   for (int k = p.r - 1; k >= 0; --k) {
@@ -359,16 +467,17 @@ __global__ void __launch_bounds__(kFacThreads) householder_kernel(QrArgs<T> p) {
     if (t == T(0)) continue;  // uniform across CTAs
     const i64 sk = kolda_inverse(p.km, k, p.R);
     const bool own_k = (sk >= r0 && sk < r1);
+    const i64 bqk = row_base(sk, R, p.J, p.r);
     const int ncol = p.r - k;  // columns j < k are untouched (exactly unchanged in Eigen too)
     double* pb = p.part + phase * G * PW;
-    for (int jj = wid; jj < ncol; jj += nw) {  // warp per column
+    for (int jj = wid; jj < ncol; jj += nw) {
       const int j = k + jj;
       double a2 = 0.0;
       for (i64 s = r0 + lane; s < r1; s += 32)
         if (p.krow[s] > k)
-          a2 += double(p.A[panel_addr(s, k, p.R, p.n)]) * double(p.Q[panel_addr(s, j, p.R, p.r)]);
+          a2 += double(p.A[row_base(s, R, p.J, p.n) + k * R]) * double(p.Q[row_base(s, R, p.J, p.r) + j * R]);
       a2 = warp_sum(a2);
-      if (lane == 0) pb[blockIdx.x * PW + jj] = a2 + (own_k ? double(p.Q[panel_addr(sk, j, p.R, p.r)]) : 0.0);
+      if (lane == 0) pb[blockIdx.x * PW + jj] = a2 + (own_k ? double(p.Q[bqk + j * R]) : 0.0);
     }
     grid_sync(p.bar);
     for (int jj = threadIdx.x; jj < ncol; jj += blockDim.x) {
@@ -380,22 +489,152 @@ __global__ void __launch_bounds__(kFacThreads) householder_kernel(QrArgs<T> p) {
     __syncthreads();
     for (i64 s = r0 + threadIdx.x; s < r1; s += blockDim.x) {
       const i64 kr = p.krow[s];
+      const i64 bq = row_base(s, R, p.J, p.r);
       if (kr > k) {
-        const T e = p.A[panel_addr(s, k, p.R, p.n)];
-        for (int jj = 0; jj < ncol; ++jj) p.Q[panel_addr(s, k + jj, p.R, p.r)] -= t * e * T(tmp[jj]);
+        const T e = p.A[row_base(s, R, p.J, p.n) + k * R];
+        for (int jj = 0; jj < ncol; ++jj) p.Q[bq + (k + jj) * R] -= t * e * T(tmp[jj]);
       } else if (kr == k) {
-        for (int jj = 0; jj < ncol; ++jj) p.Q[panel_addr(s, k + jj, p.R, p.r)] -= t * T(tmp[jj]);
+        for (int jj = 0; jj < ncol; ++jj) p.Q[bq + (k + jj) * R] -= t * T(tmp[jj]);
       }
     }
     __syncthreads();
   }
 }
 
+// -------------------------------------------------------- CholeskyQR2
+// One CTA; Y is I x n column-major (I >= n). work >= I*n doubles.
+// status: 0 = Q written, 1 = fall back to Householder.
+template <typename T>
+__global__ void __launch_bounds__(kSmallThreads) cqr2_kernel(const T* __restrict__ Y, T* __restrict__ Q, int I, int n,
+                                                             double* __restrict__ work, int* status,
+                                                             int* rank_warning) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* G = reinterpret_cast<double*>(smem_raw);  // n x n
+  double* Rm = G + n * n;                            // n x n upper Cholesky factor
+  double* dg = Rm + n * n;                           // [2][n] diagonals of R1, R2
+  double* sgn = dg + 2 * n;                          // [n]
+  __shared__ int s_fail;
+  __shared__ double s_piv;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  if (tid == 0) s_fail = 0;
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass) {
+    // G = V^T V with V = Y (pass 0) or Q1 (pass 1, in work)
+    for (int e = wid; e < n * n; e += nw) {
+      const int a = e % n, b = e / n;
+      if (a > b) continue;
+      double s = 0.0;
+      if (pass == 0) {
+        for (int i = lane; i < I; i += 32) s += double(Y[i + i64(a) * I]) * double(Y[i + i64(b) * I]);
+      } else {
+        for (int i = lane; i < I; i += 32) s += work[i + i64(a) * I] * work[i + i64(b) * I];
+      }
+      s = warp_sum(s);
+      if (lane == 0) {
+        G[a + b * n] = s;
+        G[b + a * n] = s;
+      }
+    }
+    __syncthreads();
+    // upper Cholesky G = R^T R (R in Rm, column-major upper)
+    for (int j = 0; j < n; ++j) {
+      if (tid == 0) {
+        double d = G[j + j * n];
+        for (int k = 0; k < j; ++k) d -= Rm[k + j * n] * Rm[k + j * n];
+        if (!(d > 0.0)) s_fail = 1;
+        s_piv = d > 0.0 ? sqrt(d) : 1.0;
+        Rm[j + j * n] = s_piv;
+        dg[pass * n + j] = s_piv;
+      }
+      __syncthreads();
+      const double dj = s_piv;
+      for (int c = j + 1 + tid; c < n; c += nt) {
+        double s = G[j + c * n];
+        for (int k = 0; k < j; ++k) s -= Rm[k + j * n] * Rm[k + c * n];
+        Rm[j + c * n] = s / dj;
+      }
+      __syncthreads();
+    }
+    if (s_fail) break;
+    // Ri = R^{-1} (upper; column-parallel back substitution), stored in G
+    for (int j = tid; j < n; j += nt) {
+      for (int i = j + 1; i < n; ++i) G[i + j * n] = 0.0;
+      G[j + j * n] = 1.0 / Rm[j + j * n];
+      for (int i = j - 1; i >= 0; --i) {
+        double s = 0.0;
+        for (int k = i + 1; k <= j; ++k) s += Rm[i + k * n] * G[k + j * n];
+        G[i + j * n] = -s / Rm[i + i * n];
+      }
+    }
+    __syncthreads();
+    // V <- V R^{-1}: out (i, j) = sum_{k <= j} V(i, k) Ri(k, j); pass 0 writes
+    // Q1 into work, pass 1 keeps Q1 (work) and writes Q2 to the tail half.
+    double* dst = pass == 0 ? work : work + i64(I) * n;
+    for (i64 e = tid; e < i64(I) * n; e += nt) {
+      const int i = int(e % I), j = int(e / I);
+      double s = 0.0;
+      for (int k = 0; k <= j; ++k)
+        s += (pass == 0 ? double(Y[i + i64(k) * I]) : work[i + i64(k) * I]) * G[k + j * n];
+      dst[e] = s;
+    }
+    __syncthreads();
+  }
+  if (!s_fail) {
+    for (i64 e = tid; e < i64(I) * n; e += nt) work[e] = work[e + i64(I) * n];
+    __syncthreads();
+  }
+  if (!s_fail && tid == 0) {
+    // conditioning guard: CholeskyQR2 is only used well inside its stable range
+    double mx = 0.0, mn = INFINITY;
+    for (int j = 0; j < n; ++j) {
+      mx = fmax(mx, dg[j]);
+      mn = fmin(mn, dg[j]);
+    }
+    if (!(mn > 0.0) || mx / mn > 1e6) s_fail = 1;
+  }
+  __syncthreads();
+  if (s_fail) {
+    if (tid == 0) *status = 1;
+    return;
+  }
+  // Householder sign reconstruction on the top n x n block of Q2 (in G).
+  for (int e = tid; e < n * n; e += nt) G[e] = work[(e % n) + i64(e / n) * I];
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    if (tid == 0) sgn[k] = G[k + k * n] > 0.0 ? -1.0 : 1.0;
+    __syncthreads();
+    const double sk = sgn[k];
+    if (sk < 0.0)
+      for (int i = tid; i < n; i += nt) G[i + k * n] = -G[i + k * n];
+    __syncthreads();
+    if (tid == 0) G[k + k * n] -= 1.0;
+    __syncthreads();
+    const double dkk = G[k + k * n];
+    for (int j = k + 1 + (tid >> 5); j < n; j += (nt >> 5))
+      for (int i = k + 1 + (tid & 31); i < n; i += 32) G[i + j * n] -= (G[i + k * n] / dkk) * G[k + j * n];
+    __syncthreads();
+  }
+  for (i64 e = tid; e < i64(I) * n; e += nt) Q[e] = T(work[e] * sgn[e / I]);
+  if (tid == 0) {
+    T dmax = T(0), dmin = T(INFINITY);
+    for (int j = 0; j < n; ++j) {
+      const T d = T(dg[j] * dg[n + j]);
+      dmax = d > dmax ? d : dmax;
+      dmin = d < dmin ? d : dmin;
+    }
+    if (rank_warning) *rank_warning = (dmax == T(0)) || (dmin <= T(I) * Traits<T>::eps * dmax);
+    *status = 0;
+  }
+}
+
 int pick_grid(i64 J, int n, int maxc) {
-  // ~8K panel entries per CTA; single CTA for the small I x l samples.
-  const i64 want = ceil_div(J * n, 8192);
+  // ~4K panel entries per CTA: the per-step update is latency bound
+  const i64 want = ceil_div(J * n, 4096);
   return int(std::max<i64>(1, std::min<i64>(want, maxc)));
 }
+
+size_t smem_lu_bytes(i64 I, int n, size_t tsize) { return size_t(I) * n * tsize + size_t(I) * sizeof(int); }
 
 }  // namespace
 
@@ -410,11 +649,20 @@ template <typename T>
 int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w, cudaStream_t st) {
   check_arg(n <= kMaxPanelCols, "plu_basis: panel wider than supported");
   const int r = int(std::min<i64>(J, n));
+  const size_t smem = smem_lu_bytes(J, n, sizeof(T));
+  const bool kolda_identity = (km.n_low == 0 && km.n_high == 1);
+  static const size_t lu_lim = enable_max_dyn_smem(plu_smem_kernel<T>);
+  if (R == J && kolda_identity && smem <= lu_lim) {
+    plu_smem_kernel<T><<<1, kSmallThreads, smem, st>>>(A, Z, int(J), n, w.info);
+    count_launch();
+    RCPG_LAUNCHED();
+    return r;
+  }
   init_row_keys(km, J, R, w.keys, st);
-  const int maxc = max_coop_blocks(plu_kernel<T>, kFacThreads, 0);
-  const int G = pick_grid(J, n, maxc);
+  const int maxc = max_coop_blocks(plu_coop_kernel<T>, kFacThreads, 0);
+  const int G = std::min(pick_grid(J, n, maxc), w.max_blocks);
   LuArgs<T> a{A, Z, J, R, n, r, w.keys, km, reinterpret_cast<Cand<T>*>(w.cands), w.bar, w.info};
-  launch_coop(plu_kernel<T>, G, kFacThreads, 0, st, a);
+  launch_coop(plu_coop_kernel<T>, G, kFacThreads, 0, st, a);
   return r;
 }
 
@@ -423,11 +671,21 @@ int thin_qr(T* A, T* Q, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w, 
             cudaStream_t st) {
   check_arg(n <= kMaxPanelCols, "thin_qr: panel wider than supported");
   const int r = int(std::min<i64>(J, n));
+  const bool kolda_identity = (km.n_low == 0 && km.n_high == 1);
+  const int* skip = nullptr;
+  const size_t cq_smem = (2 * size_t(n) * n + 3 * size_t(n)) * sizeof(double);
+  static const size_t cq_lim = enable_max_dyn_smem(cqr2_kernel<T>);
+  if (R == J && kolda_identity && J >= n && J <= w.cqr_rows && cq_smem <= cq_lim) {
+    cqr2_kernel<T><<<1, kSmallThreads, cq_smem, st>>>(A, Q, int(J), n, w.cqr_work, w.info + 2, rank_warning_dev);
+    count_launch();
+    RCPG_LAUNCHED();
+    skip = w.info + 2;  // the Householder kernel below runs only if CholeskyQR2 declined
+  }
   init_row_keys(km, J, R, w.keys, st);
   const int maxc = max_coop_blocks(householder_kernel<T>, kFacThreads, 0);
   const int G = std::min(pick_grid(J, n, maxc), w.max_blocks);
-  QrArgs<T> a{A, Q, J, R, n, r, w.keys, km, w.part, reinterpret_cast<T*>(w.tau), reinterpret_cast<T*>(w.diag),
-              w.bar, rank_warning_dev};
+  QrArgs<T> a{A,     Q,      J, R, n, r, w.keys, km, w.part, reinterpret_cast<T*>(w.tau), reinterpret_cast<T*>(w.diag),
+              w.bar, rank_warning_dev, skip};
   launch_coop(householder_kernel<T>, G, kFacThreads, 0, st, a);
   return r;
 }

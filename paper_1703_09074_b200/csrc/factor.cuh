@@ -17,6 +17,8 @@ struct FactorWork {
   double* part = nullptr;     // [2][max_blocks][kMaxPanelCols + 1]
   void* tau = nullptr;        // [kMaxPanelCols] (double-sized)
   void* diag = nullptr;       // [kMaxPanelCols]
+  double* cqr_work = nullptr; // [cqr_rows * kMaxPanelCols] CholeskyQR2 scratch
+  i64 cqr_rows = 0;           // largest I for the single-CTA CholeskyQR2 path
   int max_blocks = 0;
 };
 

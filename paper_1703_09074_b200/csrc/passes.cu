@@ -24,11 +24,8 @@ template <typename T, int BM, int BN, int BK, bool TXM, class LD, class EP>
 void launch_tile_gemm(dim3 grid, const LD& ld, const EP& ep, cudaStream_t st) {
   auto kern = tile_gemm_kernel<T, BM, BN, BK, TXM, LD, EP>;
   const size_t smem = sizeof(TileSmem<T, BM, BN, BK>);
-  static bool configured = false;  // per instantiation
-  if (!configured) {
-    RCPG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    configured = true;
-  }
+  static const size_t lim = enable_max_dyn_smem(kern);  // per instantiation
+  if (smem > lim) throw std::runtime_error("tile_gemm: shared memory tile too large");
   kern<<<grid, kThreads, smem, st>>>(ld, ep);
   count_launch();
   RCPG_LAUNCHED();

@@ -43,6 +43,18 @@ int max_coop_blocks(K kernel, int threads, size_t smem) {
   return per_sm * device_caps().num_sms;
 }
 
+// Opt a kernel into the largest dynamic shared memory the device allows
+// (limit minus the kernel's static shared memory); returns that size.
+template <typename K>
+size_t enable_max_dyn_smem(K kernel) {
+  cudaFuncAttributes fa{};
+  RCPG_CUDA(cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(kernel)));
+  const size_t lim = size_t(device_caps().max_smem_optin) - fa.sharedSizeBytes;
+  RCPG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(kernel),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(lim)));
+  return lim;
+}
+
 template <typename K, typename... Args>
 void launch_coop(K kernel, int blocks, int threads, size_t smem, cudaStream_t st, Args... args) {
   void* argv[] = {static_cast<void*>(&args)...};
