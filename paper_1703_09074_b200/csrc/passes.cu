@@ -1,6 +1,8 @@
 // SPDX-License-Identifier: MIT
 // Host launchers for the streamed tensor passes (see passes.cuh) and the
 // Omega generator (compress.hpp:118-124, random.hpp:75-94).
+#include <type_traits>
+
 #include "passes.cuh"
 #include "rng.cuh"
 #include "runtime.cuh"
@@ -81,9 +83,17 @@ void sketch_plan(ModeView v, i64 cols, int num_sms, i64& splits, i64& tiles_per_
 }  // namespace
 
 template <typename T>
+constexpr bool use_dmma(const ModeView& v) {
+  return std::is_same<T, double>::value && v.R > 1;
+}
+
+template <typename T>
 i64 sketch_scratch_elems(ModeView v, i64 cols, int num_sms) {
   i64 splits, tps, total;
-  sketch_plan<T>(v, cols, num_sms, splits, tps, total);
+  if (use_dmma<T>(v))
+    splits = sketch_dmma_splits(v, cols, num_sms, tps, total);
+  else
+    sketch_plan<T>(v, cols, num_sms, splits, tps, total);
   return splits * cols * v.I;
 }
 
@@ -91,6 +101,11 @@ template <typename T>
 void sketch(const T* X, ModeView v, const T* P, i64 cols, T* Y, T* scratch, i64 scratch_elems, int num_sms,
             cudaStream_t st, const int* skip) {
   i64 splits, tps, total;
+  if (use_dmma<T>(v)) {
+    splits = sketch_dmma_splits(v, cols, num_sms, tps, total);
+    if (splits * cols * v.I > scratch_elems) throw std::runtime_error("sketch: scratch too small");
+    if constexpr (std::is_same<T, double>::value) sketch_dmma(X, v, P, cols, scratch, num_sms, skip, st);
+  } else {
   sketch_plan<T>(v, cols, num_sms, splits, tps, total);
   if (splits * cols * v.I > scratch_elems) throw std::runtime_error("sketch: scratch too small");
   switch (pick_bn(cols)) {
@@ -99,6 +114,7 @@ void sketch(const T* X, ModeView v, const T* P, i64 cols, T* Y, T* scratch, i64 
     case 48: sketch_bn<T, 48>(X, v, P, cols, scratch, splits, tps, total, st, skip); break;
     case 64: sketch_bn<T, 64>(X, v, P, cols, scratch, splits, tps, total, st, skip); break;
     default: sketch_bn<T, 80>(X, v, P, cols, scratch, splits, tps, total, st, skip); break;
+  }
   }
   const i64 n = cols * v.I;
   const int blocks = int(std::min<i64>(ceil_div(n, 256), 4 * num_sms));
@@ -133,6 +149,12 @@ void project_bn(const T* X, ModeView v, const T* Q, i64 ldq, i64 cols, T* O, cud
 
 template <typename T>
 void project(const T* X, ModeView v, const T* Q, i64 ldq, i64 cols, T* O, cudaStream_t st) {
+  if constexpr (std::is_same<T, double>::value) {
+    if (v.R > 1) {
+      project_dmma(X, v, Q, ldq, cols, O, st);
+      return;
+    }
+  }
   switch (pick_bn(cols)) {
     case 16: project_bn<T, 16>(X, v, Q, ldq, cols, O, st); break;
     case 32: project_bn<T, 32>(X, v, Q, ldq, cols, O, st); break;

@@ -278,6 +278,12 @@ i64 sketch_scratch_elems(ModeView v, i64 cols, int num_sms);
 template <typename T>
 void project(const T* X, ModeView v, const T* Q, i64 ldq, i64 cols, T* O, cudaStream_t st);
 
+// FP64 tensor-core (DMMA) versions for mode views with R > 1 (passes_dmma.cu).
+i64 sketch_dmma_splits(ModeView v, i64 cols, int num_sms, i64& tps, i64& total);
+void sketch_dmma(const double* X, ModeView v, const double* P, i64 cols, double* part, int num_sms,
+                 const int* skip, cudaStream_t st);
+void project_dmma(const double* X, ModeView v, const double* Q, i64 ldq, i64 cols, double* O, cudaStream_t st);
+
 // Omega_n written in the panel layout (a, c, b): entry (s, c) is normal /
 // uniform_sym number c*J + kolda(s) of stream (seed, (compress << 32) | mode).
 template <typename T>

@@ -1,0 +1,321 @@
+// SPDX-License-Identifier: MIT
+// FP64 streamed passes on the B200 double-precision tensor cores
+// (mma.sync.m16n8k4.f64, DMMA). The fp64 configs (C1/C2) are FP64-pipe
+// bound: a pass does 2*S*l flops over S*8 bytes (AI = l/4 flop/B), so at
+// l = 30 the ~37 TFLOP/s FP64 peak caps a pass at ~75% of HBM bandwidth.
+// SIMT DFMA tiles were shared-memory-bandwidth bound (one LDS per two
+// FMAs); a DMMA does 512 FMAs per warp instruction from register fragments.
+//
+//   sketch  Y[i, c]    = sum_{a,b} X[a, i, b] P[a, c, b]   (K = (a, b), split over CTAs)
+//   project O[a, c, b] = sum_i X[a, i, b] Q[i, c]          (K = i, full per CTA)
+// (mode views with R > 1; the last mode (R = 1) keeps the SIMT kernels.)
+// Operand tiles stream through a multi-stage cp.async pipeline (16-byte
+// copies when the row strides are even, 8-byte otherwise; out-of-range
+// elements are zero-filled by the copy itself).
+#include "passes.cuh"
+#include "runtime.cuh"
+
+namespace rcpg {
+
+namespace {
+
+constexpr int kDThreads = 128;  // 4 warps, each a 16-row slab of the CTA tile
+constexpr int kDBM = 64;
+constexpr int kDBK = 32;
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool ok) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  const int n = ok ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(n));
+}
+__device__ __forceinline__ void cp_async16(double* dst, const double* src, bool ok) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  const int n = ok ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(n));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+               : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+               : "d"(a0), "d"(a1), "d"(b0));
+}
+
+template <int BN>
+constexpr int stages_for() {
+  return BN <= 32 ? 4 : (BN <= 48 ? 3 : 2);
+}
+
+// ------------------------------------------------------------- sketch
+// smem per stage: A [BM][BK+4] (m rows, k contiguous), B [BN][BK+4].
+template <int BN, bool V16>
+__global__ void __launch_bounds__(kDThreads) sketch_dmma_kernel(const double* __restrict__ X,
+                                                                const double* __restrict__ P, i64 I, i64 R, i64 cols,
+                                                                i64 nbt, i64 tiles_per_split, i64 total,
+                                                                double* __restrict__ part, const int* skip) {
+  if (skip != nullptr && *skip) return;
+  constexpr int S = stages_for<BN>();
+  constexpr int SA = kDBK + 4;
+  constexpr int NT = BN / 8;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* sA = reinterpret_cast<double*>(smem_raw);  // [S][BM][SA]
+  double* sB = sA + S * kDBM * SA;                    // [S][BN][SA]
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
+  const i64 m0 = i64(blockIdx.x) * kDBM;
+  const i64 n0 = i64(blockIdx.z) * BN;
+  const i64 t0 = blockIdx.y * tiles_per_split;
+  const i64 t1 = t0 + tiles_per_split < total ? t0 + tiles_per_split : total;
+  const int nk = int(t1 - t0);
+
+  auto load = [&](int stage, i64 tt) {
+    const i64 a = tt / nbt, b0 = (tt - a * nbt) * kDBK;
+    double* dA = sA + stage * kDBM * SA;
+    double* dB = sB + stage * BN * SA;
+    constexpr int W = V16 ? 2 : 1;       // doubles per copy
+    constexpr int CPR = kDBK / W;        // copies per row
+    for (int e = tid; e < kDBM * CPR; e += kDThreads) {
+      const int m = e / CPR, k = (e % CPR) * W;
+      const i64 i = m0 + m, b = b0 + k;
+      const bool ok = (i < I) && (b < R);
+      const double* src = X + (ok ? ((a * I + i) * R + b) : 0);
+      if (V16) cp_async16(dA + m * SA + k, src, ok); else cp_async8(dA + m * SA + k, src, ok);
+    }
+    for (int e = tid; e < BN * CPR; e += kDThreads) {
+      const int n = e / CPR, k = (e % CPR) * W;
+      const i64 c = n0 + n, b = b0 + k;
+      const bool ok = (c < cols) && (b < R);
+      const double* src = P + (ok ? ((a * cols + c) * R + b) : 0);
+      if (V16) cp_async16(dB + n * SA + k, src, ok); else cp_async8(dB + n * SA + k, src, ok);
+    }
+  };
+
+  double acc[NT][4];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) {
+    if (s < nk) load(s, t0 + s);
+    cp_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_wait<S - 2>();
+    __syncthreads();
+    const int pre = kt + S - 1;
+    if (pre < nk) load(pre % S, t0 + pre);
+    cp_commit();
+    const double* cA = sA + (kt % S) * kDBM * SA + (w * 16) * SA;
+    const double* cB = sB + (kt % S) * BN * SA;
+#pragma unroll
+    for (int kk = 0; kk < kDBK; kk += 4) {
+      const double a0 = cA[g * SA + kk + t];
+      const double a1 = cA[(g + 8) * SA + kk + t];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) dmma(acc[j], a0, a1, cB[(j * 8 + g) * SA + kk + t]);
+    }
+  }
+  cp_wait<0>();
+  // partial[split][c][i]
+  const i64 r0 = m0 + w * 16 + g;
+  double* out = part + i64(blockIdx.y) * cols * I;
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    const i64 c0 = n0 + j * 8 + 2 * t;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const i64 i = r0 + (q >> 1) * 8, c = c0 + (q & 1);
+      if (i < I && c < cols) out[c * I + i] = acc[j][q];
+    }
+  }
+}
+
+// ------------------------------------------------------------ project
+// M = b (BM), N = c, K = i. smem per stage: A [BK][BM+8] (k rows, m
+// contiguous), B [BN][BK+4].
+template <int BN, bool VA16, bool VB16>
+__global__ void __launch_bounds__(kDThreads) project_dmma_kernel(const double* __restrict__ X,
+                                                                 const double* __restrict__ Q, i64 I, i64 R, i64 cols,
+                                                                 i64 ldq, double* __restrict__ O) {
+  constexpr int S = stages_for<BN>();
+  constexpr int SAm = kDBM + 8;
+  constexpr int SB = kDBK + 4;
+  constexpr int NT = BN / 8;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* sA = reinterpret_cast<double*>(smem_raw);  // [S][BK][SAm]
+  double* sB = sA + S * kDBK * SAm;                   // [S][BN][SB]
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
+  const i64 b0 = i64(blockIdx.x) * kDBM;
+  const i64 a = blockIdx.y;
+  const i64 n0 = i64(blockIdx.z) * BN;
+  const int nk = int(ceil_div(I, kDBK));
+  const double* Xa = X + a * I * R;
+
+  auto load = [&](int stage, int kt) {
+    const i64 i0 = i64(kt) * kDBK;
+    double* dA = sA + stage * kDBK * SAm;
+    double* dB = sB + stage * BN * SB;
+    {
+      constexpr int W = VA16 ? 2 : 1;
+      constexpr int CPR = kDBM / W;
+      for (int e = tid; e < kDBK * CPR; e += kDThreads) {
+        const int k = e / CPR, m = (e % CPR) * W;
+        const i64 i = i0 + k, b = b0 + m;
+        const bool ok = (i < I) && (b < R);
+        const double* src = Xa + (ok ? (i * R + b) : 0);
+        if (VA16) cp_async16(dA + k * SAm + m, src, ok); else cp_async8(dA + k * SAm + m, src, ok);
+      }
+    }
+    {
+      constexpr int W = VB16 ? 2 : 1;
+      constexpr int CPR = kDBK / W;
+      for (int e = tid; e < BN * CPR; e += kDThreads) {
+        const int n = e / CPR, k = (e % CPR) * W;
+        const i64 c = n0 + n, i = i0 + k;
+        const bool ok = (c < cols) && (i < I);
+        const double* src = Q + (ok ? (i + c * ldq) : 0);
+        if (VB16) cp_async16(dB + n * SB + k, src, ok); else cp_async8(dB + n * SB + k, src, ok);
+      }
+    }
+  };
+
+  double acc[NT][4];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) {
+    if (s < nk) load(s, s);
+    cp_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_wait<S - 2>();
+    __syncthreads();
+    const int pre = kt + S - 1;
+    if (pre < nk) load(pre % S, pre);
+    cp_commit();
+    const double* cA = sA + (kt % S) * kDBK * SAm + w * 16;
+    const double* cB = sB + (kt % S) * BN * SB;
+#pragma unroll
+    for (int kk = 0; kk < kDBK; kk += 4) {
+      const double a0 = cA[(kk + t) * SAm + g];
+      const double a1 = cA[(kk + t) * SAm + g + 8];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) dmma(acc[j], a0, a1, cB[(j * 8 + g) * SB + kk + t]);
+    }
+  }
+  cp_wait<0>();
+  const i64 bb = b0 + w * 16 + g;
+  double* Oa = O + a * cols * R;
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    const i64 c0 = n0 + j * 8 + 2 * t;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const i64 b = bb + (q >> 1) * 8, c = c0 + (q & 1);
+      if (b < R && c < cols) Oa[c * R + b] = acc[j][q];
+    }
+  }
+}
+
+int pick_bn8(i64 cols) {
+  if (cols <= 16) return 16;
+  if (cols <= 32) return 32;
+  if (cols <= 48) return 48;
+  if (cols <= 64) return 64;
+  return 80;
+}
+
+template <int BN, bool V>
+void launch_sketch(dim3 grid, const double* X, const double* P, ModeView v, i64 cols, i64 nbt, i64 tps, i64 total,
+                   double* part, const int* skip, cudaStream_t st) {
+  constexpr int S = stages_for<BN>();
+  const size_t smem = size_t(S) * (kDBM + BN) * (kDBK + 4) * sizeof(double);
+  static const size_t lim = enable_max_dyn_smem(sketch_dmma_kernel<BN, V>);
+  if (smem > lim) throw std::runtime_error("sketch_dmma: smem plan too large");
+  sketch_dmma_kernel<BN, V><<<grid, kDThreads, smem, st>>>(X, P, v.I, v.R, cols, nbt, tps, total, part, skip);
+  count_launch();
+  RCPG_LAUNCHED();
+}
+
+template <int BN, bool VA, bool VB>
+void launch_project(dim3 grid, const double* X, const double* Q, ModeView v, i64 cols, i64 ldq, double* O,
+                    cudaStream_t st) {
+  constexpr int S = stages_for<BN>();
+  const size_t smem = size_t(S) * (kDBK * (kDBM + 8) + BN * (kDBK + 4)) * sizeof(double);
+  static const size_t lim = enable_max_dyn_smem(project_dmma_kernel<BN, VA, VB>);
+  if (smem > lim) throw std::runtime_error("project_dmma: smem plan too large");
+  project_dmma_kernel<BN, VA, VB><<<grid, kDThreads, smem, st>>>(X, Q, v.I, v.R, cols, ldq, O);
+  count_launch();
+  RCPG_LAUNCHED();
+}
+
+}  // namespace
+
+i64 sketch_dmma_splits(ModeView v, i64 cols, int num_sms, i64& tps, i64& total) {
+  const i64 mt = ceil_div(v.I, kDBM), nt = ceil_div(cols, pick_bn8(cols));
+  total = v.L * ceil_div(v.R, kDBK);
+  i64 want = ceil_div(i64(4) * num_sms, mt * nt);
+  want = std::max<i64>(1, std::min<i64>(want, 65535));
+  tps = std::max<i64>(1, ceil_div(total, want));
+  return ceil_div(total, tps);
+}
+
+void sketch_dmma(const double* X, ModeView v, const double* P, i64 cols, double* part, int num_sms, const int* skip,
+                 cudaStream_t st) {
+  i64 tps, total;
+  const i64 splits = sketch_dmma_splits(v, cols, num_sms, tps, total);
+  const int BN = pick_bn8(cols);
+  const i64 nbt = ceil_div(v.R, kDBK);
+  dim3 grid{unsigned(ceil_div(v.I, kDBM)), unsigned(splits), unsigned(ceil_div(cols, BN))};
+  const bool v16 = (v.R % 2 == 0);
+#define RCPG_SK(BNV)                                                                              \
+  case BNV:                                                                                       \
+    if (v16)                                                                                      \
+      launch_sketch<BNV, true>(grid, X, P, v, cols, nbt, tps, total, part, skip, st);             \
+    else                                                                                          \
+      launch_sketch<BNV, false>(grid, X, P, v, cols, nbt, tps, total, part, skip, st);            \
+    break;
+  switch (BN) {
+    RCPG_SK(16)
+    RCPG_SK(32)
+    RCPG_SK(48)
+    RCPG_SK(64)
+    default:
+      RCPG_SK(80)
+  }
+#undef RCPG_SK
+}
+
+void project_dmma(const double* X, ModeView v, const double* Q, i64 ldq, i64 cols, double* O, cudaStream_t st) {
+  const int BN = pick_bn8(cols);
+  const bool va = (v.R % 2 == 0), vb = (ldq % 2 == 0);
+  for (i64 a0 = 0; a0 < v.L; a0 += 65535) {
+    const i64 na = std::min<i64>(65535, v.L - a0);
+    dim3 grid{unsigned(ceil_div(v.R, kDBM)), unsigned(na), unsigned(ceil_div(cols, BN))};
+    const double* Xa = X + a0 * v.I * v.R;
+    double* Oa = O + a0 * cols * v.R;
+#define RCPG_PJ(BNV)                                                                                       \
+  case BNV:                                                                                                \
+    if (va && vb)                                                                                          \
+      launch_project<BNV, true, true>(grid, Xa, Q, v, cols, ldq, Oa, st);                                  \
+    else if (va)                                                                                           \
+      launch_project<BNV, true, false>(grid, Xa, Q, v, cols, ldq, Oa, st);                                 \
+    else                                                                                                   \
+      launch_project<BNV, false, false>(grid, Xa, Q, v, cols, ldq, Oa, st);                                \
+    break;
+    switch (BN) {
+      RCPG_PJ(16)
+      RCPG_PJ(32)
+      RCPG_PJ(48)
+      RCPG_PJ(64)
+      default:
+        RCPG_PJ(80)
+    }
+#undef RCPG_PJ
+  }
+}
+
+}  // namespace rcpg
