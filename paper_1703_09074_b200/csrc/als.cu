@@ -277,22 +277,43 @@ __global__ void zero_factor_kernel(T* F, i64 n, int R, T* gram) {
 
 // --------------------------------------------------------------- ALS
 // One mode update (solve.hpp:207-230) and, for the last mode, the fit and
-// stopping test (solve.hpp:232-254), executed by one CTA. W (I x R,
-// column-major) is the MTTKRP; `work` holds 3 R^2 + 4 R doubles.
+// stopping test (solve.hpp:232-254), executed by one CTA with everything in
+// shared memory. W (I x R, column-major) is the MTTKRP. `work` holds
+// 3 R^2 + 4 R + I R doubles.
+//
+// pinv_psd(V) (solve.hpp:62-73) drops eigenvalues <= R eps lambda_max. V is
+// inverted by Gauss-Jordan (SPD, no pivoting); if every pivot is positive and
+// 1 / ||V^-1||_F > R eps ||V||_F (which bounds lambda_min from below and
+// lambda_max from above) no eigenvalue can fall under the cutoff, so
+// pinv(V) = V^-1. Otherwise the exact eigen path runs (cyclic Jacobi).
+__device__ unsigned long long* g_als_prof = nullptr;
+#define ALS_STAMP(slot)                                                              \
+  do {                                                                               \
+    if (g_als_prof && threadIdx.x == 0) {                                            \
+      unsigned long long _t;                                                         \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                          \
+      g_als_prof[slot] += _t - _tlast;                                               \
+      _tlast = _t;                                                                   \
+    }                                                                                \
+  } while (0)
+
 template <typename T, typename WT>
 __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T* weights, double tol,
                                 int max_iter, double* trace_fit, double* trace_sec, AlsState* st, double* work) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int R = fs.rank, N = fs.order;
-  const i64 I = fs.extent[mode];
+  const int I = int(fs.extent[mode]);
   T* F = fs.f[mode];
   double* V = work;          // R x R
-  double* Lm = V + R * R;    // R x R: Cholesky factor, then V^{-1}
-  double* X = Lm + R * R;    // R x R: L^{-1} / eigenvectors
+  double* A = V + R * R;     // R x R: Gauss-Jordan in place -> V^{-1}
+  double* X = A + R * R;     // R x R: eigenvectors (fallback)
   double* ev = X + R * R;    // R
   int* ord = reinterpret_cast<int*>(ev + R);
+  double* Fs = ev + 2 * R;   // I x R new factor (double, smem)
+  double* nr = Fs + i64(I) * R;  // R column norms
   __shared__ int s_ok;
-  __shared__ double s_piv;
+  unsigned long long _tlast = 0;
+  if (g_als_prof && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_tlast));
 
   // 1. V = Hadamard of the other modes' Grams (solve.hpp:209-211)
   for (int e = tid; e < R * R; e += nt) {
@@ -300,69 +321,59 @@ __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T
     for (int k = 0; k < N; ++k)
       if (k != mode) v *= double(fs.gram[k][e]);
     V[e] = double(T(v));
+    A[e] = V[e];
   }
+  if (tid == 0) s_ok = 1;
   __syncthreads();
-  double fro = 0.0;
-  for (int e = tid; e < R * R; e += nt) fro += V[e] * V[e];
-  fro = sqrt(block_reduce_sum(fro));
-  // 2. pinv_psd (solve.hpp:62-73). Fast path: when V - tau_up I is positive
-  //    definite with tau_up = R eps ||V||_F >= R eps lambda_max, every
-  //    eigenvalue exceeds the reference's cutoff and pinv(V) = V^{-1}.
-  const double tau_up = double(R) * double(Traits<T>::eps) * fro;
-  for (int pass = 0; pass < 2; ++pass) {
-    const double shift = pass == 0 ? tau_up : 0.0;
-    if (tid == 0) s_ok = 1;
-    __syncthreads();
-    for (int j = 0; j < R; ++j) {
-      if (tid == 0) {
-        double d = V[j + j * R] - shift;
-        for (int k = 0; k < j; ++k) d -= Lm[j + k * R] * Lm[j + k * R];
-        if (!(d > 0.0)) s_ok = 0;
-        s_piv = d > 0.0 ? sqrt(d) : 1.0;
-        Lm[j + j * R] = s_piv;
+  // 2. Gauss-Jordan inverse of the SPD matrix: ping-pong between A and X,
+  //    one barrier per pivot
+  const int R2 = R * R;
+  double* src = A;
+  double* dst = X;
+  const int lane0 = tid & 31, wid0 = tid >> 5, nw0 = nt >> 5;
+  for (int k = 0; k < R; ++k) {
+    const double p = src[k + k * R];
+    const double ip = 1.0 / p;
+    for (int j = wid0; j < R; j += nw0) {
+      const double akj = src[k + j * R] * ip;
+      for (int i = lane0; i < R; i += 32) {
+        const double aik = src[i + k * R];
+        double v;
+        if (j != k)
+          v = (i != k) ? src[i + j * R] - aik * akj : akj;
+        else
+          v = (i != k) ? -aik * ip : ip;
+        dst[i + j * R] = v;
       }
-      __syncthreads();
-      if (!s_ok) break;
-      const double dj = s_piv;
-      for (int i = j + 1 + tid; i < R; i += nt) {
-        double s = V[i + j * R];
-        for (int k = 0; k < j; ++k) s -= Lm[i + k * R] * Lm[j + k * R];
-        Lm[i + j * R] = s / dj;
-      }
-      __syncthreads();
     }
-    if (!s_ok) break;
+    if (tid == 0 && !(p > 0.0)) s_ok = 0;
+    __syncthreads();
+    double* t = src;
+    src = dst;
+    dst = t;
   }
-  const bool chol = s_ok != 0;
-  double* Pm;
-  if (chol) {
-    // X = L^{-1} (column-parallel), then Lm = X^T X = V^{-1}
-    for (int j = tid; j < R; j += nt) {
-      for (int i = 0; i < j; ++i) X[i + j * R] = 0.0;
-      X[j + j * R] = 1.0 / Lm[j + j * R];
-      for (int i = j + 1; i < R; ++i) {
-        double s = 0.0;
-        for (int k = j; k < i; ++k) s += Lm[i + k * R] * X[k + j * R];
-        X[i + j * R] = -s / Lm[i + i * R];
-      }
-    }
+  if (src != A) {
+    for (int e = tid; e < R2; e += nt) A[e] = src[e];
     __syncthreads();
-    for (int e = tid; e < R * R; e += nt) {
-      const int a = e % R, b = e / R;
-      const int k0 = a > b ? a : b;
-      double s = 0.0;
-      for (int k = k0; k < R; ++k) s += X[k + a * R] * X[k + b * R];
-      Lm[e] = s;
-    }
-    Pm = Lm;
-  } else {
-    for (int e = tid; e < R * R; e += nt) Lm[e] = V[e];
+  }
+  ALS_STAMP(8);
+  double fro = 0.0, ifro = 0.0;
+  for (int e = tid; e < R2; e += nt) {
+    fro += V[e] * V[e];
+    ifro += A[e] * A[e];
+  }
+  fro = sqrt(block_reduce_sum(fro));
+  ifro = sqrt(block_reduce_sum(ifro));
+  const bool direct = s_ok && isfinite(ifro) && ifro > 0.0 && (1.0 / ifro) > double(R) * double(Traits<T>::eps) * fro;
+  double* Pm = A;
+  if (!direct) {
+    for (int e = tid; e < R2; e += nt) A[e] = V[e];
     __syncthreads();
-    jacobi_eig(Lm, X, R, ev, ord);
+    jacobi_eig(A, X, R, ev, ord);
     T lmax = T(0);
     for (int k = 0; k < R; ++k) lmax = T(ev[k]) > lmax ? T(ev[k]) : lmax;
     const T tau = T(R) * Traits<T>::eps * lmax;
-    for (int e = tid; e < R * R; e += nt) {
+    for (int e = tid; e < R2; e += nt) {
       const int a = e % R, b = e / R;
       double s = 0.0;
       for (int k = 0; k < R; ++k) {
@@ -376,52 +387,65 @@ __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T
     }
     Pm = V;
     if (tid == 0) st->pivots_fallback += 1;
+    __syncthreads();
   }
+  ALS_STAMP(9);
+  // 3. F = W pinv(V), rounded to Scalar like the reference's factor
+  for (int r = wid0; r < R; r += nw0)
+    for (int i = lane0; i < I; i += 32) {
+      double s = 0.0;
+      for (int k = 0; k < R; ++k) s += double(W[i + k * I]) * Pm[k + r * R];
+      Fs[i + r * I] = double(T(s));
+    }
   __syncthreads();
-  // 3. F = W pinv(V)
-  for (i64 e = tid; e < I * R; e += nt) {
-    const i64 i = e % I;
-    const int r = int(e / I);
-    double s = 0.0;
-    for (int k = 0; k < R; ++k) s += double(W[i + k * I]) * Pm[k + r * R];
-    F[i + r * I] = T(s);
-  }
-  __syncthreads();
-  // 4. column normalization; weights from the last mode (solve.hpp:215-229)
+  ALS_STAMP(10);
+  // 4. column norms; weights from the last mode (solve.hpp:215-229)
   const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
   for (int r = wid; r < R; r += nw) {
     double s = 0.0;
-    for (i64 i = lane; i < I; i += 32) s += double(F[i + r * I]) * double(F[i + r * I]);
+    for (int i = lane; i < I; i += 32) s += Fs[i + r * I] * Fs[i + r * I];
     s = warp_sum(s);
-    const T nrm = T(sqrt(s));
-    if (mode == N - 1 && lane == 0) weights[r] = nrm;
-    if (nrm > T(0))
-      for (i64 i = lane; i < I; i += 32) F[i + r * I] = F[i + r * I] / nrm;
+    if (lane == 0) {
+      const T nrm = T(sqrt(s));
+      nr[r] = double(nrm);
+      if (mode == N - 1) weights[r] = nrm;
+    }
   }
   __syncthreads();
+  for (int r = wid0; r < R; r += nw0) {
+    const T nrm = T(nr[r]);
+    for (int i = lane0; i < I; i += 32) {
+      const int e = i + r * I;
+      const T v = nrm > T(0) ? T(Fs[e]) / nrm : T(Fs[e]);
+      Fs[e] = double(v);
+      F[e] = v;
+    }
+  }
+  __syncthreads();
+  ALS_STAMP(11);
   // 5. Gram of the new factor
-  for (int e = tid; e < R * R; e += nt) {
+  for (int e = tid; e < R2; e += nt) {
     const int a = e % R, b = e / R;
     double s = 0.0;
-    for (i64 i = 0; i < I; ++i) s += double(F[i + a * I]) * double(F[i + b * I]);
+    for (int i = 0; i < I; ++i) s += Fs[i + a * I] * Fs[i + b * I];
     fs.gram[mode][e] = T(s);
+    V[e] = double(T(s));  // this mode's Gram, for the fit
   }
   __syncthreads();
+  ALS_STAMP(12);
   if (mode != N - 1) return;
   // 6. fit (solve.hpp:232-254), double accumulation
   double m2 = 0.0;
-  for (int e = tid; e < R * R; e += nt) {
+  for (int e = tid; e < R2; e += nt) {
     const int a = e % R, b = e / R;
-    double g = 1.0;
-    for (int k = 0; k < N; ++k) g *= double(fs.gram[k][e]);
-    m2 += double(weights[a]) * double(T(g)) * double(weights[b]);
+    double g = V[e];
+    for (int k = 0; k < N; ++k)
+      if (k != mode) g *= double(fs.gram[k][e]);
+    m2 += nr[a] * double(T(g)) * nr[b];
   }
   m2 = block_reduce_sum(m2);
   double xi = 0.0;
-  for (i64 e = tid; e < I * R; e += nt) {
-    const int r = int(e / I);
-    xi += double(W[e]) * double(F[e]) * double(weights[r]);
-  }
+  for (int e = tid; e < I * R; e += nt) xi += double(W[e]) * Fs[e] * nr[e / I];
   xi = block_reduce_sum(xi);
   if (tid == 0) {
     const double model2 = m2 > 0.0 ? m2 : 0.0;
@@ -446,6 +470,7 @@ __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T
     }
   }
   __syncthreads();
+  ALS_STAMP(13);
 }
 
 template <typename T>
@@ -454,7 +479,7 @@ __global__ void __launch_bounds__(kSmallThreads)
                       double* trace_fit, double* trace_sec, AlsState* st, double* work) {
   if (st->done) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  if (fs.rank <= kAlsSmemRank) work = reinterpret_cast<double*>(smem_raw);
+  work = reinterpret_cast<double*>(smem_raw);
   als_mode_update<T, T>(fs, mode, W, weights, tol, max_iter, trace_fit, trace_sec, st, work);
 }
 
@@ -481,10 +506,19 @@ struct AlsLoopArgs {
   double* part;  // [2][G][max I*R]
   i64 part_stride;
   GridBarrier* bar;
+  unsigned long long* prof;  // optional [8] ns per phase (CTA 0): A, bar1, B, bar2
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 template <typename T>
 __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p) {
+  __shared__ int pidx[kAlsBatch * kMaxOrder];
+  __shared__ int sfoff[kMaxOrder], sext[kMaxOrder];
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* sm = reinterpret_cast<double*>(smem_raw);
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -499,6 +533,8 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
       for (int k = m + 1; k < N; ++k) Rr *= p.sh.e[k];
       const i64 J = L * Rr;
       const int nout = int(I) * R;
+      unsigned long long tp0 = 0;
+      if (p.prof && g == 0 && tid == 0) tp0 = gtimer();
       // ---- A: partial MTTKRP over positions [j0, j1)
       double acc[kAlsAcc];
 #pragma unroll
@@ -507,6 +543,26 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
       const i64 j0 = g * chunk, j1 = j0 + chunk < J ? j0 + chunk : J;
       double* fib = sm;                       // [kAlsBatch][I]
       double* kc = sm + kAlsBatch * I;        // [kAlsBatch][R]
+      double* fsm = kc + kAlsBatch * R;       // staged factors of the other modes
+      {
+        __syncthreads();
+        if (tid == 0) {
+          int off = 0;
+          for (int k = 0; k < N; ++k) {
+            sfoff[k] = off;
+            sext[k] = int(p.sh.e[k]);
+            if (k != m) off += int(p.sh.e[k]) * R;
+          }
+        }
+        __syncthreads();
+        for (int k = 0; k < N; ++k) {
+          if (k == m) continue;
+          const int nk = sext[k] * R;
+          const T* src = p.fs.f[k];
+          for (int e = tid; e < nk; e += nt) fsm[sfoff[k] + e] = double(src[e]);
+        }
+        __syncthreads();
+      }
       for (i64 pb = j0; pb < j1; pb += kAlsBatch) {
         const int np = int(j1 - pb < kAlsBatch ? j1 - pb : kAlsBatch);
         for (int e = tid; e < kAlsBatch * int(I); e += nt) {
@@ -518,24 +574,26 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
           }
           fib[pp * I + i] = v;
         }
+        if (tid < kAlsBatch) {  // multi-index digits of each position, once
+          const i64 s = pb + tid;
+          i64 a = s / Rr, b = s - a * Rr;
+          for (int k = N - 1; k > m; --k) {
+            pidx[tid * kMaxOrder + k] = int(b % p.sh.e[k]);
+            b /= p.sh.e[k];
+          }
+          for (int k = m - 1; k >= 0; --k) {
+            pidx[tid * kMaxOrder + k] = int(a % p.sh.e[k]);
+            a /= p.sh.e[k];
+          }
+        }
+        __syncthreads();
         for (int e = tid; e < kAlsBatch * R; e += nt) {
           const int pp = e / R, r = e % R;
           double v = 0.0;
           if (pp < np) {
-            const i64 s = pb + pp;
-            i64 a = s / Rr, b = s - a * Rr;
-            i64 idx[kMaxOrder];
-            for (int k = N - 1; k > m; --k) {
-              idx[k] = b % p.sh.e[k];
-              b /= p.sh.e[k];
-            }
-            for (int k = m - 1; k >= 0; --k) {
-              idx[k] = a % p.sh.e[k];
-              a /= p.sh.e[k];
-            }
             T prod = T(1);
             for (int k = N - 1; k >= 0; --k)  // highest mode first (kruskal.hpp:58-62)
-              if (k != m) prod *= p.fs.f[k][idx[k] + i64(r) * p.sh.e[k]];
+              if (k != m) prod *= T(fsm[sfoff[k] + pidx[pp * kMaxOrder + k] + r * sext[k]]);
             v = double(prod);
           }
           kc[pp * R + r] = v;
@@ -559,7 +617,11 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
         const int o = tid + q * nt;
         if (o < nout) pt[o] = acc[q];
       }
+      unsigned long long tp1 = 0;
+      if (p.prof && g == 0 && tid == 0) tp1 = gtimer();
       grid_sync(p.bar);
+      unsigned long long tp2 = 0;
+      if (p.prof && g == 0 && tid == 0) tp2 = gtimer();
       // ---- B: reduce + mode update on CTA 0
       if (g == 0) {
         double* W = sm;                   // I x R
@@ -567,15 +629,40 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
         const double* pp0 = p.part + i64(parity) * G * p.part_stride;
         for (int o = tid; o < nout; o += nt) {
           double s = 0.0;
-          for (int q = 0; q < G; ++q) s += ldcg(&pp0[i64(q) * p.part_stride + o]);
+          int q = 0;
+          for (; q + 4 <= G; q += 4) {
+            const double v0 = ldcg(&pp0[i64(q) * p.part_stride + o]);
+            const double v1 = ldcg(&pp0[i64(q + 1) * p.part_stride + o]);
+            const double v2 = ldcg(&pp0[i64(q + 2) * p.part_stride + o]);
+            const double v3 = ldcg(&pp0[i64(q + 3) * p.part_stride + o]);
+            s += v0;
+            s += v1;
+            s += v2;
+            s += v3;
+          }
+          for (; q < G; ++q) s += ldcg(&pp0[i64(q) * p.part_stride + o]);
           W[o] = s;
         }
         __syncthreads();
+        if (p.prof && tid == 0) {
+          g_als_prof = p.prof;
+          p.prof[14] += gtimer() - tp2;
+        }
         FactorSet<T> fs = p.fs;
         als_mode_update<T, double>(fs, m, W, p.weights, p.tol, p.max_iter, p.trace_fit, p.trace_sec, p.st, work);
       }
+      unsigned long long tp3 = 0;
+      if (p.prof && g == 0 && tid == 0) tp3 = gtimer();
       parity ^= 1;
       grid_sync(p.bar);
+      if (p.prof && g == 0 && tid == 0) {
+        const unsigned long long tp4 = gtimer();
+        p.prof[0] += tp1 - tp0;
+        p.prof[1] += tp2 - tp1;
+        p.prof[2] += tp3 - tp2;
+        p.prof[3] += tp4 - tp3;
+        p.prof[4] += 1;
+      }
     }
     if (ldcg(&p.st->done)) break;
   }
@@ -754,54 +841,71 @@ __global__ void sum_pairs_kernel(const double* part, int nblocks, double* out) {
   }
 }
 
-constexpr int kResRows = 8;
+constexpr int kResRows = 16;
 
+// ||X - Xhat||^2 and ||X||^2 streamed over X (row-major prefix x last mode):
+// Xhat(p, l) = sum_r coef[p][r] A_last[l][r], coef = lambda_r prod_{m<N-1} A_m.
+// Each CTA takes kResRows prefix rows at a time; the 16 X loads per thread
+// are independent (memory-level parallelism), A_last is read once per r for
+// all 16 rows.
 template <typename T>
 __global__ void __launch_bounds__(256) residual_kernel(const T* X, ShapeArg sh, FactorSet<T> fs, const T* w,
                                                        double* part) {
-  __shared__ T coef[kResRows][kMaxRank];
+  __shared__ T coef[kMaxRank][kResRows];
+  __shared__ int dig[kResRows][kMaxOrder];
+  __shared__ const T* fptr[kMaxOrder];
+  __shared__ int ext[kMaxOrder];
   const int R = fs.rank, N = sh.n;
+  if (threadIdx.x < kMaxOrder) {
+    fptr[threadIdx.x] = threadIdx.x < N ? fs.f[threadIdx.x] : nullptr;
+    ext[threadIdx.x] = threadIdx.x < N ? int(sh.e[threadIdx.x]) : 1;
+  }
   const i64 last = sh.e[N - 1];
   i64 prefix = 1;
   for (int m = 0; m < N - 1; ++m) prefix *= sh.e[m];
   const T* Al = fs.f[N - 1];
   double acc_r = 0.0, acc_x = 0.0;
+  __syncthreads();
   for (i64 p0 = i64(blockIdx.x) * kResRows; p0 < prefix; p0 += i64(gridDim.x) * kResRows) {
     __syncthreads();
-    for (int e = threadIdx.x; e < kResRows * R; e += blockDim.x) {
-      const int q = e / R, r = e % R;
-      const i64 p = p0 + q;
-      T v = T(0);
-      if (p < prefix) {
-        v = w[r];
-        i64 rem = p;
-        for (int m = N - 2; m >= 0; --m) {
-          const i64 im = rem % sh.e[m];
-          rem /= sh.e[m];
-          v *= fs.f[m][im + i64(r) * sh.e[m]];
-        }
+    if (threadIdx.x < kResRows) {  // multi-index digits of this row, once
+      i64 rem = p0 + threadIdx.x;
+      for (int m = N - 2; m >= 0; --m) {
+        dig[threadIdx.x][m] = int(rem % ext[m]);
+        rem /= ext[m];
       }
-      coef[q][r] = v;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kResRows * R; e += blockDim.x) {
+      const int q = e % kResRows, r = e / kResRows;
+      T v = T(0);
+      if (p0 + q < prefix) {
+        v = w[r];
+        for (int m = N - 2; m >= 0; --m) v *= fptr[m][dig[q][m] + i64(r) * ext[m]];
+      }
+      coef[r][q] = v;
     }
     __syncthreads();
     const int nrows = int(prefix - p0 < kResRows ? prefix - p0 : kResRows);
     for (i64 il = threadIdx.x; il < last; il += blockDim.x) {
+      T xv[kResRows];
+#pragma unroll
+      for (int q = 0; q < kResRows; ++q) xv[q] = q < nrows ? X[(p0 + q) * last + il] : T(0);
       T xh[kResRows];
 #pragma unroll
       for (int q = 0; q < kResRows; ++q) xh[q] = T(0);
       for (int r = 0; r < R; ++r) {
         const T a = Al[il + i64(r) * last];
 #pragma unroll
-        for (int q = 0; q < kResRows; ++q) xh[q] = fma(coef[q][r], a, xh[q]);
+        for (int q = 0; q < kResRows; ++q) xh[q] = fma(coef[r][q], a, xh[q]);
       }
 #pragma unroll
-      for (int q = 0; q < kResRows; ++q)
-        if (q < nrows) {
-          const double x = double(X[(p0 + q) * last + il]);
-          const double d = x - double(xh[q]);
-          acc_r += d * d;
-          acc_x += x * x;
-        }
+      for (int q = 0; q < kResRows; ++q) {
+        const double x = double(xv[q]);
+        const double d = x - double(xh[q]);
+        acc_r += d * d;
+        acc_x += x * x;
+      }
     }
   }
   acc_r = block_reduce_sum(acc_r);
@@ -898,7 +1002,8 @@ template <typename T>
 void als_update(const FactorSet<T>& fs, int mode, const T* W, T* weights, double tol, int max_iter,
                 double* trace_fit, double* trace_sec, AlsState* state, double* work, cudaStream_t st) {
   const int R = fs.rank;
-  const size_t smem = R <= kAlsSmemRank ? (3 * size_t(R) * R + 4 * size_t(R)) * sizeof(double) : 0;
+  const size_t smem = (3 * size_t(R) * R + 5 * size_t(R) + size_t(fs.extent[mode]) * R) * sizeof(double);
+  check_arg(R <= kAlsSmemRank && smem <= 200 * 1024, "als: mode update exceeds the shared-memory plan");
   static const size_t lim = enable_max_dyn_smem(als_update_kernel<T>);
   (void)lim;
   als_update_kernel<T><<<1, kSmallThreads, smem, st>>>(fs, mode, W, weights, tol, max_iter, trace_fit, trace_sec,
@@ -912,9 +1017,12 @@ bool als_loop_supported(const i64* shape, int order, int rank) {
   if (rank > kAlsSmemRank) return false;
   for (int m = 0; m < order; ++m) {
     if (shape[m] * rank > i64(kAlsAcc) * kAlsThreads) return false;
-    const size_t smA = (size_t(kAlsBatch) * shape[m] + size_t(kAlsBatch) * rank) * sizeof(double);
-    const size_t smB = (size_t(shape[m]) * rank + 3 * size_t(rank) * rank + 4 * size_t(rank)) * sizeof(double);
-    if (std::max(smA, smB) > 160 * 1024) return false;
+    i64 fac = 0;
+    for (int k = 0; k < order; ++k)
+      if (k != m) fac += shape[k] * rank;
+    const size_t smA = (size_t(kAlsBatch) * shape[m] + size_t(kAlsBatch) * rank + size_t(fac)) * sizeof(double);
+    const size_t smB = (2 * size_t(shape[m]) * rank + 3 * size_t(rank) * rank + 5 * size_t(rank)) * sizeof(double);
+    if (std::max(smA, smB) > 180 * 1024) return false;
   }
   return true;
 }
@@ -922,7 +1030,7 @@ bool als_loop_supported(const i64* shape, int order, int rank) {
 template <typename T>
 void als_loop(const T* B, const i64* shape, int order, const FactorSet<T>& fs, T* weights, double tol, int max_iter,
               double* trace_fit, double* trace_sec, AlsState* state, double* part, i64 part_elems, GridBarrier* bar,
-              cudaStream_t st) {
+              cudaStream_t st, unsigned long long* prof) {
   const int R = fs.rank;
   size_t smem = 0;
   i64 maxJ = 1, S = 1, maxout = 1;
@@ -930,17 +1038,20 @@ void als_loop(const T* B, const i64* shape, int order, const FactorSet<T>& fs, T
   for (int m = 0; m < order; ++m) {
     maxJ = std::max(maxJ, S / shape[m]);
     maxout = std::max(maxout, shape[m] * R);
-    const size_t smA = (size_t(kAlsBatch) * shape[m] + size_t(kAlsBatch) * R) * sizeof(double);
-    const size_t smB = (size_t(shape[m]) * R + 3 * size_t(R) * R + 4 * size_t(R)) * sizeof(double);
+    i64 fac = 0;
+    for (int k = 0; k < order; ++k)
+      if (k != m) fac += shape[k] * R;
+    const size_t smA = (size_t(kAlsBatch) * shape[m] + size_t(kAlsBatch) * R + size_t(fac)) * sizeof(double);
+    const size_t smB = (2 * size_t(shape[m]) * R + 3 * size_t(R) * R + 5 * size_t(R)) * sizeof(double);
     smem = std::max(smem, std::max(smA, smB));
   }
   static const size_t lim = enable_max_dyn_smem(als_loop_kernel<T>);
   if (smem > lim) throw std::runtime_error("als_loop: shared memory plan too large");
   const int maxc = max_coop_blocks(als_loop_kernel<T>, kAlsThreads, smem);
-  int G = int(std::max<i64>(1, std::min<i64>(ceil_div(maxJ, 4 * kAlsBatch), maxc)));
+  int G = int(std::max<i64>(1, std::min<i64>(ceil_div(maxJ, kAlsBatch), maxc)));
   G = int(std::min<i64>(G, part_elems / (2 * maxout)));
   AlsLoopArgs<T> a{B, make_shape(shape, order), fs, weights, tol, max_iter, trace_fit, trace_sec, state, part,
-                   maxout, bar};
+                   maxout, bar, prof};
   launch_coop(als_loop_kernel<T>, G, kAlsThreads, smem, st, a);
 }
 
@@ -1031,7 +1142,7 @@ void synth_tensor(const i64* shape, int order, int rank, const double* w_dev, co
   template void normalize_model<T>(const FactorSet<T>&, T*, T*, cudaStream_t);                                \
   template bool als_loop_supported<T>(const i64*, int, int);                                                  \
   template void als_loop<T>(const T*, const i64*, int, const FactorSet<T>&, T*, double, int, double*, double*, \
-                            AlsState*, double*, i64, GridBarrier*, cudaStream_t);                                \
+                            AlsState*, double*, i64, GridBarrier*, cudaStream_t, unsigned long long*);                                \
   template void small_gemm<T>(const T*, i64, i64, const T*, int, T*, cudaStream_t);                           \
   template void norm_and_finite<T>(const T*, i64, double*, double*, int, cudaStream_t);                       \
   template void residual_norms<T>(const T*, const i64*, int, const FactorSet<T>&, const T*, double*, double*, \

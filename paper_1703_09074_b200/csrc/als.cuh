@@ -63,7 +63,7 @@ bool als_loop_supported(const i64* shape, int order, int rank);
 template <typename T>
 void als_loop(const T* B, const i64* shape, int order, const FactorSet<T>& fs, T* weights, double tol, int max_iter,
               double* trace_fit, double* trace_sec, AlsState* state, double* part, i64 part_elems, GridBarrier* bar,
-              cudaStream_t st);
+              cudaStream_t st, unsigned long long* prof = nullptr);
 
 // normalize (kruskal.hpp:117-176) in place; `tmp` >= sum extents * rank + rank elements.
 template <typename T>

@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <set>
@@ -69,7 +71,7 @@ struct rcpg_context {
   int err_it = -1;
   // workspace
   DevBuf panelA, panelB, work0, work1, Y, Qy, scratch, keys, cands, bar, info, part, tau, diag, cqr;
-  DevBuf als_f, als_g, als_w, als_kr, als_work, als_trace, als_state, weights, small_tmp, nrm, als_part;
+  DevBuf als_f, als_g, als_w, als_kr, als_work, als_trace, als_state, weights, small_tmp, nrm, als_part, als_prof;
   std::vector<PassRecord> passes;
   cudaEvent_t user_events[64] = {};
   size_t pass_used = 0;
@@ -308,10 +310,24 @@ void run_compress(rcpg_context* c, const rcpg_tensor* t, const CompressCfg& cfg,
       {
         ScopedPass sp(c, "stab_w", 2.0 * J * rq * b);
         FactorWork w = factor_work(c, J);
+        const bool lu_prof = getenv("RCPG_PROFILE_LU") != nullptr;
+        if (lu_prof) {
+          c->als_prof.ensure(16 * sizeof(unsigned long long));
+          RCPG_CUDA(cudaMemsetAsync(c->als_prof.p, 0, 16 * sizeof(unsigned long long), c->st));
+          w.prof = c->als_prof.as<unsigned long long>();
+        }
         if (cfg.stabilizer == RCPG_STAB_LU)
           rz = plu_basis<T>(P, Zp, J, v.R, rq, km, w, c->st);
         else
           rz = thin_qr<T>(P, Zp, J, v.R, rq, km, w, nullptr, c->st);
+        if (lu_prof) {
+          unsigned long long h[4];
+          RCPG_CUDA(cudaMemcpyAsync(h, w.prof, sizeof(h), cudaMemcpyDeviceToHost, c->st));
+          RCPG_CUDA(cudaStreamSynchronize(c->st));
+          if (h[3])
+            fprintf(stderr, "[rcpg lu] J=%lld n=%d steps=%llu  reduce+book %.2f  update %.2f  cand+barrier %.2f us/step\n",
+                    (long long)J, rq, h[3], h[0] / 1e3 / h[3], h[1] / 1e3 / h[3], h[2] / 1e3 / h[3]);
+        }
       }
       {
         ScopedPass sp(c, "power_xz", (S + J * rz + extent * rz) * b);
@@ -453,10 +469,26 @@ AlsResult run_als(rcpg_context* c, const T* B, const i64* shape, int order, cons
     const i64 part_elems = 2 * i64(2048) * maxout;
     c->als_part.ensure(size_t(part_elems) * sizeof(double));
     c->bar.ensure(sizeof(GridBarrier));
+    unsigned long long* prof = nullptr;
+    if (getenv("RCPG_PROFILE_ALS")) {
+      c->als_prof.ensure(16 * sizeof(unsigned long long));
+      RCPG_CUDA(cudaMemsetAsync(c->als_prof.p, 0, 16 * sizeof(unsigned long long), c->st));
+      prof = c->als_prof.as<unsigned long long>();
+    }
     als_loop<T>(B, shape, order, fs, weights, cfg.tol, cfg.max_iter, tfit, tsec, state, c->als_part.as<double>(),
-                part_elems, c->bar.as<GridBarrier>(), c->st);
+                part_elems, c->bar.as<GridBarrier>(), c->st, prof);
     RCPG_CUDA(cudaMemcpyAsync(&hs, state, sizeof(AlsState), cudaMemcpyDeviceToHost, c->st));
     RCPG_CUDA(cudaStreamSynchronize(c->st));
+    if (prof) {
+      unsigned long long h[16];
+      RCPG_CUDA(cudaMemcpy(h, prof, sizeof(h), cudaMemcpyDeviceToHost));
+      fprintf(stderr, "[rcpg als B] Wred %.2f  V+GJ %.2f  norms/pinv %.2f  F %.2f  normalize %.2f  gram %.2f  fit(total) %.2f us\n",
+              h[14] / 1e3 / h[4], h[8] / 1e3 / h[4], h[9] / 1e3 / h[4], h[10] / 1e3 / h[4], h[11] / 1e3 / h[4],
+              h[12] / 1e3 / h[4], h[13] / 1e3 / h[4]);
+      fprintf(stderr, "[rcpg als] modes=%llu  A %.2f us  bar1 %.2f us  B %.2f us  bar2 %.2f us (per mode step)\n",
+              h[4], h[0] / 1e3 / double(h[4]), h[1] / 1e3 / double(h[4]), h[2] / 1e3 / double(h[4]),
+              h[3] / 1e3 / double(h[4]));
+    }
     enqueued = cfg.max_iter;
   }
   {
@@ -669,7 +701,7 @@ void rcpg_destroy(rcpg_context* c) {
   }
   for (DevBuf* b : {&c->panelA, &c->panelB, &c->work0, &c->work1, &c->Y, &c->Qy, &c->scratch, &c->keys, &c->cands,
                     &c->bar, &c->info, &c->part, &c->tau, &c->diag, &c->cqr, &c->als_f, &c->als_g, &c->als_w, &c->als_kr,
-                    &c->als_work, &c->als_trace, &c->als_state, &c->weights, &c->small_tmp, &c->nrm, &c->als_part})
+                    &c->als_work, &c->als_trace, &c->als_state, &c->weights, &c->small_tmp, &c->nrm, &c->als_part, &c->als_prof})
     b->release();
   cudaStreamDestroy(c->st);
   delete c;

@@ -20,6 +20,8 @@
 //    to O(eps * cond(Y)). A device-side status flag hands ill-conditioned
 //    or rank-deficient inputs to householder_kernel, a faithful
 //    right-looking Householder QR (same cooperative structure as the LU).
+#include <algorithm>
+
 #include "factor.cuh"
 #include "runtime.cuh"
 
@@ -47,13 +49,32 @@ __global__ void init_row_keys_kernel(KoldaMap km, i64 J, i64 R, i64* keys) {
 
 // ------------------------------------------------------------ candidates
 template <typename T>
-struct Cand {
+struct __align__(16) Cand {
   T v;       // |value|; -1 = none
   int pcol;  // physical column (tie key 1)
   int c;     // storage column
   i64 prow;  // physical row (tie key 2)
   i64 s;     // storage row
 };
+
+template <typename T>
+__device__ __forceinline__ Cand<T> load_cand_cg(const Cand<T>* p) {
+  static_assert(sizeof(Cand<T>) == 32 || sizeof(Cand<T>) == 24, "candidate layout");
+  Cand<T> x;
+  if constexpr (sizeof(Cand<T>) == 32) {
+    const int4 a = __ldcg(reinterpret_cast<const int4*>(p));
+    const int4 b = __ldcg(reinterpret_cast<const int4*>(p) + 1);
+    *reinterpret_cast<int4*>(&x) = a;
+    *(reinterpret_cast<int4*>(&x) + 1) = b;
+  } else {
+    x.v = __ldcg(&p->v);
+    x.pcol = __ldcg(&p->pcol);
+    x.c = __ldcg(&p->c);
+    x.prow = __ldcg(&p->prow);
+    x.s = __ldcg(&p->s);
+  }
+  return x;
+}
 
 template <typename T>
 __device__ __forceinline__ bool better(const Cand<T>& a, const Cand<T>& b) {
@@ -102,34 +123,74 @@ __device__ Cand<T> block_best(Cand<T> x, Cand<T>* scratch) {
 // ------------------------------------------------ LU, shared-memory CTA
 // Eigen FullPivLU verbatim on an I x n column-major panel held in shared
 // memory (physical row/column swaps, first maximum in column-major order).
+// The pivot key is (|a|, column-major index) so one 64-bit value and one
+// 32-bit index move per shuffle.
+constexpr int kSmemLuThreads = 256;
+
 template <typename T>
-__global__ void __launch_bounds__(kSmallThreads) plu_smem_kernel(const T* __restrict__ A, T* __restrict__ Z, int I,
-                                                                 int n, int* info) {
+__device__ __forceinline__ void key_better(T& v, int& idx, T ov, int oidx) {
+  if (ov > v || (ov == v && oidx < idx)) {
+    v = ov;
+    idx = oidx;
+  }
+}
+
+template <typename T>
+__device__ void block_argmax(T& v, int& idx, T* sv, int* si) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) key_better(v, idx, __shfl_xor_sync(0xffffffffu, v, o), __shfl_xor_sync(0xffffffffu, idx, o));
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (lane == 0) {
+    sv[wid] = v;
+    si[wid] = idx;
+  }
+  __syncthreads();
+  v = lane < nw ? sv[lane] : T(-1);
+  idx = lane < nw ? si[lane] : 0x7fffffff;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) key_better(v, idx, __shfl_xor_sync(0xffffffffu, v, o), __shfl_xor_sync(0xffffffffu, idx, o));
+  __syncthreads();
+}
+
+// Rows are held in physical (Kolda) order: physical row p is storage row
+// kolda_inverse(p) of the (L, n, R) panel, so the same kernel serves the
+// I x l samples (identity map) and small W panels of any mode.
+template <typename T>
+__global__ void __launch_bounds__(kSmemLuThreads) plu_smem_kernel(const T* __restrict__ A, T* __restrict__ Z, int I,
+                                                                  int n, i64 R, KoldaMap km, int* info) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* a = reinterpret_cast<T*>(smem_raw);
-  int* perm = reinterpret_cast<int*>(a + i64(I) * n);  // physical -> original row
-  __shared__ Cand<T> red[33];
+  int* perm = reinterpret_cast<int*>(a + i64(I) * n);  // physical -> original physical row
+  __shared__ T sv[32];
+  __shared__ int si[32];
   const int tid = threadIdx.x, nt = blockDim.x;
   const int r = I < n ? I : n;
-  for (int e = tid; e < I * n; e += nt) a[e] = A[e];
-  for (int i = tid; i < I; i += nt) perm[i] = i;
+  const bool ident = (R == i64(I)) && km.n_low == 0 && km.n_high == 1;
+  for (int p = tid; p < I; p += nt) {
+    perm[p] = p;
+    if (ident) continue;
+    const i64 srow = kolda_inverse(km, p, R);
+    const i64 aa = srow / R, bb = srow - aa * R;
+    const i64 base = aa * n * R + bb;
+    for (int j = 0; j < n; ++j) a[p + j * I] = A[base + j * R];
+  }
+  if (ident)
+    for (int e = tid; e < I * n; e += nt) a[e] = A[e];
   __syncthreads();
   const int tx = tid & 31, ty = tid >> 5, ny = nt >> 5;
+  // step-0 pivot search (afterwards it is fused into the update)
+  T bv = T(-1);
+  int bi = 0x7fffffff;
+  for (int j = ty; j < n; j += ny)
+    for (int i = tx; i < I; i += 32) key_better(bv, bi, T(fabs(a[i + j * I])), j * I + i);
   int k0 = r;
   for (int k = 0; k < r; ++k) {
-    // pivot search over the corner, column-major first maximum (explicit keys)
-    Cand<T> best{T(-1), 0x7fffffff, 0, 0x7fffffffffffffffll, 0};
-    for (int j = k + ty; j < n; j += ny)
-      for (int i = k + tx; i < I; i += 32) {
-        const Cand<T> x{T(fabs(a[i + j * I])), j, j, i, i};
-        if (better(x, best)) best = x;
-      }
-    best = block_best(best, red);
-    if (!(best.v > T(0))) {
+    block_argmax(bv, bi, sv, si);
+    if (!(bv > T(0))) {
       k0 = k;
       break;
     }
-    const int br = int(best.prow), bc = best.pcol;
+    const int br = bi % I, bc = bi / I;
     if (br != k) {  // row swap, then column swap (FullPivLU order)
       for (int j = tid; j < n; j += nt) {
         const T t = a[k + j * I];
@@ -154,19 +215,34 @@ __global__ void __launch_bounds__(kSmallThreads) plu_smem_kernel(const T* __rest
     const T piv = a[k + k * I];
     for (int i = k + 1 + tid; i < I; i += nt) a[i + k * I] = a[i + k * I] / piv;
     __syncthreads();
+    bv = T(-1);
+    bi = 0x7fffffff;
     if (k < r - 1) {
       for (int j = k + 1 + ty; j < n; j += ny) {
         const T u = a[k + j * I];
-        for (int i = k + 1 + tx; i < I; i += 32) a[i + j * I] -= a[i + k * I] * u;
+        for (int i = k + 1 + tx; i < I; i += 32) {
+          const T x = a[i + j * I] - a[i + k * I] * u;
+          a[i + j * I] = x;
+          key_better(bv, bi, T(fabs(x)), j * I + i);
+        }
       }
       __syncthreads();
     }
   }
   // P^{-1} L: physical row p of L goes to original row perm[p]
-  for (int e = tid; e < I * r; e += nt) {
-    const int p = e % I, j = e / I;
-    const T v = (p == j) ? T(1) : (p > j ? a[p + j * I] : T(0));
-    Z[perm[p] + i64(j) * I] = v;
+  if (ident) {
+    for (int e = tid; e < I * r; e += nt) {
+      const int p = e % I, j = e / I;
+      const T v = (p == j) ? T(1) : (p > j ? a[p + j * I] : T(0));
+      Z[perm[p] + i64(j) * I] = v;
+    }
+  } else {
+    for (int p = tid; p < I; p += nt) {
+      const i64 srow = kolda_inverse(km, perm[p], R);
+      const i64 aa = srow / R, bb = srow - aa * R;
+      const i64 base = aa * r * R + bb;
+      for (int j = 0; j < r; ++j) Z[base + j * R] = (p == j) ? T(1) : (p > j ? a[p + j * I] : T(0));
+    }
   }
   if (tid == 0) *info = k0;
 }
@@ -183,10 +259,19 @@ struct LuArgs {
   Cand<T>* cands;  // [2][gridDim]
   GridBarrier* bar;
   int* info;   // [1] nonzero pivots
+  unsigned long long* prof;  // optional [8]: ns in reduce / bookkeeping / update / barrier (CTA 0)
 };
 
+__device__ __forceinline__ unsigned long long lu_timer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+constexpr int kLuThreads = 256;
+
 template <typename T>
-__global__ void __launch_bounds__(kFacThreads) plu_coop_kernel(LuArgs<T> p) {
+__global__ void __launch_bounds__(kLuThreads) plu_coop_kernel(LuArgs<T> p) {
   __shared__ Cand<T> red[33];
   __shared__ int pcol_of[kMaxPanelCols], col_at[kMaxPanelCols];
   __shared__ T U[kMaxPanelCols];
@@ -222,16 +307,13 @@ __global__ void __launch_bounds__(kFacThreads) plu_coop_kernel(LuArgs<T> p) {
   grid_sync(p.bar);
 
   int k0 = p.r;
+  const bool prof = p.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+  unsigned long long t_a = prof ? lu_timer() : 0;
   for (int k = 0; k < p.r; ++k) {
     const Cand<T>* cb = p.cands + (k & 1) * G;
     Cand<T> g = none;
     for (int q = threadIdx.x; q < G; q += blockDim.x) {
-      Cand<T> x;
-      x.v = ldcg(&cb[q].v);
-      x.pcol = ldcg(&cb[q].pcol);
-      x.c = ldcg(&cb[q].c);
-      x.prow = ldcg(&cb[q].prow);
-      x.s = ldcg(&cb[q].s);
+      const Cand<T> x = load_cand_cg(cb + q);
       if (better(x, g)) g = x;
     }
     g = block_best(g, red);
@@ -273,6 +355,11 @@ __global__ void __launch_bounds__(kFacThreads) plu_coop_kernel(LuArgs<T> p) {
       if (u != ss && u >= r0 && u < r1) p.phys[u] = pr;
     }
     __syncthreads();
+    unsigned long long t_b = 0;
+    if (prof) {
+      t_b = lu_timer();
+      p.prof[0] += t_b - t_a;
+    }
 
     best = none;
     Cand<T>* out = p.cands + ((k + 1) & 1) * G;
@@ -294,15 +381,22 @@ __global__ void __launch_bounds__(kFacThreads) plu_coop_kernel(LuArgs<T> p) {
         for (int j = k + 1; j < p.r; ++j) p.Z[bz + j * R] = T(0);
         continue;
       }
-      const T m = p.A[ba + cs * R] / piv;
+      constexpr int B = 8;  // loads in flight per thread
+      T v[B];
+      // the pivot-column value and the first chunk are independent loads
+      const T pcv = p.A[ba + cs * R];
+#pragma unroll
+      for (int u = 0; u < B; ++u)
+        if (more && k + 1 + u < p.n) v[u] = p.A[ba + col_at[k + 1 + u] * R];
+      const T m = pcv / piv;
       p.Z[bz + k * R] = m;
       if (more) {
-        constexpr int B = 8;  // loads in flight per thread
         for (int q0 = k + 1; q0 < p.n; q0 += B) {
-          T v[B];
+          if (q0 > k + 1) {
 #pragma unroll
-          for (int u = 0; u < B; ++u)
-            if (q0 + u < p.n) v[u] = p.A[ba + col_at[q0 + u] * R];
+            for (int u = 0; u < B; ++u)
+              if (q0 + u < p.n) v[u] = p.A[ba + col_at[q0 + u] * R];
+          }
 #pragma unroll
           for (int u = 0; u < B; ++u)
             if (q0 + u < p.n) {
@@ -315,10 +409,20 @@ __global__ void __launch_bounds__(kFacThreads) plu_coop_kernel(LuArgs<T> p) {
         }
       }
     }
+    unsigned long long t_c = 0;
+    if (prof) {
+      t_c = lu_timer();
+      p.prof[1] += t_c - t_b;
+    }
     if (more) {
       best = block_best(best, red);
       if (threadIdx.x == 0) out[blockIdx.x] = best;
       grid_sync(p.bar);
+    }
+    if (prof) {
+      t_a = lu_timer();
+      p.prof[2] += t_a - t_c;
+      p.prof[3] += 1;
     }
   }
 
@@ -504,8 +608,10 @@ __global__ void __launch_bounds__(kFacThreads) householder_kernel(QrArgs<T> p) {
 // -------------------------------------------------------- CholeskyQR2
 // One CTA; Y is I x n column-major (I >= n). work >= I*n doubles.
 // status: 0 = Q written, 1 = fall back to Householder.
+constexpr int kCqrThreads = 512;
+
 template <typename T>
-__global__ void __launch_bounds__(kSmallThreads) cqr2_kernel(const T* __restrict__ Y, T* __restrict__ Q, int I, int n,
+__global__ void __launch_bounds__(kCqrThreads) cqr2_kernel(const T* __restrict__ Y, T* __restrict__ Q, int I, int n,
                                                              double* __restrict__ work, int* status,
                                                              int* rank_warning) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -650,19 +756,19 @@ int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w
   check_arg(n <= kMaxPanelCols, "plu_basis: panel wider than supported");
   const int r = int(std::min<i64>(J, n));
   const size_t smem = smem_lu_bytes(J, n, sizeof(T));
-  const bool kolda_identity = (km.n_low == 0 && km.n_high == 1);
   static const size_t lu_lim = enable_max_dyn_smem(plu_smem_kernel<T>);
-  if (R == J && kolda_identity && smem <= lu_lim) {
-    plu_smem_kernel<T><<<1, kSmallThreads, smem, st>>>(A, Z, int(J), n, w.info);
+  if (smem <= lu_lim) {
+    plu_smem_kernel<T><<<1, kSmemLuThreads, smem, st>>>(A, Z, int(J), n, R, km, w.info);
     count_launch();
     RCPG_LAUNCHED();
     return r;
   }
   init_row_keys(km, J, R, w.keys, st);
-  const int maxc = max_coop_blocks(plu_coop_kernel<T>, kFacThreads, 0);
-  const int G = std::min(pick_grid(J, n, maxc), w.max_blocks);
-  LuArgs<T> a{A, Z, J, R, n, r, w.keys, km, reinterpret_cast<Cand<T>*>(w.cands), w.bar, w.info};
-  launch_coop(plu_coop_kernel<T>, G, kFacThreads, 0, st, a);
+  const int maxc = max_coop_blocks(plu_coop_kernel<T>, kLuThreads, 0);
+  // about one panel row per thread; the per-step work is latency bound
+  const int G = int(std::max<i64>(1, std::min<i64>({ceil_div(J, kLuThreads), i64(maxc), i64(w.max_blocks)})));
+  LuArgs<T> a{A, Z, J, R, n, r, w.keys, km, reinterpret_cast<Cand<T>*>(w.cands), w.bar, w.info, w.prof};
+  launch_coop(plu_coop_kernel<T>, G, kLuThreads, 0, st, a);
   return r;
 }
 
@@ -676,7 +782,7 @@ int thin_qr(T* A, T* Q, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w, 
   const size_t cq_smem = (2 * size_t(n) * n + 3 * size_t(n)) * sizeof(double);
   static const size_t cq_lim = enable_max_dyn_smem(cqr2_kernel<T>);
   if (R == J && kolda_identity && J >= n && J <= w.cqr_rows && cq_smem <= cq_lim) {
-    cqr2_kernel<T><<<1, kSmallThreads, cq_smem, st>>>(A, Q, int(J), n, w.cqr_work, w.info + 2, rank_warning_dev);
+    cqr2_kernel<T><<<1, kCqrThreads, cq_smem, st>>>(A, Q, int(J), n, w.cqr_work, w.info + 2, rank_warning_dev);
     count_launch();
     RCPG_LAUNCHED();
     skip = w.info + 2;  // the Householder kernel below runs only if CholeskyQR2 declined

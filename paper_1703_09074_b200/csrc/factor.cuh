@@ -20,6 +20,7 @@ struct FactorWork {
   double* cqr_work = nullptr; // [cqr_rows * kMaxPanelCols] CholeskyQR2 scratch
   i64 cqr_rows = 0;           // largest I for the single-CTA CholeskyQR2 path
   int max_blocks = 0;
+  unsigned long long* prof = nullptr;  // optional phase timers (RCPG_PROFILE_LU)
 };
 
 size_t factor_cand_bytes();
