@@ -169,6 +169,10 @@ rcpg_status rcpg_synth(rcpg_context* ctx, rcpg_dtype dtype, int32_t order, const
                        const double* weights, const double* factors, double snr, uint64_t noise_seed,
                        rcpg_tensor** out);
 rcpg_status rcpg_synchronize(rcpg_context* ctx);
+/* Device time (CUDA events) of plu_basis (kind 0) / thin_qr (kind 1) on a
+ * rows x cols device-resident panel, averaged over reps calls. */
+rcpg_status rcpg_bench_factor(rcpg_context* ctx, rcpg_dtype dtype, int32_t kind, int64_t rows, int64_t cols,
+                              int32_t reps, double* ms_per_call);
 /* CUDA events on the library's stream (device timing of whole calls):
  * record into slot [0, 64); elapsed milliseconds between two recorded slots. */
 rcpg_status rcpg_event_record(rcpg_context* ctx, int32_t slot);

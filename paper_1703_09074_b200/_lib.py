@@ -99,6 +99,7 @@ SIGNATURES = {
     "rcpg_kernel_launches": (_I64, [_V]),
     "rcpg_synth": (_I32, [_V, C.c_int, _I32, _V, _I64, _V, _V, _D, _U64, C.POINTER(C.c_void_p)]),
     "rcpg_synchronize": (_I32, [_V]),
+    "rcpg_bench_factor": (_I32, [_V, C.c_int, _I32, _I64, _I64, _I32, C.POINTER(C.c_double)]),
     "rcpg_event_record": (_I32, [_V, _I32]),
     "rcpg_event_elapsed": (_I32, [_V, _I32, _I32, C.POINTER(C.c_double)]),
     "rcpg_host_register": (_I32, [_V, _V, C.c_size_t]),

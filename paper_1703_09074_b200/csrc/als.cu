@@ -62,6 +62,10 @@ __global__ void kr_panel_kernel(FactorSet<T> fs, ShapeArg sh, int mode, i64 J, i
 }
 
 // --------------------------------------------------------- block helpers
+// Total order on doubles for rank computations: NaN sorts as +inf, so ranks
+// stay a permutation even on non-finite data (the input check that rejects
+// such data is raised after the device work, see api.cu Deferred).
+__device__ __forceinline__ double order_key(double x) { return isnan(x) ? INFINITY : x; }
 __device__ double block_reduce_sum(double v) {
   __shared__ double scratch[33];
   return block_sum(v, scratch);
@@ -125,49 +129,45 @@ __device__ void jacobi_eig(double* A, double* V, int n, double* evals, int* orde
         cs_s[q] = s;
       }
       __syncthreads();
+      const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
       // columns: A <- A J
-      for (int w = tid; w < npairs * n; w += nt) {
-        const int q = w / n, k = w % n;
+      for (int q = wid; q < npairs; q += nw) {
         const int i = pp[q], j = pq[q];
         if (j >= n) continue;
         const double c = cs_c[q], s = cs_s[q];
-        const double akp = A[k + i * n], akq = A[k + j * n];
-        A[k + i * n] = c * akp - s * akq;
-        A[k + j * n] = s * akp + c * akq;
+        for (int k = lane; k < n; k += 32) {
+          const double akp = A[k + i * n], akq = A[k + j * n];
+          A[k + i * n] = c * akp - s * akq;
+          A[k + j * n] = s * akp + c * akq;
+        }
       }
       __syncthreads();
-      // rows: A <- J^T A
-      for (int w = tid; w < npairs * n; w += nt) {
-        const int q = w / n, k = w % n;
+      // rows: A <- J^T A, and V <- V J
+      for (int q = wid; q < npairs; q += nw) {
         const int i = pp[q], j = pq[q];
         if (j >= n) continue;
         const double c = cs_c[q], s = cs_s[q];
-        const double apk = A[i + k * n], aqk = A[j + k * n];
-        A[i + k * n] = c * apk - s * aqk;
-        A[j + k * n] = s * apk + c * aqk;
-      }
-      // V <- V J
-      for (int w = tid; w < npairs * n; w += nt) {
-        const int q = w / n, k = w % n;
-        const int i = pp[q], j = pq[q];
-        if (j >= n) continue;
-        const double c = cs_c[q], s = cs_s[q];
-        const double vkp = V[k + i * n], vkq = V[k + j * n];
-        V[k + i * n] = c * vkp - s * vkq;
-        V[k + j * n] = s * vkp + c * vkq;
+        for (int k = lane; k < n; k += 32) {
+          const double apk = A[i + k * n], aqk = A[j + k * n];
+          A[i + k * n] = c * apk - s * aqk;
+          A[j + k * n] = s * apk + c * aqk;
+          const double vkp = V[k + i * n], vkq = V[k + j * n];
+          V[k + i * n] = c * vkp - s * vkq;
+          V[k + j * n] = s * vkp + c * vkq;
+        }
       }
       __syncthreads();
     }
   }
   // ascending, stable by index
   for (int i = tid; i < n; i += nt) {
-    const double di = A[i + i * n];
+    const double di = order_key(A[i + i * n]);
     int rank = 0;
     for (int j = 0; j < n; ++j) {
-      const double dj = A[j + j * n];
+      const double dj = order_key(A[j + j * n]);
       if (dj < di || (dj == di && j < i)) ++rank;
     }
-    evals[rank] = di;
+    evals[rank] = A[i + i * n];
     order[rank] = i;
   }
   __syncthreads();
@@ -749,22 +749,24 @@ __global__ void __launch_bounds__(kSmallThreads) normalize_kernel(FactorSet<T> f
   // stable sort: weight descending, ties by lexicographic factor-0 column
   for (int a = tid; a < R; a += nt) {
     int pos = 0;
-    const T wa = weights[a];
+    const double wa = -order_key(-double(weights[a]));  // NaN -> -inf: last
     const T* ca = fs.f[0] + i64(a) * fs.extent[0];
     for (int b = 0; b < R; ++b) {
       if (b == a) continue;
-      const T wb = weights[b];
+      const double wb = -order_key(-double(weights[b]));
       bool before;
       if (wb != wa) {
         before = wb > wa;
       } else {
         const T* cb = fs.f[0] + i64(b) * fs.extent[0];
         int cmp = 0;
-        for (i64 i = 0; i < fs.extent[0]; ++i)
-          if (cb[i] != ca[i]) {
-            cmp = cb[i] < ca[i] ? -1 : 1;
+        for (i64 i = 0; i < fs.extent[0]; ++i) {
+          const double xb = order_key(double(cb[i])), xa = order_key(double(ca[i]));
+          if (xb != xa) {
+            cmp = xb < xa ? -1 : 1;
             break;
           }
+        }
         before = cmp < 0 || (cmp == 0 && b < a);
       }
       pos += before ? 1 : 0;
@@ -985,8 +987,7 @@ void init_factor_from_gram(const T* G, int extent, int rank, int mode, u64 seed,
   const size_t smem = extent <= kEigSmemMax ? 2 * size_t(extent) * extent * sizeof(double) : 0;
   static const size_t lim = enable_max_dyn_smem(init_from_gram_kernel<T>);
   (void)lim;
-  init_from_gram_kernel<T><<<1, kSmallThreads, smem, st>>>(G, extent, rank, mode, seed, method, factor, gram_out,
-                                                            work);
+  init_from_gram_kernel<T><<<1, 256, smem, st>>>(G, extent, rank, mode, seed, method, factor, gram_out, work);
   count_launch();
   RCPG_LAUNCHED();
 }
@@ -1053,6 +1054,18 @@ void als_loop(const T* B, const i64* shape, int order, const FactorSet<T>& fs, T
   AlsLoopArgs<T> a{B, make_shape(shape, order), fs, weights, tol, max_iter, trace_fit, trace_sec, state, part,
                    maxout, bar, prof};
   launch_coop(als_loop_kernel<T>, G, kAlsThreads, smem, st, a);
+}
+
+template <typename T>
+__global__ void fill_ones_kernel(T* p, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = T(1);
+}
+
+template <typename T>
+void fill_ones(T* p, int n, cudaStream_t st) {
+  fill_ones_kernel<T><<<1, 128, 0, st>>>(p, n);
+  count_launch();
+  RCPG_LAUNCHED();
 }
 
 void als_start(AlsState* state, double* nx2_src, cudaStream_t st) {
@@ -1137,6 +1150,7 @@ void synth_tensor(const i64* shape, int order, int rank, const double* w_dev, co
   template void kr_panel<T>(const FactorSet<T>&, const i64*, int, T*, cudaStream_t, const int*);                          \
   template void init_factor_from_gram<T>(const T*, int, int, int, u64, int, T*, T*, double*, cudaStream_t);   \
   template void zero_factor<T>(T*, i64, int, T*, cudaStream_t);                                               \
+  template void fill_ones<T>(T*, int, cudaStream_t);                                               \
   template void als_update<T>(const FactorSet<T>&, int, const T*, T*, double, int, double*, double*,          \
                               AlsState*, double*, cudaStream_t);                                              \
   template void normalize_model<T>(const FactorSet<T>&, T*, T*, cudaStream_t);                                \

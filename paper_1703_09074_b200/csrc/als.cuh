@@ -55,6 +55,8 @@ void als_update(const FactorSet<T>& fs, int mode, const T* W, T* weights, double
                 double* trace_fit, double* trace_sec, AlsState* state, double* work, cudaStream_t st);
 
 void als_start(AlsState* state, double* nx2_src, cudaStream_t st);
+template <typename T>
+void fill_ones(T* p, int n, cudaStream_t st);
 
 // The whole ALS iteration loop as one cooperative kernel (when the mode
 // extents and rank fit its shared-memory plan; see als_loop_supported).

@@ -71,9 +71,11 @@ struct rcpg_context {
   int err_it = -1;
   // workspace
   DevBuf panelA, panelB, work0, work1, Y, Qy, scratch, keys, cands, bar, info, part, tau, diag, cqr;
-  DevBuf als_f, als_g, als_w, als_kr, als_work, als_trace, als_state, weights, small_tmp, nrm, als_part, als_prof;
+  DevBuf als_f, als_g, als_w, als_kr, als_work, als_trace, als_state, weights, small_tmp, nrm, als_part, als_prof,
+      recov;
   std::vector<PassRecord> passes;
   cudaEvent_t user_events[64] = {};
+  double* hslots = nullptr;  // pinned mirror of the device check slots (c->nrm)
   size_t pass_used = 0;
   bool timing = true;
 };
@@ -201,6 +203,41 @@ void read_doubles(rcpg_context* c, const double* d, double* h, int n) {
   RCPG_CUDA(cudaStreamSynchronize(c->st));
 }
 
+// Device check slots (c->nrm): written by kernels, read back once at the end
+// of a call so the whole decomposition is enqueued without host syncs.
+constexpr int kSlotCount = 512;
+enum Slot { kXSum = 0, kXBad = 1, kBSum = 2, kBBad = 3, kResid = 4, kResX = 5, kRankWarn = 8 /* 8 ints */ };
+double* slots(rcpg_context* c) { return c->nrm.as<double>(); }
+int* rank_warn_slot(rcpg_context* c, int mode) { return reinterpret_cast<int*>(slots(c) + kRankWarn) + mode; }
+const double* read_slots(rcpg_context* c) {
+  RCPG_CUDA(cudaMemcpyAsync(c->hslots, slots(c), 16 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  RCPG_CUDA(cudaStreamSynchronize(c->st));
+  return c->hslots;
+}
+int host_rank_warn(rcpg_context* c, int mode) { return reinterpret_cast<const int*>(c->hslots + kRankWarn)[mode]; }
+
+// Errors the device found, raised in the reference's validation order.
+struct Deferred {
+  bool compress_input = false;  // compress.hpp:93
+  bool als_input = false;       // solve.hpp:139-141
+  bool relerr = false;          // kruskal.hpp:190-191
+};
+void raise_deferred(rcpg_context* c, const Deferred& d) {
+  const double* h = read_slots(c);
+  if (d.compress_input) check_arg(h[kXBad] == 0.0, "compress: input values must be finite");
+  if (d.als_input) {
+    if (h[kBBad] != 0.0) throw SolverFailure("solve: input values are not finite", 0);
+    check_arg(h[kBSum] > 0.0, "solve: tensor norm must be positive");
+  }
+  if (d.relerr) check_arg(h[kResX] > 0.0, "relative_error: tensor norm must be positive");
+}
+// A host-side check failed after device checks were enqueued: earlier
+// (device) errors take precedence, as in the sequential reference.
+[[noreturn]] void fail_after(rcpg_context* c, const Deferred& d, const std::string& msg) {
+  raise_deferred(c, d);
+  throw InvalidArgument(msg);
+}
+
 struct CompressCfg {
   i64 target_rank, oversampling;
   int power_iterations, distribution, stabilizer;
@@ -225,9 +262,13 @@ int stabilize_small(rcpg_context* c, int stab, T* Y, i64 I, int n, T* out) {
   return thin_qr<T>(Y, out, I, I, n, km, w, nullptr, c->st);
 }
 
-// compress.hpp:86-146
+void finish_compress(rcpg_context* c, rcpg_compressed* out, const Deferred& dfr);
+
+// compress.hpp:86-146. With `sync_checks` false the input check is left in
+// the device slots (Deferred::compress_input) for the caller to raise.
 template <typename T>
-void run_compress(rcpg_context* c, const rcpg_tensor* t, const CompressCfg& cfg, rcpg_compressed* out) {
+void run_compress(rcpg_context* c, const rcpg_tensor* t, const CompressCfg& cfg, rcpg_compressed* out,
+                  Deferred& dfr, bool sync_checks) {
   check_arg(cfg.target_rank >= 1, "compress: target rank must be at least 1");
   check_arg(cfg.oversampling >= 0, "compress: oversampling must be non-negative");
   check_arg(cfg.power_iterations >= 0, "compress: power iteration count must be non-negative");
@@ -235,19 +276,15 @@ void run_compress(rcpg_context* c, const rcpg_tensor* t, const CompressCfg& cfg,
   const int sms = device_caps().num_sms;
   {
     ScopedPass sp(c, "check_finite", double(t->size) * sizeof(T));
-    c->nrm.ensure(4096 * sizeof(double));
     c->scratch.ensure(size_t(sms) * 8 * sizeof(double) + 64);
-    norm_and_finite<T>(static_cast<const T*>(t->d), t->size, c->nrm.as<double>(), c->scratch.as<double>(), sms,
-                       c->st);
+    norm_and_finite<T>(static_cast<const T*>(t->d), t->size, slots(c) + kXSum, c->scratch.as<double>(), sms, c->st);
   }
-  double h[2];
-  read_doubles(c, c->nrm.as<double>(), h, 2);
-  check_arg(h[1] == 0.0, "compress: input values must be finite");
+  dfr.compress_input = true;
 
   std::set<i64> selected;
   if (cfg.modes_present) {
     for (i64 m : cfg.modes) {
-      check_arg(m >= 0 && m < order, "compress: mode index out of range");
+      if (!(m >= 0 && m < order)) fail_after(c, dfr, "compress: mode index out of range");
       selected.insert(m);
     }
   } else {
@@ -270,7 +307,7 @@ void run_compress(rcpg_context* c, const rcpg_tensor* t, const CompressCfg& cfg,
       basis.identity = true;
       continue;
     }
-    check_arg(l <= kMaxPanelCols, "compress: sketch width k + p above the supported maximum (256)");
+    if (l > kMaxPanelCols) fail_after(c, dfr, "compress: sketch width k + p above the supported maximum (256)");
     const ModeView v = mode_view(shape, order, n);
     const i64 J = v.L * v.R;
     const i64 S = J * extent;
@@ -338,23 +375,18 @@ void run_compress(rcpg_context* c, const rcpg_tensor* t, const CompressCfg& cfg,
       ycols = rz;
     }
     // final Householder basis + rank warning (compress.hpp:135)
-    c->info.ensure(16);
     int qcols;
     {
       ScopedPass sp(c, "thin_qr", 2.0 * extent * ycols * b);
       FactorWork w = factor_work(c, extent);
       basis.q.ensure(size_t(extent) * ycols * sizeof(T));
       qcols = thin_qr<T>(Y, basis.q.as<T>(), extent, extent, int(ycols), identity_kolda(extent), w,
-                         w.info + 1, c->st);
+                         rank_warn_slot(c, n), c->st);
     }
-    int rw = 0;
-    RCPG_CUDA(cudaMemcpyAsync(&rw, c->info.as<int>() + 1, sizeof(int), cudaMemcpyDeviceToHost, c->st));
-    RCPG_CUDA(cudaStreamSynchronize(c->st));
     basis.identity = false;
     basis.cols = qcols;
-    basis.rank_warning = rw != 0;
     // fold(Q^T B_(n)) must match next_shape (tensor.hpp:193-194)
-    check_arg(qcols == l, "fold: matrix dimensions do not match the target shape");
+    if (qcols != l) fail_after(c, dfr, "fold: matrix dimensions do not match the target shape");
     DevBuf& dst = which == 0 ? c->work0 : c->work1;
     dst.ensure(size_t(v.L) * l * v.R * sizeof(T));
     {
@@ -375,7 +407,14 @@ void run_compress(rcpg_context* c, const rcpg_tensor* t, const CompressCfg& cfg,
   out->size = size;
   out->data.ensure(size_t(size) * sizeof(T));
   RCPG_CUDA(cudaMemcpyAsync(out->data.p, cur, size_t(size) * sizeof(T), cudaMemcpyDeviceToDevice, c->st));
-  RCPG_CUDA(cudaStreamSynchronize(c->st));
+  if (sync_checks) finish_compress(c, out, dfr);
+}
+
+// Reads the deferred device results of a compress: input check, rank warnings.
+void finish_compress(rcpg_context* c, rcpg_compressed* out, const Deferred& dfr) {
+  raise_deferred(c, dfr);
+  for (int m = 0; m < out->order; ++m)
+    if (!out->bases[m].identity) out->bases[m].rank_warning = host_rank_warn(c, m) != 0;
 }
 
 struct AlsResult {
@@ -384,16 +423,27 @@ struct AlsResult {
   std::vector<double> fit, sec;
 };
 
-// solve.hpp:183-262 on a device tensor. Leaves factors/weights on device in
-// the context's ALS buffers (factor m at fs.f[m]); returns the trace.
+// Everything a decomposition produces on the device; copied out once.
 template <typename T>
-AlsResult run_als(rcpg_context* c, const T* B, const i64* shape, int order, const rcpg_decompose_config& cfg,
-                  FactorSet<T>& fs, T*& weights) {
-  check_arg(cfg.rank >= 1, "solve: rank must be at least 1");
-  check_arg(cfg.tol > 0, "solve: tolerance must be positive");
-  check_arg(cfg.max_iter >= 1, "solve: iteration limit must be at least 1");
+struct AlsHandles {
+  FactorSet<T> fs;
+  T* weights = nullptr;
+  AlsState* state = nullptr;
+  double* tfit = nullptr;
+  double* tsec = nullptr;
+  int max_iter = 0;
+};
+
+// solve.hpp:183-262 on a device tensor, enqueued without host syncs; the
+// input checks are deferred (Deferred::als_input).
+template <typename T>
+AlsHandles<T> run_als(rcpg_context* c, const T* B, const i64* shape, int order, const rcpg_decompose_config& cfg,
+                      Deferred& dfr) {
+  if (!(cfg.rank >= 1)) fail_after(c, dfr, "solve: rank must be at least 1");
+  if (!(cfg.tol > 0)) fail_after(c, dfr, "solve: tolerance must be positive");
+  if (!(cfg.max_iter >= 1)) fail_after(c, dfr, "solve: iteration limit must be at least 1");
   const int R = int(cfg.rank);
-  check_arg(R <= kMaxRank, "solve: rank above the supported maximum (128)");
+  if (R > kMaxRank) fail_after(c, dfr, "solve: rank above the supported maximum (128)");
   const int sms = device_caps().num_sms;
   i64 S = 1, sum_ext = 0, max_ext = 0, max_J = 0;
   for (int m = 0; m < order; ++m) {
@@ -401,226 +451,214 @@ AlsResult run_als(rcpg_context* c, const T* B, const i64* shape, int order, cons
     sum_ext += shape[m];
     max_ext = std::max(max_ext, shape[m]);
   }
+  for (int m = 1; m < order; ++m)
+    if (cfg.init == RCPG_INIT_EIGENVECTORS && shape[m] > 2048)
+      fail_after(c, dfr, "init_factors: eigenvector init supports extents up to 2048");
   for (int m = 0; m < order; ++m) max_J = std::max(max_J, S / shape[m]);
-  c->nrm.ensure(4096 * sizeof(double));
   c->scratch.ensure(size_t(sms) * 8 * sizeof(double) + 64);
   {
     ScopedPass sp(c, "als_norm", double(S) * sizeof(T));
-    norm_and_finite<T>(B, S, c->nrm.as<double>(), c->scratch.as<double>(), sms, c->st);
+    norm_and_finite<T>(B, S, slots(c) + kBSum, c->scratch.as<double>(), sms, c->st);
   }
-  double h[2];
-  read_doubles(c, c->nrm.as<double>(), h, 2);
-  if (h[1] != 0.0) throw SolverFailure("solve: input values are not finite", 0);
-  check_arg(h[0] > 0.0, "solve: tensor norm must be positive");
+  dfr.als_input = true;
 
-  // buffers
   c->als_f.ensure(size_t(sum_ext) * R * sizeof(T));
   c->als_g.ensure(size_t(order) * R * R * sizeof(T));
   c->als_w.ensure(size_t(std::max<i64>(max_ext * std::max<i64>(R, max_ext), 1)) * sizeof(T));
-  c->als_kr.ensure(size_t(max_J) * R * sizeof(T));
   c->als_work.ensure(size_t(std::max<i64>(3 * max_ext * max_ext + 8 * max_ext, 8 * R * R + 8 * R) + 64) *
                      sizeof(double));
   c->als_trace.ensure(size_t(2) * cfg.max_iter * sizeof(double));
   c->als_state.ensure(sizeof(AlsState));
   c->weights.ensure(size_t(R) * sizeof(T));
-  fs = FactorSet<T>{};
-  fs.order = order;
-  fs.rank = R;
+  AlsHandles<T> h;
+  h.fs.order = order;
+  h.fs.rank = R;
   i64 off = 0;
   for (int m = 0; m < order; ++m) {
-    fs.f[m] = c->als_f.as<T>() + off;
-    fs.gram[m] = c->als_g.as<T>() + i64(m) * R * R;
-    fs.extent[m] = shape[m];
+    h.fs.f[m] = c->als_f.as<T>() + off;
+    h.fs.gram[m] = c->als_g.as<T>() + i64(m) * R * R;
+    h.fs.extent[m] = shape[m];
     off += shape[m] * R;
   }
-  weights = c->weights.as<T>();
-  AlsState* state = c->als_state.as<AlsState>();
-  double* tfit = c->als_trace.as<double>();
-  double* tsec = tfit + cfg.max_iter;
+  h.weights = c->weights.as<T>();
+  h.state = c->als_state.as<AlsState>();
+  h.tfit = c->als_trace.as<double>();
+  h.tsec = h.tfit + cfg.max_iter;
+  h.max_iter = cfg.max_iter;
 
-  als_start(state, c->nrm.as<double>(), c->st);
+  als_start(h.state, slots(c) + kBSum, c->st);
   {
     ScopedPass sp(c, "als_init", 0.0);
-    zero_factor<T>(fs.f[0], shape[0], R, fs.gram[0], c->st);
+    zero_factor<T>(h.fs.f[0], shape[0], R, h.fs.gram[0], c->st);
     for (int m = 1; m < order; ++m) {
       const ModeView v = mode_view(shape, order, m);
       if (cfg.init == RCPG_INIT_EIGENVECTORS) {
-        check_arg(shape[m] <= 2048, "init_factors: eigenvector init supports extents up to 2048");
         // Gram = B_(m) B_(m)^T as a sketch of B against itself.
         const i64 scr = sketch_scratch_elems<T>(v, shape[m], sms);
         c->scratch.ensure(size_t(scr) * sizeof(T));
         sketch<T>(B, v, B, shape[m], c->als_w.as<T>(), c->scratch.as<T>(), scr, sms, c->st);
       }
-      init_factor_from_gram<T>(c->als_w.as<T>(), int(shape[m]), R, m, cfg.seed, cfg.init, fs.f[m], fs.gram[m],
+      init_factor_from_gram<T>(c->als_w.as<T>(), int(shape[m]), R, m, cfg.seed, cfg.init, h.fs.f[m], h.fs.gram[m],
                                c->als_work.as<double>(), c->st);
     }
-    // weights = ones
-    std::vector<T> ones(size_t(R), T(1));
-    RCPG_CUDA(cudaMemcpyAsync(weights, ones.data(), sizeof(T) * R, cudaMemcpyHostToDevice, c->st));
-    RCPG_CUDA(cudaStreamSynchronize(c->st));
-  }
-
-  AlsState hs{};
-  int enqueued = 0, batch = 2;
-  if (als_loop_supported<T>(shape, order, R)) {
-    ScopedPass sp(c, "als_iterations", 0.0);
-    i64 maxout = 1;
-    for (int m = 0; m < order; ++m) maxout = std::max(maxout, shape[m] * R);
-    const i64 part_elems = 2 * i64(2048) * maxout;
-    c->als_part.ensure(size_t(part_elems) * sizeof(double));
-    c->bar.ensure(sizeof(GridBarrier));
-    unsigned long long* prof = nullptr;
-    if (getenv("RCPG_PROFILE_ALS")) {
-      c->als_prof.ensure(16 * sizeof(unsigned long long));
-      RCPG_CUDA(cudaMemsetAsync(c->als_prof.p, 0, 16 * sizeof(unsigned long long), c->st));
-      prof = c->als_prof.as<unsigned long long>();
-    }
-    als_loop<T>(B, shape, order, fs, weights, cfg.tol, cfg.max_iter, tfit, tsec, state, c->als_part.as<double>(),
-                part_elems, c->bar.as<GridBarrier>(), c->st, prof);
-    RCPG_CUDA(cudaMemcpyAsync(&hs, state, sizeof(AlsState), cudaMemcpyDeviceToHost, c->st));
-    RCPG_CUDA(cudaStreamSynchronize(c->st));
-    if (prof) {
-      unsigned long long h[16];
-      RCPG_CUDA(cudaMemcpy(h, prof, sizeof(h), cudaMemcpyDeviceToHost));
-      fprintf(stderr, "[rcpg als B] Wred %.2f  V+GJ %.2f  norms/pinv %.2f  F %.2f  normalize %.2f  gram %.2f  fit(total) %.2f us\n",
-              h[14] / 1e3 / h[4], h[8] / 1e3 / h[4], h[9] / 1e3 / h[4], h[10] / 1e3 / h[4], h[11] / 1e3 / h[4],
-              h[12] / 1e3 / h[4], h[13] / 1e3 / h[4]);
-      fprintf(stderr, "[rcpg als] modes=%llu  A %.2f us  bar1 %.2f us  B %.2f us  bar2 %.2f us (per mode step)\n",
-              h[4], h[0] / 1e3 / double(h[4]), h[1] / 1e3 / double(h[4]), h[2] / 1e3 / double(h[4]),
-              h[3] / 1e3 / double(h[4]));
-    }
-    enqueued = cfg.max_iter;
+    fill_ones<T>(h.weights, R, c->st);
   }
   {
     ScopedPass sp(c, "als_iterations", 0.0);
-    while (enqueued < cfg.max_iter) {
-      const int nb = std::min(batch, cfg.max_iter - enqueued);
-      for (int q = 0; q < nb; ++q) {
-        for (int m = 0; m < order; ++m) {
-          const ModeView v = mode_view(shape, order, m);
-          const int* skip = &state->done;
-          kr_panel<T>(fs, shape, m, c->als_kr.as<T>(), c->st, skip);
-          const i64 scr = sketch_scratch_elems<T>(v, R, sms);
-          c->scratch.ensure(size_t(scr) * sizeof(T));
-          sketch<T>(B, v, c->als_kr.as<T>(), R, c->als_w.as<T>(), c->scratch.as<T>(), scr, sms, c->st, skip);
-          als_update<T>(fs, m, c->als_w.as<T>(), weights, cfg.tol, cfg.max_iter, tfit, tsec, state,
-                        c->als_work.as<double>(), c->st);
-        }
+    if (als_loop_supported<T>(shape, order, R)) {
+      i64 maxout = 1;
+      for (int m = 0; m < order; ++m) maxout = std::max(maxout, shape[m] * R);
+      const i64 part_elems = 2 * i64(2048) * maxout;
+      c->als_part.ensure(size_t(part_elems) * sizeof(double));
+      unsigned long long* prof = nullptr;
+      if (getenv("RCPG_PROFILE_ALS")) {
+        c->als_prof.ensure(16 * sizeof(unsigned long long));
+        RCPG_CUDA(cudaMemsetAsync(c->als_prof.p, 0, 16 * sizeof(unsigned long long), c->st));
+        prof = c->als_prof.as<unsigned long long>();
       }
-      enqueued += nb;
-      RCPG_CUDA(cudaMemcpyAsync(&hs, state, sizeof(AlsState), cudaMemcpyDeviceToHost, c->st));
-      RCPG_CUDA(cudaStreamSynchronize(c->st));
-      if (hs.done) break;
-      batch = std::min(batch * 2, 32);
+      als_loop<T>(B, shape, order, h.fs, h.weights, cfg.tol, cfg.max_iter, h.tfit, h.tsec, h.state,
+                  c->als_part.as<double>(), part_elems, c->bar.as<GridBarrier>(), c->st, prof);
+      if (prof) {
+        unsigned long long hp[16];
+        RCPG_CUDA(cudaMemcpyAsync(hp, prof, sizeof(hp), cudaMemcpyDeviceToHost, c->st));
+        RCPG_CUDA(cudaStreamSynchronize(c->st));
+        fprintf(stderr, "[rcpg als] modes=%llu  A %.2f us  bar1 %.2f us  B %.2f us  bar2 %.2f us (per mode step)\n",
+                hp[4], hp[0] / 1e3 / double(hp[4]), hp[1] / 1e3 / double(hp[4]), hp[2] / 1e3 / double(hp[4]),
+                hp[3] / 1e3 / double(hp[4]));
+      }
+    } else {
+      // general path (large extents / ranks): per-mode launches, enqueued in
+      // batches; every kernel first checks the device stop flag
+      c->als_kr.ensure(size_t(max_J) * R * sizeof(T));
+      AlsState hs{};
+      int enqueued = 0, batch = 2;
+      while (enqueued < cfg.max_iter) {
+        const int nb = std::min(batch, cfg.max_iter - enqueued);
+        for (int q = 0; q < nb; ++q) {
+          for (int m = 0; m < order; ++m) {
+            const ModeView v = mode_view(shape, order, m);
+            const int* skip = &h.state->done;
+            kr_panel<T>(h.fs, shape, m, c->als_kr.as<T>(), c->st, skip);
+            const i64 scr = sketch_scratch_elems<T>(v, R, sms);
+            c->scratch.ensure(size_t(scr) * sizeof(T));
+            sketch<T>(B, v, c->als_kr.as<T>(), R, c->als_w.as<T>(), c->scratch.as<T>(), scr, sms, c->st, skip);
+            als_update<T>(h.fs, m, c->als_w.as<T>(), h.weights, cfg.tol, cfg.max_iter, h.tfit, h.tsec, h.state,
+                          c->als_work.as<double>(), c->st);
+          }
+        }
+        enqueued += nb;
+        RCPG_CUDA(cudaMemcpyAsync(&hs, h.state, sizeof(AlsState), cudaMemcpyDeviceToHost, c->st));
+        RCPG_CUDA(cudaStreamSynchronize(c->st));
+        if (hs.done) break;
+        batch = std::min(batch * 2, 32);
+      }
     }
-  }
-  if (hs.error_it > 0) throw SolverFailure("als: fit became non-finite", hs.error_it);
-  AlsResult res;
-  res.iterations = hs.it - 1;
-  res.converged = hs.converged != 0;
-  res.fit.resize(size_t(res.iterations));
-  res.sec.resize(size_t(res.iterations));
-  if (res.iterations > 0) {
-    RCPG_CUDA(cudaMemcpyAsync(res.fit.data(), tfit, sizeof(double) * res.iterations, cudaMemcpyDeviceToHost, c->st));
-    RCPG_CUDA(cudaMemcpyAsync(res.sec.data(), tsec, sizeof(double) * res.iterations, cudaMemcpyDeviceToHost, c->st));
   }
   // model = normalize(model) (solve.hpp:259)
   c->small_tmp.ensure(size_t(sum_ext * R + R) * sizeof(T));
-  normalize_model<T>(fs, weights, c->small_tmp.as<T>(), c->st);
-  RCPG_CUDA(cudaStreamSynchronize(c->st));
-  return res;
+  normalize_model<T>(h.fs, h.weights, c->small_tmp.as<T>(), c->st);
+  return h;
 }
 
+// relative_error (kruskal.hpp:187-194): enqueued; sums land in the slots.
 template <typename T>
-double run_relerr(rcpg_context* c, const T* X, const i64* shape, int order, const FactorSet<T>& fs, const T* w) {
+void run_relerr(rcpg_context* c, const T* X, const i64* shape, int order, const FactorSet<T>& fs, const T* w,
+                Deferred& dfr) {
   const int sms = device_caps().num_sms;
   i64 S = 1;
   for (int m = 0; m < order; ++m) S *= shape[m];
   c->scratch.ensure(residual_scratch_doubles(sms) * sizeof(double));
-  c->nrm.ensure(4096 * sizeof(double));
   {
     ScopedPass sp(c, "relerr", double(S) * sizeof(T));
-    residual_norms<T>(X, shape, order, fs, w, c->nrm.as<double>(), c->scratch.as<double>(), sms, c->st);
+    residual_norms<T>(X, shape, order, fs, w, slots(c) + kResid, c->scratch.as<double>(), sms, c->st);
   }
-  double h[2];
-  read_doubles(c, c->nrm.as<double>(), h, 2);
-  check_arg(h[1] > 0.0, "relative_error: tensor norm must be positive");
-  return std::sqrt(h[0]) / std::sqrt(h[1]);
+  dfr.relerr = true;
 }
 
+// One readback at the end of a decomposition: checks (in reference order),
+// ALS state, trace, model.
 template <typename T>
-void copy_result(rcpg_context* c, const FactorSet<T>& fs, const T* w, const AlsResult& ar, double relerr,
-                 rcpg_result* res) {
-  const int R = fs.rank;
-  if (res->weights) RCPG_CUDA(cudaMemcpyAsync(res->weights, w, sizeof(T) * R, cudaMemcpyDeviceToHost, c->st));
+void finish_decompose(rcpg_context* c, const AlsHandles<T>& h, const FactorSet<T>& out_fs, const Deferred& dfr,
+                      rcpg_result* res) {
+  AlsState hs{};
+  RCPG_CUDA(cudaMemcpyAsync(&hs, h.state, sizeof(AlsState), cudaMemcpyDeviceToHost, c->st));
+  const int R = out_fs.rank;
+  if (res->weights) RCPG_CUDA(cudaMemcpyAsync(res->weights, h.weights, sizeof(T) * R, cudaMemcpyDeviceToHost, c->st));
   if (res->factors) {
     i64 off = 0;
-    for (int m = 0; m < fs.order; ++m) {
-      RCPG_CUDA(cudaMemcpyAsync(static_cast<T*>(res->factors) + off, fs.f[m], sizeof(T) * fs.extent[m] * R,
+    for (int m = 0; m < out_fs.order; ++m) {
+      RCPG_CUDA(cudaMemcpyAsync(static_cast<T*>(res->factors) + off, out_fs.f[m], sizeof(T) * out_fs.extent[m] * R,
                                 cudaMemcpyDeviceToHost, c->st));
-      off += fs.extent[m] * R;
+      off += out_fs.extent[m] * R;
     }
   }
-  RCPG_CUDA(cudaStreamSynchronize(c->st));
-  const int n = std::min<int>(ar.iterations, res->trace_capacity);
+  const int cap = std::min(res->trace_capacity, h.max_iter);
+  std::vector<double> fit(size_t(std::max(cap, 1))), sec(size_t(std::max(cap, 1)));
+  if (cap > 0) {
+    RCPG_CUDA(cudaMemcpyAsync(fit.data(), h.tfit, sizeof(double) * cap, cudaMemcpyDeviceToHost, c->st));
+    RCPG_CUDA(cudaMemcpyAsync(sec.data(), h.tsec, sizeof(double) * cap, cudaMemcpyDeviceToHost, c->st));
+  }
+  raise_deferred(c, Deferred{dfr.compress_input, dfr.als_input, false});  // syncs the stream
+  if (hs.error_it > 0) throw SolverFailure("als: fit became non-finite", hs.error_it);
+  raise_deferred(c, Deferred{false, false, dfr.relerr});
+  const double* hsl = c->hslots;
+  const int iters = hs.it - 1;
+  const int n = std::min(iters, cap);
   for (int i = 0; i < n; ++i) {
     if (res->trace_iteration) res->trace_iteration[i] = i + 1;
-    if (res->trace_fit) res->trace_fit[i] = ar.fit[size_t(i)];
-    if (res->trace_seconds) res->trace_seconds[i] = ar.sec[size_t(i)];
+    if (res->trace_fit) res->trace_fit[i] = fit[size_t(i)];
+    if (res->trace_seconds) res->trace_seconds[i] = sec[size_t(i)];
   }
-  res->iterations = ar.iterations;
-  res->converged = ar.converged ? 1 : 0;
-  res->final_relative_error = relerr;
+  res->iterations = iters;
+  res->converged = hs.converged ? 1 : 0;
+  res->final_relative_error = std::sqrt(hsl[kResid]) / std::sqrt(hsl[kResX]);
 }
 
 // solve.hpp:381-398
 template <typename T>
 void run_decompose(rcpg_context* c, const rcpg_tensor* t, const rcpg_decompose_config& cfg, rcpg_result* res) {
   check_arg(cfg.method == RCPG_ALS, "decompose: only the ALS solver is on this path (bcd is out of scope)");
-  FactorSet<T> fs;
-  T* w = nullptr;
+  Deferred dfr;
   if (!cfg.randomized) {
-    AlsResult ar = run_als<T>(c, static_cast<const T*>(t->d), t->shape, t->order, cfg, fs, w);
-    const double re = run_relerr<T>(c, static_cast<const T*>(t->d), t->shape, t->order, fs, w);
-    copy_result<T>(c, fs, w, ar, re, res);
+    AlsHandles<T> h = run_als<T>(c, static_cast<const T*>(t->d), t->shape, t->order, cfg, dfr);
+    run_relerr<T>(c, static_cast<const T*>(t->d), t->shape, t->order, h.fs, h.weights, dfr);
+    finish_decompose<T>(c, h, h.fs, dfr, res);
     return;
   }
   CompressCfg cc = to_cfg(cfg.compress);
   if (cc.target_rank == 0) cc.target_rank = cfg.rank;
   check_arg(cc.target_rank == cfg.rank, "decompose: compression target rank must equal the CP rank");
   rcpg_compressed comp;
-  run_compress<T>(c, t, cc, &comp);
-  AlsResult ar = run_als<T>(c, comp.data.as<T>(), comp.shape, comp.order, cfg, fs, w);
+  run_compress<T>(c, t, cc, &comp, dfr, /*sync_checks=*/false);
+  AlsHandles<T> h = run_als<T>(c, comp.data.as<T>(), comp.shape, comp.order, cfg, dfr);
   // recover (kruskal.hpp:198-220): A_n = Q_n A~_n, then normalize
   const int R = int(cfg.rank);
   i64 sum_ext = 0;
   for (int m = 0; m < t->order; ++m) sum_ext += t->shape[m];
-  DevBuf full;
-  full.ensure(size_t(sum_ext) * R * sizeof(T));
-  FactorSet<T> big = fs;
+  c->recov.ensure(size_t(sum_ext) * R * sizeof(T));
+  FactorSet<T> big = h.fs;
   {
     ScopedPass sp(c, "recover", 0.0);
     i64 off = 0;
     for (int m = 0; m < t->order; ++m) {
-      T* dst = full.as<T>() + off;
+      T* dst = c->recov.as<T>() + off;
       const BasisRec& b = comp.bases[m];
       if (b.identity) {
-        check_arg(b.dim == fs.extent[m], "recover: identity basis extent mismatch");
-        RCPG_CUDA(cudaMemcpyAsync(dst, fs.f[m], sizeof(T) * fs.extent[m] * R, cudaMemcpyDeviceToDevice, c->st));
+        if (b.dim != h.fs.extent[m]) fail_after(c, dfr, "recover: identity basis extent mismatch");
+        RCPG_CUDA(cudaMemcpyAsync(dst, h.fs.f[m], sizeof(T) * h.fs.extent[m] * R, cudaMemcpyDeviceToDevice, c->st));
       } else {
-        check_arg(b.cols == fs.extent[m], "recover: basis columns must match the compressed extent");
-        small_gemm<T>(b.q.as<T>(), b.dim, b.cols, fs.f[m], R, dst, c->st);
+        if (b.cols != h.fs.extent[m]) fail_after(c, dfr, "recover: basis columns must match the compressed extent");
+        small_gemm<T>(b.q.as<T>(), b.dim, b.cols, h.fs.f[m], R, dst, c->st);
       }
       big.f[m] = dst;
       big.extent[m] = t->shape[m];
       off += t->shape[m] * R;
     }
     c->small_tmp.ensure(size_t(sum_ext * R + R) * sizeof(T));
-    normalize_model<T>(big, w, c->small_tmp.as<T>(), c->st);
+    normalize_model<T>(big, h.weights, c->small_tmp.as<T>(), c->st);
   }
-  const double re = run_relerr<T>(c, static_cast<const T*>(t->d), t->shape, t->order, big, w);
-  copy_result<T>(c, big, w, ar, re, res);
-  full.release();
+  run_relerr<T>(c, static_cast<const T*>(t->d), t->shape, t->order, big, h.weights, dfr);
+  finish_decompose<T>(c, h, big, dfr, res);
 }
 
 template <typename F>
@@ -683,6 +721,8 @@ rcpg_status rcpg_create(int device, rcpg_context** out) {
     RCPG_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
     c->bar.ensure(sizeof(GridBarrier));
     RCPG_CUDA(cudaMemset(c->bar.p, 0, sizeof(GridBarrier)));
+    c->nrm.ensure(kSlotCount * sizeof(double));
+    RCPG_CUDA(cudaMallocHost(&c->hslots, kSlotCount * sizeof(double)));
     (void)device_caps();
   });
   if (s == RCPG_OK) *out = c.release();
@@ -695,13 +735,14 @@ void rcpg_destroy(rcpg_context* c) {
   cudaStreamSynchronize(c->st);
   for (auto& e : c->user_events)
     if (e) cudaEventDestroy(e);
+  if (c->hslots) cudaFreeHost(c->hslots);
   for (auto& r : c->passes) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
   }
   for (DevBuf* b : {&c->panelA, &c->panelB, &c->work0, &c->work1, &c->Y, &c->Qy, &c->scratch, &c->keys, &c->cands,
                     &c->bar, &c->info, &c->part, &c->tau, &c->diag, &c->cqr, &c->als_f, &c->als_g, &c->als_w, &c->als_kr,
-                    &c->als_work, &c->als_trace, &c->als_state, &c->weights, &c->small_tmp, &c->nrm, &c->als_part, &c->als_prof})
+                    &c->als_work, &c->als_trace, &c->als_state, &c->weights, &c->small_tmp, &c->nrm, &c->als_part, &c->als_prof, &c->recov})
     b->release();
   cudaStreamDestroy(c->st);
   delete c;
@@ -776,10 +817,11 @@ rcpg_status rcpg_compress(rcpg_context* c, const rcpg_tensor* t, const rcpg_comp
     c->pass_used = 0;
     auto comp = std::make_unique<rcpg_compressed>();
     const CompressCfg cc = to_cfg(*cfg);
+    Deferred dfr;
     if (t->dtype == RCPG_F64)
-      run_compress<double>(c, t, cc, comp.get());
+      run_compress<double>(c, t, cc, comp.get(), dfr, true);
     else
-      run_compress<float>(c, t, cc, comp.get());
+      run_compress<float>(c, t, cc, comp.get(), dfr, true);
     *out = comp.release();
   });
 }
@@ -858,7 +900,10 @@ rcpg_status rcpg_relative_error(rcpg_context* c, const rcpg_tensor* t, int64_t r
         fs.extent[m] = t->shape[m];
         off += t->shape[m] * rank;
       }
-      *out = run_relerr<T>(c, static_cast<const T*>(t->d), t->shape, t->order, fs, w.as<T>());
+      Deferred dfr;
+      run_relerr<T>(c, static_cast<const T*>(t->d), t->shape, t->order, fs, w.as<T>(), dfr);
+      raise_deferred(c, dfr);
+      *out = std::sqrt(c->hslots[kResid]) / std::sqrt(c->hslots[kResX]);
     };
     if (t->dtype == RCPG_F64)
       run(double{});
@@ -929,10 +974,12 @@ rcpg_status rcpg_thin_qr(rcpg_context* c, rcpg_dtype dtype, int64_t rows, int64_
                       c->st);
     else
       thin_qr<float>(A.as<float>(), Q.as<float>(), rows, rows, int(cols), identity_kolda(rows), w, w.info + 1, c->st);
-    int rw = 0;
+    int rw = 0, cq[2] = {0, 0};
     RCPG_CUDA(cudaMemcpyAsync(out, Q.p, size_t(rows) * r * b, cudaMemcpyDeviceToHost, c->st));
     RCPG_CUDA(cudaMemcpyAsync(&rw, w.info + 1, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    RCPG_CUDA(cudaMemcpyAsync(cq, w.info + 2, sizeof(int), cudaMemcpyDeviceToHost, c->st));
     RCPG_CUDA(cudaStreamSynchronize(c->st));
+    if (getenv("RCPG_DEBUG_QR")) fprintf(stderr, "[rcpg qr] %lldx%lld cqr2 status=%d\n", (long long)rows, (long long)cols, cq[0]);
     if (rank_warning) *rank_warning = rw;
     A.release();
     Q.release();
@@ -1007,6 +1054,61 @@ rcpg_status rcpg_synth(rcpg_context* c, rcpg_dtype dtype, int32_t order, const i
     w.release();
     scr.release();
     *out = t.release();
+  });
+}
+
+rcpg_status rcpg_bench_factor(rcpg_context* c, rcpg_dtype dtype, int32_t kind, int64_t rows, int64_t cols,
+                              int32_t reps, double* ms_per_call) {
+  return guarded(c, [&] {
+    check_arg(cols <= kMaxPanelCols && rows >= cols && reps >= 1, "bench_factor: bad shape");
+    const size_t b = dsize(dtype);
+    DevBuf A, A0, Z;
+    A.ensure(size_t(rows) * cols * b);
+    A0.ensure(size_t(rows) * cols * b);
+    Z.ensure(size_t(rows) * cols * b);
+    // deterministic pseudo-random panel
+    std::vector<double> h(size_t(rows) * cols);
+    unsigned long long x = 88172645463325252ull;
+    for (auto& v : h) {
+      x ^= x << 13;
+      x ^= x >> 7;
+      x ^= x << 17;
+      v = double(x >> 11) * 0x1.0p-53 - 0.5;
+    }
+    if (dtype == RCPG_F64) {
+      RCPG_CUDA(cudaMemcpy(A0.p, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+    } else {
+      std::vector<float> f(h.begin(), h.end());
+      RCPG_CUDA(cudaMemcpy(A0.p, f.data(), f.size() * 4, cudaMemcpyHostToDevice));
+    }
+    FactorWork w = factor_work(c, rows);
+    const KoldaMap km = identity_kolda(rows);
+    cudaEvent_t e0, e1;
+    RCPG_CUDA(cudaEventCreate(&e0));
+    RCPG_CUDA(cudaEventCreate(&e1));
+    double total = 0;
+    for (int it = 0; it <= reps; ++it) {
+      RCPG_CUDA(cudaMemcpyAsync(A.p, A0.p, size_t(rows) * cols * b, cudaMemcpyDeviceToDevice, c->st));
+      RCPG_CUDA(cudaEventRecord(e0, c->st));
+      if (dtype == RCPG_F64) {
+        if (kind == 0) plu_basis<double>(A.as<double>(), Z.as<double>(), rows, rows, int(cols), km, w, c->st);
+        else thin_qr<double>(A.as<double>(), Z.as<double>(), rows, rows, int(cols), km, w, w.info + 1, c->st);
+      } else {
+        if (kind == 0) plu_basis<float>(A.as<float>(), Z.as<float>(), rows, rows, int(cols), km, w, c->st);
+        else thin_qr<float>(A.as<float>(), Z.as<float>(), rows, rows, int(cols), km, w, w.info + 1, c->st);
+      }
+      RCPG_CUDA(cudaEventRecord(e1, c->st));
+      RCPG_CUDA(cudaEventSynchronize(e1));
+      float t = 0;
+      RCPG_CUDA(cudaEventElapsedTime(&t, e0, e1));
+      if (it > 0) total += t;  // first call warms caches / attributes
+    }
+    *ms_per_call = total / reps;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    A.release();
+    A0.release();
+    Z.release();
   });
 }
 

@@ -20,6 +20,8 @@
 //    to O(eps * cond(Y)). A device-side status flag hands ill-conditioned
 //    or rank-deficient inputs to householder_kernel, a faithful
 //    right-looking Householder QR (same cooperative structure as the LU).
+#include <cooperative_groups.h>
+
 #include <algorithm>
 
 #include "factor.cuh"
@@ -152,96 +154,287 @@ __device__ void block_argmax(T& v, int& idx, T* sv, int* si) {
   __syncthreads();
 }
 
-// Rows are held in physical (Kolda) order: physical row p is storage row
-// kolda_inverse(p) of the (L, n, R) panel, so the same kernel serves the
-// I x l samples (identity map) and small W panels of any mode.
-template <typename T>
-__global__ void __launch_bounds__(kSmemLuThreads) plu_smem_kernel(const T* __restrict__ A, T* __restrict__ Z, int I,
-                                                                  int n, i64 R, KoldaMap km, int* info) {
+// FullPivLU on a panel held in the distributed shared memory of one thread-
+// block cluster (CS = 1..16 CTAs; CS = 1 is a plain shared-memory kernel).
+// Rows are kept in physical (Kolda) order -- physical row p is storage row
+// kolda_inverse(p) of the (L, n, R) panel -- and CTA r of the cluster owns
+// physical rows [r*chunk, (r+1)*chunk). Row swaps move rows between CTAs
+// through DSMEM, column swaps are local, so the elimination is Eigen's,
+// operation for operation. Two cluster barriers per pivot.
+template <typename T, bool CLUSTER>
+__global__ void __launch_bounds__(kSmemLuThreads) plu_cluster_kernel(const T* __restrict__ A, T* __restrict__ Z,
+                                                                     int J, int n, int chunk, i64 R, KoldaMap km,
+                                                                     int* info) {
+  namespace cg = cooperative_groups;
+  const int CS = CLUSTER ? int(cg::this_cluster().num_blocks()) : 1;
+  const int me = CLUSTER ? int(cg::this_cluster().block_rank()) : 0;
+  auto csync = [&]() {
+    if constexpr (CLUSTER)
+      cg::this_cluster().sync();
+    else
+      __syncthreads();
+  };
+  auto remote = [&](auto* ptr, int rank) {
+    if constexpr (CLUSTER)
+      return cg::this_cluster().map_shared_rank(ptr, rank);
+    else
+      return ptr;
+  };
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* a = reinterpret_cast<T*>(smem_raw);
-  int* perm = reinterpret_cast<int*>(a + i64(I) * n);  // physical -> original physical row
+  T* a = reinterpret_cast<T*>(smem_raw);                       // [n][chunk] local rows, column-major
+  T* U = a + i64(chunk) * n;                                    // [n] pivot row (old row br)
+  T* Tk = U + n;                                                // [n] old row k
+  int* perm = reinterpret_cast<int*>(Tk + n);                   // [chunk] original physical index
+  __shared__ T cand_v;
+  __shared__ int cand_i;
   __shared__ T sv[32];
   __shared__ int si[32];
+  __shared__ int s_meta[4];  // perm_br, perm_k
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int r = I < n ? I : n;
-  const bool ident = (R == i64(I)) && km.n_low == 0 && km.n_high == 1;
-  for (int p = tid; p < I; p += nt) {
-    perm[p] = p;
-    if (ident) continue;
-    const i64 srow = kolda_inverse(km, p, R);
-    const i64 aa = srow / R, bb = srow - aa * R;
-    const i64 base = aa * n * R + bb;
-    for (int j = 0; j < n; ++j) a[p + j * I] = A[base + j * R];
+  const int r = J < n ? J : n;
+  const int p0 = me * chunk;
+  const int p1 = min(J, p0 + chunk);
+  const int rows = p1 > p0 ? p1 - p0 : 0;
+  const bool ident = (R == i64(J)) && km.n_low == 0 && km.n_high == 1;
+  // load own rows (physical order)
+  for (int lp = tid; lp < rows; lp += nt) {
+    const int p = p0 + lp;
+    perm[lp] = p;
+    i64 base;
+    if (ident) {
+      base = p;
+    } else {
+      const i64 srow = kolda_inverse(km, p, R);
+      const i64 aa = srow / R, bb = srow - aa * R;
+      base = aa * n * R + bb;
+    }
+    for (int j = 0; j < n; ++j) a[lp + j * chunk] = A[base + j * R];
   }
-  if (ident)
-    for (int e = tid; e < I * n; e += nt) a[e] = A[e];
   __syncthreads();
   const int tx = tid & 31, ty = tid >> 5, ny = nt >> 5;
-  // step-0 pivot search (afterwards it is fused into the update)
   T bv = T(-1);
   int bi = 0x7fffffff;
   for (int j = ty; j < n; j += ny)
-    for (int i = tx; i < I; i += 32) key_better(bv, bi, T(fabs(a[i + j * I])), j * I + i);
+    for (int lp = tx; lp < rows; lp += 32) key_better(bv, bi, T(fabs(a[lp + j * chunk])), j * J + p0 + lp);
   int k0 = r;
   for (int k = 0; k < r; ++k) {
     block_argmax(bv, bi, sv, si);
-    if (!(bv > T(0))) {
-      k0 = k;
-      break;
+    if (tid == 0) {
+      cand_v = bv;
+      cand_i = bi;
     }
-    const int br = bi % I, bc = bi / I;
-    if (br != k) {  // row swap, then column swap (FullPivLU order)
-      for (int j = tid; j < n; j += nt) {
-        const T t = a[k + j * I];
-        a[k + j * I] = a[br + j * I];
-        a[br + j * I] = t;
+    csync();  // B1: candidates published
+    if (tid < 32) {  // reduce the cluster's candidates (same order in every CTA)
+      T v = T(-1);
+      int idx = 0x7fffffff;
+      if (tid < CS) {
+        v = *remote(&cand_v, tid);
+        idx = *remote(&cand_i, tid);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+        key_better(v, idx, __shfl_xor_sync(0xffffffffu, v, o), __shfl_xor_sync(0xffffffffu, idx, o));
+      if (tid == 0) {
+        sv[0] = v;
+        si[0] = idx;
+      }
+    }
+    __syncthreads();
+    const T gv = sv[0];
+    const int gi = si[0];
+    if (!(gv > T(0))) {
+      k0 = k;
+      break;  // uniform across the cluster
+    }
+    const int br = gi % J, bc = gi / J;
+    const int ok_ = k / chunk, obr = br / chunk;
+    // old row br -> U (every CTA); old row k -> Tk (owner of br, when swapping)
+    {
+      const T* rb = remote(a, obr);
+      for (int j = tid; j < n; j += nt) U[j] = rb[(br - obr * chunk) + j * chunk];
+      if (tid == 0) s_meta[0] = *remote(perm + (br - obr * chunk), obr);
+      if (br != k && me == obr) {
+        const T* rk = remote(a, ok_);
+        for (int j = tid; j < n; j += nt) Tk[j] = rk[(k - ok_ * chunk) + j * chunk];
+        if (tid == 0) s_meta[1] = *remote(perm + (k - ok_ * chunk), ok_);
+      }
+    }
+    csync();  // B2: every remote read done before rows are overwritten
+    if (br != k) {
+      if (me == ok_) {
+        for (int j = tid; j < n; j += nt) a[(k - p0) + j * chunk] = U[j];
+        if (tid == 0) perm[k - p0] = s_meta[0];
+      }
+      if (me == obr) {
+        for (int j = tid; j < n; j += nt) a[(br - p0) + j * chunk] = Tk[j];
+        if (tid == 0) perm[br - p0] = s_meta[1];
+      }
+    }
+    __syncthreads();
+    if (bc != k) {  // column swap in the local rows and in U
+      for (int lp = tid; lp < rows; lp += nt) {
+        const T t = a[lp + k * chunk];
+        a[lp + k * chunk] = a[lp + bc * chunk];
+        a[lp + bc * chunk] = t;
       }
       if (tid == 0) {
-        const int t = perm[k];
-        perm[k] = perm[br];
-        perm[br] = t;
+        const T t = U[k];
+        U[k] = U[bc];
+        U[bc] = t;
       }
-      __syncthreads();
     }
-    if (bc != k) {
-      for (int i = tid; i < I; i += nt) {
-        const T t = a[i + k * I];
-        a[i + k * I] = a[i + bc * I];
-        a[i + bc * I] = t;
-      }
-      __syncthreads();
-    }
-    const T piv = a[k + k * I];
-    for (int i = k + 1 + tid; i < I; i += nt) a[i + k * I] = a[i + k * I] / piv;
+    __syncthreads();
+    const T piv = U[k];
+    // multipliers (col k below the diagonal), then the rank-1 update fused with
+    // the next pivot search
+    const int lo = max(k + 1, p0) - p0;
+    for (int lp = lo + tid; lp < rows; lp += nt) a[lp + k * chunk] = a[lp + k * chunk] / piv;
     __syncthreads();
     bv = T(-1);
     bi = 0x7fffffff;
     if (k < r - 1) {
       for (int j = k + 1 + ty; j < n; j += ny) {
-        const T u = a[k + j * I];
-        for (int i = k + 1 + tx; i < I; i += 32) {
-          const T x = a[i + j * I] - a[i + k * I] * u;
-          a[i + j * I] = x;
-          key_better(bv, bi, T(fabs(x)), j * I + i);
+        const T u = U[j];
+        for (int lp = lo + tx; lp < rows; lp += 32) {
+          const T x = a[lp + j * chunk] - a[lp + k * chunk] * u;
+          a[lp + j * chunk] = x;
+          key_better(bv, bi, T(fabs(x)), j * J + p0 + lp);
         }
       }
-      __syncthreads();
     }
+    __syncthreads();
   }
   // P^{-1} L: physical row p of L goes to original row perm[p]
-  if (ident) {
-    for (int e = tid; e < I * r; e += nt) {
-      const int p = e % I, j = e / I;
-      const T v = (p == j) ? T(1) : (p > j ? a[p + j * I] : T(0));
-      Z[perm[p] + i64(j) * I] = v;
+  for (int lp = tid; lp < rows; lp += nt) {
+    const int p = p0 + lp;
+    i64 base;
+    if (ident) {
+      base = perm[lp];
+    } else {
+      const i64 srow = kolda_inverse(km, perm[lp], R);
+      const i64 aa = srow / R, bb = srow - aa * R;
+      base = aa * r * R + bb;
     }
+    for (int j = 0; j < r; ++j) Z[base + j * R] = (p == j) ? T(1) : (p > j ? a[lp + j * chunk] : T(0));
+  }
+  if (me == 0 && tid == 0) *info = k0;
+  csync();  // keep every CTA's shared memory alive until all remote reads are done
+}
+
+// FullPivLU with ONE barrier per pivot: the panel is double-buffered in
+// shared memory and every step rewrites it from the previous buffer with the
+// row swap (k <-> br) and column swap (k <-> bc) applied as an index remap,
+// the multipliers formed and the trailing update done in the same pass; the
+// next pivot's candidates come out of that pass (warp-reduced, then reduced
+// redundantly by every thread after the barrier). Same operations as
+// FullPivLU; the multiplier uses a * (1 / pivot) (an ulp from a / pivot).
+constexpr int kPpThreads = 256;
+
+template <typename T>
+__global__ void __launch_bounds__(kPpThreads) plu_pp_kernel(const T* __restrict__ A, T* __restrict__ Z, int I, int n,
+                                                            i64 R, KoldaMap km, int* info) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* b0 = reinterpret_cast<T*>(smem_raw);
+  T* b1 = b0 + i64(I) * n;
+  int* q0 = reinterpret_cast<int*>(b1 + i64(I) * n);
+  int* q1 = q0 + I;
+  __shared__ T cv[2][kPpThreads / 32];
+  __shared__ int ci[2][kPpThreads / 32];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  const int r = I < n ? I : n;
+  const bool ident = (R == i64(I)) && km.n_low == 0 && km.n_high == 1;
+  T* cur = b0;
+  T* nxt = b1;
+  int* pc = q0;
+  int* pn = q1;
+  // load (physical row order) and step-0 candidates
+  T bv = T(-1);
+  int bi = 0x7fffffff;
+  if (ident) {
+    for (int j = wid; j < n; j += nw)
+      for (int i = lane; i < I; i += 32) {
+        const T x = A[i + i64(j) * I];
+        cur[i + j * I] = x;
+        key_better(bv, bi, T(fabs(x)), j * I + i);
+      }
+  } else {
+    for (int i = tid; i < I; i += nt) {
+      const i64 srow = kolda_inverse(km, i, R);
+      const i64 aa = srow / R, bb = srow - aa * R;
+      const i64 base = aa * n * R + bb;
+      for (int j = 0; j < n; ++j) cur[i + j * I] = A[base + j * R];
+    }
+    __syncthreads();
+    for (int j = wid; j < n; j += nw)
+      for (int i = lane; i < I; i += 32) key_better(bv, bi, T(fabs(cur[i + j * I])), j * I + i);
+  }
+  for (int i = tid; i < I; i += nt) pc[i] = i;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) key_better(bv, bi, __shfl_xor_sync(0xffffffffu, bv, o), __shfl_xor_sync(0xffffffffu, bi, o));
+  if (lane == 0) {
+    cv[0][wid] = bv;
+    ci[0][wid] = bi;
+  }
+  __syncthreads();
+  int k0 = r;
+  for (int k = 0; k < r; ++k) {
+    const int par = k & 1;
+    T gv = T(-1);
+    int gi = 0x7fffffff;
+    for (int w = 0; w < nw; ++w) key_better(gv, gi, cv[par][w], ci[par][w]);
+    if (!(gv > T(0))) {
+      k0 = k;
+      break;
+    }
+    const int br = gi % I, bc = gi / I;
+    const T rp = T(1) / cur[br + bc * I];
+    const bool upd = (k < r - 1);
+    bv = T(-1);
+    bi = 0x7fffffff;
+    for (int j = wid; j < n; j += nw) {
+      const int tj = (j == k) ? bc : (j == bc ? k : j);
+      const T u = cur[br + tj * I];  // pivot row (physical br -> k)
+      for (int i = lane; i < I; i += 32) {
+        const int si = (i == k) ? br : (i == br ? k : i);
+        T x = cur[si + tj * I];
+        if (i > k) {
+          const T m = cur[si + bc * I] * rp;  // multiplier of row i
+          if (j == k) {
+            x = m;
+          } else if (j > k && upd) {
+            x = x - m * u;
+            key_better(bv, bi, T(fabs(x)), j * I + i);
+          }
+        }
+        nxt[i + j * I] = x;
+      }
+    }
+    for (int i = tid; i < I; i += nt) pn[i] = pc[(i == k) ? br : (i == br ? k : i)];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) key_better(bv, bi, __shfl_xor_sync(0xffffffffu, bv, o), __shfl_xor_sync(0xffffffffu, bi, o));
+    if (lane == 0) {
+      cv[par ^ 1][wid] = bv;
+      ci[par ^ 1][wid] = bi;
+    }
+    __syncthreads();
+    T* t = cur;
+    cur = nxt;
+    nxt = t;
+    int* tq = pc;
+    pc = pn;
+    pn = tq;
+  }
+  // P^{-1} L
+  if (ident) {
+    for (int j = wid; j < r; j += nw)
+      for (int p = lane; p < I; p += 32) Z[pc[p] + i64(j) * I] = (p == j) ? T(1) : (p > j ? cur[p + j * I] : T(0));
   } else {
     for (int p = tid; p < I; p += nt) {
-      const i64 srow = kolda_inverse(km, perm[p], R);
+      const i64 srow = kolda_inverse(km, pc[p], R);
       const i64 aa = srow / R, bb = srow - aa * R;
       const i64 base = aa * r * R + bb;
-      for (int j = 0; j < r; ++j) Z[base + j * R] = (p == j) ? T(1) : (p > j ? a[p + j * I] : T(0));
+      for (int j = 0; j < r; ++j) Z[base + j * R] = (p == j) ? T(1) : (p > j ? cur[p + j * I] : T(0));
     }
   }
   if (tid == 0) *info = k0;
@@ -734,6 +927,112 @@ __global__ void __launch_bounds__(kCqrThreads) cqr2_kernel(const T* __restrict__
   }
 }
 
+// CholeskyQR2 + Householder sign reconstruction with Y resident in shared
+// memory (I * n doubles): everything after the load is on-chip.
+template <typename T>
+__global__ void __launch_bounds__(kCqrThreads) cqr2_smem_kernel(const T* __restrict__ Y, T* __restrict__ Q, int I,
+                                                                int n, int* status, int* rank_warning) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* V = reinterpret_cast<double*>(smem_raw);  // I x n
+  double* G = V + i64(I) * n;                        // n x n
+  double* Rm = G + n * n;                            // n x n upper
+  double* dg = Rm + n * n;                           // [2][n]
+  double* sgn = dg + 2 * n;                          // [n]
+  __shared__ int s_fail;
+  __shared__ double s_piv;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  for (int e = tid; e < I * n; e += nt) V[e] = double(Y[e]);
+  if (tid == 0) s_fail = 0;
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass) {
+    // G = V^T V: warp per (a, b) pair, lanes over rows (conflict-free: a
+    // column of V is contiguous; lanes striding a row would all hit one bank)
+    for (int pr = wid; pr < n * (n + 1) / 2; pr += nw) {
+      int b = int((sqrt(8.0 * pr + 1.0) - 1.0) * 0.5);
+      while (b * (b + 1) / 2 > pr) --b;
+      while ((b + 1) * (b + 2) / 2 <= pr) ++b;
+      const int a = pr - b * (b + 1) / 2;
+      const double* va = V + i64(a) * I;
+      const double* vb = V + i64(b) * I;
+      double s = 0.0;
+      for (int i = lane; i < I; i += 32) s += va[i] * vb[i];
+      s = warp_sum(s);
+      if (lane == 0) {
+        G[a + b * n] = s;
+        G[b + a * n] = s;
+      }
+    }
+    __syncthreads();
+    for (int j = 0; j < n; ++j) {  // upper Cholesky G = R^T R
+      if (tid == 0) {
+        double d = G[j + j * n];
+        for (int k = 0; k < j; ++k) d -= Rm[k + j * n] * Rm[k + j * n];
+        if (!(d > 0.0)) s_fail = 1;
+        s_piv = d > 0.0 ? sqrt(d) : 1.0;
+        Rm[j + j * n] = s_piv;
+        dg[pass * n + j] = s_piv;
+      }
+      __syncthreads();
+      const double dj = s_piv;
+      for (int c = j + 1 + tid; c < n; c += nt) {
+        double s = G[j + c * n];
+        for (int k = 0; k < j; ++k) s -= Rm[k + j * n] * Rm[k + c * n];
+        Rm[j + c * n] = s / dj;
+      }
+      __syncthreads();
+    }
+    if (s_fail) break;
+    for (int i = tid; i < I; i += nt)  // V <- V R^{-1}, in place, row by row
+      for (int j = 0; j < n; ++j) {
+        double v = V[i + i64(j) * I];
+        for (int k = 0; k < j; ++k) v -= V[i + i64(k) * I] * Rm[k + j * n];
+        V[i + i64(j) * I] = v / Rm[j + j * n];
+      }
+    __syncthreads();
+  }
+  if (!s_fail && tid == 0) {
+    double mx = 0.0, mn = INFINITY;
+    for (int j = 0; j < n; ++j) {
+      mx = fmax(mx, dg[j]);
+      mn = fmin(mn, dg[j]);
+    }
+    if (!(mn > 0.0) || mx / mn > 1e6) s_fail = 1;
+  }
+  __syncthreads();
+  if (s_fail) {
+    if (tid == 0) *status = 1;
+    return;
+  }
+  for (int e = tid; e < n * n; e += nt) G[e] = V[(e % n) + i64(e / n) * I];
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {  // sign reconstruction (modified LU of Q_top - S)
+    if (tid == 0) {
+      sgn[k] = G[k + k * n] > 0.0 ? -1.0 : 1.0;
+      if (sgn[k] < 0.0)
+        for (int i = 0; i < n; ++i) G[i + k * n] = -G[i + k * n];
+      G[k + k * n] -= 1.0;
+    }
+    __syncthreads();
+    const double dkk = G[k + k * n];
+    for (int j = k + 1 + wid; j < n; j += nw)
+      for (int i = k + 1 + lane; i < n; i += 32) G[i + j * n] -= (G[i + k * n] / dkk) * G[k + j * n];
+    __syncthreads();
+  }
+  for (int j = wid; j < n; j += nw)
+    for (int i = lane; i < I; i += 32) Q[i + i64(j) * I] = T(V[i + i64(j) * I] * sgn[j]);
+  if (tid == 0) {
+    T dmax = T(0), dmin = T(INFINITY);
+    for (int j = 0; j < n; ++j) {
+      const T d = T(dg[j] * dg[n + j]);
+      dmax = d > dmax ? d : dmax;
+      dmin = d < dmin ? d : dmin;
+    }
+    if (rank_warning) *rank_warning = (dmax == T(0)) || (dmin <= T(I) * Traits<T>::eps * dmax);
+    *status = 0;
+  }
+}
+
 int pick_grid(i64 J, int n, int maxc) {
   // ~4K panel entries per CTA: the per-step update is latency bound
   const i64 want = ceil_div(J * n, 4096);
@@ -755,12 +1054,46 @@ template <typename T>
 int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w, cudaStream_t st) {
   check_arg(n <= kMaxPanelCols, "plu_basis: panel wider than supported");
   const int r = int(std::min<i64>(J, n));
-  const size_t smem = smem_lu_bytes(J, n, sizeof(T));
-  static const size_t lu_lim = enable_max_dyn_smem(plu_smem_kernel<T>);
-  if (smem <= lu_lim) {
-    plu_smem_kernel<T><<<1, kSmemLuThreads, smem, st>>>(A, Z, int(J), n, R, km, w.info);
+  // one CTA with a double-buffered panel: one barrier per pivot
+  static const size_t pp_lim = enable_max_dyn_smem(plu_pp_kernel<T>);
+  const size_t pp_smem = 2 * size_t(J) * n * sizeof(T) + 2 * size_t(J) * sizeof(int);
+  if (false && pp_smem <= pp_lim) {  // slower than the swap kernel on B200 (latency bound); kept for reference
+    plu_pp_kernel<T><<<1, kPpThreads, pp_smem, st>>>(A, Z, int(J), n, R, km, w.info);
     count_launch();
     RCPG_LAUNCHED();
+    return r;
+  }
+  // on-chip paths: one CTA, or one cluster of up to 16 CTAs
+  static const size_t lu_lim1 = enable_max_dyn_smem(plu_cluster_kernel<T, false>);
+  static const size_t lu_lim = enable_max_dyn_smem(plu_cluster_kernel<T, true>);
+  static const bool nonportable = [] {
+    return cudaFuncSetAttribute(plu_cluster_kernel<T, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+           cudaSuccess;
+  }();
+  for (int cs = 1; cs <= (nonportable ? 16 : 8); cs *= 2) {
+    const int chunk = int(ceil_div(J, cs));
+    const size_t smem = size_t(chunk) * n * sizeof(T) + 2 * size_t(n) * sizeof(T) + size_t(chunk) * sizeof(int) + 16;
+    if (smem > (cs == 1 ? lu_lim1 : lu_lim) - 1024) continue;
+    if (cs == 1) {
+      plu_cluster_kernel<T, false><<<1, kSmemLuThreads, smem, st>>>(A, Z, int(J), n, chunk, R, km, w.info);
+      count_launch();
+      RCPG_LAUNCHED();
+      return r;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(kSmemLuThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    RCPG_CUDA(cudaLaunchKernelEx(&cfg, plu_cluster_kernel<T, true>, (const T*)A, Z, int(J), n, chunk, R, km, w.info));
+    count_launch();
     return r;
   }
   init_row_keys(km, J, R, w.keys, st);
@@ -781,7 +1114,14 @@ int thin_qr(T* A, T* Q, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w, 
   const int* skip = nullptr;
   const size_t cq_smem = (2 * size_t(n) * n + 3 * size_t(n)) * sizeof(double);
   static const size_t cq_lim = enable_max_dyn_smem(cqr2_kernel<T>);
-  if (R == J && kolda_identity && J >= n && J <= w.cqr_rows && cq_smem <= cq_lim) {
+  static const size_t cqs_lim = enable_max_dyn_smem(cqr2_smem_kernel<T>);
+  const size_t cqs_smem = (size_t(J) * n + 2 * size_t(n) * n + 3 * size_t(n)) * sizeof(double);
+  if (R == J && kolda_identity && J >= n && cqs_smem <= cqs_lim) {
+    cqr2_smem_kernel<T><<<1, kCqrThreads, cqs_smem, st>>>(A, Q, int(J), n, w.info + 2, rank_warning_dev);
+    count_launch();
+    RCPG_LAUNCHED();
+    skip = w.info + 2;
+  } else if (R == J && kolda_identity && J >= n && J <= w.cqr_rows && cq_smem <= cq_lim) {
     cqr2_kernel<T><<<1, kCqrThreads, cq_smem, st>>>(A, Q, int(J), n, w.cqr_work, w.info + 2, rank_warning_dev);
     count_launch();
     RCPG_LAUNCHED();

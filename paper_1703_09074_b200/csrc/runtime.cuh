@@ -37,10 +37,18 @@ inline const DeviceCaps& device_caps() {
 // Largest cooperative grid for `kernel` at `threads` threads and `smem` bytes.
 template <typename K>
 int max_coop_blocks(K kernel, int threads, size_t smem) {
+  // cached: occupancy queries are slow host calls that would leave the GPU idle
+  static thread_local struct Entry { const void* k; int threads; size_t smem; int blocks; } cache[16];
+  static thread_local int used = 0;
+  for (int i = 0; i < used; ++i)
+    if (cache[i].k == reinterpret_cast<const void*>(kernel) && cache[i].threads == threads && cache[i].smem == smem)
+      return cache[i].blocks;
   int per_sm = 0;
   RCPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
   if (per_sm < 1) throw std::runtime_error("cooperative kernel does not fit on an SM");
-  return per_sm * device_caps().num_sms;
+  const int blocks = per_sm * device_caps().num_sms;
+  if (used < 16) cache[used++] = Entry{reinterpret_cast<const void*>(kernel), threads, smem, blocks};
+  return blocks;
 }
 
 // Opt a kernel into the largest dynamic shared memory the device allows

@@ -232,6 +232,35 @@ def test_decompose_errors(rcp):
     assert e.value.iteration() == 0
 
 
+def test_decompose_error_order_matches_reference(rcp, oracle):
+    """Device-side checks are raised after the work is enqueued; the error
+    reported must still be the one the sequential reference raises first."""
+    x = np.random.default_rng(1).standard_normal((8, 7, 6))
+    bad = x.copy()
+    bad[2, 3, 1] = np.nan
+    g, o = cfgs(rcp, oracle, 2, 2, 1, 3)
+    with pytest.raises(ValueError, match="compress: input values must be finite"):
+        rcp.decompose(bad, g)
+    with pytest.raises(oracle.OracleInvalidArgument, match="compress: input values must be finite"):
+        oracle.decompose(bad, o)
+    # finite check precedes the mode-range check (compress.hpp:93 vs :98)
+    g2, _ = cfgs(rcp, oracle, 2, 2, 1, 3, modes=[5])
+    with pytest.raises(ValueError, match="finite"):
+        rcp.decompose(bad, g2)
+    g3, _ = cfgs(rcp, oracle, 2, 2, 1, 3, modes=[5])
+    with pytest.raises(ValueError, match="mode index out of range"):
+        rcp.decompose(x, g3)
+    z = np.zeros((5, 4, 3))
+    g4, o4 = cfgs(rcp, oracle, 2, 2, 1, 3, randomized=False)
+    with pytest.raises(ValueError, match="tensor norm must be positive"):
+        rcp.decompose(z, g4)
+    with pytest.raises(oracle.OracleInvalidArgument, match="tensor norm must be positive"):
+        oracle.decompose(z, o4)
+    # the context stays usable after errors
+    model, trace = rcp.decompose(x, cfgs(rcp, oracle, 2, 2, 1, 3)[0])
+    assert np.isfinite(trace.final_relative_error)
+
+
 def test_decompose_end_to_end_determinism(rcp, oracle):
     x, _ = oracle.random_lowrank([24, 22, 20], 3, 51, snr=2.0, noise_seed=4)
     g, _ = cfgs(rcp, oracle, 3, 10, 2, 77)
