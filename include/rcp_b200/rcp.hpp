@@ -1,0 +1,306 @@
+// SPDX-License-Identifier: MIT
+// Drop-in C++ front end for the B200 rCP path: the reference's `namespace rcp`
+// entry points for rcp::decompose / rcp::compress / rcp::relative_error
+// (/root/reference/proj/include/rcp/{solve,compress,kruskal}.hpp), same names,
+// same argument meaning and exceptions, implemented over the C ABI in
+// include/rcpg.h (link with -lrcpg). Eigen is not required: Matrix/Vector are
+// minimal column-major stand-ins exposing the members callers use
+// (rows, cols, operator(), data, size).
+#pragma once
+
+#include <cstdint>
+#include <limits>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../rcpg.h"
+
+namespace rcp {
+
+using Index = std::int64_t;
+using Shape = std::vector<Index>;
+
+template <typename S>
+class Matrix {
+ public:
+  Matrix() = default;
+  Matrix(Index r, Index c) : r_(r), c_(c), v_(std::size_t(r * c), S(0)) {}
+  Index rows() const { return r_; }
+  Index cols() const { return c_; }
+  Index size() const { return r_ * c_; }
+  S& operator()(Index i, Index j) { return v_[std::size_t(i + j * r_)]; }
+  const S& operator()(Index i, Index j) const { return v_[std::size_t(i + j * r_)]; }
+  S* data() { return v_.data(); }
+  const S* data() const { return v_.data(); }
+
+ private:
+  Index r_ = 0, c_ = 0;
+  std::vector<S> v_;
+};
+
+template <typename S>
+using Vector = std::vector<S>;
+
+// tensor.hpp:19-108 (row-major values, last index fastest)
+template <typename S>
+class Tensor {
+ public:
+  Tensor() = default;
+  Tensor(Shape shape, std::vector<S> values) : shape_(std::move(shape)), values_(std::move(values)) {}
+  Index order() const { return Index(shape_.size()); }
+  const Shape& shape() const { return shape_; }
+  Index extent(Index m) const { return shape_[std::size_t(m)]; }
+  Index size() const { return Index(values_.size()); }
+  const std::vector<S>& values() const { return values_; }
+  std::vector<S>& values() { return values_; }
+  const S* data() const { return values_.data(); }
+
+ private:
+  Shape shape_;
+  std::vector<S> values_;
+};
+
+enum class RandomDistribution { gaussian = RCPG_GAUSSIAN, uniform = RCPG_UNIFORM };
+enum class PowerStabilizer { lu = RCPG_STAB_LU, qr = RCPG_STAB_QR };
+enum class SolveMethod { als = RCPG_ALS, bcd = RCPG_BCD };
+enum class InitMethod { eigenvectors = RCPG_INIT_EIGENVECTORS, random = RCPG_INIT_RANDOM };
+
+// compress.hpp:23-33
+struct CompressConfig {
+  Index target_rank = 0;
+  Index oversampling = 10;
+  int power_iterations = 2;
+  std::optional<std::vector<Index>> modes;
+  RandomDistribution distribution = RandomDistribution::gaussian;
+  PowerStabilizer stabilizer = PowerStabilizer::lu;
+  std::uint64_t seed = 0;
+};
+
+// solve.hpp:22-31
+struct DecomposeConfig {
+  Index rank = 1;
+  SolveMethod method = SolveMethod::als;
+  bool randomized = true;
+  CompressConfig compress;
+  double tol = 1e-5;
+  int max_iter = 500;
+  std::uint64_t seed = 0;
+  InitMethod init = InitMethod::eigenvectors;
+};
+
+template <typename S>
+struct Kruskal {
+  Vector<S> weights;
+  std::vector<Matrix<S>> factors;
+  Index rank() const { return Index(weights.size()); }
+  Index order() const { return Index(factors.size()); }
+};
+
+// solve.hpp:35-45
+struct FitTrace {
+  struct Entry {
+    int iteration;
+    double fit;
+    double seconds;
+  };
+  std::vector<Entry> entries;
+  double final_relative_error = std::numeric_limits<double>::quiet_NaN();
+  int iterations = 0;
+  bool converged = false;
+};
+
+// solve.hpp:48-57
+class SolverError : public std::runtime_error {
+ public:
+  SolverError(const std::string& message, int iteration) : std::runtime_error(message), iteration_(iteration) {}
+  int iteration() const { return iteration_; }
+
+ private:
+  int iteration_;
+};
+
+// types.hpp:60-76
+template <typename S>
+struct ModeBasis {
+  Matrix<S> q;
+  bool identity = false;
+  Index dim = 0;
+  bool rank_warning = false;
+};
+
+template <typename S>
+struct CompressionResult {
+  Tensor<S> compressed;
+  std::vector<ModeBasis<S>> bases;
+};
+
+namespace detail {
+
+template <typename S>
+constexpr rcpg_dtype dtype() {
+  static_assert(std::is_same_v<S, float> || std::is_same_v<S, double>, "rcp: float or double");
+  return std::is_same_v<S, double> ? RCPG_F64 : RCPG_F32;
+}
+
+// One context per thread (rcpg is single-stream per context).
+inline rcpg_context* context() {
+  struct Holder {
+    rcpg_context* ctx = nullptr;
+    ~Holder() {
+      if (ctx) rcpg_destroy(ctx);
+    }
+  };
+  static thread_local Holder h;
+  if (!h.ctx && rcpg_create(0, &h.ctx) != RCPG_OK) throw std::runtime_error("rcp: no usable CUDA device");
+  return h.ctx;
+}
+
+inline void check(rcpg_context* c, rcpg_status st) {
+  if (st == RCPG_OK) return;
+  const std::string msg = rcpg_last_error(c);
+  if (st == RCPG_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  if (st == RCPG_SOLVER_ERROR) throw SolverError(msg, rcpg_last_error_iteration(c));
+  throw std::runtime_error(msg);
+}
+
+struct CCompress {
+  rcpg_compress_config c{};
+  std::vector<std::int64_t> modes;
+  explicit CCompress(const CompressConfig& cfg) {
+    c.target_rank = cfg.target_rank;
+    c.oversampling = cfg.oversampling;
+    c.power_iterations = cfg.power_iterations;
+    c.distribution = int32_t(cfg.distribution);
+    c.stabilizer = int32_t(cfg.stabilizer);
+    c.seed = cfg.seed;
+    if (cfg.modes) {
+      modes.assign(cfg.modes->begin(), cfg.modes->end());
+      c.modes_present = 1;
+      c.n_modes = std::int64_t(modes.size());
+      c.modes = modes.empty() ? nullptr : modes.data();
+    }
+  }
+};
+
+struct DeviceTensor {
+  rcpg_context* c;
+  rcpg_tensor* t = nullptr;
+  template <typename S>
+  DeviceTensor(rcpg_context* ctx, const Tensor<S>& x) : c(ctx) {
+    check(c, rcpg_tensor_upload(c, dtype<S>(), int32_t(x.order()), x.shape().data(), x.data(), &t));
+  }
+  ~DeviceTensor() { rcpg_tensor_free(t); }
+};
+
+}  // namespace detail
+
+// solve.hpp:381-398
+template <typename S>
+std::pair<Kruskal<S>, FitTrace> decompose(const Tensor<S>& t, const DecomposeConfig& cfg) {
+  rcpg_context* c = detail::context();
+  detail::CCompress cc(cfg.compress);
+  rcpg_decompose_config d{};
+  d.rank = cfg.rank;
+  d.method = int32_t(cfg.method);
+  d.randomized = cfg.randomized ? 1 : 0;
+  d.compress = cc.c;
+  d.tol = cfg.tol;
+  d.max_iter = cfg.max_iter;
+  d.init = int32_t(cfg.init);
+  d.seed = cfg.seed;
+  const Index R = cfg.rank > 0 ? cfg.rank : 1;
+  Index sum_ext = 0;
+  for (Index e : t.shape()) sum_ext += e;
+  std::vector<S> w(static_cast<std::size_t>(R)), f(static_cast<std::size_t>(sum_ext * R));
+  const int cap = cfg.max_iter > 0 ? cfg.max_iter : 1;
+  std::vector<int32_t> it(static_cast<std::size_t>(cap));
+  std::vector<double> fit(static_cast<std::size_t>(cap)), sec(static_cast<std::size_t>(cap));
+  rcpg_result res{};
+  res.weights = w.data();
+  res.factors = f.data();
+  res.trace_iteration = it.data();
+  res.trace_fit = fit.data();
+  res.trace_seconds = sec.data();
+  res.trace_capacity = cap;
+  detail::DeviceTensor dt(c, t);
+  detail::check(c, rcpg_decompose(c, dt.t, &d, &res));
+  Kruskal<S> model;
+  model.weights = w;
+  Index off = 0;
+  for (Index e : t.shape()) {
+    Matrix<S> m(e, R);
+    for (Index i = 0; i < e * R; ++i) m.data()[i] = f[std::size_t(off + i)];
+    off += e * R;
+    model.factors.push_back(std::move(m));
+  }
+  FitTrace trace;
+  for (int i = 0; i < std::min(res.iterations, cap); ++i) trace.entries.push_back({it[size_t(i)], fit[size_t(i)], sec[size_t(i)]});
+  trace.iterations = res.iterations;
+  trace.converged = res.converged != 0;
+  trace.final_relative_error = res.final_relative_error;
+  return {std::move(model), trace};
+}
+
+// compress.hpp:86-146
+template <typename S>
+CompressionResult<S> compress(const Tensor<S>& t, const CompressConfig& cfg) {
+  rcpg_context* c = detail::context();
+  detail::CCompress cc(cfg);
+  detail::DeviceTensor dt(c, t);
+  rcpg_compressed* out = nullptr;
+  detail::check(c, rcpg_compress(c, dt.t, &cc.c, &out));
+  CompressionResult<S> r;
+  const int32_t order = rcpg_compressed_order(out);
+  Shape shape(static_cast<std::size_t>(order));
+  rcpg_compressed_shape(out, shape.data());
+  Index n = 1;
+  for (Index e : shape) n *= e;
+  std::vector<S> vals(static_cast<std::size_t>(n));
+  detail::check(c, rcpg_compressed_download(c, out, vals.data()));
+  r.compressed = Tensor<S>(shape, std::move(vals));
+  for (int32_t m = 0; m < order; ++m) {
+    int32_t ident = 0, rw = 0;
+    int64_t dim = 0, cols = 0;
+    rcpg_compressed_basis_info(out, m, &ident, &dim, &cols, &rw);
+    ModeBasis<S> b;
+    b.identity = ident != 0;
+    b.dim = dim;
+    b.rank_warning = rw != 0;
+    if (!b.identity) {
+      b.q = Matrix<S>(dim, cols);
+      detail::check(c, rcpg_compressed_basis_download(c, out, m, b.q.data()));
+    }
+    r.bases.push_back(std::move(b));
+  }
+  rcpg_compressed_free(out);
+  return r;
+}
+
+// kruskal.hpp:187-194
+template <typename S>
+S relative_error(const Tensor<S>& x, const Kruskal<S>& k) {
+  rcpg_context* c = detail::context();
+  std::vector<S> f;
+  for (const auto& m : k.factors) f.insert(f.end(), m.data(), m.data() + m.size());
+  detail::DeviceTensor dt(c, x);
+  double out = 0;
+  detail::check(c, rcpg_relative_error(c, dt.t, k.rank(), k.weights.data(), f.data(), &out));
+  return S(out);
+}
+
+inline std::uint64_t mix64(std::uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+// random.hpp:48-56
+enum class StreamDomain : std::uint64_t { compress = 1, init = 2, factors = 3, noise = 4, phases = 5, trial = 6 };
+inline std::uint64_t stream_id(StreamDomain d, std::uint64_t k = 0) { return (std::uint64_t(d) << 32) | k; }
+inline std::uint64_t derive_seed(std::uint64_t seed, std::uint64_t salt) {
+  return mix64(seed + 0x9e3779b97f4a7c15ULL * (salt + 1));
+}
+
+}  // namespace rcp
