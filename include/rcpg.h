@@ -149,6 +149,13 @@ rcpg_status rcpg_relative_error(rcpg_context* ctx, const rcpg_tensor* t, int64_t
  * draws it, on the device, and copies it to host. */
 rcpg_status rcpg_sketch_matrix(rcpg_context* ctx, rcpg_dtype dtype, uint64_t seed, int64_t mode,
                                int64_t rows, int64_t cols, int32_t distribution, void* host);
+/* One streamed mode-n pass on host inputs (mode view L x I x R of a row-major
+ * tensor, x[(a*I + i)*R + b]):
+ *   kind 0, sketch:     out[c*I + i]     = sum_{a,b} x[a,i,b] p[(a*cols + c)*R + b]
+ *   kind 1, projection: out[(a*cols + c)*R + b] = sum_i x[a,i,b] p[i + c*I]
+ * (the X_(n) Omega / X_(n)^T Q / Q^T X_(n) products of compress.hpp:118-145). */
+rcpg_status rcpg_stream_pass(rcpg_context* ctx, rcpg_dtype dtype, int32_t kind, int64_t L, int64_t I, int64_t R,
+                             int64_t cols, const void* x, const void* p, void* out);
 /* plu_basis / thin_qr (compress.hpp:47-73) of a host column-major matrix, on device. */
 rcpg_status rcpg_plu_basis(rcpg_context* ctx, rcpg_dtype dtype, int64_t rows, int64_t cols, const void* in,
                            void* out);

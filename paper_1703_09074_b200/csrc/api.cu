@@ -936,6 +936,41 @@ rcpg_status rcpg_sketch_matrix(rcpg_context* c, rcpg_dtype dtype, uint64_t seed,
   });
 }
 
+rcpg_status rcpg_stream_pass(rcpg_context* c, rcpg_dtype dtype, int32_t kind, int64_t L, int64_t I, int64_t R,
+                             int64_t cols, const void* x, const void* p, void* out) {
+  return guarded(c, [&] {
+    check_arg(kind == 0 || kind == 1, "stream_pass: kind must be 0 (sketch) or 1 (projection)");
+    check_arg(L >= 1 && I >= 1 && R >= 1 && cols >= 1, "stream_pass: empty view");
+    const size_t b = dsize(dtype);
+    const ModeView v{L, I, R};
+    const size_t nx = size_t(L * I * R), np_ = size_t(kind == 0 ? L * cols * R : I * cols),
+                 no = size_t(kind == 0 ? I * cols : L * cols * R);
+    DevBuf X, P, O, S;
+    X.ensure(nx * b);
+    P.ensure(np_ * b);
+    O.ensure(no * b);
+    RCPG_CUDA(cudaMemcpyAsync(X.p, x, nx * b, cudaMemcpyHostToDevice, c->st));
+    RCPG_CUDA(cudaMemcpyAsync(P.p, p, np_ * b, cudaMemcpyHostToDevice, c->st));
+    const int sms = device_caps().num_sms;
+    auto run = [&](auto tag) {
+      using T = decltype(tag);
+      if (kind == 0) {
+        const i64 scr = sketch_scratch_elems<T>(v, cols, sms);
+        S.ensure(size_t(scr) * b);
+        sketch<T>(X.as<T>(), v, P.as<T>(), cols, O.as<T>(), S.as<T>(), scr, sms, c->st);
+      } else {
+        project<T>(X.as<T>(), v, P.as<T>(), I, cols, O.as<T>(), c->st);
+      }
+    };
+    if (dtype == RCPG_F64)
+      run(double{});
+    else
+      run(float{});
+    RCPG_CUDA(cudaMemcpyAsync(out, O.p, no * b, cudaMemcpyDeviceToHost, c->st));
+    RCPG_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+
 rcpg_status rcpg_plu_basis(rcpg_context* c, rcpg_dtype dtype, int64_t rows, int64_t cols, const void* in,
                            void* out) {
   return guarded(c, [&] {

@@ -94,6 +94,8 @@ i64 sketch_scratch_elems(ModeView v, i64 cols, int num_sms) {
     splits = sketch_dmma_splits(v, cols, num_sms, tps, total);
   else
     sketch_plan<T>(v, cols, num_sms, splits, tps, total);
+  if (std::is_same<T, float>::value && v.R > 1)
+    splits = std::max(splits, sketch_tc_splits(v, cols, num_sms, tps, total));
   return splits * cols * v.I;
 }
 
@@ -101,7 +103,13 @@ template <typename T>
 void sketch(const T* X, ModeView v, const T* P, i64 cols, T* Y, T* scratch, i64 scratch_elems, int num_sms,
             cudaStream_t st, const int* skip) {
   i64 splits, tps, total;
-  if (use_dmma<T>(v)) {
+  bool tc = false;
+  if constexpr (std::is_same<T, float>::value) tc = tc_sketch_ok(X, P, v);
+  if (tc) {
+    splits = sketch_tc_splits(v, cols, num_sms, tps, total);
+    if (splits * cols * v.I > scratch_elems) throw std::runtime_error("sketch: scratch too small");
+    if constexpr (std::is_same<T, float>::value) sketch_tc(X, v, P, cols, scratch, num_sms, skip, st);
+  } else if (use_dmma<T>(v)) {
     splits = sketch_dmma_splits(v, cols, num_sms, tps, total);
     if (splits * cols * v.I > scratch_elems) throw std::runtime_error("sketch: scratch too small");
     if constexpr (std::is_same<T, double>::value) sketch_dmma(X, v, P, cols, scratch, num_sms, skip, st);
@@ -152,6 +160,11 @@ void project(const T* X, ModeView v, const T* Q, i64 ldq, i64 cols, T* O, cudaSt
   if constexpr (std::is_same<T, double>::value) {
     if (v.R > 1) {
       project_dmma(X, v, Q, ldq, cols, O, st);
+      return;
+    }
+  } else {
+    if (tc_project_ok(X, Q, v, ldq)) {
+      project_tc(X, v, Q, ldq, cols, O, device_caps().num_sms, st);
       return;
     }
   }

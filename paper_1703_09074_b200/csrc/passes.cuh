@@ -284,6 +284,18 @@ void sketch_dmma(const double* X, ModeView v, const double* P, i64 cols, double*
                  const int* skip, cudaStream_t st);
 void project_dmma(const double* X, ModeView v, const double* Q, i64 ldq, i64 cols, double* O, cudaStream_t st);
 
+// FP32 tcgen05 (3xTF32, TMEM accumulator) versions for mode views with R > 1
+// (passes_tc.cu). RCPG_NO_TC=1 in the environment routes fp32 to the SIMT
+// kernels instead (A/B testing only).
+bool tc_enabled();
+bool tc_sketch_ok(const float* X, const float* P, ModeView v);
+bool tc_project_ok(const float* X, const float* Q, ModeView v, i64 ldq);
+i64 sketch_tc_splits(ModeView v, i64 cols, int num_sms, i64& tps, i64& total);
+void sketch_tc(const float* X, ModeView v, const float* P, i64 cols, float* part, int num_sms, const int* skip,
+               cudaStream_t st);
+void project_tc(const float* X, ModeView v, const float* Q, i64 ldq, i64 cols, float* O, int num_sms,
+                cudaStream_t st);
+
 // Omega_n written in the panel layout (a, c, b): entry (s, c) is normal /
 // uniform_sym number c*J + kolda(s) of stream (seed, (compress << 32) | mode).
 template <typename T>

@@ -390,6 +390,33 @@ def sketch_matrix(seed: int, mode: int, rows: int, cols: int, distribution: int 
     return out
 
 
+def stream_pass(kind: str, x: np.ndarray, p: np.ndarray, cols: int, ctx: Optional[Context] = None) -> np.ndarray:
+    """One streamed mode-n pass on the GPU (compress.hpp:118-145 products).
+
+    ``x`` is a mode view of shape (L, I, R) (row-major). ``kind="sketch"``: ``p`` has
+    shape (L, cols, R), returns Y (I, cols) = sum_{a,b} x[a,:,b] p[a,:,b]^T.
+    ``kind="project"``: ``p`` is Q (I, cols), returns O (L, cols, R) = Q^T x[a].
+    """
+    ctx = ctx or default_context()
+    x = np.ascontiguousarray(x)
+    L, I, R = x.shape
+    if kind == "sketch":
+        p = np.ascontiguousarray(p, dtype=x.dtype)
+        assert p.shape == (L, cols, R)
+        out = np.empty((cols, I), dtype=x.dtype)
+        k = 0
+    elif kind == "project":
+        p = np.asfortranarray(p, dtype=x.dtype)
+        assert p.shape == (I, cols)
+        out = np.empty((L, cols, R), dtype=x.dtype)
+        k = 1
+    else:
+        raise ValueError(kind)
+    ctx.check(ctx.lib.rcpg_stream_pass(ctx.h, _dtype_code(x.dtype), k, L, I, R, cols, x.ctypes.data,
+                                       p.ctypes.data, out.ctypes.data))
+    return out.T if k == 0 else out
+
+
 def plu_basis(m: np.ndarray, ctx: Optional[Context] = None) -> np.ndarray:
     """detail::plu_basis (compress.hpp:47-58) on the GPU."""
     ctx = ctx or default_context()

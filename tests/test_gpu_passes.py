@@ -1,0 +1,93 @@
+"""Streamed-pass kernels (compress.hpp:118-145 products) against an fp64 numpy product.
+
+fp32 views with R % 4 == 0 run on the tcgen05 3xTF32 kernels (passes_tc.cu), the rest on
+the SIMT tiles; fp64 views with R > 1 on the DMMA kernels (passes_dmma.cu). The fp32 bound
+(normwise relative error 1e-5) is met by 3xTF32 (~1e-7) and missed by plain TF32 (~5e-4).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+# (L, I, R, cols): ragged M/N/K edges, several UMMA N widths, multi-n-tile (cols > 128),
+# R % 4 != 0 and I % 4 != 0 (SIMT fallbacks), the last-mode view (R = 1).
+VIEWS = [
+    (1, 200, 1000, 70),
+    (3, 130, 68, 17),
+    (2, 64, 4, 48),
+    (1, 1024, 4096, 80),
+    (5, 37, 12, 150),
+    (4, 96, 256, 128),
+    (2, 50, 30, 20),
+    (3, 42, 40, 33),
+    (700, 20, 1, 30),
+    (1, 8, 100000, 64),
+]
+
+TOL = {np.float32: 1e-5, np.float64: 1e-12}
+
+
+def _inputs(L, I, R, cols, dtype, seed):
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((L, I, R)).astype(dtype)
+    p = rng.standard_normal((L, cols, R)).astype(dtype)
+    q = rng.standard_normal((I, cols)).astype(dtype)
+    return x, p, q
+
+
+def _check(out, ref, ref_abs, dtype):
+    err = np.linalg.norm(out.astype(np.float64) - ref) / max(np.linalg.norm(ref), 1e-300)
+    assert err < TOL[dtype], f"normwise relative error {err:.3e}"
+    elem = np.max(np.abs(out.astype(np.float64) - ref) / np.maximum(ref_abs, 1e-300))
+    assert elem < 50 * TOL[dtype], f"elementwise error / (|x||p|) {elem:.3e}"
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("view", VIEWS)
+def test_sketch_pass(rcp, view, dtype):
+    L, I, R, cols = view
+    x, p, _ = _inputs(L, I, R, cols, dtype, 11)
+    out = rcp.stream_pass("sketch", x, p, cols)
+    assert out.shape == (I, cols)
+    xd, pd = x.astype(np.float64), p.astype(np.float64)
+    ref = np.einsum("aib,acb->ic", xd, pd)
+    ref_abs = np.einsum("aib,acb->ic", np.abs(xd), np.abs(pd))
+    _check(out, ref, ref_abs, dtype)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("view", VIEWS)
+def test_project_pass(rcp, view, dtype):
+    L, I, R, cols = view
+    x, _, q = _inputs(L, I, R, cols, dtype, 12)
+    out = rcp.stream_pass("project", x, q, cols)
+    assert out.shape == (L, cols, R)
+    xd, qd = x.astype(np.float64), q.astype(np.float64)
+    ref = np.einsum("aib,ic->acb", xd, qd)
+    ref_abs = np.einsum("aib,ic->acb", np.abs(xd), np.abs(qd))
+    _check(out, ref, ref_abs, dtype)
+
+
+def test_pass_scaled_inputs(rcp):
+    """Wide dynamic range: the lo plane must keep its own exponent (no flush)."""
+    L, I, R, cols = 1, 256, 512, 64
+    x, p, q = _inputs(L, I, R, cols, np.float32, 13)
+    x *= np.float32(1e-20)
+    p *= np.float32(1e15)
+    q *= np.float32(1e15)
+    out = rcp.stream_pass("sketch", x, p, cols)
+    ref = np.einsum("aib,acb->ic", x.astype(np.float64), p.astype(np.float64))
+    assert np.linalg.norm(out - ref) / np.linalg.norm(ref) < 1e-5
+    out = rcp.stream_pass("project", x, q, cols)
+    ref = np.einsum("aib,ic->acb", x.astype(np.float64), q.astype(np.float64))
+    assert np.linalg.norm(out - ref) / np.linalg.norm(ref) < 1e-5
+
+
+def test_pass_deterministic(rcp):
+    x, p, q = _inputs(2, 300, 2000, 70, np.float32, 14)
+    a = rcp.stream_pass("sketch", x, p, 70)
+    b = rcp.stream_pass("sketch", x, p, 70)
+    assert np.array_equal(a, b)
+    a = rcp.stream_pass("project", x, q, 70)
+    b = rcp.stream_pass("project", x, q, 70)
+    assert np.array_equal(a, b)
