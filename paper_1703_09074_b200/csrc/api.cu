@@ -64,6 +64,8 @@ struct PassRecord {
 
 }  // namespace
 
+struct rcpg_compressed;
+
 struct rcpg_context {
   int device = 0;
   cudaStream_t st = nullptr;
@@ -78,6 +80,9 @@ struct rcpg_context {
   double* hslots = nullptr;  // pinned mirror of the device check slots (c->nrm)
   size_t pass_used = 0;
   bool timing = true;
+  // decompose's compressed tensor + bases: kept across calls so repeated
+  // decompositions reuse its buffers (a cudaFree per call drains the device)
+  rcpg_compressed* dcomp = nullptr;
 };
 
 struct rcpg_tensor {
@@ -295,8 +300,13 @@ void run_compress(rcpg_context* c, const rcpg_tensor* t, const CompressCfg& cfg,
   for (int m = 0; m < order; ++m) shape[m] = t->shape[m];
   const T* cur = static_cast<const T*>(t->d);
   int which = 0;
-  out->bases.clear();
-  out->bases.resize(order);
+  // keep existing basis buffers (reused across calls); reset their metadata
+  if (out->bases.size() < size_t(order)) out->bases.resize(size_t(order));
+  for (auto& b : out->bases) {
+    b.identity = true;
+    b.dim = b.cols = 0;
+    b.rank_warning = false;
+  }
 
   for (int n = 0; n < order; ++n) {
     const i64 extent = shape[n];
@@ -628,7 +638,8 @@ void run_decompose(rcpg_context* c, const rcpg_tensor* t, const rcpg_decompose_c
   CompressCfg cc = to_cfg(cfg.compress);
   if (cc.target_rank == 0) cc.target_rank = cfg.rank;
   check_arg(cc.target_rank == cfg.rank, "decompose: compression target rank must equal the CP rank");
-  rcpg_compressed comp;
+  if (c->dcomp == nullptr) c->dcomp = new rcpg_compressed();
+  rcpg_compressed& comp = *c->dcomp;
   run_compress<T>(c, t, cc, &comp, dfr, /*sync_checks=*/false);
   AlsHandles<T> h = run_als<T>(c, comp.data.as<T>(), comp.shape, comp.order, cfg, dfr);
   // recover (kruskal.hpp:198-220): A_n = Q_n A~_n, then normalize
@@ -740,6 +751,7 @@ void rcpg_destroy(rcpg_context* c) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
   }
+  delete c->dcomp;
   for (DevBuf* b : {&c->panelA, &c->panelB, &c->work0, &c->work1, &c->Y, &c->Qy, &c->scratch, &c->keys, &c->cands,
                     &c->bar, &c->info, &c->part, &c->tau, &c->diag, &c->cqr, &c->als_f, &c->als_g, &c->als_w, &c->als_kr,
                     &c->als_work, &c->als_trace, &c->als_state, &c->weights, &c->small_tmp, &c->nrm, &c->als_part, &c->als_prof, &c->recov})
