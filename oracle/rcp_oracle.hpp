@@ -1018,6 +1018,9 @@ class SolverError : public std::runtime_error {
 // ascending, unit eigenvectors in the columns of `vec` (n x n, col-major).
 inline void sym_eig(int n, const double* a_in, double* evals, double* vec) {
   std::vector<double> a(a_in, a_in + std::size_t(n) * std::size_t(n));
+  // Eigen::SelfAdjointEigenSolver reads the lower triangle only (solve.hpp:65, 110)
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < j; ++i) a[std::size_t(i + j * n)] = a[std::size_t(j + i * n)];
   std::vector<double> v(std::size_t(n) * std::size_t(n), 0.0);
   for (int i = 0; i < n; ++i) v[std::size_t(i * n + i)] = 1.0;
   auto A = [&](int i, int j) -> double& { return a[std::size_t(i + j * n)]; };

@@ -79,6 +79,13 @@ __device__ void jacobi_eig(double* A, double* V, int n, double* evals, int* orde
   __shared__ int pp[kMaxRank * 8], pq[kMaxRank * 8];
   __shared__ int s_stop;
   const int tid = threadIdx.x, nt = blockDim.x;
+  // SelfAdjointEigenSolver (solve.hpp:65, 110) reads the lower triangle only:
+  // mirror it, so an input that is symmetric only up to rounding (a tensor-core
+  // Gram) is treated exactly like the reference treats it.
+  for (int e = tid; e < n * n; e += nt) {
+    const int i = e % n, j = e / n;
+    if (i < j) A[e] = A[j + i * n];
+  }
   for (int e = tid; e < n * n; e += nt) V[e] = (e % n == e / n) ? 1.0 : 0.0;
   __syncthreads();
   const int m = n + (n & 1);  // players (one dummy when n is odd)
