@@ -1,3 +1,25 @@
+__device__ void sign_reconstruct(double* G, int n, int ld, int rows, double* sgn) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  for (int k = 0; k < n; ++k) {
+    const double sk = (G[k + k * ld] > 0.0) != (k == rows - 1) ? -1.0 : 1.0;
+    __syncthreads();
+    for (int i = tid; i < n; i += nt)
+      if (i != k && sk < 0.0) G[i + k * ld] = -G[i + k * ld];
+    if (tid == 0) {
+      G[k + k * ld] = sk * G[k + k * ld] - 1.0;
+      sgn[k] = sk;
+    }
+    __syncthreads();
+    const double rdkk = 1.0 / G[k + k * ld];
+    for (int j = k + 1 + wid; j < n; j += nw) {  // warp per column, lanes over rows
+      const double gkj = G[k + j * ld] * rdkk;
+      for (int i = k + 1 + lane; i < n; i += 32) G[i + j * ld] -= G[i + k * ld] * gkj;
+    }
+    __syncthreads();
+  }
+}
+
 // SPDX-License-Identifier: MIT
 // Tall-skinny factorizations of the power-iteration chain (SURVEY.md §2.2
 // K5/K6/K8), restating the reference's Eigen calls:
@@ -23,6 +45,10 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+
+#include <cstdio>
+#include <cstdlib>
+#include <string>
 
 #include "factor.cuh"
 #include "runtime.cuh"
@@ -901,7 +927,9 @@ __global__ void __launch_bounds__(kCqrThreads) cqr2_kernel(const T* __restrict__
   for (int e = tid; e < n * n; e += nt) G[e] = work[(e % n) + i64(e / n) * I];
   __syncthreads();
   for (int k = 0; k < n; ++k) {
-    if (tid == 0) sgn[k] = G[k + k * n] > 0.0 ? -1.0 : 1.0;
+    // Eigen's Householder leaves the last column of a square panel unreflected
+    // (empty tail: tau = 0, beta = c0), so its sign is the opposite one
+    if (tid == 0) sgn[k] = (G[k + k * n] > 0.0) != (k == I - 1) ? -1.0 : 1.0;
     __syncthreads();
     const double sk = sgn[k];
     if (sk < 0.0)
@@ -924,6 +952,267 @@ __global__ void __launch_bounds__(kCqrThreads) cqr2_kernel(const T* __restrict__
     }
     if (rank_warning) *rank_warning = (dmax == T(0)) || (dmin <= T(I) * Traits<T>::eps * dmax);
     *status = 0;
+  }
+}
+
+// ------------------------------------------------ CholeskyQR2, all SMs
+// Small dense steps shared by the CholeskyQR2 kernels, one CTA, matrices in
+// shared memory with an odd leading dimension ld (bank spread):
+//   chol_inv_small: upper Cholesky A = R^T R (right-looking, in place in A's
+//     upper triangle), dg[j] = R(j, j), then X = R^{-1} (upper), *fail on breakdown;
+//   sign_reconstruct: signs of Eigen's HouseholderQR Q relative to the
+//     CholeskyQR Q from the top n x n block (modified LU of Q_top - S).
+__device__ void chol_inv_small(double* A, double* X, int n, int ld, double* dg, int* fail) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  for (int j = 0; j < n; ++j) {
+    if (tid == 0) {
+      const double d = A[j + j * ld];
+      if (!(d > 0.0)) *fail = 1;
+      const double piv = d > 0.0 ? sqrt(d) : 1.0;
+      A[j + j * ld] = piv;
+      dg[j] = piv;
+    }
+    __syncthreads();
+    const double rinv = 1.0 / A[j + j * ld];
+    for (int c = j + 1 + tid; c < n; c += nt) A[j + c * ld] *= rinv;
+    __syncthreads();
+    // trailing update of the upper triangle: warp per column c2, lanes over rows c1 <= c2
+    for (int c2 = j + 1 + wid; c2 < n; c2 += nw) {
+      const double r2 = A[j + c2 * ld];
+      for (int c1 = j + 1 + lane; c1 <= c2; c1 += 32) A[c1 + c2 * ld] -= A[j + c1 * ld] * r2;
+    }
+    __syncthreads();
+  }
+  // X = R^{-1}, upper: rows from the bottom, all columns j >= i in parallel
+  for (int e = tid; e < n * ld; e += nt) X[e] = 0.0;
+  __syncthreads();
+  for (int i = n - 1; i >= 0; --i) {
+    const double rii = 1.0 / A[i + i * ld];
+    for (int j = i + tid; j < n; j += nt) {
+      double s0 = (i == j) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int k = i + 1;
+      for (; k + 3 <= j; k += 4) {
+        s0 -= A[i + k * ld] * X[k + j * ld];
+        s1 -= A[i + (k + 1) * ld] * X[k + 1 + j * ld];
+        s2 -= A[i + (k + 2) * ld] * X[k + 2 + j * ld];
+        s3 -= A[i + (k + 3) * ld] * X[k + 3 + j * ld];
+      }
+      for (; k <= j; ++k) s0 -= A[i + k * ld] * X[k + j * ld];
+      X[i + j * ld] = ((s0 + s1) + (s2 + s3)) * rii;
+    }
+    __syncthreads();
+  }
+}
+
+// G: top n x n block of Q2 (ld), destroyed. rows = panel height (square
+// panels: Eigen leaves the last column unreflected, opposite sign).
+__device__ void sign_reconstruct(double* G, int n, int ld, int rows, double* sgn) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int k = 0; k < n; ++k) {
+    const double sk = (G[k + k * ld] > 0.0) != (k == rows - 1) ? -1.0 : 1.0;
+    __syncthreads();
+    for (int i = tid; i < n; i += nt)
+      if (i != k && sk < 0.0) G[i + k * ld] = -G[i + k * ld];
+    if (tid == 0) {
+      G[k + k * ld] = sk * G[k + k * ld] - 1.0;
+      sgn[k] = sk;
+    }
+    __syncthreads();
+    const double dkk = G[k + k * ld];
+    const int m = n - k - 1;
+    for (int e = tid; e < m * m; e += nt) {
+      const int i = k + 1 + e % m, j = k + 1 + e / m;
+      G[i + j * ld] -= (G[i + k * ld] / dkk) * G[k + j * ld];
+    }
+    __syncthreads();
+  }
+}
+
+// The same CholeskyQR2 + Householder sign reconstruction as cqr2_kernel,
+// spread over a cooperative grid: each CTA keeps a contiguous chunk of rows
+// of V in shared memory (fp64) for both passes; the Gram is accumulated per
+// CTA in 4x4 register blocks of the upper triangle and reduced in fixed CTA
+// order (deterministic); CTA 0 factors it (Cholesky, R^{-1}) while the grid
+// waits; V <- V R^{-1} is parallel over (row, column). Workspace (doubles):
+// part [G][NB(NB+1)/2][16] | Gram n*n | R^{-1} n*n | top n*n | sgn n | dg 2n.
+constexpr int kCqrCoopThreads = 256;
+
+template <typename T>
+struct CqrCoopArgs {
+  const T* Y;
+  T* Q;
+  int I, n, rows_per;  // rows_per: chunk of rows per CTA
+  double* work;
+  GridBarrier* bar;
+  int* status;
+  int* rank_warning;
+  unsigned long long* prof;  // optional phase stamps (RCPG_PROFILE_QR)
+};
+
+__device__ __forceinline__ void cqr_stamp(unsigned long long* prof, int slot) {
+  if (prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    prof[slot] = t;
+  }
+}
+
+__host__ __device__ inline int cqr_nb(int n) { return (n + 3) / 4; }
+
+template <typename T>
+__global__ void __launch_bounds__(kCqrCoopThreads) cqr2_coop_kernel(CqrCoopArgs<T> p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int n = p.n, NB = cqr_nb(n), n4 = 4 * NB, NP = NB * (NB + 1) / 2;
+  const int ld = p.rows_per + 1;                                 // odd column stride: fewer bank conflicts
+  double* V = reinterpret_cast<double*>(smem_raw);              // [n4][ld] own rows, column-major
+  double* Ri = V + i64(n4) * ld;                                // n x n R^{-1} (upper), or scratch
+  __shared__ int s_fail;
+  __shared__ double dg_loc[2 * kMaxPanelCols];  // diagonals of R1, R2 (this CTA's copy)
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int r0 = blockIdx.x * p.rows_per;
+  const int rows = max(0, min(p.rows_per, p.I - r0));
+  double* part = p.work;
+  double* Gf = part + i64(gridDim.x) * NP * 16;
+  double* Rg = Gf + n * n;
+  double* top = Rg + n * n;
+  double* sgn = top + n * n;
+  double* dg = sgn + n;
+
+  for (int e = tid; e < n4 * ld; e += nt) {
+    const int i = e % ld, j = e / ld;
+    V[e] = (i < rows && j < n) ? double(p.Y[(r0 + i) + i64(j) * p.I]) : 0.0;
+  }
+  if (tid == 0) s_fail = 0;
+  __syncthreads();
+  cqr_stamp(p.prof, 0);
+
+  for (int pass = 0; pass < 2; ++pass) {
+    // 1. partial Gram of own rows, 4x4 blocks (A <= B) of the upper triangle
+    for (int pb = tid; pb < NP; pb += nt) {
+      int B = int((sqrt(8.0 * pb + 1.0) - 1.0) * 0.5);
+      while (B * (B + 1) / 2 > pb) --B;
+      while ((B + 1) * (B + 2) / 2 <= pb) ++B;
+      const int A = pb - B * (B + 1) / 2;
+      double acc[4][4] = {};
+      const double* va = V + i64(4 * A) * ld;
+      const double* vb = V + i64(4 * B) * ld;
+      for (int i = 0; i < rows; ++i) {
+        double x[4], y[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          x[u] = va[u * ld + i];
+          y[u] = vb[u * ld + i];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u][v] += x[u] * y[v];
+      }
+      double* dst = part + (i64(blockIdx.x) * NP + pb) * 16;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) dst[u * 4 + v] = acc[u][v];
+    }
+    cqr_stamp(p.prof, 1 + 5 * pass);
+    grid_sync(p.bar);
+    // 2. reduce the partials in CTA order; scatter into the full symmetric Gram
+    for (i64 e = blockIdx.x * i64(nt) + tid; e < i64(NP) * 16; e += i64(gridDim.x) * nt) {
+      const int pb = int(e / 16), uv = int(e % 16);
+      double s = 0.0;
+      for (int q = 0; q < int(gridDim.x); ++q) s += ldcg(&part[(i64(q) * NP + pb) * 16 + uv]);
+      int B = int((sqrt(8.0 * pb + 1.0) - 1.0) * 0.5);
+      while (B * (B + 1) / 2 > pb) --B;
+      while ((B + 1) * (B + 2) / 2 <= pb) ++B;
+      const int A = pb - B * (B + 1) / 2;
+      const int a = 4 * A + uv / 4, b = 4 * B + uv % 4;
+      if (a < n && b < n && a <= b) {
+        Gf[a + b * n] = s;
+        Gf[b + a * n] = s;
+      }
+    }
+    cqr_stamp(p.prof, 2 + 5 * pass);
+    grid_sync(p.bar);
+    // 3. every CTA factors the (identical) Gram itself: upper Cholesky, R^{-1}
+    //    (deterministic, so all CTAs agree; no barrier, nobody waits on CTA 0)
+    const int ldn = n + 1;
+    double* As = Ri;              // n x ldn Gram -> R
+    double* Xs = Ri + n * ldn;    // n x ldn R^{-1}
+    for (int e = tid; e < n * n; e += nt) As[(e % n) + (e / n) * ldn] = ldcg(&Gf[e]);
+    __syncthreads();
+    chol_inv_small(As, Xs, n, ldn, dg_loc + pass * n, &s_fail);
+    if (blockIdx.x == 0)
+      for (int j = tid; j < n; j += nt) dg[pass * n + j] = dg_loc[pass * n + j];
+    cqr_stamp(p.prof, 3 + 5 * pass);
+    if (s_fail) {  // Cholesky broke down (same verdict in every CTA): Householder runs instead
+      if (blockIdx.x == 0 && tid == 0) *p.status = 1;
+      return;
+    }
+    // 4. V <- V R^{-1} (own rows): out(i, j) = sum_{k <= j} V(i, k) Ri(k, j)
+    {
+      double* out = Xs + n * ldn;  // [n][ld] staging, then copied back over V
+      for (int e = tid; e < n * rows; e += nt) {
+        const int i = e % rows, j = e / rows;
+        double s = 0.0;
+        for (int k = 0; k <= j; ++k) s += V[k * ld + i] * Xs[k + j * ldn];
+        out[j * ld + i] = s;
+      }
+      __syncthreads();
+      for (int e = tid; e < n * rows; e += nt) {
+        const int i = e % rows, j = e / rows;
+        V[j * ld + i] = out[j * ld + i];
+      }
+      __syncthreads();
+    }
+    cqr_stamp(p.prof, 4 + 5 * pass);
+  }
+  // conditioning guard (CholeskyQR2 only well inside its stable range); every
+  // CTA evaluates it on its own (identical) diagonals
+  {
+    __shared__ int s_bad;
+    if (tid == 0) {
+      double mx = 0.0, mn = INFINITY;
+      for (int j = 0; j < n; ++j) {
+        mx = fmax(mx, dg_loc[j]);
+        mn = fmin(mn, dg_loc[j]);
+      }
+      s_bad = (!(mn > 0.0) || mx / mn > 1e6) ? 1 : 0;
+    }
+    __syncthreads();
+    if (s_bad) {
+      if (blockIdx.x == 0 && tid == 0) *p.status = 1;
+      return;
+    }
+  }
+  // rows < n of Q2 -> top (for the sign reconstruction)
+  for (int e = tid; e < n * rows; e += nt) {
+    const int i = e % rows, j = e / rows;
+    if (r0 + i < n) top[(r0 + i) + j * n] = V[j * ld + i];
+  }
+  grid_sync(p.bar);
+  cqr_stamp(p.prof, 11);
+  // every CTA reconstructs the Householder signs from the top block itself
+  const int ldn = n + 1;
+  double* Gs = Ri;
+  __shared__ double sg[kMaxPanelCols];
+  for (int e = tid; e < n * n; e += nt) Gs[(e % n) + (e / n) * ldn] = ldcg(&top[e]);
+  __syncthreads();
+  sign_reconstruct(Gs, n, ldn, p.I, sg);
+  cqr_stamp(p.prof, 12);
+  if (blockIdx.x == 0 && tid == 0) {
+    T dmax = T(0), dmin = T(INFINITY);
+    for (int j = 0; j < n; ++j) {
+      const T d = T(dg[j] * dg[n + j]);
+      dmax = d > dmax ? d : dmax;
+      dmin = d < dmin ? d : dmin;
+    }
+    if (p.rank_warning) *p.rank_warning = (dmax == T(0)) || (dmin <= T(p.I) * Traits<T>::eps * dmax);
+    *p.status = 0;
+  }
+  for (int e = tid; e < n * rows; e += nt) {
+    const int i = e % rows, j = e / rows;
+    p.Q[(r0 + i) + i64(j) * p.I] = T(V[j * ld + i] * sg[j]);
   }
 }
 
@@ -1008,7 +1297,7 @@ __global__ void __launch_bounds__(kCqrThreads) cqr2_smem_kernel(const T* __restr
   __syncthreads();
   for (int k = 0; k < n; ++k) {  // sign reconstruction (modified LU of Q_top - S)
     if (tid == 0) {
-      sgn[k] = G[k + k * n] > 0.0 ? -1.0 : 1.0;
+      sgn[k] = (G[k + k * n] > 0.0) != (k == I - 1) ? -1.0 : 1.0;  // square panel: see cqr2_kernel
       if (sgn[k] < 0.0)
         for (int i = 0; i < n; ++i) G[i + k * n] = -G[i + k * n];
       G[k + k * n] -= 1.0;
@@ -1116,12 +1405,54 @@ int thin_qr(T* A, T* Q, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w, 
   static const size_t cq_lim = enable_max_dyn_smem(cqr2_kernel<T>);
   static const size_t cqs_lim = enable_max_dyn_smem(cqr2_smem_kernel<T>);
   const size_t cqs_smem = (size_t(J) * n + 2 * size_t(n) * n + 3 * size_t(n)) * sizeof(double);
-  if (R == J && kolda_identity && J >= n && cqs_smem <= cqs_lim) {
+  // CholeskyQR2 over all SMs for panels too tall for one SM to factor quickly
+  static const size_t cc_lim = enable_max_dyn_smem(cqr2_coop_kernel<T>);
+  const int nb4 = 4 * cqr_nb(n);
+  const char* qp = std::getenv("RCPG_QR_PATH");  // A/B testing: smem | global | coop | householder
+  const std::string path = qp ? qp : "";
+  bool done = false;
+  if (R == J && kolda_identity && J >= n && w.cqr_work != nullptr && path != "smem" && path != "global" &&
+      path != "householder" && (path == "coop" || J * n >= 4096)) {
+    const int maxc = max_coop_blocks(cqr2_coop_kernel<T>, kCqrCoopThreads, cc_lim);
+    // >= 32 rows per CTA; the chunk (plus 2 n x n fp64) must fit in shared memory
+    int rows_per = int(std::max<i64>(32, ceil_div(J, i64(std::min(maxc, w.max_blocks)))));
+    // V chunk [4 NB][rp + 1] | R, R^{-1} [n][n + 1] each | staging [n][rp + 1]  (doubles)
+    auto smem_of = [&](int rp) {
+      return (size_t(nb4) * (rp + 1) + 2 * size_t(n) * (n + 1) + size_t(n) * (rp + 1)) * 8;
+    };
+    const int G = int(ceil_div(J, i64(rows_per)));
+    const size_t need = (size_t(G) * (cqr_nb(n) * (cqr_nb(n) + 1) / 2) * 16 + 3 * size_t(n) * n + 3 * size_t(n)) * 8;
+    if (smem_of(rows_per) <= cc_lim && G <= maxc && need <= size_t(2) * w.cqr_rows * kMaxPanelCols * 8) {
+      static unsigned long long* qprof = nullptr;
+      const bool want_prof = std::getenv("RCPG_PROFILE_QR") != nullptr;
+      if (want_prof && qprof == nullptr) RCPG_CUDA(cudaMalloc(&qprof, 16 * sizeof(unsigned long long)));
+      CqrCoopArgs<T> a{A, Q, int(J), n, rows_per, w.cqr_work, w.bar, w.info + 2, rank_warning_dev,
+                       want_prof ? qprof : nullptr};
+      launch_coop(cqr2_coop_kernel<T>, G, kCqrCoopThreads, smem_of(rows_per), st, a);
+      RCPG_LAUNCHED();
+      if (want_prof) {
+        unsigned long long h[16];
+        RCPG_CUDA(cudaMemcpyAsync(h, qprof, sizeof(h), cudaMemcpyDeviceToHost, st));
+        RCPG_CUDA(cudaStreamSynchronize(st));
+        fprintf(stderr, "[rcpg qr] %lldx%d G=%d rows/CTA=%d us:", (long long)J, n, G, rows_per);
+        const char* nm[] = {"gram0", "red0", "chol0", "apply0", "-", "gram1", "red1", "chol1", "apply1", "top", "sign"};
+        const int at[] = {1, 2, 3, 4, -1, 6, 7, 8, 9, 11, 12};
+        const int from[] = {0, 1, 2, 3, -1, 4, 6, 7, 8, 9, 11};
+        for (int q = 0; q < 11; ++q)
+          if (at[q] >= 0) fprintf(stderr, " %s %.1f", nm[q], (h[at[q]] - h[from[q]]) * 1e-3);
+        fprintf(stderr, "\n");
+      }
+      skip = w.info + 2;
+      done = true;
+    }
+  }
+  if (done) {
+  } else if (R == J && kolda_identity && J >= n && cqs_smem <= cqs_lim && path != "global" && path != "householder") {
     cqr2_smem_kernel<T><<<1, kCqrThreads, cqs_smem, st>>>(A, Q, int(J), n, w.info + 2, rank_warning_dev);
     count_launch();
     RCPG_LAUNCHED();
     skip = w.info + 2;
-  } else if (R == J && kolda_identity && J >= n && J <= w.cqr_rows && cq_smem <= cq_lim) {
+  } else if (R == J && kolda_identity && J >= n && J <= w.cqr_rows && cq_smem <= cq_lim && path != "householder") {
     cqr2_kernel<T><<<1, kCqrThreads, cq_smem, st>>>(A, Q, int(J), n, w.cqr_work, w.info + 2, rank_warning_dev);
     count_launch();
     RCPG_LAUNCHED();
