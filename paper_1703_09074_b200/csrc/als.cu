@@ -836,7 +836,8 @@ __global__ void norm_finite_kernel(const T* x, i64 n, double* part) {
 }
 
 // Fixed-order (deterministic) sum of nblocks (a, b) pairs by one CTA.
-__global__ void sum_pairs_kernel(const double* part, int nblocks, double* out) {
+__global__ void sum_pairs_kernel(const double* part, int nblocks, double* out, const int* skip = nullptr) {
+  if (skip != nullptr && *skip) return;
   double a = 0.0, b = 0.0;
   for (int q = threadIdx.x; q < nblocks; q += blockDim.x) {
     a += part[2 * q];
@@ -859,7 +860,8 @@ constexpr int kResRows = 16;
 // all 16 rows.
 template <typename T>
 __global__ void __launch_bounds__(256) residual_kernel(const T* X, ShapeArg sh, FactorSet<T> fs, const T* w,
-                                                       double* part) {
+                                                       double* part, const int* skip = nullptr) {
+  if (skip != nullptr && *skip) return;
   __shared__ T coef[kMaxRank][kResRows];
   __shared__ int dig[kResRows][kMaxOrder];
   __shared__ const T* fptr[kMaxOrder];

@@ -87,6 +87,7 @@ void residual_norms(const T* X, const i64* shape, int order, const FactorSet<T>&
                     double* out2, double* scratch, int num_sms, cudaStream_t st);
 size_t residual_scratch_doubles(int num_sms);
 
+
 // Dense reconstruction of a model given in double + add_noise (synthetic data).
 template <typename T>
 void synth_tensor(const i64* shape, int order, int rank, const double* w_dev, const double* const* f_dev,

@@ -579,6 +579,8 @@ void run_relerr(rcpg_context* c, const T* X, const i64* shape, int order, const 
   for (int m = 0; m < order; ++m) S *= shape[m];
   c->scratch.ensure(residual_scratch_doubles(sms) * sizeof(double));
   {
+    // exact streamed residual: the Gram form ||X||^2 - 2<X,Xhat> + ||Xhat||^2
+    // cancels badly in fp32 (a fp32-accumulated MTTKRP over ~10^6 terms)
     ScopedPass sp(c, "relerr", double(S) * sizeof(T));
     residual_norms<T>(X, shape, order, fs, w, slots(c) + kResid, c->scratch.as<double>(), sms, c->st);
   }

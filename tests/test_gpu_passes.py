@@ -91,3 +91,24 @@ def test_pass_deterministic(rcp):
     a = rcp.stream_pass("project", x, q, 70)
     b = rcp.stream_pass("project", x, q, 70)
     assert np.array_equal(a, b)
+
+
+# ------------------------------------------------------- relative error
+# kruskal.hpp:187-194: ||X - Xhat|| / ||X||, accumulated in fp64, for a visible residual and
+# for a near-exact model (where a Gram-form evaluation would cancel).
+@pytest.mark.parametrize("dtype,tol", [(np.float64, 1e-10), (np.float32, 1e-4)])
+@pytest.mark.parametrize("shape,rank", [((40, 30, 20), 5), ((64, 48, 32), 12), ((9, 130, 17), 3)])
+def test_relative_error_gram_and_exact(rcp, dtype, tol, shape, rank):
+    rng = np.random.default_rng(sum(shape))
+    fac = [rng.standard_normal((n, rank)).astype(dtype).astype(np.float64) for n in shape]
+    w = np.linspace(1.0, 2.0, rank).astype(dtype).astype(np.float64)
+    xh = np.einsum("r,ir,jr,kr->ijk", w, *fac)
+    for noise in (0.3, 1e-7):
+        x = (xh + noise * np.linalg.norm(xh) / np.sqrt(xh.size) * rng.standard_normal(shape)).astype(dtype)
+        want = np.linalg.norm(x.astype(np.float64) - xh) / np.linalg.norm(x.astype(np.float64))
+        k = rcp.Kruskal(weights=w.astype(dtype), factors=[f.astype(dtype) for f in fac])
+        got = rcp.relative_error(x, k)
+        if noise > 1e-3:
+            assert abs(got - want) <= tol * want, (got, want)
+        else:
+            assert abs(got - want) <= (1e-12 if dtype == np.float64 else 2e-6), (got, want)
