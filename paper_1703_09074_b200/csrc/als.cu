@@ -316,8 +316,9 @@ __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T
   double* X = A + R * R;     // R x R: eigenvectors (fallback)
   double* ev = X + R * R;    // R
   int* ord = reinterpret_cast<int*>(ev + R);
-  double* Fs = ev + 2 * R;   // I x R new factor (double, smem)
-  double* nr = Fs + i64(I) * R;  // R column norms
+  const int ldf = I | 1;     // odd leading dimension: column-strided reads spread over the banks
+  double* Fs = ev + 2 * R;   // I x R new factor (double, smem, leading dimension ldf)
+  double* nr = Fs + i64(ldf) * R;  // R column norms
   __shared__ int s_ok;
   unsigned long long _tlast = 0;
   if (g_als_prof && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_tlast));
@@ -339,19 +340,28 @@ __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T
   double* dst = X;
   const int lane0 = tid & 31, wid0 = tid >> 5, nw0 = nt >> 5;
   for (int k = 0; k < R; ++k) {
-    const double p = src[k + k * R];
+    // restrict-qualified with the pivot column hoisted: without it every
+    // store may alias the next column's loads and the step serializes
+    const double* __restrict__ sp = src;
+    double* __restrict__ dp = dst;
+    const double p = sp[k + k * R];
     const double ip = 1.0 / p;
+    const double aik0 = lane0 < R ? sp[lane0 + k * R] : 0.0;
+    const double aik1 = lane0 + 32 < R ? sp[lane0 + 32 + k * R] : 0.0;
     for (int j = wid0; j < R; j += nw0) {
-      const double akj = src[k + j * R] * ip;
-      for (int i = lane0; i < R; i += 32) {
-        const double aik = src[i + k * R];
-        double v;
-        if (j != k)
-          v = (i != k) ? src[i + j * R] - aik * akj : akj;
-        else
-          v = (i != k) ? -aik * ip : ip;
-        dst[i + j * R] = v;
+      const double akj = sp[k + j * R] * ip;
+      const double s0 = lane0 < R ? sp[lane0 + j * R] : 0.0;
+      const double s1 = lane0 + 32 < R ? sp[lane0 + 32 + j * R] : 0.0;
+      double v0, v1;
+      if (j != k) {
+        v0 = (lane0 != k) ? s0 - aik0 * akj : akj;
+        v1 = (lane0 + 32 != k) ? s1 - aik1 * akj : akj;
+      } else {
+        v0 = (lane0 != k) ? -aik0 * ip : ip;
+        v1 = (lane0 + 32 != k) ? -aik1 * ip : ip;
       }
+      if (lane0 < R) dp[lane0 + j * R] = v0;
+      if (lane0 + 32 < R) dp[lane0 + 32 + j * R] = v1;
     }
     if (tid == 0 && !(p > 0.0)) s_ok = 0;
     __syncthreads();
@@ -398,19 +408,32 @@ __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T
   }
   ALS_STAMP(9);
   // 3. F = W pinv(V), rounded to Scalar like the reference's factor
-  for (int r = wid0; r < R; r += nw0)
-    for (int i = lane0; i < I; i += 32) {
-      double s = 0.0;
-      for (int k = 0; k < R; ++k) s += double(W[i + k * I]) * Pm[k + r * R];
-      Fs[i + r * I] = double(T(s));
-    }
+  {
+    // each lane: rows lane, lane + 32, ... as independent accumulation chains
+    // (per output the k order is unchanged)
+    const WT* __restrict__ Wr = W;
+    const double* __restrict__ Pr = Pm;
+    for (int r = wid0; r < R; r += nw0)
+      for (int i0 = lane0; i0 < I; i0 += 128) {
+        double s[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int k = 0; k < R; ++k) {
+          const double pk = Pr[k + r * R];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (i0 + 32 * u < I) s[u] += double(Wr[i0 + 32 * u + k * I]) * pk;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (i0 + 32 * u < I) Fs[i0 + 32 * u + r * ldf] = double(T(s[u]));
+      }
+  }
   __syncthreads();
   ALS_STAMP(10);
   // 4. column norms; weights from the last mode (solve.hpp:215-229)
   const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
   for (int r = wid; r < R; r += nw) {
     double s = 0.0;
-    for (int i = lane; i < I; i += 32) s += Fs[i + r * I] * Fs[i + r * I];
+    for (int i = lane; i < I; i += 32) s += Fs[i + r * ldf] * Fs[i + r * ldf];
     s = warp_sum(s);
     if (lane == 0) {
       const T nrm = T(sqrt(s));
@@ -422,21 +445,46 @@ __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T
   for (int r = wid0; r < R; r += nw0) {
     const T nrm = T(nr[r]);
     for (int i = lane0; i < I; i += 32) {
-      const int e = i + r * I;
+      const int e = i + r * ldf;
       const T v = nrm > T(0) ? T(Fs[e]) / nrm : T(Fs[e]);
       Fs[e] = double(v);
-      F[e] = v;
+      F[i + r * I] = v;
     }
   }
   __syncthreads();
   ALS_STAMP(11);
   // 5. Gram of the new factor
-  for (int e = tid; e < R2; e += nt) {
-    const int a = e % R, b = e / R;
-    double s = 0.0;
-    for (int i = 0; i < I; ++i) s += Fs[i + a * I] * Fs[i + b * I];
-    fs.gram[mode][e] = T(s);
-    V[e] = double(T(s));  // this mode's Gram, for the fit
+  {
+    // pairs a <= b (the product is symmetric: same value, same summation
+    // order), four pairs per thread as independent chains
+    const double* __restrict__ Fr = Fs;
+    const int NPR = R * (R + 1) / 2;
+    for (int q0 = tid; q0 < NPR; q0 += 4 * nt) {
+      int pa[4], pb[4];
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int q = q0 + u * nt;
+        int b = int((sqrt(8.0 * q + 1.0) - 1.0) * 0.5);
+        while (b * (b + 1) / 2 > q) --b;
+        while ((b + 1) * (b + 2) / 2 <= q) ++b;
+        pb[u] = q < NPR ? b : 0;
+        pa[u] = q < NPR ? q - b * (b + 1) / 2 : 0;
+      }
+      for (int i = 0; i < I; ++i) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] += Fr[i + pa[u] * ldf] * Fr[i + pb[u] * ldf];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (q0 + u * nt >= NPR) continue;
+        const T g = T(acc[u]);
+        fs.gram[mode][pa[u] + pb[u] * R] = g;
+        fs.gram[mode][pb[u] + pa[u] * R] = g;
+        V[pa[u] + pb[u] * R] = double(g);  // this mode's Gram, for the fit
+        V[pb[u] + pa[u] * R] = double(g);
+      }
+    }
   }
   __syncthreads();
   ALS_STAMP(12);
@@ -452,7 +500,7 @@ __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T
   }
   m2 = block_reduce_sum(m2);
   double xi = 0.0;
-  for (int e = tid; e < I * R; e += nt) xi += double(W[e]) * Fs[e] * nr[e / I];
+  for (int e = tid; e < I * R; e += nt) xi += double(W[e]) * Fs[(e % I) + (e / I) * ldf] * nr[e / I];
   xi = block_reduce_sum(xi);
   if (tid == 0) {
     const double model2 = m2 > 0.0 ? m2 : 0.0;
@@ -629,12 +677,14 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
       grid_sync(p.bar);
       unsigned long long tp2 = 0;
       if (p.prof && g == 0 && tid == 0) tp2 = gtimer();
-      // ---- B: reduce + mode update on CTA 0
-      if (g == 0) {
-        double* W = sm;                   // I x R
-        double* work = sm + nout;         // 3 R^2 + 4 R
+      // ---- reduction of the partials, spread over all CTAs (fixed CTA
+      //      order per output: deterministic), into Wg after the partials
+      double* Wg = p.part + 2 * i64(G) * p.part_stride;
+      {
         const double* pp0 = p.part + i64(parity) * G * p.part_stride;
-        for (int o = tid; o < nout; o += nt) {
+        const int ch = (nout + G - 1) / G;
+        const int o1 = min(nout, (g + 1) * ch);
+        for (int o = g * ch + tid; o < o1; o += nt) {
           double s = 0.0;
           int q = 0;
           for (; q + 4 <= G; q += 4) {
@@ -648,8 +698,15 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
             s += v3;
           }
           for (; q < G; ++q) s += ldcg(&pp0[i64(q) * p.part_stride + o]);
-          W[o] = s;
+          Wg[o] = s;
         }
+      }
+      grid_sync(p.bar);
+      // ---- B: mode update on CTA 0
+      if (g == 0) {
+        double* W = sm;                   // I x R
+        double* work = sm + nout;         // 3 R^2 + 4 R
+        for (int o = tid; o < nout; o += nt) W[o] = ldcg(&Wg[o]);
         __syncthreads();
         if (p.prof && tid == 0) {
           g_als_prof = p.prof;
@@ -1031,7 +1088,7 @@ bool als_loop_supported(const i64* shape, int order, int rank) {
     for (int k = 0; k < order; ++k)
       if (k != m) fac += shape[k] * rank;
     const size_t smA = (size_t(kAlsBatch) * shape[m] + size_t(kAlsBatch) * rank + size_t(fac)) * sizeof(double);
-    const size_t smB = (2 * size_t(shape[m]) * rank + 3 * size_t(rank) * rank + 5 * size_t(rank)) * sizeof(double);
+    const size_t smB = (2 * size_t(shape[m]) * rank + 3 * size_t(rank) * rank + 6 * size_t(rank)) * sizeof(double);
     if (std::max(smA, smB) > 180 * 1024) return false;
   }
   return true;
@@ -1052,14 +1109,14 @@ void als_loop(const T* B, const i64* shape, int order, const FactorSet<T>& fs, T
     for (int k = 0; k < order; ++k)
       if (k != m) fac += shape[k] * R;
     const size_t smA = (size_t(kAlsBatch) * shape[m] + size_t(kAlsBatch) * R + size_t(fac)) * sizeof(double);
-    const size_t smB = (2 * size_t(shape[m]) * R + 3 * size_t(R) * R + 5 * size_t(R)) * sizeof(double);
+    const size_t smB = (2 * size_t(shape[m]) * R + 3 * size_t(R) * R + 6 * size_t(R)) * sizeof(double);
     smem = std::max(smem, std::max(smA, smB));
   }
   static const size_t lim = enable_max_dyn_smem(als_loop_kernel<T>);
   if (smem > lim) throw std::runtime_error("als_loop: shared memory plan too large");
   const int maxc = max_coop_blocks(als_loop_kernel<T>, kAlsThreads, smem);
   int G = int(std::max<i64>(1, std::min<i64>(ceil_div(maxJ, kAlsBatch), maxc)));
-  G = int(std::min<i64>(G, part_elems / (2 * maxout)));
+  G = int(std::min<i64>(G, part_elems / (2 * maxout) - 1));  // + one slot for the reduced W
   AlsLoopArgs<T> a{B, make_shape(shape, order), fs, weights, tol, max_iter, trace_fit, trace_sec, state, part,
                    maxout, bar, prof};
   launch_coop(als_loop_kernel<T>, G, kAlsThreads, smem, st, a);

@@ -535,6 +535,11 @@ AlsHandles<T> run_als(rcpg_context* c, const T* B, const i64* shape, int order, 
         fprintf(stderr, "[rcpg als] modes=%llu  A %.2f us  bar1 %.2f us  B %.2f us  bar2 %.2f us (per mode step)\n",
                 hp[4], hp[0] / 1e3 / double(hp[4]), hp[1] / 1e3 / double(hp[4]), hp[2] / 1e3 / double(hp[4]),
                 hp[3] / 1e3 / double(hp[4]));
+        const char* nm[] = {"reduceW", "GJ", "pinv-check", "F=W*Pm", "norms", "gram", "fit"};
+        const int sl[] = {14, 8, 9, 10, 11, 12, 13};
+        fprintf(stderr, "[rcpg als B]");
+        for (int q = 0; q < 7; ++q) fprintf(stderr, " %s %.2f", nm[q], hp[sl[q]] / 1e3 / double(hp[4]));
+        fprintf(stderr, " us (per mode step)\n");
       }
     } else {
       // general path (large extents / ranks): per-mode launches, enqueued in
