@@ -570,6 +570,34 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+constexpr int kAlsTiles = 8;  // 16x8 output tiles per warp: ceil(I/16) ceil(R/8) <= 8 warps x kAlsTiles
+
+__host__ __device__ constexpr int als_ld(int n) { return (n + 15) / 16 * 16 + 4; }
+
+template <typename T>
+__host__ __device__ constexpr i64 als_fib_doubles(i64 I) {  // [2][kAlsBatch][I] raw T, in doubles
+  return (2 * kAlsBatch * I * i64(sizeof(T)) + 15) / 16 * 2;
+}
+
+template <typename T>
+__device__ __forceinline__ void als_cp_elem(T* dst, const T* src, bool ok) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  if (sizeof(T) == 4)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "r"(ok ? 4 : 0));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(ok ? 8 : 0));
+}
+__device__ __forceinline__ void als_cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void als_cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void als_dmma(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+               : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+               : "d"(a0), "d"(a1), "d"(b0));
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p) {
   __shared__ int pidx[kAlsBatch * kMaxOrder];
@@ -590,15 +618,25 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
       const int nout = int(I) * R;
       unsigned long long tp0 = 0;
       if (p.prof && g == 0 && tid == 0) tp0 = gtimer();
-      // ---- A: partial MTTKRP over positions [j0, j1)
-      double acc[kAlsAcc];
+      // ---- A: partial MTTKRP over positions [j0, j1): W_part = Fib^T KC on
+      //      the FP64 tensor cores (mma.m16n8k4, M = i, N = r, K = positions);
+      //      each warp keeps its 16x8 output tiles in registers. Fibers are
+      //      gathered with cp.async into a double buffer: batch b+1 lands
+      //      while batch b's Khatri-Rao rows are formed and multiplied.
+      const int lane = tid & 31, wrp = tid >> 5, nwarp = nt >> 5, gq = lane >> 2, tq = lane & 3;
+      const int I16 = (int(I) + 15) / 16, R8 = (R + 7) / 8, NTILE = I16 * R8;
+      double acc[kAlsTiles][4];
 #pragma unroll
-      for (int q = 0; q < kAlsAcc; ++q) acc[q] = 0.0;
+      for (int t = 0; t < kAlsTiles; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.0;
       const i64 chunk = ceil_div(J, G);
       const i64 j0 = g * chunk, j1 = j0 + chunk < J ? j0 + chunk : J;
-      double* fib = sm;                       // [kAlsBatch][I]
-      double* kc = sm + kAlsBatch * I;        // [kAlsBatch][R]
-      double* fsm = kc + kAlsBatch * R;       // staged factors of the other modes
+      // padded row strides (== 4 mod 16 doubles): the MMA fragment loads of
+      // rows pp = 4 ks + tq hit distinct banks
+      const int ldI = als_ld(int(I)), ldR = als_ld(R);
+      T* fibT = reinterpret_cast<T*>(sm);                  // [2][kAlsBatch][I], raw T (cp.async)
+      double* fibD = sm + als_fib_doubles<T>(I);           // [kAlsBatch][ldI], converted once
+      double* kc = fibD + kAlsBatch * ldI;                 // [kAlsBatch][ldR]
+      T* fsm = reinterpret_cast<T*>(kc + kAlsBatch * ldR); // other modes' factors, row-major (rank fastest)
       {
         __syncthreads();
         if (tid == 0) {
@@ -614,31 +652,56 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
           if (k == m) continue;
           const int nk = sext[k] * R;
           const T* src = p.fs.f[k];
-          for (int e = tid; e < nk; e += nt) fsm[sfoff[k] + e] = double(src[e]);
+          const int ek = sext[k];
+          for (int e = tid; e < nk; e += nt) {  // transpose: a warp then reads one row's ranks
+            const int row = e / R, r = e % R;
+            fsm[sfoff[k] + e] = src[row + r * ek];
+          }
         }
         __syncthreads();
       }
-      for (i64 pb = j0; pb < j1; pb += kAlsBatch) {
-        const int np = int(j1 - pb < kAlsBatch ? j1 - pb : kAlsBatch);
-        for (int e = tid; e < kAlsBatch * int(I); e += nt) {
-          const int pp = e % kAlsBatch, i = e / kAlsBatch;
-          double v = 0.0;
-          if (pp < np) {
-            const i64 s = pb + pp, a = s / Rr, b = s - a * Rr;
-            v = double(p.B[(a * I + i) * Rr + b]);
-          }
-          fib[pp * I + i] = v;
+      // gather: thread tid always handles position pp = tid % kAlsBatch
+      auto gather = [&](i64 pb, int buf) {
+        const int pp = tid % kAlsBatch;
+        const bool ok = pb + pp < j1;
+        const unsigned s_ = unsigned(ok ? pb + pp : pb);
+        const unsigned a = s_ / unsigned(Rr), b = s_ - a * unsigned(Rr);
+        const T* src = p.B + i64(a) * I * Rr + b;
+        T* dst = fibT + buf * kAlsBatch * int(I) + pp * int(I);
+        for (int i = tid / kAlsBatch; i < int(I); i += nt / kAlsBatch) als_cp_elem(dst + i, src + i64(i) * Rr, ok);
+        als_cp_commit();
+      };
+      const bool stampA = p.prof != nullptr && g == 0 && tid == 0;
+      unsigned long long ts = stampA ? gtimer() : 0;
+      auto stampa = [&](int slot) {
+        if (stampA) {
+          const unsigned long long t = gtimer();
+          p.prof[slot] += t - ts;
+          ts = t;
         }
-        if (tid < kAlsBatch) {  // multi-index digits of each position, once
-          const i64 s = pb + tid;
-          i64 a = s / Rr, b = s - a * Rr;
+      };
+      if (j0 < j1) gather(j0, 0);
+      stampa(16);
+      int buf = 0;
+      for (i64 pb = j0; pb < j1; pb += kAlsBatch, buf ^= 1) {
+        const int np = int(j1 - pb < kAlsBatch ? j1 - pb : kAlsBatch);
+        if (pb + kAlsBatch < j1)
+          gather(pb + kAlsBatch, buf ^ 1);
+        else
+          als_cp_commit();  // keep one group per iteration
+        stampa(17);
+        if (tid < kAlsBatch) {  // multi-index digits of each position, once (32-bit: J < 2^31)
+          const unsigned s_ = unsigned(pb) + unsigned(tid);
+          unsigned a = s_ / unsigned(Rr), b = s_ - a * unsigned(Rr);
           for (int k = N - 1; k > m; --k) {
-            pidx[tid * kMaxOrder + k] = int(b % p.sh.e[k]);
-            b /= p.sh.e[k];
+            const unsigned ek = unsigned(sext[k]);
+            pidx[tid * kMaxOrder + k] = int(b % ek);
+            b /= ek;
           }
           for (int k = m - 1; k >= 0; --k) {
-            pidx[tid * kMaxOrder + k] = int(a % p.sh.e[k]);
-            a /= p.sh.e[k];
+            const unsigned ek = unsigned(sext[k]);
+            pidx[tid * kMaxOrder + k] = int(a % ek);
+            a /= ek;
           }
         }
         __syncthreads();
@@ -648,29 +711,56 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
           if (pp < np) {
             T prod = T(1);
             for (int k = N - 1; k >= 0; --k)  // highest mode first (kruskal.hpp:58-62)
-              if (k != m) prod *= T(fsm[sfoff[k] + pidx[pp * kMaxOrder + k] + r * sext[k]]);
+              if (k != m) prod *= fsm[sfoff[k] + pidx[pp * kMaxOrder + k] * R + r];
             v = double(prod);
           }
-          kc[pp * R + r] = v;
+          kc[pp * ldR + r] = v;
+        }
+        stampa(18);
+        als_cp_wait<1>();  // this batch's fibers (own copies) have landed
+        {  // each thread converts the elements it copied itself (no barrier needed before)
+          const int pp = tid % kAlsBatch;
+          const T* src = fibT + buf * kAlsBatch * int(I) + pp * int(I);
+          double* dst = fibD + pp * ldI;
+          for (int i = tid / kAlsBatch; i < int(I); i += nt / kAlsBatch) dst[i] = double(src[i]);
         }
         __syncthreads();
+        stampa(19);
+        const double* fb = fibD;
+#pragma unroll 2
+        for (int ks = 0; ks < kAlsBatch / 4; ++ks) {
+          const int pp = 4 * ks + tq;
+          const double* frow = fb + pp * ldI;
+          const double* krow = kc + pp * ldR;
 #pragma unroll
-        for (int q = 0; q < kAlsAcc; ++q) {
-          const int o = tid + q * nt;
-          if (o < nout) {
-            const int i = o % int(I), r = o / int(I);
-            double s = acc[q];
-            for (int pp = 0; pp < np; ++pp) s = fma(fib[pp * I + i], kc[pp * R + r], s);
-            acc[q] = s;
+          for (int t = 0; t < kAlsTiles; ++t) {
+            const int tile = wrp + t * nwarp;
+            if (tile < NTILE) {
+              const int i0 = 16 * (tile % I16) + gq, r0 = 8 * (tile / I16) + gq;
+              const double a0 = i0 < I ? frow[i0] : 0.0;
+              const double a1 = i0 + 8 < I ? frow[i0 + 8] : 0.0;
+              const double b0 = r0 < R ? krow[r0] : 0.0;
+              als_dmma(acc[t], a0, a1, b0);
+            }
           }
         }
-        __syncthreads();
+        __syncthreads();  // buffers are refilled next iteration
+        stampa(20);
+        if (stampA) p.prof[21] += 1;
       }
+      als_cp_wait<0>();
       double* pt = p.part + (i64(parity) * G + g) * p.part_stride;
 #pragma unroll
-      for (int q = 0; q < kAlsAcc; ++q) {
-        const int o = tid + q * nt;
-        if (o < nout) pt[o] = acc[q];
+      for (int t = 0; t < kAlsTiles; ++t) {
+        const int tile = wrp + t * nwarp;
+        if (tile < NTILE) {
+          const int ib = 16 * (tile % I16) + gq, rb = 8 * (tile / I16) + 2 * tq;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int i = ib + (q >> 1) * 8, r = rb + (q & 1);
+            if (i < I && r < R) pt[i + i64(r) * I] = acc[t][q];
+          }
+        }
       }
       unsigned long long tp1 = 0;
       if (p.prof && g == 0 && tid == 0) tp1 = gtimer();
@@ -687,15 +777,12 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
         for (int o = g * ch + tid; o < o1; o += nt) {
           double s = 0.0;
           int q = 0;
-          for (; q + 4 <= G; q += 4) {
-            const double v0 = ldcg(&pp0[i64(q) * p.part_stride + o]);
-            const double v1 = ldcg(&pp0[i64(q + 1) * p.part_stride + o]);
-            const double v2 = ldcg(&pp0[i64(q + 2) * p.part_stride + o]);
-            const double v3 = ldcg(&pp0[i64(q + 3) * p.part_stride + o]);
-            s += v0;
-            s += v1;
-            s += v2;
-            s += v3;
+          for (; q + 16 <= G; q += 16) {  // 16 loads in flight, then the adds in order
+            double v[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) v[u] = ldcg(&pp0[i64(q + u) * p.part_stride + o]);
+#pragma unroll
+            for (int u = 0; u < 16; ++u) s += v[u];
           }
           for (; q < G; ++q) s += ldcg(&pp0[i64(q) * p.part_stride + o]);
           Wg[o] = s;
@@ -1082,12 +1169,17 @@ void als_update(const FactorSet<T>& fs, int mode, const T* W, T* weights, double
 template <typename T>
 bool als_loop_supported(const i64* shape, int order, int rank) {
   if (rank > kAlsSmemRank) return false;
+  i64 S = 1;
+  for (int m = 0; m < order; ++m) S *= shape[m];
+  if (S >= (i64(1) << 31)) return false;  // 32-bit position arithmetic in the loop kernel
   for (int m = 0; m < order; ++m) {
     if (shape[m] * rank > i64(kAlsAcc) * kAlsThreads) return false;
     i64 fac = 0;
     for (int k = 0; k < order; ++k)
       if (k != m) fac += shape[k] * rank;
-    const size_t smA = (size_t(kAlsBatch) * shape[m] + size_t(kAlsBatch) * rank + size_t(fac)) * sizeof(double);
+    const size_t smA = (size_t(als_fib_doubles<T>(shape[m])) + size_t(kAlsBatch) * (als_ld(int(shape[m])) + als_ld(rank))) * sizeof(double) +
+                       size_t(fac) * sizeof(T);
+    if (((shape[m] + 15) / 16) * ((rank + 7) / 8) > i64(kAlsTiles) * (kAlsThreads / 32)) return false;
     const size_t smB = (2 * size_t(shape[m]) * rank + 3 * size_t(rank) * rank + 6 * size_t(rank)) * sizeof(double);
     if (std::max(smA, smB) > 180 * 1024) return false;
   }
@@ -1108,7 +1200,8 @@ void als_loop(const T* B, const i64* shape, int order, const FactorSet<T>& fs, T
     i64 fac = 0;
     for (int k = 0; k < order; ++k)
       if (k != m) fac += shape[k] * R;
-    const size_t smA = (size_t(kAlsBatch) * shape[m] + size_t(kAlsBatch) * R + size_t(fac)) * sizeof(double);
+    const size_t smA = (size_t(als_fib_doubles<T>(shape[m])) + size_t(kAlsBatch) * (als_ld(int(shape[m])) + als_ld(R))) * sizeof(double) +
+                       size_t(fac) * sizeof(T);
     const size_t smB = (2 * size_t(shape[m]) * R + 3 * size_t(R) * R + 6 * size_t(R)) * sizeof(double);
     smem = std::max(smem, std::max(smA, smB));
   }

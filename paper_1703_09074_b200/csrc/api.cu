@@ -522,16 +522,19 @@ AlsHandles<T> run_als(rcpg_context* c, const T* B, const i64* shape, int order, 
       c->als_part.ensure(size_t(part_elems) * sizeof(double));
       unsigned long long* prof = nullptr;
       if (getenv("RCPG_PROFILE_ALS")) {
-        c->als_prof.ensure(16 * sizeof(unsigned long long));
-        RCPG_CUDA(cudaMemsetAsync(c->als_prof.p, 0, 16 * sizeof(unsigned long long), c->st));
+        c->als_prof.ensure(32 * sizeof(unsigned long long));
+        RCPG_CUDA(cudaMemsetAsync(c->als_prof.p, 0, 32 * sizeof(unsigned long long), c->st));
         prof = c->als_prof.as<unsigned long long>();
       }
       als_loop<T>(B, shape, order, h.fs, h.weights, cfg.tol, cfg.max_iter, h.tfit, h.tsec, h.state,
                   c->als_part.as<double>(), part_elems, c->bar.as<GridBarrier>(), c->st, prof);
       if (prof) {
-        unsigned long long hp[16];
+        unsigned long long hp[32];
         RCPG_CUDA(cudaMemcpyAsync(hp, prof, sizeof(hp), cudaMemcpyDeviceToHost, c->st));
         RCPG_CUDA(cudaStreamSynchronize(c->st));
+        fprintf(stderr, "[rcpg als A] batches/mode %.1f: gather0 %.2f issue %.2f kc %.2f wait+cvt %.2f mma %.2f us (per mode step)\n",
+                hp[21] / double(hp[4]), hp[16] / 1e3 / double(hp[4]), hp[17] / 1e3 / double(hp[4]),
+                hp[18] / 1e3 / double(hp[4]), hp[19] / 1e3 / double(hp[4]), hp[20] / 1e3 / double(hp[4]));
         fprintf(stderr, "[rcpg als] modes=%llu  A %.2f us  bar1 %.2f us  B %.2f us  bar2 %.2f us (per mode step)\n",
                 hp[4], hp[0] / 1e3 / double(hp[4]), hp[1] / 1e3 / double(hp[4]), hp[2] / 1e3 / double(hp[4]),
                 hp[3] / 1e3 / double(hp[4]));
