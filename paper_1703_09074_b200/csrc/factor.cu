@@ -584,8 +584,6 @@ __global__ void __launch_bounds__(kLuThreads) plu_coop_kernel(LuArgs<T> p) {
     Cand<T>* out = p.cands + ((k + 1) & 1) * G;
     const bool more = (k + 1 < p.r);
     for (i64 s = r0 + threadIdx.x; s < r1; s += blockDim.x) {
-      const i64 ps = p.phys[s];
-      if (ps < k) continue;  // pivoted earlier
       i64 ba, bz;
       if (unit) {
         ba = s;
@@ -595,21 +593,30 @@ __global__ void __launch_bounds__(kLuThreads) plu_coop_kernel(LuArgs<T> p) {
         ba = aa * p.n * R + bb;
         bz = aa * p.r * R + bb;
       }
+      constexpr int B = 8;  // loads in flight per thread
+      T v[B];
+      // the row's physical position, its pivot-column value and the first
+      // chunk are independent loads: one memory round trip, not two (rows
+      // pivoted earlier are rare, their loads are simply dropped)
+      const i64 ps = p.phys[s];
+      const T pcv = p.A[ba + cs * R];
+#pragma unroll
+      for (int u = 0; u < B; ++u)
+        if (more && k + 1 + u < p.n) v[u] = p.A[ba + col_at[k + 1 + u] * R];
+      if (ps < k) continue;  // pivoted earlier
       if (s == ss) {
         p.Z[bz + k * R] = T(1);
         for (int j = k + 1; j < p.r; ++j) p.Z[bz + j * R] = T(0);
         continue;
       }
-      constexpr int B = 8;  // loads in flight per thread
-      T v[B];
-      // the pivot-column value and the first chunk are independent loads
-      const T pcv = p.A[ba + cs * R];
-#pragma unroll
-      for (int u = 0; u < B; ++u)
-        if (more && k + 1 + u < p.n) v[u] = p.A[ba + col_at[k + 1 + u] * R];
       const T m = pcv / piv;
       p.Z[bz + k * R] = m;
       if (more) {
+        // the row's first maximum in physical-column order (one float compare
+        // per entry), then one full candidate comparison per row: the same
+        // pick as comparing every entry (all share the physical row ps)
+        T rv = T(-1);
+        int rq = 0, rc = 0;
         for (int q0 = k + 1; q0 < p.n; q0 += B) {
           if (q0 > k + 1) {
 #pragma unroll
@@ -622,10 +629,16 @@ __global__ void __launch_bounds__(kLuThreads) plu_coop_kernel(LuArgs<T> p) {
               const int c = col_at[q0 + u];
               const T x = v[u] - m * U[c];
               p.A[ba + c * R] = x;
-              const Cand<T> cd{T(fabs(x)), q0 + u, c, ps, s};
-              if (better(cd, best)) best = cd;
+              const T ax = fabs(x);
+              if (ax > rv) {
+                rv = ax;
+                rq = q0 + u;
+                rc = c;
+              }
             }
         }
+        const Cand<T> cd{rv, rq, rc, ps, s};
+        if (better(cd, best)) best = cd;
       }
     }
     unsigned long long t_c = 0;
