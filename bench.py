@@ -30,6 +30,27 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 STREAMED = ("sketch", "power_xtq", "power_xz", "project")
+# Omega is generated into a panel before the sketch (SURVEY.md 8(d) counts its bytes as 0):
+# its time is charged to the streamed passes
+STREAMED_TIME = STREAMED + ("omega",)
+# FP64 DMMA / DFMA peak measured on this pool's B200 by tools/microbench/fp64_peak.cu
+# (not in MEASURED_PEAKS.json, which carries HBM and bf16 only)
+FP64_PEAK_TFLOPS = 37.0
+
+
+def streamed_flops(cfg) -> float:
+    """Algorithmic flops of the streamed passes: 2 S_n l per pass,
+    1 sketch + q X^T Q + q X Z + 1 projection per compressed mode, tensor shrinking."""
+    shape = list(cfg.shape)
+    total = 0.0
+    for n in range(len(shape)):
+        l = min(cfg.rank + cfg.oversampling, shape[n])
+        if l >= shape[n]:
+            continue
+        S = float(np.prod(shape))
+        total += (2 + 2 * cfg.power_iterations) * 2.0 * S * l
+        shape[n] = l
+    return total
 
 
 def parse():
@@ -267,7 +288,7 @@ def main():
 
     if rank == 0:
         peak, peak_kind = measured_peaks()
-        sm_ms = sum(pass_ms.get(n, 0.0) for n in STREAMED)
+        sm_ms = sum(pass_ms.get(n, 0.0) for n in STREAMED_TIME)
         sm_by = sum(pass_bytes.get(n, 0.0) for n in STREAMED)
         achieved = (sm_by / 1e9) / (sm_ms / 1e3) if sm_ms > 0 else 0.0
         passes = {n: {"ms_per_step": pass_ms[n] / args.steps,
@@ -286,12 +307,17 @@ def main():
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if peak else None, "traffic": profile_traffic(cfg.name),
-                         "kernel": "streamed mode-n passes (sketch / X^T Q / X Z / projection)",
+                         "kernel": "streamed mode-n passes (Omega + sketch / X^T Q / X Z / projection)",
                          "peak_source": peak_kind},
             "clocks": clk.summary(),
             "relerr": trace.final_relative_error, "iterations": trace.iterations, "converged": trace.converged,
             "passes": passes,
         }
+        if cfg.dtype == np.float64 and sm_ms > 0:
+            tf = streamed_flops(cfg) * args.steps / (sm_ms / 1e3) / 1e12
+            line["fp64_pipe"] = {"achieved": tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                                 "frac": tf / FP64_PEAK_TFLOPS,
+                                 "peak_source": "tools/microbench/fp64_peak.cu (own measurement)"}
         if e2e:
             line["e2e"] = e2e
         if world == 1 and not args.no_cpu_baseline:
