@@ -137,6 +137,28 @@ rcpg_status rcpg_decompose(rcpg_context* ctx, const rcpg_tensor* t, const rcpg_d
 rcpg_status rcpg_decompose_host(rcpg_context* ctx, rcpg_dtype dtype, int32_t order, const int64_t* shape,
                                 const void* host, const rcpg_decompose_config* cfg, rcpg_result* result);
 
+/* ---- sharding across GPUs (no counterpart in the serial
+ * reference) ------------------------------------------------------------------
+ * One context per GPU / rank. A tensor split in slabs along its LAST mode is
+ * decomposed with the same rcpg_decompose / rcpg_compress calls on every rank
+ * (collectively); results (model, trace, compressed tensor) are replicated. */
+/* 128-byte NCCL unique id (rank 0 creates it, the caller broadcasts it). */
+rcpg_status rcpg_comm_unique_id(void* out128);
+/* Join an NCCL communicator of nranks ranks (one per GPU, one process each). */
+rcpg_status rcpg_comm_init_nccl(rcpg_context* ctx, int32_t nranks, int32_t rank, const void* id128);
+/* Virtual ranks inside one process (ctxs[r] is rank r; one host thread each,
+ * any devices, including one shared GPU): tests the sharded path on one GPU. */
+rcpg_status rcpg_comm_init_loopback(rcpg_context** ctxs, int32_t n);
+rcpg_status rcpg_comm_rank(rcpg_context* ctx, int32_t* rank, int32_t* size);
+/* The balanced contiguous split [lo, hi) of [0, extent) used for slabs (host only). */
+void rcpg_slab_range(int64_t extent, int32_t nranks, int32_t rank, int64_t* lo, int64_t* hi);
+/* Slab [lo, hi) of the last mode of a device tensor (copied; `full` unchanged). */
+rcpg_status rcpg_tensor_slab(rcpg_context* ctx, const rcpg_tensor* full, int64_t lo, int64_t hi, rcpg_tensor** out);
+/* Slab from host: global_shape of the whole tensor, host_slab row-major with
+ * last extent hi - lo. */
+rcpg_status rcpg_tensor_upload_slab(rcpg_context* ctx, rcpg_dtype dtype, int32_t order, const int64_t* global_shape,
+                                    int64_t lo, int64_t hi, const void* host_slab, rcpg_tensor** out);
+
 /* ---- model utilities on device ------------------------------------------ */
 /* relative_error (kruskal.hpp:187-194) of a Kruskal model (weights [R],
  * factors column-major concatenated, host pointers) against a device tensor;

@@ -8,11 +8,11 @@ from .rcp import (  # noqa: F401
     ALS, BCD, COMPRESS, EIGENVECTORS, FACTORS, GAUSSIAN, INIT, LU, NOISE, QR, RANDOM, UNIFORM,
     CompressConfig, CompressionResult, Context, CudaError, DecomposeConfig, DeviceTensor, FitTrace, Kruskal,
     ModeBasis, SolverError, compress, decompose, default_context, derive_seed, plu_basis, relative_error,
-    sketch_matrix, stream_id, stream_pass, thin_qr,
+    sketch_matrix, stream_id, stream_pass, thin_qr, comm_unique_id, comm_init_loopback, slab_range,
 )
 from ._lib import LIB_PATH, build  # noqa: F401
 
 __all__ = [
     "CompressConfig", "DecomposeConfig", "Kruskal", "FitTrace", "SolverError", "ModeBasis", "CompressionResult",
-    "compress", "decompose", "relative_error", "sketch_matrix", "stream_pass", "plu_basis", "thin_qr", "DeviceTensor", "Context",
+    "compress", "decompose", "relative_error", "sketch_matrix", "stream_pass", "comm_unique_id", "comm_init_loopback", "slab_range", "plu_basis", "thin_qr", "DeviceTensor", "Context",
 ]

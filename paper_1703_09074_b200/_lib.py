@@ -93,6 +93,13 @@ SIGNATURES = {
     "rcpg_decompose_host": (_I32, [_V, C.c_int, _I32, _V, _V, C.POINTER(DecomposeConfigC), C.POINTER(ResultC)]),
     "rcpg_relative_error": (_I32, [_V, _V, _I64, _V, _V, C.POINTER(C.c_double)]),
     "rcpg_sketch_matrix": (_I32, [_V, C.c_int, _U64, _I64, _I64, _I64, _I32, _V]),
+    "rcpg_comm_unique_id": (_I32, [_V]),
+    "rcpg_comm_init_nccl": (_I32, [_V, C.c_int32, C.c_int32, _V]),
+    "rcpg_comm_init_loopback": (_I32, [_V, C.c_int32]),
+    "rcpg_comm_rank": (_I32, [_V, _V, _V]),
+    "rcpg_slab_range": (None, [_I64, C.c_int32, C.c_int32, _V, _V]),
+    "rcpg_tensor_slab": (_I32, [_V, _V, _I64, _I64, _V]),
+    "rcpg_tensor_upload_slab": (_I32, [_V, C.c_int, C.c_int32, _V, _I64, _I64, _V, _V]),
     "rcpg_stream_pass": (_I32, [_V, C.c_int, C.c_int32, _I64, _I64, _I64, _I64, _V, _V, _V]),
     "rcpg_plu_basis": (_I32, [_V, C.c_int, _I64, _I64, _V, _V]),
     "rcpg_thin_qr": (_I32, [_V, C.c_int, _I64, _I64, _V, _V, _V]),

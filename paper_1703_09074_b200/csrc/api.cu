@@ -83,16 +83,23 @@ struct rcpg_context {
   // decompose's compressed tensor + bases: kept across calls so repeated
   // decompositions reuse its buffers (a cudaFree per call drains the device)
   rcpg_compressed* dcomp = nullptr;
+  // ranks of a sharded decomposition; null = unsharded
+  std::unique_ptr<rcpg::Comm> comm;
+  DevBuf dl_phys, dl_cand_loc, dl_cand_all, dl_U, dl_state, sh_send, sh_recv, sh_fac;
 };
 
 struct rcpg_tensor {
   rcpg_context* ctx = nullptr;
   int dtype = 0;
   int order = 0;
-  i64 shape[kMaxOrder] = {};
+  i64 shape[kMaxOrder] = {};  // local shape (a slab's last extent is hi - lo)
   i64 size = 0;
   void* d = nullptr;
   bool owned = false;
+  // slab of a tensor sharded along its last mode over the context's ranks
+  bool slab = false;
+  i64 slab_lo = 0, slab_hi = 0, global_last = 0;
+  i64 gshape(int m) const { return (slab && m == order - 1) ? global_last : shape[m]; }
 };
 
 struct BasisRec {
@@ -420,6 +427,346 @@ void run_compress(rcpg_context* c, const rcpg_tensor* t, const CompressCfg& cfg,
   if (sync_checks) finish_compress(c, out, dfr);
 }
 
+// ------------------------------------------------------------- sharding
+// the tensor is split in slabs along its last mode s; rank g
+// holds mode-s rows [lo_g, hi_g). Modes n < s: Y = sum_g X_g Omega_g
+// (all-reduce I_n x l), the small factorizations redundant, W = X^T Q row-
+// sharded and its complete-pivot LU distributed (plu_basis_dist), the
+// projection local (the working tensor stays sharded along s). Mode s: Y rows
+// local (all-gather), W = sum_g X_g^T Q_g (all-reduce J_s x l), the LU of the
+// small W redundant, the projection an all-reduce of the l x J_s partials.
+// ALS, recover and the model are then replicated; the relative error sums
+// per-slab residuals (all-reduce of two doubles).
+struct SlabList {
+  int n = 1;
+  i64 lo[kDluMaxRanks] = {}, hi[kDluMaxRanks] = {};
+  i64 maxext() const {
+    i64 m = 0;
+    for (int g = 0; g < n; ++g) m = std::max(m, hi[g] - lo[g]);
+    return m;
+  }
+};
+
+__device__ __forceinline__ int slab_of(const SlabList& sl, i64 d) {
+  int g = 0;
+  while (g + 1 < sl.n && d >= sl.hi[g]) ++g;
+  return g;
+}
+
+// out[p * (hi - lo) + j] = in[p * E + lo + j]
+template <typename T>
+__global__ void slab_extract_kernel(const T* in, i64 prefix, i64 E, i64 lo, i64 ext, T* out) {
+  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < prefix * ext; e += i64(gridDim.x) * blockDim.x) {
+    const i64 pp = e / ext, j = e - pp * ext;
+    out[e] = in[pp * E + lo + j];
+  }
+}
+
+// full[p * E + d] = recv[g][p * ext_g + d - lo_g]   (per-rank blocks `stride` apart)
+template <typename T>
+__global__ void slab_assemble_kernel(const T* recv, i64 stride, SlabList sl, i64 prefix, i64 E, T* full) {
+  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < prefix * E; e += i64(gridDim.x) * blockDim.x) {
+    const i64 pp = e / E, d = e - pp * E;
+    const int g = slab_of(sl, d);
+    full[e] = recv[g * stride + pp * (sl.hi[g] - sl.lo[g]) + (d - sl.lo[g])];
+  }
+}
+
+// Y (extent x cols, column-major) from per-rank row blocks recv[g][c][maxloc]
+template <typename T>
+__global__ void rows_assemble_kernel(const T* recv, i64 maxloc, int cols, SlabList sl, i64 extent, T* Y) {
+  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < extent * cols; e += i64(gridDim.x) * blockDim.x) {
+    const i64 i = e % extent, cc = e / extent;
+    const int g = slab_of(sl, i);
+    Y[e] = recv[g * maxloc * cols + cc * maxloc + (i - sl.lo[g])];
+  }
+}
+
+int grid_for(i64 n) { return int(std::max<i64>(1, std::min<i64>(ceil_div(n, 256), 148 * 8))); }
+
+CommType comm_type(int bytes) { return bytes == 8 ? CommType::f64 : CommType::f32; }
+
+// Rows [lo, hi) of every rank's Yloc (ld = its row count) -> the full Y on every rank.
+template <typename T>
+void gather_rows(rcpg_context* c, const SlabList& sl, const T* Yloc, i64 Iloc, int cols, i64 extent, T* Y) {
+  Comm& comm = *c->comm;
+  const i64 maxloc = sl.maxext();
+  const size_t blk = size_t(maxloc) * size_t(cols);
+  c->sh_send.ensure(blk * sizeof(T));
+  c->sh_recv.ensure(blk * size_t(comm.size) * sizeof(T));
+  if (Iloc > 0)
+    RCPG_CUDA(cudaMemcpy2DAsync(c->sh_send.p, size_t(maxloc) * sizeof(T), Yloc, size_t(Iloc) * sizeof(T),
+                                size_t(Iloc) * sizeof(T), size_t(cols), cudaMemcpyDeviceToDevice, c->st));
+  comm.allgather(c->sh_send.p, c->sh_recv.p, blk * sizeof(T), c->st);
+  rows_assemble_kernel<T><<<grid_for(extent * cols), 256, 0, c->st>>>(c->sh_recv.as<T>(), maxloc, cols, sl, extent, Y);
+  count_launch();
+  RCPG_LAUNCHED();
+}
+
+template <typename T>
+void run_compress_sharded(rcpg_context* c, const rcpg_tensor* t, const CompressCfg& cfg, rcpg_compressed* out,
+                          Deferred& dfr) {
+  check_arg(cfg.target_rank >= 1, "compress: target rank must be at least 1");
+  check_arg(cfg.oversampling >= 0, "compress: oversampling must be non-negative");
+  check_arg(cfg.power_iterations >= 0, "compress: power iteration count must be non-negative");
+  check_arg(c->comm != nullptr, "compress: a sharded tensor needs a communicator (rcpg_comm_init_*)");
+  Comm& comm = *c->comm;
+  const int order = t->order, sm_ = order - 1;
+  const int sms = device_caps().num_sms;
+  const cudaStream_t st = c->st;
+  {
+    ScopedPass sp(c, "check_finite", double(t->size) * sizeof(T));
+    c->scratch.ensure(size_t(sms) * 8 * sizeof(double) + 64);
+    norm_and_finite<T>(static_cast<const T*>(t->d), t->size, slots(c) + kXSum, c->scratch.as<double>(), sms, st);
+    comm.allreduce_sum(slots(c) + kXSum, 2, CommType::f64, st);  // ||X||^2 and the non-finite count
+  }
+  dfr.compress_input = true;
+
+  SlabList sl;
+  sl.n = comm.size;
+  {
+    const i64 mine[2] = {t->slab_lo, t->slab_hi};
+    c->sh_send.ensure(sizeof(mine));
+    c->sh_recv.ensure(sizeof(mine) * size_t(comm.size));
+    RCPG_CUDA(cudaMemcpyAsync(c->sh_send.p, mine, sizeof(mine), cudaMemcpyHostToDevice, st));
+    comm.allgather(c->sh_send.p, c->sh_recv.p, sizeof(mine), st);
+    std::vector<i64> all(2 * size_t(comm.size));
+    RCPG_CUDA(cudaMemcpyAsync(all.data(), c->sh_recv.p, all.size() * sizeof(i64), cudaMemcpyDeviceToHost, st));
+    RCPG_CUDA(cudaStreamSynchronize(st));
+    i64 next = 0;
+    for (int g = 0; g < comm.size; ++g) {
+      sl.lo[g] = all[2 * size_t(g)];
+      sl.hi[g] = all[2 * size_t(g) + 1];
+      check_arg(sl.lo[g] == next && sl.hi[g] >= sl.lo[g], "compress: slabs must tile the last mode in rank order");
+      next = sl.hi[g];
+    }
+    check_arg(next == t->global_last, "compress: slabs must tile the last mode in rank order");
+  }
+
+  std::set<i64> selected;
+  if (cfg.modes_present) {
+    for (i64 m : cfg.modes) {
+      if (!(m >= 0 && m < order)) fail_after(c, dfr, "compress: mode index out of range");
+      selected.insert(m);
+    }
+  } else {
+    for (i64 m = 0; m < order; ++m) selected.insert(m);
+  }
+  check_arg(cfg.stabilizer == RCPG_STAB_LU || cfg.power_iterations == 0,
+            "compress: sharded tensors use the LU stabilizer (the distributed QR stabilizer is not implemented)");
+
+  i64 lsh[kMaxOrder], gsh[kMaxOrder];
+  for (int m = 0; m < order; ++m) {
+    lsh[m] = t->shape[m];
+    gsh[m] = t->gshape(m);
+  }
+  const T* cur = static_cast<const T*>(t->d);
+  int which = 0;
+  bool sharded = true;
+  if (out->bases.size() < size_t(order)) out->bases.resize(size_t(order));
+  for (auto& b : out->bases) {
+    b.identity = true;
+    b.dim = b.cols = 0;
+    b.rank_warning = false;
+  }
+  const i64 lo = t->slab_lo;
+
+  for (int n = 0; n < order; ++n) {
+    const i64 extent = gsh[n];
+    const i64 l = std::min(cfg.target_rank + cfg.oversampling, extent);
+    BasisRec& basis = out->bases[n];
+    basis.dim = extent;
+    if (selected.count(n) == 0 || l >= extent) {
+      basis.identity = true;
+      continue;
+    }
+    if (l > kMaxPanelCols) fail_after(c, dfr, "compress: sketch width k + p above the supported maximum (256)");
+    const ModeView v = mode_view(lsh, order, n);
+    const i64 J = v.L * v.R;
+    const double b = sizeof(T);
+    c->Y.ensure(size_t(extent) * l * sizeof(T));
+    c->Qy.ensure(size_t(extent) * l * sizeof(T));
+    c->panelA.ensure(size_t(J) * l * sizeof(T));
+    c->panelB.ensure(size_t(J) * l * sizeof(T));
+    T* P = c->panelA.as<T>();
+    T* Zp = c->panelB.as<T>();
+    T* Y = c->Y.as<T>();
+    T* Qy = c->Qy.as<T>();
+    i64 ycols = l;
+    DevBuf& dst = which == 0 ? c->work0 : c->work1;
+    if (n < sm_) {
+      const ModeView vg = mode_view(gsh, order, n);
+      const i64 Jg = vg.L * vg.R, S = J * extent;
+      KoldaMap km = mode_kolda(lsh, order, n);
+      km.high_last_off = lo;
+      SlabMap smap;
+      smap.kmg = mode_kolda(gsh, order, n);
+      smap.Rg = vg.R;
+      smap.Es = gsh[sm_];
+      smap.nranks = sl.n;
+      for (int g = 0; g < sl.n; ++g) {
+        smap.lo[g] = sl.lo[g];
+        smap.hi[g] = sl.hi[g];
+      }
+      const i64 scr = sketch_scratch_elems<T>(v, l, sms);
+      c->scratch.ensure(size_t(scr) * sizeof(T));
+      {
+        ScopedPass sp(c, "omega", 0.0);
+        omega_panel<T>(cfg.seed, n, km, v, l, cfg.distribution, P, st, Jg);
+      }
+      {
+        ScopedPass sp(c, "sketch", (S + extent * l) * b);
+        sketch<T>(cur, v, P, l, Y, c->scratch.as<T>(), scr, sms, st);
+        comm.allreduce_sum(Y, size_t(extent * l), comm_type(sizeof(T)), st);
+      }
+      for (int it = 0; it < cfg.power_iterations; ++it) {
+        int rq;
+        {
+          ScopedPass sp(c, "stab_y", 2.0 * extent * ycols * b);
+          rq = stabilize_small<T>(c, cfg.stabilizer, Y, extent, int(ycols), Qy);
+        }
+        {
+          ScopedPass sp(c, "power_xtq", (S + J * rq) * b);
+          project<T>(cur, v, Qy, extent, rq, P, st);
+        }
+        int rz;
+        {
+          ScopedPass sp(c, "stab_w", 2.0 * J * rq * b);
+          const int G = 4 * sms;
+          c->dl_phys.ensure(size_t(J) * sizeof(i64));
+          c->dl_cand_loc.ensure(size_t(G) * factor_cand_bytes());
+          c->dl_cand_all.ensure(size_t(G) * size_t(comm.size) * factor_cand_bytes());
+          c->dl_U.ensure(size_t(kMaxPanelCols) * sizeof(double));
+          c->dl_state.ensure(dlu_state_bytes());
+          DluWork w;
+          w.phys = c->dl_phys.as<i64>();
+          w.cand_loc = c->dl_cand_loc.p;
+          w.cand_all = c->dl_cand_all.p;
+          w.U = c->dl_U.p;
+          w.state = c->dl_state.p;
+          w.G = G;
+          rz = plu_basis_dist<T>(P, Zp, J, v.R, rq, Jg, km, smap, comm, w, st);
+        }
+        {
+          ScopedPass sp(c, "power_xz", (S + J * rz + extent * rz) * b);
+          const i64 scr2 = sketch_scratch_elems<T>(v, rz, sms);
+          c->scratch.ensure(size_t(scr2) * sizeof(T));
+          sketch<T>(cur, v, Zp, rz, Y, c->scratch.as<T>(), scr2, sms, st);
+          comm.allreduce_sum(Y, size_t(extent * rz), comm_type(sizeof(T)), st);
+        }
+        ycols = rz;
+      }
+      int qcols;
+      {
+        ScopedPass sp(c, "thin_qr", 2.0 * extent * ycols * b);
+        FactorWork w = factor_work(c, extent);
+        basis.q.ensure(size_t(extent) * ycols * sizeof(T));
+        qcols = thin_qr<T>(Y, basis.q.as<T>(), extent, extent, int(ycols), identity_kolda(extent), w,
+                           rank_warn_slot(c, n), st);
+      }
+      basis.identity = false;
+      basis.cols = qcols;
+      if (qcols != l) fail_after(c, dfr, "fold: matrix dimensions do not match the target shape");
+      dst.ensure(size_t(v.L) * l * v.R * sizeof(T));
+      {
+        ScopedPass sp(c, "project", (S + l * J) * b);
+        project<T>(cur, v, basis.q.as<T>(), extent, l, dst.as<T>(), st);
+      }
+    } else {
+      // the sharded mode: Y rows are local, the J_s-row panels are replicated
+      const i64 Iloc = v.I, Jn = v.L, S = Jn * Iloc;
+      const KoldaMap km = mode_kolda(gsh, order, n);
+      c->sh_fac.ensure(size_t(std::max<i64>(Iloc, 1)) * l * sizeof(T));
+      T* Yloc = c->sh_fac.as<T>();
+      const i64 scr = sketch_scratch_elems<T>(v, l, sms);
+      c->scratch.ensure(size_t(scr) * sizeof(T));
+      {
+        ScopedPass sp(c, "omega", 0.0);
+        omega_panel<T>(cfg.seed, n, km, v, l, cfg.distribution, P, st);
+      }
+      {
+        ScopedPass sp(c, "sketch", (S + extent * l) * b);
+        sketch<T>(cur, v, P, l, Yloc, c->scratch.as<T>(), scr, sms, st);
+        gather_rows<T>(c, sl, Yloc, Iloc, int(l), extent, Y);
+      }
+      for (int it = 0; it < cfg.power_iterations; ++it) {
+        int rq;
+        {
+          ScopedPass sp(c, "stab_y", 2.0 * extent * ycols * b);
+          rq = stabilize_small<T>(c, cfg.stabilizer, Y, extent, int(ycols), Qy);
+        }
+        {
+          ScopedPass sp(c, "power_xtq", (S + Jn * rq) * b);
+          project<T>(cur, v, Qy + lo, extent, rq, P, st);  // this slab's rows of Q
+          comm.allreduce_sum(P, size_t(Jn * rq), comm_type(sizeof(T)), st);
+        }
+        int rz;
+        {
+          ScopedPass sp(c, "stab_w", 2.0 * Jn * rq * b);
+          FactorWork w = factor_work(c, Jn);
+          rz = plu_basis<T>(P, Zp, Jn, 1, rq, km, w, st);
+        }
+        {
+          ScopedPass sp(c, "power_xz", (S + Jn * rz + extent * rz) * b);
+          const i64 scr2 = sketch_scratch_elems<T>(v, rz, sms);
+          c->scratch.ensure(size_t(scr2) * sizeof(T));
+          sketch<T>(cur, v, Zp, rz, Yloc, c->scratch.as<T>(), scr2, sms, st);
+          gather_rows<T>(c, sl, Yloc, Iloc, rz, extent, Y);
+        }
+        ycols = rz;
+      }
+      int qcols;
+      {
+        ScopedPass sp(c, "thin_qr", 2.0 * extent * ycols * b);
+        FactorWork w = factor_work(c, extent);
+        basis.q.ensure(size_t(extent) * ycols * sizeof(T));
+        qcols = thin_qr<T>(Y, basis.q.as<T>(), extent, extent, int(ycols), identity_kolda(extent), w,
+                           rank_warn_slot(c, n), st);
+      }
+      basis.identity = false;
+      basis.cols = qcols;
+      if (qcols != l) fail_after(c, dfr, "fold: matrix dimensions do not match the target shape");
+      dst.ensure(size_t(Jn) * l * sizeof(T));
+      {
+        ScopedPass sp(c, "project", (S + l * Jn) * b);
+        project<T>(cur, v, basis.q.as<T>() + lo, extent, l, dst.as<T>(), st);
+        comm.allreduce_sum(dst.p, size_t(Jn * l), comm_type(sizeof(T)), st);
+      }
+      sharded = false;
+    }
+    cur = dst.as<T>();
+    which ^= 1;
+    lsh[n] = gsh[n] = l;
+  }
+  if (sharded) {  // the sharded mode stayed uncompressed: assemble the full tensor everywhere
+    i64 prefix = 1;
+    for (int m = 0; m < sm_; ++m) prefix *= lsh[m];
+    const i64 stride = prefix * sl.maxext();
+    c->sh_send.ensure(size_t(stride) * sizeof(T));
+    c->sh_recv.ensure(size_t(stride) * size_t(comm.size) * sizeof(T));
+    RCPG_CUDA(cudaMemcpyAsync(c->sh_send.p, cur, size_t(prefix * lsh[sm_]) * sizeof(T), cudaMemcpyDeviceToDevice, st));
+    comm.allgather(c->sh_send.p, c->sh_recv.p, size_t(stride) * sizeof(T), st);
+    DevBuf& dst = which == 0 ? c->work0 : c->work1;
+    dst.ensure(size_t(prefix * gsh[sm_]) * sizeof(T));
+    slab_assemble_kernel<T><<<grid_for(prefix * gsh[sm_]), 256, 0, st>>>(c->sh_recv.as<T>(), stride, sl, prefix,
+                                                                        gsh[sm_], dst.as<T>());
+    count_launch();
+    RCPG_LAUNCHED();
+    cur = dst.as<T>();
+    lsh[sm_] = gsh[sm_];
+  }
+  out->dtype = t->dtype;
+  out->order = order;
+  i64 size = 1;
+  for (int m = 0; m < order; ++m) {
+    out->shape[m] = gsh[m];
+    size *= gsh[m];
+  }
+  out->size = size;
+  out->data.ensure(size_t(size) * sizeof(T));
+  RCPG_CUDA(cudaMemcpyAsync(out->data.p, cur, size_t(size) * sizeof(T), cudaMemcpyDeviceToDevice, st));
+}
+
 // Reads the deferred device results of a compress: input check, rank warnings.
 void finish_compress(rcpg_context* c, rcpg_compressed* out, const Deferred& dfr) {
   raise_deferred(c, dfr);
@@ -595,6 +942,35 @@ void run_relerr(rcpg_context* c, const T* X, const i64* shape, int order, const 
   dfr.relerr = true;
 }
 
+// Sharded relative error: this slab's residual against the rows [lo, hi) of
+// the last factor, then the two sums all-reduced.
+template <typename T>
+void run_relerr_sharded(rcpg_context* c, const rcpg_tensor* t, const FactorSet<T>& fs, const T* w, Deferred& dfr) {
+  const int sms = device_caps().num_sms;
+  const int sm_ = t->order - 1, R = fs.rank;
+  const i64 Iloc = t->slab_hi - t->slab_lo;
+  c->sh_fac.ensure(size_t(std::max<i64>(Iloc, 1)) * R * sizeof(T));
+  FactorSet<T> loc = fs;
+  if (Iloc > 0)
+    RCPG_CUDA(cudaMemcpy2DAsync(c->sh_fac.p, size_t(Iloc) * sizeof(T), fs.f[sm_] + t->slab_lo,
+                                size_t(fs.extent[sm_]) * sizeof(T), size_t(Iloc) * sizeof(T), size_t(R),
+                                cudaMemcpyDeviceToDevice, c->st));
+  loc.f[sm_] = c->sh_fac.as<T>();
+  loc.extent[sm_] = Iloc;
+  c->scratch.ensure(residual_scratch_doubles(sms) * sizeof(double));
+  {
+    ScopedPass sp(c, "relerr", double(t->size) * sizeof(T));
+    if (Iloc > 0) {
+      residual_norms<T>(static_cast<const T*>(t->d), t->shape, t->order, loc, w, slots(c) + kResid,
+                        c->scratch.as<double>(), sms, c->st);
+    } else {
+      RCPG_CUDA(cudaMemsetAsync(slots(c) + kResid, 0, 2 * sizeof(double), c->st));
+    }
+    c->comm->allreduce_sum(slots(c) + kResid, 2, CommType::f64, c->st);
+  }
+  dfr.relerr = true;
+}
+
 // One readback at the end of a decomposition: checks (in reference order),
 // ALS state, trace, model.
 template <typename T>
@@ -639,6 +1015,7 @@ template <typename T>
 void run_decompose(rcpg_context* c, const rcpg_tensor* t, const rcpg_decompose_config& cfg, rcpg_result* res) {
   check_arg(cfg.method == RCPG_ALS, "decompose: only the ALS solver is on this path (bcd is out of scope)");
   Deferred dfr;
+  check_arg(!(t->slab && !cfg.randomized), "decompose: sharded tensors are decomposed with randomized = true");
   if (!cfg.randomized) {
     AlsHandles<T> h = run_als<T>(c, static_cast<const T*>(t->d), t->shape, t->order, cfg, dfr);
     run_relerr<T>(c, static_cast<const T*>(t->d), t->shape, t->order, h.fs, h.weights, dfr);
@@ -650,12 +1027,15 @@ void run_decompose(rcpg_context* c, const rcpg_tensor* t, const rcpg_decompose_c
   check_arg(cc.target_rank == cfg.rank, "decompose: compression target rank must equal the CP rank");
   if (c->dcomp == nullptr) c->dcomp = new rcpg_compressed();
   rcpg_compressed& comp = *c->dcomp;
-  run_compress<T>(c, t, cc, &comp, dfr, /*sync_checks=*/false);
+  if (t->slab)
+    run_compress_sharded<T>(c, t, cc, &comp, dfr);
+  else
+    run_compress<T>(c, t, cc, &comp, dfr, /*sync_checks=*/false);
   AlsHandles<T> h = run_als<T>(c, comp.data.as<T>(), comp.shape, comp.order, cfg, dfr);
   // recover (kruskal.hpp:198-220): A_n = Q_n A~_n, then normalize
   const int R = int(cfg.rank);
   i64 sum_ext = 0;
-  for (int m = 0; m < t->order; ++m) sum_ext += t->shape[m];
+  for (int m = 0; m < t->order; ++m) sum_ext += t->gshape(m);
   c->recov.ensure(size_t(sum_ext) * R * sizeof(T));
   FactorSet<T> big = h.fs;
   {
@@ -672,13 +1052,16 @@ void run_decompose(rcpg_context* c, const rcpg_tensor* t, const rcpg_decompose_c
         small_gemm<T>(b.q.as<T>(), b.dim, b.cols, h.fs.f[m], R, dst, c->st);
       }
       big.f[m] = dst;
-      big.extent[m] = t->shape[m];
-      off += t->shape[m] * R;
+      big.extent[m] = t->gshape(m);
+      off += t->gshape(m) * R;
     }
     c->small_tmp.ensure(size_t(sum_ext * R + R) * sizeof(T));
     normalize_model<T>(big, h.weights, c->small_tmp.as<T>(), c->st);
   }
-  run_relerr<T>(c, static_cast<const T*>(t->d), t->shape, t->order, big, h.weights, dfr);
+  if (t->slab)
+    run_relerr_sharded<T>(c, t, big, h.weights, dfr);
+  else
+    run_relerr<T>(c, static_cast<const T*>(t->d), t->shape, t->order, big, h.weights, dfr);
   finish_decompose<T>(c, h, big, dfr, res);
 }
 
@@ -762,6 +1145,10 @@ void rcpg_destroy(rcpg_context* c) {
     cudaEventDestroy(r.b);
   }
   delete c->dcomp;
+  c->comm.reset();
+  for (DevBuf* b : {&c->dl_phys, &c->dl_cand_loc, &c->dl_cand_all, &c->dl_U, &c->dl_state, &c->sh_send, &c->sh_recv,
+                    &c->sh_fac})
+    b->release();
   for (DevBuf* b : {&c->panelA, &c->panelB, &c->work0, &c->work1, &c->Y, &c->Qy, &c->scratch, &c->keys, &c->cands,
                     &c->bar, &c->info, &c->part, &c->tau, &c->diag, &c->cqr, &c->als_f, &c->als_g, &c->als_w, &c->als_kr,
                     &c->als_work, &c->als_trace, &c->als_state, &c->weights, &c->small_tmp, &c->nrm, &c->als_part, &c->als_prof, &c->recov})
@@ -840,10 +1227,17 @@ rcpg_status rcpg_compress(rcpg_context* c, const rcpg_tensor* t, const rcpg_comp
     auto comp = std::make_unique<rcpg_compressed>();
     const CompressCfg cc = to_cfg(*cfg);
     Deferred dfr;
-    if (t->dtype == RCPG_F64)
+    if (t->slab) {
+      if (t->dtype == RCPG_F64)
+        run_compress_sharded<double>(c, t, cc, comp.get(), dfr);
+      else
+        run_compress_sharded<float>(c, t, cc, comp.get(), dfr);
+      finish_compress(c, comp.get(), dfr);
+    } else if (t->dtype == RCPG_F64) {
       run_compress<double>(c, t, cc, comp.get(), dfr, true);
-    else
+    } else {
       run_compress<float>(c, t, cc, comp.get(), dfr, true);
+    }
     *out = comp.release();
   });
 }
@@ -897,6 +1291,119 @@ rcpg_status rcpg_decompose_host(rcpg_context* c, rcpg_dtype dtype, int32_t order
   s = rcpg_decompose(c, t, cfg, res);
   rcpg_tensor_free(t);
   return s;
+}
+
+// ------------------------------------------------------------ sharding
+rcpg_status rcpg_comm_unique_id(void* out128) {
+  try {
+    nccl_unique_id(out128);
+    return RCPG_OK;
+  } catch (const std::exception&) {
+    return RCPG_NCCL_ERROR;
+  }
+}
+
+rcpg_status rcpg_comm_init_nccl(rcpg_context* c, int32_t nranks, int32_t rank, const void* id128) {
+  return guarded(c, [&] {
+    check_arg(nranks >= 1 && nranks <= kDluMaxRanks && rank >= 0 && rank < nranks, "comm: bad rank / size");
+    c->comm = make_nccl_comm(nranks, rank, id128);
+  });
+}
+
+rcpg_status rcpg_comm_init_loopback(rcpg_context** ctxs, int32_t n) {
+  if (ctxs == nullptr || n < 1 || n > kDluMaxRanks) return RCPG_INVALID_ARGUMENT;
+  return guarded(ctxs[0], [&] {
+    auto hub = make_loopback_hub(n);
+    for (int r = 0; r < n; ++r) ctxs[r]->comm = make_loopback_comm(hub, r);
+  });
+}
+
+rcpg_status rcpg_comm_rank(rcpg_context* c, int32_t* rank, int32_t* size) {
+  *rank = c->comm ? c->comm->rank : 0;
+  *size = c->comm ? c->comm->size : 1;
+  return RCPG_OK;
+}
+
+void rcpg_slab_range(int64_t extent, int32_t nranks, int32_t rank, int64_t* lo, int64_t* hi) {
+  i64 a, b;
+  slab_range(extent, nranks, rank, a, b);
+  *lo = a;
+  *hi = b;
+}
+
+rcpg_status rcpg_tensor_slab(rcpg_context* c, const rcpg_tensor* full, int64_t lo, int64_t hi, rcpg_tensor** out) {
+  return guarded(c, [&] {
+    check_arg(!full->slab, "tensor_slab: the input is already a slab");
+    const int order = full->order;
+    const i64 E = full->shape[order - 1];
+    check_arg(lo >= 0 && lo <= hi && hi <= E, "tensor_slab: [lo, hi) outside the last mode");
+    auto t = std::make_unique<rcpg_tensor>();
+    t->ctx = c;
+    t->dtype = full->dtype;
+    t->order = order;
+    t->size = 1;
+    for (int m = 0; m < order; ++m) {
+      t->shape[m] = m == order - 1 ? hi - lo : full->shape[m];
+      t->size *= t->shape[m];
+    }
+    t->slab = true;
+    t->slab_lo = lo;
+    t->slab_hi = hi;
+    t->global_last = E;
+    const size_t bytes = size_t(std::max<i64>(t->size, 1)) * dsize(t->dtype);
+    cudaError_t e = cudaMalloc(&t->d, bytes);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      throw CudaFailure("rcpg_tensor_slab: cudaMalloc failed", e);
+    }
+    t->owned = true;
+    const i64 prefix = t->size / std::max<i64>(hi - lo, 1);
+    if (hi > lo) {
+      if (t->dtype == RCPG_F64)
+        slab_extract_kernel<double><<<grid_for(t->size), 256, 0, c->st>>>(static_cast<const double*>(full->d), prefix,
+                                                                           E, lo, hi - lo, static_cast<double*>(t->d));
+      else
+        slab_extract_kernel<float><<<grid_for(t->size), 256, 0, c->st>>>(static_cast<const float*>(full->d), prefix,
+                                                                          E, lo, hi - lo, static_cast<float*>(t->d));
+      count_launch();
+      RCPG_LAUNCHED();
+    }
+    RCPG_CUDA(cudaStreamSynchronize(c->st));
+    *out = t.release();
+  });
+}
+
+rcpg_status rcpg_tensor_upload_slab(rcpg_context* c, rcpg_dtype dtype, int32_t order, const int64_t* global_shape,
+                                    int64_t lo, int64_t hi, const void* host_slab, rcpg_tensor** out) {
+  return guarded(c, [&] {
+    validate_tensor_args(dtype, order, global_shape);
+    const i64 E = global_shape[order - 1];
+    check_arg(lo >= 0 && lo <= hi && hi <= E, "tensor_upload_slab: [lo, hi) outside the last mode");
+    auto t = std::make_unique<rcpg_tensor>();
+    t->ctx = c;
+    t->dtype = dtype;
+    t->order = order;
+    t->size = 1;
+    for (int m = 0; m < order; ++m) {
+      t->shape[m] = m == order - 1 ? hi - lo : global_shape[m];
+      t->size *= t->shape[m];
+    }
+    t->slab = true;
+    t->slab_lo = lo;
+    t->slab_hi = hi;
+    t->global_last = E;
+    const size_t bytes = size_t(std::max<i64>(t->size, 1)) * dsize(dtype);
+    cudaError_t e = cudaMalloc(&t->d, bytes);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      throw CudaFailure("rcpg_tensor_upload_slab: cudaMalloc failed", e);
+    }
+    t->owned = true;
+    if (t->size > 0)
+      RCPG_CUDA(cudaMemcpyAsync(t->d, host_slab, size_t(t->size) * dsize(dtype), cudaMemcpyHostToDevice, c->st));
+    RCPG_CUDA(cudaStreamSynchronize(c->st));
+    *out = t.release();
+  });
 }
 
 rcpg_status rcpg_relative_error(rcpg_context* c, const rcpg_tensor* t, int64_t rank, const void* weights,

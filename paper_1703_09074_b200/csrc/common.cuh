@@ -154,6 +154,10 @@ struct KoldaMap {
   i64 low_ext[8];
   i64 high_ext[8];
   i64 L = 1;
+  // slab of a sharded tensor: the last high digit is local, the global
+  // column rank adds high_last_off times that digit's stride (the last
+  // digit's stride does not depend on its own extent)
+  i64 high_last_off = 0;
 };
 
 __host__ __device__ inline i64 colmajor_rank(i64 rowmajor, const i64* ext, int k) {
@@ -173,7 +177,13 @@ __host__ __device__ inline i64 colmajor_rank(i64 rowmajor, const i64* ext, int k
 }
 
 __host__ __device__ inline i64 kolda_index(const KoldaMap& km, i64 a, i64 b) {
-  return colmajor_rank(a, km.low_ext, km.n_low) + km.L * colmajor_rank(b, km.high_ext, km.n_high);
+  i64 hi = colmajor_rank(b, km.high_ext, km.n_high);
+  if (km.high_last_off != 0) {
+    i64 stride = 1;
+    for (int m = 0; m + 1 < km.n_high; ++m) stride *= km.high_ext[m];
+    hi += km.high_last_off * stride;
+  }
+  return colmajor_rank(a, km.low_ext, km.n_low) + km.L * hi;
 }
 
 // Inverse: Kolda column j -> storage row s = a*R + b.

@@ -1480,6 +1480,230 @@ int thin_qr(T* A, T* Q, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w, 
   return r;
 }
 
+namespace {
+
+// ------------------------------------- complete-pivoting LU, row-sharded
+// the rows of W whose last-mode index lies in this rank's
+// slab are local; a row is identified by its global Kolda index (= its
+// initial physical position). Per pivot every rank (1) applies the previous
+// pivot to its rows and reduces its candidates per CTA, (2) all-gathers the
+// candidates, (3) runs the identical choice and bookkeeping (the same total
+// order as plu_coop: |value|, then physical column, then physical row), and
+// (4) all-reduces the pivot row, which only its owner fills.
+constexpr int kDluThreads = 256;
+
+template <typename T>
+struct DluState {
+  int k0, done, cs, owner, n_ov;
+  i64 srow;  // owner-local storage row of the current pivot
+  int col_at[kMaxPanelCols];
+  i64 ov_pos[kMaxPanelCols], ov_row[kMaxPanelCols];  // position -> global row id (latest wins)
+};
+
+template <typename T>
+struct DluArgs {
+  T* A;
+  T* Z;
+  i64 J, R;  // local rows, local R of the mode view
+  int n, r;
+  i64* phys;
+  Cand<T>* cand_loc;        // [G]
+  const Cand<T>* cand_all;  // [nranks * G]
+  T* U;                     // [n]
+  DluState<T>* st;
+  int rank, G;
+  SlabMap sm;
+};
+
+__device__ void dlu_locate(const SlabMap& sm, i64 rowid, int& owner, i64& sloc) {
+  const i64 row = kolda_inverse(sm.kmg, rowid, sm.Rg);  // a * Rg + b (global)
+  const i64 a = row / sm.Rg, bg = row - a * sm.Rg;
+  const i64 d = bg % sm.Es, rest = bg / sm.Es;  // last mode is b's fastest digit
+  int g = 0;
+  while (g + 1 < sm.nranks && d >= sm.hi[g]) ++g;
+  owner = g;
+  const i64 ext = sm.hi[g] - sm.lo[g];
+  sloc = a * ((sm.Rg / sm.Es) * ext) + rest * ext + (d - sm.lo[g]);
+}
+
+template <typename T>
+__global__ void dlu_init_kernel(DluState<T>* st, int n, int r) {
+  if (threadIdx.x == 0) {
+    st->k0 = r;
+    st->done = 0;
+    st->n_ov = 0;
+    st->owner = -1;
+    st->srow = -1;
+    st->cs = 0;
+  }
+  for (int c = threadIdx.x; c < n; c += blockDim.x) st->col_at[c] = c;
+}
+
+// k >= 0: apply pivot k (Z column k) and reduce the candidates for k + 1;
+// k == -1: initial scan.
+template <typename T>
+__global__ void __launch_bounds__(kDluThreads) dlu_update_kernel(DluArgs<T> p, int k) {
+  __shared__ Cand<T> red[33];
+  __shared__ int col_at[kMaxPanelCols];
+  __shared__ T U[kMaxPanelCols];
+  const Cand<T> none{T(-1), 0x7fffffff, 0, 0x7fffffffffffffffll, 0};
+  const DluState<T>* st = p.st;
+  const i64 R = p.R;
+  if (k >= 0 && st->done) {
+    if (st->k0 == k) {  // exactly-zero corner: unit vectors at positions k0..r-1
+      for (i64 s = blockIdx.x * i64(blockDim.x) + threadIdx.x; s < p.J; s += i64(gridDim.x) * blockDim.x) {
+        const i64 ps = p.phys[s];
+        if (ps < k) continue;
+        const i64 a = s / R, b = s - a * R, bz = a * p.r * R + b;
+        for (int j = k; j < p.r; ++j) p.Z[bz + j * R] = (ps == j) ? T(1) : T(0);
+      }
+    }
+    if (threadIdx.x == 0) p.cand_loc[blockIdx.x] = none;
+    return;
+  }
+  for (int c = threadIdx.x; c < p.n; c += blockDim.x) {
+    col_at[c] = k < 0 ? c : st->col_at[c];
+    U[c] = k < 0 ? T(0) : p.U[c];
+  }
+  __syncthreads();
+  const int cs = k < 0 ? 0 : st->cs;
+  const T piv = k < 0 ? T(1) : U[cs];
+  const bool own_piv = k >= 0 && st->owner == p.rank;
+  const i64 srow = st->srow;
+  const bool more = (k + 1 < p.r);
+  const i64 tag = i64(p.rank) << 40;
+  Cand<T> best = none;
+  for (i64 s = blockIdx.x * i64(blockDim.x) + threadIdx.x; s < p.J; s += i64(gridDim.x) * blockDim.x) {
+    const i64 ps = p.phys[s];
+    if (ps < k) continue;  // pivoted earlier
+    const i64 a = s / R, b = s - a * R;
+    const i64 ba = a * p.n * R + b, bz = a * p.r * R + b;
+    if (own_piv && s == srow) {
+      p.Z[bz + k * R] = T(1);
+      for (int j = k + 1; j < p.r; ++j) p.Z[bz + j * R] = T(0);
+      continue;
+    }
+    T rv = T(-1);
+    int rq = 0, rc = 0;
+    if (k < 0) {
+      for (int c = 0; c < p.n; ++c) {
+        const T ax = fabs(p.A[ba + c * R]);
+        if (ax > rv) {
+          rv = ax;
+          rq = c;
+          rc = c;
+        }
+      }
+    } else {
+      const T m = p.A[ba + cs * R] / piv;
+      p.Z[bz + k * R] = m;
+      if (!more) continue;
+      for (int q = k + 1; q < p.n; ++q) {
+        const int c = col_at[q];
+        const T x = p.A[ba + c * R] - m * U[c];
+        p.A[ba + c * R] = x;
+        const T ax = fabs(x);
+        if (ax > rv) {
+          rv = ax;
+          rq = q;
+          rc = c;
+        }
+      }
+    }
+    const Cand<T> cd{rv, rq, rc, ps, tag | s};
+    if (better(cd, best)) best = cd;
+  }
+  best = block_best(best, red);
+  if (threadIdx.x == 0) p.cand_loc[blockIdx.x] = best;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kDluThreads) dlu_pick_kernel(DluArgs<T> p, int k, int total) {
+  __shared__ Cand<T> red[33];
+  DluState<T>* st = p.st;
+  if (st->done) {
+    for (int c = threadIdx.x; c < p.n; c += blockDim.x) p.U[c] = T(0);
+    return;
+  }
+  const Cand<T> none{T(-1), 0x7fffffff, 0, 0x7fffffffffffffffll, 0};
+  Cand<T> g = none;
+  for (int q = threadIdx.x; q < total; q += blockDim.x) {
+    const Cand<T> x = load_cand_cg(p.cand_all + q);
+    if (better(x, g)) g = x;
+  }
+  g = block_best(g, red);
+  if (!(g.v > T(0))) {  // exactly-zero corner (FullPivLU early stop)
+    if (threadIdx.x == 0) {
+      st->done = 1;
+      st->k0 = k;
+    }
+    for (int c = threadIdx.x; c < p.n; c += blockDim.x) p.U[c] = T(0);
+    return;
+  }
+  const int owner = int(g.s >> 40);
+  const i64 sloc = g.s & ((i64(1) << 40) - 1);
+  if (threadIdx.x == 0) {
+    i64 u = -1;  // global id of the row at physical position k before the swap
+    for (int q = st->n_ov - 1; q >= 0; --q)
+      if (st->ov_pos[q] == k) {
+        u = st->ov_row[q];
+        break;
+      }
+    if (u < 0) u = k;
+    if (g.prow != k) {
+      st->ov_pos[st->n_ov] = g.prow;
+      st->ov_row[st->n_ov] = u;
+      st->n_ov += 1;
+      int uo;
+      i64 uloc;
+      dlu_locate(p.sm, u, uo, uloc);
+      if (uo == p.rank) p.phys[uloc] = g.prow;
+    }
+    const int colk = st->col_at[k];
+    st->col_at[k] = g.c;
+    st->col_at[g.pcol] = colk;
+    st->cs = g.c;
+    st->owner = owner;
+    st->srow = sloc;
+    if (owner == p.rank) p.phys[sloc] = k;
+  }
+  const i64 R = p.R;
+  const i64 base = (sloc / R) * p.n * R + (sloc % R);
+  for (int c = threadIdx.x; c < p.n; c += blockDim.x) p.U[c] = owner == p.rank ? p.A[base + c * R] : T(0);
+}
+
+}  // namespace
+
+size_t dlu_state_bytes() { return sizeof(DluState<double>); }
+
+template <typename T>
+int plu_basis_dist(T* A, T* Z, i64 J, i64 R, int n, i64 J_global, const KoldaMap& km, const SlabMap& sm, Comm& comm,
+                   const DluWork& w, cudaStream_t st) {
+  check_arg(n <= kMaxPanelCols, "plu_basis: panel wider than supported");
+  const int r = int(std::min<i64>(J_global, n));
+  init_row_keys(km, J, R, w.phys, st);
+  DluState<T>* state = reinterpret_cast<DluState<T>*>(w.state);
+  dlu_init_kernel<T><<<1, 256, 0, st>>>(state, n, r);
+  DluArgs<T> a{A, Z, J, R, n, r, w.phys, reinterpret_cast<Cand<T>*>(w.cand_loc),
+               reinterpret_cast<const Cand<T>*>(w.cand_all), reinterpret_cast<T*>(w.U), state, comm.rank, w.G, sm};
+  dlu_update_kernel<T><<<w.G, kDluThreads, 0, st>>>(a, -1);
+  count_launch(2);
+  for (int k = 0; k < r; ++k) {
+    comm.allgather(w.cand_loc, w.cand_all, size_t(w.G) * sizeof(Cand<T>), st);
+    dlu_pick_kernel<T><<<1, kDluThreads, 0, st>>>(a, k, w.G * comm.size);
+    comm.allreduce_sum(w.U, size_t(n), sizeof(T) == 8 ? CommType::f64 : CommType::f32, st);
+    dlu_update_kernel<T><<<w.G, kDluThreads, 0, st>>>(a, k);
+    count_launch(2);
+  }
+  RCPG_LAUNCHED();
+  return r;
+}
+
+template int plu_basis_dist<float>(float*, float*, i64, i64, int, i64, const KoldaMap&, const SlabMap&, Comm&,
+                                   const DluWork&, cudaStream_t);
+template int plu_basis_dist<double>(double*, double*, i64, i64, int, i64, const KoldaMap&, const SlabMap&, Comm&,
+                                    const DluWork&, cudaStream_t);
+
 size_t factor_cand_bytes() { return sizeof(Cand<double>); }
 
 template int plu_basis<float>(float*, float*, i64, i64, int, const KoldaMap&, FactorWork&, cudaStream_t);

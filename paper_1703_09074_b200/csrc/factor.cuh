@@ -2,6 +2,7 @@
 // Tall-skinny factorizations (plu_basis / thin_qr), see factor.cu.
 #pragma once
 
+#include "comm.cuh"
 #include "common.cuh"
 
 namespace rcpg {
@@ -24,6 +25,34 @@ struct FactorWork {
 };
 
 size_t factor_cand_bytes();
+
+// ------------------------------------------------ sharded
+constexpr int kDluMaxRanks = 64;
+
+// Locates a global panel row (its Kolda index) among the slabs of the last
+// mode: kmg is the unsharded Kolda map, Rg the unsharded R of the mode view.
+struct SlabMap {
+  KoldaMap kmg;
+  i64 Rg = 1, Es = 1;
+  int nranks = 1;
+  i64 lo[kDluMaxRanks] = {}, hi[kDluMaxRanks] = {};
+};
+
+struct DluWork {
+  i64* phys = nullptr;        // [J local]
+  void* cand_loc = nullptr;   // [G] candidates
+  void* cand_all = nullptr;   // [nranks][G]
+  void* U = nullptr;          // [n] pivot row
+  void* state = nullptr;      // dlu_state_bytes()
+  int G = 0;                  // CTAs per rank (equal on all ranks)
+};
+size_t dlu_state_bytes();
+
+// Row-sharded FullPivLU (P^{-1} L of the rows this rank holds); km maps the
+// local rows to their global Kolda index (high_last_off set). Returns r.
+template <typename T>
+int plu_basis_dist(T* A, T* Z, i64 J, i64 R, int n, i64 J_global, const KoldaMap& km, const SlabMap& sm, Comm& comm,
+                   const DluWork& w, cudaStream_t st);
 
 void init_row_keys(const KoldaMap& km, i64 J, i64 R, i64* keys, cudaStream_t st);
 

@@ -180,13 +180,13 @@ void project(const T* X, ModeView v, const T* Q, i64 ldq, i64 cols, T* O, cudaSt
 // ---------------------------------------------------------------- Omega
 namespace {
 template <typename T>
-__global__ void omega_panel_kernel(u64 s0, KoldaMap km, i64 J, i64 R, i64 cols, int distribution, T* P) {
+__global__ void omega_panel_kernel(u64 s0, KoldaMap km, i64 J, i64 R, i64 cols, int distribution, T* P, i64 Jg) {
   for (i64 s = blockIdx.x * i64(blockDim.x) + threadIdx.x; s < J; s += i64(gridDim.x) * blockDim.x) {
     const i64 a = s / R, b = s - a * R;
     const i64 j = kolda_index(km, a, b);
     T* dst = P + a * cols * R + b;
     for (i64 c = 0; c < cols; ++c) {
-      const u64 e = u64(c) * u64(J) + u64(j);
+      const u64 e = u64(c) * u64(Jg) + u64(j);  // Jg: rows of the (global) unfolding
       const double v = distribution == 0 ? normal_at(s0, e) : uniform_sym_at(s0, e);
       dst[c * R] = T(v);
     }
@@ -196,11 +196,11 @@ __global__ void omega_panel_kernel(u64 s0, KoldaMap km, i64 J, i64 R, i64 cols, 
 
 template <typename T>
 void omega_panel(u64 seed, i64 mode, const KoldaMap& km, ModeView v, i64 cols, int distribution, T* P,
-                 cudaStream_t st) {
+                 cudaStream_t st, i64 J_global) {
   const u64 s0 = derive_seed(seed, stream_id(kDomainCompress, u64(mode)));
   const i64 J = v.L * v.R;
   const int blocks = int(std::max<i64>(1, std::min<i64>(ceil_div(J, 256), 148 * 16)));
-  omega_panel_kernel<T><<<blocks, 256, 0, st>>>(s0, km, J, v.R, cols, distribution, P);
+  omega_panel_kernel<T><<<blocks, 256, 0, st>>>(s0, km, J, v.R, cols, distribution, P, J_global > 0 ? J_global : J);
   count_launch();
   RCPG_LAUNCHED();
 }
@@ -209,7 +209,7 @@ void omega_panel(u64 seed, i64 mode, const KoldaMap& km, ModeView v, i64 cols, i
   template i64 sketch_scratch_elems<T>(ModeView, i64, int);                                              \
   template void sketch<T>(const T*, ModeView, const T*, i64, T*, T*, i64, int, cudaStream_t, const int*);             \
   template void project<T>(const T*, ModeView, const T*, i64, i64, T*, cudaStream_t);                    \
-  template void omega_panel<T>(u64, i64, const KoldaMap&, ModeView, i64, int, T*, cudaStream_t);
+  template void omega_panel<T>(u64, i64, const KoldaMap&, ModeView, i64, int, T*, cudaStream_t, i64);
 RCPG_INST(float)
 RCPG_INST(double)
 #undef RCPG_INST

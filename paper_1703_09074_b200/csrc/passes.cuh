@@ -300,6 +300,6 @@ void project_tc(const float* X, ModeView v, const float* Q, i64 ldq, i64 cols, f
 // uniform_sym number c*J + kolda(s) of stream (seed, (compress << 32) | mode).
 template <typename T>
 void omega_panel(u64 seed, i64 mode, const KoldaMap& km, ModeView v, i64 cols, int distribution, T* P,
-                 cudaStream_t st);
+                 cudaStream_t st, i64 J_global = 0);
 
 }  // namespace rcpg

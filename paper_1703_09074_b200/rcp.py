@@ -176,6 +176,18 @@ class Context:
         except Exception:
             pass
 
+    # ----- sharding: one context per rank / GPU
+    def comm_init_nccl(self, nranks: int, rank: int, unique_id: bytes) -> None:
+        """Join an NCCL communicator (unique_id from comm_unique_id() on rank 0, broadcast by the caller)."""
+        assert len(unique_id) == 128
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        self.check(self.lib.rcpg_comm_init_nccl(self.h, int(nranks), int(rank), buf))
+
+    def comm_rank(self) -> Tuple[int, int]:
+        r, n = C.c_int32(), C.c_int32()
+        self.lib.rcpg_comm_rank(self.h, C.byref(r), C.byref(n))
+        return r.value, n.value
+
     def check(self, status: int) -> None:
         if status == _L.RCPG_OK:
             return
@@ -242,11 +254,32 @@ def _dtype_code(dt) -> int:
 class DeviceTensor:
     """A tensor resident in HBM (rcpg_tensor)."""
 
-    def __init__(self, ctx: Context, handle, shape, dtype):
+    def __init__(self, ctx: Context, handle, shape, dtype, global_shape=None, slab=None):
         self.ctx = ctx
         self.h = handle
-        self.shape = tuple(int(e) for e in shape)
+        self.shape = tuple(int(e) for e in shape)  # local shape (a slab's last extent is hi - lo)
         self.dtype = np.dtype(dtype)
+        self.global_shape = tuple(int(e) for e in (global_shape if global_shape is not None else shape))
+        self.slab_range = slab  # (lo, hi) along the last mode, or None
+
+    def slab(self, lo: int, hi: int, ctx: Optional[Context] = None) -> "DeviceTensor":
+        """Slab [lo, hi) of the last mode (a device copy) for a sharded decomposition."""
+        ctx = ctx or self.ctx
+        h = C.c_void_p()
+        ctx.check(ctx.lib.rcpg_tensor_slab(ctx.h, self.h, int(lo), int(hi), C.byref(h)))
+        return DeviceTensor(ctx, h, self.shape[:-1] + (int(hi) - int(lo),), self.dtype, self.shape, (int(lo), int(hi)))
+
+    @classmethod
+    def upload_slab(cls, x_slab: np.ndarray, global_shape: Sequence[int], lo: int, hi: int,
+                    ctx: Optional[Context] = None) -> "DeviceTensor":
+        """Upload this rank's slab (row-major, last extent hi - lo) of a tensor of `global_shape`."""
+        ctx = ctx or default_context()
+        x = np.ascontiguousarray(x_slab)
+        gs = np.asarray(global_shape, dtype=np.int64)
+        h = C.c_void_p()
+        ctx.check(ctx.lib.rcpg_tensor_upload_slab(ctx.h, _dtype_code(x.dtype), len(gs), gs.ctypes.data, int(lo),
+                                                  int(hi), x.ctypes.data, C.byref(h)))
+        return cls(ctx, h, x.shape, x.dtype, tuple(global_shape), (int(lo), int(hi)))
 
     @classmethod
     def upload(cls, x: np.ndarray, ctx: Optional[Context] = None) -> "DeviceTensor":
@@ -286,6 +319,29 @@ class DeviceTensor:
             self.free()
         except Exception:
             pass
+
+
+def comm_unique_id() -> bytes:
+    """128-byte NCCL unique id (create on rank 0, broadcast, then Context.comm_init_nccl on every rank)."""
+    lib = _L.lib()
+    buf = C.create_string_buffer(128)
+    st = lib.rcpg_comm_unique_id(buf)
+    if st != _L.RCPG_OK:
+        raise CudaError(f"rcpg_comm_unique_id failed with status {st}")
+    return buf.raw
+
+
+def comm_init_loopback(contexts: Sequence[Context]) -> None:
+    """Virtual ranks in one process (contexts[r] is rank r, one host thread each, any GPU)."""
+    arr = (C.c_void_p * len(contexts))(*[c.h.value if isinstance(c.h, C.c_void_p) else c.h for c in contexts])
+    contexts[0].check(contexts[0].lib.rcpg_comm_init_loopback(arr, len(contexts)))
+
+
+def slab_range(extent: int, nranks: int, rank: int) -> Tuple[int, int]:
+    """The balanced split [lo, hi) of [0, extent) that rank `rank` holds (host only)."""
+    lo, hi = C.c_int64(), C.c_int64()
+    _L.lib().rcpg_slab_range(int(extent), int(nranks), int(rank), C.byref(lo), C.byref(hi))
+    return lo.value, hi.value
 
 
 def _as_device(x, ctx):
@@ -336,7 +392,7 @@ def decompose(t, cfg: DecomposeConfig, ctx: Optional[Context] = None) -> Tuple[K
         R = max(int(cfg.rank), 1)
         cap = max(int(cfg.max_iter), 1)
         w = np.zeros(R, dtype=dt.dtype)
-        f = np.zeros(sum(dt.shape) * R, dtype=dt.dtype)
+        f = np.zeros(sum(dt.global_shape) * R, dtype=dt.dtype)
         ti = np.zeros(cap, dtype=np.int32)
         tf = np.zeros(cap, dtype=np.float64)
         ts = np.zeros(cap, dtype=np.float64)
@@ -349,7 +405,7 @@ def decompose(t, cfg: DecomposeConfig, ctx: Optional[Context] = None) -> Tuple[K
         res.trace_capacity = cap
         ctx.check(ctx.lib.rcpg_decompose(ctx.h, dt.h, C.byref(c), C.byref(res)))
         facs, off = [], 0
-        for e in dt.shape:
+        for e in dt.global_shape:
             facs.append(f[off:off + e * R].reshape((e, R), order="F").copy(order="F"))
             off += e * R
         n = int(res.iterations)
