@@ -62,6 +62,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: N independent decompositions instead of one sharded along the last mode")
+    ap.add_argument("--shard", action="store_true",
+                    help="force the sharded path (NCCL communicator) also at N = 1")
     return ap.parse_args()
 
 
@@ -79,8 +83,13 @@ class Dist:
         if world > 1:
             import torch
             import torch.distributed as td
-            torch.cuda.set_device(local)
-            td.init_process_group("nccl", device_id=torch.device("cuda", local))
+            if torch.cuda.is_available():
+                torch.cuda.set_device(local)
+                td.init_process_group("nccl", device_id=torch.device("cuda", local))
+                self.dev = "cuda"
+            else:  # host-side tests (gloo, world_size 2 on CPU)
+                td.init_process_group("gloo")
+                self.dev = "cpu"
             self.td, self.torch = td, torch
 
     def barrier(self):
@@ -90,9 +99,17 @@ class Dist:
     def max(self, v: float) -> float:
         if self.world == 1:
             return v
-        t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda")
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.dev)
         self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
         return float(t.item())
+
+    def broadcast_bytes(self, b: bytes, root: int = 0) -> bytes:
+        """Rank root's bytes on every rank (the NCCL unique id of the library's communicator)."""
+        if self.world == 1:
+            return b
+        t = self.torch.tensor(list(b), dtype=self.torch.uint8, device=self.dev)
+        self.td.broadcast(t, src=root)
+        return bytes(t.cpu().tolist())
 
     def close(self):
         if self.world > 1:
@@ -229,6 +246,8 @@ def cpu_baseline(cfg, x_host, c):
 
 def main():
     args = parse()
+    # stdout carries exactly one JSON line: keep NCCL's version banner off it
+    os.environ["NCCL_DEBUG"] = os.environ.get("RCPG_NCCL_DEBUG", "WARN")
     world, rank, local = dist_env()
     dist = Dist(world, rank, local)
     from paper_1703_09074_b200.synthetic import CONFIGS
@@ -241,8 +260,20 @@ def main():
     import paper_1703_09074_b200 as rcp
     from paper_1703_09074_b200 import synthetic
     ctx = rcp.Context(local)
+    # N > 1: one decomposition sharded in slabs along the last mode, the
+    # library's own NCCL communicator (id broadcast through torch.distributed)
+    shard = (world > 1 and not args.replicas) or args.shard
+    if shard:
+        uid = dist.broadcast_bytes(rcp.comm_unique_id() if rank == 0 else bytes(128))
+        ctx.comm_init_nccl(world, rank, uid)
     w, facs = synthetic.model(cfg.kind, cfg.shape, cfg.rank, cfg.seed)
     X = rcp.DeviceTensor.synth(cfg.shape, w, facs, cfg.snr, cfg.seed, dtype=cfg.dtype, ctx=ctx)
+    slo, shi = 0, cfg.shape[-1]
+    if shard:
+        slo, shi = rcp.slab_range(cfg.shape[-1], world, rank)
+        Xs = X.slab(slo, shi)
+        X.free()
+        X = Xs
     c = configs(cfg, rcp)
     dcfg = rcp.DecomposeConfig(rank=c["rank"], tol=c["tol"], max_iter=c["max_iter"], seed=c["seed"],
                                compress=rcp.CompressConfig(**c["compress"]))
@@ -271,20 +302,30 @@ def main():
     x_host = None
     if not args.no_e2e or (rank == 0 and world == 1 and not args.no_cpu_baseline):
         x_host = X.download()
+    def e2e_step():
+        if not shard:
+            return rcp.decompose(x_host, dcfg, ctx=ctx)
+        t = rcp.DeviceTensor.upload_slab(x_host, cfg.shape, slo, shi, ctx=ctx)
+        try:
+            return rcp.decompose(t, dcfg, ctx=ctx)
+        finally:
+            t.free()
+
     if not args.no_e2e:
         ctx.host_register(x_host)
         for _ in range(max(1, args.warmup // 2)):
-            rcp.decompose(x_host, dcfg, ctx=ctx)
+            e2e_step()
         ctx.synchronize()
         dist.barrier()
         ctx.event_record(2)
         for _ in range(args.steps):
-            m2, t2 = rcp.decompose(x_host, dcfg, ctx=ctx)
+            m2, t2 = e2e_step()
         ctx.event_record(3)
         e2e_ms = dist.max(ctx.event_elapsed_ms(2, 3) / args.steps)
         ctx.host_unregister(x_host)
         d2h = (cfg.rank + sum(cfg.shape) * cfg.rank) * np.dtype(cfg.dtype).itemsize + 2 * 8 * t2.iterations
-        e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": int(x_host.nbytes), "d2h_bytes_per_step": int(d2h)}
+        h2d = int(x_host.nbytes) * (world if shard else 1)  # every rank uploads its slab
+        e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(d2h)}
 
     if rank == 0:
         peak, peak_kind = measured_peaks()
@@ -297,12 +338,14 @@ def main():
         line = {
             "metric": "rCP time-to-solution", "value": ms_step, "unit": "ms", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if cfg.dtype == np.float64 else "f32",
+            "scaling": "strong" if shard else "weak", "vs_baseline": None,
+            "dtype": "f64" if cfg.dtype == np.float64 else "f32",
             "data": "synthetic (device-generated Kruskal model + add_noise, BASELINE.json shape/distribution)",
             "config": {"workload": f"{cfg.name}: {'x'.join(map(str, cfg.shape))} rank {cfg.rank} "
                                    f"p={cfg.oversampling} q={cfg.power_iterations} tol={cfg.tol:g} "
                                    f"max_iter={cfg.max_iter}",
-                       "parallelism": "replicas" if world > 1 else "single GPU",
+                       "parallelism": (f"slab-sharded along the last mode over {world} GPUs (NCCL)" if shard
+                                       else ("replicas" if world > 1 else "single GPU")),
                        "l2": "tensor larger than L2 (no flush needed)" if cfg.nbytes() > 126e6 else "L2-resident"},
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

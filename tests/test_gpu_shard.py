@@ -109,3 +109,15 @@ def test_sharded_rejects_unsupported(rcp, oracle):
     det = rcp.DecomposeConfig(rank=3, randomized=False, tol=1e-8, max_iter=50)
     with pytest.raises(ValueError, match="randomized"):
         _run_ranks(rcp, x, 1, lambda t, c: rcp.decompose(t, det, ctx=c))
+
+
+def test_sharded_through_nccl_single_rank(rcp, oracle):
+    """The NCCL communicator (loaded at run time) on one rank: same result as unsharded."""
+    x, _ = oracle.random_lowrank([30, 26, 22], 3, 17, snr=3.0, noise_seed=17)
+    cfg = _cfg(rcp, 3, 4, 2, 17)
+    want = rcp.decompose(x, cfg)
+    ctx = rcp.Context(0)
+    ctx.comm_init_nccl(1, 0, rcp.comm_unique_id())
+    assert ctx.comm_rank() == (0, 1)
+    t = rcp.DeviceTensor.upload_slab(x, x.shape, 0, x.shape[-1], ctx=ctx)
+    _check_vs_single(rcp.decompose(t, cfg, ctx=ctx), want, 1e-8)
