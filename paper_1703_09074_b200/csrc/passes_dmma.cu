@@ -21,7 +21,7 @@ namespace {
 
 constexpr int kDThreads = 128;  // 4 warps, each a 16-row slab of the CTA tile
 constexpr int kDBM = 64;
-constexpr int kDBK = 32;
+constexpr int kDBK = 16;  // 16: four CTAs (16 warps) per SM hide the DMMA accumulator latency
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool ok) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
@@ -257,7 +257,15 @@ void launch_project(dim3 grid, const double* X, const double* Q, ModeView v, i64
 i64 sketch_dmma_splits(ModeView v, i64 cols, int num_sms, i64& tps, i64& total) {
   const i64 mt = ceil_div(v.I, kDBM), nt = ceil_div(cols, pick_bn8(cols));
   total = v.L * ceil_div(v.R, kDBK);
-  i64 want = ceil_div(i64(4) * num_sms, mt * nt);
+  // whole waves of resident CTAs: a grid a few CTAs over a wave boundary
+  // leaves most SMs idle for the last wave (residency from the smem plan,
+  // capped by registers: ~80 per thread x 128 threads)
+  const int bn = pick_bn8(cols);
+  const int S = bn <= 32 ? 4 : (bn <= 48 ? 3 : 2);
+  const i64 smem = i64(S) * (kDBM + bn) * (kDBK + 4) * 8 + 1024;
+  const i64 per_sm = std::max<i64>(1, std::min<i64>(6, (227 * 1024) / smem));
+  const i64 slots = per_sm * i64(num_sms), waves = 2;
+  i64 want = std::max<i64>(1, (waves * slots) / (mt * nt));
   want = std::max<i64>(1, std::min<i64>(want, 65535));
   tps = std::max<i64>(1, ceil_div(total, want));
   return ceil_div(total, tps);
