@@ -7,8 +7,10 @@
 // of launches with no host round trip; each launch first checks the
 // device-side `done` flag so the host can enqueue iterations ahead.
 #include <cfloat>
+#include <type_traits>
 
 #include "als.cuh"
+#include "passes.cuh"
 #include "rng.cuh"
 #include "runtime.cuh"
 
@@ -1257,12 +1259,27 @@ void norm_and_finite(const T* x, i64 n, double* out2, double* scratch, int num_s
   RCPG_LAUNCHED();
 }
 
-size_t residual_scratch_doubles(int num_sms) { return size_t(num_sms) * 8 * 2 + 16; }
+size_t residual_scratch_doubles(int num_sms, i64 last_extent, int rank) {
+  // per-CTA partial pairs (+ the C^T hi / lo planes of the tensor-core path)
+  return size_t(num_sms) * 8 * 2 + 16 + (residual_tc_scratch_floats(last_extent, rank) + 1) / 2 + 16;
+}
 
 template <typename T>
 void residual_norms(const T* X, const i64* shape, int order, const FactorSet<T>& fs, const T* weights,
                     double* out2, double* scratch, int num_sms, cudaStream_t st) {
   check_arg(fs.rank <= kMaxRank, "relative_error: rank above the supported maximum");
+  if constexpr (std::is_same<T, float>::value) {
+    if (tc_residual_ok(shape, order, fs.rank)) {  // Xhat on the tensor cores (passes_tc.cu)
+      int blocks = 0;
+      double* part = scratch;
+      float* ct = reinterpret_cast<float*>(scratch + size_t(num_sms) * 2 + 16);
+      residual_tc(X, shape, order, fs.f, weights, fs.rank, ct, part, num_sms, blocks, st);
+      sum_pairs_kernel<<<1, 256, 0, st>>>(part, blocks, out2);
+      count_launch();
+      RCPG_LAUNCHED();
+      return;
+    }
+  }
   const ShapeArg sh = make_shape(shape, order);
   i64 prefix = 1;
   for (int m = 0; m < order - 1; ++m) prefix *= shape[m];

@@ -85,7 +85,7 @@ void norm_and_finite(const T* x, i64 n, double* out2 /* [2]: sumsq, nonfinite */
 template <typename T>
 void residual_norms(const T* X, const i64* shape, int order, const FactorSet<T>& fs, const T* weights,
                     double* out2, double* scratch, int num_sms, cudaStream_t st);
-size_t residual_scratch_doubles(int num_sms);
+size_t residual_scratch_doubles(int num_sms, i64 last_extent, int rank);
 
 
 // Dense reconstruction of a model given in double + add_noise (synthetic data).

@@ -932,7 +932,7 @@ void run_relerr(rcpg_context* c, const T* X, const i64* shape, int order, const 
   const int sms = device_caps().num_sms;
   i64 S = 1;
   for (int m = 0; m < order; ++m) S *= shape[m];
-  c->scratch.ensure(residual_scratch_doubles(sms) * sizeof(double));
+  c->scratch.ensure(residual_scratch_doubles(sms, shape[order - 1], fs.rank) * sizeof(double));
   {
     // exact streamed residual: the Gram form ||X||^2 - 2<X,Xhat> + ||Xhat||^2
     // cancels badly in fp32 (a fp32-accumulated MTTKRP over ~10^6 terms)
@@ -957,7 +957,7 @@ void run_relerr_sharded(rcpg_context* c, const rcpg_tensor* t, const FactorSet<T
                                 cudaMemcpyDeviceToDevice, c->st));
   loc.f[sm_] = c->sh_fac.as<T>();
   loc.extent[sm_] = Iloc;
-  c->scratch.ensure(residual_scratch_doubles(sms) * sizeof(double));
+  c->scratch.ensure(residual_scratch_doubles(sms, t->shape[t->order - 1], fs.rank) * sizeof(double));
   {
     ScopedPass sp(c, "relerr", double(t->size) * sizeof(T));
     if (Iloc > 0) {

@@ -295,6 +295,12 @@ void sketch_tc(const float* X, ModeView v, const float* P, i64 cols, float* part
                cudaStream_t st);
 void project_tc(const float* X, ModeView v, const float* Q, i64 ldq, i64 cols, float* O, int num_sms,
                 cudaStream_t st);
+// ||X - Xhat||^2, ||X||^2 partials per CTA (part[2 * blocks]) with Xhat on tcgen05;
+// rank <= 64, last extent % 4 == 0. ct_scratch: residual_tc_scratch_floats().
+bool tc_residual_ok(const i64* shape, int order, int rank);
+size_t residual_tc_scratch_floats(i64 E, int rank);
+void residual_tc(const float* X, const i64* shape, int order, const float* const* factors, const float* weights,
+                 int rank, float* ct_scratch, double* part, int num_sms, int& blocks, cudaStream_t st);
 
 // Omega_n written in the panel layout (a, c, b): entry (s, c) is normal /
 // uniform_sym number c*J + kolda(s) of stream (seed, (compress << 32) | mode).

@@ -385,6 +385,243 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 
 constexpr i64 kMaxCoord = (i64(1) << 31) - 1;
 
+// ------------------------------------------------- residual (relerr)
+// ||X - Xhat||^2 and ||X||^2 with Xhat on tcgen05 (kruskal.hpp:187-194):
+// rows p of X (all modes but the last, row-major) x the last mode k,
+//   Xhat[p, k] = sum_r coef[p, r] C[k, r],  coef[p, r] = lambda_r prod_m A_m[d_m(p), r],
+// an M = 128 (p) x N = 128 (k) x K = R (padded) GEMM per work item, 3xTF32.
+// The coef rows are formed by the epilogue warps (lane = row = TMEM lane)
+// and stored hi / lo into TMEM (A operand); C^T hi / lo (K-major, prepared
+// once) and the X tile arrive by TMA; the epilogue reads Xhat from TMEM and
+// X from smem and accumulates both sums in fp64. Out-of-range rows / columns
+// are zero on both sides (zero coef, TMA zero fill), so they add nothing.
+constexpr int kResMaxOrder = 8;
+constexpr int kRBM = 128, kRBN = 64;
+constexpr int kResThreads = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 coef + epilogue
+
+struct ResArgs {
+  i64 P, E;
+  int R, N;                      // rank, tensor order
+  i64 ext[kResMaxOrder];         // extents of modes 0 .. N-2
+  const float* f[kResMaxOrder];
+  const float* w;
+  i64 mtiles, ntiles, items, chunk;
+  double* part;  // [gridDim][2]
+};
+
+// Items are (m-tile, n-tile) with the n-tile fastest: the coef rows of an
+// m-tile are formed once and stay in TMEM for all of its n-tiles; each item
+// streams its X tile and its C^T tile (hi | lo) through a 2-stage ring.
+template <int KP>
+struct ResPlan {
+  static constexpr int KB = KP / 32;                  // 32-wide swizzle boxes along K
+  static constexpr int B_PLANE = KP * kRBN * 4;       // one plane of the C^T tile
+  static constexpr int X_BYTES = kRBM * kRBN * 4;     // 32 KB: 2 boxes of 32 columns
+  static constexpr int STAGE = X_BYTES + 2 * B_PLANE;
+  static constexpr int SMEM = 2 * STAGE + 1024;
+  static constexpr uint32_t ACOL = 0;                 // A slots: 2 x (hi KP | lo KP)
+  static constexpr uint32_t DCOL = 4 * KP;            // accumulators: 2 x kRBN
+  static constexpr uint32_t TMEM_COLS = 512;
+  static constexpr uint32_t IDESC = idesc_tf32(kRBM, kRBN, 0, 0);
+  static_assert(DCOL + 2 * kRBN <= TMEM_COLS, "TMEM plan");
+};
+
+template <int KP>
+__global__ void __launch_bounds__(kResThreads, 1)
+    residual_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmBh,
+                       const __grid_constant__ CUtensorMap tmBl, ResArgs p) {
+  using G = ResPlan<KP>;
+  extern __shared__ unsigned char smem_dyn[];
+  unsigned char* smem = smem_dyn + ((1024 - (smem_u32(smem_dyn) & 1023)) & 1023);
+  __shared__ __align__(8) uint64_t full[2], empty[2], afull[2], aempty[2], accf[2], acce[2];
+  __shared__ uint32_t tmem_sh;
+  __shared__ double red[2][8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const i64 c0 = i64(blockIdx.x) * p.chunk;
+  const i64 c1 = c0 + p.chunk < p.items ? c0 + p.chunk : p.items;
+  const int n_items = c1 > c0 ? int(c1 - c0) : 0;
+  const i64 mt0 = c0 / p.ntiles;  // first m-tile of this CTA; A slot of m-tile mt = (mt - mt0) & 1
+
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], 128);
+      mbar_init(&afull[b], 128);
+      mbar_init(&aempty[b], 1);
+      mbar_init(&accf[b], 1);
+      mbar_init(&acce[b], 128);
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&tmX);
+    tma_prefetch_desc(&tmBh);
+    tma_prefetch_desc(&tmBl);
+  }
+  if (warp == 1) tmem_alloc(&tmem_sh, G::TMEM_COLS);
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem = tmem_sh;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      for (int j = 0; j < n_items; ++j) {
+        const i64 id = c0 + j, mt = id / p.ntiles, nt = id - mt * p.ntiles;
+        const int s = j & 1;
+        if (j >= 2) mbar_wait(&empty[s], uint32_t(((j >> 1) - 1) & 1));
+        unsigned char* st = smem + s * G::STAGE;
+        mbar_arrive_tx(&full[s], G::STAGE);
+#pragma unroll
+        for (int g = 0; g < kRBN / 32; ++g)
+          tma_load_2d(st + g * (kRBM * 128), &tmX, int(nt * kRBN) + 32 * g, int(mt * kRBM), &full[s]);
+#pragma unroll
+        for (int kb = 0; kb < G::KB; ++kb) {
+          tma_load_2d(st + G::X_BYTES + kb * (kRBN * 128), &tmBh, 32 * kb, int(nt * kRBN), &full[s]);
+          tma_load_2d(st + G::X_BYTES + G::B_PLANE + kb * (kRBN * 128), &tmBl, 32 * kb, int(nt * kRBN), &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      for (int j = 0; j < n_items; ++j) {
+        const i64 id = c0 + j, mt = id / p.ntiles, nt = id - mt * p.ntiles;
+        const int s = j & 1, buf = j & 1, u = int((mt - mt0) & 1);
+        const int tloc = int(mt - mt0);
+        const bool first = (nt == 0 || j == 0), last = (nt == p.ntiles - 1 || j == n_items - 1);
+        mbar_wait(&full[s], uint32_t((j >> 1) & 1));
+        if (first) mbar_wait(&afull[u], uint32_t((tloc >> 1) & 1));
+        if (j >= 2) mbar_wait(&acce[buf], uint32_t(((j >> 1) - 1) & 1));
+        fence_after_sync();
+        const uint32_t d = tmem + G::DCOL + uint32_t(buf) * kRBN;
+        const uint32_t ah = tmem + G::ACOL + uint32_t(u) * 2 * KP, al = ah + KP;
+        const uint32_t bh0 = smem_u32(smem + s * G::STAGE + G::X_BYTES), bl0 = bh0 + G::B_PLANE;
+#pragma unroll
+        for (int k8 = 0; k8 < KP / 8; ++k8) {
+          const uint32_t off = uint32_t((k8 >> 2) * (kRBN * 128) + (k8 & 3) * 32);
+          const uint64_t bh = sdesc_sw128(bh0 + off), bl = sdesc_sw128(bl0 + off);
+          mma_tf32_ta(d, al + 8 * k8, bh, G::IDESC, k8 > 0 ? 1u : 0u);
+          mma_tf32_ta(d, ah + 8 * k8, bl, G::IDESC, 1u);
+          mma_tf32_ta(d, ah + 8 * k8, bh, G::IDESC, 1u);
+        }
+        mma_commit(&accf[buf]);
+        if (last) mma_commit(&aempty[u]);
+      }
+    }
+  } else {
+    // ------------------------------------- coef rows + residual epilogue
+    const int qd = warp & 3;
+    const int m = qd * 32 + lane;
+    const uint32_t my_lanes = tmem + tmem_lane(qd);
+    double acc_r = 0.0, acc_x = 0.0;
+    for (int j = 0; j <= n_items; ++j) {
+      if (j < n_items) {
+        const i64 id = c0 + j, mt = id / p.ntiles, nt = id - mt * p.ntiles;
+        if (nt == 0 || j == 0) {  // coef rows of a new m-tile -> A slot u
+          const int tloc = int(mt - mt0), u = tloc & 1;
+          const i64 prow = mt * kRBM + m;
+          const bool valid = prow < p.P;
+          i64 dig[kResMaxOrder];
+          {
+            i64 rem = valid ? prow : 0;
+            for (int q = p.N - 2; q >= 0; --q) {
+              dig[q] = rem % p.ext[q];
+              rem /= p.ext[q];
+            }
+          }
+          if (tloc >= 2) mbar_wait(&aempty[u], uint32_t(((tloc >> 1) - 1) & 1));
+          fence_after_sync();
+#pragma unroll
+          for (int h = 0; h < KP / 32; ++h) {
+            float hi[32], lo[32];
+#pragma unroll
+            for (int rr = 0; rr < 32; ++rr) {
+              const int r = 32 * h + rr;
+              hi[rr] = (valid && r < p.R) ? p.w[r] : 0.f;
+            }
+            for (int q = p.N - 2; q >= 0; --q) {  // all 32 loads of a mode in flight together
+              const float* fq = p.f[q] + dig[q];
+              const i64 eq = p.ext[q];
+              float fv[32];
+#pragma unroll
+              for (int rr = 0; rr < 32; ++rr) fv[rr] = (32 * h + rr < p.R) ? __ldg(fq + i64(32 * h + rr) * eq) : 0.f;
+#pragma unroll
+              for (int rr = 0; rr < 32; ++rr) hi[rr] *= fv[rr];
+            }
+#pragma unroll
+            for (int rr = 0; rr < 32; ++rr) lo[rr] = hi[rr] - __uint_as_float(__float_as_uint(hi[rr]) & 0xFFFFE000u);
+            tmem_st32(my_lanes + G::ACOL + uint32_t(u) * 2 * KP + 32 * h, hi);
+            tmem_st32(my_lanes + G::ACOL + uint32_t(u) * 2 * KP + KP + 32 * h, lo);
+          }
+          tmem_st_wait();
+          fence_before_sync();
+          mbar_arrive(&afull[u]);
+        }
+      }
+      if (j > 0) {
+        const int jj = j - 1, pb = jj & 1;
+        mbar_wait(&accf[pb], uint32_t((jj >> 1) & 1));
+        mbar_wait(&full[pb], uint32_t((jj >> 1) & 1));
+        fence_after_sync();
+        const unsigned char* xs = smem + pb * G::STAGE;
+        const uint32_t taddr = my_lanes + G::DCOL + uint32_t(pb) * kRBN;
+#pragma unroll 4
+        for (int c8 = 0; c8 < kRBN; c8 += 8) {
+          float xh[8];
+          tmem_ld8(taddr + c8, xh);
+          const unsigned char* box = xs + (c8 >> 5) * (kRBM * 128) + m * 128;
+          const int ch = (c8 & 31) >> 2;
+          const float4 x0 = *reinterpret_cast<const float4*>(box + (((ch) ^ (m & 7)) << 4));
+          const float4 x1 = *reinterpret_cast<const float4*>(box + (((ch + 1) ^ (m & 7)) << 4));
+          const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+          float sr = 0.f, sx = 0.f;  // 8-term partial sums, then fp64
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const float dd = xv[u] - xh[u];
+            sr = fmaf(dd, dd, sr);
+            sx = fmaf(xv[u], xv[u], sx);
+          }
+          acc_r += double(sr);
+          acc_x += double(sx);
+        }
+        fence_before_sync();
+        mbar_arrive(&acce[pb]);
+        mbar_arrive(&empty[pb]);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      acc_r += __shfl_xor_sync(0xffffffffu, acc_r, o);
+      acc_x += __shfl_xor_sync(0xffffffffu, acc_x, o);
+    }
+    if (lane == 0) {
+      red[0][warp - 2] = acc_r;
+      red[1][warp - 2] = acc_x;
+    }
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    p.part[2 * blockIdx.x] = ((red[0][0] + red[0][1]) + red[0][2]) + red[0][3];
+    p.part[2 * blockIdx.x + 1] = ((red[1][0] + red[1][1]) + red[1][2]) + red[1][3];
+  }
+  if (warp == 1) {
+    fence_after_sync();
+    tmem_dealloc(tmem, G::TMEM_COLS);
+  }
+}
+
+// C^T hi / lo planes (E x KP, K-major, zero beyond R) from the column-major last factor
+__global__ void residual_ct_kernel(const float* C, i64 E, int R, int KP, float* hi, float* lo) {
+  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < E * KP; e += i64(gridDim.x) * blockDim.x) {
+    const i64 k = e / KP;
+    const int r = int(e - k * KP);
+    const float v = r < R ? C[k + i64(r) * E] : 0.f;
+    hi[e] = v;
+    lo[e] = v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+  }
+}
+
 }  // namespace
 
 bool tc_enabled() {
@@ -464,6 +701,59 @@ void project_tc(const float* X, ModeView v, const float* Q, i64 ldq, i64 cols, f
   const CUtensorMap mq = tensor_map(Q, 2, qd, qs, qb);
   const int grid = int(std::min<i64>(a.items, num_sms));
   dispatch<true>(bn, mx, mq, a, grid, st);
+}
+
+bool tc_residual_ok(const i64* shape, int order, int rank) {
+  return tc_enabled() && order >= 2 && rank <= 64 && shape[order - 1] % 4 == 0 && shape[order - 1] <= kMaxCoord;
+}
+
+size_t residual_tc_scratch_floats(i64 E, int rank) { return size_t(2 * E * (rank <= 32 ? 32 : 64)); }
+
+void residual_tc(const float* X, const i64* shape, int order, const float* const* factors, const float* weights,
+                 int rank, float* ct_scratch, double* part, int num_sms, int& blocks, cudaStream_t st) {
+  const int KP = rank <= 32 ? 32 : 64;
+  ResArgs a{};
+  a.N = order;
+  a.R = rank;
+  a.E = shape[order - 1];
+  a.P = 1;
+  for (int m = 0; m < order - 1; ++m) {
+    a.ext[m] = shape[m];
+    a.f[m] = factors[m];
+    a.P *= shape[m];
+  }
+  a.w = weights;
+  a.mtiles = ceil_div(a.P, kRBM);
+  a.ntiles = ceil_div(a.E, kRBN);
+  a.items = a.mtiles * a.ntiles;
+  blocks = int(std::max<i64>(1, std::min<i64>(a.items, num_sms)));
+  a.chunk = ceil_div(a.items, blocks);
+  blocks = int(ceil_div(a.items, a.chunk));
+  a.part = part;
+  float* hi = ct_scratch;
+  float* lo = ct_scratch + a.E * KP;
+  residual_ct_kernel<<<int(std::min<i64>(ceil_div(a.E * KP, 256), 1024)), 256, 0, st>>>(factors[order - 1], a.E,
+                                                                                           rank, KP, hi, lo);
+  const cuuint64_t xd[2] = {cuuint64_t(a.E), cuuint64_t(a.P)};
+  const cuuint64_t xs[1] = {cuuint64_t(a.E) * 4};
+  const cuuint32_t xb[2] = {32, kRBM};
+  const cuuint64_t bd[2] = {cuuint64_t(KP), cuuint64_t(a.E)};
+  const cuuint64_t bs[1] = {cuuint64_t(KP) * 4};
+  const cuuint32_t bb[2] = {32, kRBN};
+  const CUtensorMap mx = tensor_map(X, 2, xd, xs, xb);
+  const CUtensorMap mh = tensor_map(hi, 2, bd, bs, bb);
+  const CUtensorMap ml = tensor_map(lo, 2, bd, bs, bb);
+  if (KP == 32) {
+    static const size_t lim = enable_max_dyn_smem(residual_tc_kernel<32>);
+    if (size_t(ResPlan<32>::SMEM) > lim) throw std::runtime_error("residual_tc: smem plan too large");
+    residual_tc_kernel<32><<<blocks, kResThreads, ResPlan<32>::SMEM, st>>>(mx, mh, ml, a);
+  } else {
+    static const size_t lim = enable_max_dyn_smem(residual_tc_kernel<64>);
+    if (size_t(ResPlan<64>::SMEM) > lim) throw std::runtime_error("residual_tc: smem plan too large");
+    residual_tc_kernel<64><<<blocks, kResThreads, ResPlan<64>::SMEM, st>>>(mx, mh, ml, a);
+  }
+  count_launch(2);
+  RCPG_LAUNCHED();
 }
 
 }  // namespace rcpg
