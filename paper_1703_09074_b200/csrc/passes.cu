@@ -192,6 +192,32 @@ __global__ void omega_panel_kernel(u64 s0, KoldaMap km, i64 J, i64 R, i64 cols, 
     }
   }
 }
+// Gaussian Omega, one Box-Muller pair per thread and column: entries e = c Jg + j
+// and e + 1 form pair e / 2 (cos, sin). With Jg even and j even they share the
+// column c, and j + 1 increments the fastest Kolda digit, whose storage stride
+// (in panel rows) is `sig` -- so the thread owning row s (that digit even)
+// writes rows s and s + sig, both coalesced across the warp, and every pair is
+// computed once instead of twice.
+template <typename T>
+__global__ void omega_pairs_kernel(u64 s0, KoldaMap km, i64 J, i64 R, i64 cols, T* P, i64 Jg, i64 sig, i64 Ef) {
+  const i64 half = J / 2;
+  for (i64 q = blockIdx.x * i64(blockDim.x) + threadIdx.x; q < half; q += i64(gridDim.x) * blockDim.x) {
+    const i64 lo = q % sig, rest = q / sig;
+    const i64 t = rest % (Ef / 2), hi = rest / (Ef / 2);
+    const i64 s = hi * Ef * sig + 2 * t * sig + lo;  // storage row with an even fastest Kolda digit
+    const i64 a = s / R, b = s - a * R;
+    const i64 s2 = s + sig, a2 = s2 / R, b2 = s2 - a2 * R;
+    const i64 j = kolda_index(km, a, b);
+    T* d1 = P + a * cols * R + b;
+    T* d2 = P + a2 * cols * R + b2;
+    for (i64 c = 0; c < cols; ++c) {
+      double cs, sn;
+      normal_pair(s0, (u64(c) * u64(Jg) + u64(j)) >> 1, cs, sn);
+      d1[c * R] = T(cs);
+      d2[c * R] = T(sn);
+    }
+  }
+}
 }  // namespace
 
 template <typename T>
@@ -199,8 +225,32 @@ void omega_panel(u64 seed, i64 mode, const KoldaMap& km, ModeView v, i64 cols, i
                  cudaStream_t st, i64 J_global) {
   const u64 s0 = derive_seed(seed, stream_id(kDomainCompress, u64(mode)));
   const i64 J = v.L * v.R;
+  const i64 Jg = J_global > 0 ? J_global : J;
+  // fastest Kolda digit: low mode 0 if there are low modes, else high mode 0;
+  // its stride in panel rows s = a R + b
+  i64 Ef, sig;
+  if (km.n_low > 0) {
+    Ef = km.low_ext[0];
+    sig = v.R;
+    for (int m = 1; m < km.n_low; ++m) sig *= km.low_ext[m];
+  } else {
+    Ef = km.n_high > 0 ? km.high_ext[0] : 1;
+    sig = 1;
+    for (int m = 1; m < km.n_high; ++m) sig *= km.high_ext[m];
+  }
+  // (a slab's last digit carries an offset but is never the fastest Kolda digit
+  // when there are other high modes; with one high mode Ef is its local extent)
+  const bool pairs = distribution == 0 && Jg % 2 == 0 && J % 2 == 0 && Ef % 2 == 0 && Ef >= 2 &&
+                     !(km.n_low == 0 && km.n_high == 1 && km.high_last_off % 2 != 0);
+  if (pairs) {
+    const int blocks = int(std::max<i64>(1, std::min<i64>(ceil_div(J / 2, 256), 148 * 16)));
+    omega_pairs_kernel<T><<<blocks, 256, 0, st>>>(s0, km, J, v.R, cols, P, Jg, sig, Ef);
+    count_launch();
+    RCPG_LAUNCHED();
+    return;
+  }
   const int blocks = int(std::max<i64>(1, std::min<i64>(ceil_div(J, 256), 148 * 16)));
-  omega_panel_kernel<T><<<blocks, 256, 0, st>>>(s0, km, J, v.R, cols, distribution, P, J_global > 0 ? J_global : J);
+  omega_panel_kernel<T><<<blocks, 256, 0, st>>>(s0, km, J, v.R, cols, distribution, P, Jg);
   count_launch();
   RCPG_LAUNCHED();
 }
