@@ -76,7 +76,9 @@ __device__ double block_reduce_sum(double v) {
 // Parallel cyclic Jacobi (round-robin pairs) on a symmetric n x n matrix in
 // global memory A (destroyed; diagonal -> eigenvalues), V <- eigenvectors.
 // On exit evals[0..n) ascending, order[0..n) the column of V for each.
-__device__ void jacobi_eig(double* A, double* V, int n, double* evals, int* order) {
+// A, V: n x n with leading dimension ld (odd ld keeps the row-wise rotations,
+// which stride by ld, off a single shared-memory bank)
+__device__ void jacobi_eig(double* A, double* V, int n, int ld, double* evals, int* order) {
   __shared__ double cs_c[kMaxRank * 8], cs_s[kMaxRank * 8];
   __shared__ int pp[kMaxRank * 8], pq[kMaxRank * 8];
   __shared__ int s_stop;
@@ -86,16 +88,16 @@ __device__ void jacobi_eig(double* A, double* V, int n, double* evals, int* orde
   // Gram) is treated exactly like the reference treats it.
   for (int e = tid; e < n * n; e += nt) {
     const int i = e % n, j = e / n;
-    if (i < j) A[e] = A[j + i * n];
+    if (i < j) A[i + j * ld] = A[j + i * ld];
   }
-  for (int e = tid; e < n * n; e += nt) V[e] = (e % n == e / n) ? 1.0 : 0.0;
+  for (int e = tid; e < n * n; e += nt) V[(e % n) + (e / n) * ld] = (e % n == e / n) ? 1.0 : 0.0;
   __syncthreads();
   const int m = n + (n & 1);  // players (one dummy when n is odd)
   const int npairs = m / 2;
   for (int sweep = 0; sweep < 60; ++sweep) {
     double off = 0.0, dg = 0.0;
     for (int e = tid; e < n * n; e += nt) {
-      const double x = A[e];
+      const double x = A[(e % n) + (e / n) * ld];
       if (e % n == e / n)
         dg += x * x;
       else
@@ -123,9 +125,9 @@ __device__ void jacobi_eig(double* A, double* V, int n, double* evals, int* orde
         }
         double c = 1.0, s = 0.0;
         if (j < n) {
-          const double apq = A[i + j * n];
+          const double apq = A[i + j * ld];
           if (apq != 0.0) {
-            const double app = A[i + i * n], aqq = A[j + j * n];
+            const double app = A[i + i * ld], aqq = A[j + j * ld];
             const double theta = (aqq - app) / (2.0 * apq);
             const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
             c = 1.0 / sqrt(t * t + 1.0);
@@ -145,9 +147,9 @@ __device__ void jacobi_eig(double* A, double* V, int n, double* evals, int* orde
         if (j >= n) continue;
         const double c = cs_c[q], s = cs_s[q];
         for (int k = lane; k < n; k += 32) {
-          const double akp = A[k + i * n], akq = A[k + j * n];
-          A[k + i * n] = c * akp - s * akq;
-          A[k + j * n] = s * akp + c * akq;
+          const double akp = A[k + i * ld], akq = A[k + j * ld];
+          A[k + i * ld] = c * akp - s * akq;
+          A[k + j * ld] = s * akp + c * akq;
         }
       }
       __syncthreads();
@@ -157,12 +159,12 @@ __device__ void jacobi_eig(double* A, double* V, int n, double* evals, int* orde
         if (j >= n) continue;
         const double c = cs_c[q], s = cs_s[q];
         for (int k = lane; k < n; k += 32) {
-          const double apk = A[i + k * n], aqk = A[j + k * n];
-          A[i + k * n] = c * apk - s * aqk;
-          A[j + k * n] = s * apk + c * aqk;
-          const double vkp = V[k + i * n], vkq = V[k + j * n];
-          V[k + i * n] = c * vkp - s * vkq;
-          V[k + j * n] = s * vkp + c * vkq;
+          const double apk = A[i + k * ld], aqk = A[j + k * ld];
+          A[i + k * ld] = c * apk - s * aqk;
+          A[j + k * ld] = s * apk + c * aqk;
+          const double vkp = V[k + i * ld], vkq = V[k + j * ld];
+          V[k + i * ld] = c * vkp - s * vkq;
+          V[k + j * ld] = s * vkp + c * vkq;
         }
       }
       __syncthreads();
@@ -170,13 +172,13 @@ __device__ void jacobi_eig(double* A, double* V, int n, double* evals, int* orde
   }
   // ascending, stable by index
   for (int i = tid; i < n; i += nt) {
-    const double di = order_key(A[i + i * n]);
+    const double di = order_key(A[i + i * ld]);
     int rank = 0;
     for (int j = 0; j < n; ++j) {
-      const double dj = order_key(A[j + j * n]);
+      const double dj = order_key(A[j + j * ld]);
       if (dj < di || (dj == di && j < i)) ++rank;
     }
-    evals[rank] = A[i + i * n];
+    evals[rank] = A[i + i * ld];
     order[rank] = i;
   }
   __syncthreads();
@@ -190,9 +192,10 @@ __global__ void __launch_bounds__(kSmallThreads) init_from_gram_kernel(const T* 
   const int tid = threadIdx.x, nt = blockDim.x;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const bool in_smem = n <= kEigSmemMax;  // A and V resident in shared memory
+  const int ld = n | 1;                   // odd leading dimension (bank spread)
   double* A = in_smem ? reinterpret_cast<double*>(smem_raw) : work;
-  double* V = A + i64(n) * n;
-  double* ev = work + 2 * i64(n) * n;
+  double* V = A + i64(n) * ld;
+  double* ev = work + 2 * i64(n) * ld;
   int* ord = reinterpret_cast<int*>(ev + n);
   double* col = ev + 2 * n;  // [n] padding scratch
   __shared__ int s_filled;
@@ -200,13 +203,13 @@ __global__ void __launch_bounds__(kSmallThreads) init_from_gram_kernel(const T* 
   __syncthreads();
   int filled = 0;
   if (method == 0) {
-    for (i64 e = tid; e < i64(n) * n; e += nt) A[e] = double(G[e]);
+    for (i64 e = tid; e < i64(n) * n; e += nt) A[(e % n) + (e / n) * ld] = double(G[e]);
     __syncthreads();
-    jacobi_eig(A, V, n, ev, ord);
+    jacobi_eig(A, V, n, ld, ev, ord);
     filled = R < n ? R : n;
     for (i64 e = tid; e < i64(n) * filled; e += nt) {
       const int i = int(e % n), j = int(e / n);
-      F[i + i64(j) * n] = T(V[i + i64(ord[n - 1 - j]) * n]);
+      F[i + i64(j) * n] = T(V[i + i64(ord[n - 1 - j]) * ld]);
     }
     __syncthreads();
     // canonicalize_column_signs (solve.hpp:77-84): first max |entry| >= 0
@@ -388,7 +391,7 @@ __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T
   if (!direct) {
     for (int e = tid; e < R2; e += nt) A[e] = V[e];
     __syncthreads();
-    jacobi_eig(A, X, R, ev, ord);
+    jacobi_eig(A, X, R, R, ev, ord);
     T lmax = T(0);
     for (int k = 0; k < R; ++k) lmax = T(ev[k]) > lmax ? T(ev[k]) : lmax;
     const T tau = T(R) * Traits<T>::eps * lmax;
@@ -1139,7 +1142,7 @@ template <typename T>
 void init_factor_from_gram(const T* G, int extent, int rank, int mode, u64 seed, int method, T* factor,
                            T* gram_out, double* work, cudaStream_t st) {
   check_arg(rank <= kMaxRank, "init_factors: rank above the supported maximum");
-  const size_t smem = extent <= kEigSmemMax ? 2 * size_t(extent) * extent * sizeof(double) : 0;
+  const size_t smem = extent <= kEigSmemMax ? 2 * size_t(extent) * size_t(extent | 1) * sizeof(double) : 0;
   static const size_t lim = enable_max_dyn_smem(init_from_gram_kernel<T>);
   (void)lim;
   init_from_gram_kernel<T><<<1, 256, smem, st>>>(G, extent, rank, mode, seed, method, factor, gram_out, work);
