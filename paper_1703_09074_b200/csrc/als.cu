@@ -579,9 +579,9 @@ constexpr int kAlsTiles = 8;  // 16x8 output tiles per warp: ceil(I/16) ceil(R/8
 
 __host__ __device__ constexpr int als_ld(int n) { return (n + 15) / 16 * 16 + 4; }
 
-template <typename T>
-__host__ __device__ constexpr i64 als_fib_doubles(i64 I) {  // [2][kAlsBatch][I] raw T, in doubles
-  return (2 * kAlsBatch * I * i64(sizeof(T)) + 15) / 16 * 2;
+template <typename T, int BATCH = kAlsBatch>
+__host__ __device__ constexpr i64 als_fib_doubles(i64 I) {  // [2][BATCH][I] raw T, in doubles
+  return (2 * BATCH * I * i64(sizeof(T)) + 15) / 16 * 2;
 }
 
 template <typename T>
@@ -603,9 +603,9 @@ __device__ __forceinline__ void als_dmma(double (&c)[4], double a0, double a1, d
                : "d"(a0), "d"(a1), "d"(b0));
 }
 
-template <typename T>
+template <typename T, int BATCH>
 __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p) {
-  __shared__ int pidx[kAlsBatch * kMaxOrder];
+  __shared__ int pidx[BATCH * kMaxOrder];
   __shared__ int sfoff[kMaxOrder], sext[kMaxOrder];
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* sm = reinterpret_cast<double*>(smem_raw);
@@ -638,10 +638,10 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
       // padded row strides (== 4 mod 16 doubles): the MMA fragment loads of
       // rows pp = 4 ks + tq hit distinct banks
       const int ldI = als_ld(int(I)), ldR = als_ld(R);
-      T* fibT = reinterpret_cast<T*>(sm);                  // [2][kAlsBatch][I], raw T (cp.async)
-      double* fibD = sm + als_fib_doubles<T>(I);           // [kAlsBatch][ldI], converted once
-      double* kc = fibD + kAlsBatch * ldI;                 // [kAlsBatch][ldR]
-      T* fsm = reinterpret_cast<T*>(kc + kAlsBatch * ldR); // other modes' factors, row-major (rank fastest)
+      T* fibT = reinterpret_cast<T*>(sm);                  // [2][BATCH][I], raw T (cp.async)
+      double* fibD = sm + als_fib_doubles<T, BATCH>(I);           // [BATCH][ldI], converted once
+      double* kc = fibD + BATCH * ldI;                 // [BATCH][ldR]
+      T* fsm = reinterpret_cast<T*>(kc + BATCH * ldR); // other modes' factors, row-major (rank fastest)
       {
         __syncthreads();
         if (tid == 0) {
@@ -665,15 +665,15 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
         }
         __syncthreads();
       }
-      // gather: thread tid always handles position pp = tid % kAlsBatch
+      // gather: thread tid always handles position pp = tid % BATCH
       auto gather = [&](i64 pb, int buf) {
-        const int pp = tid % kAlsBatch;
+        const int pp = tid % BATCH;
         const bool ok = pb + pp < j1;
         const unsigned s_ = unsigned(ok ? pb + pp : pb);
         const unsigned a = s_ / unsigned(Rr), b = s_ - a * unsigned(Rr);
         const T* src = p.B + i64(a) * I * Rr + b;
-        T* dst = fibT + buf * kAlsBatch * int(I) + pp * int(I);
-        for (int i = tid / kAlsBatch; i < int(I); i += nt / kAlsBatch) als_cp_elem(dst + i, src + i64(i) * Rr, ok);
+        T* dst = fibT + buf * BATCH * int(I) + pp * int(I);
+        for (int i = tid / BATCH; i < int(I); i += nt / BATCH) als_cp_elem(dst + i, src + i64(i) * Rr, ok);
         als_cp_commit();
       };
       const bool stampA = p.prof != nullptr && g == 0 && tid == 0;
@@ -688,14 +688,14 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
       if (j0 < j1) gather(j0, 0);
       stampa(16);
       int buf = 0;
-      for (i64 pb = j0; pb < j1; pb += kAlsBatch, buf ^= 1) {
-        const int np = int(j1 - pb < kAlsBatch ? j1 - pb : kAlsBatch);
-        if (pb + kAlsBatch < j1)
-          gather(pb + kAlsBatch, buf ^ 1);
+      for (i64 pb = j0; pb < j1; pb += BATCH, buf ^= 1) {
+        const int np = int(j1 - pb < BATCH ? j1 - pb : BATCH);
+        if (pb + BATCH < j1)
+          gather(pb + BATCH, buf ^ 1);
         else
           als_cp_commit();  // keep one group per iteration
         stampa(17);
-        if (tid < kAlsBatch) {  // multi-index digits of each position, once (32-bit: J < 2^31)
+        if (tid < BATCH) {  // multi-index digits of each position, once (32-bit: J < 2^31)
           const unsigned s_ = unsigned(pb) + unsigned(tid);
           unsigned a = s_ / unsigned(Rr), b = s_ - a * unsigned(Rr);
           for (int k = N - 1; k > m; --k) {
@@ -710,7 +710,7 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
           }
         }
         __syncthreads();
-        for (int e = tid; e < kAlsBatch * R; e += nt) {
+        for (int e = tid; e < BATCH * R; e += nt) {
           const int pp = e / R, r = e % R;
           double v = 0.0;
           if (pp < np) {
@@ -724,16 +724,16 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
         stampa(18);
         als_cp_wait<1>();  // this batch's fibers (own copies) have landed
         {  // each thread converts the elements it copied itself (no barrier needed before)
-          const int pp = tid % kAlsBatch;
-          const T* src = fibT + buf * kAlsBatch * int(I) + pp * int(I);
+          const int pp = tid % BATCH;
+          const T* src = fibT + buf * BATCH * int(I) + pp * int(I);
           double* dst = fibD + pp * ldI;
-          for (int i = tid / kAlsBatch; i < int(I); i += nt / kAlsBatch) dst[i] = double(src[i]);
+          for (int i = tid / BATCH; i < int(I); i += nt / BATCH) dst[i] = double(src[i]);
         }
         __syncthreads();
         stampa(19);
         const double* fb = fibD;
 #pragma unroll 2
-        for (int ks = 0; ks < kAlsBatch / 4; ++ks) {
+        for (int ks = 0; ks < BATCH / 4; ++ks) {
           const int pp = 4 * ks + tq;
           const double* frow = fb + pp * ldI;
           const double* krow = kc + pp * ldR;
@@ -1191,33 +1191,51 @@ bool als_loop_supported(const i64* shape, int order, int rank) {
   return true;
 }
 
+template <typename T, int BATCH>
+size_t als_loop_smem(const i64* shape, int order, int R) {
+  size_t smem = 0;
+  for (int m = 0; m < order; ++m) {
+    i64 fac = 0;
+    for (int k = 0; k < order; ++k)
+      if (k != m) fac += shape[k] * R;
+    const size_t smA = (size_t(als_fib_doubles<T, BATCH>(shape[m])) +
+                        size_t(BATCH) * (als_ld(int(shape[m])) + als_ld(R))) * sizeof(double) +
+                       size_t(fac) * sizeof(T);
+    const size_t smB = (2 * size_t(shape[m]) * R + 3 * size_t(R) * R + 6 * size_t(R)) * sizeof(double);
+    smem = std::max(smem, std::max(smA, smB));
+  }
+  return smem;
+}
+
 template <typename T>
 void als_loop(const T* B, const i64* shape, int order, const FactorSet<T>& fs, T* weights, double tol, int max_iter,
               double* trace_fit, double* trace_sec, AlsState* state, double* part, i64 part_elems, GridBarrier* bar,
               cudaStream_t st, unsigned long long* prof) {
   const int R = fs.rank;
-  size_t smem = 0;
   i64 maxJ = 1, S = 1, maxout = 1;
   for (int m = 0; m < order; ++m) S *= shape[m];
   for (int m = 0; m < order; ++m) {
     maxJ = std::max(maxJ, S / shape[m]);
     maxout = std::max(maxout, shape[m] * R);
-    i64 fac = 0;
-    for (int k = 0; k < order; ++k)
-      if (k != m) fac += shape[k] * R;
-    const size_t smA = (size_t(als_fib_doubles<T>(shape[m])) + size_t(kAlsBatch) * (als_ld(int(shape[m])) + als_ld(R))) * sizeof(double) +
-                       size_t(fac) * sizeof(T);
-    const size_t smB = (2 * size_t(shape[m]) * R + 3 * size_t(R) * R + 6 * size_t(R)) * sizeof(double);
-    smem = std::max(smem, std::max(smA, smB));
   }
-  static const size_t lim = enable_max_dyn_smem(als_loop_kernel<T>);
-  if (smem > lim) throw std::runtime_error("als_loop: shared memory plan too large");
-  const int maxc = max_coop_blocks(als_loop_kernel<T>, kAlsThreads, smem);
-  int G = int(std::max<i64>(1, std::min<i64>(ceil_div(maxJ, kAlsBatch), maxc)));
-  G = int(std::min<i64>(G, part_elems / (2 * maxout) - 1));  // + one slot for the reduced W
   AlsLoopArgs<T> a{B, make_shape(shape, order), fs, weights, tol, max_iter, trace_fit, trace_sec, state, part,
                    maxout, bar, prof};
-  launch_coop(als_loop_kernel<T>, G, kAlsThreads, smem, st, a);
+  // 64-position batches when they fit: half the per-batch latency chains
+  static const size_t lim64 = enable_max_dyn_smem(als_loop_kernel<T, 64>);
+  static const size_t lim32 = enable_max_dyn_smem(als_loop_kernel<T, 32>);
+  (void)lim64;
+  (void)lim32;
+  auto run = [&](auto kern, size_t smem, int batch) {
+    const int maxc = max_coop_blocks(kern, kAlsThreads, smem);
+    int G = int(std::max<i64>(1, std::min<i64>(ceil_div(maxJ, batch), maxc)));
+    G = int(std::min<i64>(G, part_elems / (2 * maxout) - 1));  // + one slot for the reduced W
+    launch_coop(kern, G, kAlsThreads, smem, st, a);
+  };
+  const size_t s64 = als_loop_smem<T, 64>(shape, order, R);
+  if (s64 <= 180 * 1024)
+    run(als_loop_kernel<T, 64>, s64, 64);
+  else
+    run(als_loop_kernel<T, 32>, als_loop_smem<T, 32>(shape, order, R), 32);
 }
 
 template <typename T>

@@ -862,7 +862,9 @@ AlsHandles<T> run_als(rcpg_context* c, const T* B, const i64* shape, int order, 
   }
   {
     ScopedPass sp(c, "als_iterations", 0.0);
-    if (als_loop_supported<T>(shape, order, R)) {
+    const char* als_path = getenv("RCPG_ALS_PATH");  // A/B testing: loop | general
+    const bool force_general = als_path != nullptr && std::strcmp(als_path, "general") == 0;
+    if (!force_general && als_loop_supported<T>(shape, order, R)) {
       i64 maxout = 1;
       for (int m = 0; m < order; ++m) maxout = std::max(maxout, shape[m] * R);
       const i64 part_elems = 2 * i64(2048) * maxout;
