@@ -10,7 +10,8 @@ import os
 import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librcpg.so")
+# RCPG_LIB: load another build of the same library (A/B timing of two builds)
+LIB_PATH = os.environ.get("RCPG_LIB") or os.path.join(_HERE, "librcpg.so")
 
 RCPG_OK, RCPG_INVALID_ARGUMENT, RCPG_SOLVER_ERROR, RCPG_CUDA_ERROR, RCPG_OOM, RCPG_NCCL_ERROR = range(6)
 RCPG_F32, RCPG_F64 = 0, 1

@@ -489,7 +489,25 @@ __device__ __forceinline__ unsigned long long lu_timer() {
 
 constexpr int kLuThreads = 256;
 
-template <typename T>
+// V consecutive panel rows per thread (16-byte loads/stores when V > 1): the
+// sweep is read-latency bound, so V multiplies the bytes each load keeps in
+// flight. Requires J % V == 0, R % V == 0 and 16-byte aligned A and Z.
+template <typename T, int V>
+struct alignas(sizeof(T) * V) LuVec {
+  T x[V];
+};
+
+template <typename T, int V>
+__device__ __forceinline__ LuVec<T, V> ld_lv(const T* p) {
+  return *reinterpret_cast<const LuVec<T, V>*>(p);
+}
+
+template <typename T, int V>
+__device__ __forceinline__ void st_lv(T* p, const LuVec<T, V>& v) {
+  *reinterpret_cast<LuVec<T, V>*>(p) = v;
+}
+
+template <typename T, int V>
 __global__ void __launch_bounds__(kLuThreads) plu_coop_kernel(LuArgs<T> p) {
   __shared__ Cand<T> red[33];
   __shared__ int pcol_of[kMaxPanelCols], col_at[kMaxPanelCols];
@@ -499,7 +517,7 @@ __global__ void __launch_bounds__(kLuThreads) plu_coop_kernel(LuArgs<T> p) {
   __shared__ i64 s_u;
 
   const int G = gridDim.x;
-  const i64 chunk = ceil_div(p.J, G);
+  const i64 chunk = ceil_div(p.J, i64(G) * V) * V;
   const i64 r0 = blockIdx.x * chunk;
   const i64 r1 = r0 + chunk < p.J ? r0 + chunk : p.J;
   const Cand<T> none{T(-1), 0x7fffffff, 0, 0x7fffffffffffffffll, 0};
@@ -583,62 +601,89 @@ __global__ void __launch_bounds__(kLuThreads) plu_coop_kernel(LuArgs<T> p) {
     best = none;
     Cand<T>* out = p.cands + ((k + 1) & 1) * G;
     const bool more = (k + 1 < p.r);
-    for (i64 s = r0 + threadIdx.x; s < r1; s += blockDim.x) {
+    for (i64 s0 = r0 + i64(threadIdx.x) * V; s0 < r1; s0 += i64(blockDim.x) * V) {
       i64 ba, bz;
       if (unit) {
-        ba = s;
-        bz = s;
-      } else {
-        const i64 aa = s / R, bb = s - aa * R;
+        ba = s0;
+        bz = s0;
+      } else {  // the V rows share one Kolda slice (R % V == 0)
+        const i64 aa = s0 / R, bb = s0 - aa * R;
         ba = aa * p.n * R + bb;
         bz = aa * p.r * R + bb;
       }
-      constexpr int B = 8;  // loads in flight per thread
-      T v[B];
-      // the row's physical position, its pivot-column value and the first
-      // chunk are independent loads: one memory round trip, not two (rows
-      // pivoted earlier are rare, their loads are simply dropped)
-      const i64 ps = p.phys[s];
-      const T pcv = p.A[ba + cs * R];
+      constexpr int B = 8;  // vector loads in flight per thread
+      LuVec<T, V> v[B];
+      // the rows' physical positions, pivot-column values and the first chunk
+      // are independent loads: one memory round trip, not two
+      i64 ps[V];
+#pragma unroll
+      for (int e = 0; e < V; ++e) ps[e] = p.phys[s0 + e];
+      const LuVec<T, V> pcv = ld_lv<T, V>(p.A + ba + cs * R);
 #pragma unroll
       for (int u = 0; u < B; ++u)
-        if (more && k + 1 + u < p.n) v[u] = p.A[ba + col_at[k + 1 + u] * R];
-      if (ps < k) continue;  // pivoted earlier
-      if (s == ss) {
-        p.Z[bz + k * R] = T(1);
-        for (int j = k + 1; j < p.r; ++j) p.Z[bz + j * R] = T(0);
-        continue;
+        if (more && k + 1 + u < p.n) v[u] = ld_lv<T, V>(p.A + ba + col_at[k + 1 + u] * R);
+      bool act[V], anyact = false;
+      int ispiv = -1;
+      LuVec<T, V> zk;
+      T m[V];
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        // rows pivoted earlier keep their L row (zeros past their step) and
+        // their panel values; the pivot row gets its unit entry
+        act[e] = ps[e] >= k && s0 + e != ss;
+        if (s0 + e == ss) ispiv = e;
+        anyact |= act[e];
+        m[e] = act[e] ? pcv.x[e] / piv : T(0);
+        zk.x[e] = s0 + e == ss ? T(1) : m[e];
       }
-      const T m = pcv / piv;
-      p.Z[bz + k * R] = m;
-      if (more) {
-        // the row's first maximum in physical-column order (one float compare
+      if (!anyact && ispiv < 0) continue;  // all pivoted earlier
+      st_lv<T, V>(p.Z + bz + k * R, zk);
+      if (ispiv >= 0)
+        for (int j = k + 1; j < p.r; ++j) p.Z[bz + ispiv + j * R] = T(0);
+      if (more && anyact) {
+        // each row's first maximum in physical-column order (one float compare
         // per entry), then one full candidate comparison per row: the same
         // pick as comparing every entry (all share the physical row ps)
-        T rv = T(-1);
-        int rq = 0, rc = 0;
+        T rv[V];
+        int rq[V], rc[V];
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          rv[e] = T(-1);
+          rq[e] = 0;
+          rc[e] = 0;
+        }
         for (int q0 = k + 1; q0 < p.n; q0 += B) {
           if (q0 > k + 1) {
 #pragma unroll
             for (int u = 0; u < B; ++u)
-              if (q0 + u < p.n) v[u] = p.A[ba + col_at[q0 + u] * R];
+              if (q0 + u < p.n) v[u] = ld_lv<T, V>(p.A + ba + col_at[q0 + u] * R);
           }
 #pragma unroll
           for (int u = 0; u < B; ++u)
             if (q0 + u < p.n) {
               const int c = col_at[q0 + u];
-              const T x = v[u] - m * U[c];
-              p.A[ba + c * R] = x;
-              const T ax = fabs(x);
-              if (ax > rv) {
-                rv = ax;
-                rq = q0 + u;
-                rc = c;
+              const T uc = U[c];
+              LuVec<T, V> x;
+#pragma unroll
+              for (int e = 0; e < V; ++e) {
+                // inactive rows are written back unchanged (same bits)
+                x.x[e] = act[e] ? v[u].x[e] - m[e] * uc : v[u].x[e];
+                const T ax = fabs(x.x[e]);
+                if (act[e] && ax > rv[e]) {
+                  rv[e] = ax;
+                  rq[e] = q0 + u;
+                  rc[e] = c;
+                }
               }
+              st_lv<T, V>(p.A + ba + c * R, x);
             }
         }
-        const Cand<T> cd{rv, rq, rc, ps, s};
-        if (better(cd, best)) best = cd;
+#pragma unroll
+        for (int e = 0; e < V; ++e)
+          if (act[e]) {
+            const Cand<T> cd{rv[e], rq[e], rc[e], ps[e], s0 + e};
+            if (better(cd, best)) best = cd;
+          }
       }
     }
     unsigned long long t_c = 0;
@@ -1399,11 +1444,20 @@ int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w
     return r;
   }
   init_row_keys(km, J, R, w.keys, st);
-  const int maxc = max_coop_blocks(plu_coop_kernel<T>, kLuThreads, 0);
-  // about one panel row per thread; the per-step work is latency bound
-  const int G = int(std::max<i64>(1, std::min<i64>({ceil_div(J, kLuThreads), i64(maxc), i64(w.max_blocks)})));
   LuArgs<T> a{A, Z, J, R, n, r, w.keys, km, reinterpret_cast<Cand<T>*>(w.cands), w.bar, w.info, w.prof};
-  launch_coop(plu_coop_kernel<T>, G, kLuThreads, 0, st, a);
+  // about one group of V panel rows per thread; the per-step work is latency bound
+  auto run = [&](auto kern, int V) {
+    const int maxc = max_coop_blocks(kern, kLuThreads, 0);
+    const int G = int(std::max<i64>(1, std::min<i64>({ceil_div(J, i64(kLuThreads) * V), i64(maxc), i64(w.max_blocks)})));
+    launch_coop(kern, G, kLuThreads, 0, st, a);
+  };
+  constexpr int VV = 16 / int(sizeof(T));
+  const bool vec = std::getenv("RCPG_LU_SCALAR") == nullptr && J % VV == 0 && R % VV == 0 &&
+                   reinterpret_cast<uintptr_t>(A) % 16 == 0 && reinterpret_cast<uintptr_t>(Z) % 16 == 0;
+  if (vec)
+    run(plu_coop_kernel<T, VV>, VV);
+  else
+    run(plu_coop_kernel<T, 1>, 1);
   return r;
 }
 
