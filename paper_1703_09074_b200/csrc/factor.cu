@@ -479,6 +479,7 @@ struct LuArgs {
   GridBarrier* bar;
   int* info;   // [1] nonzero pivots
   unsigned long long* prof;  // optional [8]: ns in reduce / bookkeeping / update / barrier (CTA 0)
+  int delay;   // 1: store the panel after odd pivots only (see plu_coop_kernel)
 };
 
 __device__ __forceinline__ unsigned long long lu_timer() {
@@ -511,7 +512,9 @@ template <typename T, int V>
 __global__ void __launch_bounds__(kLuThreads) plu_coop_kernel(LuArgs<T> p) {
   __shared__ Cand<T> red[33];
   __shared__ int pcol_of[kMaxPanelCols], col_at[kMaxPanelCols];
-  __shared__ T U[kMaxPanelCols];
+  __shared__ T U[kMaxPanelCols], Uprev[kMaxPanelCols];
+  __shared__ T s_pivprev;
+  __shared__ int s_cprev;
   __shared__ i64 ov_pos[kMaxPanelCols], ov_row[kMaxPanelCols];
   __shared__ int n_ov;
   __shared__ i64 s_u;
@@ -563,7 +566,12 @@ __global__ void __launch_bounds__(kLuThreads) plu_coop_kernel(LuArgs<T> p) {
     const i64 pr = g.prow;
     const int pc = g.pcol;
     const i64 bss = row_base(ss, R, p.J, p.n);
-    const T piv = ldcg(&p.A[bss + cs * R]);
+    // Delayed write-back (p.delay): the panel is stored only after odd pivots.
+    // On odd k the stored rows hold a^(k-1) and pivot k-1 is re-applied on the
+    // fly with the identical expression (bit-identical to storing it), so a
+    // pair of pivots costs two reads and one write of the trailing panel.
+    const bool pend = p.delay && (k & 1) != 0;
+    const bool wr = !p.delay || (k & 1) != 0;
     if (threadIdx.x == 0) {
       i64 u = -1;  // row at physical position k before the swap
       for (int q = n_ov - 1; q >= 0; --q)
@@ -584,8 +592,16 @@ __global__ void __launch_bounds__(kLuThreads) plu_coop_kernel(LuArgs<T> p) {
       col_at[k] = cs;
       col_at[pc] = colk;
     }
-    for (int c = threadIdx.x; c < p.n; c += blockDim.x) U[c] = ldcg(&p.A[bss + c * R]);
+    {
+      // the pivot row at state k (stored as a^(k-1) when pend)
+      const T mprev = pend ? ldcg(&p.A[bss + s_cprev * R]) / s_pivprev : T(0);
+      for (int c = threadIdx.x; c < p.n; c += blockDim.x) {
+        const T st = ldcg(&p.A[bss + c * R]);
+        U[c] = pend ? st - mprev * Uprev[c] : st;
+      }
+    }
     __syncthreads();
+    const T piv = U[cs];
     const i64 u = s_u;
     if (threadIdx.x == 0) {
       if (ss >= r0 && ss < r1) p.phys[ss] = k;
@@ -601,6 +617,8 @@ __global__ void __launch_bounds__(kLuThreads) plu_coop_kernel(LuArgs<T> p) {
     best = none;
     Cand<T>* out = p.cands + ((k + 1) & 1) * G;
     const bool more = (k + 1 < p.r);
+    const int cprev = s_cprev;
+    const T pivprev = s_pivprev;
     for (i64 s0 = r0 + i64(threadIdx.x) * V; s0 < r1; s0 += i64(blockDim.x) * V) {
       i64 ba, bz;
       if (unit) {
@@ -619,13 +637,15 @@ __global__ void __launch_bounds__(kLuThreads) plu_coop_kernel(LuArgs<T> p) {
 #pragma unroll
       for (int e = 0; e < V; ++e) ps[e] = p.phys[s0 + e];
       const LuVec<T, V> pcv = ld_lv<T, V>(p.A + ba + cs * R);
+      LuVec<T, V> pvv;
+      if (pend) pvv = ld_lv<T, V>(p.A + ba + cprev * R);
 #pragma unroll
       for (int u = 0; u < B; ++u)
         if (more && k + 1 + u < p.n) v[u] = ld_lv<T, V>(p.A + ba + col_at[k + 1 + u] * R);
       bool act[V], anyact = false;
       int ispiv = -1;
       LuVec<T, V> zk;
-      T m[V];
+      T m[V], m1[V];
 #pragma unroll
       for (int e = 0; e < V; ++e) {
         // rows pivoted earlier keep their L row (zeros past their step) and
@@ -633,7 +653,10 @@ __global__ void __launch_bounds__(kLuThreads) plu_coop_kernel(LuArgs<T> p) {
         act[e] = ps[e] >= k && s0 + e != ss;
         if (s0 + e == ss) ispiv = e;
         anyact |= act[e];
-        m[e] = act[e] ? pcv.x[e] / piv : T(0);
+        // multiplier of the pending pivot k-1, exactly as written to Z then
+        m1[e] = pend && act[e] ? pvv.x[e] / pivprev : T(0);
+        const T pc = pend ? pcv.x[e] - m1[e] * Uprev[cs] : pcv.x[e];
+        m[e] = act[e] ? pc / piv : T(0);
         zk.x[e] = s0 + e == ss ? T(1) : m[e];
       }
       if (!anyact && ispiv < 0) continue;  // all pivoted earlier
@@ -663,11 +686,13 @@ __global__ void __launch_bounds__(kLuThreads) plu_coop_kernel(LuArgs<T> p) {
             if (q0 + u < p.n) {
               const int c = col_at[q0 + u];
               const T uc = U[c];
+              const T up = pend ? Uprev[c] : T(0);
               LuVec<T, V> x;
 #pragma unroll
               for (int e = 0; e < V; ++e) {
                 // inactive rows are written back unchanged (same bits)
-                x.x[e] = act[e] ? v[u].x[e] - m[e] * uc : v[u].x[e];
+                const T x1 = pend ? v[u].x[e] - m1[e] * up : v[u].x[e];
+                x.x[e] = act[e] ? x1 - m[e] * uc : v[u].x[e];
                 const T ax = fabs(x.x[e]);
                 if (act[e] && ax > rv[e]) {
                   rv[e] = ax;
@@ -675,7 +700,7 @@ __global__ void __launch_bounds__(kLuThreads) plu_coop_kernel(LuArgs<T> p) {
                   rc[e] = c;
                 }
               }
-              st_lv<T, V>(p.A + ba + c * R, x);
+              if (wr) st_lv<T, V>(p.A + ba + c * R, x);
             }
         }
 #pragma unroll
@@ -696,6 +721,15 @@ __global__ void __launch_bounds__(kLuThreads) plu_coop_kernel(LuArgs<T> p) {
       if (threadIdx.x == 0) out[blockIdx.x] = best;
       grid_sync(p.bar);
     }
+    // pivot k becomes the pending one of the next step (after every thread of
+    // the block is done reading Uprev: the last step has no grid_sync)
+    __syncthreads();
+    for (int c = threadIdx.x; c < p.n; c += blockDim.x) Uprev[c] = U[c];
+    if (threadIdx.x == 0) {
+      s_cprev = cs;
+      s_pivprev = piv;
+    }
+    __syncthreads();
     if (prof) {
       t_a = lu_timer();
       p.prof[2] += t_a - t_c;
@@ -1444,7 +1478,8 @@ int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w
     return r;
   }
   init_row_keys(km, J, R, w.keys, st);
-  LuArgs<T> a{A, Z, J, R, n, r, w.keys, km, reinterpret_cast<Cand<T>*>(w.cands), w.bar, w.info, w.prof};
+  LuArgs<T> a{A, Z, J, R, n, r, w.keys, km, reinterpret_cast<Cand<T>*>(w.cands), w.bar, w.info, w.prof,
+              std::getenv("RCPG_LU_NODELAY") == nullptr ? 1 : 0};
   // about one group of V panel rows per thread; the per-step work is latency bound
   auto run = [&](auto kern, int V) {
     const int maxc = max_coop_blocks(kern, kLuThreads, 0);
