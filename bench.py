@@ -287,11 +287,12 @@ def main():
         ctx.event_record(0)
         for _ in range(args.steps):
             model, trace = rcp.decompose(X, dcfg, ctx=ctx)
-            for name, ms, by in ctx.pass_timings():
-                pass_ms[name] = pass_ms.get(name, 0.0) + ms
-                pass_bytes[name] = pass_bytes.get(name, 0.0) + by
         ctx.event_record(1)
         total_ms = ctx.event_elapsed_ms(0, 1)
+    # per-pass breakdown of the last timed step (read after the timed region)
+    for name, ms, by in ctx.pass_timings():
+        pass_ms[name] = pass_ms.get(name, 0.0) + ms * args.steps
+        pass_bytes[name] = pass_bytes.get(name, 0.0) + by * args.steps
     ctx.synchronize()
     launches = ctx.kernel_launches() - l0
     dist.barrier()

@@ -187,6 +187,9 @@ rcpg_status rcpg_thin_qr(rcpg_context* ctx, rcpg_dtype dtype, int64_t rows, int6
  * names: NUL-separated list in `names` (capacity names_cap); returns count. */
 int32_t rcpg_pass_timings(const rcpg_context* ctx, char* names, int32_t names_cap, double* ms,
                           double* bytes, int32_t cap);
+/* Start of each pass of the last call, ms after the first pass started (same
+ * order as rcpg_pass_timings); gaps between passes are device idle time. */
+int32_t rcpg_pass_offsets(const rcpg_context* ctx, double* start_ms, int32_t cap);
 /* Number of kernels the library launched since context creation. */
 int64_t rcpg_kernel_launches(const rcpg_context* ctx);
 /* Synthetic test-data generator on device (not the hot path): dense

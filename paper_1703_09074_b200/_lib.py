@@ -105,6 +105,7 @@ SIGNATURES = {
     "rcpg_plu_basis": (_I32, [_V, C.c_int, _I64, _I64, _V, _V]),
     "rcpg_thin_qr": (_I32, [_V, C.c_int, _I64, _I64, _V, _V, _V]),
     "rcpg_pass_timings": (_I32, [_V, C.c_char_p, _I32, _V, _V, _I32]),
+    "rcpg_pass_offsets": (_I32, [_V, _V, _I32]),
     "rcpg_kernel_launches": (_I64, [_V]),
     "rcpg_synth": (_I32, [_V, C.c_int, _I32, _V, _I64, _V, _V, _D, _U64, C.POINTER(C.c_void_p)]),
     "rcpg_synchronize": (_I32, [_V]),

@@ -1572,6 +1572,17 @@ int32_t rcpg_pass_timings(const rcpg_context* c, char* names, int32_t names_cap,
   return n;
 }
 
+int32_t rcpg_pass_offsets(const rcpg_context* c, double* start_ms, int32_t cap) {
+  if (!c || c->pass_used == 0) return 0;
+  int32_t n = 0;
+  for (size_t i = 0; i < c->pass_used && n < cap; ++i) {
+    float t = 0;
+    if (cudaEventElapsedTime(&t, c->passes[0].a, c->passes[i].a) != cudaSuccess) t = -1;
+    start_ms[n++] = t;
+  }
+  return n;
+}
+
 int64_t rcpg_kernel_launches(const rcpg_context*) { return launch_counter().load(); }
 
 rcpg_status rcpg_synth(rcpg_context* c, rcpg_dtype dtype, int32_t order, const int64_t* shape, int64_t rank,

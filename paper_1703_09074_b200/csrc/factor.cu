@@ -347,6 +347,164 @@ __global__ void __launch_bounds__(kSmemLuThreads) plu_cluster_kernel(const T* __
   csync();  // keep every CTA's shared memory alive until all remote reads are done
 }
 
+// FullPivLU of a panel that fits one CTA's shared memory, without moving data:
+// slot i holds the row at Kolda (physical) index i, column-major, each thread
+// owning whole rows. Row and column swaps are bookkept (phys/rowat,
+// col_at/pcol_of) and the pivot key is (|a|, physical column, physical row) --
+// the same pick as Eigen's first maximum in column-major order on the swapped
+// matrix (see plu_coop_kernel). The multiplier of row i at step k overwrites
+// its entry in the pivot column, the rank-1 update is fused with the next
+// pivot search: four block barriers per pivot.
+template <typename T>
+__global__ void __launch_bounds__(1024) plu_onchip_kernel(const T* __restrict__ A, T* __restrict__ Z, int J, int n,
+                                                          i64 R, KoldaMap km, int W, int* info) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* a = reinterpret_cast<T*>(smem_raw);                   // [n][J]
+  int* phys = reinterpret_cast<int*>(a + i64(J) * n);     // [J] physical row of slot i
+  int* rowat = phys + J;                                   // [J] slot at physical row p
+  __shared__ int col_at[kMaxPanelCols];                    // storage column at physical column q
+  __shared__ T red_v[32];
+  __shared__ int red_i[32];
+  __shared__ int s_ss, s_cs, s_stop;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  // W row lanes x tpr column groups: thread (g, i0) updates rows i0, i0 + W, ...
+  // in physical columns k+1+g, k+1+g+tpr, ... (tpr > 1 only when W >= J)
+  const int tpr = nt / W, g = tid / W, i0 = tid - g * W;
+  const int r = J < n ? J : n;
+  const bool ident = (R == i64(J)) && km.n_low == 0 && km.n_high == 1;
+  for (int c = tid; c < n; c += nt) col_at[c] = c;
+  // panel load, coalesced along columns with many loads in flight per thread;
+  // Kolda row bases go through the phys/rowat area (one i64 per row) first
+  i64* rbase = reinterpret_cast<i64*>(phys);
+  if (!ident) {
+    for (int i = tid; i < J; i += nt) {
+      const i64 srow = kolda_inverse(km, i, R);
+      const i64 aa = srow / R, bb = srow - aa * R;
+      rbase[i] = aa * n * R + bb;
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < J; i += nt) {
+    const i64 base = ident ? i64(i) : rbase[i];
+    int c = 0;
+    for (; c + 8 <= n; c += 8) {
+      T v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = A[base + (c + u) * R];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[i + i64(c + u) * J] = v[u];
+    }
+    for (; c < n; ++c) a[i + i64(c) * J] = A[base + c * R];
+  }
+  __syncthreads();
+  for (int i = tid; i < J; i += nt) {
+    phys[i] = i;
+    rowat[i] = i;
+  }
+  __syncthreads();
+  // candidate key: (|a| desc, physical column asc, physical row asc) with the
+  // two positions packed as pcol * J + prow (< 2^31 for on-chip panels)
+  T bv = T(-1);
+  int bi = 0x7fffffff;
+  for (int i = i0; i < J; i += W)
+    for (int c = g; c < n; c += tpr) key_better(bv, bi, T(fabs(a[i + i64(c) * J])), c * J + i);
+  int k0 = r;
+  T m_pend = T(0);  // tpr > 1: the multiplier of the previous step, stored one step late
+  int c_pend = -1;
+  for (int k = 0; k < r; ++k) {
+    // one block reduction; warp 0 finishes it and does the bookkeeping
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+      key_better(bv, bi, __shfl_xor_sync(0xffffffffu, bv, o), __shfl_xor_sync(0xffffffffu, bi, o));
+    if ((tid & 31) == 0) {
+      red_v[tid >> 5] = bv;
+      red_i[tid >> 5] = bi;
+    }
+    __syncthreads();
+    if (tid < 32) {
+      bv = tid < (nt >> 5) ? red_v[tid] : T(-1);
+      bi = tid < (nt >> 5) ? red_i[tid] : 0x7fffffff;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+        key_better(bv, bi, __shfl_xor_sync(0xffffffffu, bv, o), __shfl_xor_sync(0xffffffffu, bi, o));
+      if (tid == 0) {
+        s_stop = !(bv > T(0));
+        if (bv > T(0)) {
+          const int pc = bi / J, pr = bi - pc * J;
+          const int ss = rowat[pr], cs = col_at[pc];
+          const int u = rowat[k];  // slot at physical row k moves to the pivot's physical row
+          phys[ss] = k;
+          rowat[k] = ss;
+          phys[u] = pr;
+          rowat[pr] = u;
+          col_at[pc] = col_at[k];
+          col_at[k] = cs;
+          s_ss = ss;
+          s_cs = cs;
+        }
+      }
+    }
+    __syncthreads();
+    if (c_pend >= 0) {  // every sibling has read it (two barriers ago)
+      a[i0 + i64(c_pend) * J] = m_pend;
+      c_pend = -1;
+    }
+    if (s_stop) {  // exactly-zero corner (FullPivLU early stop)
+      k0 = k;
+      break;
+    }
+    // the pivot row is read in place (broadcast): nobody writes it this step
+    const int ss = s_ss, cs = s_cs;
+    const T* __restrict__ up = a + ss;
+    const T piv = up[i64(cs) * J];
+    bv = T(-1);
+    bi = 0x7fffffff;
+    const bool more = k + 1 < r;
+    for (int i = i0; i < J; i += W) {
+      const int ps = phys[i];
+      if (ps <= k) continue;  // pivoted (the pivot row itself has ps == k)
+      const T m = a[i + i64(cs) * J] / piv;
+      if (tpr == 1) {
+        a[i + i64(cs) * J] = m;
+      } else if (g == 0) {
+        m_pend = m;
+        c_pend = cs;
+      }
+      if (!more) continue;
+      T rv = T(-1);
+      int rq = 0;
+#pragma unroll 4
+      for (int q = k + 1 + g; q < n; q += tpr) {
+        const i64 co = i64(col_at[q]) * J;
+        const T x = a[i + co] - m * up[co];
+        a[i + co] = x;
+        if (fabs(x) > rv) {
+          rv = fabs(x);
+          rq = q;
+        }
+      }
+      key_better(bv, bi, rv, rq * J + ps);
+    }
+  }
+  __syncthreads();
+  if (c_pend >= 0) a[i0 + i64(c_pend) * J] = m_pend;
+  __syncthreads();
+  // P^{-1} L: slot i (Kolda row i) at physical row p: multipliers left of p
+  // (columns before an early stop), its unit entry at p, zeros right of it
+  for (int i = tid; i < J; i += nt) {
+    const int p = phys[i];
+    i64 base = i;
+    if (!ident) {
+      const i64 srow = kolda_inverse(km, i, R);
+      const i64 aa = srow / R, bb = srow - aa * R;
+      base = aa * r * R + bb;
+    }
+    for (int j = 0; j < r; ++j)
+      Z[base + j * R] = (p == j) ? T(1) : (j < p && j < k0 ? a[i + i64(col_at[j]) * J] : T(0));
+  }
+  if (tid == 0) *info = k0;
+}
+
 // FullPivLU with ONE barrier per pivot: the panel is double-buffered in
 // shared memory and every step rewrites it from the previous buffer with the
 // row swap (k <-> br) and column swap (k <-> bc) applied as an index remap,
@@ -1440,6 +1598,19 @@ int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w
   const size_t pp_smem = 2 * size_t(J) * n * sizeof(T) + 2 * size_t(J) * sizeof(int);
   if (false && pp_smem <= pp_lim) {  // slower than the swap kernel on B200 (latency bound); kept for reference
     plu_pp_kernel<T><<<1, kPpThreads, pp_smem, st>>>(A, Z, int(J), n, R, km, w.info);
+    count_launch();
+    RCPG_LAUNCHED();
+    return r;
+  }
+  // one CTA, rows owned by threads, swaps bookkept
+  static const size_t oc_lim = enable_max_dyn_smem(plu_onchip_kernel<T>);
+  const size_t oc_smem = size_t(J) * n * sizeof(T) + 2 * size_t(J) * sizeof(int);
+  if (oc_smem <= oc_lim && J * i64(n) < (i64(1) << 31) && std::getenv("RCPG_LU_CLUSTER") == nullptr) {
+    // W row lanes (whole warps) x tpr column groups, at most 1024 threads
+    const int W = int(std::min<i64>(1024, ceil_div(J, 32) * 32));
+    const char* tp = std::getenv("RCPG_LU_TPR");
+    const int tpr = tp ? std::max(1, std::min(atoi(tp), 1024 / W)) : 1;
+    plu_onchip_kernel<T><<<1, W * tpr, oc_smem, st>>>(A, Z, int(J), n, R, km, W, w.info);
     count_launch();
     RCPG_LAUNCHED();
     return r;

@@ -210,6 +210,11 @@ class Context:
         raw = names.raw.split(b"\0")
         return [(raw[i].decode(), float(ms[i]), float(by[i])) for i in range(n)]
 
+    def pass_offsets(self):
+        st = np.zeros(4096, dtype=np.float64)
+        n = self.lib.rcpg_pass_offsets(self.h, st.ctypes.data, 4096)
+        return [float(x) for x in st[:n]]
+
     def kernel_launches(self) -> int:
         return int(self.lib.rcpg_kernel_launches(self.h))
 

@@ -85,6 +85,29 @@ def test_plu_basis_rank_deficient_and_ties(rcp, oracle):
     assert np.array_equal(rcp.plu_basis(t), oracle.plu_basis(t))
 
 
+@pytest.mark.parametrize("rows,cols,dt", [(200, 20, np.float64), (400, 30, np.float64), (900, 30, np.float64),
+                                         (37, 5, np.float64), (64, 64, np.float64), (3000, 8, np.float64),
+                                         (1024, 48, np.float32), (128, 48, np.float32)])
+def test_plu_basis_onchip_matches_cluster_path(rcp, oracle, rows, cols, dt, monkeypatch):
+    """The one-CTA LU (rows owned by threads, swaps bookkept) against the cluster LU (Eigen's
+    physical swaps): same pivots, same arithmetic in the same order -> identical bits."""
+    rng = np.random.default_rng(rows * cols)
+    m = np.asfortranarray(rng.standard_normal((rows, cols)).astype(dt))
+    got = rcp.plu_basis(m)
+    monkeypatch.setenv("RCPG_LU_CLUSTER", "1")
+    alt = rcp.plu_basis(m)
+    monkeypatch.delenv("RCPG_LU_CLUSTER")
+    assert np.array_equal(got, alt)
+    want = oracle.plu_basis(m.astype(np.float64))
+    assert np.max(np.abs(got - want)) <= (1e-12 if dt == np.float64 else 1e-3)
+    # integer panels: many exact ties, decided by the column-major first maximum
+    t = np.asfortranarray(rng.integers(-2, 3, (rows, cols)).astype(dt))
+    monkeypatch.setenv("RCPG_LU_CLUSTER", "1")
+    alt = rcp.plu_basis(t)
+    monkeypatch.delenv("RCPG_LU_CLUSTER")
+    assert np.array_equal(rcp.plu_basis(t), alt)
+
+
 @pytest.mark.parametrize("rows,cols", [(100, 20), (1024, 70)])
 def test_thin_qr_matches_householder(rcp, oracle, rows, cols):
     rng = np.random.default_rng(rows)
