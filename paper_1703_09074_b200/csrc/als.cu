@@ -186,9 +186,8 @@ __device__ void jacobi_eig(double* A, double* V, int n, int ld, double* evals, i
 
 // ------------------------------------------------------------- init
 template <typename T>
-__global__ void __launch_bounds__(kSmallThreads) init_from_gram_kernel(const T* G, int n, int R, int mode,
-                                                                       u64 seed, int method, T* F, T* gram,
-                                                                       double* work) {
+__device__ void init_from_gram_body(const T* G, int n, int R, int mode, u64 seed, int method, T* F, T* gram,
+                                    double* work) {
   const int tid = threadIdx.x, nt = blockDim.x;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const bool in_smem = n <= kEigSmemMax;  // A and V resident in shared memory
@@ -278,6 +277,14 @@ __global__ void __launch_bounds__(kSmallThreads) init_from_gram_kernel(const T* 
     for (int i = 0; i < n; ++i) s += double(F[i + i64(a) * n]) * double(F[i + i64(b) * n]);
     gram[e] = T(s);
   }
+}
+
+// Every initialized mode in one launch, one CTA per mode (the eigenproblems
+// are independent and each is latency bound on one SM).
+template <typename T>
+__global__ void __launch_bounds__(kSmallThreads) init_from_gram_kernel(InitBatch<T> b, int R, u64 seed, int method) {
+  const int q = blockIdx.x;
+  init_from_gram_body<T>(b.G[q], b.n[q], R, b.mode[q], seed, method, b.F[q], b.gram[q], b.work[q]);
 }
 
 template <typename T>
@@ -1139,16 +1146,20 @@ void kr_panel(const FactorSet<T>& fs, const i64* shape, int mode, T* out, cudaSt
 }
 
 template <typename T>
-void init_factor_from_gram(const T* G, int extent, int rank, int mode, u64 seed, int method, T* factor,
-                           T* gram_out, double* work, cudaStream_t st) {
+void init_factors_from_grams(const InitBatch<T>& b, int count, int rank, u64 seed, int method, cudaStream_t st) {
   check_arg(rank <= kMaxRank, "init_factors: rank above the supported maximum");
-  const size_t smem = extent <= kEigSmemMax ? 2 * size_t(extent) * size_t(extent | 1) * sizeof(double) : 0;
+  check_arg(count >= 1 && count <= kMaxOrder, "init_factors: mode count");
+  size_t smem = 0;
+  for (int q = 0; q < count; ++q)
+    if (b.n[q] <= kEigSmemMax) smem = std::max(smem, 2 * size_t(b.n[q]) * size_t(b.n[q] | 1) * sizeof(double));
   static const size_t lim = enable_max_dyn_smem(init_from_gram_kernel<T>);
   (void)lim;
-  init_from_gram_kernel<T><<<1, 256, smem, st>>>(G, extent, rank, mode, seed, method, factor, gram_out, work);
+  init_from_gram_kernel<T><<<count, 256, smem, st>>>(b, rank, seed, method);
   count_launch();
   RCPG_LAUNCHED();
 }
+
+size_t init_work_doubles(int n) { return 2 * size_t(n) * size_t(n | 1) + 4 * size_t(n) + 64; }
 
 template <typename T>
 void zero_factor(T* factor, i64 extent, int rank, T* gram_out, cudaStream_t st) {
@@ -1345,7 +1356,7 @@ void synth_tensor(const i64* shape, int order, int rank, const double* w_dev, co
 
 #define RCPG_INST(T)                                                                                          \
   template void kr_panel<T>(const FactorSet<T>&, const i64*, int, T*, cudaStream_t, const int*);                          \
-  template void init_factor_from_gram<T>(const T*, int, int, int, u64, int, T*, T*, double*, cudaStream_t);   \
+  template void init_factors_from_grams<T>(const InitBatch<T>&, int, int, u64, int, cudaStream_t);           \
   template void zero_factor<T>(T*, i64, int, T*, cudaStream_t);                                               \
   template void fill_ones<T>(T*, int, cudaStream_t);                                               \
   template void als_update<T>(const FactorSet<T>&, int, const T*, T*, double, int, double*, double*,          \

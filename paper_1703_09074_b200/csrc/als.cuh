@@ -39,12 +39,23 @@ template <typename T>
 void kr_panel(const FactorSet<T>& fs, const i64* shape, int mode, T* out, cudaStream_t st,
               const int* skip = nullptr);
 
-// init_factors (solve.hpp:93-131) for mode `mode` >= 1 from the Gram matrix
-// G = B_(m) B_(m)^T (extent x extent, T, column-major). Writes factor and its
-// Gram. `work` >= 3 * extent^2 + 4 * extent doubles.
+// init_factors (solve.hpp:93-131) for modes >= 1, each from its Gram matrix
+// G = B_(m) B_(m)^T (extent x extent, T, column-major), one CTA per mode:
+// leading eigenvectors, sign-canonicalized, padded from the init stream.
+// Writes each factor and its Gram; work[q] >= init_work_doubles(n[q]).
 template <typename T>
-void init_factor_from_gram(const T* G, int extent, int rank, int mode, u64 seed, int method, T* factor,
-                           T* gram_out, double* work, cudaStream_t st);
+struct InitBatch {
+  const T* G[kMaxOrder];
+  int n[kMaxOrder];
+  int mode[kMaxOrder];
+  T* F[kMaxOrder];
+  T* gram[kMaxOrder];
+  double* work[kMaxOrder];
+};
+template <typename T>
+void init_factors_from_grams(const InitBatch<T>& b, int count, int rank, u64 seed, int method, cudaStream_t st);
+// doubles of `work` one mode of extent n needs
+size_t init_work_doubles(int n);
 template <typename T>
 void zero_factor(T* factor, i64 extent, int rank, T* gram_out, cudaStream_t st);
 

@@ -847,17 +847,35 @@ AlsHandles<T> run_als(rcpg_context* c, const T* B, const i64* shape, int order, 
   {
     ScopedPass sp(c, "als_init", 0.0);
     zero_factor<T>(h.fs.f[0], shape[0], R, h.fs.gram[0], c->st);
+    // every Gram first (each a slice of als_w), then all eigenproblems in one launch
+    i64 gram_elems = 0, work_doubles = 0;
     for (int m = 1; m < order; ++m) {
-      const ModeView v = mode_view(shape, order, m);
+      gram_elems += shape[m] * shape[m];
+      work_doubles += i64(init_work_doubles(int(shape[m])));
+    }
+    c->als_w.ensure(size_t(std::max<i64>(gram_elems, 1)) * sizeof(T));
+    c->als_work.ensure(size_t(work_doubles) * sizeof(double));
+    InitBatch<T> ib{};
+    i64 goff = 0, woff = 0;
+    for (int m = 1; m < order; ++m) {
+      const int q = m - 1;
+      ib.G[q] = c->als_w.as<T>() + goff;
+      ib.n[q] = int(shape[m]);
+      ib.mode[q] = m;
+      ib.F[q] = h.fs.f[m];
+      ib.gram[q] = h.fs.gram[m];
+      ib.work[q] = c->als_work.as<double>() + woff;
       if (cfg.init == RCPG_INIT_EIGENVECTORS) {
         // Gram = B_(m) B_(m)^T as a sketch of B against itself.
+        const ModeView v = mode_view(shape, order, m);
         const i64 scr = sketch_scratch_elems<T>(v, shape[m], sms);
         c->scratch.ensure(size_t(scr) * sizeof(T));
-        sketch<T>(B, v, B, shape[m], c->als_w.as<T>(), c->scratch.as<T>(), scr, sms, c->st);
+        sketch<T>(B, v, B, shape[m], c->als_w.as<T>() + goff, c->scratch.as<T>(), scr, sms, c->st);
       }
-      init_factor_from_gram<T>(c->als_w.as<T>(), int(shape[m]), R, m, cfg.seed, cfg.init, h.fs.f[m], h.fs.gram[m],
-                               c->als_work.as<double>(), c->st);
+      goff += shape[m] * shape[m];
+      woff += i64(init_work_doubles(int(shape[m])));
     }
+    if (order > 1) init_factors_from_grams<T>(ib, order - 1, R, cfg.seed, cfg.init, c->st);
     fill_ones<T>(h.weights, R, c->st);
   }
   {
