@@ -1215,33 +1215,77 @@ __global__ void __launch_bounds__(kCqrThreads) cqr2_kernel(const T* __restrict__
 __device__ void chol_inv_small(double* A, double* X, int n, int ld, double* dg, int* fail) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
-  for (int j = 0; j < n; ++j) {
-    if (tid == 0) {
-      const double d = A[j + j * ld];
-      if (!(d > 0.0)) *fail = 1;
-      const double piv = d > 0.0 ? sqrt(d) : 1.0;
-      A[j + j * ld] = piv;
-      dg[j] = piv;
+  __shared__ double rdg[kMaxPanelCols];  // 1 / R(j, j)
+  // Blocked right-looking upper Cholesky, 8 columns per block: warp 0 factors
+  // the diagonal block (warp barriers only), every thread solves one column
+  // of the block's panel, then one trailing update per block. Each entry
+  // sees the same operations in the same order as the unblocked algorithm
+  // (subtract R(s, r) R(s, c) for s = 0, 1, ..., then scale by 1 / R(j, j)).
+  constexpr int NB = 8;
+  for (int kb = 0; kb < n; kb += NB) {
+    const int ke = min(kb + NB, n);
+    if (wid == 0) {
+      for (int j = kb; j < ke; ++j) {
+        const double d = A[j + j * ld];
+        const double piv = d > 0.0 ? sqrt(d) : 1.0;
+        const double rinv = 1.0 / piv;
+        if (lane == 0) {
+          if (!(d > 0.0)) *fail = 1;
+          dg[j] = piv;
+          rdg[j] = rinv;
+        }
+        if (j + 1 + lane < ke) A[j + (j + 1 + lane) * ld] *= rinv;
+        __syncwarp();
+        for (int e = lane; e < NB * NB; e += 32) {
+          const int r = kb + (e % NB), c = kb + (e / NB);
+          if (r > j && r <= c && c < ke) A[r + c * ld] -= A[j + r * ld] * A[j + c * ld];
+        }
+        __syncwarp();
+      }
     }
     __syncthreads();
-    const double rinv = 1.0 / A[j + j * ld];
-    for (int c = j + 1 + tid; c < n; c += nt) A[j + c * ld] *= rinv;
+    // panel: rows kb..ke-1 of the columns right of the block
+    for (int c = ke + tid; c < n; c += nt)
+      for (int j = kb; j < ke; ++j) {
+        double x = A[j + c * ld];
+        for (int s = kb; s < j; ++s) x -= A[s + j * ld] * A[s + c * ld];
+        A[j + c * ld] = x * rdg[j];
+      }
     __syncthreads();
-    // trailing update of the upper triangle: warp per column c2, lanes over rows c1 <= c2
-    for (int c2 = j + 1 + wid; c2 < n; c2 += nw) {
-      const double r2 = A[j + c2 * ld];
-      for (int c1 = j + 1 + lane; c1 <= c2; c1 += 32) A[c1 + c2 * ld] -= A[j + c1 * ld] * r2;
+    // trailing update of the upper triangle by the block's rows
+    const int bs = ke - kb;
+    for (int c2 = ke + wid; c2 < n; c2 += nw) {
+      double rc[NB];
+#pragma unroll
+      for (int t = 0; t < NB; ++t) rc[t] = t < bs ? A[kb + t + c2 * ld] : 0.0;
+      for (int c1 = ke + lane; c1 <= c2; c1 += 32) {
+        double x = A[c1 + c2 * ld];
+#pragma unroll
+        for (int t = 0; t < NB; ++t)
+          if (t < bs) x -= A[kb + t + c1 * ld] * rc[t];
+        A[c1 + c2 * ld] = x;
+      }
     }
     __syncthreads();
   }
-  // X = R^{-1}, upper: rows from the bottom, all columns j >= i in parallel
-  for (int e = tid; e < n * ld; e += nt) X[e] = 0.0;
+  for (int j = tid; j < n; j += nt) A[j + j * ld] = dg[j];
   __syncthreads();
-  for (int i = n - 1; i >= 0; --i) {
-    const double rii = 1.0 / A[i + i * ld];
-    for (int j = i + tid; j < n; j += nt) {
+  // X = R^{-1} (upper), blocked back substitution over 8-row blocks from the
+  // bottom: first every (row of the block, column) pair sums what the rows
+  // below the block contribute (all threads), then a short triangular solve
+  // inside the block per column. Two barriers per block instead of one serial
+  // chain of n^2/2 steps per column.
+  for (int e = tid; e < n * n; e += nt) {
+    const int i = e % n, j = e / n;
+    if (i > j) X[i + j * ld] = 0.0;
+  }
+  for (int ib = ((n - 1) / NB) * NB; ib >= 0; ib -= NB) {
+    const int ie = min(ib + NB, n), bs = ie - ib;
+    for (int e = tid; e < bs * (n - ib); e += nt) {
+      const int i = ib + e % bs, j = ib + e / bs;
+      if (i > j) continue;
       double s0 = (i == j) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      int k = i + 1;
+      int k = ie;
       for (; k + 3 <= j; k += 4) {
         s0 -= A[i + k * ld] * X[k + j * ld];
         s1 -= A[i + (k + 1) * ld] * X[k + 1 + j * ld];
@@ -1249,31 +1293,34 @@ __device__ void chol_inv_small(double* A, double* X, int n, int ld, double* dg, 
         s3 -= A[i + (k + 3) * ld] * X[k + 3 + j * ld];
       }
       for (; k <= j; ++k) s0 -= A[i + k * ld] * X[k + j * ld];
-      X[i + j * ld] = ((s0 + s1) + (s2 + s3)) * rii;
+      X[i + j * ld] = (s0 + s1) + (s2 + s3);
     }
+    __syncthreads();
+    for (int j = ib + tid; j < n; j += nt)
+      for (int i = min(ie - 1, j); i >= ib; --i) {
+        double x = X[i + j * ld];
+        for (int k = i + 1; k <= min(ie - 1, j); ++k) x -= A[i + k * ld] * X[k + j * ld];
+        X[i + j * ld] = x * rdg[i];
+      }
     __syncthreads();
   }
 }
 
 // G: top n x n block of Q2 (ld), destroyed. rows = panel height (square
 // panels: Eigen leaves the last column unreflected, opposite sign).
+// One barrier per step: the sign flip of column k is folded into the
+// multipliers (negation is exact), one division per row.
 __device__ void sign_reconstruct(double* G, int n, int ld, int rows, double* sgn) {
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
   for (int k = 0; k < n; ++k) {
-    const double sk = (G[k + k * ld] > 0.0) != (k == rows - 1) ? -1.0 : 1.0;
-    __syncthreads();
-    for (int i = tid; i < n; i += nt)
-      if (i != k && sk < 0.0) G[i + k * ld] = -G[i + k * ld];
-    if (tid == 0) {
-      G[k + k * ld] = sk * G[k + k * ld] - 1.0;
-      sgn[k] = sk;
-    }
-    __syncthreads();
-    const double dkk = G[k + k * ld];
-    const int m = n - k - 1;
-    for (int e = tid; e < m * m; e += nt) {
-      const int i = k + 1 + e % m, j = k + 1 + e / m;
-      G[i + j * ld] -= (G[i + k * ld] / dkk) * G[k + j * ld];
+    const double gkk = G[k + k * ld];
+    const double sk = (gkk > 0.0) != (k == rows - 1) ? -1.0 : 1.0;
+    const double dkk = sk * gkk - 1.0;
+    if (tid == 0) sgn[k] = sk;
+    for (int i = k + 1 + lane; i < n; i += 32) {
+      const double l = (sk * G[i + k * ld]) / dkk;
+      for (int j = k + 1 + wid; j < n; j += nw) G[i + j * ld] -= l * G[k + j * ld];
     }
     __syncthreads();
   }
@@ -1384,6 +1431,7 @@ __global__ void __launch_bounds__(kCqrCoopThreads) cqr2_coop_kernel(CqrCoopArgs<
     }
     cqr_stamp(p.prof, 2 + 5 * pass);
     grid_sync(p.bar);
+    cqr_stamp(p.prof, 13 + pass);
     // 3. every CTA factors the (identical) Gram itself: upper Cholesky, R^{-1}
     //    (deterministic, so all CTAs agree; no barrier, nobody waits on CTA 0)
     const int ldn = n + 1;
@@ -1708,10 +1756,11 @@ int thin_qr(T* A, T* Q, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w, 
         RCPG_CUDA(cudaMemcpyAsync(h, qprof, sizeof(h), cudaMemcpyDeviceToHost, st));
         RCPG_CUDA(cudaStreamSynchronize(st));
         fprintf(stderr, "[rcpg qr] %lldx%d G=%d rows/CTA=%d us:", (long long)J, n, G, rows_per);
-        const char* nm[] = {"gram0", "red0", "chol0", "apply0", "-", "gram1", "red1", "chol1", "apply1", "top", "sign"};
-        const int at[] = {1, 2, 3, 4, -1, 6, 7, 8, 9, 11, 12};
-        const int from[] = {0, 1, 2, 3, -1, 4, 6, 7, 8, 9, 11};
-        for (int q = 0; q < 11; ++q)
+        const char* nm[] = {"gram0", "red0", "chol0", "apply0", "-", "gram1", "red1", "chol1", "apply1", "top", "sign",
+                            "sync0", "sync1"};
+        const int at[] = {1, 2, 3, 4, -1, 6, 7, 8, 9, 11, 12, 13, 14};
+        const int from[] = {0, 1, 2, 3, -1, 4, 6, 7, 8, 9, 11, 2, 7};
+        for (int q = 0; q < 13; ++q)
           if (at[q] >= 0) fprintf(stderr, " %s %.1f", nm[q], (h[at[q]] - h[from[q]]) * 1e-3);
         fprintf(stderr, "\n");
       }
