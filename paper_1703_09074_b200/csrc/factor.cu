@@ -909,6 +909,322 @@ __global__ void __launch_bounds__(kLuThreads) plu_coop_kernel(LuArgs<T> p) {
   if (blockIdx.x == 0 && threadIdx.x == 0) *p.info = k0;
 }
 
+// ------------------------------------------------- LU, panel resident on chip
+// The whole panel stays in the SMs for the factorization: CTA b (one per SM)
+// owns rows [b*chunk, (b+1)*chunk); storage columns [0, ns) of its rows in
+// shared memory, the last RC columns in registers (RPT rows per thread).
+// Per pivot: block reduction, then each CTA publishes its best candidate with
+// that row's current values (double-buffered by step parity); one grid
+// barrier; every CTA picks the winner from the G keys, reads its row and
+// applies the bookkeeping of plu_coop_kernel. Same keys, same arithmetic,
+// same results as plu_coop_kernel; no panel traffic per pivot.
+template <typename T>
+struct LuResArgs {
+  const T* A;
+  T* Z;
+  i64 J, R;
+  int n, r, ns, chunk;
+  const i64* keys;  // [J] Kolda (physical) index of every storage row
+  KoldaMap km;
+  Cand<T>* pubk;    // [2][G]
+  T* pubr;          // [2][G][n]
+  GridBarrier* bar;
+  int* info;
+  unsigned long long* prof;  // optional [8] (CTA 0): ns in reduce+publish / barrier / pick+book / update
+};
+
+__host__ __device__ constexpr int lu_res_max_threads(int rc, int rpt) { return rc * rpt == 0 ? 1024 : 640; }
+constexpr int kResKeyLoads = 5;  // grids of up to 160 CTAs
+
+template <typename T, int RC, int RPT>
+__global__ void __launch_bounds__(lu_res_max_threads(RC, RPT), 1) plu_resident_kernel(LuResArgs<T> p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x, nt = blockDim.x, G = gridDim.x, b = blockIdx.x;
+  const int n = p.n, ns = p.ns, ldl = p.chunk;
+  const i64 R = p.R;
+  const i64 r0 = i64(b) * p.chunk;
+  const int rows = int(max(i64(0), min(i64(p.chunk), p.J - r0)));
+  T* a = reinterpret_cast<T*>(smem_raw);                                             // [ns][ldl]
+  i64* physl = reinterpret_cast<i64*>(smem_raw + ((size_t(ns) * ldl * sizeof(T) + 15) & ~size_t(15)));  // [ldl]
+  __shared__ int pcol_of[kMaxPanelCols], col_at[kMaxPanelCols];
+  __shared__ T U[kMaxPanelCols];
+  __shared__ i64 ov_pos[kMaxPanelCols], ov_row[kMaxPanelCols];
+  __shared__ int n_ov, s_w, red_w[kResKeyLoads];
+  __shared__ i64 kinv[kMaxPanelCols];  // Kolda row at physical position k (before any swap)
+  __shared__ Cand<T> red[33];
+  __shared__ Cand<T> s_g;
+  const Cand<T> none{T(-1), 0x7fffffff, 0, 0x7fffffffffffffffll, 0};
+  T rg[RPT][RC > 0 ? RC : 1];
+  for (int c = tid; c < n; c += nt) {
+    pcol_of[c] = c;
+    col_at[c] = c;
+  }
+  if (tid == 0) n_ov = 0;
+  for (int q = tid; q < p.r; q += nt) kinv[q] = kolda_inverse(p.km, q, p.R);
+  // load own rows, first candidates (all columns, physical order = storage order)
+  Cand<T> best = none;
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int lr = tid + i * nt;
+    if (lr >= rows) continue;
+    const i64 s = r0 + lr;
+    const i64 ba = row_base(s, R, p.J, n);
+    const i64 ps = p.keys[s];
+    physl[lr] = ps;
+    T rv = T(-1);
+    int rq = 0;
+    for (int c = 0; c < ns; ++c) {
+      const T x = p.A[ba + c * R];
+      a[c * ldl + lr] = x;
+      if (fabs(x) > rv) {
+        rv = fabs(x);
+        rq = c;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < RC; ++j) {
+      const T x = ns + j < n ? p.A[ba + (ns + j) * R] : T(0);
+      rg[i][j] = x;
+      if (ns + j < n && fabs(x) > rv) {
+        rv = fabs(x);
+        rq = ns + j;
+      }
+    }
+    const Cand<T> cd{rv, rq, rq, ps, s};
+    if (better(cd, best)) best = cd;
+  }
+  int k0 = p.r;
+  const bool prof = p.prof != nullptr && b == 0 && tid == 0;
+  unsigned long long t0 = prof ? lu_timer() : 0, t1 = 0;
+  for (int k = 0; k < p.r; ++k) {
+    const int par = k & 1;
+    // 1. this CTA's best, published with its row's current values
+    best = block_best(best, red);
+    if (tid == 0) p.pubk[par * G + b] = best;
+    if (best.v > T(0) && best.s >= r0 && best.s < r0 + rows) {
+      const int lr = int(best.s - r0);
+      if (lr % nt == tid) {
+        const int i = lr / nt;
+        T* dst = p.pubr + (i64(par) * G + b) * n;
+        for (int c = 0; c < ns; ++c) dst[c] = a[c * ldl + lr];
+#pragma unroll
+        for (int ii = 0; ii < RPT; ++ii)
+          if (ii == i) {
+#pragma unroll
+            for (int j = 0; j < RC; ++j)
+              if (ns + j < n) dst[ns + j] = rg[ii][j];
+          }
+      }
+    }
+    if (prof) {
+      t1 = lu_timer();
+      p.prof[0] += t1 - t0;
+      t0 = t1;
+    }
+    grid_sync(p.bar);
+    if (prof) {
+      t1 = lu_timer();
+      p.prof[1] += t1 - t0;
+      t0 = t1;
+    }
+    // 2. the winner (every CTA, same order), its row, the bookkeeping
+    // up to five warps, one key per thread: every key load in flight at once
+    if (tid < 32 * kResKeyLoads) {
+      Cand<T> g = tid < G ? load_cand_cg(p.pubk + par * G + tid) : none;
+      int gw = tid;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const Cand<T> y = shfl_cand(g, o);
+        const int yw = __shfl_xor_sync(0xffffffffu, gw, o);
+        if (better(y, g)) {
+          g = y;
+          gw = yw;
+        }
+      }
+      if ((tid & 31) == 0) {
+        red[tid >> 5] = g;
+        red_w[tid >> 5] = gw;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      Cand<T> g = red[0];
+      int gw = red_w[0];
+      for (int q = 1; q < kResKeyLoads && 32 * q < G; ++q)
+        if (better(red[q], g)) {
+          g = red[q];
+          gw = red_w[q];
+        }
+      s_g = g;
+      s_w = gw;
+    }
+    __syncthreads();
+    const Cand<T> g = s_g;
+    if (!(g.v > T(0))) {  // exactly-zero corner (FullPivLU early stop)
+      k0 = k;
+      break;
+    }
+    const i64 ss = g.s, pr = g.prow;
+    const int cs = g.c, pc = g.pcol;
+    const T* src = p.pubr + (i64(par) * G + s_w) * n;
+    for (int c = tid; c < n; c += nt) U[c] = ldcg(src + c);
+    if (tid == 0) {
+      i64 u = -1;  // row at physical position k before the swap
+      for (int q = n_ov - 1; q >= 0; --q)
+        if (ov_pos[q] == k) {
+          u = ov_row[q];
+          break;
+        }
+      if (u < 0) u = kinv[k];
+      if (pr != k) {
+        ov_pos[n_ov] = pr;
+        ov_row[n_ov] = u;
+        ++n_ov;
+      }
+      const int colk = col_at[k];
+      pcol_of[cs] = k;
+      pcol_of[colk] = pc;
+      col_at[k] = cs;
+      col_at[pc] = colk;
+      if (ss >= r0 && ss < r0 + rows) physl[ss - r0] = k;
+      if (u != ss && u >= r0 && u < r0 + rows) physl[u - r0] = pr;
+    }
+    __syncthreads();
+    const T piv = U[cs];
+    const bool more = k + 1 < p.r;
+    if (prof) {
+      t1 = lu_timer();
+      p.prof[2] += t1 - t0;
+      t0 = t1;
+    }
+    // 3. update own rows, next candidates: 8 columns per batch, every load of
+    // a batch before its stores (no smem aliasing chain), all rows together
+    best = none;
+    bool act[RPT];
+    T m[RPT], rv[RPT];
+    int rq[RPT], rcol[RPT];
+    i64 psr[RPT];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int lr = tid + i * nt;
+      act[i] = false;
+      m[i] = T(0);
+      rv[i] = T(-1);
+      rq[i] = 0x7fffffff;
+      rcol[i] = 0;
+      psr[i] = 0;
+      if (lr >= rows) continue;
+      psr[i] = physl[lr];
+      if (psr[i] <= k) continue;  // pivoted (the pivot row itself has ps == k)
+      act[i] = true;
+      T pcv;
+      if (cs < ns) {
+        pcv = a[cs * ldl + lr];
+      } else {
+        pcv = T(0);
+#pragma unroll
+        for (int j = 0; j < RC; ++j)
+          if (cs == ns + j) pcv = rg[i][j];
+      }
+      m[i] = pcv / piv;
+      if (cs < ns) {
+        a[cs * ldl + lr] = m[i];
+      } else {
+#pragma unroll
+        for (int j = 0; j < RC; ++j)
+          if (cs == ns + j) rg[i][j] = m[i];
+      }
+    }
+    if (more) {
+      constexpr int NB = RC * RPT >= 8 ? 4 : 8;
+      for (int q0 = k + 1; q0 < n; q0 += NB) {
+        int cc[NB];
+        T uc[NB];
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+          cc[u] = q0 + u < n ? col_at[q0 + u] : ns;
+          uc[u] = cc[u] < ns ? U[cc[u]] : T(0);
+        }
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+          if (!act[i]) continue;
+          const int lr = tid + i * nt;
+          T xv[NB];
+#pragma unroll
+          for (int u = 0; u < NB; ++u)
+            if (cc[u] < ns) xv[u] = a[cc[u] * ldl + lr];
+#pragma unroll
+          for (int u = 0; u < NB; ++u)
+            if (cc[u] < ns) {
+              const T x = xv[u] - m[i] * uc[u];
+              a[cc[u] * ldl + lr] = x;
+              if (fabs(x) > rv[i]) {  // columns in physical order: first maximum
+                rv[i] = fabs(x);
+                rq[i] = q0 + u;
+                rcol[i] = cc[u];
+              }
+            }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        if (!act[i]) continue;
+#pragma unroll
+        for (int j = 0; j < RC; ++j) {
+          const int c = ns + j;
+          if (c >= n) continue;
+          const int q = pcol_of[c];
+          if (q <= k) continue;
+          const T x = rg[i][j] - m[i] * U[c];
+          rg[i][j] = x;
+          const T ax = fabs(x);
+          if (ax > rv[i] || (ax == rv[i] && q < rq[i])) {
+            rv[i] = ax;
+            rq[i] = q;
+            rcol[i] = c;
+          }
+        }
+        const Cand<T> cd{rv[i], rq[i], rcol[i], psr[i], r0 + tid + i * nt};
+        if (better(cd, best)) best = cd;
+      }
+    }
+    if (prof) {
+      t1 = lu_timer();
+      p.prof[3] += t1 - t0;
+      p.prof[4] += 1;
+      t0 = t1;
+    }
+  }
+  __syncthreads();
+  // P^{-1} L for own rows: multipliers left of the row's physical position
+  // (before an early stop), the unit entry, zeros right of it
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int lr = tid + i * nt;
+    if (lr >= rows) continue;
+    const i64 s = r0 + lr;
+    const i64 pp = physl[lr];
+    const i64 bz = row_base(s, R, p.J, p.r);
+    for (int j = 0; j < p.r; ++j) {
+      T v = T(0);
+      if (pp == j) {
+        v = T(1);
+      } else if (j < pp && j < k0) {
+        const int c = col_at[j];
+        if (c < ns) {
+          v = a[c * ldl + lr];
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < RC; ++jj)
+            if (c == ns + jj) v = rg[i][jj];
+        }
+      }
+      p.Z[bz + j * R] = v;
+    }
+  }
+  if (b == 0 && tid == 0) *p.info = k0;
+}
+
 // ---------------------------------------------------------- Householder
 template <typename T>
 struct QrArgs {
@@ -1637,6 +1953,67 @@ void init_row_keys(const KoldaMap& km, i64 J, i64 R, i64* keys, cudaStream_t st)
   RCPG_LAUNCHED();
 }
 
+// Panel-resident LU (plu_resident_kernel) when the panel fits the SMs'
+// shared memory plus RC register columns: the smallest grid that fits, one
+// row per thread when possible. Returns false when it does not fit.
+template <typename T>
+bool plu_resident(T* A, T* Z, i64 J, i64 R, int n, int r, const KoldaMap& km, FactorWork& w, cudaStream_t st) {
+  const int nsm = std::min(device_caps().num_sms, 32 * kResKeyLoads);
+  if (J < 2 || J > i64(nsm) * 2 * 1024 || nsm > w.max_blocks) return false;
+  using K = void (*)(LuResArgs<T>);
+  struct V {
+    int rc, rpt;
+    K k;
+  };
+  static const V vars[] = {{0, 1, plu_resident_kernel<T, 0, 1>}, {4, 1, plu_resident_kernel<T, 4, 1>},
+                           {8, 1, plu_resident_kernel<T, 8, 1>}, {0, 2, plu_resident_kernel<T, 0, 2>},
+                           {4, 2, plu_resident_kernel<T, 4, 2>}, {8, 2, plu_resident_kernel<T, 8, 2>}};
+  static const struct Lim {
+    size_t smem[6];
+    int regs[6];
+  } lim = [] {
+    Lim l{};
+    for (int i = 0; i < 6; ++i) {
+      l.smem[i] = enable_max_dyn_smem(vars[i].k);
+      cudaFuncAttributes fa{};
+      RCPG_CUDA(cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(vars[i].k)));
+      l.regs[i] = fa.numRegs;
+    }
+    return l;
+  }();
+  for (int rpt = 1; rpt <= 2; ++rpt)
+    for (i64 G = std::max<i64>(1, ceil_div(J, i64(1024) * rpt)); G <= nsm; ++G) {
+      const int chunk = int(ceil_div(J, G));
+      const int nt = int(ceil_div(ceil_div(i64(chunk), rpt), 32) * 32);
+      for (int i = 0; i < 6; ++i) {
+        if (vars[i].rpt != rpt) continue;
+        const int rc = vars[i].rc;
+        const int ns = std::max(0, n - rc);
+        if (nt > lu_res_max_threads(rc, rpt) || nt * lim.regs[i] > 65536) continue;
+        if (rc > 0 && n - ns > rc) continue;
+        const size_t smem = ((size_t(ns) * chunk * sizeof(T) + 15) & ~size_t(15)) + size_t(chunk) * sizeof(i64);
+        if (smem > lim.smem[i]) continue;
+        if (ceil_div(J, i64(chunk)) != G) continue;  // every CTA owns rows
+        init_row_keys(km, J, R, w.keys, st);
+        LuResArgs<T> a{A, Z, J, R, n, r, ns, chunk, w.keys, km, reinterpret_cast<Cand<T>*>(w.cands),
+                       reinterpret_cast<T*>(w.part), w.bar, w.info, w.prof};
+        launch_coop(vars[i].k, int(G), nt, smem, st, a);
+        RCPG_LAUNCHED();
+        if (w.prof) {
+          unsigned long long h[8];
+          RCPG_CUDA(cudaMemcpyAsync(h, w.prof, sizeof(h), cudaMemcpyDeviceToHost, st));
+          RCPG_CUDA(cudaStreamSynchronize(st));
+          if (h[4])
+            fprintf(stderr, "[rcpg lu resident] J=%lld n=%d G=%d nt=%d rc=%d rpt=%d: reduce+publish %.2f  barrier %.2f  "
+                            "pick+book %.2f  update %.2f us/step\n", (long long)J, n, int(G), nt, rc, rpt,
+                    h[0] / 1e3 / h[4], h[1] / 1e3 / h[4], h[2] / 1e3 / h[4], h[3] / 1e3 / h[4]);
+        }
+        return true;
+      }
+    }
+  return false;
+}
+
 template <typename T>
 int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w, cudaStream_t st) {
   check_arg(n <= kMaxPanelCols, "plu_basis: panel wider than supported");
@@ -1653,7 +2030,11 @@ int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w
   // one CTA, rows owned by threads, swaps bookkept
   static const size_t oc_lim = enable_max_dyn_smem(plu_onchip_kernel<T>);
   const size_t oc_smem = size_t(J) * n * sizeof(T) + 2 * size_t(J) * sizeof(int);
-  if (oc_smem <= oc_lim && J * i64(n) < (i64(1) << 31) && std::getenv("RCPG_LU_CLUSTER") == nullptr) {
+  // A/B testing: RCPG_LU_PATH = cluster | resident | coop starts the chain
+  // (one CTA -> one cluster -> panel resident in the SMs -> grid) further down
+  const char* lp = std::getenv("RCPG_LU_PATH");
+  const std::string lpath = lp ? lp : "";
+  if (oc_smem <= oc_lim && J * i64(n) < (i64(1) << 31) && lpath.empty()) {
     // W row lanes (whole warps) x tpr column groups, at most 1024 threads
     const int W = int(std::min<i64>(1024, ceil_div(J, 32) * 32));
     const char* tp = std::getenv("RCPG_LU_TPR");
@@ -1670,7 +2051,7 @@ int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w
     return cudaFuncSetAttribute(plu_cluster_kernel<T, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
            cudaSuccess;
   }();
-  for (int cs = 1; cs <= (nonportable ? 16 : 8); cs *= 2) {
+  for (int cs = 1; cs <= (nonportable ? 16 : 8) && lpath != "coop" && lpath != "resident"; cs *= 2) {
     const int chunk = int(ceil_div(J, cs));
     const size_t smem = size_t(chunk) * n * sizeof(T) + 2 * size_t(n) * sizeof(T) + size_t(chunk) * sizeof(int) + 16;
     if (smem > (cs == 1 ? lu_lim1 : lu_lim) - 1024) continue;
@@ -1696,6 +2077,8 @@ int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w
     count_launch();
     return r;
   }
+  // panel resident in the SMs (grid of up to one CTA per SM, one grid barrier per pivot)
+  if (lpath != "coop" && plu_resident<T>(A, Z, J, R, n, r, km, w, st)) return r;
   init_row_keys(km, J, R, w.keys, st);
   LuArgs<T> a{A, Z, J, R, n, r, w.keys, km, reinterpret_cast<Cand<T>*>(w.cands), w.bar, w.info, w.prof,
               std::getenv("RCPG_LU_NODELAY") == nullptr ? 1 : 0};

@@ -87,25 +87,33 @@ def test_plu_basis_rank_deficient_and_ties(rcp, oracle):
 
 @pytest.mark.parametrize("rows,cols,dt", [(200, 20, np.float64), (400, 30, np.float64), (900, 30, np.float64),
                                          (37, 5, np.float64), (64, 64, np.float64), (3000, 8, np.float64),
-                                         (1024, 48, np.float32), (128, 48, np.float32)])
-def test_plu_basis_onchip_matches_cluster_path(rcp, oracle, rows, cols, dt, monkeypatch):
-    """The one-CTA LU (rows owned by threads, swaps bookkept) against the cluster LU (Eigen's
-    physical swaps): same pivots, same arithmetic in the same order -> identical bits."""
+                                         (1024, 48, np.float32), (128, 48, np.float32), (12000, 30, np.float64),
+                                         (20000, 70, np.float32), (160000, 30, np.float64), (50000, 48, np.float32)])
+def test_plu_basis_paths_agree_bitwise(rcp, oracle, rows, cols, dt, monkeypatch):
+    """Every LU path -- one CTA (rows owned by threads, swaps bookkept), panel resident in the SMs
+    (smem + register columns, one grid barrier per pivot), one cluster (Eigen's physical swaps),
+    grid over HBM (delayed write-back) -- makes the same pivots with the same arithmetic in the
+    same order: identical bits, on random panels and on integer panels full of exact ties."""
     rng = np.random.default_rng(rows * cols)
     m = np.asfortranarray(rng.standard_normal((rows, cols)).astype(dt))
-    got = rcp.plu_basis(m)
-    monkeypatch.setenv("RCPG_LU_CLUSTER", "1")
-    alt = rcp.plu_basis(m)
-    monkeypatch.delenv("RCPG_LU_CLUSTER")
-    assert np.array_equal(got, alt)
-    want = oracle.plu_basis(m.astype(np.float64))
-    assert np.max(np.abs(got - want)) <= (1e-12 if dt == np.float64 else 1e-3)
-    # integer panels: many exact ties, decided by the column-major first maximum
     t = np.asfortranarray(rng.integers(-2, 3, (rows, cols)).astype(dt))
-    monkeypatch.setenv("RCPG_LU_CLUSTER", "1")
-    alt = rcp.plu_basis(t)
-    monkeypatch.delenv("RCPG_LU_CLUSTER")
-    assert np.array_equal(rcp.plu_basis(t), alt)
+
+    def run(x, path):
+        if path:
+            monkeypatch.setenv("RCPG_LU_PATH", path)
+        else:
+            monkeypatch.delenv("RCPG_LU_PATH", raising=False)
+        return rcp.plu_basis(x)
+
+    got, tie = run(m, ""), run(t, "")
+    paths = ["resident", "coop"] + (["cluster"] if rows * cols * m.itemsize <= 3_000_000 else [])
+    for path in paths:
+        assert np.array_equal(run(m, path), got), path
+        assert np.array_equal(run(t, path), tie), path
+    monkeypatch.delenv("RCPG_LU_PATH", raising=False)
+    if rows * cols <= 600_000:
+        want = oracle.plu_basis(m.astype(np.float64))
+        assert np.max(np.abs(got - want)) <= (1e-12 if dt == np.float64 else 1e-3)
 
 
 @pytest.mark.parametrize("rows,cols", [(100, 20), (1024, 70)])
