@@ -936,8 +936,12 @@ struct LuResArgs {
 __host__ __device__ constexpr int lu_res_max_threads(int rc, int rpt) { return rc * rpt == 0 ? 1024 : 640; }
 constexpr int kResKeyLoads = 5;  // grids of up to 160 CTAs
 
-template <typename T, int RC, int RPT>
+// CL: the grid is one thread-block cluster; candidates and the winner's row
+// are exchanged through distributed shared memory, one cluster barrier per
+// pivot instead of a grid barrier.
+template <typename T, int RC, int RPT, bool CL>
 __global__ void __launch_bounds__(lu_res_max_threads(RC, RPT), 1) plu_resident_kernel(LuResArgs<T> p) {
+  namespace cg = cooperative_groups;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, nt = blockDim.x, G = gridDim.x, b = blockIdx.x;
   const int n = p.n, ns = p.ns, ldl = p.chunk;
@@ -953,6 +957,8 @@ __global__ void __launch_bounds__(lu_res_max_threads(RC, RPT), 1) plu_resident_k
   __shared__ i64 kinv[kMaxPanelCols];  // Kolda row at physical position k (before any swap)
   __shared__ Cand<T> red[33];
   __shared__ Cand<T> s_g;
+  __shared__ Cand<T> cpub[CL ? 2 : 1];                       // CL: this CTA's candidate per parity
+  __shared__ __align__(16) T rpub[CL ? 2 : 1][CL ? kMaxPanelCols : 1];  // CL: its row
   const Cand<T> none{T(-1), 0x7fffffff, 0, 0x7fffffffffffffffll, 0};
   T rg[RPT][RC > 0 ? RC : 1];
   for (int c = tid; c < n; c += nt) {
@@ -1000,12 +1006,17 @@ __global__ void __launch_bounds__(lu_res_max_threads(RC, RPT), 1) plu_resident_k
     const int par = k & 1;
     // 1. this CTA's best, published with its row's current values
     best = block_best(best, red);
-    if (tid == 0) p.pubk[par * G + b] = best;
+    if (tid == 0) {
+      if constexpr (CL)
+        cpub[par] = best;
+      else
+        p.pubk[par * G + b] = best;
+    }
     if (best.v > T(0) && best.s >= r0 && best.s < r0 + rows) {
       const int lr = int(best.s - r0);
       if (lr % nt == tid) {
         const int i = lr / nt;
-        T* dst = p.pubr + (i64(par) * G + b) * n;
+        T* dst = CL ? &rpub[par & (CL ? 1 : 0)][0] : p.pubr + (i64(par) * G + b) * n;
         for (int c = 0; c < ns; ++c) dst[c] = a[c * ldl + lr];
 #pragma unroll
         for (int ii = 0; ii < RPT; ++ii)
@@ -1021,7 +1032,10 @@ __global__ void __launch_bounds__(lu_res_max_threads(RC, RPT), 1) plu_resident_k
       p.prof[0] += t1 - t0;
       t0 = t1;
     }
-    grid_sync(p.bar);
+    if constexpr (CL)
+      cg::this_cluster().sync();
+    else
+      grid_sync(p.bar);
     if (prof) {
       t1 = lu_timer();
       p.prof[1] += t1 - t0;
@@ -1030,7 +1044,13 @@ __global__ void __launch_bounds__(lu_res_max_threads(RC, RPT), 1) plu_resident_k
     // 2. the winner (every CTA, same order), its row, the bookkeeping
     // up to five warps, one key per thread: every key load in flight at once
     if (tid < 32 * kResKeyLoads) {
-      Cand<T> g = tid < G ? load_cand_cg(p.pubk + par * G + tid) : none;
+      Cand<T> g = none;
+      if (tid < G) {
+        if constexpr (CL)
+          g = *cg::this_cluster().map_shared_rank(&cpub[par & (CL ? 1 : 0)], tid);
+        else
+          g = load_cand_cg(p.pubk + par * G + tid);
+      }
       int gw = tid;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -1066,8 +1086,13 @@ __global__ void __launch_bounds__(lu_res_max_threads(RC, RPT), 1) plu_resident_k
     }
     const i64 ss = g.s, pr = g.prow;
     const int cs = g.c, pc = g.pcol;
-    const T* src = p.pubr + (i64(par) * G + s_w) * n;
-    for (int c = tid; c < n; c += nt) U[c] = ldcg(src + c);
+    if constexpr (CL) {
+      const T* src = cg::this_cluster().map_shared_rank(&rpub[par & (CL ? 1 : 0)][0], s_w);
+      for (int c = tid; c < n; c += nt) U[c] = src[c];
+    } else {
+      const T* src = p.pubr + (i64(par) * G + s_w) * n;
+      for (int c = tid; c < n; c += nt) U[c] = ldcg(src + c);
+    }
     if (tid == 0) {
       i64 u = -1;  // row at physical position k before the swap
       for (int q = n_ov - 1; q >= 0; --q)
@@ -1223,6 +1248,7 @@ __global__ void __launch_bounds__(lu_res_max_threads(RC, RPT), 1) plu_resident_k
     }
   }
   if (b == 0 && tid == 0) *p.info = k0;
+  if constexpr (CL) cg::this_cluster().sync();  // keep this CTA's smem alive for remote readers
 }
 
 // ---------------------------------------------------------- Householder
@@ -1965,9 +1991,9 @@ bool plu_resident(T* A, T* Z, i64 J, i64 R, int n, int r, const KoldaMap& km, Fa
     int rc, rpt;
     K k;
   };
-  static const V vars[] = {{0, 1, plu_resident_kernel<T, 0, 1>}, {4, 1, plu_resident_kernel<T, 4, 1>},
-                           {8, 1, plu_resident_kernel<T, 8, 1>}, {0, 2, plu_resident_kernel<T, 0, 2>},
-                           {4, 2, plu_resident_kernel<T, 4, 2>}, {8, 2, plu_resident_kernel<T, 8, 2>}};
+  static const V vars[] = {{0, 1, plu_resident_kernel<T, 0, 1, false>}, {4, 1, plu_resident_kernel<T, 4, 1, false>},
+                           {8, 1, plu_resident_kernel<T, 8, 1, false>}, {0, 2, plu_resident_kernel<T, 0, 2, false>},
+                           {4, 2, plu_resident_kernel<T, 4, 2, false>}, {8, 2, plu_resident_kernel<T, 8, 2, false>}};
   static const struct Lim {
     size_t smem[6];
     int regs[6];
@@ -2014,6 +2040,54 @@ bool plu_resident(T* A, T* Z, i64 J, i64 R, int n, int r, const KoldaMap& km, Fa
   return false;
 }
 
+// The same resident LU on one thread-block cluster (2..16 CTAs, panel in
+// their shared memory): the smallest cluster that holds the panel with one
+// row per thread, else two. Returns false when no cluster holds it.
+template <typename T>
+bool plu_resident_cluster(T* A, T* Z, i64 J, i64 R, int n, int r, const KoldaMap& km, FactorWork& w,
+                          cudaStream_t st) {
+  using K = void (*)(LuResArgs<T>);
+  static const K k1 = plu_resident_kernel<T, 0, 1, true>, k2 = plu_resident_kernel<T, 0, 2, true>;
+  static const struct Lim {
+    size_t smem1, smem2;
+    bool nonportable;
+  } lim = [] {
+    Lim l{};
+    l.smem1 = enable_max_dyn_smem(k1);
+    l.smem2 = enable_max_dyn_smem(k2);
+    l.nonportable = cudaFuncSetAttribute(k1, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+                    cudaFuncSetAttribute(k2, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+    return l;
+  }();
+  const int csmax = lim.nonportable ? 16 : 8;
+  for (int rpt = 1; rpt <= 2; ++rpt)
+    for (int cs = 2; cs <= csmax; ++cs) {
+      const int chunk = int(ceil_div(J, i64(cs)));
+      const int nt = int(ceil_div(ceil_div(i64(chunk), rpt), 32) * 32);
+      if (nt > 1024 || ceil_div(J, i64(chunk)) != cs) continue;
+      const size_t smem = ((size_t(n) * chunk * sizeof(T) + 15) & ~size_t(15)) + size_t(chunk) * sizeof(i64);
+      if (smem > (rpt == 1 ? lim.smem1 : lim.smem2)) continue;
+      init_row_keys(km, J, R, w.keys, st);
+      LuResArgs<T> a{A, Z, J, R, n, r, n, chunk, w.keys, km, nullptr, nullptr, nullptr, w.info, nullptr};
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(cs);
+      cfg.blockDim = dim3(nt);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = cs;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      RCPG_CUDA(cudaLaunchKernelEx(&cfg, rpt == 1 ? k1 : k2, a));
+      count_launch();
+      return true;
+    }
+  return false;
+}
+
 template <typename T>
 int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w, cudaStream_t st) {
   check_arg(n <= kMaxPanelCols, "plu_basis: panel wider than supported");
@@ -2030,8 +2104,9 @@ int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w
   // one CTA, rows owned by threads, swaps bookkept
   static const size_t oc_lim = enable_max_dyn_smem(plu_onchip_kernel<T>);
   const size_t oc_smem = size_t(J) * n * sizeof(T) + 2 * size_t(J) * sizeof(int);
-  // A/B testing: RCPG_LU_PATH = cluster | resident | coop starts the chain
-  // (one CTA -> one cluster -> panel resident in the SMs -> grid) further down
+  // A/B testing: RCPG_LU_PATH = rcluster | cluster | resident | coop starts the
+  // chain (one CTA -> one cluster, swaps bookkept -> one cluster, Eigen's
+  // physical swaps -> panel resident in the SMs -> grid) further down
   const char* lp = std::getenv("RCPG_LU_PATH");
   const std::string lpath = lp ? lp : "";
   if (oc_smem <= oc_lim && J * i64(n) < (i64(1) << 31) && lpath.empty()) {
@@ -2044,6 +2119,9 @@ int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w
     RCPG_LAUNCHED();
     return r;
   }
+  // one thread-block cluster, panel resident, swaps bookkept (A/B only: its
+  // fixed per-pivot cost loses to the swap kernel below at these sizes)
+  if (lpath == "rcluster" && plu_resident_cluster<T>(A, Z, J, R, n, r, km, w, st)) return r;
   // on-chip paths: one CTA, or one cluster of up to 16 CTAs
   static const size_t lu_lim1 = enable_max_dyn_smem(plu_cluster_kernel<T, false>);
   static const size_t lu_lim = enable_max_dyn_smem(plu_cluster_kernel<T, true>);

@@ -90,10 +90,11 @@ def test_plu_basis_rank_deficient_and_ties(rcp, oracle):
                                          (1024, 48, np.float32), (128, 48, np.float32), (12000, 30, np.float64),
                                          (20000, 70, np.float32), (160000, 30, np.float64), (50000, 48, np.float32)])
 def test_plu_basis_paths_agree_bitwise(rcp, oracle, rows, cols, dt, monkeypatch):
-    """Every LU path -- one CTA (rows owned by threads, swaps bookkept), panel resident in the SMs
-    (smem + register columns, one grid barrier per pivot), one cluster (Eigen's physical swaps),
-    grid over HBM (delayed write-back) -- makes the same pivots with the same arithmetic in the
-    same order: identical bits, on random panels and on integer panels full of exact ties."""
+    """Every LU path -- one CTA (rows owned by threads, swaps bookkept), one cluster with the
+    panel resident and swaps bookkept (DSMEM exchange), one cluster with Eigen's physical swaps,
+    panel resident in the SMs (smem + register columns, one grid barrier per pivot), grid over
+    HBM (delayed write-back) -- makes the same pivots with the same arithmetic in the same
+    order: identical bits, on random panels and on integer panels full of exact ties."""
     rng = np.random.default_rng(rows * cols)
     m = np.asfortranarray(rng.standard_normal((rows, cols)).astype(dt))
     t = np.asfortranarray(rng.integers(-2, 3, (rows, cols)).astype(dt))
@@ -106,7 +107,7 @@ def test_plu_basis_paths_agree_bitwise(rcp, oracle, rows, cols, dt, monkeypatch)
         return rcp.plu_basis(x)
 
     got, tie = run(m, ""), run(t, "")
-    paths = ["resident", "coop"] + (["cluster"] if rows * cols * m.itemsize <= 3_000_000 else [])
+    paths = ["resident", "coop"] + (["cluster", "rcluster"] if rows * cols * m.itemsize <= 3_000_000 else [])
     for path in paths:
         assert np.array_equal(run(m, path), got), path
         assert np.array_equal(run(t, path), tie), path
