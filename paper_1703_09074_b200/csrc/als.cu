@@ -1083,6 +1083,110 @@ __global__ void __launch_bounds__(256) residual_kernel(const T* X, ShapeArg sh, 
   }
 }
 
+// fp64 ||X - Xhat||^2 and ||X||^2 with Xhat on the FP64 tensor cores
+// (mma.m16n8k4): X viewed as prefix x last (row-major), Xhat(p, l) =
+// sum_r coef[p][r] A_last[l][r]. A_last^T stays in smem for the whole
+// launch; per block of 64 prefix rows the coefficients are formed once and
+// every warp keeps its 16-row A fragments in registers while it walks half
+// of the n8 column tiles. X is read straight into the accumulator fragment
+// layout (two consecutive doubles per row per thread) and compared in fp64.
+// The SIMT residual_kernel is smem bound (one shared load per FMA); here a
+// DMMA does 512 FMAs from three register fragments.
+constexpr int kRdRows = 64;  // 4 m16 tiles per block step, 8 warps
+
+template <int KS>  // k4 steps: rank <= 4 * KS
+__global__ void __launch_bounds__(256) residual_dmma_kernel(const double* __restrict__ X, ShapeArg sh,
+                                                            FactorSet<double> fs, const double* __restrict__ w,
+                                                            double* part) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int dig[kRdRows][kMaxOrder];
+  const int R = fs.rank, N = sh.n;
+  const int L = int(sh.e[N - 1]);
+  const int NT8 = (L + 7) / 8;
+  constexpr int ldb = 4 * KS + 1;  // odd: the fragment reads spread over the banks
+  double* Bs = reinterpret_cast<double*>(smem_raw);  // [NT8 * 8][ldb] A_last rows (zero padded)
+  double* Cs = Bs + i64(NT8) * 8 * ldb;               // [kRdRows][ldb] coefficients
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  const double* Al = fs.f[N - 1];
+  for (int e = tid; e < NT8 * 8 * 4 * KS; e += blockDim.x) {
+    const int l = e / (4 * KS), r = e - l * (4 * KS);
+    Bs[l * ldb + r] = (l < L && r < R) ? Al[l + i64(r) * L] : 0.0;
+  }
+  i64 prefix = 1;
+  for (int m = 0; m < N - 1; ++m) prefix *= sh.e[m];
+  const int mt = warp & 3, nh = warp >> 2;
+  const bool v16 = (L & 1) == 0;
+  double acc_r = 0.0, acc_x = 0.0;
+  for (i64 p0 = i64(blockIdx.x) * kRdRows; p0 < prefix; p0 += i64(gridDim.x) * kRdRows) {
+    __syncthreads();
+    if (tid < kRdRows) {
+      i64 rem = p0 + tid;
+      for (int m = N - 2; m >= 0; --m) {
+        dig[tid][m] = int(rem % sh.e[m]);
+        rem /= sh.e[m];
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < kRdRows * 4 * KS; e += blockDim.x) {
+      const int q = e % kRdRows, r = e / kRdRows;
+      double v = 0.0;
+      if (p0 + q < prefix && r < R) {
+        v = w[r];
+        for (int m = N - 2; m >= 0; --m) v *= fs.f[m][dig[q][m] + i64(r) * sh.e[m]];
+      }
+      Cs[q * ldb + r] = v;
+    }
+    __syncthreads();
+    double a0[KS], a1[KS];
+#pragma unroll
+    for (int s = 0; s < KS; ++s) {
+      a0[s] = Cs[(mt * 16 + g) * ldb + 4 * s + t];
+      a1[s] = Cs[(mt * 16 + g + 8) * ldb + 4 * s + t];
+    }
+    const i64 row0 = p0 + mt * 16 + g, row1 = row0 + 8;
+    const bool ok0 = row0 < prefix, ok1 = row1 < prefix;
+    const double* x0 = X + row0 * L;
+    const double* x1 = X + row1 * L;
+#pragma unroll 4
+    for (int nt = nh; nt < NT8; nt += 2) {
+      const int c = nt * 8 + 2 * t;
+      double x00 = 0.0, x01 = 0.0, x10 = 0.0, x11 = 0.0;
+      if (v16 && c + 1 < L) {
+        if (ok0) {
+          const double2 v = *reinterpret_cast<const double2*>(x0 + c);
+          x00 = v.x;
+          x01 = v.y;
+        }
+        if (ok1) {
+          const double2 v = *reinterpret_cast<const double2*>(x1 + c);
+          x10 = v.x;
+          x11 = v.y;
+        }
+      } else {
+        if (ok0 && c < L) x00 = x0[c];
+        if (ok0 && c + 1 < L) x01 = x0[c + 1];
+        if (ok1 && c < L) x10 = x1[c];
+        if (ok1 && c + 1 < L) x11 = x1[c + 1];
+      }
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int s = 0; s < KS; ++s) als_dmma(acc, a0[s], a1[s], Bs[(nt * 8 + g) * ldb + 4 * s + t]);
+      // acc: (row g, col c), (g, c + 1), (g + 8, c), (g + 8, c + 1); padding is zero on both sides
+      const double d00 = x00 - acc[0], d01 = x01 - acc[1], d10 = x10 - acc[2], d11 = x11 - acc[3];
+      const bool c0 = c < L, c1 = c + 1 < L;
+      acc_r += (ok0 && c0 ? d00 * d00 : 0.0) + (ok0 && c1 ? d01 * d01 : 0.0) + (ok1 && c0 ? d10 * d10 : 0.0) +
+               (ok1 && c1 ? d11 * d11 : 0.0);
+      acc_x += (x00 * x00 + x01 * x01) + (x10 * x10 + x11 * x11);
+    }
+  }
+  acc_r = block_reduce_sum(acc_r);
+  acc_x = block_reduce_sum(acc_x);
+  if (tid == 0) {
+    part[2 * blockIdx.x] = acc_r;
+    part[2 * blockIdx.x + 1] = acc_x;
+  }
+}
+
 // ------------------------------------------------------------ synthetic
 struct DFactors {
   const double* f[kMaxOrder];
@@ -1291,6 +1395,19 @@ void norm_and_finite(const T* x, i64 n, double* out2, double* scratch, int num_s
   RCPG_LAUNCHED();
 }
 
+template <int KS>
+bool launch_residual_dmma(const double* X, const ShapeArg& sh, const FactorSet<double>& fs, const double* w,
+                          double* part, int blocks, i64 L, cudaStream_t st) {
+  // [NT8 * 8 + kRdRows][4 KS + 1] doubles, the kernel's own layout
+  const size_t smem = (size_t(ceil_div(L, 8)) * 8 + kRdRows) * size_t(4 * KS + 1) * sizeof(double);
+  static const size_t lim = enable_max_dyn_smem(residual_dmma_kernel<KS>);
+  if (smem > lim) return false;
+  residual_dmma_kernel<KS><<<blocks, 256, smem, st>>>(X, sh, fs, w, part);
+  count_launch();
+  RCPG_LAUNCHED();
+  return true;
+}
+
 size_t residual_scratch_doubles(int num_sms, i64 last_extent, int rank) {
   // per-CTA partial pairs (+ the C^T hi / lo planes of the tensor-core path)
   return size_t(num_sms) * 8 * 2 + 16 + (residual_tc_scratch_floats(last_extent, rank) + 1) / 2 + 16;
@@ -1315,6 +1432,26 @@ void residual_norms(const T* X, const i64* shape, int order, const FactorSet<T>&
   const ShapeArg sh = make_shape(shape, order);
   i64 prefix = 1;
   for (int m = 0; m < order - 1; ++m) prefix *= shape[m];
+  if constexpr (std::is_same<T, double>::value) {
+    const i64 L = shape[order - 1];
+    const int KS = (fs.rank + 3) / 4;
+    if (order >= 2 && KS <= 8 && L >= 8 && std::getenv("RCPG_RESIDUAL_SIMT") == nullptr) {
+      const int blocks = int(std::max<i64>(1, std::min<i64>(ceil_div(prefix, kRdRows), i64(num_sms) * 2)));
+      bool done = false;
+      if (KS <= 2) done = launch_residual_dmma<2>(X, sh, fs, weights, scratch, blocks, L, st);
+      else if (KS <= 3) done = launch_residual_dmma<3>(X, sh, fs, weights, scratch, blocks, L, st);
+      else if (KS <= 4) done = launch_residual_dmma<4>(X, sh, fs, weights, scratch, blocks, L, st);
+      else if (KS <= 5) done = launch_residual_dmma<5>(X, sh, fs, weights, scratch, blocks, L, st);
+      else if (KS <= 6) done = launch_residual_dmma<6>(X, sh, fs, weights, scratch, blocks, L, st);
+      else done = launch_residual_dmma<8>(X, sh, fs, weights, scratch, blocks, L, st);
+      if (done) {
+        sum_pairs_kernel<<<1, 256, 0, st>>>(scratch, blocks, out2);
+        count_launch();
+        RCPG_LAUNCHED();
+        return;
+      }
+    }
+  }
   const int blocks = int(std::max<i64>(1, std::min<i64>(ceil_div(prefix, kResRows), i64(num_sms) * 8)));
   residual_kernel<T><<<blocks, 256, 0, st>>>(X, sh, fs, weights, scratch);
   sum_pairs_kernel<<<1, 256, 0, st>>>(scratch, blocks, out2);
