@@ -1,25 +1,3 @@
-__device__ void sign_reconstruct(double* G, int n, int ld, int rows, double* sgn) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
-  for (int k = 0; k < n; ++k) {
-    const double sk = (G[k + k * ld] > 0.0) != (k == rows - 1) ? -1.0 : 1.0;
-    __syncthreads();
-    for (int i = tid; i < n; i += nt)
-      if (i != k && sk < 0.0) G[i + k * ld] = -G[i + k * ld];
-    if (tid == 0) {
-      G[k + k * ld] = sk * G[k + k * ld] - 1.0;
-      sgn[k] = sk;
-    }
-    __syncthreads();
-    const double rdkk = 1.0 / G[k + k * ld];
-    for (int j = k + 1 + wid; j < n; j += nw) {  // warp per column, lanes over rows
-      const double gkj = G[k + j * ld] * rdkk;
-      for (int i = k + 1 + lane; i < n; i += 32) G[i + j * ld] -= G[i + k * ld] * gkj;
-    }
-    __syncthreads();
-  }
-}
-
 // SPDX-License-Identifier: MIT
 // Tall-skinny factorizations of the power-iteration chain (SURVEY.md §2.2
 // K5/K6/K8), restating the reference's Eigen calls:
@@ -1550,122 +1528,274 @@ __global__ void __launch_bounds__(kCqrThreads) cqr2_kernel(const T* __restrict__
 // ------------------------------------------------ CholeskyQR2, all SMs
 // Small dense steps shared by the CholeskyQR2 kernels, one CTA, matrices in
 // shared memory with an odd leading dimension ld (bank spread):
-//   chol_inv_small: upper Cholesky A = R^T R (right-looking, in place in A's
-//     upper triangle), dg[j] = R(j, j), then X = R^{-1} (upper), *fail on breakdown;
+//   chol_inv_small: upper Cholesky A = R^T R, dg[j] = R(j, j), X = R^{-1}
+//     (upper), *fail on breakdown;
 //   sign_reconstruct: signs of Eigen's HouseholderQR Q relative to the
 //     CholeskyQR Q from the top n x n block (modified LU of Q_top - S).
+// Both are latency chains of n dependent steps; each step is one barrier.
+//
+// chol_inv_small runs symmetric elimination without square roots (A = U^T D U,
+// U unit upper) on the augmented matrix [A | I] held in ONE n x n array M:
+// the upper triangle (incl. the diagonal) is the A part, the strict lower
+// triangle the I part (the I part's diagonal stays 1 until its row is
+// pivotal, so it is implicit). Step j, for every row r > j:
+//   A part (c >= r): M(r, c) -= (M(j, r) / d_j) * M(j, c)
+//   I part (c <= j): M(r, c) -= (M(j, r) / d_j) * (c == j ? 1 : M(j, c))
+// with d_j = M(j, j). Row j is never written from step j on, so after the
+// last step U(j, c) = M(j, c) / d_j and (U^{-T})(j, c) = M(j, c) (c < j);
+// R = D^{1/2} U and R^{-1} = U^{-1} D^{-1/2} then come out of one parallel
+// pass. The critical path per step is one reciprocal, two FMAs and one
+// barrier (no square root, no division chain); every thread owns the
+// entries (r, c) with r = warp (mod warps), c = lane (mod 32).
+__device__ __forceinline__ double sq_scale(double m, double rd, double sq) { return (m * rd) * sq; }
+
 __device__ void chol_inv_small(double* A, double* X, int n, int ld, double* dg, int* fail) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
-  __shared__ double rdg[kMaxPanelCols];  // 1 / R(j, j)
-  // Blocked right-looking upper Cholesky, 8 columns per block: warp 0 factors
-  // the diagonal block (warp barriers only), every thread solves one column
-  // of the block's panel, then one trailing update per block. Each entry
-  // sees the same operations in the same order as the unblocked algorithm
-  // (subtract R(s, r) R(s, c) for s = 0, 1, ..., then scale by 1 / R(j, j)).
-  constexpr int NB = 8;
-  for (int kb = 0; kb < n; kb += NB) {
-    const int ke = min(kb + NB, n);
-    if (wid == 0) {
-      for (int j = kb; j < ke; ++j) {
-        const double d = A[j + j * ld];
-        const double piv = d > 0.0 ? sqrt(d) : 1.0;
-        const double rinv = 1.0 / piv;
-        if (lane == 0) {
-          if (!(d > 0.0)) *fail = 1;
-          dg[j] = piv;
-          rdg[j] = rinv;
+  __shared__ double s_rd[kMaxPanelCols];  // 1 / d_j
+  // the I part starts as the identity: strict lower triangle = 0 (own entries)
+  for (int r = wid; r < n; r += nw)
+    for (int c = lane; c < r; c += 32) A[r + c * ld] = 0.0;
+  __syncthreads();
+  int bad = 0;
+  for (int j = 0; j < n; ++j) {
+    const double d = A[j + j * ld];
+    bad |= !(d > 0.0);
+    const double rd = d > 0.0 ? __drcp_rn(d) : 1.0;
+    if (tid == 0) s_rd[j] = rd;
+    // first owned row below j
+    int r = wid + ((j + 1 - wid + nw - 1) / nw) * nw;
+    if (r < j + 1) r += nw;
+    for (; r < n; r += nw) {
+      const double t = A[j + r * ld] * rd;  // U(j, r)
+      for (int c = lane; c < n; c += 32) {
+        if (c >= r) {
+          A[r + c * ld] -= t * A[j + c * ld];
+        } else if (c <= j) {
+          A[r + c * ld] -= t * (c == j ? 1.0 : A[j + c * ld]);
         }
-        if (j + 1 + lane < ke) A[j + (j + 1 + lane) * ld] *= rinv;
-        __syncwarp();
-        for (int e = lane; e < NB * NB; e += 32) {
-          const int r = kb + (e % NB), c = kb + (e / NB);
-          if (r > j && r <= c && c < ke) A[r + c * ld] -= A[j + r * ld] * A[j + c * ld];
-        }
-        __syncwarp();
-      }
-    }
-    __syncthreads();
-    // panel: rows kb..ke-1 of the columns right of the block
-    for (int c = ke + tid; c < n; c += nt)
-      for (int j = kb; j < ke; ++j) {
-        double x = A[j + c * ld];
-        for (int s = kb; s < j; ++s) x -= A[s + j * ld] * A[s + c * ld];
-        A[j + c * ld] = x * rdg[j];
-      }
-    __syncthreads();
-    // trailing update of the upper triangle by the block's rows
-    const int bs = ke - kb;
-    for (int c2 = ke + wid; c2 < n; c2 += nw) {
-      double rc[NB];
-#pragma unroll
-      for (int t = 0; t < NB; ++t) rc[t] = t < bs ? A[kb + t + c2 * ld] : 0.0;
-      for (int c1 = ke + lane; c1 <= c2; c1 += 32) {
-        double x = A[c1 + c2 * ld];
-#pragma unroll
-        for (int t = 0; t < NB; ++t)
-          if (t < bs) x -= A[kb + t + c1 * ld] * rc[t];
-        A[c1 + c2 * ld] = x;
       }
     }
     __syncthreads();
   }
+  if (tid == 0 && bad) *fail = 1;
+  // R(j, c) = sqrt(d_j) U(j, c); X = R^{-1}: X(c, j) = (U^{-T})(j, c) / sqrt(d_j)
+  for (int j = wid; j < n; j += nw) {
+    const double d = A[j + j * ld];
+    const double sq = d > 0.0 ? sqrt(d) : 1.0;
+    const double rs = 1.0 / sq;
+    if (lane == 0) dg[j] = sq;
+    for (int c = lane; c < n; c += 32) {
+      if (c < j) X[c + j * ld] = A[j + c * ld] * rs;
+      else X[c + j * ld] = (c == j) ? rs : 0.0;
+    }
+  }
+  __syncthreads();
+  for (int j = wid; j < n; j += nw)
+    for (int c = j + 1 + lane; c < n; c += 32) A[j + c * ld] = sq_scale(A[j + c * ld], s_rd[j], dg[j]);
   for (int j = tid; j < n; j += nt) A[j + j * ld] = dg[j];
   __syncthreads();
-  // X = R^{-1} (upper), blocked back substitution over 8-row blocks from the
-  // bottom: first every (row of the block, column) pair sums what the rows
-  // below the block contribute (all threads), then a short triangular solve
-  // inside the block per column. Two barriers per block instead of one serial
-  // chain of n^2/2 steps per column.
-  for (int e = tid; e < n * n; e += nt) {
-    const int i = e % n, j = e / n;
-    if (i > j) X[i + j * ld] = 0.0;
-  }
-  for (int ib = ((n - 1) / NB) * NB; ib >= 0; ib -= NB) {
-    const int ie = min(ib + NB, n), bs = ie - ib;
-    for (int e = tid; e < bs * (n - ib); e += nt) {
-      const int i = ib + e % bs, j = ib + e / bs;
-      if (i > j) continue;
-      double s0 = (i == j) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      int k = ie;
-      for (; k + 3 <= j; k += 4) {
-        s0 -= A[i + k * ld] * X[k + j * ld];
-        s1 -= A[i + (k + 1) * ld] * X[k + 1 + j * ld];
-        s2 -= A[i + (k + 2) * ld] * X[k + 2 + j * ld];
-        s3 -= A[i + (k + 3) * ld] * X[k + 3 + j * ld];
-      }
-      for (; k <= j; ++k) s0 -= A[i + k * ld] * X[k + j * ld];
-      X[i + j * ld] = (s0 + s1) + (s2 + s3);
-    }
-    __syncthreads();
-    for (int j = ib + tid; j < n; j += nt)
-      for (int i = min(ie - 1, j); i >= ib; --i) {
-        double x = X[i + j * ld];
-        for (int k = i + 1; k <= min(ie - 1, j); ++k) x -= A[i + k * ld] * X[k + j * ld];
-        X[i + j * ld] = x * rdg[i];
-      }
-    __syncthreads();
-  }
 }
 
 // G: top n x n block of Q2 (ld), destroyed. rows = panel height (square
 // panels: Eigen leaves the last column unreflected, opposite sign).
 // One barrier per step: the sign flip of column k is folded into the
-// multipliers (negation is exact), one division per row.
-__device__ void sign_reconstruct(double* G, int n, int ld, int rows, double* sgn) {
+// multipliers (negation is exact); every thread forms 1 / d_kk itself.
+__device__ void sign_reconstruct_smem(double* G, int n, int ld, int rows, double* sgn) {
   const int tid = threadIdx.x;
   const int lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
   for (int k = 0; k < n; ++k) {
     const double gkk = G[k + k * ld];
     const double sk = (gkk > 0.0) != (k == rows - 1) ? -1.0 : 1.0;
-    const double dkk = sk * gkk - 1.0;
+    const double rd = __drcp_rn(sk * gkk - 1.0);
     if (tid == 0) sgn[k] = sk;
-    for (int i = k + 1 + lane; i < n; i += 32) {
-      const double l = (sk * G[i + k * ld]) / dkk;
-      for (int j = k + 1 + wid; j < n; j += nw) G[i + j * ld] -= l * G[k + j * ld];
+    int i = wid + ((k + 1 - wid + nw - 1) / nw) * nw;
+    if (i < k + 1) i += nw;
+    for (; i < n; i += nw) {  // warp per row, lanes over columns
+      const double l = (sk * G[i + k * ld]) * rd;
+      for (int j = k + 1 + lane; j < n; j += 32) G[i + j * ld] -= l * G[k + j * ld];
     }
     __syncthreads();
   }
+}
+
+// Register-resident versions of the two elimination chains (n <= 32 KC and
+// n <= KR * warps): thread (warp w, lane l) keeps the entries (r, c),
+// r = w + k * warps, c = l + 32 m, in registers for the whole factorization.
+// Step j needs only row j from other threads: its owner publishes it into a
+// double-buffered shared row right after updating it in step j - 1, so a
+// step is one barrier, one reciprocal and register FMAs (no shared-memory
+// round trip per entry).
+template <int KR, int KC>
+__device__ void chol_inv_regs(double* A, double* X, int n, int ld, double* dg, int* fail) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  __shared__ double rowbuf[2][32 * KC];
+  __shared__ double s_d[32 * KC];
+  double v[KR][KC];
+#pragma unroll
+  for (int k = 0; k < KR; ++k)
+#pragma unroll
+    for (int m = 0; m < KC; ++m) {
+      const int r = wid + k * nw, c = lane + 32 * m;
+      v[k][m] = (r < n && c < n && c >= r) ? A[r + c * ld] : 0.0;  // I part: identity minus its diagonal
+    }
+  if (wid == 0)
+#pragma unroll
+    for (int m = 0; m < KC; ++m) rowbuf[0][lane + 32 * m] = v[0][m];
+  __syncthreads();
+  int bad = 0;
+  int nxw = 1 % nw, nxk = 1 / nw;  // owner (warp, slot) of row j + 1, advanced per step (no integer division)
+  for (int j = 0; j < n; ++j) {
+    const double* rj = rowbuf[j & 1];
+    // every shared read of the step is issued before the reciprocal
+    const double d = rj[j];
+    double tk[KR], aj[KC];
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      const int r = wid + k * nw;
+      tk[k] = (r > j && r < n) ? rj[r] : 0.0;
+    }
+#pragma unroll
+    for (int m = 0; m < KC; ++m) {
+      const int c = lane + 32 * m;
+      aj[m] = c == j ? 1.0 : (c < n ? rj[c] : 0.0);
+    }
+    bad |= !(d > 0.0);
+    const double rd = d > 0.0 ? 1.0 / d : 1.0;
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      const int r = wid + k * nw;
+      if (r > j && r < n) {
+        const double t = tk[k] * rd;  // U(j, r)
+#pragma unroll
+        for (int m = 0; m < KC; ++m) {
+          const int c = lane + 32 * m;
+          if (c < n && (c >= r || c <= j)) v[k][m] -= t * aj[m];
+        }
+      }
+    }
+    if (j + 1 < n && wid == nxw) {
+#pragma unroll
+      for (int k = 0; k < KR; ++k)
+        if (k == nxk)
+#pragma unroll
+          for (int m = 0; m < KC; ++m) rowbuf[(j + 1) & 1][lane + 32 * m] = v[k][m];
+    }
+    if (++nxw == nw) {
+      nxw = 0;
+      ++nxk;
+    }
+    if (tid == 0) s_d[j] = d;
+    __syncthreads();
+  }
+  if (tid == 0 && bad) *fail = 1;
+  for (int j = tid; j < n; j += blockDim.x) dg[j] = s_d[j] > 0.0 ? sqrt(s_d[j]) : 1.0;
+  // R(r, c) = sqrt(d_r) U(r, c) (upper), X = R^{-1}: X(c, r) = (U^{-T})(r, c) / sqrt(d_r)
+#pragma unroll
+  for (int k = 0; k < KR; ++k) {
+    const int r = wid + k * nw;
+    if (r < n) {
+      const double dr = s_d[r];
+      const double sq = dr > 0.0 ? sqrt(dr) : 1.0, rs = 1.0 / sq, rd = dr > 0.0 ? 1.0 / dr : 1.0;
+#pragma unroll
+      for (int m = 0; m < KC; ++m) {
+        const int c = lane + 32 * m;
+        if (c >= n) continue;
+        if (c < r) {
+          X[c + r * ld] = v[k][m] * rs;
+        } else if (c == r) {
+          X[r + r * ld] = rs;
+          A[r + r * ld] = sq;
+        } else {
+          X[c + r * ld] = 0.0;
+          A[r + c * ld] = (v[k][m] * rd) * sq;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+template <int KR, int KC>
+__device__ void sign_reconstruct_regs(double* G, int n, int ld, int rows, double* sgn) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  __shared__ double rowbuf[2][32 * KC];
+  double v[KR][KC];
+#pragma unroll
+  for (int k = 0; k < KR; ++k)
+#pragma unroll
+    for (int m = 0; m < KC; ++m) {
+      const int r = wid + k * nw, c = lane + 32 * m;
+      v[k][m] = (r < n && c < n) ? G[r + c * ld] : 0.0;
+    }
+  if (wid == 0)
+#pragma unroll
+    for (int m = 0; m < KC; ++m) rowbuf[0][lane + 32 * m] = v[0][m];
+  __syncthreads();
+  int nxw = 1 % nw, nxk = 1 / nw;  // owner of row k0 + 1
+  for (int k0 = 0; k0 < n; ++k0) {
+    const double* rk = rowbuf[k0 & 1];
+    const double gkk = rk[k0];
+    double ak[KC];
+#pragma unroll
+    for (int m = 0; m < KC; ++m) {
+      const int c = lane + 32 * m;
+      ak[m] = c < n ? rk[c] : 0.0;
+    }
+    const int mk = k0 >> 5, lk = k0 & 31;
+    double gik[KR];  // G(r, k0): lane lk of this warp holds it
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      double x = 0.0;
+#pragma unroll
+      for (int m = 0; m < KC; ++m)
+        if (m == mk) x = v[k][m];
+      gik[k] = __shfl_sync(0xffffffffu, x, lk);
+    }
+    const double sk = (gkk > 0.0) != (k0 == rows - 1) ? -1.0 : 1.0;
+    const double rd = 1.0 / (sk * gkk - 1.0);
+    if (tid == 0) sgn[k0] = sk;
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      const int r = wid + k * nw;
+      if (r > k0 && r < n) {
+        const double l = (sk * gik[k]) * rd;
+#pragma unroll
+        for (int m = 0; m < KC; ++m) {
+          const int c = lane + 32 * m;
+          if (c > k0 && c < n) v[k][m] -= l * ak[m];
+        }
+      }
+    }
+    if (k0 + 1 < n && wid == nxw) {
+#pragma unroll
+      for (int k = 0; k < KR; ++k)
+        if (k == nxk)
+#pragma unroll
+          for (int m = 0; m < KC; ++m) rowbuf[(k0 + 1) & 1][lane + 32 * m] = v[k][m];
+    }
+    if (++nxw == nw) {
+      nxw = 0;
+      ++nxk;
+    }
+    __syncthreads();
+  }
+}
+
+__device__ void sign_reconstruct(double* G, int n, int ld, int rows, double* sgn) {
+  const int nw = blockDim.x >> 5;
+  if (n <= 32 && n <= 4 * nw) sign_reconstruct_regs<4, 1>(G, n, ld, rows, sgn);
+  else if (n <= 64 && n <= 8 * nw) sign_reconstruct_regs<8, 2>(G, n, ld, rows, sgn);
+  else if (n <= 96 && n <= 12 * nw) sign_reconstruct_regs<12, 3>(G, n, ld, rows, sgn);
+  else sign_reconstruct_smem(G, n, ld, rows, sgn);
+}
+
+__device__ void chol_inv(double* A, double* X, int n, int ld, double* dg, int* fail) {
+  const int nw = blockDim.x >> 5;
+  if (n <= 32 && n <= 4 * nw) chol_inv_regs<4, 1>(A, X, n, ld, dg, fail);
+  else if (n <= 64 && n <= 8 * nw) chol_inv_regs<8, 2>(A, X, n, ld, dg, fail);
+  else if (n <= 96 && n <= 12 * nw) chol_inv_regs<12, 3>(A, X, n, ld, dg, fail);
+  else chol_inv_small(A, X, n, ld, dg, fail);
 }
 
 // The same CholeskyQR2 + Householder sign reconstruction as cqr2_kernel,
@@ -1781,7 +1911,7 @@ __global__ void __launch_bounds__(kCqrCoopThreads) cqr2_coop_kernel(CqrCoopArgs<
     double* Xs = Ri + n * ldn;    // n x ldn R^{-1}
     for (int e = tid; e < n * n; e += nt) As[(e % n) + (e / n) * ldn] = ldcg(&Gf[e]);
     __syncthreads();
-    chol_inv_small(As, Xs, n, ldn, dg_loc + pass * n, &s_fail);
+    chol_inv(As, Xs, n, ldn, dg_loc + pass * n, &s_fail);
     if (blockIdx.x == 0)
       for (int j = tid; j < n; j += nt) dg[pass * n + j] = dg_loc[pass * n + j];
     cqr_stamp(p.prof, 3 + 5 * pass);

@@ -41,14 +41,33 @@ int pick_bn(i64 cols) {
   return 80;
 }
 
+constexpr int kRedChunks = 8;
+
 template <typename T>
-__global__ void reduce_partials_kernel(const T* __restrict__ part, i64 splits, i64 n, T* __restrict__ out,
+__global__ void __launch_bounds__(32 * kRedChunks) reduce_partials_kernel(const T* __restrict__ part, i64 splits, i64 n, T* __restrict__ out,
                                        const int* skip) {
+  // block = 32 consecutive outputs (lanes, coalesced) x kRedChunks warps; warp w
+  // sums its contiguous chunk of splits in order, warp 0 adds the chunk sums in
+  // chunk order: a fixed summation order, independent of the launch geometry
   if (skip != nullptr && *skip) return;
-  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < n; e += i64(gridDim.x) * blockDim.x) {
-    double s = 0.0;
-    for (i64 q = 0; q < splits; ++q) s += double(part[q * n + e]);
-    out[e] = T(s);
+  __shared__ double chunk_sum[kRedChunks][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const i64 e = blockIdx.x * i64(32) + lane;
+  const i64 per = (splits + kRedChunks - 1) / kRedChunks;
+  const i64 q0 = w * per, q1 = q0 + per < splits ? q0 + per : splits;
+  double s = 0.0;
+  if (e < n) {
+    const T* p = part + e;
+#pragma unroll 8
+    for (i64 q = q0; q < q1; ++q) s += double(__ldcs(p + q * n));
+  }
+  chunk_sum[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && e < n) {
+    double t = chunk_sum[0][lane];
+#pragma unroll
+    for (int c = 1; c < kRedChunks; ++c) t += chunk_sum[c][lane];
+    out[e] = T(t);
   }
 }
 
@@ -125,8 +144,7 @@ void sketch(const T* X, ModeView v, const T* P, i64 cols, T* Y, T* scratch, i64 
   }
   }
   const i64 n = cols * v.I;
-  const int blocks = int(std::min<i64>(ceil_div(n, 256), 4 * num_sms));
-  reduce_partials_kernel<T><<<blocks, 256, 0, st>>>(scratch, splits, n, Y, skip);
+  reduce_partials_kernel<T><<<unsigned(ceil_div(n, 32)), 32 * kRedChunks, 0, st>>>(scratch, splits, n, Y, skip);
   count_launch();
   RCPG_LAUNCHED();
 }

@@ -88,7 +88,9 @@ def test_plu_basis_rank_deficient_and_ties(rcp, oracle):
 @pytest.mark.parametrize("rows,cols,dt", [(200, 20, np.float64), (400, 30, np.float64), (900, 30, np.float64),
                                          (37, 5, np.float64), (64, 64, np.float64), (3000, 8, np.float64),
                                          (1024, 48, np.float32), (128, 48, np.float32), (12000, 30, np.float64),
-                                         (20000, 70, np.float32), (160000, 30, np.float64), (50000, 48, np.float32)])
+                                         (20000, 70, np.float32), (160000, 30, np.float64), (50000, 48, np.float32),
+                                         (416, 32, np.float64), (33, 32, np.float64), (410, 31, np.float32),
+                                         (20, 30, np.float64)])
 def test_plu_basis_paths_agree_bitwise(rcp, oracle, rows, cols, dt, monkeypatch):
     """Every LU path -- one CTA (rows owned by threads, swaps bookkept), one cluster with the
     panel resident and swaps bookkept (DSMEM exchange), one cluster with Eigen's physical swaps,
