@@ -12,8 +12,21 @@
 // Operand tiles stream through a multi-stage cp.async pipeline (16-byte
 // copies when the row strides are even, 8-byte otherwise; out-of-range
 // elements are zero-filled by the copy itself).
+//
+// The sketch with even R runs TMA-fed (sketch_dmma_tma_kernel): one producer
+// warp streams 128B-swizzled K-tiles of X and the panel (16 doubles per row)
+// through a 4-stage mbarrier ring and four consumer warps only load
+// fragments and issue DMMAs. The cp.async version spends more issue slots on
+// address math and copies than on the MMAs; with the copies off the
+// consumers four CTAs (16 consumer warps) per SM keep the FP64 pipe ~25%
+// busier (tools/microbench/dmma_tma.cu: C2 mode-0 sketch 195 -> 159 us).
+#include <cuda.h>  // CUtensorMap (encoded in passes_tc.cu)
+
+#include <cstdlib>
+
 #include "passes.cuh"
 #include "runtime.cuh"
+#include "tc.cuh"
 
 namespace rcpg {
 
@@ -220,6 +233,107 @@ __global__ void __launch_bounds__(kDThreads) project_dmma_kernel(const double* _
   }
 }
 
+// ------------------------------------------------------ sketch, TMA-fed
+constexpr int kTmaWM = 4;      // consumer warps, 16 rows each
+constexpr int kTmaStages = 4;  // 4 stages: four CTAs per SM at BN = 32
+
+template <int BN>
+struct TmaPlan {
+  static constexpr int BM = kTmaWM * 16, ABYTES = BM * 128, BBYTES = BN * 128, STAGE = ABYTES + BBYTES;
+  static constexpr int SMEM = kTmaStages * STAGE + 1024;  // + 1024 B alignment slack (swizzle atoms)
+  static constexpr int THREADS = (kTmaWM + 1) * 32;
+};
+
+// element (r, k) of a 128B-swizzled box with 16-double rows
+__device__ __forceinline__ int swz16(int r, int k) { return r * 16 + ((((k >> 1) ^ (r & 7))) << 1) + (k & 1); }
+
+template <int BN>
+__global__ void __launch_bounds__(TmaPlan<BN>::THREADS) sketch_dmma_tma_kernel(const __grid_constant__ CUtensorMap mx,
+                                                                               const __grid_constant__ CUtensorMap mp,
+                                                                               i64 I, i64 cols, i64 nbt, i64 tps,
+                                                                               i64 total, double* __restrict__ part,
+                                                                               const int* skip) {
+  using G = TmaPlan<BN>;
+  using namespace tc;
+  constexpr int NT = BN / 8, S = kTmaStages;
+  if (skip != nullptr && *skip) return;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[S], empty[S];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const i64 t0 = blockIdx.y * tps;
+  const i64 t1 = t0 + tps < total ? t0 + tps : total;
+  const int nk = int(t1 - t0);
+  const int m0 = blockIdx.x * G::BM, n0 = blockIdx.z * BN;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kTmaWM);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (w == kTmaWM) {  // producer: one thread issues both boxes of a K-tile
+    if (lane == 0) {
+      for (int kt = 0; kt < nk; ++kt) {
+        const int s = kt % S;
+        if (kt >= S) mbar_wait(&empty[s], uint32_t(((kt / S) - 1) & 1));
+        const i64 tt = t0 + kt, a = tt / nbt, b0 = (tt - a * nbt) * 16;
+        mbar_arrive_tx(&full[s], G::STAGE);
+        unsigned char* st = smem + s * G::STAGE;
+        tma_load_3d(st, &mx, int(b0), m0, int(a), &full[s]);
+        tma_load_3d(st + G::ABYTES, &mp, int(b0), n0, int(a), &full[s]);
+      }
+    }
+    return;
+  }
+  const int g = lane >> 2, t = lane & 3, r0 = w * 16 + g;
+  double acc[NT][4];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+  for (int kt = 0; kt < nk; ++kt) {
+    const int s = kt % S;
+    mbar_wait(&full[s], uint32_t((kt / S) & 1));
+    const double* A = reinterpret_cast<const double*>(smem + s * G::STAGE);
+    const double* B = reinterpret_cast<const double*>(smem + s * G::STAGE + G::ABYTES);
+#pragma unroll
+    for (int kk = 0; kk < 16; kk += 4) {
+      const double a0 = A[swz16(r0, kk + t)];
+      const double a1 = A[swz16(r0 + 8, kk + t)];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) dmma(acc[j], a0, a1, B[swz16(j * 8 + g, kk + t)]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  // partial[split][c][i]
+  const i64 ri = m0 + r0;
+  double* out = part + i64(blockIdx.y) * cols * I;
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    const i64 c0 = n0 + j * 8 + 2 * t;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const i64 i = ri + (q >> 1) * 8, c = c0 + (q & 1);
+      if (i < I && c < cols) out[c * I + i] = acc[j][q];
+    }
+  }
+}
+
+template <int BN>
+int tma_ctas_per_sm() {
+  static const int per = [] {
+    const size_t lim = enable_max_dyn_smem(sketch_dmma_tma_kernel<BN>);
+    if (size_t(TmaPlan<BN>::SMEM) > lim) return 0;
+    int n = 0;
+    RCPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sketch_dmma_tma_kernel<BN>, TmaPlan<BN>::THREADS,
+                                                            TmaPlan<BN>::SMEM));
+    return n;
+  }();
+  return per;
+}
+
 int pick_bn8(i64 cols) {
   if (cols <= 16) return 16;
   if (cols <= 32) return 32;
@@ -254,16 +368,41 @@ void launch_project(dim3 grid, const double* X, const double* Q, ModeView v, i64
 
 }  // namespace
 
+namespace {
+bool tma_sketch_shape_ok(ModeView v, i64 cols) {
+  constexpr i64 kMax = (i64(1) << 31) - 1;
+  return v.R % 2 == 0 && v.R <= kMax && v.I <= kMax && v.L <= kMax && cols <= kMax &&
+         std::getenv("RCPG_DMMA_CPASYNC") == nullptr;
+}
+
+int tma_per_sm(int bn) {
+  switch (bn) {
+    case 16: return tma_ctas_per_sm<16>();
+    case 32: return tma_ctas_per_sm<32>();
+    case 48: return tma_ctas_per_sm<48>();
+    case 64: return tma_ctas_per_sm<64>();
+    default: return tma_ctas_per_sm<80>();
+  }
+}
+}  // namespace
+
 i64 sketch_dmma_splits(ModeView v, i64 cols, int num_sms, i64& tps, i64& total) {
-  const i64 mt = ceil_div(v.I, kDBM), nt = ceil_div(cols, pick_bn8(cols));
-  total = v.L * ceil_div(v.R, kDBK);
-  // whole waves of resident CTAs: a grid a few CTAs over a wave boundary
-  // leaves most SMs idle for the last wave (residency from the smem plan,
-  // capped by registers: ~80 per thread x 128 threads)
   const int bn = pick_bn8(cols);
-  const int S = bn <= 32 ? 4 : (bn <= 48 ? 3 : 2);
-  const i64 smem = i64(S) * (kDBM + bn) * (kDBK + 4) * 8 + 1024;
-  const i64 per_sm = std::max<i64>(1, std::min<i64>(6, (227 * 1024) / smem));
+  total = v.L * ceil_div(v.R, kDBK);
+  i64 mt, per_sm;
+  if (tma_sketch_shape_ok(v, cols) && tma_per_sm(bn) > 0) {
+    mt = ceil_div(v.I, i64(kTmaWM * 16));
+    per_sm = tma_per_sm(bn);
+  } else {
+    // residency from the smem plan, capped by registers: ~80 per thread x 128 threads
+    mt = ceil_div(v.I, kDBM);
+    const int S = bn <= 32 ? 4 : (bn <= 48 ? 3 : 2);
+    const i64 smem = i64(S) * (kDBM + bn) * (kDBK + 4) * 8 + 1024;
+    per_sm = std::max<i64>(1, std::min<i64>(6, (227 * 1024) / smem));
+  }
+  const i64 nt = ceil_div(cols, i64(bn));
+  // whole waves of resident CTAs: a grid a few CTAs over a wave boundary
+  // leaves most SMs idle for the last wave
   const i64 slots = per_sm * i64(num_sms), waves = 2;
   i64 want = std::max<i64>(1, (waves * slots) / (mt * nt));
   want = std::max<i64>(1, std::min<i64>(want, 65535));
@@ -271,12 +410,39 @@ i64 sketch_dmma_splits(ModeView v, i64 cols, int num_sms, i64& tps, i64& total) 
   return ceil_div(total, tps);
 }
 
+namespace {
+template <int BN>
+void launch_sketch_tma(const double* X, ModeView v, const double* P, i64 cols, i64 tps, i64 total, i64 splits,
+                       double* part, const int* skip, cudaStream_t st) {
+  alignas(64) unsigned char mx[128], mp[128];
+  tensor_map_f64_3d(mx, X, v.R, v.I, v.L, kTmaWM * 16);
+  tensor_map_f64_3d(mp, P, v.R, cols, v.L, BN);
+  dim3 grid{unsigned(ceil_div(v.I, i64(kTmaWM * 16))), unsigned(splits), unsigned(ceil_div(cols, i64(BN)))};
+  sketch_dmma_tma_kernel<BN><<<grid, TmaPlan<BN>::THREADS, TmaPlan<BN>::SMEM, st>>>(
+      *reinterpret_cast<const CUtensorMap*>(mx), *reinterpret_cast<const CUtensorMap*>(mp), v.I, cols,
+      ceil_div(v.R, kDBK), tps, total, part, skip);
+  count_launch();
+  RCPG_LAUNCHED();
+}
+}  // namespace
+
 void sketch_dmma(const double* X, ModeView v, const double* P, i64 cols, double* part, int num_sms, const int* skip,
                  cudaStream_t st) {
   i64 tps, total;
   const i64 splits = sketch_dmma_splits(v, cols, num_sms, tps, total);
   const int BN = pick_bn8(cols);
   const i64 nbt = ceil_div(v.R, kDBK);
+  const bool aligned = reinterpret_cast<uintptr_t>(X) % 16 == 0 && reinterpret_cast<uintptr_t>(P) % 16 == 0;
+  if (tma_sketch_shape_ok(v, cols) && aligned && tma_per_sm(BN) > 0) {
+    switch (BN) {
+      case 16: launch_sketch_tma<16>(X, v, P, cols, tps, total, splits, part, skip, st); break;
+      case 32: launch_sketch_tma<32>(X, v, P, cols, tps, total, splits, part, skip, st); break;
+      case 48: launch_sketch_tma<48>(X, v, P, cols, tps, total, splits, part, skip, st); break;
+      case 64: launch_sketch_tma<64>(X, v, P, cols, tps, total, splits, part, skip, st); break;
+      default: launch_sketch_tma<80>(X, v, P, cols, tps, total, splits, part, skip, st); break;
+    }
+    return;
+  }
   dim3 grid{unsigned(ceil_div(v.I, kDBM)), unsigned(splits), unsigned(ceil_div(cols, BN))};
   const bool v16 = (v.R % 2 == 0);
 #define RCPG_SK(BNV)                                                                              \

@@ -624,6 +624,21 @@ __global__ void residual_ct_kernel(const float* C, i64 E, int R, int KP, float* 
 
 }  // namespace
 
+// fp64 3-D tiled map over a (d0 fastest, d1, d2) row-major view, box {16, b1, 1}
+// (128 B rows), SWIZZLE_128B, zero fill out of range: the DMMA sketch operands.
+void tensor_map_f64_3d(void* out, const double* base, i64 d0, i64 d1, i64 d2, int b1) {
+  static_assert(sizeof(CUtensorMap) == 128, "tensor map size");
+  const cuuint64_t dims[3] = {cuuint64_t(d0), cuuint64_t(d1), cuuint64_t(d2)};
+  const cuuint64_t strides[2] = {cuuint64_t(d0) * 8, cuuint64_t(d0 * d1) * 8};
+  const cuuint32_t box[3] = {16, cuuint32_t(b1), 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = encode_tiled()(static_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+                                    const_cast<double*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaFailure("cuTensorMapEncodeTiled (f64) failed (" + std::to_string(int(r)) + ")", cudaErrorInvalidValue);
+}
+
 bool tc_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("RCPG_NO_TC");
