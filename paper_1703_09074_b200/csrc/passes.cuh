@@ -279,7 +279,7 @@ template <typename T>
 void project(const T* X, ModeView v, const T* Q, i64 ldq, i64 cols, T* O, cudaStream_t st);
 
 // 128-byte CUtensorMap (opaque here) for an fp64 (d0, d1, d2) view, box {16, b1, 1}, 128B swizzle.
-void tensor_map_f64_3d(void* out, const double* base, i64 d0, i64 d1, i64 d2, int b1);
+void tensor_map_f64_3d(void* out, const double* base, i64 d0, i64 d1, i64 d2, int b1, i64 pitch = 0);
 // FP64 tensor-core (DMMA) versions for mode views with R > 1 (passes_dmma.cu).
 i64 sketch_dmma_splits(ModeView v, i64 cols, int num_sms, i64& tps, i64& total);
 void sketch_dmma(const double* X, ModeView v, const double* P, i64 cols, double* part, int num_sms,

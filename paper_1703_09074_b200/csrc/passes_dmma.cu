@@ -321,6 +321,79 @@ __global__ void __launch_bounds__(TmaPlan<BN>::THREADS) sketch_dmma_tma_kernel(c
   }
 }
 
+// ---------------------------------------------------- project, TMA-fed
+// O[a, c, b] = sum_i X[a, i, b] Q[i, c]: M = b (four 16-wide boxes of X per
+// stage, one per consumer warp), N = c, K = i (16 per stage), no split.
+template <int BN>
+__global__ void __launch_bounds__(TmaPlan<BN>::THREADS) project_dmma_tma_kernel(const __grid_constant__ CUtensorMap mx,
+                                                                                const __grid_constant__ CUtensorMap mq,
+                                                                                i64 I, i64 R, i64 cols, int a_base,
+                                                                                double* __restrict__ O) {
+  using G = TmaPlan<BN>;
+  using namespace tc;
+  constexpr int NT = BN / 8, S = kTmaStages;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[S], empty[S];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int nk = int(ceil_div(I, i64(16)));
+  const int b0 = blockIdx.x * G::BM, n0 = blockIdx.z * BN;
+  const int a = a_base + int(blockIdx.y);
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kTmaWM);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (w == kTmaWM) {
+    if (lane == 0) {
+      for (int kt = 0; kt < nk; ++kt) {
+        const int s = kt % S;
+        if (kt >= S) mbar_wait(&empty[s], uint32_t(((kt / S) - 1) & 1));
+        mbar_arrive_tx(&full[s], G::STAGE);
+        unsigned char* st = smem + s * G::STAGE;
+#pragma unroll
+        for (int q = 0; q < kTmaWM; ++q) tma_load_3d(st + q * 2048, &mx, b0 + 16 * q, kt * 16, a, &full[s]);
+        tma_load_3d(st + G::ABYTES, &mq, kt * 16, n0, 0, &full[s]);
+      }
+    }
+    return;
+  }
+  const int g = lane >> 2, t = lane & 3;
+  double acc[NT][4];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+  for (int kt = 0; kt < nk; ++kt) {
+    const int s = kt % S;
+    mbar_wait(&full[s], uint32_t((kt / S) & 1));
+    const double* A = reinterpret_cast<const double*>(smem + s * G::STAGE) + w * 256;  // box of this warp's b's
+    const double* B = reinterpret_cast<const double*>(smem + s * G::STAGE + G::ABYTES);
+#pragma unroll
+    for (int kk = 0; kk < 16; kk += 4) {
+      const double a0 = A[swz16(kk + t, g)];
+      const double a1 = A[swz16(kk + t, g + 8)];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) dmma(acc[j], a0, a1, B[swz16(j * 8 + g, kk + t)]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  const i64 bb = b0 + w * 16 + g;
+  double* Oa = O + i64(blockIdx.y) * cols * R;
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    const i64 c0 = n0 + j * 8 + 2 * t;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const i64 b = bb + (q >> 1) * 8, c = c0 + (q & 1);
+      if (b < R && c < cols) Oa[c * R + b] = acc[j][q];
+    }
+  }
+}
+
 template <int BN>
 int tma_ctas_per_sm() {
   static const int per = [] {
@@ -463,8 +536,40 @@ void sketch_dmma(const double* X, ModeView v, const double* P, i64 cols, double*
 #undef RCPG_SK
 }
 
+namespace {
+template <int BN>
+void launch_project_tma(const double* X, ModeView v, const double* Q, i64 ldq, i64 cols, double* O,
+                        cudaStream_t st) {
+  static const size_t lim = enable_max_dyn_smem(project_dmma_tma_kernel<BN>);
+  if (size_t(TmaPlan<BN>::SMEM) > lim) throw std::runtime_error("project_dmma_tma: smem plan too large");
+  alignas(64) unsigned char mx[128], mq[128];
+  tensor_map_f64_3d(mx, X, v.R, v.I, v.L, 16);
+  tensor_map_f64_3d(mq, Q, v.I, cols, 1, BN, ldq);  // Q column-major: i fastest (pitch ldq), c; rows >= I read as 0
+  for (i64 a0 = 0; a0 < v.L; a0 += 65535) {
+    const i64 na = std::min<i64>(65535, v.L - a0);
+    dim3 grid{unsigned(ceil_div(v.R, i64(kTmaWM * 16))), unsigned(na), unsigned(ceil_div(cols, i64(BN)))};
+    project_dmma_tma_kernel<BN><<<grid, TmaPlan<BN>::THREADS, TmaPlan<BN>::SMEM, st>>>(
+        *reinterpret_cast<const CUtensorMap*>(mx), *reinterpret_cast<const CUtensorMap*>(mq), v.I, v.R, cols,
+        int(a0), O + a0 * cols * v.R);
+    count_launch();
+    RCPG_LAUNCHED();
+  }
+}
+}  // namespace
+
 void project_dmma(const double* X, ModeView v, const double* Q, i64 ldq, i64 cols, double* O, cudaStream_t st) {
   const int BN = pick_bn8(cols);
+  const bool aligned = reinterpret_cast<uintptr_t>(X) % 16 == 0 && reinterpret_cast<uintptr_t>(Q) % 16 == 0;
+  if (tma_sketch_shape_ok(v, cols) && ldq % 2 == 0 && ldq >= v.I && aligned) {
+    switch (BN) {
+      case 16: launch_project_tma<16>(X, v, Q, ldq, cols, O, st); break;
+      case 32: launch_project_tma<32>(X, v, Q, ldq, cols, O, st); break;
+      case 48: launch_project_tma<48>(X, v, Q, ldq, cols, O, st); break;
+      case 64: launch_project_tma<64>(X, v, Q, ldq, cols, O, st); break;
+      default: launch_project_tma<80>(X, v, Q, ldq, cols, O, st); break;
+    }
+    return;
+  }
   const bool va = (v.R % 2 == 0), vb = (ldq % 2 == 0);
   for (i64 a0 = 0; a0 < v.L; a0 += 65535) {
     const i64 na = std::min<i64>(65535, v.L - a0);

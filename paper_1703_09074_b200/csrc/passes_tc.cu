@@ -624,12 +624,13 @@ __global__ void residual_ct_kernel(const float* C, i64 E, int R, int KP, float* 
 
 }  // namespace
 
-// fp64 3-D tiled map over a (d0 fastest, d1, d2) row-major view, box {16, b1, 1}
+// fp64 3-D tiled map over a (d0 fastest, d1, d2) view with row pitch `pitch` (0: d0), box {16, b1, 1}
 // (128 B rows), SWIZZLE_128B, zero fill out of range: the DMMA sketch operands.
-void tensor_map_f64_3d(void* out, const double* base, i64 d0, i64 d1, i64 d2, int b1) {
+void tensor_map_f64_3d(void* out, const double* base, i64 d0, i64 d1, i64 d2, int b1, i64 pitch) {
+  if (pitch <= 0) pitch = d0;
   static_assert(sizeof(CUtensorMap) == 128, "tensor map size");
   const cuuint64_t dims[3] = {cuuint64_t(d0), cuuint64_t(d1), cuuint64_t(d2)};
-  const cuuint64_t strides[2] = {cuuint64_t(d0) * 8, cuuint64_t(d0 * d1) * 8};
+  const cuuint64_t strides[2] = {cuuint64_t(pitch) * 8, cuuint64_t(pitch * d1) * 8};
   const cuuint32_t box[3] = {16, cuuint32_t(b1), 1};
   const cuuint32_t es[3] = {1, 1, 1};
   const CUresult r = encode_tiled()(static_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
