@@ -316,6 +316,86 @@ __device__ unsigned long long* g_als_prof = nullptr;
     }                                                                                \
   } while (0)
 
+// Gauss-Jordan inverse of an R x R matrix in place (A column-major, smem),
+// with the entries in registers: thread (warp w, lane l) holds (i, j),
+// i = w + k * warps, j = l + 32 m. Step k needs row k (published by its
+// owner into a double-buffered shared row after its update in step k - 1)
+// and the own row's column-k entry (a shuffle from lane k % 32): one barrier
+// per pivot. Same arithmetic, in the same order, as the shared-memory
+// ping-pong version (bitwise identical). *ok = 0 if a pivot is not > 0.
+template <int KR, int KC>
+__device__ void gj_inverse_regs(double* A, int R, int* ok) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  __shared__ double rowbuf[2][32 * KC];
+  double v[KR][KC];
+#pragma unroll
+  for (int q = 0; q < KR; ++q)
+#pragma unroll
+    for (int m = 0; m < KC; ++m) {
+      const int i = wid + q * nw, j = lane + 32 * m;
+      v[q][m] = (i < R && j < R) ? A[i + j * R] : 0.0;
+    }
+  if (wid == 0)
+#pragma unroll
+    for (int m = 0; m < KC; ++m) rowbuf[0][lane + 32 * m] = v[0][m];
+  __syncthreads();
+  int bad = 0;
+  int nxw = 1 % nw, nxq = 1 / nw;  // owner (warp, slot) of row k + 1
+  for (int k = 0; k < R; ++k) {
+    const double* rk = rowbuf[k & 1];
+    const double p = rk[k];
+    double rkj[KC];
+#pragma unroll
+    for (int m = 0; m < KC; ++m) rkj[m] = rk[lane + 32 * m];
+    const int mk = k >> 5, lk = k & 31;
+    double aik[KR];
+#pragma unroll
+    for (int q = 0; q < KR; ++q) {
+      double x = 0.0;
+#pragma unroll
+      for (int m = 0; m < KC; ++m)
+        if (m == mk) x = v[q][m];
+      aik[q] = __shfl_sync(0xffffffffu, x, lk);
+    }
+    bad |= !(p > 0.0);
+    const double ip = 1.0 / p;
+#pragma unroll
+    for (int m = 0; m < KC; ++m) {
+      const int j = lane + 32 * m;
+      const double akj = rkj[m] * ip;
+#pragma unroll
+      for (int q = 0; q < KR; ++q) {
+        const int i = wid + q * nw;
+        if (j != k)
+          v[q][m] = (i != k) ? v[q][m] - aik[q] * akj : akj;
+        else
+          v[q][m] = (i != k) ? -aik[q] * ip : ip;
+      }
+    }
+    if (k + 1 < R && wid == nxw) {
+#pragma unroll
+      for (int q = 0; q < KR; ++q)
+        if (q == nxq)
+#pragma unroll
+          for (int m = 0; m < KC; ++m) rowbuf[(k + 1) & 1][lane + 32 * m] = v[q][m];
+    }
+    if (++nxw == nw) {
+      nxw = 0;
+      ++nxq;
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < KR; ++q)
+#pragma unroll
+    for (int m = 0; m < KC; ++m) {
+      const int i = wid + q * nw, j = lane + 32 * m;
+      if (i < R && j < R) A[i + j * R] = v[q][m];
+    }
+  if (tid == 0 && bad) *ok = 0;
+  __syncthreads();
+}
+
 template <typename T, typename WT>
 __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T* weights, double tol,
                                 int max_iter, double* trace_fit, double* trace_sec, AlsState* st, double* work) {
@@ -345,12 +425,17 @@ __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T
   }
   if (tid == 0) s_ok = 1;
   __syncthreads();
-  // 2. Gauss-Jordan inverse of the SPD matrix: ping-pong between A and X,
-  //    one barrier per pivot
+  // 2. Gauss-Jordan inverse of the SPD matrix, one barrier per pivot
   const int R2 = R * R;
+  const int lane0 = tid & 31, wid0 = tid >> 5, nw0 = nt >> 5;
+  if (R <= 32 && R <= 4 * nw0) {
+    gj_inverse_regs<4, 1>(A, R, &s_ok);
+  } else if (R <= 64 && R <= 8 * nw0) {
+    gj_inverse_regs<8, 2>(A, R, &s_ok);
+  } else {
+  // ping-pong between A and X
   double* src = A;
   double* dst = X;
-  const int lane0 = tid & 31, wid0 = tid >> 5, nw0 = nt >> 5;
   for (int k = 0; k < R; ++k) {
     // restrict-qualified with the pivot column hoisted: without it every
     // store may alias the next column's loads and the step serializes
@@ -384,6 +469,7 @@ __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T
   if (src != A) {
     for (int e = tid; e < R2; e += nt) A[e] = src[e];
     __syncthreads();
+  }
   }
   ALS_STAMP(8);
   double fro = 0.0, ifro = 0.0;

@@ -8,6 +8,8 @@
 // Every numeric step runs on the device (passes.cu, factor.cu, als.cu); the
 // host only sequences launches, validates arguments in the reference's
 // order, and reads back a few scalars (norm checks, the ALS stop flag).
+#include <mutex>
+#include <unordered_set>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1132,6 +1134,17 @@ extern "C" {
 
 const char* rcpg_version(void) { return "rcpg 0.1 (sm_100a)"; }
 
+namespace {
+std::mutex& live_mu() {
+  static std::mutex m;
+  return m;
+}
+std::unordered_set<const rcpg_context*>& live_contexts() {
+  static std::unordered_set<const rcpg_context*> s;
+  return s;
+}
+}  // namespace
+
 rcpg_status rcpg_create(int device, rcpg_context** out) {
   if (!out) return RCPG_INVALID_ARGUMENT;
   *out = nullptr;
@@ -1143,18 +1156,32 @@ rcpg_status rcpg_create(int device, rcpg_context** out) {
     if (device < 0 || device >= n) throw CudaFailure("rcpg_create: no such CUDA device", cudaErrorInvalidDevice);
     RCPG_CUDA(cudaSetDevice(device));
     RCPG_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    // uploaded tensors come from the device's default pool; keep freed blocks
+    // in the pool so per-call uploads reuse them
+    cudaMemPool_t pool;
+    RCPG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = ~uint64_t(0);
+    RCPG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     c->bar.ensure(sizeof(GridBarrier));
     RCPG_CUDA(cudaMemset(c->bar.p, 0, sizeof(GridBarrier)));
     c->nrm.ensure(kSlotCount * sizeof(double));
     RCPG_CUDA(cudaMallocHost(&c->hslots, kSlotCount * sizeof(double)));
     (void)device_caps();
   });
-  if (s == RCPG_OK) *out = c.release();
+  if (s == RCPG_OK) {
+    std::lock_guard<std::mutex> lk(live_mu());
+    live_contexts().insert(c.get());
+    *out = c.release();
+  }
   return s;
 }
 
 void rcpg_destroy(rcpg_context* c) {
   if (!c) return;
+  {
+    std::lock_guard<std::mutex> lk(live_mu());
+    live_contexts().erase(c);
+  }
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->st);
   for (auto& e : c->user_events)
@@ -1194,10 +1221,13 @@ rcpg_status rcpg_tensor_upload(rcpg_context* c, rcpg_dtype dtype, int32_t order,
       t->size *= shape[m];
     }
     const size_t bytes = size_t(t->size) * dsize(dtype);
-    cudaError_t e = cudaMalloc(&t->d, bytes);
+    // stream-ordered from the device pool, which keeps freed memory (release
+    // threshold set in rcpg_create): repeated uploads of the same size cost no
+    // cudaMalloc / cudaFree (those synchronize the device and map pages)
+    cudaError_t e = cudaMallocAsync(&t->d, bytes, c->st);
     if (e != cudaSuccess) {
       (void)cudaGetLastError();
-      throw CudaFailure("rcpg_tensor_upload: cudaMalloc failed", e);
+      throw CudaFailure("rcpg_tensor_upload: cudaMallocAsync failed", e);
     }
     t->owned = true;
     RCPG_CUDA(cudaMemcpyAsync(t->d, host, bytes, cudaMemcpyHostToDevice, c->st));
@@ -1236,7 +1266,16 @@ void* rcpg_tensor_device_ptr(const rcpg_tensor* t) { return t ? t->d : nullptr; 
 
 void rcpg_tensor_free(rcpg_tensor* t) {
   if (!t) return;
-  if (t->owned && t->d) cudaFree(t->d);
+  if (t->owned && t->d) {
+    // stream-ordered free on the owning context's stream while it is alive;
+    // a tensor that outlived its context (e.g. garbage-collected late) is
+    // freed with the synchronizing cudaFree, which accepts pool memory too
+    std::lock_guard<std::mutex> lk(live_mu());
+    if (live_contexts().count(t->ctx))
+      cudaFreeAsync(t->d, t->ctx->st);
+    else
+      cudaFree(t->d);
+  }
   delete t;
 }
 
@@ -1371,10 +1410,10 @@ rcpg_status rcpg_tensor_slab(rcpg_context* c, const rcpg_tensor* full, int64_t l
     t->slab_hi = hi;
     t->global_last = E;
     const size_t bytes = size_t(std::max<i64>(t->size, 1)) * dsize(t->dtype);
-    cudaError_t e = cudaMalloc(&t->d, bytes);
+    cudaError_t e = cudaMallocAsync(&t->d, bytes, c->st);  // device pool (see rcpg_tensor_upload)
     if (e != cudaSuccess) {
       (void)cudaGetLastError();
-      throw CudaFailure("rcpg_tensor_slab: cudaMalloc failed", e);
+      throw CudaFailure("rcpg_tensor_slab: cudaMallocAsync failed", e);
     }
     t->owned = true;
     const i64 prefix = t->size / std::max<i64>(hi - lo, 1);
@@ -1413,10 +1452,10 @@ rcpg_status rcpg_tensor_upload_slab(rcpg_context* c, rcpg_dtype dtype, int32_t o
     t->slab_hi = hi;
     t->global_last = E;
     const size_t bytes = size_t(std::max<i64>(t->size, 1)) * dsize(dtype);
-    cudaError_t e = cudaMalloc(&t->d, bytes);
+    cudaError_t e = cudaMallocAsync(&t->d, bytes, c->st);  // device pool (see rcpg_tensor_upload)
     if (e != cudaSuccess) {
       (void)cudaGetLastError();
-      throw CudaFailure("rcpg_tensor_upload_slab: cudaMalloc failed", e);
+      throw CudaFailure("rcpg_tensor_upload_slab: cudaMallocAsync failed", e);
     }
     t->owned = true;
     if (t->size > 0)
@@ -1632,7 +1671,7 @@ rcpg_status rcpg_synth(rcpg_context* c, rcpg_dtype dtype, int32_t order, const i
     t->order = order;
     t->size = total;
     for (int m = 0; m < order; ++m) t->shape[m] = shape[m];
-    cudaError_t e = cudaMalloc(&t->d, size_t(total) * dsize(dtype));
+    cudaError_t e = cudaMallocAsync(&t->d, size_t(total) * dsize(dtype), c->st);  // device pool
     if (e != cudaSuccess) {
       (void)cudaGetLastError();
       throw CudaFailure("rcpg_synth: cudaMalloc failed", e);

@@ -4,3 +4,4 @@ python tools/bench_factor.py > gpurun_out/bf.txt 2>&1
 RCPG_PROFILE_QR=1 python tools/one_factor.py 1 400 30 > gpurun_out/qr_prof.txt 2>&1
 RCPG_PROFILE_QR=1 python tools/one_factor.py 1 1024 70 0 >> gpurun_out/qr_prof.txt 2>&1
 timeout 300 python bench.py --no-cpu-baseline > gpurun_out/bench_C2.json 2> gpurun_out/bench_C2.err
+RCPG_PROFILE_ALS=1 python tools/profile_step.py --config C2 > gpurun_out/als_prof.txt 2>&1
