@@ -8,11 +8,15 @@
 // (rows, cols, operator(), data, size).
 #pragma once
 
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <limits>
+#include <numeric>
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -291,6 +295,143 @@ S relative_error(const Tensor<S>& x, const Kruskal<S>& k) {
   return S(out);
 }
 
+inline const char* method_name(SolveMethod m) { return m == SolveMethod::bcd ? "bcd" : "als"; }
+
+// kruskal.hpp:117-176 (host side; models are small): unit-norm columns (left
+// alone within 32 eps of 1), zero columns -> e1 with weight 0, non-negative
+// weights, the largest-magnitude entry of each first-factor column
+// non-negative (compensated in factor 1), stable sort by weight descending,
+// ties by the lexicographically smaller first-factor column. Norms are
+// accumulated in double (the documented deviation for float).
+template <typename S>
+Kruskal<S> normalize(Kruskal<S> k) {
+  const Index r = k.rank(), n = k.order();
+  if (r < 1 || n < 1) throw std::invalid_argument("normalize: model needs rank >= 1 and order >= 1");
+  for (const auto& f : k.factors)
+    if (f.cols() != r || f.rows() < 1) throw std::invalid_argument("normalize: factor shape does not match the rank");
+  const S window = S(32) * std::numeric_limits<S>::epsilon();
+  for (Index j = 0; j < r; ++j) {
+    auto& w = k.weights[std::size_t(j)];
+    for (Index m = 0; m < n; ++m) {
+      auto& f = k.factors[std::size_t(m)];
+      double ss = 0.0;
+      for (Index i = 0; i < f.rows(); ++i) ss += double(f(i, j)) * double(f(i, j));
+      const S nrm = S(std::sqrt(ss));
+      if (nrm == S(0)) {
+        for (Index i = 0; i < f.rows(); ++i) f(i, j) = S(0);
+        f(0, j) = S(1);
+        w = S(0);
+      } else if (std::abs(nrm - S(1)) > window) {
+        for (Index i = 0; i < f.rows(); ++i) f(i, j) /= nrm;
+        w *= nrm;
+      }
+    }
+    if (w < S(0)) {
+      w = -w;
+      for (Index i = 0; i < k.factors[0].rows(); ++i) k.factors[0](i, j) = -k.factors[0](i, j);
+    }
+    if (n >= 2) {
+      auto& lead = k.factors[0];
+      Index at = 0;
+      for (Index i = 1; i < lead.rows(); ++i)
+        if (std::abs(lead(i, j)) > std::abs(lead(at, j))) at = i;
+      if (lead(at, j) < S(0)) {
+        for (Index i = 0; i < lead.rows(); ++i) lead(i, j) = -lead(i, j);
+        for (Index i = 0; i < k.factors[1].rows(); ++i) k.factors[1](i, j) = -k.factors[1](i, j);
+      }
+    }
+  }
+  std::vector<Index> ord(static_cast<std::size_t>(r));
+  std::iota(ord.begin(), ord.end(), Index(0));
+  const auto& lead = k.factors[0];
+  std::stable_sort(ord.begin(), ord.end(), [&](Index a, Index b) {
+    if (k.weights[std::size_t(a)] != k.weights[std::size_t(b)]) return k.weights[std::size_t(a)] > k.weights[std::size_t(b)];
+    for (Index i = 0; i < lead.rows(); ++i)
+      if (lead(i, a) != lead(i, b)) return lead(i, a) < lead(i, b);
+    return false;
+  });
+  bool ident = true;
+  for (Index j = 0; j < r; ++j) ident = ident && ord[std::size_t(j)] == j;
+  if (ident) return k;
+  Kruskal<S> out = k;
+  for (Index j = 0; j < r; ++j) {
+    const Index src = ord[std::size_t(j)];
+    out.weights[std::size_t(j)] = k.weights[std::size_t(src)];
+    for (Index m = 0; m < n; ++m)
+      for (Index i = 0; i < k.factors[std::size_t(m)].rows(); ++i)
+        out.factors[std::size_t(m)](i, j) = k.factors[std::size_t(m)](i, src);
+  }
+  return out;
+}
+
+namespace detail {
+// Dense model (plus optional add_noise at amplitude SNR `snr` from stream
+// (noise_seed, noise)) generated on the device by rcpg_synth, downloaded.
+template <typename S>
+Tensor<S> synth_dense(const Kruskal<S>& k, double snr, std::uint64_t noise_seed) {
+  rcpg_context* c = context();
+  Shape shape;
+  std::vector<double> w(k.weights.begin(), k.weights.end()), f;
+  for (const auto& m : k.factors) {
+    shape.push_back(m.rows());
+    f.insert(f.end(), m.data(), m.data() + m.size());
+  }
+  rcpg_tensor* t = nullptr;
+  check(c, rcpg_synth(c, dtype<S>(), int32_t(shape.size()), shape.data(), k.rank(), w.data(), f.data(), snr,
+                      noise_seed, &t));
+  Index n = 1;
+  for (Index e : shape) n *= e;
+  std::vector<S> v(static_cast<std::size_t>(n));
+  const rcpg_status st = rcpg_tensor_download(c, t, v.data());
+  rcpg_tensor_free(t);
+  check(c, st);
+  return Tensor<S>(std::move(shape), std::move(v));
+}
+}  // namespace detail
+
+// kruskal.hpp:104-110: the dense tensor of the model (computed on the GPU).
+template <typename S>
+Tensor<S> reconstruct(const Kruskal<S>& k) {
+  if (k.rank() < 1 || k.order() < 1) throw std::invalid_argument("reconstruct: empty model");
+  return detail::synth_dense(k, 0.0, 0);
+}
+
+inline std::uint64_t mix64(std::uint64_t z);
+inline std::uint64_t derive_seed(std::uint64_t seed, std::uint64_t salt);
+
+// random.hpp:16-107: SplitMix64 stream with Box-Muller normals (pairs cached).
+class RandomStream {
+ public:
+  RandomStream(std::uint64_t seed, std::uint64_t id) : state_(derive_seed(seed, id)) {}
+  std::uint64_t bits() {
+    state_ += 0x9e3779b97f4a7c15ULL;
+    return mix64(state_);
+  }
+  double uniform01() { return double(bits() >> 11) * 0x1.0p-53; }
+  double normal() {
+    if (cached_ok_) {
+      cached_ok_ = false;
+      return cached_;
+    }
+    const double u1 = double((bits() >> 11) + 1) * 0x1.0p-53;  // (0, 1]
+    const double u2 = uniform01();
+    const double rr = std::sqrt(-2.0 * std::log(u1)), th = 2.0 * 3.14159265358979323846 * u2;
+    cached_ = rr * std::sin(th);
+    cached_ok_ = true;
+    return rr * std::cos(th);
+  }
+  template <typename S>
+  void fill_gaussian(Matrix<S>& m) {  // column-major order
+    for (Index j = 0; j < m.cols(); ++j)
+      for (Index i = 0; i < m.rows(); ++i) m(i, j) = S(normal());
+  }
+
+ private:
+  std::uint64_t state_;
+  double cached_ = 0.0;
+  bool cached_ok_ = false;
+};
+
 inline std::uint64_t mix64(std::uint64_t z) {
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
   z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
@@ -301,6 +442,28 @@ enum class StreamDomain : std::uint64_t { compress = 1, init = 2, factors = 3, n
 inline std::uint64_t stream_id(StreamDomain d, std::uint64_t k = 0) { return (std::uint64_t(d) << 32) | k; }
 inline std::uint64_t derive_seed(std::uint64_t seed, std::uint64_t salt) {
   return mix64(seed + 0x9e3779b97f4a7c15ULL * (salt + 1));
+}
+
+// synthetic.hpp:21-38: N(0, 1) factors from stream (seed, factors, m), unit
+// weights, normalized, reconstructed (on the GPU). With snr > 0 the
+// add_noise step (synthetic.hpp:42-58, stream (noise_seed, noise)) is fused
+// into the same device pass (the CLI's `synth --snr`).
+template <typename S>
+std::pair<Tensor<S>, Kruskal<S>> random_lowrank(const Shape& shape, Index rank, std::uint64_t seed, double snr = 0.0,
+                                                std::uint64_t noise_seed = 0) {
+  if (rank < 1) throw std::invalid_argument("random_lowrank: rank must be at least 1");
+  if (shape.empty()) throw std::invalid_argument("random_lowrank: shape must not be empty");
+  Kruskal<S> truth;
+  truth.weights.assign(static_cast<std::size_t>(rank), S(1));
+  for (std::size_t m = 0; m < shape.size(); ++m) {
+    if (shape[m] < 1) throw std::invalid_argument("random_lowrank: extents must be positive");
+    RandomStream rs(seed, stream_id(StreamDomain::factors, m));
+    Matrix<S> f(shape[m], rank);
+    rs.fill_gaussian(f);
+    truth.factors.push_back(std::move(f));
+  }
+  truth = normalize(std::move(truth));
+  return {detail::synth_dense(truth, snr, noise_seed), truth};
 }
 
 }  // namespace rcp
