@@ -323,10 +323,13 @@ __device__ unsigned long long* g_als_prof = nullptr;
 // and the own row's column-k entry (a shuffle from lane k % 32): one barrier
 // per pivot. Same arithmetic, in the same order, as the shared-memory
 // ping-pong version (bitwise identical). *ok = 0 if a pivot is not > 0.
+// `scratch` (2 * 32 * KC doubles of dynamic shared memory) holds the row
+// buffers: static shared memory here would shrink the dynamic budget of the
+// ALS loop kernel that inlines this (and push it to a smaller MTTKRP batch).
 template <int KR, int KC>
-__device__ void gj_inverse_regs(double* A, int R, int* ok) {
+__device__ void gj_inverse_regs(double* A, int R, int* ok, double* scratch) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-  __shared__ double rowbuf[2][32 * KC];
+  double (*rowbuf)[32 * KC] = reinterpret_cast<double (*)[32 * KC]>(scratch);
   double v[KR][KC];
 #pragma unroll
   for (int q = 0; q < KR; ++q)
@@ -428,10 +431,11 @@ __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T
   // 2. Gauss-Jordan inverse of the SPD matrix, one barrier per pivot
   const int R2 = R * R;
   const int lane0 = tid & 31, wid0 = tid >> 5, nw0 = nt >> 5;
-  if (R <= 32 && R <= 4 * nw0) {
-    gj_inverse_regs<4, 1>(A, R, &s_ok);
-  } else if (R <= 64 && R <= 8 * nw0) {
-    gj_inverse_regs<8, 2>(A, R, &s_ok);
+  // X (R x R, used only by the eigen fallback afterwards) holds the row buffers
+  if (R <= 32 && R <= 4 * nw0 && R * R >= 64) {
+    gj_inverse_regs<4, 1>(A, R, &s_ok, X);
+  } else if (R <= 64 && R <= 8 * nw0 && R * R >= 128) {
+    gj_inverse_regs<8, 2>(A, R, &s_ok, X);
   } else {
   // ping-pong between A and X
   double* src = A;
