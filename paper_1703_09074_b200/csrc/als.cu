@@ -1064,15 +1064,44 @@ __global__ void small_gemm_kernel(const T* Q, i64 dim, i64 l, const T* A, int ra
 
 // ------------------------------------------------------------ reductions
 template <typename T>
-__global__ void norm_finite_kernel(const T* x, i64 n, double* part) {
+__global__ void __launch_bounds__(256) norm_finite_kernel(const T* __restrict__ x, i64 n, double* part) {
+  // 16-byte loads, four in flight per thread (a streaming reduction needs many
+  // bytes in flight per SM to reach HBM bandwidth); scalar head/tail
+  using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+  constexpr int W = 16 / int(sizeof(T));
   double s = 0.0, bad = 0.0;
-  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < n; e += i64(gridDim.x) * blockDim.x) {
-    const double v = double(x[e]);
+  auto acc = [&](T t) {
+    const double v = double(t);
     if (isfinite(v))
       s += v * v;
     else
       bad += 1.0;
+  };
+  const i64 head = i64((16 - (reinterpret_cast<uintptr_t>(x) & 15)) & 15) / i64(sizeof(T));
+  const i64 h = head < n ? head : n;
+  const i64 nv = (n - h) / W;
+  const V* xv = reinterpret_cast<const V*>(x + h);
+  const i64 tid = blockIdx.x * i64(blockDim.x) + threadIdx.x, nth = i64(gridDim.x) * blockDim.x;
+  if (tid < h) acc(x[tid]);
+  i64 e = tid;
+  for (; e + 3 * nth < nv; e += 4 * nth) {
+    V v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldcs(xv + e + u * nth);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const T* t = reinterpret_cast<const T*>(&v[u]);
+#pragma unroll
+      for (int w = 0; w < W; ++w) acc(t[w]);
+    }
   }
+  for (; e < nv; e += nth) {
+    const V v = __ldcs(xv + e);
+    const T* t = reinterpret_cast<const T*>(&v);
+#pragma unroll
+    for (int w = 0; w < W; ++w) acc(t[w]);
+  }
+  for (i64 r = h + nv * W + tid; r < n; r += nth) acc(x[r]);
   s = block_reduce_sum(s);
   bad = block_reduce_sum(bad);
   if (threadIdx.x == 0) {
