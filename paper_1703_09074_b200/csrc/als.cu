@@ -1377,7 +1377,8 @@ void init_factors_from_grams(const InitBatch<T>& b, int count, int rank, u64 see
     if (b.n[q] <= kEigSmemMax) smem = std::max(smem, 2 * size_t(b.n[q]) * size_t(b.n[q] | 1) * sizeof(double));
   static const size_t lim = enable_max_dyn_smem(init_from_gram_kernel<T>);
   (void)lim;
-  init_from_gram_kernel<T><<<count, 256, smem, st>>>(b, rank, seed, method);
+  // 1024 threads: a Jacobi round rotates up to 48 row/column pairs, one warp each
+  init_from_gram_kernel<T><<<count, kSmallThreads, smem, st>>>(b, rank, seed, method);
   count_launch();
   RCPG_LAUNCHED();
 }
