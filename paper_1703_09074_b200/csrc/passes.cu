@@ -113,9 +113,12 @@ i64 sketch_scratch_elems(ModeView v, i64 cols, int num_sms) {
     splits = sketch_dmma_splits(v, cols, num_sms, tps, total);
   else
     sketch_plan<T>(v, cols, num_sms, splits, tps, total);
-  if (std::is_same<T, float>::value && v.R > 1)
+  i64 extra = 0;
+  if (std::is_same<T, float>::value && v.R > 1) {
     splits = std::max(splits, sketch_tc_splits(v, cols, num_sms, tps, total));
-  return splits * cols * v.I;
+    extra = sketch_tc_panel_floats(v, cols);
+  }
+  return ceil_div(splits * cols * v.I, 4) * 4 + extra;
 }
 
 template <typename T>
@@ -127,7 +130,13 @@ void sketch(const T* X, ModeView v, const T* P, i64 cols, T* Y, T* scratch, i64 
   if (tc) {
     splits = sketch_tc_splits(v, cols, num_sms, tps, total);
     if (splits * cols * v.I > scratch_elems) throw std::runtime_error("sketch: scratch too small");
-    if constexpr (std::is_same<T, float>::value) sketch_tc(X, v, P, cols, scratch, num_sms, skip, st);
+    if constexpr (std::is_same<T, float>::value) {
+      const i64 pf = sketch_tc_panel_floats(v, cols);
+      // the blocked panel copy lives behind the partials (16-byte aligned) when the caller's scratch has room
+      const i64 off = ceil_div(splits * cols * v.I, 4) * 4;
+      float* pblk = (pf > 0 && off + pf <= scratch_elems) ? scratch + off : nullptr;
+      sketch_tc(X, v, P, cols, scratch, pblk, num_sms, skip, st);
+    }
   } else if (use_dmma<T>(v)) {
     splits = sketch_dmma_splits(v, cols, num_sms, tps, total);
     if (splits * cols * v.I > scratch_elems) throw std::runtime_error("sketch: scratch too small");

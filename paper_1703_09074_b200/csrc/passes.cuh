@@ -293,8 +293,12 @@ bool tc_enabled();
 bool tc_sketch_ok(const float* X, const float* P, ModeView v);
 bool tc_project_ok(const float* X, const float* Q, ModeView v, i64 ldq);
 i64 sketch_tc_splits(ModeView v, i64 cols, int num_sms, i64& tps, i64& total);
-void sketch_tc(const float* X, ModeView v, const float* P, i64 cols, float* part, int num_sms, const int* skip,
-               cudaStream_t st);
+// pblk: sketch_tc_panel_floats() of scratch for the K-tile-blocked panel copy
+// (nullptr: read the (a, c, b) panel directly). RCPG_TC_PBLK=0|1|2 selects
+// direct / blocked raw / blocked hi+lo planes (A/B hook; default 1).
+i64 sketch_tc_panel_floats(ModeView v, i64 cols);
+void sketch_tc(const float* X, ModeView v, const float* P, i64 cols, float* part, float* pblk, int num_sms,
+               const int* skip, cudaStream_t st);
 void project_tc(const float* X, ModeView v, const float* Q, i64 ldq, i64 cols, float* O, int num_sms,
                 cudaStream_t st);
 // ||X - Xhat||^2, ||X||^2 partials per CTA (part[2 * blocks]) with Xhat on tcgen05;

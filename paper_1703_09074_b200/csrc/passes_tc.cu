@@ -93,6 +93,8 @@ struct TcArgs {
   i64 nbt, tps, total;  // sketch: K-tiles per slab row, K-tiles per split, total K-tiles
   float* out;           // sketch: partials [split][c][i]; projection: O (a, c, b)
   const int* skip;
+  int pblk;             // sketch panel: 0 (a, c, b) map; 1 blocked raw; 2 blocked hi | lo planes
+  i64 cpad;             // blocked panel: columns per K-tile block (n-tiles x BN)
 };
 
 // Work item id -> (n-tile fastest, then m-tile, then split / slab): CTAs
@@ -174,10 +176,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = q % S;
           if (q >= S) mbar_wait(&empty[s], uint32_t(((q / S) - 1) & 1));
           unsigned char* st = smem + s * G::STAGE;
-          mbar_arrive_tx(&full[s], G::TX);
+          mbar_arrive_tx(&full[s], G::TX + (!PROJ && p.pblk == 2 ? uint32_t(G::B_BYTES) : 0u));
           if (!PROJ) {
             tma_load_3d(st, &tmX, int(bt * kBK), int(it.m0), int(a), &full[s]);
-            tma_load_3d(st + G::A_BYTES, &tmP, int(bt * kBK), n0, int(a), &full[s]);
+            if (p.pblk == 0) {
+              tma_load_3d(st + G::A_BYTES, &tmP, int(bt * kBK), n0, int(a), &full[s]);
+            } else {  // K-tile block (a, bt): rows [plane][cpad] of 32 contiguous values
+              const i64 blk = (a * p.nbt + bt) * (p.pblk == 2 ? 2 : 1);
+              tma_load_2d(st + G::A_BYTES, &tmP, 0, int(blk * p.cpad + n0), &full[s]);
+              if (p.pblk == 2) tma_load_2d(st + G::A_BYTES + G::B_BYTES, &tmP, 0, int((blk + 1) * p.cpad + n0), &full[s]);
+            }
             if (++bt == p.nbt) {
               bt = 0;
               ++a;
@@ -283,8 +291,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < 32; ++k)
             hi[k] = *reinterpret_cast<const float*>(box + k * 128 + ((((lane >> 2) ^ (k & 7))) << 4));
         }
-        // lo plane of the panel tile (same swizzled positions)
-        {
+        // lo plane of the panel tile (same swizzled positions), unless it came by TMA
+        if (PROJ || p.pblk != 2) {
           const unsigned char* braw = st + G::A_BYTES;
           unsigned char* blo = st + G::A_BYTES + G::B_BYTES;
           constexpr int NB = (G::B_CH + 127) / 128;
@@ -622,6 +630,34 @@ __global__ void residual_ct_kernel(const float* C, i64 E, int R, int KP, float* 
   }
 }
 
+// Blocked sketch panel: K-tile block (a, bt) holds [plane][cpad][32] with the
+// 32 b values of column c contiguous (zero beyond R and cols), so one panel
+// tile is a single contiguous TMA box instead of BN rows R*4 bytes apart.
+// planes == 2 stores hi (raw) and lo = x - TF32(x).
+__global__ void panel_block_kernel(const float* __restrict__ P, i64 L, i64 R, i64 cols, i64 nbt, i64 cpad, int planes,
+                                   float* __restrict__ PB) {
+  const i64 n = L * nbt * cpad * 32;
+  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < n; e += i64(gridDim.x) * blockDim.x) {
+    const int kk = int(e & 31);
+    const i64 rest = e >> 5, c = rest % cpad, blk = rest / cpad, a = blk / nbt, b = (blk - a * nbt) * kBK + kk;
+    const float v = (c < cols && b < R) ? __ldg(P + (a * cols + c) * R + b) : 0.f;
+    if (planes == 2) {
+      PB[(2 * blk * cpad + c) * 32 + kk] = v;
+      PB[((2 * blk + 1) * cpad + c) * 32 + kk] = lo_part(v);
+    } else {
+      PB[e] = v;
+    }
+  }
+}
+
+int panel_block_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("RCPG_TC_PBLK");
+    return e != nullptr ? std::atoi(e) : 1;
+  }();
+  return m;
+}
+
 }  // namespace
 
 // fp64 3-D tiled map over a (d0 fastest, d1, d2) view with row pitch `pitch` (0: d0), box {16, b1, 1}
@@ -668,8 +704,23 @@ i64 sketch_tc_splits(ModeView v, i64 cols, int num_sms, i64& tps, i64& total) {
   return ceil_div(total, tps);
 }
 
-void sketch_tc(const float* X, ModeView v, const float* P, i64 cols, float* part, int num_sms, const int* skip,
-               cudaStream_t st) {
+// Only for streamed passes over big tensors whose panel is small next to X
+// (I >= 8 cols: the copy costs <= ~25% of the pass's bytes and is re-read by
+// >= 8 m-tiles). Measured (bench.py, one B200): C5 mode-0 sketch 6.24 -> 5.59 ms,
+// X Z 6.20 -> 5.59 ms; C3 1.76 -> 1.72 / 3.55 -> 3.45 ms; C4 mode 0 (I = 128,
+// a 1.6 GB panel) 2.3 -> 4.7 ms, hence the rule.
+constexpr i64 kPanelBlockMinElems = i64(1) << 26;
+
+bool panel_block_pays(ModeView v, i64 cols) { return v.L * v.I * v.R >= kPanelBlockMinElems && v.I >= 8 * cols; }
+
+i64 sketch_tc_panel_floats(ModeView v, i64 cols) {
+  if (panel_block_mode() == 0 || !panel_block_pays(v, cols)) return 0;
+  const int bn = pick_bn_tc(cols);
+  return v.L * ceil_div(v.R, kBK) * ceil_div(cols, bn) * bn * 32 * 2;
+}
+
+void sketch_tc(const float* X, ModeView v, const float* P, i64 cols, float* part, float* pblk, int num_sms,
+               const int* skip, cudaStream_t st) {
   const int bn = pick_bn_tc(cols);
   TcArgs a{};
   a.L = v.L;
@@ -686,11 +737,28 @@ void sketch_tc(const float* X, ModeView v, const float* P, i64 cols, float* part
   const cuuint64_t xd[3] = {cuuint64_t(v.R), cuuint64_t(v.I), cuuint64_t(v.L)};
   const cuuint64_t xs[2] = {cuuint64_t(v.R) * 4, cuuint64_t(v.I * v.R) * 4};
   const cuuint32_t xb[3] = {kBK, kBM, 1};
-  const cuuint64_t pd[3] = {cuuint64_t(v.R), cuuint64_t(cols), cuuint64_t(v.L)};
-  const cuuint64_t ps[2] = {cuuint64_t(v.R) * 4, cuuint64_t(cols * v.R) * 4};
-  const cuuint32_t pb[3] = {kBK, cuuint32_t(bn), 1};
+  a.cpad = a.n_ntiles * bn;
+  const i64 blk_rows = v.L * a.nbt * a.cpad * 2;
+  a.pblk = (pblk != nullptr && blk_rows <= kMaxCoord && panel_block_pays(v, cols)) ? panel_block_mode() : 0;
   const CUtensorMap mx = tensor_map(X, 3, xd, xs, xb);
-  const CUtensorMap mp = tensor_map(P, 3, pd, ps, pb);
+  CUtensorMap mp;
+  if (a.pblk != 0) {
+    const int planes = a.pblk == 2 ? 2 : 1;
+    const i64 n = v.L * a.nbt * a.cpad * 32;
+    panel_block_kernel<<<int(std::min<i64>(ceil_div(n, 256), i64(num_sms) * 16)), 256, 0, st>>>(P, v.L, v.R, cols, a.nbt,
+                                                                                              a.cpad, planes, pblk);
+    count_launch();
+    RCPG_LAUNCHED();
+    const cuuint64_t pd[2] = {32, cuuint64_t(v.L * a.nbt * a.cpad * planes)};
+    const cuuint64_t ps[1] = {128};
+    const cuuint32_t pb[2] = {kBK, cuuint32_t(bn)};
+    mp = tensor_map(pblk, 2, pd, ps, pb);
+  } else {
+    const cuuint64_t pd[3] = {cuuint64_t(v.R), cuuint64_t(cols), cuuint64_t(v.L)};
+    const cuuint64_t ps[2] = {cuuint64_t(v.R) * 4, cuuint64_t(cols * v.R) * 4};
+    const cuuint32_t pb[3] = {kBK, cuuint32_t(bn), 1};
+    mp = tensor_map(P, 3, pd, ps, pb);
+  }
   const int grid = int(std::min<i64>(a.items, num_sms));
   dispatch<false>(bn, mx, mp, a, grid, st);
 }

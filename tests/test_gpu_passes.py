@@ -112,3 +112,20 @@ def test_relative_error_gram_and_exact(rcp, dtype, tol, shape, rank):
             assert abs(got - want) <= tol * want, (got, want)
         else:
             assert abs(got - want) <= (1e-12 if dtype == np.float64 else 2e-6), (got, want)
+
+
+# Views big enough (L*I*R >= 2^26, I >= 8 cols) for the fp32 sketch to stream a K-tile-
+# blocked copy of the panel (passes_tc.cu panel_block_kernel): R % 32 != 0 (zero-padded
+# last block), cols not a multiple of the UMMA N (zero-padded columns), several slabs.
+@pytest.mark.parametrize("view", [(1, 600, 131076, 70), (2, 300, 131076, 33)])
+def test_sketch_pass_blocked_panel(rcp, view):
+    L, I, R, cols = view
+    x, p, _ = _inputs(L, I, R, cols, np.float32, 13)
+    out = rcp.stream_pass("sketch", x, p, cols)
+    ref = np.zeros((I, cols))
+    ref_abs = np.zeros((I, cols))
+    for a in range(L):
+        xd, pd = x[a].astype(np.float64), p[a].astype(np.float64)
+        ref += xd @ pd.T
+        ref_abs += np.abs(xd) @ np.abs(pd).T
+    _check(out, ref, ref_abs, np.float32)
