@@ -775,6 +775,7 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
       };
       const bool stampA = p.prof != nullptr && g == 0 && tid == 0;
       unsigned long long ts = stampA ? gtimer() : 0;
+      if (stampA) p.prof[22] += ts - tp0;
       auto stampa = [&](int slot) {
         if (stampA) {
           const unsigned long long t = gtimer();
@@ -865,7 +866,11 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
         }
       }
       unsigned long long tp1 = 0;
-      if (p.prof && g == 0 && tid == 0) tp1 = gtimer();
+      if (p.prof && g == 0 && tid == 0) {
+        tp1 = gtimer();
+        p.prof[23] += tp1 - ts;
+        p.prof[24] = G;
+      }
       grid_sync(p.bar);
       unsigned long long tp2 = 0;
       if (p.prof && g == 0 && tid == 0) tp2 = gtimer();

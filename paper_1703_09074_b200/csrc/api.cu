@@ -901,6 +901,8 @@ AlsHandles<T> run_als(rcpg_context* c, const T* B, const i64* shape, int order, 
         unsigned long long hp[32];
         RCPG_CUDA(cudaMemcpyAsync(hp, prof, sizeof(hp), cudaMemcpyDeviceToHost, c->st));
         RCPG_CUDA(cudaStreamSynchronize(c->st));
+        fprintf(stderr, "[rcpg als A0] G=%llu factors->smem %.2f  tail+partials %.2f us (per mode step)\n", hp[24],
+                hp[22] / 1e3 / double(hp[4]), hp[23] / 1e3 / double(hp[4]));
         fprintf(stderr, "[rcpg als A] batches/mode %.1f: gather0 %.2f issue %.2f kc %.2f wait+cvt %.2f mma %.2f us (per mode step)\n",
                 hp[21] / double(hp[4]), hp[16] / 1e3 / double(hp[4]), hp[17] / 1e3 / double(hp[4]),
                 hp[18] / 1e3 / double(hp[4]), hp[19] / 1e3 / double(hp[4]), hp[20] / 1e3 / double(hp[4]));

@@ -716,7 +716,7 @@ bool panel_block_pays(ModeView v, i64 cols) { return v.L * v.I * v.R >= kPanelBl
 i64 sketch_tc_panel_floats(ModeView v, i64 cols) {
   if (panel_block_mode() == 0 || !panel_block_pays(v, cols)) return 0;
   const int bn = pick_bn_tc(cols);
-  return v.L * ceil_div(v.R, kBK) * ceil_div(cols, bn) * bn * 32 * 2;
+  return v.L * ceil_div(v.R, kBK) * ceil_div(cols, bn) * bn * 32 * (panel_block_mode() == 2 ? 2 : 1);
 }
 
 void sketch_tc(const float* X, ModeView v, const float* P, i64 cols, float* part, float* pblk, int num_sms,
