@@ -509,25 +509,41 @@ __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T
     __syncthreads();
   }
   ALS_STAMP(9);
-  // 3. F = W pinv(V), rounded to Scalar like the reference's factor
+  // 3. F = W pinv(V), rounded to Scalar like the reference's factor.
+  // Register tile per thread: rows lane + 32u (u < 4) x 4 consecutive columns,
+  // so one smem load of W feeds 4 FMAs; every output is still the chain
+  // s = sum_k W[i, k] Pm[k, r] in k order from 0 (same bits as one chain per output).
   {
-    // each lane: rows lane, lane + 32, ... as independent accumulation chains
-    // (per output the k order is unchanged)
     const WT* __restrict__ Wr = W;
     const double* __restrict__ Pr = Pm;
-    for (int r = wid0; r < R; r += nw0)
-      for (int i0 = lane0; i0 < I; i0 += 128) {
-        double s[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int k = 0; k < R; ++k) {
-          const double pk = Pr[k + r * R];
+    constexpr int TR = 4;
+    const int ngrp = (R + TR - 1) / TR;
+    for (int item = wid0; item < ngrp * ((I + 127) / 128); item += nw0) {
+      const int rg = item % ngrp, ib = (item / ngrp) * 128 + lane0;
+      const int r0 = rg * TR;
+      double s[4][TR];
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (i0 + 32 * u < I) s[u] += double(Wr[i0 + 32 * u + k * I]) * pk;
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int j = 0; j < TR; ++j) s[u][j] = 0.0;
+      for (int k = 0; k < R; ++k) {
+        double pk[TR];
+#pragma unroll
+        for (int j = 0; j < TR; ++j) pk[j] = r0 + j < R ? Pr[k + (r0 + j) * R] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = ib + 32 * u;
+          const double w = i < I ? double(Wr[i + k * I]) : 0.0;
+#pragma unroll
+          for (int j = 0; j < TR; ++j) s[u][j] += w * pk[j];
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (i0 + 32 * u < I) Fs[i0 + 32 * u + r * ldf] = double(T(s[u]));
       }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int j = 0; j < TR; ++j)
+          if (ib + 32 * u < I && r0 + j < R) Fs[ib + 32 * u + (r0 + j) * ldf] = double(T(s[u][j]));
+    }
   }
   __syncthreads();
   ALS_STAMP(10);
@@ -555,37 +571,54 @@ __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T
   }
   __syncthreads();
   ALS_STAMP(11);
-  // 5. Gram of the new factor
+  // 5. Gram of the new factor: 4 x 4 blocks (a-block <= b-block) per thread,
+  // 8 loads per i for 16 FMAs; entry (a, b), a <= b, is the chain
+  // sum_i F[i, a] F[i, b] in i order (same bits as one chain per pair) and is
+  // written to both (a, b) and (b, a)
   {
-    // pairs a <= b (the product is symmetric: same value, same summation
-    // order), four pairs per thread as independent chains
     const double* __restrict__ Fr = Fs;
-    const int NPR = R * (R + 1) / 2;
-    for (int q0 = tid; q0 < NPR; q0 += 4 * nt) {
-      int pa[4], pb[4];
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const int nb = (R + 3) / 4, nblk = nb * (nb + 1) / 2;
+    for (int q = tid; q < nblk; q += nt) {
+      int bb = int((sqrt(8.0 * q + 1.0) - 1.0) * 0.5);
+      while (bb * (bb + 1) / 2 > q) --bb;
+      while ((bb + 1) * (bb + 2) / 2 <= q) ++bb;
+      const int ab = q - bb * (bb + 1) / 2;  // ab <= bb
+      const int a0 = 4 * ab, b0 = 4 * bb;
+      double acc[4][4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int q = q0 + u * nt;
-        int b = int((sqrt(8.0 * q + 1.0) - 1.0) * 0.5);
-        while (b * (b + 1) / 2 > q) --b;
-        while ((b + 1) * (b + 2) / 2 <= q) ++b;
-        pb[u] = q < NPR ? b : 0;
-        pa[u] = q < NPR ? q - b * (b + 1) / 2 : 0;
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
+      int ca[4], cb[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        ca[x] = (a0 + x < R ? a0 + x : a0) * ldf;
+        cb[x] = (b0 + x < R ? b0 + x : b0) * ldf;
       }
       for (int i = 0; i < I; ++i) {
+        double fa[4], fb[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) acc[u] += Fr[i + pa[u] * ldf] * Fr[i + pb[u] * ldf];
+        for (int x = 0; x < 4; ++x) {
+          fa[x] = Fr[i + ca[x]];
+          fb[x] = Fr[i + cb[x]];
+        }
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) acc[x][y] += fa[x] * fb[y];
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (q0 + u * nt >= NPR) continue;
-        const T g = T(acc[u]);
-        fs.gram[mode][pa[u] + pb[u] * R] = g;
-        fs.gram[mode][pb[u] + pa[u] * R] = g;
-        V[pa[u] + pb[u] * R] = double(g);  // this mode's Gram, for the fit
-        V[pb[u] + pa[u] * R] = double(g);
-      }
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) {
+          const int a = a0 + x, b = b0 + y;
+          if (a >= R || b >= R || a > b) continue;
+          const T g = T(acc[x][y]);
+          fs.gram[mode][a + b * R] = g;
+          fs.gram[mode][b + a * R] = g;
+          V[a + b * R] = double(g);  // this mode's Gram, for the fit
+          V[b + a * R] = double(g);
+        }
     }
   }
   __syncthreads();
@@ -783,6 +816,20 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
           ts = t;
         }
       };
+      // fibD rows beyond I and kc rows beyond R stay zero for the whole mode
+      // step (the per-batch writes cover [0, I) and [0, R) only), so the MMA
+      // fragment loads below need no bounds checks
+      for (int e = tid; e < BATCH * (ldI + ldR); e += nt) fibD[e] = 0.0;  // kc follows fibD
+      // this warp's tiles: packed (i0 | r0 << 16), the divisions done once
+      int toff[kAlsTiles];
+#pragma unroll
+      for (int t = 0; t < kAlsTiles; ++t) {
+        const int tile = wrp + t * nwarp;
+        toff[t] = tile < NTILE ? ((16 * (tile % I16) + gq) | ((8 * (tile / I16) + gq) << 16)) : 0;
+      }
+      // Khatri-Rao rows: thread -> (column kr_r, first position kr_p0), stride kr_ps
+      const int kr_ps = nt / R, kr_r = tid % R, kr_p0 = tid / R;
+      __syncthreads();
       if (j0 < j1) gather(j0, 0);
       stampa(16);
       int buf = 0;
@@ -794,30 +841,36 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
           als_cp_commit();  // keep one group per iteration
         stampa(17);
         if (tid < BATCH) {  // multi-index digits of each position, once (32-bit: J < 2^31)
+          // stored as smem offsets of the factor rows, slot j = j-th other mode
+          // from the highest down (the product order of kruskal.hpp:58-62)
           const unsigned s_ = unsigned(pb) + unsigned(tid);
           unsigned a = s_ / unsigned(Rr), b = s_ - a * unsigned(Rr);
-          for (int k = N - 1; k > m; --k) {
+          int j = 0;
+          for (int k = N - 1; k > m; --k, ++j) {
             const unsigned ek = unsigned(sext[k]);
-            pidx[tid * kMaxOrder + k] = int(b % ek);
+            pidx[tid * kMaxOrder + j] = sfoff[k] + int(b % ek) * R;
             b /= ek;
           }
-          for (int k = m - 1; k >= 0; --k) {
+          for (int k = m - 1; k >= 0; --k, ++j) {
             const unsigned ek = unsigned(sext[k]);
-            pidx[tid * kMaxOrder + k] = int(a % ek);
+            pidx[tid * kMaxOrder + j] = sfoff[k] + int(a % ek) * R;
             a /= ek;
           }
         }
         __syncthreads();
-        for (int e = tid; e < BATCH * R; e += nt) {
-          const int pp = e / R, r = e % R;
-          double v = 0.0;
-          if (pp < np) {
-            T prod = T(1);
-            for (int k = N - 1; k >= 0; --k)  // highest mode first (kruskal.hpp:58-62)
-              if (k != m) prod *= fsm[sfoff[k] + pidx[pp * kMaxOrder + k] * R + r];
-            v = double(prod);
+        if (kr_p0 < kr_ps) {
+          for (int pp = kr_p0; pp < BATCH; pp += kr_ps) {
+            double v = 0.0;
+            if (pp < np) {
+              const int* po = pidx + pp * kMaxOrder;
+              T prod = T(1);
+#pragma unroll
+              for (int j = 0; j < kMaxOrder - 1; ++j)
+                if (j < N - 1) prod *= fsm[po[j] + kr_r];
+              v = double(prod);
+            }
+            kc[pp * ldR + kr_r] = v;
           }
-          kc[pp * ldR + r] = v;
         }
         stampa(18);
         als_cp_wait<1>();  // this batch's fibers (own copies) have landed
@@ -837,13 +890,9 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
           const double* krow = kc + pp * ldR;
 #pragma unroll
           for (int t = 0; t < kAlsTiles; ++t) {
-            const int tile = wrp + t * nwarp;
-            if (tile < NTILE) {
-              const int i0 = 16 * (tile % I16) + gq, r0 = 8 * (tile / I16) + gq;
-              const double a0 = i0 < I ? frow[i0] : 0.0;
-              const double a1 = i0 + 8 < I ? frow[i0 + 8] : 0.0;
-              const double b0 = r0 < R ? krow[r0] : 0.0;
-              als_dmma(acc[t], a0, a1, b0);
+            if (wrp + t * nwarp < NTILE) {  // zero padding beyond I and R (see above)
+              const int i0 = toff[t] & 0xffff, r0 = toff[t] >> 16;
+              als_dmma(acc[t], frow[i0], frow[i0 + 8], krow[r0]);
             }
           }
         }
@@ -879,20 +928,30 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
       double* Wg = p.part + 2 * i64(G) * p.part_stride;
       {
         const double* pp0 = p.part + i64(parity) * G * p.part_stride;
+        // `sub` threads (a power of two <= 32, within one warp) per output:
+        // member l sums partials l, l + sub, ... (16 loads in flight), then a
+        // fixed butterfly over the group -- deterministic for a given G
         const int ch = (nout + G - 1) / G;
         const int o1 = min(nout, (g + 1) * ch);
-        for (int o = g * ch + tid; o < o1; o += nt) {
+        int sub = 1;
+        while (sub < 32 && 2 * sub * ch <= nt) sub *= 2;
+        const int gi = tid / sub, l = tid % sub, ng = nt / sub;
+        for (int ob = g * ch; ob < o1; ob += ng) {  // uniform trip count: the shuffles see full warps
+          const int o = ob + gi;
+          const bool on = o < o1;
           double s = 0.0;
-          int q = 0;
-          for (; q + 16 <= G; q += 16) {  // 16 loads in flight, then the adds in order
+          for (int q0 = l; q0 < G; q0 += 16 * sub) {
             double v[16];
 #pragma unroll
-            for (int u = 0; u < 16; ++u) v[u] = ldcg(&pp0[i64(q + u) * p.part_stride + o]);
+            for (int u = 0; u < 16; ++u) {
+              const int q = q0 + sub * u;
+              v[u] = (on && q < G) ? ldcg(&pp0[i64(q) * p.part_stride + o]) : 0.0;
+            }
 #pragma unroll
             for (int u = 0; u < 16; ++u) s += v[u];
           }
-          for (; q < G; ++q) s += ldcg(&pp0[i64(q) * p.part_stride + o]);
-          Wg[o] = s;
+          for (int off = sub / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+          if (on && l == 0) Wg[o] = s;
         }
       }
       grid_sync(p.bar);
