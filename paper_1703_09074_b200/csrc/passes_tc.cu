@@ -634,18 +634,20 @@ __global__ void residual_ct_kernel(const float* C, i64 E, int R, int KP, float* 
 // 32 b values of column c contiguous (zero beyond R and cols), so one panel
 // tile is a single contiguous TMA box instead of BN rows R*4 bytes apart.
 // planes == 2 stores hi (raw) and lo = x - TF32(x).
-__global__ void panel_block_kernel(const float* __restrict__ P, i64 L, i64 R, i64 cols, i64 nbt, i64 cpad, int planes,
-                                   float* __restrict__ PB) {
-  const i64 n = L * nbt * cpad * 32;
-  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < n; e += i64(gridDim.x) * blockDim.x) {
-    const int kk = int(e & 31);
-    const i64 rest = e >> 5, c = rest % cpad, blk = rest / cpad, a = blk / nbt, b = (blk - a * nbt) * kBK + kk;
-    const float v = (c < cols && b < R) ? __ldg(P + (a * cols + c) * R + b) : 0.f;
-    if (planes == 2) {
-      PB[(2 * blk * cpad + c) * 32 + kk] = v;
-      PB[((2 * blk + 1) * cpad + c) * 32 + kk] = lo_part(v);
-    } else {
-      PB[e] = v;
+__global__ void __launch_bounds__(256) panel_block_kernel(const float* __restrict__ P, i64 L, i64 R, i64 cols, i64 nbt,
+                                                          i64 cpad, int planes, float* __restrict__ PB) {
+  // one K-tile block per CTA iteration: one 64-bit division per block, then
+  // (c, kk) = (e / 32, e % 32): 128-byte reads per column, contiguous writes
+  const int per = int(cpad) * 32;
+  for (i64 blk = blockIdx.x; blk < L * nbt; blk += gridDim.x) {
+    const i64 a = blk / nbt, b0 = (blk - a * nbt) * kBK;
+    const float* src = P + a * cols * R + b0;
+    float* dst = PB + blk * planes * i64(per);
+    for (int e = threadIdx.x; e < per; e += blockDim.x) {
+      const int c = e >> 5, kk = e & 31;
+      const float v = (c < cols && b0 + kk < R) ? __ldg(src + i64(c) * R + kk) : 0.f;
+      dst[e] = v;
+      if (planes == 2) dst[per + e] = lo_part(v);
     }
   }
 }
@@ -744,9 +746,8 @@ void sketch_tc(const float* X, ModeView v, const float* P, i64 cols, float* part
   CUtensorMap mp;
   if (a.pblk != 0) {
     const int planes = a.pblk == 2 ? 2 : 1;
-    const i64 n = v.L * a.nbt * a.cpad * 32;
-    panel_block_kernel<<<int(std::min<i64>(ceil_div(n, 256), i64(num_sms) * 16)), 256, 0, st>>>(P, v.L, v.R, cols, a.nbt,
-                                                                                              a.cpad, planes, pblk);
+    panel_block_kernel<<<int(std::min<i64>(v.L * a.nbt, i64(num_sms) * 8)), 256, 0, st>>>(P, v.L, v.R, cols, a.nbt,
+                                                                                       a.cpad, planes, pblk);
     count_launch();
     RCPG_LAUNCHED();
     const cuuint64_t pd[2] = {32, cuuint64_t(v.L * a.nbt * a.cpad * planes)};
