@@ -308,7 +308,7 @@ __global__ void zero_factor_kernel(T* F, i64 n, int R, T* gram) {
 __device__ unsigned long long* g_als_prof = nullptr;
 #define ALS_STAMP(slot)                                                              \
   do {                                                                               \
-    if (g_als_prof && threadIdx.x == 0) {                                            \
+    if (g_als_prof && threadIdx.x == 0 && blockIdx.x == 0) {                         \
       unsigned long long _t;                                                         \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                          \
       g_als_prof[slot] += _t - _tlast;                                               \
@@ -399,9 +399,14 @@ __device__ void gj_inverse_regs(double* A, int R, int* ok, double* scratch) {
   __syncthreads();
 }
 
+// part 0: the whole mode update. part 1: only V and pinv(V) (steps 1-2), written
+// to pm_io (R x R doubles) -- they depend only on the other modes' Grams, so the
+// loop kernel computes them on one CTA while the others run the MTTKRP.
+// part 2: steps 3-6 with pinv(V) read from pm_io.
 template <typename T, typename WT>
 __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T* weights, double tol,
-                                int max_iter, double* trace_fit, double* trace_sec, AlsState* st, double* work) {
+                                int max_iter, double* trace_fit, double* trace_sec, AlsState* st, double* work,
+                                int part = 0, double* pm_io = nullptr) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int R = fs.rank, N = fs.order;
   const int I = int(fs.extent[mode]);
@@ -418,6 +423,13 @@ __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T
   unsigned long long _tlast = 0;
   if (g_als_prof && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_tlast));
 
+  const int R2 = R * R;
+  const int lane0 = tid & 31, wid0 = tid >> 5, nw0 = nt >> 5;
+  double* Pm = A;
+  if (part == 2) {
+    for (int e = tid; e < R2; e += nt) A[e] = ldcg(&pm_io[e]);
+    __syncthreads();
+  } else {
   // 1. V = Hadamard of the other modes' Grams (solve.hpp:209-211)
   for (int e = tid; e < R * R; e += nt) {
     double v = 1.0;
@@ -429,8 +441,6 @@ __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T
   if (tid == 0) s_ok = 1;
   __syncthreads();
   // 2. Gauss-Jordan inverse of the SPD matrix, one barrier per pivot
-  const int R2 = R * R;
-  const int lane0 = tid & 31, wid0 = tid >> 5, nw0 = nt >> 5;
   // X (R x R, used only by the eigen fallback afterwards) holds the row buffers
   if (R <= 32 && R <= 4 * nw0 && R * R >= 64) {
     gj_inverse_regs<4, 1>(A, R, &s_ok, X);
@@ -484,7 +494,6 @@ __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T
   fro = sqrt(block_reduce_sum(fro));
   ifro = sqrt(block_reduce_sum(ifro));
   const bool direct = s_ok && isfinite(ifro) && ifro > 0.0 && (1.0 / ifro) > double(R) * double(Traits<T>::eps) * fro;
-  double* Pm = A;
   if (!direct) {
     for (int e = tid; e < R2; e += nt) A[e] = V[e];
     __syncthreads();
@@ -507,6 +516,11 @@ __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T
     Pm = V;
     if (tid == 0) st->pivots_fallback += 1;
     __syncthreads();
+  }
+  if (part == 1) {
+    for (int e = tid; e < R2; e += nt) pm_io[e] = Pm[e];
+    return;
+  }
   }
   ALS_STAMP(9);
   // 3. F = W pinv(V), rounded to Scalar like the reference's factor.
@@ -694,6 +708,7 @@ struct AlsLoopArgs {
   double* trace_sec;
   AlsState* st;
   double* part;  // [2][G][max I*R]
+  double* pm;    // R x R pinv(V) from the last CTA (nullptr: CTA 0 does the whole update)
   i64 part_stride;
   GridBarrier* bar;
   unsigned long long* prof;  // optional [8] ns per phase (CTA 0): A, bar1, B, bar2
@@ -753,6 +768,15 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
       const int nout = int(I) * R;
       unsigned long long tp0 = 0;
       if (p.prof && g == 0 && tid == 0) tp0 = gtimer();
+      // the last CTA computes pinv(V) of this mode (it needs only the other
+      // modes' Grams) while CTAs 0 .. G-2 run the MTTKRP
+      const bool split = p.pm != nullptr && G >= 2;
+      const int GA = split ? G - 1 : G;
+      if (split && g == G - 1) {
+        FactorSet<T> fs = p.fs;
+        als_mode_update<T, double>(fs, m, static_cast<const double*>(nullptr), p.weights, p.tol, p.max_iter,
+                                   p.trace_fit, p.trace_sec, p.st, sm, 1, p.pm);
+      }
       // ---- A: partial MTTKRP over positions [j0, j1): W_part = Fib^T KC on
       //      the FP64 tensor cores (mma.m16n8k4, M = i, N = r, K = positions);
       //      each warp keeps its 16x8 output tiles in registers. Fibers are
@@ -763,8 +787,8 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
       double acc[kAlsTiles][4];
 #pragma unroll
       for (int t = 0; t < kAlsTiles; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.0;
-      const i64 chunk = ceil_div(J, G);
-      const i64 j0 = g * chunk, j1 = j0 + chunk < J ? j0 + chunk : J;
+      const i64 chunk = ceil_div(J, GA);
+      const i64 j0 = g < GA ? g * chunk : J, j1 = j0 + chunk < J ? j0 + chunk : J;
       // padded row strides (== 4 mod 16 doubles): the MMA fragment loads of
       // rows pp = 4 ks + tq hit distinct banks
       const int ldI = als_ld(int(I)), ldR = als_ld(R);
@@ -940,12 +964,12 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
           const int o = ob + gi;
           const bool on = o < o1;
           double s = 0.0;
-          for (int q0 = l; q0 < G; q0 += 16 * sub) {
+          for (int q0 = l; q0 < GA; q0 += 16 * sub) {
             double v[16];
 #pragma unroll
             for (int u = 0; u < 16; ++u) {
               const int q = q0 + sub * u;
-              v[u] = (on && q < G) ? ldcg(&pp0[i64(q) * p.part_stride + o]) : 0.0;
+              v[u] = (on && q < GA) ? ldcg(&pp0[i64(q) * p.part_stride + o]) : 0.0;
             }
 #pragma unroll
             for (int u = 0; u < 16; ++u) s += v[u];
@@ -966,7 +990,8 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
           p.prof[14] += gtimer() - tp2;
         }
         FactorSet<T> fs = p.fs;
-        als_mode_update<T, double>(fs, m, W, p.weights, p.tol, p.max_iter, p.trace_fit, p.trace_sec, p.st, work);
+        als_mode_update<T, double>(fs, m, W, p.weights, p.tol, p.max_iter, p.trace_fit, p.trace_sec, p.st, work,
+                                   split ? 2 : 0, p.pm);
       }
       unsigned long long tp3 = 0;
       if (p.prof && g == 0 && tid == 0) tp3 = gtimer();
@@ -1518,7 +1543,7 @@ void als_loop(const T* B, const i64* shape, int order, const FactorSet<T>& fs, T
     maxout = std::max(maxout, shape[m] * R);
   }
   AlsLoopArgs<T> a{B, make_shape(shape, order), fs, weights, tol, max_iter, trace_fit, trace_sec, state, part,
-                   maxout, bar, prof};
+                   nullptr, maxout, bar, prof};
   // 64-position batches when they fit: half the per-batch latency chains
   static const size_t lim64 = enable_max_dyn_smem(als_loop_kernel<T, 64>);
   static const size_t lim32 = enable_max_dyn_smem(als_loop_kernel<T, 32>);
@@ -1528,6 +1553,12 @@ void als_loop(const T* B, const i64* shape, int order, const FactorSet<T>& fs, T
     const int maxc = max_coop_blocks(kern, kAlsThreads, smem);
     int G = int(std::max<i64>(1, std::min<i64>(ceil_div(maxJ, batch), maxc)));
     G = int(std::min<i64>(G, part_elems / (2 * maxout) - 1));  // + one slot for the reduced W
+    // pinv(V) of the mode on the last CTA, concurrently with the MTTKRP (after the reduced W);
+    // RCPG_ALS_SPLIT=0: CTA 0 does the whole mode update after the MTTKRP (A/B hook)
+    const char* sp = std::getenv("RCPG_ALS_SPLIT");
+    const bool split_ok = !(sp != nullptr && sp[0] == '0') && G >= 3 && i64(R) * R <= maxout &&
+                          (2 * i64(G) + 2) * maxout <= part_elems;
+    a.pm = split_ok ? part + (2 * i64(G) + 1) * maxout : nullptr;
     launch_coop(kern, G, kAlsThreads, smem, st, a);
   };
   const size_t s64 = als_loop_smem<T, 64>(shape, order, R);
