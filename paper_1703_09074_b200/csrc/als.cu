@@ -1551,13 +1551,14 @@ void als_loop(const T* B, const i64* shape, int order, const FactorSet<T>& fs, T
   (void)lim32;
   auto run = [&](auto kern, size_t smem, int batch) {
     const int maxc = max_coop_blocks(kern, kAlsThreads, smem);
-    int G = int(std::max<i64>(1, std::min<i64>(ceil_div(maxJ, batch), maxc)));
-    G = int(std::min<i64>(G, part_elems / (2 * maxout) - 1));  // + one slot for the reduced W
-    // pinv(V) of the mode on the last CTA, concurrently with the MTTKRP (after the reduced W);
-    // RCPG_ALS_SPLIT=0: CTA 0 does the whole mode update after the MTTKRP (A/B hook)
+    // pinv(V) of the mode on one extra CTA, concurrently with the MTTKRP (stored after the
+    // reduced W); RCPG_ALS_SPLIT=0: CTA 0 does the whole mode update after the MTTKRP (A/B hook)
     const char* sp = std::getenv("RCPG_ALS_SPLIT");
-    const bool split_ok = !(sp != nullptr && sp[0] == '0') && G >= 3 && i64(R) * R <= maxout &&
-                          (2 * i64(G) + 2) * maxout <= part_elems;
+    const bool want_split = !(sp != nullptr && sp[0] == '0') && i64(R) * R <= maxout;
+    int G = int(std::max<i64>(1, std::min<i64>(ceil_div(maxJ, batch) + (want_split ? 1 : 0), maxc)));
+    G = int(std::min<i64>(G, part_elems / (2 * maxout) - 2));  // + slots for the reduced W and pinv(V)
+    G = std::max(G, 1);
+    const bool split_ok = want_split && G >= 3 && (2 * i64(G) + 2) * maxout <= part_elems;
     a.pm = split_ok ? part + (2 * i64(G) + 1) * maxout : nullptr;
     launch_coop(kern, G, kAlsThreads, smem, st, a);
   };
