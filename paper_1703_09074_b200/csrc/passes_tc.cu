@@ -418,20 +418,28 @@ struct ResArgs {
 };
 
 // Items are (m-tile, n-tile) with the n-tile fastest: the coef rows of an
-// m-tile are formed once and stay in TMEM for all of its n-tiles; each item
-// streams its X tile and its C^T tile (hi | lo) through a 2-stage ring.
+// m-tile are formed once and stay in TMEM for all of its n-tiles. X tiles
+// stream through an SX-deep ring freed by the epilogue (the kernel's bytes);
+// the C^T tiles (hi | lo, from L2) through an SB-deep ring freed by the MMA
+// commit (a C^T tile is reloaded per item; with only two in flight the MMA
+// waited on its L2 latency and the epilogue on the MMA: ncu, C5).
 template <int KP>
 struct ResPlan {
   static constexpr int KB = KP / 32;                  // 32-wide swizzle boxes along K
   static constexpr int B_PLANE = KP * kRBN * 4;       // one plane of the C^T tile
   static constexpr int X_BYTES = kRBM * kRBN * 4;     // 32 KB: 2 boxes of 32 columns
-  static constexpr int STAGE = X_BYTES + 2 * B_PLANE;
-  static constexpr int SMEM = 2 * STAGE + 1024;
+  static constexpr int B_STAGE = 2 * B_PLANE;
+  static constexpr int SB = KP >= 64 ? 3 : 4;
+  static constexpr int SX_FIT = (200 * 1024 - SB * B_STAGE) / X_BYTES;
+  static constexpr int SX = SX_FIT < 6 ? SX_FIT : 6;
+  static constexpr int SMEM = SX * X_BYTES + SB * B_STAGE + 1024;
   static constexpr uint32_t ACOL = 0;                 // A slots: 2 x (hi KP | lo KP)
-  static constexpr uint32_t DCOL = 4 * KP;            // accumulators: 2 x kRBN
+  static constexpr uint32_t DCOL = 4 * KP;            // accumulators: NACC x kRBN
+  static constexpr int NACC = 4;                      // MMA runs up to 3 items ahead of the epilogue
   static constexpr uint32_t TMEM_COLS = 512;
   static constexpr uint32_t IDESC = idesc_tf32(kRBM, kRBN, 0, 0);
-  static_assert(DCOL + 2 * kRBN <= TMEM_COLS, "TMEM plan");
+  static_assert(DCOL + NACC * kRBN <= TMEM_COLS, "TMEM plan");
+  static_assert(SX >= 2, "X ring depth");
 };
 
 template <int KP>
@@ -439,9 +447,12 @@ __global__ void __launch_bounds__(kResThreads, 1)
     residual_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmBh,
                        const __grid_constant__ CUtensorMap tmBl, ResArgs p) {
   using G = ResPlan<KP>;
+  constexpr int SX = G::SX, SB = G::SB;
   extern __shared__ unsigned char smem_dyn[];
   unsigned char* smem = smem_dyn + ((1024 - (smem_u32(smem_dyn) & 1023)) & 1023);
-  __shared__ __align__(8) uint64_t full[2], empty[2], afull[2], aempty[2], accf[2], acce[2];
+  unsigned char* bsm = smem + SX * G::X_BYTES;  // C^T ring
+  constexpr int NA = G::NACC;
+  __shared__ __align__(8) uint64_t fullx[SX], emptyx[SX], fullb[SB], emptyb[SB], afull[2], aempty[2], accf[NA], acce[NA];
   __shared__ uint32_t tmem_sh;
   __shared__ double red[2][8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -451,11 +462,19 @@ __global__ void __launch_bounds__(kResThreads, 1)
   const i64 mt0 = c0 / p.ntiles;  // first m-tile of this CTA; A slot of m-tile mt = (mt - mt0) & 1
 
   if (threadIdx.x == 0) {
+    for (int b = 0; b < SX; ++b) {
+      mbar_init(&fullx[b], 1);
+      mbar_init(&emptyx[b], 128);
+    }
+    for (int b = 0; b < SB; ++b) {
+      mbar_init(&fullb[b], 1);
+      mbar_init(&emptyb[b], 1);
+    }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&full[b], 1);
-      mbar_init(&empty[b], 128);
       mbar_init(&afull[b], 128);
       mbar_init(&aempty[b], 1);
+    }
+    for (int b = 0; b < NA; ++b) {
       mbar_init(&accf[b], 1);
       mbar_init(&acce[b], 128);
     }
@@ -475,17 +494,20 @@ __global__ void __launch_bounds__(kResThreads, 1)
     if (lane == 0) {
       for (int j = 0; j < n_items; ++j) {
         const i64 id = c0 + j, mt = id / p.ntiles, nt = id - mt * p.ntiles;
-        const int s = j & 1;
-        if (j >= 2) mbar_wait(&empty[s], uint32_t(((j >> 1) - 1) & 1));
-        unsigned char* st = smem + s * G::STAGE;
-        mbar_arrive_tx(&full[s], G::STAGE);
+        const int sx = j % SX, sb = j % SB;
+        if (j >= SX) mbar_wait(&emptyx[sx], uint32_t(((j / SX) - 1) & 1));
+        unsigned char* xs = smem + sx * G::X_BYTES;
+        mbar_arrive_tx(&fullx[sx], G::X_BYTES);
 #pragma unroll
         for (int g = 0; g < kRBN / 32; ++g)
-          tma_load_2d(st + g * (kRBM * 128), &tmX, int(nt * kRBN) + 32 * g, int(mt * kRBM), &full[s]);
+          tma_load_2d(xs + g * (kRBM * 128), &tmX, int(nt * kRBN) + 32 * g, int(mt * kRBM), &fullx[sx]);
+        if (j >= SB) mbar_wait(&emptyb[sb], uint32_t(((j / SB) - 1) & 1));
+        unsigned char* bs = bsm + sb * G::B_STAGE;
+        mbar_arrive_tx(&fullb[sb], G::B_STAGE);
 #pragma unroll
         for (int kb = 0; kb < G::KB; ++kb) {
-          tma_load_2d(st + G::X_BYTES + kb * (kRBN * 128), &tmBh, 32 * kb, int(nt * kRBN), &full[s]);
-          tma_load_2d(st + G::X_BYTES + G::B_PLANE + kb * (kRBN * 128), &tmBl, 32 * kb, int(nt * kRBN), &full[s]);
+          tma_load_2d(bs + kb * (kRBN * 128), &tmBh, 32 * kb, int(nt * kRBN), &fullb[sb]);
+          tma_load_2d(bs + G::B_PLANE + kb * (kRBN * 128), &tmBl, 32 * kb, int(nt * kRBN), &fullb[sb]);
         }
       }
     }
@@ -494,16 +516,16 @@ __global__ void __launch_bounds__(kResThreads, 1)
     if (lane == 0) {
       for (int j = 0; j < n_items; ++j) {
         const i64 id = c0 + j, mt = id / p.ntiles, nt = id - mt * p.ntiles;
-        const int s = j & 1, buf = j & 1, u = int((mt - mt0) & 1);
+        const int sb = j % SB, buf = j % NA, u = int((mt - mt0) & 1);
         const int tloc = int(mt - mt0);
         const bool first = (nt == 0 || j == 0), last = (nt == p.ntiles - 1 || j == n_items - 1);
-        mbar_wait(&full[s], uint32_t((j >> 1) & 1));
+        mbar_wait(&fullb[sb], uint32_t((j / SB) & 1));
         if (first) mbar_wait(&afull[u], uint32_t((tloc >> 1) & 1));
-        if (j >= 2) mbar_wait(&acce[buf], uint32_t(((j >> 1) - 1) & 1));
+        if (j >= NA) mbar_wait(&acce[buf], uint32_t(((j / NA) - 1) & 1));
         fence_after_sync();
         const uint32_t d = tmem + G::DCOL + uint32_t(buf) * kRBN;
         const uint32_t ah = tmem + G::ACOL + uint32_t(u) * 2 * KP, al = ah + KP;
-        const uint32_t bh0 = smem_u32(smem + s * G::STAGE + G::X_BYTES), bl0 = bh0 + G::B_PLANE;
+        const uint32_t bh0 = smem_u32(bsm + sb * G::B_STAGE), bl0 = bh0 + G::B_PLANE;
 #pragma unroll
         for (int k8 = 0; k8 < KP / 8; ++k8) {
           const uint32_t off = uint32_t((k8 >> 2) * (kRBN * 128) + (k8 & 3) * 32);
@@ -513,6 +535,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
           mma_tf32_ta(d, ah + 8 * k8, bh, G::IDESC, 1u);
         }
         mma_commit(&accf[buf]);
+        mma_commit(&emptyb[sb]);
         if (last) mma_commit(&aempty[u]);
       }
     }
@@ -522,79 +545,96 @@ __global__ void __launch_bounds__(kResThreads, 1)
     const int m = qd * 32 + lane;
     const uint32_t my_lanes = tmem + tmem_lane(qd);
     double acc_r = 0.0, acc_x = 0.0;
-    for (int j = 0; j <= n_items; ++j) {
-      if (j < n_items) {
-        const i64 id = c0 + j, mt = id / p.ntiles, nt = id - mt * p.ntiles;
-        if (nt == 0 || j == 0) {  // coef rows of a new m-tile -> A slot u
-          const int tloc = int(mt - mt0), u = tloc & 1;
-          const i64 prow = mt * kRBM + m;
-          const bool valid = prow < p.P;
-          i64 dig[kResMaxOrder];
-          {
-            i64 rem = valid ? prow : 0;
-            for (int q = p.N - 2; q >= 0; --q) {
-              dig[q] = rem % p.ext[q];
-              rem /= p.ext[q];
-            }
-          }
-          if (tloc >= 2) mbar_wait(&aempty[u], uint32_t(((tloc >> 1) - 1) & 1));
-          fence_after_sync();
-#pragma unroll
-          for (int h = 0; h < KP / 32; ++h) {
-            float hi[32], lo[32];
-#pragma unroll
-            for (int rr = 0; rr < 32; ++rr) {
-              const int r = 32 * h + rr;
-              hi[rr] = (valid && r < p.R) ? p.w[r] : 0.f;
-            }
-            for (int q = p.N - 2; q >= 0; --q) {  // all 32 loads of a mode in flight together
-              const float* fq = p.f[q] + dig[q];
-              const i64 eq = p.ext[q];
-              float fv[32];
-#pragma unroll
-              for (int rr = 0; rr < 32; ++rr) fv[rr] = (32 * h + rr < p.R) ? __ldg(fq + i64(32 * h + rr) * eq) : 0.f;
-#pragma unroll
-              for (int rr = 0; rr < 32; ++rr) hi[rr] *= fv[rr];
-            }
-#pragma unroll
-            for (int rr = 0; rr < 32; ++rr) lo[rr] = hi[rr] - __uint_as_float(__float_as_uint(hi[rr]) & 0xFFFFE000u);
-            tmem_st32(my_lanes + G::ACOL + uint32_t(u) * 2 * KP + 32 * h, hi);
-            tmem_st32(my_lanes + G::ACOL + uint32_t(u) * 2 * KP + KP + 32 * h, lo);
-          }
-          tmem_st_wait();
-          fence_before_sync();
-          mbar_arrive(&afull[u]);
+    // coef rows of m-tile mt -> A slot (mt - mt0) & 1, formed one m-tile ahead
+    // of the MMA (at the first item of m-tile t: coef(t + 1)), so the MMA never
+    // waits on these gathers
+    auto form_coef = [&](i64 mt) {
+      const int tloc = int(mt - mt0), u = tloc & 1;
+      const i64 prow = mt * kRBM + m;
+      const bool valid = prow < p.P;
+      i64 dig[kResMaxOrder];
+      {
+        i64 rem = valid ? prow : 0;
+        for (int q = p.N - 2; q >= 0; --q) {
+          dig[q] = rem % p.ext[q];
+          rem /= p.ext[q];
         }
       }
-      if (j > 0) {
-        const int jj = j - 1, pb = jj & 1;
-        mbar_wait(&accf[pb], uint32_t((jj >> 1) & 1));
-        mbar_wait(&full[pb], uint32_t((jj >> 1) & 1));
-        fence_after_sync();
-        const unsigned char* xs = smem + pb * G::STAGE;
-        const uint32_t taddr = my_lanes + G::DCOL + uint32_t(pb) * kRBN;
-#pragma unroll 4
-        for (int c8 = 0; c8 < kRBN; c8 += 8) {
-          float xh[8];
-          tmem_ld8(taddr + c8, xh);
-          const unsigned char* box = xs + (c8 >> 5) * (kRBM * 128) + m * 128;
-          const int ch = (c8 & 31) >> 2;
-          const float4 x0 = *reinterpret_cast<const float4*>(box + (((ch) ^ (m & 7)) << 4));
-          const float4 x1 = *reinterpret_cast<const float4*>(box + (((ch + 1) ^ (m & 7)) << 4));
-          const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-          float sr = 0.f, sx = 0.f;  // 8-term partial sums, then fp64
+      if (tloc >= 2) mbar_wait(&aempty[u], uint32_t(((tloc >> 1) - 1) & 1));
+      fence_after_sync();
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const float dd = xv[u] - xh[u];
-            sr = fmaf(dd, dd, sr);
-            sx = fmaf(xv[u], xv[u], sx);
+      for (int h = 0; h < KP / 32; ++h) {
+        float hi[32], lo[32];
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) {
+          const int r = 32 * h + rr;
+          hi[rr] = (valid && r < p.R) ? p.w[r] : 0.f;
+        }
+        for (int q = p.N - 2; q >= 0; --q) {  // all 32 loads of a mode in flight together
+          const float* fq = p.f[q] + dig[q];
+          const i64 eq = p.ext[q];
+          float fv[32];
+#pragma unroll
+          for (int rr = 0; rr < 32; ++rr) fv[rr] = (32 * h + rr < p.R) ? __ldg(fq + i64(32 * h + rr) * eq) : 0.f;
+#pragma unroll
+          for (int rr = 0; rr < 32; ++rr) hi[rr] *= fv[rr];
+        }
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) lo[rr] = hi[rr] - __uint_as_float(__float_as_uint(hi[rr]) & 0xFFFFE000u);
+        tmem_st32(my_lanes + G::ACOL + uint32_t(u) * 2 * KP + 32 * h, hi);
+        tmem_st32(my_lanes + G::ACOL + uint32_t(u) * 2 * KP + KP + 32 * h, lo);
+      }
+      tmem_st_wait();
+      fence_before_sync();
+      mbar_arrive(&afull[u]);
+    };
+    const i64 mt_last = n_items > 0 ? (c1 - 1) / p.ntiles : mt0 - 1;
+    if (n_items > 0) {
+      form_coef(mt0);
+      if (mt0 + 1 <= mt_last) form_coef(mt0 + 1);
+    }
+    for (int j = 1; j <= n_items; ++j) {
+      if (j > 0) {
+        const int jj = j - 1, pb = jj % NA;
+        const int xsl = jj % SX;
+        mbar_wait(&accf[pb], uint32_t((jj / NA) & 1));
+        mbar_wait(&fullx[xsl], uint32_t((jj / SX) & 1));
+        fence_after_sync();
+        const unsigned char* xs = smem + xsl * G::X_BYTES;
+        const uint32_t taddr = my_lanes + G::DCOL + uint32_t(pb) * kRBN;
+        // 32 accumulator columns per TMEM load, one wait per load (not per 8 columns);
+        // the X reads of the 32-column box are issued before the wait
+#pragma unroll
+        for (int c32 = 0; c32 < kRBN; c32 += 32) {
+          uint32_t xr[32];
+          tmem_ld32_nw(taddr + c32, xr);
+          const unsigned char* box = xs + (c32 >> 5) * (kRBM * 128) + m * 128;
+          float4 xq[8];
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch) xq[ch] = *reinterpret_cast<const float4*>(box + ((ch ^ (m & 7)) << 4));
+          tmem_ld_wait();
+#pragma unroll
+          for (int c8 = 0; c8 < 32; c8 += 8) {
+            const float4 x0 = xq[c8 >> 2], x1 = xq[(c8 >> 2) + 1];
+            const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+            float sr = 0.f, sx = 0.f;  // 8-term partial sums, then fp64 (same order as before)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const float dd = xv[u] - __uint_as_float(xr[c8 + u]);
+              sr = fmaf(dd, dd, sr);
+              sx = fmaf(xv[u], xv[u], sx);
+            }
+            acc_r += double(sr);
+            acc_x += double(sx);
           }
-          acc_r += double(sr);
-          acc_x += double(sx);
         }
         fence_before_sync();
         mbar_arrive(&acce[pb]);
-        mbar_arrive(&empty[pb]);
+        mbar_arrive(&emptyx[xsl]);
+      }
+      if (j < n_items) {
+        const i64 id = c0 + j, mt = id / p.ntiles, nt = id - mt * p.ntiles;
+        if (nt == 0 && mt > mt0 && mt + 1 <= mt_last) form_coef(mt + 1);
       }
     }
 #pragma unroll
