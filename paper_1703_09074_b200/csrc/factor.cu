@@ -2259,13 +2259,18 @@ int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w
     return cudaFuncSetAttribute(plu_cluster_kernel<T, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
            cudaSuccess;
   }();
-  // When the panel needs a cluster, 8 CTAs beat the smallest cluster that fits:
-  // 1024 x 70 fp32 (C3's samples) 403 us on 2 CTAs, 290 on 4, 250 on 8, 256 on 16
-  // (tools/lu_cluster_sizes.py). RCPG_LU_MINCS overrides the smallest size tried (A/B).
+  // When the panel needs a cluster, ~128 rows per CTA (at least 8 CTAs) beat the
+  // smallest cluster that fits: 1024 x 70 fp32 (C3's samples) 403 us on 2 CTAs, 290
+  // on 4, 250 on 8, 256 on 16; 4096 x 48 fp32 354 / 239 / 195 us on 4 / 8 / 16
+  // (tools/lu_cluster_sizes.py, tools/lu_onchip_vs_cluster.py; same bits on every
+  // size). RCPG_LU_MINCS overrides the smallest size tried (A/B).
   const char* mcs = std::getenv("RCPG_LU_MINCS");
+  const int max_cs = nonportable ? 16 : 8;
+  int want_cs = 8;
+  while (want_cs < max_cs && J > 128 * i64(want_cs)) want_cs *= 2;
   const int min_cs = mcs ? std::max(1, atoi(mcs)) : 1;
-  for (int cs = 1; cs <= (nonportable ? 16 : 8) && lpath != "coop" && lpath != "resident"; cs *= 2) {
-    if (cs < min_cs || (mcs == nullptr && cs > 1 && cs < 8)) continue;
+  for (int cs = 1; cs <= max_cs && lpath != "coop" && lpath != "resident"; cs *= 2) {
+    if (cs < min_cs || (mcs == nullptr && cs > 1 && cs < want_cs)) continue;
     const int chunk = int(ceil_div(J, cs));
     const size_t smem = size_t(chunk) * n * sizeof(T) + 2 * size_t(n) * sizeof(T) + size_t(chunk) * sizeof(int) + 16;
     if (smem > (cs == 1 ? lu_lim1 : lu_lim) - 1024) continue;
