@@ -2137,8 +2137,14 @@ bool plu_resident(T* A, T* Z, i64 J, i64 R, int n, int r, const KoldaMap& km, Fa
     }
     return l;
   }();
+  // Rows per CTA: ~512 when that many CTAs are resident (71680 x 70 fp32 821 -> 715 us,
+  // 40000 x 80 fp32 921 -> 834 us), else as few CTAs as fit; fewer rows (256, 128)
+  // lose (tools/lu_resident_rows.py). RCPG_LU_RES_ROWS overrides the target (A/B).
+  const char* rr = std::getenv("RCPG_LU_RES_ROWS");
+  i64 res_rows = rr ? std::max(32, atoi(rr)) : 512;
+  if (rr == nullptr && ceil_div(J, res_rows) > nsm) res_rows = 0;
   for (int rpt = 1; rpt <= 2; ++rpt)
-    for (i64 G = std::max<i64>(1, ceil_div(J, i64(1024) * rpt)); G <= nsm; ++G) {
+    for (i64 G = std::max<i64>({i64(1), ceil_div(J, i64(1024) * rpt), res_rows ? ceil_div(J, res_rows) : 1}); G <= nsm; ++G) {
       const int chunk = int(ceil_div(J, G));
       const int nt = int(ceil_div(ceil_div(i64(chunk), rpt), 32) * 32);
       for (int i = 0; i < 6; ++i) {
