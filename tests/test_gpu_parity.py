@@ -227,6 +227,21 @@ def test_decompose_c1_parity(rcp, oracle):
     _check_fp64(model, trace, ref)
 
 
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_decompose_als_pinv_placement(rcp, oracle, split, monkeypatch):
+    """pinv(V) on CTA 0 after the MTTKRP (RCPG_ALS_SPLIT=0) or on its own CTA during it
+    (default): both meet the fp64 bar against the oracle (C1 and a 4-way tensor)."""
+    monkeypatch.setenv("RCPG_ALS_SPLIT", split)
+    x, _ = oracle.random_lowrank([100, 100, 100], 10, 1, snr=10.0, noise_seed=1)
+    g, o = cfgs(rcp, oracle, 10, 10, 2, 1)
+    model, trace = rcp.decompose(x, g)
+    _check_fp64(model, trace, oracle.decompose(x, o))
+    x, _ = oracle.random_lowrank([16, 14, 12, 10], 3, 3, snr=5.0, noise_seed=3)
+    g, o = cfgs(rcp, oracle, 3, 4, 2, 3)
+    model, trace = rcp.decompose(x, g)
+    _check_fp64(model, trace, oracle.decompose(x, o))
+
+
 def test_decompose_four_way_and_options(rcp, oracle):
     x, _ = oracle.random_lowrank([16, 14, 12, 10], 3, 3, snr=5.0, noise_seed=3)
     for kw in [dict(), dict(stab=1), dict(dist=1), dict(modes=[0, 2])]:
