@@ -11,8 +11,11 @@ and the model copied out inside the timed region.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
 
-Multi-GPU (torchrun, one process per GPU): every rank decomposes its own
-tensor (replicas), value = max over ranks.
+Multi-GPU: one process per GPU (torchrun; `--gpus N` without torchrun re-launches
+itself under torch.distributed.run with N ranks). The tensor is sharded in slabs
+along its last mode and decomposed collectively; value = the
+max over ranks of the device time. The same line carries `scaling_config`: C3
+(1024^3 fp32, BASELINE's sharded config) timed the same way at this N.
 """
 from __future__ import annotations
 
@@ -53,6 +56,52 @@ def streamed_flops(cfg) -> float:
     return total
 
 
+def workload_str(cfg) -> str:
+    """The config string both arms print (identical, so the driver's same_config holds)."""
+    return (f"{cfg.name}: {'x'.join(map(str, cfg.shape))} rank {cfg.rank} p={cfg.oversampling} "
+            f"q={cfg.power_iterations} tol={cfg.tol:g} max_iter={cfg.max_iter}")
+
+
+def fms(w1, f1, w2, f2) -> float:
+    """Factor match score: greedy |congruence| matching of components,
+    mean over components of (1 - |dlambda| / max lambda) * prod_n |a_n . b_n|."""
+    R = len(w1)
+    score = np.ones((R, R))
+    for a, b in zip(f1, f2):
+        an = a / np.maximum(np.linalg.norm(a, axis=0), 1e-300)
+        bn = b / np.maximum(np.linalg.norm(b, axis=0), 1e-300)
+        score *= np.abs(an.T.astype(np.float64) @ bn.astype(np.float64))
+    used, tot = set(), 0.0
+    for i in range(R):
+        j = next(j for j in np.argsort(-score[i]) if j not in used)
+        used.add(j)
+        lam = 1 - abs(float(w1[i]) - float(w2[j])) / max(abs(float(w1[i])), abs(float(w2[j])), 1e-300)
+        tot += lam * score[i, j]
+    return tot / R
+
+
+def parity_record(cfg, model, trace, ref) -> dict:
+    """GPU result vs the oracle on the same input (north_star bars): fp64 factors and relerr
+    within 1e-8 relative with equal iteration counts; fp32 fit within 1e-4 relative and FMS >= 0.99."""
+    fit_g = 1.0 - trace.final_relative_error ** 2
+    fit_o = 1.0 - ref.final_relative_error ** 2
+    rec = {"oracle_relerr": ref.final_relative_error, "gpu_relerr": trace.final_relative_error,
+           "oracle_iterations": ref.iterations, "gpu_iterations": trace.iterations,
+           "fit_rel_diff": abs(fit_g - fit_o) / abs(fit_o),
+           "relerr_rel_diff": abs(trace.final_relative_error - ref.final_relative_error) / ref.final_relative_error,
+           "fms": fms(model.weights, model.factors, ref.weights, ref.factors)}
+    if cfg.dtype == np.float64:
+        fd = max(float(np.linalg.norm(a.astype(np.float64) - b) / np.linalg.norm(b))
+                 for a, b in zip(model.factors, ref.factors))
+        rec["factor_rel_diff_max"] = fd
+        rec["bar"] = "fp64: factors and relerr <= 1e-8 relative, equal iterations"
+        rec["pass"] = bool(fd <= 1e-8 and rec["relerr_rel_diff"] <= 1e-8 and ref.iterations == trace.iterations)
+    else:
+        rec["bar"] = "fp32: fit <= 1e-4 relative, FMS >= 0.99"
+        rec["pass"] = bool(rec["fit_rel_diff"] <= 1e-4 and rec["fms"] >= 0.99)
+    return rec
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -66,6 +115,12 @@ def parse():
                     help="N>1: N independent decompositions instead of one sharded along the last mode")
     ap.add_argument("--shard", action="store_true",
                     help="force the sharded path (NCCL communicator) also at N = 1")
+    ap.add_argument("--no-scaling-config", action="store_true",
+                    help="skip the scaling_config (C3) sub-record")
+    ap.add_argument("--host-check", action="store_true",
+                    help="launch / process-group / max-over-ranks plumbing only (no GPU work; CPU tests)")
+    ap.add_argument("--omega-host", action="store_true",
+                    help="Omega evaluated on the host and uploaded (bit-identical; slower)")
     return ap.parse_args()
 
 
@@ -74,6 +129,19 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_cmd(gpus: int, argv) -> list:
+    """`bench.py --gpus N` outside torchrun: the same command under torch.distributed.run, N ranks."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + list(argv)
 
 
 class Dist:
@@ -218,8 +286,7 @@ def run_reference(args, dist, cfg):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64" if cfg.dtype == np.float64 else "f32", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: {'x'.join(map(str, cfg.shape))} rank {cfg.rank} p={cfg.oversampling} "
-                               f"q={cfg.power_iterations} tol={cfg.tol:g}", "parallelism": "host threads"},
+        "config": {"workload": workload_str(cfg), "parallelism": "host threads"},
         "cpu_baseline": {"value": ms, "unit": "ms", "cores": cores, "kind": "port",
                          "sample": f"full {cfg.name} decompose per step (C++ oracle restatement, "
                                    f"std::thread x{cores}, -O3)"},
@@ -229,27 +296,152 @@ def run_reference(args, dist, cfg):
     print(json.dumps(line), flush=True)
 
 
+def _oracle_cfg(oracle, c):
+    return oracle.DecomposeConfig(rank=c["rank"], tol=c["tol"], max_iter=c["max_iter"], seed=c["seed"],
+                                  compress=oracle.CompressConfig(**c["compress"]))
+
+
 def cpu_baseline(cfg, x_host, c):
+    """The oracle (C++ restatement of the reference) on the box's host cores, all threads, on
+    the downloaded input. Returns (record, oracle result) -- the result is also the parity check."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     cores = os.cpu_count() or 1
     os.environ["RCPO_THREADS"] = str(cores)
     import pyoracle as oracle
-    ocfg = oracle.DecomposeConfig(rank=c["rank"], tol=c["tol"], max_iter=c["max_iter"], seed=c["seed"],
-                                  compress=oracle.CompressConfig(**c["compress"]))
     t0 = time.perf_counter()
-    res = oracle.decompose(x_host, ocfg)
+    res = oracle.decompose(x_host, _oracle_cfg(oracle, c))
     dt = (time.perf_counter() - t0) * 1e3
-    return {"value": dt, "unit": "ms", "cores": cores, "kind": "port",
-            "sample": f"1 full {cfg.name} decompose on the downloaded input (C++ oracle, std::thread x{cores})",
-            "relerr": res.final_relative_error, "iterations": res.iterations}
+    rec = {"value": dt, "unit": "ms", "cores": cores, "kind": "port",
+           "sample": f"1 full {cfg.name} decompose on the downloaded input (C++ oracle, std::thread x{cores}, "
+                     f"-O3 no -march)",
+           "relerr": res.final_relative_error, "iterations": res.iterations}
+    return rec, res
+
+
+SINGLE_WORKER = r"""
+import os, sys, time, json
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import pyoracle as oracle
+x = np.load(sys.argv[2])
+c = json.loads(sys.argv[3])
+cfg = oracle.DecomposeConfig(rank=c["rank"], tol=c["tol"], max_iter=c["max_iter"], seed=c["seed"],
+                             compress=oracle.CompressConfig(**c["compress"]))
+t0 = time.perf_counter()
+r = oracle.decompose(x, cfg)
+print(json.dumps({"ms": (time.perf_counter() - t0) * 1e3, "relerr": r.final_relative_error,
+                  "iterations": r.iterations}))
+"""
+
+
+def cpu_baseline_single(cfg, x_host, c):
+    """Reference-faithful CPU number: the oracle with one
+    thread (the reference's build has no OpenMP / threads), in a subprocess so the thread
+    count is fresh. Only for inputs it finishes within a few minutes (C1, C2)."""
+    if x_host.nbytes > 600e6:
+        return {"value": None, "cores": 1, "skipped": "input above 600 MB: minutes of single-thread work"}
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        fn = os.path.join(d, "x.npy")
+        np.save(fn, x_host)
+        env = dict(os.environ, RCPO_THREADS="1")
+        out = subprocess.run([sys.executable, "-c", SINGLE_WORKER, os.path.join(ROOT, "oracle"), fn, json.dumps(c)],
+                             env=env, capture_output=True, text=True, timeout=600)
+    if out.returncode != 0:
+        return {"value": None, "cores": 1, "error": out.stderr[-300:]}
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    return {"value": r["ms"], "unit": "ms", "cores": 1, "kind": "port",
+            "sample": f"1 full {cfg.name} decompose, oracle with 1 thread (-O3, no -march: the reference's build)",
+            "relerr": r["relerr"], "iterations": r["iterations"]}
+
+
+def pass_roofline(pass_ms, pass_bytes, steps):
+    peak, peak_kind = measured_peaks()
+    sm_ms = sum(pass_ms.get(n, 0.0) for n in STREAMED_TIME)
+    sm_by = sum(pass_bytes.get(n, 0.0) for n in STREAMED)
+    achieved = (sm_by / 1e9) / (sm_ms / 1e3) if sm_ms > 0 else 0.0
+    return sm_ms, achieved, peak, peak_kind
+
+
+def timed_decompositions(rcp, ctx, X, dcfg, steps, warmup, dist):
+    """W untimed + K timed decompositions on the device; device time per step (max over ranks),
+    per-pass times of the timed steps, launches, the last model."""
+    for _ in range(warmup):
+        model, trace = rcp.decompose(X, dcfg, ctx=ctx)
+    ctx.synchronize()
+    dist.barrier()
+    l0 = ctx.kernel_launches()
+    pass_ms, pass_bytes = {}, {}
+    ctx.event_record(0)
+    for _ in range(steps):
+        model, trace = rcp.decompose(X, dcfg, ctx=ctx)
+    ctx.event_record(1)
+    total_ms = ctx.event_elapsed_ms(0, 1)
+    for name, ms, by in ctx.pass_timings():  # last timed step
+        pass_ms[name] = pass_ms.get(name, 0.0) + ms * steps
+        pass_bytes[name] = pass_bytes.get(name, 0.0) + by * steps
+    ctx.synchronize()
+    launches = ctx.kernel_launches() - l0
+    dist.barrier()
+    return dist.max(total_ms / steps), pass_ms, pass_bytes, launches, model, trace
+
+
+def make_tensor(rcp, synthetic, cfg, ctx, shard, world, rank):
+    w, facs = synthetic.model(cfg.kind, cfg.shape, cfg.rank, cfg.seed)
+    X = rcp.DeviceTensor.synth(cfg.shape, w, facs, cfg.snr, cfg.seed, dtype=cfg.dtype, ctx=ctx)
+    slo, shi = 0, cfg.shape[-1]
+    if shard:
+        slo, shi = rcp.slab_range(cfg.shape[-1], world, rank)
+        Xs = X.slab(slo, shi)
+        X.free()
+        X = Xs
+    return X, slo, shi
+
+
+def scaling_record(args, dist, rcp, synthetic, ctx, world, rank, shard):
+    """scaling_config: C3 (1024^3 fp32 rank 50, BASELINE's config sharded along mode 3 at
+    1/2/4/8 GPUs) device-timed at this N, with its streamed-pass roofline."""
+    from paper_1703_09074_b200.synthetic import CONFIGS
+    cfg = CONFIGS["C3"]
+    X, _, _ = make_tensor(rcp, synthetic, cfg, ctx, shard, world, rank)
+    c = configs(cfg, rcp)
+    dcfg = rcp.DecomposeConfig(rank=c["rank"], tol=c["tol"], max_iter=c["max_iter"], seed=c["seed"],
+                               compress=rcp.CompressConfig(**c["compress"]))
+    steps = max(2, min(args.steps, 5))
+    ms, pass_ms, pass_bytes, launches, model, trace = timed_decompositions(rcp, ctx, X, dcfg, steps, 1, dist)
+    X.free()
+    sm_ms, achieved, peak, peak_kind = pass_roofline(pass_ms, pass_bytes, steps)
+    return {"workload": workload_str(cfg), "metric": "rCP time-to-solution", "value": ms, "unit": "ms",
+            "n_gpus": world, "steps": steps, "warmup": 1, "higher_is_better": False,
+            "scaling": "strong" if shard else "weak",
+            "parallelism": (f"slab-sharded along the last mode over {world} GPUs (NCCL)" if shard else "single GPU"),
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak if peak else None,
+                         "kernel": "streamed mode-n passes (Omega + sketch / X^T Q / X Z / projection)",
+                         "peak_source": peak_kind},
+            "passes_ms": {n: pass_ms[n] / steps for n in pass_ms},
+            "relerr": trace.final_relative_error, "iterations": trace.iterations}
 
 
 def main():
     args = parse()
-    # stdout carries exactly one JSON line: keep NCCL's version banner off it
-    os.environ["NCCL_DEBUG"] = os.environ.get("RCPG_NCCL_DEBUG", "WARN")
     world, rank, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torch.distributed.run
+        sys.exit(subprocess.run(spawn_cmd(args.gpus, sys.argv[1:])).returncode)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (launch one rank per GPU)")
+    # stdout carries exactly one JSON line: NCCL's INFO log (communicator lines) goes to stderr
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     dist = Dist(world, rank, local)
+    if args.host_check:
+        m = dist.max(float(rank))
+        if rank == 0:
+            print(json.dumps({"host_check": True, "world": world, "max_rank": m}), flush=True)
+        dist.close()
+        return
     from paper_1703_09074_b200.synthetic import CONFIGS
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -260,49 +452,28 @@ def main():
     import paper_1703_09074_b200 as rcp
     from paper_1703_09074_b200 import synthetic
     ctx = rcp.Context(local)
+    if args.omega_host:
+        ctx.set_option("omega_host", 1)
     # N > 1: one decomposition sharded in slabs along the last mode, the
     # library's own NCCL communicator (id broadcast through torch.distributed)
     shard = (world > 1 and not args.replicas) or args.shard
     if shard:
         uid = dist.broadcast_bytes(rcp.comm_unique_id() if rank == 0 else bytes(128))
         ctx.comm_init_nccl(world, rank, uid)
-    w, facs = synthetic.model(cfg.kind, cfg.shape, cfg.rank, cfg.seed)
-    X = rcp.DeviceTensor.synth(cfg.shape, w, facs, cfg.snr, cfg.seed, dtype=cfg.dtype, ctx=ctx)
-    slo, shi = 0, cfg.shape[-1]
-    if shard:
-        slo, shi = rcp.slab_range(cfg.shape[-1], world, rank)
-        Xs = X.slab(slo, shi)
-        X.free()
-        X = Xs
+    X, slo, shi = make_tensor(rcp, synthetic, cfg, ctx, shard, world, rank)
     c = configs(cfg, rcp)
     dcfg = rcp.DecomposeConfig(rank=c["rank"], tol=c["tol"], max_iter=c["max_iter"], seed=c["seed"],
                                compress=rcp.CompressConfig(**c["compress"]))
-    for _ in range(args.warmup):
-        model, trace = rcp.decompose(X, dcfg, ctx=ctx)
-    ctx.synchronize()
-    dist.barrier()
-    l0 = ctx.kernel_launches()
-    pass_ms, pass_bytes = {}, {}
     with ClockSampler(local) as clk:
-        ctx.event_record(0)
-        for _ in range(args.steps):
-            model, trace = rcp.decompose(X, dcfg, ctx=ctx)
-        ctx.event_record(1)
-        total_ms = ctx.event_elapsed_ms(0, 1)
-    # per-pass breakdown of the last timed step (read after the timed region)
-    for name, ms, by in ctx.pass_timings():
-        pass_ms[name] = pass_ms.get(name, 0.0) + ms * args.steps
-        pass_bytes[name] = pass_bytes.get(name, 0.0) + by * args.steps
-    ctx.synchronize()
-    launches = ctx.kernel_launches() - l0
-    dist.barrier()
-    ms_step = dist.max(total_ms / args.steps)
+        ms_step, pass_ms, pass_bytes, launches, model, trace = timed_decompositions(
+            rcp, ctx, X, dcfg, args.steps, args.warmup, dist)
 
     # e2e through the C ABI with host buffers (pinned), copies inside the timed region
     e2e = None
     x_host = None
     if not args.no_e2e or (rank == 0 and world == 1 and not args.no_cpu_baseline):
         x_host = X.download()
+
     def e2e_step():
         if not shard:
             return rcp.decompose(x_host, dcfg, ctx=ctx)
@@ -327,12 +498,14 @@ def main():
         d2h = (cfg.rank + sum(cfg.shape) * cfg.rank) * np.dtype(cfg.dtype).itemsize + 2 * 8 * t2.iterations
         h2d = int(x_host.nbytes) * (world if shard else 1)  # every rank uploads its slab
         e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(d2h)}
+    X.free()
+
+    scaling = None
+    if not args.no_scaling_config and args.config != "C3":
+        scaling = scaling_record(args, dist, rcp, synthetic, ctx, world, rank, shard)
 
     if rank == 0:
-        peak, peak_kind = measured_peaks()
-        sm_ms = sum(pass_ms.get(n, 0.0) for n in STREAMED_TIME)
-        sm_by = sum(pass_bytes.get(n, 0.0) for n in STREAMED)
-        achieved = (sm_by / 1e9) / (sm_ms / 1e3) if sm_ms > 0 else 0.0
+        sm_ms, achieved, peak, peak_kind = pass_roofline(pass_ms, pass_bytes, args.steps)
         passes = {n: {"ms_per_step": pass_ms[n] / args.steps,
                       "gbs": (pass_bytes[n] / 1e9) / (pass_ms[n] / 1e3) if pass_ms[n] > 0 and pass_bytes[n] > 0
                       else None} for n in pass_ms}
@@ -342,12 +515,11 @@ def main():
             "scaling": "strong" if shard else "weak", "vs_baseline": None,
             "dtype": "f64" if cfg.dtype == np.float64 else "f32",
             "data": "synthetic (device-generated Kruskal model + add_noise, BASELINE.json shape/distribution)",
-            "config": {"workload": f"{cfg.name}: {'x'.join(map(str, cfg.shape))} rank {cfg.rank} "
-                                   f"p={cfg.oversampling} q={cfg.power_iterations} tol={cfg.tol:g} "
-                                   f"max_iter={cfg.max_iter}",
+            "config": {"workload": workload_str(cfg),
                        "parallelism": (f"slab-sharded along the last mode over {world} GPUs (NCCL)" if shard
                                        else ("replicas" if world > 1 else "single GPU")),
-                       "l2": "tensor larger than L2 (no flush needed)" if cfg.nbytes() > 126e6 else "L2-resident"},
+                       "l2": "tensor larger than L2 (no flush needed)" if cfg.nbytes() > 126e6 else "L2-resident",
+                       "omega": "host-evaluated, uploaded" if args.omega_host else "device"},
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if peak else None, "traffic": profile_traffic(cfg.name),
@@ -364,8 +536,15 @@ def main():
                                  "peak_source": "tools/microbench/fp64_peak.cu (own measurement)"}
         if e2e:
             line["e2e"] = e2e
+        if scaling:
+            line["scaling_config"] = scaling
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(cfg, x_host, c)
+            rec, ref = cpu_baseline(cfg, x_host, c)
+            rec["single_thread"] = cpu_baseline_single(cfg, x_host, c)
+            line["cpu_baseline"] = rec
+            line["parity"] = parity_record(cfg, model, trace, ref)
+            if not line["parity"]["pass"]:
+                print(f"bench.py: PARITY FAILURE vs the oracle: {json.dumps(line['parity'])}", file=sys.stderr)
         print(json.dumps(line), flush=True)
     dist.close()
 

@@ -201,6 +201,17 @@ rcpg_status rcpg_synth(rcpg_context* ctx, rcpg_dtype dtype, int32_t order, const
                        const double* weights, const double* factors, double snr, uint64_t noise_seed,
                        rcpg_tensor** out);
 rcpg_status rcpg_synchronize(rcpg_context* ctx);
+/* Context options (no counterpart in the reference; defaults keep its semantics):
+ *   "fp32_arith"  0 (default): fp32 tensors run every GEMM with fp32 operands and
+ *                 fp64 products/sums rounded once to float (the oracle's
+ *                 double-accumulated GEMMs), factorizations in the reference's
+ *                 float operation order; 1: 3xTF32 tcgen05 passes (fast, ~1e-7
+ *                 relative per pass, not bit-faithful). Env RCPG_FP32=fast sets 1.
+ *   "omega_host"  0 (default): Omega on the device (CUDA libm, a few ulp from
+ *                 glibc on ~0.1% of draws); 1: Omega evaluated on the host with
+ *                 the reference's std::log/sin/cos and uploaded (bit-identical). */
+rcpg_status rcpg_set_option(rcpg_context* ctx, const char* name, int64_t value);
+rcpg_status rcpg_get_option(const rcpg_context* ctx, const char* name, int64_t* value);
 /* Device time (CUDA events) of plu_basis (kind 0) / thin_qr (kind 1) on a
  * rows x cols device-resident panel, averaged over reps calls. */
 rcpg_status rcpg_bench_factor(rcpg_context* ctx, rcpg_dtype dtype, int32_t kind, int64_t rows, int64_t cols,

@@ -430,12 +430,13 @@ __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T
     for (int e = tid; e < R2; e += nt) A[e] = ldcg(&pm_io[e]);
     __syncthreads();
   } else {
-  // 1. V = Hadamard of the other modes' Grams (solve.hpp:209-211)
+  // 1. V = Hadamard of the other modes' Grams (solve.hpp:209-211): the
+  // reference's Scalar product chain, v = 1, then v *= G_k for k ascending
   for (int e = tid; e < R * R; e += nt) {
-    double v = 1.0;
+    T v = T(1);
     for (int k = 0; k < N; ++k)
-      if (k != mode) v *= double(fs.gram[k][e]);
-    V[e] = double(T(v));
+      if (k != mode) v = mul_rn(v, fs.gram[k][e]);
+    V[e] = double(v);
     A[e] = V[e];
   }
   if (tid == 0) s_ok = 1;
@@ -517,6 +518,10 @@ __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T
     if (tid == 0) st->pivots_fallback += 1;
     __syncthreads();
   }
+  // pinv_psd returns Matrix<Scalar> (solve.hpp:62-73): F = W pinv(V) uses
+  // the Scalar-rounded pseudo-inverse
+  for (int e = tid; e < R2; e += nt) Pm[e] = double(T(Pm[e]));
+  __syncthreads();
   if (part == 1) {
     for (int e = tid; e < R2; e += nt) pm_io[e] = Pm[e];
     return;
@@ -638,14 +643,14 @@ __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T
   __syncthreads();
   ALS_STAMP(12);
   if (mode != N - 1) return;
-  // 6. fit (solve.hpp:232-254), double accumulation
+  // 6. fit (solve.hpp:232-254), double accumulation; g = the Scalar
+  // Hadamard chain of all Grams (g = 1, g *= G_k for k ascending)
   double m2 = 0.0;
   for (int e = tid; e < R2; e += nt) {
     const int a = e % R, b = e / R;
-    double g = V[e];
-    for (int k = 0; k < N; ++k)
-      if (k != mode) g *= double(fs.gram[k][e]);
-    m2 += nr[a] * double(T(g)) * nr[b];
+    T g = T(1);
+    for (int k = 0; k < N; ++k) g = mul_rn(g, k == mode ? T(V[e]) : fs.gram[k][e]);
+    m2 += nr[a] * double(g) * nr[b];
   }
   m2 = block_reduce_sum(m2);
   double xi = 0.0;
@@ -983,7 +988,8 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
       if (g == 0) {
         double* W = sm;                   // I x R
         double* work = sm + nout;         // 3 R^2 + 4 R
-        for (int o = tid; o < nout; o += nt) W[o] = ldcg(&Wg[o]);
+        // the MTTKRP result is a Matrix<Scalar> (solve.hpp:212-213): rounded once
+        for (int o = tid; o < nout; o += nt) W[o] = double(T(ldcg(&Wg[o])));
         __syncthreads();
         if (p.prof && tid == 0) {
           g_als_prof = p.prof;

@@ -88,6 +88,16 @@ struct rcpg_context {
   // ranks of a sharded decomposition; null = unsharded
   std::unique_ptr<rcpg::Comm> comm;
   DevBuf dl_phys, dl_cand_loc, dl_cand_all, dl_U, dl_state, sh_send, sh_recv, sh_fac;
+  // fp32 arithmetic (rcpg_set_option "fp32_arith"): false = fp64 products and
+  // sums with the reference's Scalar roundings (faithful, default); true = the
+  // 3xTF32 tcgen05 passes and CholeskyQR2 (fast, ~1e-7 relative per pass)
+  bool fp32_fast = false;
+  DevBuf Q64;  // fp64 copy of a small basis (faithful fp32 passes)
+  DevBuf B64;  // fp64 copy of the compressed tensor / KR panel (faithful fp32 ALS)
+  // Omega source (rcpg_set_option "omega_host"): false = generated on the device
+  // (CUDA libm, <= a few ulp from glibc), true = generated on the host with the
+  // reference's own libm calls and uploaded (bit-identical)
+  bool omega_host = false;
 };
 
 struct rcpg_tensor {
@@ -190,7 +200,7 @@ FactorWork factor_work(rcpg_context* c, i64 rows) {
   c->cands.ensure(2 * size_t(maxb) * factor_cand_bytes());
   c->bar.ensure(sizeof(GridBarrier));
   c->info.ensure(16);
-  c->part.ensure(2 * size_t(maxb) * (kMaxPanelCols + 1) * sizeof(double));
+  c->part.ensure((2 * size_t(maxb) + 1) * (kMaxPanelCols + 1) * sizeof(double));
   c->tau.ensure(kMaxPanelCols * sizeof(double));
   c->diag.ensure(kMaxPanelCols * sizeof(double));
   FactorWork w;
@@ -199,6 +209,7 @@ FactorWork factor_work(rcpg_context* c, i64 rows) {
   w.bar = c->bar.as<GridBarrier>();
   w.info = c->info.as<int>();
   w.part = c->part.as<double>();
+  w.rowk = w.part + 2 * size_t(maxb) * (kMaxPanelCols + 1);
   w.tau = c->tau.p;
   w.diag = c->diag.p;
   w.max_blocks = maxb;
@@ -267,10 +278,41 @@ CompressCfg to_cfg(const rcpg_compress_config& c) {
   return r;
 }
 
+// Omega_n into a device panel: on the device, or (omega_host) on the host with
+// the reference's libm and uploaded. kind: 0 float, 1 double, 2 double holding
+// float-rounded values (the faithful fp32 passes).
+template <typename TS>
+void make_omega(rcpg_context* c, u64 seed, i64 mode, const KoldaMap& km, ModeView v, i64 cols, int dist, TS* P,
+                int kind, cudaStream_t st, i64 Jg = 0) {
+  if (c->omega_host) {
+    const size_t bytes = size_t(v.L * v.R) * size_t(cols) * sizeof(TS);
+    std::vector<unsigned char> h(bytes);
+    omega_host_panel(seed, mode, km, v, cols, dist, Jg, kind, h.data());
+    RCPG_CUDA(cudaMemcpyAsync(P, h.data(), bytes, cudaMemcpyHostToDevice, st));
+    RCPG_CUDA(cudaStreamSynchronize(st));  // h is pageable and local
+    return;
+  }
+  if constexpr (std::is_same<TS, double>::value) {
+    if (kind == 2) {
+      omega_panel_f32_as_f64(seed, mode, km, v, cols, dist, P, st, Jg);
+      return;
+    }
+  }
+  omega_panel<TS>(seed, mode, km, v, cols, dist, P, st, Jg);
+}
+
+// FactorWork for Scalar T: the faithful fp32 mode keeps the Householder thin_qr.
+template <typename T>
+FactorWork factor_work_t(rcpg_context* c, i64 rows) {
+  FactorWork w = factor_work(c, rows);
+  w.faithful_qr = std::is_same<T, float>::value && !c->fp32_fast;
+  return w;
+}
+
 // Stabilize an I x n sample matrix (column-major, destroyed) into out.
 template <typename T>
 int stabilize_small(rcpg_context* c, int stab, T* Y, i64 I, int n, T* out) {
-  FactorWork w = factor_work(c, I);
+  FactorWork w = factor_work_t<T>(c, I);
   const KoldaMap km = identity_kolda(I);
   if (stab == RCPG_STAB_LU) return plu_basis<T>(Y, out, I, I, n, km, w, c->st);
   return thin_qr<T>(Y, out, I, I, n, km, w, nullptr, c->st);
@@ -342,10 +384,87 @@ void run_compress(rcpg_context* c, const rcpg_tensor* t, const CompressCfg& cfg,
     T* Zp = c->panelB.as<T>();
     T* Y = c->Y.as<T>();
     T* Qy = c->Qy.as<T>();
+    if constexpr (std::is_same<T, float>::value) {
+      if (!c->fp32_fast) {
+        // Faithful fp32 (the reference's Scalar = float): every GEMM of the
+        // mode step as the oracle's gemm_nn / gemm_tn -- fp32 operands, fp64
+        // products and sums, one rounding to float -- on the FP64 tensor
+        // cores, with the panels (Omega, Z, Q) held in fp64 (exact copies of
+        // their float values). plu_basis / thin_qr run in float with the
+        // reference's operation order (factor.cu).
+        DevBuf& dst = which == 0 ? c->work0 : c->work1;
+        dst.ensure(size_t(v.L) * l * v.R * sizeof(T));
+        c->panelA.ensure(size_t(J) * l * sizeof(double));
+        c->Q64.ensure(size_t(extent) * l * sizeof(double));
+        const i64 scr64 = sketch_mixed_scratch_doubles(v, l, sms);
+        c->scratch.ensure(size_t(scr64) * sizeof(double));
+        double* P64 = c->panelA.as<double>();
+        float* Wf = c->panelB.as<float>();
+        float* Zf = dst.as<float>();  // free until the projection
+        double* Q64 = c->Q64.as<double>();
+        double* scr = c->scratch.as<double>();
+        {
+          ScopedPass sp(c, "omega", 0.0);
+          make_omega<double>(c, cfg.seed, n, km, v, l, cfg.distribution, P64, 2, c->st);
+        }
+        {
+          ScopedPass sp(c, "sketch", (S + extent * l) * b);
+          sketch_mixed(cur, v, P64, l, Y, scr, scr64, sms, c->st);
+        }
+        i64 ycols = l;
+        for (int it = 0; it < cfg.power_iterations; ++it) {
+          int rq;
+          {
+            ScopedPass sp(c, "stab_y", 2.0 * extent * ycols * b);
+            rq = stabilize_small<T>(c, cfg.stabilizer, Y, extent, int(ycols), Qy);
+          }
+          {
+            ScopedPass sp(c, "power_xtq", (S + J * rq) * b);
+            widen_f32(Qy, Q64, extent * rq, c->st);
+            project_mixed(cur, v, Q64, extent, rq, Wf, c->st);
+          }
+          int rz;
+          {
+            ScopedPass sp(c, "stab_w", 2.0 * J * rq * b);
+            FactorWork w = factor_work_t<T>(c, J);
+            if (cfg.stabilizer == RCPG_STAB_LU)
+              rz = plu_basis<T>(Wf, Zf, J, v.R, rq, km, w, c->st);
+            else
+              rz = thin_qr<T>(Wf, Zf, J, v.R, rq, km, w, nullptr, c->st);
+          }
+          {
+            ScopedPass sp(c, "power_xz", (S + J * rz + extent * rz) * b);
+            widen_f32(Zf, P64, J * rz, c->st);
+            sketch_mixed(cur, v, P64, rz, Y, scr, scr64, sms, c->st);
+          }
+          ycols = rz;
+        }
+        int qcols;
+        {
+          ScopedPass sp(c, "thin_qr", 2.0 * extent * ycols * b);
+          FactorWork w = factor_work_t<T>(c, extent);
+          basis.q.ensure(size_t(extent) * ycols * sizeof(T));
+          qcols = thin_qr<T>(Y, basis.q.as<T>(), extent, extent, int(ycols), identity_kolda(extent), w,
+                             rank_warn_slot(c, n), c->st);
+        }
+        basis.identity = false;
+        basis.cols = qcols;
+        if (qcols != l) fail_after(c, dfr, "fold: matrix dimensions do not match the target shape");
+        {
+          ScopedPass sp(c, "project", (S + l * J) * b);
+          widen_f32(basis.q.as<float>(), Q64, extent * l, c->st);
+          project_mixed(cur, v, Q64, extent, l, dst.as<float>(), c->st);
+        }
+        cur = dst.as<T>();
+        which ^= 1;
+        shape[n] = l;
+        continue;
+      }
+    }
 
     {
       ScopedPass sp(c, "omega", 0.0);
-      omega_panel<T>(cfg.seed, n, km, v, l, cfg.distribution, P, c->st);
+      make_omega<T>(c, cfg.seed, n, km, v, l, cfg.distribution, P, sizeof(T) == 4 ? 0 : 1, c->st);
     }
     {
       ScopedPass sp(c, "sketch", (S + extent * l) * b);
@@ -365,7 +484,7 @@ void run_compress(rcpg_context* c, const rcpg_tensor* t, const CompressCfg& cfg,
       int rz;
       {
         ScopedPass sp(c, "stab_w", 2.0 * J * rq * b);
-        FactorWork w = factor_work(c, J);
+        FactorWork w = factor_work_t<T>(c, J);
         const bool lu_prof = getenv("RCPG_PROFILE_LU") != nullptr;
         if (lu_prof) {
           c->als_prof.ensure(16 * sizeof(unsigned long long));
@@ -397,7 +516,7 @@ void run_compress(rcpg_context* c, const rcpg_tensor* t, const CompressCfg& cfg,
     int qcols;
     {
       ScopedPass sp(c, "thin_qr", 2.0 * extent * ycols * b);
-      FactorWork w = factor_work(c, extent);
+      FactorWork w = factor_work_t<T>(c, extent);
       basis.q.ensure(size_t(extent) * ycols * sizeof(T));
       qcols = thin_qr<T>(Y, basis.q.as<T>(), extent, extent, int(ycols), identity_kolda(extent), w,
                          rank_warn_slot(c, n), c->st);
@@ -614,7 +733,7 @@ void run_compress_sharded(rcpg_context* c, const rcpg_tensor* t, const CompressC
       c->scratch.ensure(size_t(scr) * sizeof(T));
       {
         ScopedPass sp(c, "omega", 0.0);
-        omega_panel<T>(cfg.seed, n, km, v, l, cfg.distribution, P, st, Jg);
+        make_omega<T>(c, cfg.seed, n, km, v, l, cfg.distribution, P, sizeof(T) == 4 ? 0 : 1, st, Jg);
       }
       {
         ScopedPass sp(c, "sketch", (S + extent * l) * b);
@@ -661,7 +780,7 @@ void run_compress_sharded(rcpg_context* c, const rcpg_tensor* t, const CompressC
       int qcols;
       {
         ScopedPass sp(c, "thin_qr", 2.0 * extent * ycols * b);
-        FactorWork w = factor_work(c, extent);
+        FactorWork w = factor_work_t<T>(c, extent);
         basis.q.ensure(size_t(extent) * ycols * sizeof(T));
         qcols = thin_qr<T>(Y, basis.q.as<T>(), extent, extent, int(ycols), identity_kolda(extent), w,
                            rank_warn_slot(c, n), st);
@@ -684,7 +803,7 @@ void run_compress_sharded(rcpg_context* c, const rcpg_tensor* t, const CompressC
       c->scratch.ensure(size_t(scr) * sizeof(T));
       {
         ScopedPass sp(c, "omega", 0.0);
-        omega_panel<T>(cfg.seed, n, km, v, l, cfg.distribution, P, st);
+        make_omega<T>(c, cfg.seed, n, km, v, l, cfg.distribution, P, sizeof(T) == 4 ? 0 : 1, st);
       }
       {
         ScopedPass sp(c, "sketch", (S + extent * l) * b);
@@ -705,7 +824,7 @@ void run_compress_sharded(rcpg_context* c, const rcpg_tensor* t, const CompressC
         int rz;
         {
           ScopedPass sp(c, "stab_w", 2.0 * Jn * rq * b);
-          FactorWork w = factor_work(c, Jn);
+          FactorWork w = factor_work_t<T>(c, Jn);
           rz = plu_basis<T>(P, Zp, Jn, 1, rq, km, w, st);
         }
         {
@@ -720,7 +839,7 @@ void run_compress_sharded(rcpg_context* c, const rcpg_tensor* t, const CompressC
       int qcols;
       {
         ScopedPass sp(c, "thin_qr", 2.0 * extent * ycols * b);
-        FactorWork w = factor_work(c, extent);
+        FactorWork w = factor_work_t<T>(c, extent);
         basis.q.ensure(size_t(extent) * ycols * sizeof(T));
         qcols = thin_qr<T>(Y, basis.q.as<T>(), extent, extent, int(ycols), identity_kolda(extent), w,
                            rank_warn_slot(c, n), st);
@@ -870,9 +989,25 @@ AlsHandles<T> run_als(rcpg_context* c, const T* B, const i64* shape, int order, 
       if (cfg.init == RCPG_INIT_EIGENVECTORS) {
         // Gram = B_(m) B_(m)^T as a sketch of B against itself.
         const ModeView v = mode_view(shape, order, m);
-        const i64 scr = sketch_scratch_elems<T>(v, shape[m], sms);
-        c->scratch.ensure(size_t(scr) * sizeof(T));
-        sketch<T>(B, v, B, shape[m], c->als_w.as<T>() + goff, c->scratch.as<T>(), scr, sms, c->st);
+        bool done = false;
+        if constexpr (std::is_same<T, float>::value) {
+          if (!c->fp32_fast) {  // gemm_nt of the oracle: fp64 sums, one rounding
+            if (m == 1) {
+              c->B64.ensure(size_t(S) * sizeof(double));
+              widen_f32(B, c->B64.as<double>(), S, c->st);
+            }
+            const i64 scr = sketch_mixed_scratch_doubles(v, shape[m], sms);
+            c->scratch.ensure(size_t(scr) * sizeof(double));
+            sketch_mixed(B, v, c->B64.as<double>(), shape[m], c->als_w.as<T>() + goff, c->scratch.as<double>(),
+                         scr, sms, c->st);
+            done = true;
+          }
+        }
+        if (!done) {
+          const i64 scr = sketch_scratch_elems<T>(v, shape[m], sms);
+          c->scratch.ensure(size_t(scr) * sizeof(T));
+          sketch<T>(B, v, B, shape[m], c->als_w.as<T>() + goff, c->scratch.as<T>(), scr, sms, c->st);
+        }
       }
       goff += shape[m] * shape[m];
       woff += i64(init_work_doubles(int(shape[m])));
@@ -928,9 +1063,24 @@ AlsHandles<T> run_als(rcpg_context* c, const T* B, const i64* shape, int order, 
             const ModeView v = mode_view(shape, order, m);
             const int* skip = &h.state->done;
             kr_panel<T>(h.fs, shape, m, c->als_kr.as<T>(), c->st, skip);
-            const i64 scr = sketch_scratch_elems<T>(v, R, sms);
-            c->scratch.ensure(size_t(scr) * sizeof(T));
-            sketch<T>(B, v, c->als_kr.as<T>(), R, c->als_w.as<T>(), c->scratch.as<T>(), scr, sms, c->st, skip);
+            bool done = false;
+            if constexpr (std::is_same<T, float>::value) {
+              if (!c->fp32_fast) {  // MTTKRP as the oracle's gemm_nn: fp64 sums of the Scalar KR panel
+                const i64 Jm = S / shape[m];
+                c->B64.ensure(size_t(Jm) * R * sizeof(double));
+                widen_f32(c->als_kr.as<float>(), c->B64.as<double>(), Jm * R, c->st);
+                const i64 scr = sketch_mixed_scratch_doubles(v, R, sms);
+                c->scratch.ensure(size_t(scr) * sizeof(double));
+                sketch_mixed(B, v, c->B64.as<double>(), R, c->als_w.as<T>(), c->scratch.as<double>(), scr, sms,
+                             c->st, skip);
+                done = true;
+              }
+            }
+            if (!done) {
+              const i64 scr = sketch_scratch_elems<T>(v, R, sms);
+              c->scratch.ensure(size_t(scr) * sizeof(T));
+              sketch<T>(B, v, c->als_kr.as<T>(), R, c->als_w.as<T>(), c->scratch.as<T>(), scr, sms, c->st, skip);
+            }
             als_update<T>(h.fs, m, c->als_w.as<T>(), h.weights, cfg.tol, cfg.max_iter, h.tfit, h.tsec, h.state,
                           c->als_work.as<double>(), c->st);
           }
@@ -1166,6 +1316,8 @@ rcpg_status rcpg_create(int device, rcpg_context** out) {
     RCPG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     c->bar.ensure(sizeof(GridBarrier));
     RCPG_CUDA(cudaMemset(c->bar.p, 0, sizeof(GridBarrier)));
+    const char* f32 = std::getenv("RCPG_FP32");  // "fast": 3xTF32 passes (A/B), default faithful
+    c->fp32_fast = f32 != nullptr && (std::strcmp(f32, "fast") == 0 || std::strcmp(f32, "tf32") == 0);
     c->nrm.ensure(kSlotCount * sizeof(double));
     RCPG_CUDA(cudaMallocHost(&c->hslots, kSlotCount * sizeof(double)));
     (void)device_caps();
@@ -1517,9 +1669,9 @@ rcpg_status rcpg_sketch_matrix(rcpg_context* c, rcpg_dtype dtype, uint64_t seed,
     DevBuf buf;
     buf.ensure(size_t(rows) * cols * dsize(dtype));
     if (dtype == RCPG_F64)
-      omega_panel<double>(seed, mode, km, v, cols, distribution, buf.as<double>(), c->st);
+      make_omega<double>(c, seed, mode, km, v, cols, distribution, buf.as<double>(), 1, c->st);
     else
-      omega_panel<float>(seed, mode, km, v, cols, distribution, buf.as<float>(), c->st);
+      make_omega<float>(c, seed, mode, km, v, cols, distribution, buf.as<float>(), 0, c->st);
     RCPG_CUDA(cudaMemcpyAsync(host, buf.p, size_t(rows) * cols * dsize(dtype), cudaMemcpyDeviceToHost, c->st));
     RCPG_CUDA(cudaStreamSynchronize(c->st));
     buf.release();
@@ -1594,6 +1746,7 @@ rcpg_status rcpg_thin_qr(rcpg_context* c, rcpg_dtype dtype, int64_t rows, int64_
     Q.ensure(size_t(rows) * r * b);
     RCPG_CUDA(cudaMemcpyAsync(A.p, in, size_t(rows) * cols * b, cudaMemcpyHostToDevice, c->st));
     FactorWork w = factor_work(c, rows);
+    w.faithful_qr = dtype == RCPG_F32 && !c->fp32_fast;
     if (dtype == RCPG_F64)
       thin_qr<double>(A.as<double>(), Q.as<double>(), rows, rows, int(cols), identity_kolda(rows), w, w.info + 1,
                       c->st);
@@ -1746,6 +1899,35 @@ rcpg_status rcpg_bench_factor(rcpg_context* c, rcpg_dtype dtype, int32_t kind, i
     A0.release();
     Z.release();
   });
+}
+
+rcpg_status rcpg_set_option(rcpg_context* c, const char* name, int64_t value) {
+  return guarded(c, [&] {
+    check_arg(name != nullptr, "set_option: null option name");
+    const std::string n = name;
+    if (n == "fp32_arith") {
+      check_arg(value == 0 || value == 1, "set_option: fp32_arith is 0 (faithful fp64) or 1 (fast 3xTF32)");
+      c->fp32_fast = value == 1;
+    } else if (n == "omega_host") {
+      check_arg(value == 0 || value == 1, "set_option: omega_host is 0 (device) or 1 (host upload)");
+      c->omega_host = value == 1;
+    } else {
+      check_arg(false, "set_option: unknown option '" + n + "'");
+    }
+  });
+}
+
+rcpg_status rcpg_get_option(const rcpg_context* c, const char* name, int64_t* value) {
+  if (!c || !name || !value) return RCPG_INVALID_ARGUMENT;
+  const std::string n = name;
+  if (n == "fp32_arith") {
+    *value = c->fp32_fast ? 1 : 0;
+  } else if (n == "omega_host") {
+    *value = c->omega_host ? 1 : 0;
+  } else {
+    return RCPG_INVALID_ARGUMENT;
+  }
+  return RCPG_OK;
 }
 
 rcpg_status rcpg_synchronize(rcpg_context* c) {

@@ -59,6 +59,20 @@ struct Traits<double> {
 
 __host__ __device__ inline i64 ceil_div(i64 a, i64 b) { return (a + b - 1) / b; }
 
+// x - m * u and m * u with separate roundings (no FMA contraction): the
+// elimination updates of Eigen's FullPivLU / HouseholderQR in the reference's
+// SSE2 build (no -march, so no FMA) and in the oracle (-ffp-contract=off).
+// The __*_rn intrinsics are never contracted by nvcc, so these keep the
+// GPU's factorizations bit-identical to the oracle's on any input.
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+template <typename T>
+__device__ __forceinline__ T sub_mul_rn(T x, T m, T u) { return sub_rn(x, mul_rn(m, u)); }
+
 // ---------------------------------------------------------- warp helpers
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

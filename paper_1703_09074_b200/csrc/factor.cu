@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(kSmemLuThreads) plu_cluster_kernel(const T* __
       for (int j = k + 1 + ty; j < n; j += ny) {
         const T u = U[j];
         for (int lp = lo + tx; lp < rows; lp += 32) {
-          const T x = a[lp + j * chunk] - a[lp + k * chunk] * u;
+          const T x = sub_mul_rn(a[lp + j * chunk], a[lp + k * chunk], u);
           a[lp + j * chunk] = x;
           key_better(bv, bi, T(fabs(x)), j * J + p0 + lp);
         }
@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(1024) plu_onchip_kernel(const T* __restrict__ 
 #pragma unroll 4
       for (int q = k + 1 + g; q < n; q += tpr) {
         const i64 co = i64(col_at[q]) * J;
-        const T x = a[i + co] - m * up[co];
+        const T x = sub_mul_rn(a[i + co], m, up[co]);
         a[i + co] = x;
         if (fabs(x) > rv) {
           rv = fabs(x);
@@ -565,7 +565,7 @@ __global__ void __launch_bounds__(kPpThreads) plu_pp_kernel(const T* __restrict_
           if (j == k) {
             x = m;
           } else if (j > k && upd) {
-            x = x - m * u;
+            x = sub_mul_rn(x, m, u);
             key_better(bv, bi, T(fabs(x)), j * I + i);
           }
         }
@@ -733,7 +733,7 @@ __global__ void __launch_bounds__(kLuThreads) plu_coop_kernel(LuArgs<T> p) {
       const T mprev = pend ? ldcg(&p.A[bss + s_cprev * R]) / s_pivprev : T(0);
       for (int c = threadIdx.x; c < p.n; c += blockDim.x) {
         const T st = ldcg(&p.A[bss + c * R]);
-        U[c] = pend ? st - mprev * Uprev[c] : st;
+        U[c] = pend ? sub_mul_rn(st, mprev, Uprev[c]) : st;
       }
     }
     __syncthreads();
@@ -791,7 +791,7 @@ __global__ void __launch_bounds__(kLuThreads) plu_coop_kernel(LuArgs<T> p) {
         anyact |= act[e];
         // multiplier of the pending pivot k-1, exactly as written to Z then
         m1[e] = pend && act[e] ? pvv.x[e] / pivprev : T(0);
-        const T pc = pend ? pcv.x[e] - m1[e] * Uprev[cs] : pcv.x[e];
+        const T pc = pend ? sub_mul_rn(pcv.x[e], m1[e], Uprev[cs]) : pcv.x[e];
         m[e] = act[e] ? pc / piv : T(0);
         zk.x[e] = s0 + e == ss ? T(1) : m[e];
       }
@@ -827,8 +827,8 @@ __global__ void __launch_bounds__(kLuThreads) plu_coop_kernel(LuArgs<T> p) {
 #pragma unroll
               for (int e = 0; e < V; ++e) {
                 // inactive rows are written back unchanged (same bits)
-                const T x1 = pend ? v[u].x[e] - m1[e] * up : v[u].x[e];
-                x.x[e] = act[e] ? x1 - m[e] * uc : v[u].x[e];
+                const T x1 = pend ? sub_mul_rn(v[u].x[e], m1[e], up) : v[u].x[e];
+                x.x[e] = act[e] ? sub_mul_rn(x1, m[e], uc) : v[u].x[e];
                 const T ax = fabs(x.x[e]);
                 if (act[e] && ax > rv[e]) {
                   rv[e] = ax;
@@ -1159,7 +1159,7 @@ __global__ void __launch_bounds__(lu_res_max_threads(RC, RPT), 1) plu_resident_k
 #pragma unroll
           for (int u = 0; u < NB; ++u)
             if (cc[u] < ns) {
-              const T x = xv[u] - m[i] * uc[u];
+              const T x = sub_mul_rn(xv[u], m[i], uc[u]);
               a[cc[u] * ldl + lr] = x;
               if (fabs(x) > rv[i]) {  // columns in physical order: first maximum
                 rv[i] = fabs(x);
@@ -1178,7 +1178,7 @@ __global__ void __launch_bounds__(lu_res_max_threads(RC, RPT), 1) plu_resident_k
           if (c >= n) continue;
           const int q = pcol_of[c];
           if (q <= k) continue;
-          const T x = rg[i][j] - m[i] * U[c];
+          const T x = sub_mul_rn(rg[i][j], m[i], U[c]);
           rg[i][j] = x;
           const T ax = fabs(x);
           if (ax > rv[i] || (ax == rv[i] && q < rq[i])) {
@@ -1244,6 +1244,7 @@ struct QrArgs {
   GridBarrier* bar;
   int* rank_warning;
   const int* skip;  // when non-null and *skip == 0: CholeskyQR2 already produced Q
+  double* rowk;     // [kMaxPanelCols] row k before step k's update (FactorWork::rowk)
 };
 
 template <typename T>
@@ -1286,7 +1287,7 @@ __global__ void __launch_bounds__(kFacThreads) householder_kernel(QrArgs<T> p) {
       t = T(0);
       beta = c0;
     } else {
-      beta = sqrt(c0 * c0 + tail_sq);
+      beta = sqrt(add_rn(mul_rn(c0, c0), tail_sq));
       if (c0 >= T(0)) beta = -beta;
       t = (beta - c0) / beta;
     }
@@ -1315,13 +1316,17 @@ __global__ void __launch_bounds__(kFacThreads) householder_kernel(QrArgs<T> p) {
           a2 += double(p.A[b + k * R]) * double(p.A[b + j * R]);
         }
       a2 = warp_sum(a2);
-      if (lane == 0) pb[blockIdx.x * PW + jj] = a2 + (own_k ? double(p.A[bk + j * R]) : 0.0);
+      if (lane == 0) pb[blockIdx.x * PW + jj] = a2;
     }
+    if (own_k)  // row k as it is before this step's update (read by every CTA after the barrier)
+      for (int jj = threadIdx.x; jj < ncol; jj += blockDim.x) p.rowk[jj] = double(p.A[bk + (k + 1 + jj) * R]);
     grid_sync(p.bar);
+    // tmp_j = Scalar(v_tail . A(tail, j)) + A(k, j): the dot product in double,
+    // rounded to Scalar, then one Scalar addition (the oracle's thin_qr order)
     for (int jj = threadIdx.x; jj < ncol; jj += blockDim.x) {
       double s = 0.0;
       for (int q = 0; q < G; ++q) s += ldcg(&pb[q * PW + jj]);
-      tmp[jj] = s;
+      tmp[jj] = double(add_rn(T(s), T(ldcg(&p.rowk[jj]))));
     }
     phase ^= 1;
     __syncthreads();
@@ -1331,9 +1336,16 @@ __global__ void __launch_bounds__(kFacThreads) householder_kernel(QrArgs<T> p) {
       const i64 b = row_base(s, R, p.J, p.n);
       if (kr > k) {
         const T e = p.A[b + k * R];
-        for (int jj = 0; jj < ncol; ++jj) p.A[b + (k + 1 + jj) * R] -= t * e * T(tmp[jj]);
+        const T te = mul_rn(t, e);
+        for (int jj = 0; jj < ncol; ++jj) {
+          T& x = p.A[b + (k + 1 + jj) * R];
+          x = sub_mul_rn(x, te, T(tmp[jj]));
+        }
       } else if (kr == k) {
-        for (int jj = 0; jj < ncol; ++jj) p.A[b + (k + 1 + jj) * R] -= t * T(tmp[jj]);
+        for (int jj = 0; jj < ncol; ++jj) {
+          T& x = p.A[b + (k + 1 + jj) * R];
+          x = sub_mul_rn(x, t, T(tmp[jj]));
+        }
       }
     }
   }
@@ -1370,13 +1382,15 @@ __global__ void __launch_bounds__(kFacThreads) householder_kernel(QrArgs<T> p) {
         if (p.krow[s] > k)
           a2 += double(p.A[row_base(s, R, p.J, p.n) + k * R]) * double(p.Q[row_base(s, R, p.J, p.r) + j * R]);
       a2 = warp_sum(a2);
-      if (lane == 0) pb[blockIdx.x * PW + jj] = a2 + (own_k ? double(p.Q[bqk + j * R]) : 0.0);
+      if (lane == 0) pb[blockIdx.x * PW + jj] = a2;
     }
+    if (own_k)
+      for (int jj = threadIdx.x; jj < ncol; jj += blockDim.x) p.rowk[jj] = double(p.Q[bqk + (k + jj) * R]);
     grid_sync(p.bar);
     for (int jj = threadIdx.x; jj < ncol; jj += blockDim.x) {
       double s = 0.0;
       for (int q = 0; q < G; ++q) s += ldcg(&pb[q * PW + jj]);
-      tmp[jj] = s;
+      tmp[jj] = double(add_rn(T(s), T(ldcg(&p.rowk[jj]))));
     }
     phase ^= 1;
     __syncthreads();
@@ -1385,9 +1399,16 @@ __global__ void __launch_bounds__(kFacThreads) householder_kernel(QrArgs<T> p) {
       const i64 bq = row_base(s, R, p.J, p.r);
       if (kr > k) {
         const T e = p.A[row_base(s, R, p.J, p.n) + k * R];
-        for (int jj = 0; jj < ncol; ++jj) p.Q[bq + (k + jj) * R] -= t * e * T(tmp[jj]);
+        const T te = mul_rn(t, e);
+        for (int jj = 0; jj < ncol; ++jj) {
+          T& x = p.Q[bq + (k + jj) * R];
+          x = sub_mul_rn(x, te, T(tmp[jj]));
+        }
       } else if (kr == k) {
-        for (int jj = 0; jj < ncol; ++jj) p.Q[bq + (k + jj) * R] -= t * T(tmp[jj]);
+        for (int jj = 0; jj < ncol; ++jj) {
+          T& x = p.Q[bq + (k + jj) * R];
+          x = sub_mul_rn(x, t, T(tmp[jj]));
+        }
       }
     }
     __syncthreads();
@@ -2338,7 +2359,8 @@ int thin_qr(T* A, T* Q, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w, 
   static const size_t cc_lim = enable_max_dyn_smem(cqr2_coop_kernel<T>);
   const int nb4 = 4 * cqr_nb(n);
   const char* qp = std::getenv("RCPG_QR_PATH");  // A/B testing: smem | global | coop | householder
-  const std::string path = qp ? qp : "";
+  // faithful: the Householder QR with the reference's operation order only
+  const std::string path = w.faithful_qr ? "householder" : (qp ? qp : "");
   bool done = false;
   if (R == J && kolda_identity && J >= n && w.cqr_work != nullptr && path != "smem" && path != "global" &&
       path != "householder" && (path == "coop" || J * n >= 4096)) {
@@ -2392,7 +2414,7 @@ int thin_qr(T* A, T* Q, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w, 
   const int maxc = max_coop_blocks(householder_kernel<T>, kFacThreads, 0);
   const int G = std::min(pick_grid(J, n, maxc), w.max_blocks);
   QrArgs<T> a{A,     Q,      J, R, n, r, w.keys, km, w.part, reinterpret_cast<T*>(w.tau), reinterpret_cast<T*>(w.diag),
-              w.bar, rank_warning_dev, skip};
+              w.bar, rank_warning_dev, skip, w.rowk};
   launch_coop(householder_kernel<T>, G, kFacThreads, 0, st, a);
   return r;
 }
@@ -2517,7 +2539,7 @@ __global__ void __launch_bounds__(kDluThreads) dlu_update_kernel(DluArgs<T> p, i
       if (!more) continue;
       for (int q = k + 1; q < p.n; ++q) {
         const int c = col_at[q];
-        const T x = p.A[ba + c * R] - m * U[c];
+        const T x = sub_mul_rn(p.A[ba + c * R], m, U[c]);
         p.A[ba + c * R] = x;
         const T ax = fabs(x);
         if (ax > rv) {

@@ -22,6 +22,8 @@ struct FactorWork {
   i64 cqr_rows = 0;           // largest I for the single-CTA CholeskyQR2 path
   int max_blocks = 0;
   unsigned long long* prof = nullptr;  // optional phase timers (RCPG_PROFILE_LU)
+  double* rowk = nullptr;     // [kMaxPanelCols] Householder: row k before its update
+  bool faithful_qr = false;   // thin_qr: always the faithful Householder (no CholeskyQR2)
 };
 
 size_t factor_cand_bytes();

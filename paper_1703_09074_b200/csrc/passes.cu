@@ -43,8 +43,8 @@ int pick_bn(i64 cols) {
 
 constexpr int kRedChunks = 8;
 
-template <typename T>
-__global__ void __launch_bounds__(32 * kRedChunks) reduce_partials_kernel(const T* __restrict__ part, i64 splits, i64 n, T* __restrict__ out,
+template <typename T, typename TO = T>
+__global__ void __launch_bounds__(32 * kRedChunks) reduce_partials_kernel(const T* __restrict__ part, i64 splits, i64 n, TO* __restrict__ out,
                                        const int* skip) {
   // block = 32 consecutive outputs (lanes, coalesced) x kRedChunks warps; warp w
   // sums its contiguous chunk of splits in order, warp 0 adds the chunk sums in
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(32 * kRedChunks) reduce_partials_kernel(const 
     double t = chunk_sum[0][lane];
 #pragma unroll
     for (int c = 1; c < kRedChunks; ++c) t += chunk_sum[c][lane];
-    out[e] = T(t);
+    out[e] = TO(t);
   }
 }
 
@@ -99,7 +99,105 @@ void sketch_plan(ModeView v, i64 cols, int num_sms, i64& splits, i64& tiles_per_
   splits = ceil_div(total, tiles_per_split);
 }
 
+// SIMT fallbacks of the mixed (fp32 X, fp64 panel and arithmetic) passes
+template <int BN>
+void sketch_bn_mixed(const float* X, ModeView v, const double* P, i64 cols, double* part, i64 splits,
+                     i64 tiles_per_split, i64 total, cudaStream_t st, const int* skip) {
+  constexpr int BM = TileCfg<double>::BM, BK = TileCfg<double>::BK;
+  const i64 mt = ceil_div(v.I, BM), nt = ceil_div(cols, BN);
+  dim3 grid{unsigned(mt), unsigned(splits), unsigned(nt)};
+  SketchEpilogue<double, BM, BN> ep{part, v.I, cols};
+  if (v.R > 1) {
+    SketchLoader<double, BM, BN, BK, float, double> ld{X,    P,          v.L,   v.I, v.R, cols, ceil_div(v.R, BK),
+                                                       tiles_per_split, total, skip};
+    launch_tile_gemm<double, BM, BN, BK, false>(grid, ld, ep, st);
+  } else {
+    SketchLastLoader<double, BM, BN, BK, float, double> ld{X, P, v.L, v.I, cols, tiles_per_split, total, skip};
+    launch_tile_gemm<double, BM, BN, BK, false>(grid, ld, ep, st);
+  }
+}
+
+template <int BN>
+void project_bn_mixed(const float* X, ModeView v, const double* Q, i64 ldq, i64 cols, float* O, cudaStream_t st) {
+  constexpr int BM = TileCfg<double>::BM, BK = TileCfg<double>::BK;
+  const i64 nt = ceil_div(cols, BN), kt = ceil_div(v.I, BK);
+  if (v.R > 1) {
+    for (i64 a0 = 0; a0 < v.L; a0 += 65535) {
+      const i64 na = std::min<i64>(65535, v.L - a0);
+      dim3 grid{unsigned(ceil_div(v.R, BM)), unsigned(na), unsigned(nt)};
+      const i64 off = a0 * v.I * v.R, ooff = a0 * cols * v.R;
+      ProjectLoader<double, BM, BN, BK, float, double> ld{X + off, Q, v.I, v.R, cols, ldq, kt};
+      ProjectEpilogue<double, BM, BN, float> ep{O + ooff, v.R, cols};
+      launch_tile_gemm<double, BM, BN, BK, true>(grid, ld, ep, st);
+    }
+  } else {
+    dim3 grid{unsigned(ceil_div(v.L, BM)), 1u, unsigned(nt)};
+    ProjectLastLoader<double, BM, BN, BK, float, double> ld{X, Q, v.L, v.I, cols, ldq, kt};
+    ProjectLastEpilogue<double, BM, BN, float> ep{O, v.L, cols};
+    launch_tile_gemm<double, BM, BN, BK, false>(grid, ld, ep, st);
+  }
+}
+
+__global__ void widen_kernel(const float* __restrict__ src, double* __restrict__ dst, i64 n) {
+  for (i64 i = blockIdx.x * i64(blockDim.x) + threadIdx.x; i < n; i += i64(gridDim.x) * blockDim.x)
+    dst[i] = double(src[i]);
+}
+
 }  // namespace
+
+i64 sketch_mixed_scratch_doubles(ModeView v, i64 cols, int num_sms) {
+  i64 splits = 1, tps, total;
+  sketch_plan<double>(v, cols, num_sms, splits, tps, total);
+  if (v.R > 1) splits = std::max(splits, sketch_dmma_f32_splits(v, cols, num_sms, tps, total));
+  return ceil_div(splits * cols * v.I, 4) * 4;
+}
+
+void sketch_mixed(const float* X, ModeView v, const double* P, i64 cols, float* Y, double* scratch,
+                  i64 scratch_doubles, int num_sms, cudaStream_t st, const int* skip) {
+  i64 splits = 0, tps, total;
+  bool done = false;
+  if (v.R > 1) {
+    splits = sketch_dmma_f32_splits(v, cols, num_sms, tps, total);
+    if (splits * cols * v.I > scratch_doubles) throw std::runtime_error("sketch_mixed: scratch too small");
+    done = sketch_dmma_f32(X, v, P, cols, scratch, num_sms, skip, st);
+  }
+  if (!done) {
+    sketch_plan<double>(v, cols, num_sms, splits, tps, total);
+    if (splits * cols * v.I > scratch_doubles) throw std::runtime_error("sketch_mixed: scratch too small");
+    switch (pick_bn(cols)) {
+      case 16: sketch_bn_mixed<16>(X, v, P, cols, scratch, splits, tps, total, st, skip); break;
+      case 32: sketch_bn_mixed<32>(X, v, P, cols, scratch, splits, tps, total, st, skip); break;
+      case 48: sketch_bn_mixed<48>(X, v, P, cols, scratch, splits, tps, total, st, skip); break;
+      case 64: sketch_bn_mixed<64>(X, v, P, cols, scratch, splits, tps, total, st, skip); break;
+      default: sketch_bn_mixed<80>(X, v, P, cols, scratch, splits, tps, total, st, skip); break;
+    }
+  }
+  // fp64 partials summed in a fixed order, then one rounding to fp32
+  const i64 n = cols * v.I;
+  reduce_partials_kernel<double, float><<<unsigned(ceil_div(n, 32)), 32 * kRedChunks, 0, st>>>(scratch, splits, n, Y,
+                                                                                                skip);
+  count_launch();
+  RCPG_LAUNCHED();
+}
+
+void project_mixed(const float* X, ModeView v, const double* Q, i64 ldq, i64 cols, float* O, cudaStream_t st) {
+  if (v.R > 1 && project_dmma_f32(X, v, Q, ldq, cols, O, st)) return;
+  switch (pick_bn(cols)) {
+    case 16: project_bn_mixed<16>(X, v, Q, ldq, cols, O, st); break;
+    case 32: project_bn_mixed<32>(X, v, Q, ldq, cols, O, st); break;
+    case 48: project_bn_mixed<48>(X, v, Q, ldq, cols, O, st); break;
+    case 64: project_bn_mixed<64>(X, v, Q, ldq, cols, O, st); break;
+    default: project_bn_mixed<80>(X, v, Q, ldq, cols, O, st); break;
+  }
+}
+
+void widen_f32(const float* src, double* dst, i64 n, cudaStream_t st) {
+  if (n <= 0) return;
+  const int blocks = int(std::max<i64>(1, std::min<i64>(ceil_div(n, 256), 148 * 16)));
+  widen_kernel<<<blocks, 256, 0, st>>>(src, dst, n);
+  count_launch();
+  RCPG_LAUNCHED();
+}
 
 template <typename T>
 constexpr bool use_dmma(const ModeView& v) {
@@ -153,7 +251,7 @@ void sketch(const T* X, ModeView v, const T* P, i64 cols, T* Y, T* scratch, i64 
   }
   }
   const i64 n = cols * v.I;
-  reduce_partials_kernel<T><<<unsigned(ceil_div(n, 32)), 32 * kRedChunks, 0, st>>>(scratch, splits, n, Y, skip);
+  reduce_partials_kernel<T, T><<<unsigned(ceil_div(n, 32)), 32 * kRedChunks, 0, st>>>(scratch, splits, n, Y, skip);
   count_launch();
   RCPG_LAUNCHED();
 }
@@ -206,7 +304,7 @@ void project(const T* X, ModeView v, const T* Q, i64 ldq, i64 cols, T* O, cudaSt
 
 // ---------------------------------------------------------------- Omega
 namespace {
-template <typename T>
+template <typename T, typename TV = T>
 __global__ void omega_panel_kernel(u64 s0, KoldaMap km, i64 J, i64 R, i64 cols, int distribution, T* P, i64 Jg) {
   for (i64 s = blockIdx.x * i64(blockDim.x) + threadIdx.x; s < J; s += i64(gridDim.x) * blockDim.x) {
     const i64 a = s / R, b = s - a * R;
@@ -215,7 +313,7 @@ __global__ void omega_panel_kernel(u64 s0, KoldaMap km, i64 J, i64 R, i64 cols, 
     for (i64 c = 0; c < cols; ++c) {
       const u64 e = u64(c) * u64(Jg) + u64(j);  // Jg: rows of the (global) unfolding
       const double v = distribution == 0 ? normal_at(s0, e) : uniform_sym_at(s0, e);
-      dst[c * R] = T(v);
+      dst[c * R] = T(TV(v));
     }
   }
 }
@@ -225,7 +323,7 @@ __global__ void omega_panel_kernel(u64 s0, KoldaMap km, i64 J, i64 R, i64 cols, 
 // (in panel rows) is `sig` -- so the thread owning row s (that digit even)
 // writes rows s and s + sig, both coalesced across the warp, and every pair is
 // computed once instead of twice.
-template <typename T>
+template <typename T, typename TV = T>
 __global__ void omega_pairs_kernel(u64 s0, KoldaMap km, i64 J, i64 R, i64 cols, T* P, i64 Jg, i64 sig, i64 Ef) {
   const i64 half = J / 2;
   for (i64 q = blockIdx.x * i64(blockDim.x) + threadIdx.x; q < half; q += i64(gridDim.x) * blockDim.x) {
@@ -240,16 +338,19 @@ __global__ void omega_pairs_kernel(u64 s0, KoldaMap km, i64 J, i64 R, i64 cols, 
     for (i64 c = 0; c < cols; ++c) {
       double cs, sn;
       normal_pair(s0, (u64(c) * u64(Jg) + u64(j)) >> 1, cs, sn);
-      d1[c * R] = T(cs);
-      d2[c * R] = T(sn);
+      d1[c * R] = T(TV(cs));
+      d2[c * R] = T(TV(sn));
     }
   }
 }
 }  // namespace
 
-template <typename T>
-void omega_panel(u64 seed, i64 mode, const KoldaMap& km, ModeView v, i64 cols, int distribution, T* P,
-                 cudaStream_t st, i64 J_global) {
+namespace {
+// TV: the Scalar type the reference stores Omega in (Matrix<S>, compress.hpp:120);
+// T: the panel's storage type (fp64 for the fp32 configs' faithful passes)
+template <typename T, typename TV>
+void omega_panel_impl(u64 seed, i64 mode, const KoldaMap& km, ModeView v, i64 cols, int distribution, T* P,
+                      cudaStream_t st, i64 J_global) {
   const u64 s0 = derive_seed(seed, stream_id(kDomainCompress, u64(mode)));
   const i64 J = v.L * v.R;
   const i64 Jg = J_global > 0 ? J_global : J;
@@ -271,15 +372,27 @@ void omega_panel(u64 seed, i64 mode, const KoldaMap& km, ModeView v, i64 cols, i
                      !(km.n_low == 0 && km.n_high == 1 && km.high_last_off % 2 != 0);
   if (pairs) {
     const int blocks = int(std::max<i64>(1, std::min<i64>(ceil_div(J / 2, 256), 148 * 16)));
-    omega_pairs_kernel<T><<<blocks, 256, 0, st>>>(s0, km, J, v.R, cols, P, Jg, sig, Ef);
+    omega_pairs_kernel<T, TV><<<blocks, 256, 0, st>>>(s0, km, J, v.R, cols, P, Jg, sig, Ef);
     count_launch();
     RCPG_LAUNCHED();
     return;
   }
   const int blocks = int(std::max<i64>(1, std::min<i64>(ceil_div(J, 256), 148 * 16)));
-  omega_panel_kernel<T><<<blocks, 256, 0, st>>>(s0, km, J, v.R, cols, distribution, P, Jg);
+  omega_panel_kernel<T, TV><<<blocks, 256, 0, st>>>(s0, km, J, v.R, cols, distribution, P, Jg);
   count_launch();
   RCPG_LAUNCHED();
+}
+}  // namespace
+
+template <typename T>
+void omega_panel(u64 seed, i64 mode, const KoldaMap& km, ModeView v, i64 cols, int distribution, T* P,
+                 cudaStream_t st, i64 J_global) {
+  omega_panel_impl<T, T>(seed, mode, km, v, cols, distribution, P, st, J_global);
+}
+
+void omega_panel_f32_as_f64(u64 seed, i64 mode, const KoldaMap& km, ModeView v, i64 cols, int distribution,
+                            double* P, cudaStream_t st, i64 J_global) {
+  omega_panel_impl<double, float>(seed, mode, km, v, cols, distribution, P, st, J_global);
 }
 
 #define RCPG_INST(T)                                                                                     \

@@ -127,11 +127,11 @@ __global__ void __launch_bounds__(kThreads) tile_gemm_kernel(LD ld, EP ep) {
 // ------------------------------------------------------------- sketch
 // Y = X_(n) P: partial[split][c][i] over the CTA's k tiles.
 // General mode (R > 1): k = (a, b), tiles of BK consecutive b within one a.
-template <typename T, int BM, int BN, int BK>
+template <typename T, int BM, int BN, int BK, typename TX = T, typename TP = T>
 struct SketchLoader {
   static constexpr bool A_KC = true, B_KC = true;
-  const T* X;
-  const T* P;
+  const TX* X;
+  const TP* P;
   i64 L, I, R, cols, nbt, tiles_per_split, total;
   const int* skip = nullptr;
   struct Tile {
@@ -147,20 +147,20 @@ struct SketchLoader {
   }
   __device__ T a(const Tile& tl, int k, int m) const {
     const i64 i = i64(blockIdx.x) * BM + m, b = tl.b0 + k;
-    return (i < I && b < R) ? X[(tl.a * I + i) * R + b] : T(0);
+    return (i < I && b < R) ? T(X[(tl.a * I + i) * R + b]) : T(0);
   }
   __device__ T b(const Tile& tl, int k, int n) const {
     const i64 c = i64(blockIdx.z) * BN + n, b = tl.b0 + k;
-    return (c < cols && b < R) ? P[(tl.a * cols + c) * R + b] : T(0);
+    return (c < cols && b < R) ? T(P[(tl.a * cols + c) * R + b]) : T(0);
   }
 };
 
 // Last mode (R == 1): k = a; X rows contiguous in i, P rows contiguous in c.
-template <typename T, int BM, int BN, int BK>
+template <typename T, int BM, int BN, int BK, typename TX = T, typename TP = T>
 struct SketchLastLoader {
   static constexpr bool A_KC = false, B_KC = false;
-  const T* X;
-  const T* P;
+  const TX* X;
+  const TP* P;
   i64 L, I, cols, tiles_per_split, total;
   const int* skip = nullptr;
   struct Tile {
@@ -173,11 +173,11 @@ struct SketchLastLoader {
   __device__ Tile tile(i64 t) const { return {t * BK}; }
   __device__ T a(const Tile& tl, int k, int m) const {
     const i64 i = i64(blockIdx.x) * BM + m, a = tl.a0 + k;
-    return (i < I && a < L) ? X[a * I + i] : T(0);
+    return (i < I && a < L) ? T(X[a * I + i]) : T(0);
   }
   __device__ T b(const Tile& tl, int k, int n) const {
     const i64 c = i64(blockIdx.z) * BN + n, a = tl.a0 + k;
-    return (c < cols && a < L) ? P[a * cols + c] : T(0);
+    return (c < cols && a < L) ? T(P[a * cols + c]) : T(0);
   }
 };
 
@@ -193,11 +193,11 @@ struct SketchEpilogue {
 
 // ------------------------------------------------------------ project
 // O[a, c, b] = sum_i Q[i, c] X[a, i, b]; M = b (BM), N = c (BN), K = i.
-template <typename T, int BM, int BN, int BK>
+template <typename T, int BM, int BN, int BK, typename TX = T, typename TP = T>
 struct ProjectLoader {
   static constexpr bool A_KC = false, B_KC = true;
-  const T* X;
-  const T* Q;  // column-major I x cols (ld = ldq)
+  const TX* X;
+  const TP* Q;  // column-major I x cols (ld = ldq)
   i64 I, R, cols, ldq, ktiles;
   const int* skip = nullptr;
   struct Tile {
@@ -210,30 +210,30 @@ struct ProjectLoader {
   __device__ Tile tile(i64 t) const { return {t * BK}; }
   __device__ T a(const Tile& tl, int k, int m) const {
     const i64 b = i64(blockIdx.x) * BM + m, i = tl.i0 + k, a = blockIdx.y;
-    return (b < R && i < I) ? X[(a * I + i) * R + b] : T(0);
+    return (b < R && i < I) ? T(X[(a * I + i) * R + b]) : T(0);
   }
   __device__ T b(const Tile& tl, int k, int n) const {
     const i64 c = i64(blockIdx.z) * BN + n, i = tl.i0 + k;
-    return (c < cols && i < I) ? Q[i + c * ldq] : T(0);
+    return (c < cols && i < I) ? T(Q[i + c * ldq]) : T(0);
   }
 };
 
-template <typename T, int BM, int BN>
+template <typename T, int BM, int BN, typename TO = T>
 struct ProjectEpilogue {
-  T* O;
+  TO* O;
   i64 R, cols;
   __device__ void operator()(int m, int n, T v) const {
     const i64 b = i64(blockIdx.x) * BM + m, c = i64(blockIdx.z) * BN + n, a = blockIdx.y;
-    if (b < R && c < cols) O[(a * cols + c) * R + b] = v;
+    if (b < R && c < cols) O[(a * cols + c) * R + b] = TO(v);
   }
 };
 
 // Last mode (R == 1): O[a, c] = sum_i X[a, i] Q[i, c]; M = a, N = c, K = i.
-template <typename T, int BM, int BN, int BK>
+template <typename T, int BM, int BN, int BK, typename TX = T, typename TP = T>
 struct ProjectLastLoader {
   static constexpr bool A_KC = true, B_KC = true;
-  const T* X;
-  const T* Q;
+  const TX* X;
+  const TP* Q;
   i64 L, I, cols, ldq, ktiles;
   const int* skip = nullptr;
   struct Tile {
@@ -246,21 +246,21 @@ struct ProjectLastLoader {
   __device__ Tile tile(i64 t) const { return {t * BK}; }
   __device__ T a(const Tile& tl, int k, int m) const {
     const i64 a = i64(blockIdx.x) * BM + m, i = tl.i0 + k;
-    return (a < L && i < I) ? X[a * I + i] : T(0);
+    return (a < L && i < I) ? T(X[a * I + i]) : T(0);
   }
   __device__ T b(const Tile& tl, int k, int n) const {
     const i64 c = i64(blockIdx.z) * BN + n, i = tl.i0 + k;
-    return (c < cols && i < I) ? Q[i + c * ldq] : T(0);
+    return (c < cols && i < I) ? T(Q[i + c * ldq]) : T(0);
   }
 };
 
-template <typename T, int BM, int BN>
+template <typename T, int BM, int BN, typename TO = T>
 struct ProjectLastEpilogue {
-  T* O;
+  TO* O;
   i64 L, cols;
   __device__ void operator()(int m, int n, T v) const {
     const i64 a = i64(blockIdx.x) * BM + m, c = i64(blockIdx.z) * BN + n;
-    if (a < L && c < cols) O[a * cols + c] = v;
+    if (a < L && c < cols) O[a * cols + c] = TO(v);
   }
 };
 
@@ -280,11 +280,28 @@ void project(const T* X, ModeView v, const T* Q, i64 ldq, i64 cols, T* O, cudaSt
 
 // 128-byte CUtensorMap (opaque here) for an fp64 (d0, d1, d2) view, box {16, b1, 1}, 128B swizzle.
 void tensor_map_f64_3d(void* out, const double* base, i64 d0, i64 d1, i64 d2, int b1, i64 pitch = 0);
+// fp32 (d0, d1, d2) view, box {16, b1, 1}, 64B swizzle (fp32 X of the fp64-arithmetic passes).
+void tensor_map_f32_3d_sw64(void* out, const float* base, i64 d0, i64 d1, i64 d2, int b1, i64 pitch = 0);
 // FP64 tensor-core (DMMA) versions for mode views with R > 1 (passes_dmma.cu).
 i64 sketch_dmma_splits(ModeView v, i64 cols, int num_sms, i64& tps, i64& total);
 void sketch_dmma(const double* X, ModeView v, const double* P, i64 cols, double* part, int num_sms,
                  const int* skip, cudaStream_t st);
 void project_dmma(const double* X, ModeView v, const double* Q, i64 ldq, i64 cols, double* O, cudaStream_t st);
+// fp32 X with fp64 products and sums (the fp32 configs' faithful passes); false
+// when the view does not suit the TMA kernels (the caller takes the SIMT path).
+i64 sketch_dmma_f32_splits(ModeView v, i64 cols, int num_sms, i64& tps, i64& total);
+bool sketch_dmma_f32(const float* X, ModeView v, const double* P, i64 cols, double* part, int num_sms,
+                     const int* skip, cudaStream_t st);
+bool project_dmma_f32(const float* X, ModeView v, const double* Q, i64 ldq, i64 cols, float* O, cudaStream_t st);
+// Mixed passes of the faithful fp32 path: X fp32, panel fp64, fp64 accumulation,
+// one rounding of each result to fp32 (Y [I x cols] column-major, O in the
+// (a, c, b) layout). scratch: sketch_mixed_scratch_doubles().
+i64 sketch_mixed_scratch_doubles(ModeView v, i64 cols, int num_sms);
+void sketch_mixed(const float* X, ModeView v, const double* P, i64 cols, float* Y, double* scratch,
+                  i64 scratch_doubles, int num_sms, cudaStream_t st, const int* skip = nullptr);
+void project_mixed(const float* X, ModeView v, const double* Q, i64 ldq, i64 cols, float* O, cudaStream_t st);
+// dst[i] = double(src[i]) (exact)
+void widen_f32(const float* src, double* dst, i64 n, cudaStream_t st);
 
 // FP32 tcgen05 (3xTF32, TMEM accumulator) versions for mode views with R > 1
 // (passes_tc.cu). RCPG_NO_TC=1 in the environment routes fp32 to the SIMT
@@ -313,5 +330,12 @@ void residual_tc(const float* X, const i64* shape, int order, const float* const
 template <typename T>
 void omega_panel(u64 seed, i64 mode, const KoldaMap& km, ModeView v, i64 cols, int distribution, T* P,
                  cudaStream_t st, i64 J_global = 0);
+// Omega generated on the host with the reference's libm (omega_host.cu);
+// out_kind 0 float, 1 double, 2 double holding the float-rounded value.
+void omega_host_panel(u64 seed, i64 mode, const KoldaMap& km, ModeView v, i64 cols, int distribution, i64 Jg,
+                      int out_kind, void* host_out);
+// Omega rounded to fp32 (the fp32 configs' Matrix<float> Omega) stored as fp64.
+void omega_panel_f32_as_f64(u64 seed, i64 mode, const KoldaMap& km, ModeView v, i64 cols, int distribution,
+                            double* P, cudaStream_t st, i64 J_global = 0);
 
 }  // namespace rcpg

@@ -237,23 +237,33 @@ __global__ void __launch_bounds__(kDThreads) project_dmma_kernel(const double* _
 constexpr int kTmaWM = 4;      // consumer warps, 16 rows each
 constexpr int kTmaStages = 4;  // 4 stages: four CTAs per SM at BN = 32
 
-template <int BN>
+// TX = element type of X in HBM: double (128-byte box rows, 128B swizzle) or
+// float (64-byte box rows, 64B swizzle; the fp32 configs' faithful passes,
+// converted to fp64 when a fragment is loaded). The panel is always fp64.
+template <int BN, typename TX = double>
 struct TmaPlan {
-  static constexpr int BM = kTmaWM * 16, ABYTES = BM * 128, BBYTES = BN * 128, STAGE = ABYTES + BBYTES;
+  static constexpr int BM = kTmaWM * 16, ABYTES = BM * 16 * int(sizeof(TX)), BBYTES = BN * 128,
+                       STAGE = ABYTES + BBYTES;
   static constexpr int SMEM = kTmaStages * STAGE + 1024;  // + 1024 B alignment slack (swizzle atoms)
   static constexpr int THREADS = (kTmaWM + 1) * 32;
 };
 
 // element (r, k) of a 128B-swizzled box with 16-double rows
 __device__ __forceinline__ int swz16(int r, int k) { return r * 16 + ((((k >> 1) ^ (r & 7))) << 1) + (k & 1); }
+// element (r, k) of a 64B-swizzled box with 16-float rows (16-byte chunk k / 4
+// XOR bits 7-8 of the row's byte offset): the 8 rows x 4 k of a fragment load
+// hit 32 distinct banks
+__device__ __forceinline__ int swz16f(int r, int k) { return r * 16 + ((((k >> 2) ^ ((r >> 1) & 3))) << 2) + (k & 3); }
+__device__ __forceinline__ double ldsx(const double* A, int r, int k) { return A[swz16(r, k)]; }
+__device__ __forceinline__ double ldsx(const float* A, int r, int k) { return double(A[swz16f(r, k)]); }
 
-template <int BN>
-__global__ void __launch_bounds__(TmaPlan<BN>::THREADS) sketch_dmma_tma_kernel(const __grid_constant__ CUtensorMap mx,
+template <int BN, typename TX>
+__global__ void __launch_bounds__(TmaPlan<BN, TX>::THREADS) sketch_dmma_tma_kernel(const __grid_constant__ CUtensorMap mx,
                                                                                const __grid_constant__ CUtensorMap mp,
                                                                                i64 I, i64 cols, i64 nbt, i64 tps,
                                                                                i64 total, double* __restrict__ part,
                                                                                const int* skip) {
-  using G = TmaPlan<BN>;
+  using G = TmaPlan<BN, TX>;
   using namespace tc;
   constexpr int NT = BN / 8, S = kTmaStages;
   if (skip != nullptr && *skip) return;
@@ -295,12 +305,12 @@ __global__ void __launch_bounds__(TmaPlan<BN>::THREADS) sketch_dmma_tma_kernel(c
   for (int kt = 0; kt < nk; ++kt) {
     const int s = kt % S;
     mbar_wait(&full[s], uint32_t((kt / S) & 1));
-    const double* A = reinterpret_cast<const double*>(smem + s * G::STAGE);
+    const TX* A = reinterpret_cast<const TX*>(smem + s * G::STAGE);
     const double* B = reinterpret_cast<const double*>(smem + s * G::STAGE + G::ABYTES);
 #pragma unroll
     for (int kk = 0; kk < 16; kk += 4) {
-      const double a0 = A[swz16(r0, kk + t)];
-      const double a1 = A[swz16(r0 + 8, kk + t)];
+      const double a0 = ldsx(A, r0, kk + t);
+      const double a1 = ldsx(A, r0 + 8, kk + t);
 #pragma unroll
       for (int j = 0; j < NT; ++j) dmma(acc[j], a0, a1, B[swz16(j * 8 + g, kk + t)]);
     }
@@ -324,12 +334,12 @@ __global__ void __launch_bounds__(TmaPlan<BN>::THREADS) sketch_dmma_tma_kernel(c
 // ---------------------------------------------------- project, TMA-fed
 // O[a, c, b] = sum_i X[a, i, b] Q[i, c]: M = b (four 16-wide boxes of X per
 // stage, one per consumer warp), N = c, K = i (16 per stage), no split.
-template <int BN>
-__global__ void __launch_bounds__(TmaPlan<BN>::THREADS) project_dmma_tma_kernel(const __grid_constant__ CUtensorMap mx,
+template <int BN, typename TX, typename TO>
+__global__ void __launch_bounds__(TmaPlan<BN, TX>::THREADS) project_dmma_tma_kernel(const __grid_constant__ CUtensorMap mx,
                                                                                 const __grid_constant__ CUtensorMap mq,
                                                                                 i64 I, i64 R, i64 cols, int a_base,
-                                                                                double* __restrict__ O) {
-  using G = TmaPlan<BN>;
+                                                                                TO* __restrict__ O) {
+  using G = TmaPlan<BN, TX>;
   using namespace tc;
   constexpr int NT = BN / 8, S = kTmaStages;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -356,7 +366,8 @@ __global__ void __launch_bounds__(TmaPlan<BN>::THREADS) project_dmma_tma_kernel(
         mbar_arrive_tx(&full[s], G::STAGE);
         unsigned char* st = smem + s * G::STAGE;
 #pragma unroll
-        for (int q = 0; q < kTmaWM; ++q) tma_load_3d(st + q * 2048, &mx, b0 + 16 * q, kt * 16, a, &full[s]);
+        for (int q = 0; q < kTmaWM; ++q)
+          tma_load_3d(st + q * 256 * int(sizeof(TX)), &mx, b0 + 16 * q, kt * 16, a, &full[s]);
         tma_load_3d(st + G::ABYTES, &mq, kt * 16, n0, 0, &full[s]);
       }
     }
@@ -369,12 +380,12 @@ __global__ void __launch_bounds__(TmaPlan<BN>::THREADS) project_dmma_tma_kernel(
   for (int kt = 0; kt < nk; ++kt) {
     const int s = kt % S;
     mbar_wait(&full[s], uint32_t((kt / S) & 1));
-    const double* A = reinterpret_cast<const double*>(smem + s * G::STAGE) + w * 256;  // box of this warp's b's
+    const TX* A = reinterpret_cast<const TX*>(smem + s * G::STAGE) + w * 256;  // box of this warp's b's
     const double* B = reinterpret_cast<const double*>(smem + s * G::STAGE + G::ABYTES);
 #pragma unroll
     for (int kk = 0; kk < 16; kk += 4) {
-      const double a0 = A[swz16(kk + t, g)];
-      const double a1 = A[swz16(kk + t, g + 8)];
+      const double a0 = ldsx(A, kk + t, g);
+      const double a1 = ldsx(A, kk + t, g + 8);
 #pragma unroll
       for (int j = 0; j < NT; ++j) dmma(acc[j], a0, a1, B[swz16(j * 8 + g, kk + t)]);
     }
@@ -382,26 +393,26 @@ __global__ void __launch_bounds__(TmaPlan<BN>::THREADS) project_dmma_tma_kernel(
     if (lane == 0) mbar_arrive(&empty[s]);
   }
   const i64 bb = b0 + w * 16 + g;
-  double* Oa = O + i64(blockIdx.y) * cols * R;
+  TO* Oa = O + i64(blockIdx.y) * cols * R;
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
     const i64 c0 = n0 + j * 8 + 2 * t;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const i64 b = bb + (q >> 1) * 8, c = c0 + (q & 1);
-      if (b < R && c < cols) Oa[c * R + b] = acc[j][q];
+      if (b < R && c < cols) Oa[c * R + b] = TO(acc[j][q]);
     }
   }
 }
 
-template <int BN>
+template <int BN, typename TX = double>
 int tma_ctas_per_sm() {
   static const int per = [] {
-    const size_t lim = enable_max_dyn_smem(sketch_dmma_tma_kernel<BN>);
-    if (size_t(TmaPlan<BN>::SMEM) > lim) return 0;
+    const size_t lim = enable_max_dyn_smem(sketch_dmma_tma_kernel<BN, TX>);
+    if (size_t(TmaPlan<BN, TX>::SMEM) > lim) return 0;
     int n = 0;
-    RCPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sketch_dmma_tma_kernel<BN>, TmaPlan<BN>::THREADS,
-                                                            TmaPlan<BN>::SMEM));
+    RCPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sketch_dmma_tma_kernel<BN, TX>,
+                                                            TmaPlan<BN, TX>::THREADS, TmaPlan<BN, TX>::SMEM));
     return n;
   }();
   return per;
@@ -442,30 +453,34 @@ void launch_project(dim3 grid, const double* X, const double* Q, ModeView v, i64
 }  // namespace
 
 namespace {
+// TMA needs 16-byte row pitches: R even for fp64 X, R % 4 == 0 for fp32 X
+template <typename TX>
 bool tma_sketch_shape_ok(ModeView v, i64 cols) {
   constexpr i64 kMax = (i64(1) << 31) - 1;
-  return v.R % 2 == 0 && v.R <= kMax && v.I <= kMax && v.L <= kMax && cols <= kMax &&
+  constexpr i64 vec = 16 / i64(sizeof(TX));
+  return v.R % vec == 0 && v.R <= kMax && v.I <= kMax && v.L <= kMax && cols <= kMax &&
          std::getenv("RCPG_DMMA_CPASYNC") == nullptr;
 }
 
+template <typename TX>
 int tma_per_sm(int bn) {
   switch (bn) {
-    case 16: return tma_ctas_per_sm<16>();
-    case 32: return tma_ctas_per_sm<32>();
-    case 48: return tma_ctas_per_sm<48>();
-    case 64: return tma_ctas_per_sm<64>();
-    default: return tma_ctas_per_sm<80>();
+    case 16: return tma_ctas_per_sm<16, TX>();
+    case 32: return tma_ctas_per_sm<32, TX>();
+    case 48: return tma_ctas_per_sm<48, TX>();
+    case 64: return tma_ctas_per_sm<64, TX>();
+    default: return tma_ctas_per_sm<80, TX>();
   }
 }
-}  // namespace
 
-i64 sketch_dmma_splits(ModeView v, i64 cols, int num_sms, i64& tps, i64& total) {
+template <typename TX>
+i64 sketch_dmma_splits_t(ModeView v, i64 cols, int num_sms, i64& tps, i64& total) {
   const int bn = pick_bn8(cols);
   total = v.L * ceil_div(v.R, kDBK);
   i64 mt, per_sm;
-  if (tma_sketch_shape_ok(v, cols) && tma_per_sm(bn) > 0) {
+  if (tma_sketch_shape_ok<TX>(v, cols) && tma_per_sm<TX>(bn) > 0) {
     mt = ceil_div(v.I, i64(kTmaWM * 16));
-    per_sm = tma_per_sm(bn);
+    per_sm = tma_per_sm<TX>(bn);
   } else {
     // residency from the smem plan, capped by registers: ~80 per thread x 128 threads
     mt = ceil_div(v.I, kDBM);
@@ -483,39 +498,88 @@ i64 sketch_dmma_splits(ModeView v, i64 cols, int num_sms, i64& tps, i64& total) 
   return ceil_div(total, tps);
 }
 
-namespace {
-template <int BN>
-void launch_sketch_tma(const double* X, ModeView v, const double* P, i64 cols, i64 tps, i64 total, i64 splits,
+void tensor_map_x(void* out, const double* X, ModeView v, int b1) { tensor_map_f64_3d(out, X, v.R, v.I, v.L, b1); }
+void tensor_map_x(void* out, const float* X, ModeView v, int b1) { tensor_map_f32_3d_sw64(out, X, v.R, v.I, v.L, b1); }
+
+template <int BN, typename TX>
+void launch_sketch_tma(const TX* X, ModeView v, const double* P, i64 cols, i64 tps, i64 total, i64 splits,
                        double* part, const int* skip, cudaStream_t st) {
+  using G = TmaPlan<BN, TX>;
+  static const size_t lim = enable_max_dyn_smem(sketch_dmma_tma_kernel<BN, TX>);
+  if (size_t(G::SMEM) > lim) throw std::runtime_error("sketch_dmma_tma: smem plan too large");
   alignas(64) unsigned char mx[128], mp[128];
-  tensor_map_f64_3d(mx, X, v.R, v.I, v.L, kTmaWM * 16);
+  tensor_map_x(mx, X, v, kTmaWM * 16);
   tensor_map_f64_3d(mp, P, v.R, cols, v.L, BN);
   dim3 grid{unsigned(ceil_div(v.I, i64(kTmaWM * 16))), unsigned(splits), unsigned(ceil_div(cols, i64(BN)))};
-  sketch_dmma_tma_kernel<BN><<<grid, TmaPlan<BN>::THREADS, TmaPlan<BN>::SMEM, st>>>(
+  sketch_dmma_tma_kernel<BN, TX><<<grid, G::THREADS, G::SMEM, st>>>(
       *reinterpret_cast<const CUtensorMap*>(mx), *reinterpret_cast<const CUtensorMap*>(mp), v.I, cols,
       ceil_div(v.R, kDBK), tps, total, part, skip);
   count_launch();
   RCPG_LAUNCHED();
 }
+
+template <typename TX>
+bool sketch_tma_dispatch(const TX* X, ModeView v, const double* P, i64 cols, double* part, i64 tps, i64 total,
+                         i64 splits, const int* skip, cudaStream_t st) {
+  const int BN = pick_bn8(cols);
+  const bool aligned = reinterpret_cast<uintptr_t>(X) % 16 == 0 && reinterpret_cast<uintptr_t>(P) % 16 == 0;
+  if (!(tma_sketch_shape_ok<TX>(v, cols) && aligned && tma_per_sm<TX>(BN) > 0)) return false;
+  switch (BN) {
+    case 16: launch_sketch_tma<16, TX>(X, v, P, cols, tps, total, splits, part, skip, st); break;
+    case 32: launch_sketch_tma<32, TX>(X, v, P, cols, tps, total, splits, part, skip, st); break;
+    case 48: launch_sketch_tma<48, TX>(X, v, P, cols, tps, total, splits, part, skip, st); break;
+    case 64: launch_sketch_tma<64, TX>(X, v, P, cols, tps, total, splits, part, skip, st); break;
+    default: launch_sketch_tma<80, TX>(X, v, P, cols, tps, total, splits, part, skip, st); break;
+  }
+  return true;
+}
+
+template <int BN, typename TX, typename TO>
+void launch_project_tma(const TX* X, ModeView v, const double* Q, i64 ldq, i64 cols, TO* O, cudaStream_t st) {
+  using G = TmaPlan<BN, TX>;
+  static const size_t lim = enable_max_dyn_smem(project_dmma_tma_kernel<BN, TX, TO>);
+  if (size_t(G::SMEM) > lim) throw std::runtime_error("project_dmma_tma: smem plan too large");
+  alignas(64) unsigned char mx[128], mq[128];
+  tensor_map_x(mx, X, v, 16);
+  tensor_map_f64_3d(mq, Q, v.I, cols, 1, BN, ldq);  // Q column-major: i fastest (pitch ldq), c; rows >= I read as 0
+  for (i64 a0 = 0; a0 < v.L; a0 += 65535) {
+    const i64 na = std::min<i64>(65535, v.L - a0);
+    dim3 grid{unsigned(ceil_div(v.R, i64(kTmaWM * 16))), unsigned(na), unsigned(ceil_div(cols, i64(BN)))};
+    project_dmma_tma_kernel<BN, TX, TO><<<grid, G::THREADS, G::SMEM, st>>>(
+        *reinterpret_cast<const CUtensorMap*>(mx), *reinterpret_cast<const CUtensorMap*>(mq), v.I, v.R, cols,
+        int(a0), O + a0 * cols * v.R);
+    count_launch();
+    RCPG_LAUNCHED();
+  }
+}
+
+template <typename TX, typename TO>
+bool project_tma_dispatch(const TX* X, ModeView v, const double* Q, i64 ldq, i64 cols, TO* O, cudaStream_t st) {
+  const int BN = pick_bn8(cols);
+  const bool aligned = reinterpret_cast<uintptr_t>(X) % 16 == 0 && reinterpret_cast<uintptr_t>(Q) % 16 == 0;
+  if (!(tma_sketch_shape_ok<TX>(v, cols) && ldq % 2 == 0 && ldq >= v.I && aligned)) return false;
+  switch (BN) {
+    case 16: launch_project_tma<16, TX, TO>(X, v, Q, ldq, cols, O, st); break;
+    case 32: launch_project_tma<32, TX, TO>(X, v, Q, ldq, cols, O, st); break;
+    case 48: launch_project_tma<48, TX, TO>(X, v, Q, ldq, cols, O, st); break;
+    case 64: launch_project_tma<64, TX, TO>(X, v, Q, ldq, cols, O, st); break;
+    default: launch_project_tma<80, TX, TO>(X, v, Q, ldq, cols, O, st); break;
+  }
+  return true;
+}
 }  // namespace
+
+i64 sketch_dmma_splits(ModeView v, i64 cols, int num_sms, i64& tps, i64& total) {
+  return sketch_dmma_splits_t<double>(v, cols, num_sms, tps, total);
+}
 
 void sketch_dmma(const double* X, ModeView v, const double* P, i64 cols, double* part, int num_sms, const int* skip,
                  cudaStream_t st) {
   i64 tps, total;
   const i64 splits = sketch_dmma_splits(v, cols, num_sms, tps, total);
+  if (sketch_tma_dispatch<double>(X, v, P, cols, part, tps, total, splits, skip, st)) return;
   const int BN = pick_bn8(cols);
   const i64 nbt = ceil_div(v.R, kDBK);
-  const bool aligned = reinterpret_cast<uintptr_t>(X) % 16 == 0 && reinterpret_cast<uintptr_t>(P) % 16 == 0;
-  if (tma_sketch_shape_ok(v, cols) && aligned && tma_per_sm(BN) > 0) {
-    switch (BN) {
-      case 16: launch_sketch_tma<16>(X, v, P, cols, tps, total, splits, part, skip, st); break;
-      case 32: launch_sketch_tma<32>(X, v, P, cols, tps, total, splits, part, skip, st); break;
-      case 48: launch_sketch_tma<48>(X, v, P, cols, tps, total, splits, part, skip, st); break;
-      case 64: launch_sketch_tma<64>(X, v, P, cols, tps, total, splits, part, skip, st); break;
-      default: launch_sketch_tma<80>(X, v, P, cols, tps, total, splits, part, skip, st); break;
-    }
-    return;
-  }
   dim3 grid{unsigned(ceil_div(v.I, kDBM)), unsigned(splits), unsigned(ceil_div(cols, BN))};
   const bool v16 = (v.R % 2 == 0);
 #define RCPG_SK(BNV)                                                                              \
@@ -536,40 +600,9 @@ void sketch_dmma(const double* X, ModeView v, const double* P, i64 cols, double*
 #undef RCPG_SK
 }
 
-namespace {
-template <int BN>
-void launch_project_tma(const double* X, ModeView v, const double* Q, i64 ldq, i64 cols, double* O,
-                        cudaStream_t st) {
-  static const size_t lim = enable_max_dyn_smem(project_dmma_tma_kernel<BN>);
-  if (size_t(TmaPlan<BN>::SMEM) > lim) throw std::runtime_error("project_dmma_tma: smem plan too large");
-  alignas(64) unsigned char mx[128], mq[128];
-  tensor_map_f64_3d(mx, X, v.R, v.I, v.L, 16);
-  tensor_map_f64_3d(mq, Q, v.I, cols, 1, BN, ldq);  // Q column-major: i fastest (pitch ldq), c; rows >= I read as 0
-  for (i64 a0 = 0; a0 < v.L; a0 += 65535) {
-    const i64 na = std::min<i64>(65535, v.L - a0);
-    dim3 grid{unsigned(ceil_div(v.R, i64(kTmaWM * 16))), unsigned(na), unsigned(ceil_div(cols, i64(BN)))};
-    project_dmma_tma_kernel<BN><<<grid, TmaPlan<BN>::THREADS, TmaPlan<BN>::SMEM, st>>>(
-        *reinterpret_cast<const CUtensorMap*>(mx), *reinterpret_cast<const CUtensorMap*>(mq), v.I, v.R, cols,
-        int(a0), O + a0 * cols * v.R);
-    count_launch();
-    RCPG_LAUNCHED();
-  }
-}
-}  // namespace
-
 void project_dmma(const double* X, ModeView v, const double* Q, i64 ldq, i64 cols, double* O, cudaStream_t st) {
+  if (project_tma_dispatch<double, double>(X, v, Q, ldq, cols, O, st)) return;
   const int BN = pick_bn8(cols);
-  const bool aligned = reinterpret_cast<uintptr_t>(X) % 16 == 0 && reinterpret_cast<uintptr_t>(Q) % 16 == 0;
-  if (tma_sketch_shape_ok(v, cols) && ldq % 2 == 0 && ldq >= v.I && aligned) {
-    switch (BN) {
-      case 16: launch_project_tma<16>(X, v, Q, ldq, cols, O, st); break;
-      case 32: launch_project_tma<32>(X, v, Q, ldq, cols, O, st); break;
-      case 48: launch_project_tma<48>(X, v, Q, ldq, cols, O, st); break;
-      case 64: launch_project_tma<64>(X, v, Q, ldq, cols, O, st); break;
-      default: launch_project_tma<80>(X, v, Q, ldq, cols, O, st); break;
-    }
-    return;
-  }
   const bool va = (v.R % 2 == 0), vb = (ldq % 2 == 0);
   for (i64 a0 = 0; a0 < v.L; a0 += 65535) {
     const i64 na = std::min<i64>(65535, v.L - a0);
@@ -595,6 +628,26 @@ void project_dmma(const double* X, ModeView v, const double* Q, i64 ldq, i64 col
     }
 #undef RCPG_PJ
   }
+}
+
+// ------------------------------------------------ fp32 X, fp64 arithmetic
+// The fp32 configs' faithful passes: X stays fp32 in HBM, every product and
+// sum is fp64 (DMMA), so the Scalar-rounded results equal the oracle's
+// double-accumulated GEMMs (the checker's gemm_nn / gemm_tn) except where
+// the exact sum lies within fp64 rounding of a float rounding boundary.
+i64 sketch_dmma_f32_splits(ModeView v, i64 cols, int num_sms, i64& tps, i64& total) {
+  return sketch_dmma_splits_t<float>(v, cols, num_sms, tps, total);
+}
+
+bool sketch_dmma_f32(const float* X, ModeView v, const double* P, i64 cols, double* part, int num_sms,
+                     const int* skip, cudaStream_t st) {
+  i64 tps, total;
+  const i64 splits = sketch_dmma_f32_splits(v, cols, num_sms, tps, total);
+  return sketch_tma_dispatch<float>(X, v, P, cols, part, tps, total, splits, skip, st);
+}
+
+bool project_dmma_f32(const float* X, ModeView v, const double* Q, i64 ldq, i64 cols, float* O, cudaStream_t st) {
+  return project_tma_dispatch<float, float>(X, v, Q, ldq, cols, O, st);
 }
 
 }  // namespace rcpg

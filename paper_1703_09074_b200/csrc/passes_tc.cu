@@ -718,6 +718,21 @@ void tensor_map_f64_3d(void* out, const double* base, i64 d0, i64 d1, i64 d2, in
   if (r != CUDA_SUCCESS) throw CudaFailure("cuTensorMapEncodeTiled (f64) failed (" + std::to_string(int(r)) + ")", cudaErrorInvalidValue);
 }
 
+void tensor_map_f32_3d_sw64(void* out, const float* base, i64 d0, i64 d1, i64 d2, int b1, i64 pitch) {
+  if (pitch <= 0) pitch = d0;
+  const cuuint64_t dims[3] = {cuuint64_t(d0), cuuint64_t(d1), cuuint64_t(d2)};
+  const cuuint64_t strides[2] = {cuuint64_t(pitch) * 4, cuuint64_t(pitch * d1) * 4};
+  const cuuint32_t box[3] = {16, cuuint32_t(b1), 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = encode_tiled()(static_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                                    const_cast<float*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                    CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw CudaFailure("cuTensorMapEncodeTiled (f32, 64B swizzle) failed (" + std::to_string(int(r)) + ")",
+                      cudaErrorInvalidValue);
+}
+
 bool tc_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("RCPG_NO_TC");

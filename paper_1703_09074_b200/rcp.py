@@ -200,6 +200,17 @@ class Context:
             raise MemoryError(msg)
         raise CudaError(msg)
 
+    # options (include/rcpg.h rcpg_set_option) ---------------------------
+    def set_option(self, name: str, value: int) -> None:
+        """"fp32_arith": 0 faithful fp64 arithmetic (default) / 1 fast 3xTF32;
+        "omega_host": 0 device Omega (default) / 1 host-evaluated, uploaded (bit-identical)."""
+        self.check(self.lib.rcpg_set_option(self.h, name.encode(), int(value)))
+
+    def get_option(self, name: str) -> int:
+        v = C.c_int64()
+        self.check(self.lib.rcpg_get_option(self.h, name.encode(), C.byref(v)))
+        return int(v.value)
+
     # diagnostics -------------------------------------------------------
     def pass_timings(self):
         cap = 4096

@@ -67,3 +67,28 @@ def test_gloo_world2_host_logic(rcp):
     for r, (p, o) in enumerate(zip(procs, outs)):
         assert p.returncode == 0, o[-2000:]
         assert f"RANK_OK {r}" in o
+
+
+@pytest.mark.timeout(300)
+def test_bench_spawns_one_rank_per_gpu():
+    """`bench.py --gpus 2` outside torchrun re-launches itself under torch.distributed.run with
+    two ranks (gloo here, no GPU), asserts WORLD_SIZE == --gpus, and rank 0 alone prints one
+    JSON line carrying the max over ranks."""
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--host-check"],
+                         env=env, capture_output=True, text=True, timeout=240)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    import json
+    rec = json.loads(lines[0])
+    assert rec == {"host_check": True, "world": 2, "max_rank": 1.0}
+
+
+def test_bench_rejects_world_mismatch():
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="", WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--host-check"],
+                         env=env, capture_output=True, text=True, timeout=120)
+    assert out.returncode != 0 and "WORLD_SIZE=1" in out.stderr
