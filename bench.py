@@ -13,7 +13,7 @@ and the model copied out inside the timed region.
 
 Multi-GPU: one process per GPU (torchrun; `--gpus N` without torchrun re-launches
 itself under torch.distributed.run with N ranks). The tensor is sharded in slabs
-along its last mode and decomposed collectively; value = the
+along the BASELINE slab mode (C5: mode 1, else the last) and decomposed collectively; value = the
 max over ranks of the device time. The same line carries `scaling_config`: C3
 (1024^3 fp32, BASELINE's sharded config) timed the same way at this N.
 """
@@ -112,7 +112,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--replicas", action="store_true",
-                    help="N>1: N independent decompositions instead of one sharded along the last mode")
+                    help="N>1: N independent decompositions instead of one sharded along the slab mode")
     ap.add_argument("--shard", action="store_true",
                     help="force the sharded path (NCCL communicator) also at N = 1")
     ap.add_argument("--no-scaling-config", action="store_true",
@@ -386,13 +386,23 @@ def timed_decompositions(rcp, ctx, X, dcfg, steps, warmup, dist):
     return dist.max(total_ms / steps), pass_ms, pass_bytes, launches, model, trace
 
 
+def shard_mode(cfg) -> int:
+    """The slab mode of the multi-GPU runs (BASELINE.json: C3 mode 3, C4 mode 4, C5 mode 1)."""
+    return cfg.shard_mode if cfg.shard_mode >= 0 else len(cfg.shape) - 1
+
+
+def shard_desc(cfg, world) -> str:
+    return f"slab-sharded along mode {shard_mode(cfg) + 1} over {world} GPUs (NCCL)"
+
+
 def make_tensor(rcp, synthetic, cfg, ctx, shard, world, rank):
     w, facs = synthetic.model(cfg.kind, cfg.shape, cfg.rank, cfg.seed)
     X = rcp.DeviceTensor.synth(cfg.shape, w, facs, cfg.snr, cfg.seed, dtype=cfg.dtype, ctx=ctx)
-    slo, shi = 0, cfg.shape[-1]
+    sm = shard_mode(cfg)
+    slo, shi = 0, cfg.shape[sm]
     if shard:
-        slo, shi = rcp.slab_range(cfg.shape[-1], world, rank)
-        Xs = X.slab(slo, shi)
+        slo, shi = rcp.slab_range(cfg.shape[sm], world, rank)
+        Xs = X.slab(slo, shi, mode=sm)
         X.free()
         X = Xs
     return X, slo, shi
@@ -414,7 +424,7 @@ def scaling_record(args, dist, rcp, synthetic, ctx, world, rank, shard):
     return {"workload": workload_str(cfg), "metric": "rCP time-to-solution", "value": ms, "unit": "ms",
             "n_gpus": world, "steps": steps, "warmup": 1, "higher_is_better": False,
             "scaling": "strong" if shard else "weak",
-            "parallelism": (f"slab-sharded along the last mode over {world} GPUs (NCCL)" if shard else "single GPU"),
+            "parallelism": (shard_desc(cfg, world) if shard else "single GPU"),
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if peak else None,
@@ -454,7 +464,7 @@ def main():
     ctx = rcp.Context(local)
     if args.omega_host:
         ctx.set_option("omega_host", 1)
-    # N > 1: one decomposition sharded in slabs along the last mode, the
+    # N > 1: one decomposition sharded in slabs along the slab mode, the
     # library's own NCCL communicator (id broadcast through torch.distributed)
     shard = (world > 1 and not args.replicas) or args.shard
     if shard:
@@ -477,7 +487,7 @@ def main():
     def e2e_step():
         if not shard:
             return rcp.decompose(x_host, dcfg, ctx=ctx)
-        t = rcp.DeviceTensor.upload_slab(x_host, cfg.shape, slo, shi, ctx=ctx)
+        t = rcp.DeviceTensor.upload_slab(x_host, cfg.shape, slo, shi, ctx=ctx, mode=shard_mode(cfg))
         try:
             return rcp.decompose(t, dcfg, ctx=ctx)
         finally:
@@ -516,7 +526,7 @@ def main():
             "dtype": "f64" if cfg.dtype == np.float64 else "f32",
             "data": "synthetic (device-generated Kruskal model + add_noise, BASELINE.json shape/distribution)",
             "config": {"workload": workload_str(cfg),
-                       "parallelism": (f"slab-sharded along the last mode over {world} GPUs (NCCL)" if shard
+                       "parallelism": (shard_desc(cfg, world) if shard
                                        else ("replicas" if world > 1 else "single GPU")),
                        "l2": "tensor larger than L2 (no flush needed)" if cfg.nbytes() > 126e6 else "L2-resident",
                        "omega": "host-evaluated, uploaded" if args.omega_host else "device"},

@@ -139,9 +139,10 @@ rcpg_status rcpg_decompose_host(rcpg_context* ctx, rcpg_dtype dtype, int32_t ord
 
 /* ---- sharding across GPUs (no counterpart in the serial
  * reference) ------------------------------------------------------------------
- * One context per GPU / rank. A tensor split in slabs along its LAST mode is
- * decomposed with the same rcpg_decompose / rcpg_compress calls on every rank
- * (collectively); results (model, trace, compressed tensor) are replicated. */
+ * One context per GPU / rank. A tensor split in slabs along its LAST mode (or,
+ * with the *_mode variants, its FIRST mode) is decomposed with the same
+ * rcpg_decompose / rcpg_compress calls on every rank (collectively); results
+ * (model, trace, compressed tensor) are replicated. */
 /* 128-byte NCCL unique id (rank 0 creates it, the caller broadcasts it). */
 rcpg_status rcpg_comm_unique_id(void* out128);
 /* Join an NCCL communicator of nranks ranks (one per GPU, one process each). */
@@ -152,12 +153,19 @@ rcpg_status rcpg_comm_init_loopback(rcpg_context** ctxs, int32_t n);
 rcpg_status rcpg_comm_rank(rcpg_context* ctx, int32_t* rank, int32_t* size);
 /* The balanced contiguous split [lo, hi) of [0, extent) used for slabs (host only). */
 void rcpg_slab_range(int64_t extent, int32_t nranks, int32_t rank, int64_t* lo, int64_t* hi);
+/* Slab [lo, hi) of mode `mode` (0 or order-1) of a device tensor (copied; `full` unchanged). */
+rcpg_status rcpg_tensor_slab_mode(rcpg_context* ctx, const rcpg_tensor* full, int32_t mode, int64_t lo, int64_t hi,
+                                  rcpg_tensor** out);
 /* Slab [lo, hi) of the last mode of a device tensor (copied; `full` unchanged). */
 rcpg_status rcpg_tensor_slab(rcpg_context* ctx, const rcpg_tensor* full, int64_t lo, int64_t hi, rcpg_tensor** out);
 /* Slab from host: global_shape of the whole tensor, host_slab row-major with
  * last extent hi - lo. */
 rcpg_status rcpg_tensor_upload_slab(rcpg_context* ctx, rcpg_dtype dtype, int32_t order, const int64_t* global_shape,
                                     int64_t lo, int64_t hi, const void* host_slab, rcpg_tensor** out);
+/* Slab of mode `mode` from host: host_slab row-major with extent hi - lo in that mode. */
+rcpg_status rcpg_tensor_upload_slab_mode(rcpg_context* ctx, rcpg_dtype dtype, int32_t order,
+                                         const int64_t* global_shape, int32_t mode, int64_t lo, int64_t hi,
+                                         const void* host_slab, rcpg_tensor** out);
 
 /* ---- model utilities on device ------------------------------------------ */
 /* relative_error (kruskal.hpp:187-194) of a Kruskal model (weights [R],

@@ -101,6 +101,8 @@ SIGNATURES = {
     "rcpg_slab_range": (None, [_I64, C.c_int32, C.c_int32, _V, _V]),
     "rcpg_tensor_slab": (_I32, [_V, _V, _I64, _I64, _V]),
     "rcpg_tensor_upload_slab": (_I32, [_V, C.c_int, C.c_int32, _V, _I64, _I64, _V, _V]),
+    "rcpg_tensor_slab_mode": (_I32, [_V, _V, C.c_int32, _I64, _I64, _V]),
+    "rcpg_tensor_upload_slab_mode": (_I32, [_V, C.c_int, C.c_int32, _V, C.c_int32, _I64, _I64, _V, _V]),
     "rcpg_stream_pass": (_I32, [_V, C.c_int, C.c_int32, _I64, _I64, _I64, _I64, _V, _V, _V]),
     "rcpg_plu_basis": (_I32, [_V, C.c_int, _I64, _I64, _V, _V]),
     "rcpg_thin_qr": (_I32, [_V, C.c_int, _I64, _I64, _V, _V, _V]),

@@ -98,6 +98,7 @@ struct rcpg_context {
   // (CUDA libm, <= a few ulp from glibc), true = generated on the host with the
   // reference's own libm calls and uploaded (bit-identical)
   bool omega_host = false;
+  cudaMemPool_t pool = nullptr;  // private pool of the device tensors (rcpg_tensor_*)
 };
 
 struct rcpg_tensor {
@@ -110,8 +111,10 @@ struct rcpg_tensor {
   bool owned = false;
   // slab of a tensor sharded along its last mode over the context's ranks
   bool slab = false;
-  i64 slab_lo = 0, slab_hi = 0, global_last = 0;
-  i64 gshape(int m) const { return (slab && m == order - 1) ? global_last : shape[m]; }
+  // slab of a tensor sharded along mode slab_mode: rows [slab_lo, slab_hi) of global_ext
+  int slab_mode = 0;
+  i64 slab_lo = 0, slab_hi = 0, global_ext = 0;
+  i64 gshape(int m) const { return (slab && m == slab_mode) ? global_ext : shape[m]; }
 };
 
 struct BasisRec {
@@ -320,6 +323,184 @@ int stabilize_small(rcpg_context* c, int stab, T* Y, i64 I, int n, T* out) {
 
 void finish_compress(rcpg_context* c, rcpg_compressed* out, const Deferred& dfr);
 
+// One compressed mode (compress.hpp:110-141) on an unsharded working tensor
+// `cur` of shape `shape`: Omega, sketch, power iterations, thin_qr, projection
+// into work0 / work1 (alternating with `which`). Sets shape[n] = l and returns
+// the new working tensor.
+template <typename T>
+const T* compress_mode_local(rcpg_context* c, const CompressCfg& cfg, int n, i64* shape, int order, const T* cur,
+                             int& which, BasisRec& basis, Deferred& dfr) {
+  const int sms = device_caps().num_sms;
+  const i64 extent = shape[n];
+  const i64 l = std::min(cfg.target_rank + cfg.oversampling, extent);
+  if (l > kMaxPanelCols) fail_after(c, dfr, "compress: sketch width k + p above the supported maximum (256)");
+  const ModeView v = mode_view(shape, order, n);
+  const i64 J = v.L * v.R;
+  const i64 S = J * extent;
+  const KoldaMap km = mode_kolda(shape, order, n);
+  const double b = sizeof(T);
+  c->panelA.ensure(size_t(J) * l * sizeof(T));
+  c->panelB.ensure(size_t(J) * l * sizeof(T));
+  c->Y.ensure(size_t(extent) * l * sizeof(T));
+  c->Qy.ensure(size_t(extent) * l * sizeof(T));
+  const i64 scr = sketch_scratch_elems<T>(v, l, sms);
+  c->scratch.ensure(size_t(scr) * sizeof(T));
+  T* P = c->panelA.as<T>();
+  T* Zp = c->panelB.as<T>();
+  T* Y = c->Y.as<T>();
+  T* Qy = c->Qy.as<T>();
+  if constexpr (std::is_same<T, float>::value) {
+    if (!c->fp32_fast) {
+      // Faithful fp32 (the reference's Scalar = float): every GEMM of the
+      // mode step as the oracle's gemm_nn / gemm_tn -- fp32 operands, fp64
+      // products and sums, one rounding to float -- on the FP64 tensor
+      // cores, with the panels (Omega, Z, Q) held in fp64 (exact copies of
+      // their float values). plu_basis / thin_qr run in float with the
+      // reference's operation order (factor.cu).
+      DevBuf& dst = which == 0 ? c->work0 : c->work1;
+      dst.ensure(size_t(v.L) * l * v.R * sizeof(T));
+      c->panelA.ensure(size_t(J) * l * sizeof(double));
+      c->Q64.ensure(size_t(extent) * l * sizeof(double));
+      const i64 scr64 = sketch_mixed_scratch_doubles(v, l, sms);
+      c->scratch.ensure(size_t(scr64) * sizeof(double));
+      double* P64 = c->panelA.as<double>();
+      float* Wf = c->panelB.as<float>();
+      float* Zf = dst.as<float>();  // free until the projection
+      double* Q64 = c->Q64.as<double>();
+      double* scr = c->scratch.as<double>();
+      {
+        ScopedPass sp(c, "omega", 0.0);
+        make_omega<double>(c, cfg.seed, n, km, v, l, cfg.distribution, P64, 2, c->st);
+      }
+      {
+        ScopedPass sp(c, "sketch", (S + extent * l) * b);
+        sketch_mixed(cur, v, P64, l, Y, scr, scr64, sms, c->st);
+      }
+      i64 ycols = l;
+      for (int it = 0; it < cfg.power_iterations; ++it) {
+        int rq;
+        {
+          ScopedPass sp(c, "stab_y", 2.0 * extent * ycols * b);
+          rq = stabilize_small<T>(c, cfg.stabilizer, Y, extent, int(ycols), Qy);
+        }
+        {
+          ScopedPass sp(c, "power_xtq", (S + J * rq) * b);
+          widen_f32(Qy, Q64, extent * rq, c->st);
+          project_mixed(cur, v, Q64, extent, rq, Wf, c->st);
+        }
+        int rz;
+        {
+          ScopedPass sp(c, "stab_w", 2.0 * J * rq * b);
+          FactorWork w = factor_work_t<T>(c, J);
+          if (cfg.stabilizer == RCPG_STAB_LU)
+            rz = plu_basis<T>(Wf, Zf, J, v.R, rq, km, w, c->st);
+          else
+            rz = thin_qr<T>(Wf, Zf, J, v.R, rq, km, w, nullptr, c->st);
+        }
+        {
+          ScopedPass sp(c, "power_xz", (S + J * rz + extent * rz) * b);
+          widen_f32(Zf, P64, J * rz, c->st);
+          sketch_mixed(cur, v, P64, rz, Y, scr, scr64, sms, c->st);
+        }
+        ycols = rz;
+      }
+      int qcols;
+      {
+        ScopedPass sp(c, "thin_qr", 2.0 * extent * ycols * b);
+        FactorWork w = factor_work_t<T>(c, extent);
+        basis.q.ensure(size_t(extent) * ycols * sizeof(T));
+        qcols = thin_qr<T>(Y, basis.q.as<T>(), extent, extent, int(ycols), identity_kolda(extent), w,
+                           rank_warn_slot(c, n), c->st);
+      }
+      basis.identity = false;
+      basis.cols = qcols;
+      if (qcols != l) fail_after(c, dfr, "fold: matrix dimensions do not match the target shape");
+      {
+        ScopedPass sp(c, "project", (S + l * J) * b);
+        widen_f32(basis.q.as<float>(), Q64, extent * l, c->st);
+        project_mixed(cur, v, Q64, extent, l, dst.as<float>(), c->st);
+      }
+      which ^= 1;
+      shape[n] = l;
+      return dst.as<T>();
+    }
+  }
+
+  {
+    ScopedPass sp(c, "omega", 0.0);
+    make_omega<T>(c, cfg.seed, n, km, v, l, cfg.distribution, P, sizeof(T) == 4 ? 0 : 1, c->st);
+  }
+  {
+    ScopedPass sp(c, "sketch", (S + extent * l) * b);
+    sketch<T>(cur, v, P, l, Y, c->scratch.as<T>(), scr, sms, c->st);
+  }
+  i64 ycols = l;
+  for (int it = 0; it < cfg.power_iterations; ++it) {
+    int rq;
+    {
+      ScopedPass sp(c, "stab_y", 2.0 * extent * ycols * b);
+      rq = stabilize_small<T>(c, cfg.stabilizer, Y, extent, int(ycols), Qy);
+    }
+    {
+      ScopedPass sp(c, "power_xtq", (S + J * rq) * b);
+      project<T>(cur, v, Qy, extent, rq, P, c->st);
+    }
+    int rz;
+    {
+      ScopedPass sp(c, "stab_w", 2.0 * J * rq * b);
+      FactorWork w = factor_work_t<T>(c, J);
+      const bool lu_prof = getenv("RCPG_PROFILE_LU") != nullptr;
+      if (lu_prof) {
+        c->als_prof.ensure(16 * sizeof(unsigned long long));
+        RCPG_CUDA(cudaMemsetAsync(c->als_prof.p, 0, 16 * sizeof(unsigned long long), c->st));
+        w.prof = c->als_prof.as<unsigned long long>();
+      }
+      if (cfg.stabilizer == RCPG_STAB_LU)
+        rz = plu_basis<T>(P, Zp, J, v.R, rq, km, w, c->st);
+      else
+        rz = thin_qr<T>(P, Zp, J, v.R, rq, km, w, nullptr, c->st);
+      if (lu_prof) {
+        unsigned long long h[4];
+        RCPG_CUDA(cudaMemcpyAsync(h, w.prof, sizeof(h), cudaMemcpyDeviceToHost, c->st));
+        RCPG_CUDA(cudaStreamSynchronize(c->st));
+        if (h[3])
+          fprintf(stderr, "[rcpg lu] J=%lld n=%d steps=%llu  reduce+book %.2f  update %.2f  cand+barrier %.2f us/step\n",
+                  (long long)J, rq, h[3], h[0] / 1e3 / h[3], h[1] / 1e3 / h[3], h[2] / 1e3 / h[3]);
+      }
+    }
+    {
+      ScopedPass sp(c, "power_xz", (S + J * rz + extent * rz) * b);
+      const i64 scr2 = sketch_scratch_elems<T>(v, rz, sms);
+      c->scratch.ensure(size_t(scr2) * sizeof(T));
+      sketch<T>(cur, v, Zp, rz, Y, c->scratch.as<T>(), scr2, sms, c->st);
+    }
+    ycols = rz;
+  }
+  // final Householder basis + rank warning (compress.hpp:135)
+  int qcols;
+  {
+    ScopedPass sp(c, "thin_qr", 2.0 * extent * ycols * b);
+    FactorWork w = factor_work_t<T>(c, extent);
+    basis.q.ensure(size_t(extent) * ycols * sizeof(T));
+    qcols = thin_qr<T>(Y, basis.q.as<T>(), extent, extent, int(ycols), identity_kolda(extent), w,
+                       rank_warn_slot(c, n), c->st);
+  }
+  basis.identity = false;
+  basis.cols = qcols;
+  // fold(Q^T B_(n)) must match next_shape (tensor.hpp:193-194)
+  if (qcols != l) fail_after(c, dfr, "fold: matrix dimensions do not match the target shape");
+  DevBuf& dst = which == 0 ? c->work0 : c->work1;
+  dst.ensure(size_t(v.L) * l * v.R * sizeof(T));
+  {
+    ScopedPass sp(c, "project", (S + l * J) * b);
+    project<T>(cur, v, basis.q.as<T>(), extent, l, dst.as<T>(), c->st);
+  }
+  which ^= 1;
+  shape[n] = l;
+  return dst.as<T>();
+}
+
+
 // compress.hpp:86-146. With `sync_checks` false the input check is left in
 // the device slots (Deferred::compress_input) for the caller to raise.
 template <typename T>
@@ -368,172 +549,7 @@ void run_compress(rcpg_context* c, const rcpg_tensor* t, const CompressCfg& cfg,
       basis.identity = true;
       continue;
     }
-    if (l > kMaxPanelCols) fail_after(c, dfr, "compress: sketch width k + p above the supported maximum (256)");
-    const ModeView v = mode_view(shape, order, n);
-    const i64 J = v.L * v.R;
-    const i64 S = J * extent;
-    const KoldaMap km = mode_kolda(shape, order, n);
-    const double b = sizeof(T);
-    c->panelA.ensure(size_t(J) * l * sizeof(T));
-    c->panelB.ensure(size_t(J) * l * sizeof(T));
-    c->Y.ensure(size_t(extent) * l * sizeof(T));
-    c->Qy.ensure(size_t(extent) * l * sizeof(T));
-    const i64 scr = sketch_scratch_elems<T>(v, l, sms);
-    c->scratch.ensure(size_t(scr) * sizeof(T));
-    T* P = c->panelA.as<T>();
-    T* Zp = c->panelB.as<T>();
-    T* Y = c->Y.as<T>();
-    T* Qy = c->Qy.as<T>();
-    if constexpr (std::is_same<T, float>::value) {
-      if (!c->fp32_fast) {
-        // Faithful fp32 (the reference's Scalar = float): every GEMM of the
-        // mode step as the oracle's gemm_nn / gemm_tn -- fp32 operands, fp64
-        // products and sums, one rounding to float -- on the FP64 tensor
-        // cores, with the panels (Omega, Z, Q) held in fp64 (exact copies of
-        // their float values). plu_basis / thin_qr run in float with the
-        // reference's operation order (factor.cu).
-        DevBuf& dst = which == 0 ? c->work0 : c->work1;
-        dst.ensure(size_t(v.L) * l * v.R * sizeof(T));
-        c->panelA.ensure(size_t(J) * l * sizeof(double));
-        c->Q64.ensure(size_t(extent) * l * sizeof(double));
-        const i64 scr64 = sketch_mixed_scratch_doubles(v, l, sms);
-        c->scratch.ensure(size_t(scr64) * sizeof(double));
-        double* P64 = c->panelA.as<double>();
-        float* Wf = c->panelB.as<float>();
-        float* Zf = dst.as<float>();  // free until the projection
-        double* Q64 = c->Q64.as<double>();
-        double* scr = c->scratch.as<double>();
-        {
-          ScopedPass sp(c, "omega", 0.0);
-          make_omega<double>(c, cfg.seed, n, km, v, l, cfg.distribution, P64, 2, c->st);
-        }
-        {
-          ScopedPass sp(c, "sketch", (S + extent * l) * b);
-          sketch_mixed(cur, v, P64, l, Y, scr, scr64, sms, c->st);
-        }
-        i64 ycols = l;
-        for (int it = 0; it < cfg.power_iterations; ++it) {
-          int rq;
-          {
-            ScopedPass sp(c, "stab_y", 2.0 * extent * ycols * b);
-            rq = stabilize_small<T>(c, cfg.stabilizer, Y, extent, int(ycols), Qy);
-          }
-          {
-            ScopedPass sp(c, "power_xtq", (S + J * rq) * b);
-            widen_f32(Qy, Q64, extent * rq, c->st);
-            project_mixed(cur, v, Q64, extent, rq, Wf, c->st);
-          }
-          int rz;
-          {
-            ScopedPass sp(c, "stab_w", 2.0 * J * rq * b);
-            FactorWork w = factor_work_t<T>(c, J);
-            if (cfg.stabilizer == RCPG_STAB_LU)
-              rz = plu_basis<T>(Wf, Zf, J, v.R, rq, km, w, c->st);
-            else
-              rz = thin_qr<T>(Wf, Zf, J, v.R, rq, km, w, nullptr, c->st);
-          }
-          {
-            ScopedPass sp(c, "power_xz", (S + J * rz + extent * rz) * b);
-            widen_f32(Zf, P64, J * rz, c->st);
-            sketch_mixed(cur, v, P64, rz, Y, scr, scr64, sms, c->st);
-          }
-          ycols = rz;
-        }
-        int qcols;
-        {
-          ScopedPass sp(c, "thin_qr", 2.0 * extent * ycols * b);
-          FactorWork w = factor_work_t<T>(c, extent);
-          basis.q.ensure(size_t(extent) * ycols * sizeof(T));
-          qcols = thin_qr<T>(Y, basis.q.as<T>(), extent, extent, int(ycols), identity_kolda(extent), w,
-                             rank_warn_slot(c, n), c->st);
-        }
-        basis.identity = false;
-        basis.cols = qcols;
-        if (qcols != l) fail_after(c, dfr, "fold: matrix dimensions do not match the target shape");
-        {
-          ScopedPass sp(c, "project", (S + l * J) * b);
-          widen_f32(basis.q.as<float>(), Q64, extent * l, c->st);
-          project_mixed(cur, v, Q64, extent, l, dst.as<float>(), c->st);
-        }
-        cur = dst.as<T>();
-        which ^= 1;
-        shape[n] = l;
-        continue;
-      }
-    }
-
-    {
-      ScopedPass sp(c, "omega", 0.0);
-      make_omega<T>(c, cfg.seed, n, km, v, l, cfg.distribution, P, sizeof(T) == 4 ? 0 : 1, c->st);
-    }
-    {
-      ScopedPass sp(c, "sketch", (S + extent * l) * b);
-      sketch<T>(cur, v, P, l, Y, c->scratch.as<T>(), scr, sms, c->st);
-    }
-    i64 ycols = l;
-    for (int it = 0; it < cfg.power_iterations; ++it) {
-      int rq;
-      {
-        ScopedPass sp(c, "stab_y", 2.0 * extent * ycols * b);
-        rq = stabilize_small<T>(c, cfg.stabilizer, Y, extent, int(ycols), Qy);
-      }
-      {
-        ScopedPass sp(c, "power_xtq", (S + J * rq) * b);
-        project<T>(cur, v, Qy, extent, rq, P, c->st);
-      }
-      int rz;
-      {
-        ScopedPass sp(c, "stab_w", 2.0 * J * rq * b);
-        FactorWork w = factor_work_t<T>(c, J);
-        const bool lu_prof = getenv("RCPG_PROFILE_LU") != nullptr;
-        if (lu_prof) {
-          c->als_prof.ensure(16 * sizeof(unsigned long long));
-          RCPG_CUDA(cudaMemsetAsync(c->als_prof.p, 0, 16 * sizeof(unsigned long long), c->st));
-          w.prof = c->als_prof.as<unsigned long long>();
-        }
-        if (cfg.stabilizer == RCPG_STAB_LU)
-          rz = plu_basis<T>(P, Zp, J, v.R, rq, km, w, c->st);
-        else
-          rz = thin_qr<T>(P, Zp, J, v.R, rq, km, w, nullptr, c->st);
-        if (lu_prof) {
-          unsigned long long h[4];
-          RCPG_CUDA(cudaMemcpyAsync(h, w.prof, sizeof(h), cudaMemcpyDeviceToHost, c->st));
-          RCPG_CUDA(cudaStreamSynchronize(c->st));
-          if (h[3])
-            fprintf(stderr, "[rcpg lu] J=%lld n=%d steps=%llu  reduce+book %.2f  update %.2f  cand+barrier %.2f us/step\n",
-                    (long long)J, rq, h[3], h[0] / 1e3 / h[3], h[1] / 1e3 / h[3], h[2] / 1e3 / h[3]);
-        }
-      }
-      {
-        ScopedPass sp(c, "power_xz", (S + J * rz + extent * rz) * b);
-        const i64 scr2 = sketch_scratch_elems<T>(v, rz, sms);
-        c->scratch.ensure(size_t(scr2) * sizeof(T));
-        sketch<T>(cur, v, Zp, rz, Y, c->scratch.as<T>(), scr2, sms, c->st);
-      }
-      ycols = rz;
-    }
-    // final Householder basis + rank warning (compress.hpp:135)
-    int qcols;
-    {
-      ScopedPass sp(c, "thin_qr", 2.0 * extent * ycols * b);
-      FactorWork w = factor_work_t<T>(c, extent);
-      basis.q.ensure(size_t(extent) * ycols * sizeof(T));
-      qcols = thin_qr<T>(Y, basis.q.as<T>(), extent, extent, int(ycols), identity_kolda(extent), w,
-                         rank_warn_slot(c, n), c->st);
-    }
-    basis.identity = false;
-    basis.cols = qcols;
-    // fold(Q^T B_(n)) must match next_shape (tensor.hpp:193-194)
-    if (qcols != l) fail_after(c, dfr, "fold: matrix dimensions do not match the target shape");
-    DevBuf& dst = which == 0 ? c->work0 : c->work1;
-    dst.ensure(size_t(v.L) * l * v.R * sizeof(T));
-    {
-      ScopedPass sp(c, "project", (S + l * J) * b);
-      project<T>(cur, v, basis.q.as<T>(), extent, l, dst.as<T>(), c->st);
-    }
-    cur = dst.as<T>();
-    which ^= 1;
-    shape[n] = l;
+    cur = compress_mode_local<T>(c, cfg, n, shape, order, cur, which, basis, dfr);
   }
   out->dtype = t->dtype;
   out->order = order;
@@ -574,22 +590,25 @@ __device__ __forceinline__ int slab_of(const SlabList& sl, i64 d) {
   return g;
 }
 
-// out[p * (hi - lo) + j] = in[p * E + lo + j]
+// out[(p * (hi - lo) + j) * Q + q] = in[(p * E + lo + j) * Q + q]
 template <typename T>
-__global__ void slab_extract_kernel(const T* in, i64 prefix, i64 E, i64 lo, i64 ext, T* out) {
-  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < prefix * ext; e += i64(gridDim.x) * blockDim.x) {
-    const i64 pp = e / ext, j = e - pp * ext;
-    out[e] = in[pp * E + lo + j];
+__global__ void slab_extract_kernel(const T* in, i64 prefix, i64 E, i64 lo, i64 ext, i64 suffix, T* out) {
+  const i64 total = prefix * ext * suffix;
+  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
+    const i64 q = e % suffix, pj = e / suffix, pp = pj / ext, j = pj - pp * ext;
+    out[e] = in[(pp * E + lo + j) * suffix + q];
   }
 }
 
-// full[p * E + d] = recv[g][p * ext_g + d - lo_g]   (per-rank blocks `stride` apart)
+// full[(p * E + d) * Q + q] = recv[g][(p * ext_g + d - lo_g) * Q + q]   (per-rank blocks `stride` apart)
 template <typename T>
-__global__ void slab_assemble_kernel(const T* recv, i64 stride, SlabList sl, i64 prefix, i64 E, T* full) {
-  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < prefix * E; e += i64(gridDim.x) * blockDim.x) {
-    const i64 pp = e / E, d = e - pp * E;
+__global__ void slab_assemble_kernel(const T* recv, i64 stride, SlabList sl, i64 prefix, i64 E, i64 suffix,
+                                     T* full) {
+  const i64 total = prefix * E * suffix;
+  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
+    const i64 q = e % suffix, pd = e / suffix, pp = pd / E, d = pd - pp * E;
     const int g = slab_of(sl, d);
-    full[e] = recv[g * stride + pp * (sl.hi[g] - sl.lo[g]) + (d - sl.lo[g])];
+    full[e] = recv[g * stride + (pp * (sl.hi[g] - sl.lo[g]) + (d - sl.lo[g])) * suffix + q];
   }
 }
 
@@ -632,9 +651,13 @@ void run_compress_sharded(rcpg_context* c, const rcpg_tensor* t, const CompressC
   check_arg(cfg.power_iterations >= 0, "compress: power iteration count must be non-negative");
   check_arg(c->comm != nullptr, "compress: a sharded tensor needs a communicator (rcpg_comm_init_*)");
   Comm& comm = *c->comm;
-  const int order = t->order, sm_ = order - 1;
+  const int order = t->order, sm_ = t->slab_mode;
+  check_arg(sm_ == order - 1 || sm_ == 0,
+            "compress: tensors are sharded along their first or last mode (a middle slab mode is not implemented)");
   const int sms = device_caps().num_sms;
   const cudaStream_t st = c->st;
+  // fp32 with fp64 arithmetic: partial sums cross the ranks in fp64 and are rounded once
+  const bool mixed = std::is_same<T, float>::value && !c->fp32_fast;
   {
     ScopedPass sp(c, "check_finite", double(t->size) * sizeof(T));
     c->scratch.ensure(size_t(sms) * 8 * sizeof(double) + 64);
@@ -658,10 +681,10 @@ void run_compress_sharded(rcpg_context* c, const rcpg_tensor* t, const CompressC
     for (int g = 0; g < comm.size; ++g) {
       sl.lo[g] = all[2 * size_t(g)];
       sl.hi[g] = all[2 * size_t(g) + 1];
-      check_arg(sl.lo[g] == next && sl.hi[g] >= sl.lo[g], "compress: slabs must tile the last mode in rank order");
+      check_arg(sl.lo[g] == next && sl.hi[g] >= sl.lo[g], "compress: slabs must tile the slab mode in rank order");
       next = sl.hi[g];
     }
-    check_arg(next == t->global_last, "compress: slabs must tile the last mode in rank order");
+    check_arg(next == t->global_ext, "compress: slabs must tile the slab mode in rank order");
   }
 
   std::set<i64> selected;
@@ -691,14 +714,52 @@ void run_compress_sharded(rcpg_context* c, const rcpg_tensor* t, const CompressC
     b.rank_warning = false;
   }
   const i64 lo = t->slab_lo;
+  // the slabs of every rank -> the full working tensor on every rank
+  auto assemble = [&]() {
+    i64 prefix = 1, suffix = 1;
+    for (int m = 0; m < sm_; ++m) prefix *= lsh[m];
+    for (int m = sm_ + 1; m < order; ++m) suffix *= lsh[m];
+    const i64 stride = prefix * sl.maxext() * suffix;
+    c->sh_send.ensure(size_t(stride) * sizeof(T));
+    c->sh_recv.ensure(size_t(stride) * size_t(comm.size) * sizeof(T));
+    RCPG_CUDA(cudaMemcpyAsync(c->sh_send.p, cur, size_t(prefix * lsh[sm_] * suffix) * sizeof(T),
+                              cudaMemcpyDeviceToDevice, st));
+    comm.allgather(c->sh_send.p, c->sh_recv.p, size_t(stride) * sizeof(T), st);
+    DevBuf& dst = which == 0 ? c->work0 : c->work1;
+    dst.ensure(size_t(prefix * gsh[sm_] * suffix) * sizeof(T));
+    slab_assemble_kernel<T><<<grid_for(prefix * gsh[sm_] * suffix), 256, 0, st>>>(
+        c->sh_recv.as<T>(), stride, sl, prefix, gsh[sm_], suffix, dst.as<T>());
+    count_launch();
+    RCPG_LAUNCHED();
+    cur = dst.as<T>();
+    which ^= 1;
+    lsh[sm_] = gsh[sm_];
+    sharded = false;
+  };
+  // all-reduce of n fp64 partials, then one rounding into the Scalar buffer `dst`
+  auto reduce64 = [&](double* part, i64 n, T* dst) {
+    comm.allreduce_sum(part, size_t(n), CommType::f64, st);
+    if constexpr (std::is_same<T, float>::value) narrow_f64(part, dst, n, st);
+  };
 
   for (int n = 0; n < order; ++n) {
     const i64 extent = gsh[n];
     const i64 l = std::min(cfg.target_rank + cfg.oversampling, extent);
     BasisRec& basis = out->bases[n];
     basis.dim = extent;
-    if (selected.count(n) == 0 || l >= extent) {
+    const bool compressed = selected.count(n) != 0 && l < extent;
+    if (!sharded) {  // after the slab mode: the working tensor is replicated
+      if (!compressed) {
+        basis.identity = true;
+        continue;
+      }
+      cur = compress_mode_local<T>(c, cfg, n, lsh, order, cur, which, basis, dfr);
+      gsh[n] = l;
+      continue;
+    }
+    if (!compressed) {
       basis.identity = true;
+      if (n == sm_) assemble();  // the slab mode stays: gather it, continue replicated
       continue;
     }
     if (l > kMaxPanelCols) fail_after(c, dfr, "compress: sketch width k + p above the supported maximum (256)");
@@ -707,15 +768,38 @@ void run_compress_sharded(rcpg_context* c, const rcpg_tensor* t, const CompressC
     const double b = sizeof(T);
     c->Y.ensure(size_t(extent) * l * sizeof(T));
     c->Qy.ensure(size_t(extent) * l * sizeof(T));
-    c->panelA.ensure(size_t(J) * l * sizeof(T));
+    c->panelA.ensure(size_t(J) * l * (mixed ? sizeof(double) : sizeof(T)));
     c->panelB.ensure(size_t(J) * l * sizeof(T));
     T* P = c->panelA.as<T>();
     T* Zp = c->panelB.as<T>();
     T* Y = c->Y.as<T>();
     T* Qy = c->Qy.as<T>();
+    double* P64 = c->panelA.as<double>();  // mixed: Omega / Z as fp64 (P's memory)
     i64 ycols = l;
     DevBuf& dst = which == 0 ? c->work0 : c->work1;
+    const i64 scr = mixed ? sketch_mixed_scratch_doubles(v, l, sms) : sketch_scratch_elems<T>(v, l, sms);
+    c->scratch.ensure(size_t(scr) * (mixed ? sizeof(double) : sizeof(T)));
+    if (mixed) {
+      c->Q64.ensure(size_t(extent) * l * sizeof(double));
+      c->B64.ensure(size_t(std::max(extent, J)) * l * sizeof(double));  // fp64 partials
+    }
+    const float* curf = reinterpret_cast<const float*>(cur);
+    // X_(n) P for this rank's part of the contraction: T result, or (mixed) the
+    // fp64 partial into B64
+    auto sketch_part = [&](const void* panel, i64 cols, T* out_t, bool partial) {
+      if (mixed) {
+        if (partial)
+          sketch_mixed(curf, v, static_cast<const double*>(panel), cols, c->B64.as<double>(), c->scratch.as<double>(),
+                       scr, sms, st);
+        else
+          sketch_mixed(curf, v, static_cast<const double*>(panel), cols, reinterpret_cast<float*>(out_t),
+                       c->scratch.as<double>(), scr, sms, st);
+      } else {
+        sketch<T>(cur, v, static_cast<const T*>(panel), cols, out_t, c->scratch.as<T>(), scr, sms, st);
+      }
+    };
     if (n < sm_) {
+      // modes before the (last) slab mode: X_(n) is column-sharded
       const ModeView vg = mode_view(gsh, order, n);
       const i64 Jg = vg.L * vg.R, S = J * extent;
       KoldaMap km = mode_kolda(lsh, order, n);
@@ -729,16 +813,25 @@ void run_compress_sharded(rcpg_context* c, const rcpg_tensor* t, const CompressC
         smap.lo[g] = sl.lo[g];
         smap.hi[g] = sl.hi[g];
       }
-      const i64 scr = sketch_scratch_elems<T>(v, l, sms);
-      c->scratch.ensure(size_t(scr) * sizeof(T));
       {
         ScopedPass sp(c, "omega", 0.0);
-        make_omega<T>(c, cfg.seed, n, km, v, l, cfg.distribution, P, sizeof(T) == 4 ? 0 : 1, st, Jg);
+        if (mixed)
+          make_omega<double>(c, cfg.seed, n, km, v, l, cfg.distribution, P64, 2, st, Jg);
+        else
+          make_omega<T>(c, cfg.seed, n, km, v, l, cfg.distribution, P, sizeof(T) == 4 ? 0 : 1, st, Jg);
       }
+      auto sketch_sum = [&](const void* panel, i64 cols) {  // Y = sum_g X_g P_g on every rank
+        if (mixed) {
+          sketch_part(panel, cols, Y, true);
+          reduce64(c->B64.as<double>(), extent * cols, Y);
+        } else {
+          sketch_part(panel, cols, Y, false);
+          comm.allreduce_sum(Y, size_t(extent * cols), comm_type(sizeof(T)), st);
+        }
+      };
       {
         ScopedPass sp(c, "sketch", (S + extent * l) * b);
-        sketch<T>(cur, v, P, l, Y, c->scratch.as<T>(), scr, sms, st);
-        comm.allreduce_sum(Y, size_t(extent * l), comm_type(sizeof(T)), st);
+        sketch_sum(mixed ? static_cast<const void*>(P64) : static_cast<const void*>(P), l);
       }
       for (int it = 0; it < cfg.power_iterations; ++it) {
         int rq;
@@ -747,8 +840,13 @@ void run_compress_sharded(rcpg_context* c, const rcpg_tensor* t, const CompressC
           rq = stabilize_small<T>(c, cfg.stabilizer, Y, extent, int(ycols), Qy);
         }
         {
-          ScopedPass sp(c, "power_xtq", (S + J * rq) * b);
-          project<T>(cur, v, Qy, extent, rq, P, st);
+          ScopedPass sp(c, "power_xtq", (S + J * rq) * b);  // W rows local
+          if (mixed) {
+            widen_f32(reinterpret_cast<const float*>(Qy), c->Q64.as<double>(), extent * rq, st);
+            project_mixed(curf, v, c->Q64.as<double>(), extent, rq, reinterpret_cast<float*>(Zp), st);
+          } else {
+            project<T>(cur, v, Qy, extent, rq, Zp, st);
+          }
         }
         int rz;
         {
@@ -766,14 +864,15 @@ void run_compress_sharded(rcpg_context* c, const rcpg_tensor* t, const CompressC
           w.U = c->dl_U.p;
           w.state = c->dl_state.p;
           w.G = G;
-          rz = plu_basis_dist<T>(P, Zp, J, v.R, rq, Jg, km, smap, comm, w, st);
+          // W (in Zp) -> Z; for the fp64 passes Z is then widened into P64 (P's memory)
+          dst.ensure(size_t(J) * l * sizeof(T));
+          T* Zt = mixed ? dst.as<T>() : P;
+          rz = plu_basis_dist<T>(Zp, Zt, J, v.R, rq, Jg, km, smap, comm, w, st);
+          if (mixed) widen_f32(reinterpret_cast<const float*>(Zt), P64, J * rz, st);
         }
         {
           ScopedPass sp(c, "power_xz", (S + J * rz + extent * rz) * b);
-          const i64 scr2 = sketch_scratch_elems<T>(v, rz, sms);
-          c->scratch.ensure(size_t(scr2) * sizeof(T));
-          sketch<T>(cur, v, Zp, rz, Y, c->scratch.as<T>(), scr2, sms, st);
-          comm.allreduce_sum(Y, size_t(extent * rz), comm_type(sizeof(T)), st);
+          sketch_sum(mixed ? static_cast<const void*>(P64) : static_cast<const void*>(P), rz);
         }
         ycols = rz;
       }
@@ -790,92 +889,99 @@ void run_compress_sharded(rcpg_context* c, const rcpg_tensor* t, const CompressC
       if (qcols != l) fail_after(c, dfr, "fold: matrix dimensions do not match the target shape");
       dst.ensure(size_t(v.L) * l * v.R * sizeof(T));
       {
-        ScopedPass sp(c, "project", (S + l * J) * b);
-        project<T>(cur, v, basis.q.as<T>(), extent, l, dst.as<T>(), st);
-      }
-    } else {
-      // the sharded mode: Y rows are local, the J_s-row panels are replicated
-      const i64 Iloc = v.I, Jn = v.L, S = Jn * Iloc;
-      const KoldaMap km = mode_kolda(gsh, order, n);
-      c->sh_fac.ensure(size_t(std::max<i64>(Iloc, 1)) * l * sizeof(T));
-      T* Yloc = c->sh_fac.as<T>();
-      const i64 scr = sketch_scratch_elems<T>(v, l, sms);
-      c->scratch.ensure(size_t(scr) * sizeof(T));
-      {
-        ScopedPass sp(c, "omega", 0.0);
-        make_omega<T>(c, cfg.seed, n, km, v, l, cfg.distribution, P, sizeof(T) == 4 ? 0 : 1, st);
-      }
-      {
-        ScopedPass sp(c, "sketch", (S + extent * l) * b);
-        sketch<T>(cur, v, P, l, Yloc, c->scratch.as<T>(), scr, sms, st);
-        gather_rows<T>(c, sl, Yloc, Iloc, int(l), extent, Y);
-      }
-      for (int it = 0; it < cfg.power_iterations; ++it) {
-        int rq;
-        {
-          ScopedPass sp(c, "stab_y", 2.0 * extent * ycols * b);
-          rq = stabilize_small<T>(c, cfg.stabilizer, Y, extent, int(ycols), Qy);
+        ScopedPass sp(c, "project", (S + l * J) * b);  // local: the working tensor stays sharded
+        if (mixed) {
+          widen_f32(reinterpret_cast<const float*>(basis.q.as<T>()), c->Q64.as<double>(), extent * l, st);
+          project_mixed(curf, v, c->Q64.as<double>(), extent, l, reinterpret_cast<float*>(dst.as<T>()), st);
+        } else {
+          project<T>(cur, v, basis.q.as<T>(), extent, l, dst.as<T>(), st);
         }
-        {
-          ScopedPass sp(c, "power_xtq", (S + Jn * rq) * b);
-          project<T>(cur, v, Qy + lo, extent, rq, P, st);  // this slab's rows of Q
-          comm.allreduce_sum(P, size_t(Jn * rq), comm_type(sizeof(T)), st);
-        }
-        int rz;
-        {
-          ScopedPass sp(c, "stab_w", 2.0 * Jn * rq * b);
-          FactorWork w = factor_work_t<T>(c, Jn);
-          rz = plu_basis<T>(P, Zp, Jn, 1, rq, km, w, st);
-        }
-        {
-          ScopedPass sp(c, "power_xz", (S + Jn * rz + extent * rz) * b);
-          const i64 scr2 = sketch_scratch_elems<T>(v, rz, sms);
-          c->scratch.ensure(size_t(scr2) * sizeof(T));
-          sketch<T>(cur, v, Zp, rz, Yloc, c->scratch.as<T>(), scr2, sms, st);
-          gather_rows<T>(c, sl, Yloc, Iloc, rz, extent, Y);
-        }
-        ycols = rz;
       }
-      int qcols;
-      {
-        ScopedPass sp(c, "thin_qr", 2.0 * extent * ycols * b);
-        FactorWork w = factor_work_t<T>(c, extent);
-        basis.q.ensure(size_t(extent) * ycols * sizeof(T));
-        qcols = thin_qr<T>(Y, basis.q.as<T>(), extent, extent, int(ycols), identity_kolda(extent), w,
-                           rank_warn_slot(c, n), st);
-      }
-      basis.identity = false;
-      basis.cols = qcols;
-      if (qcols != l) fail_after(c, dfr, "fold: matrix dimensions do not match the target shape");
-      dst.ensure(size_t(Jn) * l * sizeof(T));
-      {
-        ScopedPass sp(c, "project", (S + l * Jn) * b);
-        project<T>(cur, v, basis.q.as<T>() + lo, extent, l, dst.as<T>(), st);
-        comm.allreduce_sum(dst.p, size_t(Jn * l), comm_type(sizeof(T)), st);
-      }
-      sharded = false;
+      cur = dst.as<T>();
+      which ^= 1;
+      lsh[n] = gsh[n] = l;
+      continue;
     }
+    // the slab mode (n == sm_): Y rows are local, the J-row panels replicated
+    const i64 Iloc = v.I, S = J * Iloc;
+    const KoldaMap km = mode_kolda(gsh, order, n);
+    c->sh_fac.ensure(size_t(std::max<i64>(Iloc, 1)) * l * sizeof(T));
+    T* Yloc = c->sh_fac.as<T>();
+    {
+      ScopedPass sp(c, "omega", 0.0);
+      if (mixed)
+        make_omega<double>(c, cfg.seed, n, km, v, l, cfg.distribution, P64, 2, st);
+      else
+        make_omega<T>(c, cfg.seed, n, km, v, l, cfg.distribution, P, sizeof(T) == 4 ? 0 : 1, st);
+    }
+    {
+      ScopedPass sp(c, "sketch", (S + extent * l) * b);
+      sketch_part(mixed ? static_cast<const void*>(P64) : static_cast<const void*>(P), l, Yloc, false);
+      gather_rows<T>(c, sl, Yloc, Iloc, int(l), extent, Y);
+    }
+    for (int it = 0; it < cfg.power_iterations; ++it) {
+      int rq;
+      {
+        ScopedPass sp(c, "stab_y", 2.0 * extent * ycols * b);
+        rq = stabilize_small<T>(c, cfg.stabilizer, Y, extent, int(ycols), Qy);
+      }
+      {
+        ScopedPass sp(c, "power_xtq", (S + J * rq) * b);  // W = sum_g X_g^T Q_g
+        if (mixed) {
+          widen_f32(reinterpret_cast<const float*>(Qy), c->Q64.as<double>(), extent * rq, st);
+          project_mixed(curf, v, c->Q64.as<double>() + lo, extent, rq, c->B64.as<double>(), st);
+          reduce64(c->B64.as<double>(), J * rq, Zp);
+        } else {
+          project<T>(cur, v, Qy + lo, extent, rq, Zp, st);  // this slab's rows of Q
+          comm.allreduce_sum(Zp, size_t(J * rq), comm_type(sizeof(T)), st);
+        }
+      }
+      int rz;
+      {
+        ScopedPass sp(c, "stab_w", 2.0 * J * rq * b);
+        FactorWork w = factor_work_t<T>(c, J);
+        dst.ensure(size_t(J) * l * sizeof(T));
+        T* Zt = mixed ? dst.as<T>() : P;
+        rz = plu_basis<T>(Zp, Zt, J, v.R, rq, km, w, st);  // replicated (same bits on every rank)
+        if (mixed) widen_f32(reinterpret_cast<const float*>(Zt), P64, J * rz, st);
+      }
+      {
+        ScopedPass sp(c, "power_xz", (S + J * rz + extent * rz) * b);
+        sketch_part(mixed ? static_cast<const void*>(P64) : static_cast<const void*>(P), rz, Yloc, false);
+        gather_rows<T>(c, sl, Yloc, Iloc, rz, extent, Y);
+      }
+      ycols = rz;
+    }
+    int qcols;
+    {
+      ScopedPass sp(c, "thin_qr", 2.0 * extent * ycols * b);
+      FactorWork w = factor_work_t<T>(c, extent);
+      basis.q.ensure(size_t(extent) * ycols * sizeof(T));
+      qcols = thin_qr<T>(Y, basis.q.as<T>(), extent, extent, int(ycols), identity_kolda(extent), w,
+                         rank_warn_slot(c, n), st);
+    }
+    basis.identity = false;
+    basis.cols = qcols;
+    if (qcols != l) fail_after(c, dfr, "fold: matrix dimensions do not match the target shape");
+    dst.ensure(size_t(J) * l * sizeof(T));
+    {
+      ScopedPass sp(c, "project", (S + l * J) * b);  // B = sum_g Q_g^T X_g: replicated from here on
+      if (mixed) {
+        c->B64.ensure(size_t(J) * l * sizeof(double));
+        widen_f32(reinterpret_cast<const float*>(basis.q.as<T>()), c->Q64.as<double>(), extent * l, st);
+        project_mixed(curf, v, c->Q64.as<double>() + lo, extent, l, c->B64.as<double>(), st);
+        reduce64(c->B64.as<double>(), J * l, dst.as<T>());
+      } else {
+        project<T>(cur, v, basis.q.as<T>() + lo, extent, l, dst.as<T>(), st);
+        comm.allreduce_sum(dst.p, size_t(J * l), comm_type(sizeof(T)), st);
+      }
+    }
+    sharded = false;
     cur = dst.as<T>();
     which ^= 1;
     lsh[n] = gsh[n] = l;
   }
-  if (sharded) {  // the sharded mode stayed uncompressed: assemble the full tensor everywhere
-    i64 prefix = 1;
-    for (int m = 0; m < sm_; ++m) prefix *= lsh[m];
-    const i64 stride = prefix * sl.maxext();
-    c->sh_send.ensure(size_t(stride) * sizeof(T));
-    c->sh_recv.ensure(size_t(stride) * size_t(comm.size) * sizeof(T));
-    RCPG_CUDA(cudaMemcpyAsync(c->sh_send.p, cur, size_t(prefix * lsh[sm_]) * sizeof(T), cudaMemcpyDeviceToDevice, st));
-    comm.allgather(c->sh_send.p, c->sh_recv.p, size_t(stride) * sizeof(T), st);
-    DevBuf& dst = which == 0 ? c->work0 : c->work1;
-    dst.ensure(size_t(prefix * gsh[sm_]) * sizeof(T));
-    slab_assemble_kernel<T><<<grid_for(prefix * gsh[sm_]), 256, 0, st>>>(c->sh_recv.as<T>(), stride, sl, prefix,
-                                                                        gsh[sm_], dst.as<T>());
-    count_launch();
-    RCPG_LAUNCHED();
-    cur = dst.as<T>();
-    lsh[sm_] = gsh[sm_];
-  }
+  if (sharded) assemble();  // no mode was compressed
   out->dtype = t->dtype;
   out->order = order;
   i64 size = 1;
@@ -1121,7 +1227,7 @@ void run_relerr(rcpg_context* c, const T* X, const i64* shape, int order, const 
 template <typename T>
 void run_relerr_sharded(rcpg_context* c, const rcpg_tensor* t, const FactorSet<T>& fs, const T* w, Deferred& dfr) {
   const int sms = device_caps().num_sms;
-  const int sm_ = t->order - 1, R = fs.rank;
+  const int sm_ = t->slab_mode, R = fs.rank;
   const i64 Iloc = t->slab_hi - t->slab_lo;
   c->sh_fac.ensure(size_t(std::max<i64>(Iloc, 1)) * R * sizeof(T));
   FactorSet<T> loc = fs;
@@ -1308,12 +1414,16 @@ rcpg_status rcpg_create(int device, rcpg_context** out) {
     if (device < 0 || device >= n) throw CudaFailure("rcpg_create: no such CUDA device", cudaErrorInvalidDevice);
     RCPG_CUDA(cudaSetDevice(device));
     RCPG_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
-    // uploaded tensors come from the device's default pool; keep freed blocks
-    // in the pool so per-call uploads reuse them
-    cudaMemPool_t pool;
-    RCPG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    // uploaded tensors come from a private stream-ordered pool that keeps freed
+    // blocks (per-call uploads reuse them); the device's default pool, which
+    // other libraries in the host process share, is left untouched
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    RCPG_CUDA(cudaMemPoolCreate(&c->pool, &props));
     uint64_t keep = ~uint64_t(0);
-    RCPG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    RCPG_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &keep));
     c->bar.ensure(sizeof(GridBarrier));
     RCPG_CUDA(cudaMemset(c->bar.p, 0, sizeof(GridBarrier)));
     const char* f32 = std::getenv("RCPG_FP32");  // "fast": 3xTF32 passes (A/B), default faithful
@@ -1354,7 +1464,9 @@ void rcpg_destroy(rcpg_context* c) {
                     &c->bar, &c->info, &c->part, &c->tau, &c->diag, &c->cqr, &c->als_f, &c->als_g, &c->als_w, &c->als_kr,
                     &c->als_work, &c->als_trace, &c->als_state, &c->weights, &c->small_tmp, &c->nrm, &c->als_part, &c->als_prof, &c->recov})
     b->release();
+  for (DevBuf* b : {&c->Q64, &c->B64}) b->release();
   cudaStreamDestroy(c->st);
+  if (c->pool) cudaMemPoolDestroy(c->pool);  // tensors still alive keep their blocks until freed
   delete c;
 }
 
@@ -1378,7 +1490,7 @@ rcpg_status rcpg_tensor_upload(rcpg_context* c, rcpg_dtype dtype, int32_t order,
     // stream-ordered from the device pool, which keeps freed memory (release
     // threshold set in rcpg_create): repeated uploads of the same size cost no
     // cudaMalloc / cudaFree (those synchronize the device and map pages)
-    cudaError_t e = cudaMallocAsync(&t->d, bytes, c->st);
+    cudaError_t e = cudaMallocFromPoolAsync(&t->d, bytes, c->pool, c->st);
     if (e != cudaSuccess) {
       (void)cudaGetLastError();
       throw CudaFailure("rcpg_tensor_upload: cudaMallocAsync failed", e);
@@ -1544,40 +1656,47 @@ void rcpg_slab_range(int64_t extent, int32_t nranks, int32_t rank, int64_t* lo, 
   *hi = b;
 }
 
-rcpg_status rcpg_tensor_slab(rcpg_context* c, const rcpg_tensor* full, int64_t lo, int64_t hi, rcpg_tensor** out) {
+rcpg_status rcpg_tensor_slab_mode(rcpg_context* c, const rcpg_tensor* full, int32_t mode, int64_t lo, int64_t hi,
+                                  rcpg_tensor** out) {
   return guarded(c, [&] {
     check_arg(!full->slab, "tensor_slab: the input is already a slab");
     const int order = full->order;
-    const i64 E = full->shape[order - 1];
-    check_arg(lo >= 0 && lo <= hi && hi <= E, "tensor_slab: [lo, hi) outside the last mode");
+    check_arg(mode >= 0 && mode < order, "tensor_slab: mode index out of range");
+    const i64 E = full->shape[mode];
+    check_arg(lo >= 0 && lo <= hi && hi <= E, "tensor_slab: [lo, hi) outside the slab mode");
     auto t = std::make_unique<rcpg_tensor>();
     t->ctx = c;
     t->dtype = full->dtype;
     t->order = order;
     t->size = 1;
+    i64 prefix = 1, suffix = 1;
     for (int m = 0; m < order; ++m) {
-      t->shape[m] = m == order - 1 ? hi - lo : full->shape[m];
+      t->shape[m] = m == mode ? hi - lo : full->shape[m];
       t->size *= t->shape[m];
+      if (m < mode) prefix *= full->shape[m];
+      if (m > mode) suffix *= full->shape[m];
     }
     t->slab = true;
+    t->slab_mode = mode;
     t->slab_lo = lo;
     t->slab_hi = hi;
-    t->global_last = E;
+    t->global_ext = E;
     const size_t bytes = size_t(std::max<i64>(t->size, 1)) * dsize(t->dtype);
-    cudaError_t e = cudaMallocAsync(&t->d, bytes, c->st);  // device pool (see rcpg_tensor_upload)
+    cudaError_t e = cudaMallocFromPoolAsync(&t->d, bytes, c->pool, c->st);  // device pool (see rcpg_tensor_upload)
     if (e != cudaSuccess) {
       (void)cudaGetLastError();
       throw CudaFailure("rcpg_tensor_slab: cudaMallocAsync failed", e);
     }
     t->owned = true;
-    const i64 prefix = t->size / std::max<i64>(hi - lo, 1);
     if (hi > lo) {
       if (t->dtype == RCPG_F64)
         slab_extract_kernel<double><<<grid_for(t->size), 256, 0, c->st>>>(static_cast<const double*>(full->d), prefix,
-                                                                           E, lo, hi - lo, static_cast<double*>(t->d));
+                                                                           E, lo, hi - lo, suffix,
+                                                                           static_cast<double*>(t->d));
       else
         slab_extract_kernel<float><<<grid_for(t->size), 256, 0, c->st>>>(static_cast<const float*>(full->d), prefix,
-                                                                          E, lo, hi - lo, static_cast<float*>(t->d));
+                                                                          E, lo, hi - lo, suffix,
+                                                                          static_cast<float*>(t->d));
       count_launch();
       RCPG_LAUNCHED();
     }
@@ -1586,27 +1705,35 @@ rcpg_status rcpg_tensor_slab(rcpg_context* c, const rcpg_tensor* full, int64_t l
   });
 }
 
-rcpg_status rcpg_tensor_upload_slab(rcpg_context* c, rcpg_dtype dtype, int32_t order, const int64_t* global_shape,
-                                    int64_t lo, int64_t hi, const void* host_slab, rcpg_tensor** out) {
+rcpg_status rcpg_tensor_slab(rcpg_context* c, const rcpg_tensor* full, int64_t lo, int64_t hi, rcpg_tensor** out) {
+  if (!full) return RCPG_INVALID_ARGUMENT;
+  return rcpg_tensor_slab_mode(c, full, full->order - 1, lo, hi, out);
+}
+
+rcpg_status rcpg_tensor_upload_slab_mode(rcpg_context* c, rcpg_dtype dtype, int32_t order,
+                                         const int64_t* global_shape, int32_t mode, int64_t lo, int64_t hi,
+                                         const void* host_slab, rcpg_tensor** out) {
   return guarded(c, [&] {
     validate_tensor_args(dtype, order, global_shape);
-    const i64 E = global_shape[order - 1];
-    check_arg(lo >= 0 && lo <= hi && hi <= E, "tensor_upload_slab: [lo, hi) outside the last mode");
+    check_arg(mode >= 0 && mode < order, "tensor_upload_slab: mode index out of range");
+    const i64 E = global_shape[mode];
+    check_arg(lo >= 0 && lo <= hi && hi <= E, "tensor_upload_slab: [lo, hi) outside the slab mode");
     auto t = std::make_unique<rcpg_tensor>();
     t->ctx = c;
     t->dtype = dtype;
     t->order = order;
     t->size = 1;
     for (int m = 0; m < order; ++m) {
-      t->shape[m] = m == order - 1 ? hi - lo : global_shape[m];
+      t->shape[m] = m == mode ? hi - lo : global_shape[m];
       t->size *= t->shape[m];
     }
     t->slab = true;
+    t->slab_mode = mode;
     t->slab_lo = lo;
     t->slab_hi = hi;
-    t->global_last = E;
+    t->global_ext = E;
     const size_t bytes = size_t(std::max<i64>(t->size, 1)) * dsize(dtype);
-    cudaError_t e = cudaMallocAsync(&t->d, bytes, c->st);  // device pool (see rcpg_tensor_upload)
+    cudaError_t e = cudaMallocFromPoolAsync(&t->d, bytes, c->pool, c->st);  // device pool (see rcpg_tensor_upload)
     if (e != cudaSuccess) {
       (void)cudaGetLastError();
       throw CudaFailure("rcpg_tensor_upload_slab: cudaMallocAsync failed", e);
@@ -1617,6 +1744,12 @@ rcpg_status rcpg_tensor_upload_slab(rcpg_context* c, rcpg_dtype dtype, int32_t o
     RCPG_CUDA(cudaStreamSynchronize(c->st));
     *out = t.release();
   });
+}
+
+rcpg_status rcpg_tensor_upload_slab(rcpg_context* c, rcpg_dtype dtype, int32_t order, const int64_t* global_shape,
+                                    int64_t lo, int64_t hi, const void* host_slab, rcpg_tensor** out) {
+  if (order < 1) return RCPG_INVALID_ARGUMENT;
+  return rcpg_tensor_upload_slab_mode(c, dtype, order, global_shape, order - 1, lo, hi, host_slab, out);
 }
 
 rcpg_status rcpg_relative_error(rcpg_context* c, const rcpg_tensor* t, int64_t rank, const void* weights,
@@ -1704,10 +1837,25 @@ rcpg_status rcpg_stream_pass(rcpg_context* c, rcpg_dtype dtype, int32_t kind, in
         project<T>(X.as<T>(), v, P.as<T>(), I, cols, O.as<T>(), c->st);
       }
     };
-    if (dtype == RCPG_F64)
+    if (dtype == RCPG_F64) {
       run(double{});
-    else
+    } else if (!c->fp32_fast) {
+      // faithful fp32: fp64 products and sums, one rounding (the panel widened to fp64)
+      DevBuf P64;
+      P64.ensure(np_ * sizeof(double));
+      widen_f32(P.as<float>(), P64.as<double>(), i64(np_), c->st);
+      if (kind == 0) {
+        const i64 scr = sketch_mixed_scratch_doubles(v, cols, sms);
+        S.ensure(size_t(scr) * sizeof(double));
+        sketch_mixed(X.as<float>(), v, P64.as<double>(), cols, O.as<float>(), S.as<double>(), scr, sms, c->st);
+      } else {
+        project_mixed(X.as<float>(), v, P64.as<double>(), I, cols, O.as<float>(), c->st);
+      }
+      RCPG_CUDA(cudaStreamSynchronize(c->st));
+      P64.release();
+    } else {
       run(float{});
+    }
     RCPG_CUDA(cudaMemcpyAsync(out, O.p, no * b, cudaMemcpyDeviceToHost, c->st));
     RCPG_CUDA(cudaStreamSynchronize(c->st));
   });
@@ -1826,7 +1974,7 @@ rcpg_status rcpg_synth(rcpg_context* c, rcpg_dtype dtype, int32_t order, const i
     t->order = order;
     t->size = total;
     for (int m = 0; m < order; ++m) t->shape[m] = shape[m];
-    cudaError_t e = cudaMallocAsync(&t->d, size_t(total) * dsize(dtype), c->st);  // device pool
+    cudaError_t e = cudaMallocFromPoolAsync(&t->d, size_t(total) * dsize(dtype), c->pool, c->st);  // device pool
     if (e != cudaSuccess) {
       (void)cudaGetLastError();
       throw CudaFailure("rcpg_synth: cudaMalloc failed", e);

@@ -117,8 +117,8 @@ void sketch_bn_mixed(const float* X, ModeView v, const double* P, i64 cols, doub
   }
 }
 
-template <int BN>
-void project_bn_mixed(const float* X, ModeView v, const double* Q, i64 ldq, i64 cols, float* O, cudaStream_t st) {
+template <int BN, typename TO>
+void project_bn_mixed(const float* X, ModeView v, const double* Q, i64 ldq, i64 cols, TO* O, cudaStream_t st) {
   constexpr int BM = TileCfg<double>::BM, BK = TileCfg<double>::BK;
   const i64 nt = ceil_div(cols, BN), kt = ceil_div(v.I, BK);
   if (v.R > 1) {
@@ -127,13 +127,13 @@ void project_bn_mixed(const float* X, ModeView v, const double* Q, i64 ldq, i64 
       dim3 grid{unsigned(ceil_div(v.R, BM)), unsigned(na), unsigned(nt)};
       const i64 off = a0 * v.I * v.R, ooff = a0 * cols * v.R;
       ProjectLoader<double, BM, BN, BK, float, double> ld{X + off, Q, v.I, v.R, cols, ldq, kt};
-      ProjectEpilogue<double, BM, BN, float> ep{O + ooff, v.R, cols};
+      ProjectEpilogue<double, BM, BN, TO> ep{O + ooff, v.R, cols};
       launch_tile_gemm<double, BM, BN, BK, true>(grid, ld, ep, st);
     }
   } else {
     dim3 grid{unsigned(ceil_div(v.L, BM)), 1u, unsigned(nt)};
     ProjectLastLoader<double, BM, BN, BK, float, double> ld{X, Q, v.L, v.I, cols, ldq, kt};
-    ProjectLastEpilogue<double, BM, BN, float> ep{O, v.L, cols};
+    ProjectLastEpilogue<double, BM, BN, TO> ep{O, v.L, cols};
     launch_tile_gemm<double, BM, BN, BK, false>(grid, ld, ep, st);
   }
 }
@@ -142,6 +142,17 @@ __global__ void widen_kernel(const float* __restrict__ src, double* __restrict__
   for (i64 i = blockIdx.x * i64(blockDim.x) + threadIdx.x; i < n; i += i64(gridDim.x) * blockDim.x)
     dst[i] = double(src[i]);
 }
+
+__global__ void narrow_kernel(const double* __restrict__ src, float* __restrict__ dst, i64 n) {
+  for (i64 i = blockIdx.x * i64(blockDim.x) + threadIdx.x; i < n; i += i64(gridDim.x) * blockDim.x)
+    dst[i] = float(src[i]);
+}
+
+template <typename TO>
+void sketch_mixed_impl(const float* X, ModeView v, const double* P, i64 cols, TO* Y, double* scratch,
+                       i64 scratch_doubles, int num_sms, cudaStream_t st, const int* skip);
+template <typename TO>
+void project_mixed_impl(const float* X, ModeView v, const double* Q, i64 ldq, i64 cols, TO* O, cudaStream_t st);
 
 }  // namespace
 
@@ -152,8 +163,10 @@ i64 sketch_mixed_scratch_doubles(ModeView v, i64 cols, int num_sms) {
   return ceil_div(splits * cols * v.I, 4) * 4;
 }
 
-void sketch_mixed(const float* X, ModeView v, const double* P, i64 cols, float* Y, double* scratch,
-                  i64 scratch_doubles, int num_sms, cudaStream_t st, const int* skip) {
+namespace {
+template <typename TO>
+void sketch_mixed_impl(const float* X, ModeView v, const double* P, i64 cols, TO* Y, double* scratch,
+                       i64 scratch_doubles, int num_sms, cudaStream_t st, const int* skip) {
   i64 splits = 0, tps, total;
   bool done = false;
   if (v.R > 1) {
@@ -172,23 +185,52 @@ void sketch_mixed(const float* X, ModeView v, const double* P, i64 cols, float* 
       default: sketch_bn_mixed<80>(X, v, P, cols, scratch, splits, tps, total, st, skip); break;
     }
   }
-  // fp64 partials summed in a fixed order, then one rounding to fp32
+  // fp64 partials summed in a fixed order, then one rounding to fp32 (TO = float),
+  // or kept in fp64 (TO = double: a rank's partial of a sharded sum)
   const i64 n = cols * v.I;
-  reduce_partials_kernel<double, float><<<unsigned(ceil_div(n, 32)), 32 * kRedChunks, 0, st>>>(scratch, splits, n, Y,
-                                                                                                skip);
+  reduce_partials_kernel<double, TO><<<unsigned(ceil_div(n, 32)), 32 * kRedChunks, 0, st>>>(scratch, splits, n, Y,
+                                                                                             skip);
   count_launch();
   RCPG_LAUNCHED();
 }
 
-void project_mixed(const float* X, ModeView v, const double* Q, i64 ldq, i64 cols, float* O, cudaStream_t st) {
+template <typename TO>
+void project_mixed_impl(const float* X, ModeView v, const double* Q, i64 ldq, i64 cols, TO* O, cudaStream_t st) {
   if (v.R > 1 && project_dmma_f32(X, v, Q, ldq, cols, O, st)) return;
   switch (pick_bn(cols)) {
-    case 16: project_bn_mixed<16>(X, v, Q, ldq, cols, O, st); break;
-    case 32: project_bn_mixed<32>(X, v, Q, ldq, cols, O, st); break;
-    case 48: project_bn_mixed<48>(X, v, Q, ldq, cols, O, st); break;
-    case 64: project_bn_mixed<64>(X, v, Q, ldq, cols, O, st); break;
-    default: project_bn_mixed<80>(X, v, Q, ldq, cols, O, st); break;
+    case 16: project_bn_mixed<16, TO>(X, v, Q, ldq, cols, O, st); break;
+    case 32: project_bn_mixed<32, TO>(X, v, Q, ldq, cols, O, st); break;
+    case 48: project_bn_mixed<48, TO>(X, v, Q, ldq, cols, O, st); break;
+    case 64: project_bn_mixed<64, TO>(X, v, Q, ldq, cols, O, st); break;
+    default: project_bn_mixed<80, TO>(X, v, Q, ldq, cols, O, st); break;
   }
+}
+}  // namespace
+
+void sketch_mixed(const float* X, ModeView v, const double* P, i64 cols, float* Y, double* scratch,
+                  i64 scratch_doubles, int num_sms, cudaStream_t st, const int* skip) {
+  sketch_mixed_impl<float>(X, v, P, cols, Y, scratch, scratch_doubles, num_sms, st, skip);
+}
+
+void sketch_mixed(const float* X, ModeView v, const double* P, i64 cols, double* Y, double* scratch,
+                  i64 scratch_doubles, int num_sms, cudaStream_t st, const int* skip) {
+  sketch_mixed_impl<double>(X, v, P, cols, Y, scratch, scratch_doubles, num_sms, st, skip);
+}
+
+void project_mixed(const float* X, ModeView v, const double* Q, i64 ldq, i64 cols, float* O, cudaStream_t st) {
+  project_mixed_impl<float>(X, v, Q, ldq, cols, O, st);
+}
+
+void project_mixed(const float* X, ModeView v, const double* Q, i64 ldq, i64 cols, double* O, cudaStream_t st) {
+  project_mixed_impl<double>(X, v, Q, ldq, cols, O, st);
+}
+
+void narrow_f64(const double* src, float* dst, i64 n, cudaStream_t st) {
+  if (n <= 0) return;
+  const int blocks = int(std::max<i64>(1, std::min<i64>(ceil_div(n, 256), 148 * 16)));
+  narrow_kernel<<<blocks, 256, 0, st>>>(src, dst, n);
+  count_launch();
+  RCPG_LAUNCHED();
 }
 
 void widen_f32(const float* src, double* dst, i64 n, cudaStream_t st) {

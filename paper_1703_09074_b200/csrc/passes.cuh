@@ -293,6 +293,7 @@ i64 sketch_dmma_f32_splits(ModeView v, i64 cols, int num_sms, i64& tps, i64& tot
 bool sketch_dmma_f32(const float* X, ModeView v, const double* P, i64 cols, double* part, int num_sms,
                      const int* skip, cudaStream_t st);
 bool project_dmma_f32(const float* X, ModeView v, const double* Q, i64 ldq, i64 cols, float* O, cudaStream_t st);
+bool project_dmma_f32(const float* X, ModeView v, const double* Q, i64 ldq, i64 cols, double* O, cudaStream_t st);
 // Mixed passes of the faithful fp32 path: X fp32, panel fp64, fp64 accumulation,
 // one rounding of each result to fp32 (Y [I x cols] column-major, O in the
 // (a, c, b) layout). scratch: sketch_mixed_scratch_doubles().
@@ -300,6 +301,12 @@ i64 sketch_mixed_scratch_doubles(ModeView v, i64 cols, int num_sms);
 void sketch_mixed(const float* X, ModeView v, const double* P, i64 cols, float* Y, double* scratch,
                   i64 scratch_doubles, int num_sms, cudaStream_t st, const int* skip = nullptr);
 void project_mixed(const float* X, ModeView v, const double* Q, i64 ldq, i64 cols, float* O, cudaStream_t st);
+// fp64-output versions: a rank's unrounded partial of a sum sharded over ranks
+// (all-reduced in fp64, then rounded once with narrow_f64)
+void sketch_mixed(const float* X, ModeView v, const double* P, i64 cols, double* Y, double* scratch,
+                  i64 scratch_doubles, int num_sms, cudaStream_t st, const int* skip = nullptr);
+void project_mixed(const float* X, ModeView v, const double* Q, i64 ldq, i64 cols, double* O, cudaStream_t st);
+void narrow_f64(const double* src, float* dst, i64 n, cudaStream_t st);
 // dst[i] = double(src[i]) (exact)
 void widen_f32(const float* src, double* dst, i64 n, cudaStream_t st);
 

@@ -650,4 +650,8 @@ bool project_dmma_f32(const float* X, ModeView v, const double* Q, i64 ldq, i64 
   return project_tma_dispatch<float, float>(X, v, Q, ldq, cols, O, st);
 }
 
+bool project_dmma_f32(const float* X, ModeView v, const double* Q, i64 ldq, i64 cols, double* O, cudaStream_t st) {
+  return project_tma_dispatch<float, double>(X, v, Q, ldq, cols, O, st);
+}
+
 }  // namespace rcpg

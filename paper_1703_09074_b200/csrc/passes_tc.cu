@@ -844,7 +844,12 @@ void project_tc(const float* X, ModeView v, const float* Q, i64 ldq, i64 cols, f
 }
 
 bool tc_residual_ok(const i64* shape, int order, int rank) {
-  return tc_enabled() && order >= 2 && rank <= 64 && shape[order - 1] % 4 == 0 && shape[order - 1] <= kMaxCoord;
+  // the TMA coordinates are 32-bit: the last extent E and the row index p < P
+  // (the product of the leading modes) must both fit, else the SIMT residual runs
+  i64 P = 1;
+  for (int m = 0; m + 1 < order; ++m) P *= shape[m];
+  return tc_enabled() && order >= 2 && rank <= 64 && shape[order - 1] % 4 == 0 && shape[order - 1] <= kMaxCoord &&
+         P <= kMaxCoord;
 }
 
 size_t residual_tc_scratch_floats(i64 E, int rank) { return size_t(2 * E * (rank <= 32 ? 32 : 64)); }

@@ -270,32 +270,39 @@ def _dtype_code(dt) -> int:
 class DeviceTensor:
     """A tensor resident in HBM (rcpg_tensor)."""
 
-    def __init__(self, ctx: Context, handle, shape, dtype, global_shape=None, slab=None):
+    def __init__(self, ctx: Context, handle, shape, dtype, global_shape=None, slab=None, slab_mode=None):
         self.ctx = ctx
         self.h = handle
-        self.shape = tuple(int(e) for e in shape)  # local shape (a slab's last extent is hi - lo)
+        self.shape = tuple(int(e) for e in shape)  # local shape (a slab's extent is hi - lo)
         self.dtype = np.dtype(dtype)
         self.global_shape = tuple(int(e) for e in (global_shape if global_shape is not None else shape))
-        self.slab_range = slab  # (lo, hi) along the last mode, or None
+        self.slab_range = slab  # (lo, hi) along slab_mode, or None
+        self.slab_mode = slab_mode
 
-    def slab(self, lo: int, hi: int, ctx: Optional[Context] = None) -> "DeviceTensor":
-        """Slab [lo, hi) of the last mode (a device copy) for a sharded decomposition."""
+    def slab(self, lo: int, hi: int, ctx: Optional[Context] = None, mode: Optional[int] = None) -> "DeviceTensor":
+        """Slab [lo, hi) of mode `mode` (default: the last; the first is also supported) as a
+        device copy, for a sharded decomposition."""
         ctx = ctx or self.ctx
+        mode = len(self.shape) - 1 if mode is None else int(mode)
         h = C.c_void_p()
-        ctx.check(ctx.lib.rcpg_tensor_slab(ctx.h, self.h, int(lo), int(hi), C.byref(h)))
-        return DeviceTensor(ctx, h, self.shape[:-1] + (int(hi) - int(lo),), self.dtype, self.shape, (int(lo), int(hi)))
+        ctx.check(ctx.lib.rcpg_tensor_slab_mode(ctx.h, self.h, mode, int(lo), int(hi), C.byref(h)))
+        shape = list(self.shape)
+        shape[mode] = int(hi) - int(lo)
+        return DeviceTensor(ctx, h, shape, self.dtype, self.shape, (int(lo), int(hi)), mode)
 
     @classmethod
     def upload_slab(cls, x_slab: np.ndarray, global_shape: Sequence[int], lo: int, hi: int,
-                    ctx: Optional[Context] = None) -> "DeviceTensor":
-        """Upload this rank's slab (row-major, last extent hi - lo) of a tensor of `global_shape`."""
+                    ctx: Optional[Context] = None, mode: Optional[int] = None) -> "DeviceTensor":
+        """Upload this rank's slab (row-major, extent hi - lo along `mode`, default the last) of a
+        tensor of `global_shape`."""
         ctx = ctx or default_context()
         x = np.ascontiguousarray(x_slab)
         gs = np.asarray(global_shape, dtype=np.int64)
+        mode = len(gs) - 1 if mode is None else int(mode)
         h = C.c_void_p()
-        ctx.check(ctx.lib.rcpg_tensor_upload_slab(ctx.h, _dtype_code(x.dtype), len(gs), gs.ctypes.data, int(lo),
-                                                  int(hi), x.ctypes.data, C.byref(h)))
-        return cls(ctx, h, x.shape, x.dtype, tuple(global_shape), (int(lo), int(hi)))
+        ctx.check(ctx.lib.rcpg_tensor_upload_slab_mode(ctx.h, _dtype_code(x.dtype), len(gs), gs.ctypes.data, mode,
+                                                       int(lo), int(hi), x.ctypes.data, C.byref(h)))
+        return cls(ctx, h, x.shape, x.dtype, tuple(global_shape), (int(lo), int(hi)), mode)
 
     @classmethod
     def upload(cls, x: np.ndarray, ctx: Optional[Context] = None) -> "DeviceTensor":

@@ -101,6 +101,7 @@ class Config:
     tol: float
     max_iter: int
     seed: int = 1
+    shard_mode: int = -1  # slab mode of the multi-GPU runs (BASELINE.json; -1 = the last mode)
 
     @property
     def snr(self) -> float:  # amplitude ratio (synthetic.hpp:40-52)
@@ -116,5 +117,5 @@ CONFIGS = {
     "C2": Config("C2", 2, [400, 400, 400], np.float64, 20, 10, 2, 10.0, 1e-8, 200, 2),
     "C3": Config("C3", 3, [1024, 1024, 1024], np.float32, 50, 20, 2, 15.0, 1e-5, 500, 3),
     "C4": Config("C4", 4, [128, 128, 128, 512], np.float32, 32, 16, 2, 10.0, 1e-5, 500, 4),
-    "C5": Config("C5", 5, [10000, 1000, 500], np.float32, 64, 16, 1, 20.0, 1e-5, 500, 5),
+    "C5": Config("C5", 5, [10000, 1000, 500], np.float32, 64, 16, 1, 20.0, 1e-5, 500, 5, 0),  # sharded along mode 1
 }

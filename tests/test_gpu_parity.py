@@ -61,6 +61,52 @@ def test_sketch_matrix_matches_reference_stream(rcp, oracle):
     assert np.max(np.abs(gf - wf)) <= 1e-6
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("dist", [0, 1])
+def test_omega_host_upload_bit_identical(rcp, oracle, dtype, dist):
+    """north_star: Omega "bit-identical to the reference's RNG, or uploaded from host". With
+    omega_host = 1 the library evaluates RandomStream::normal() (random.hpp:75-87) with the
+    host's libm and uploads it: array_equal with the oracle's fill_gaussian / fill_uniform over
+    10^7 draws (the device generator differs from glibc in the last ulp for ~0.1% of draws)."""
+    ctx = rcp.Context(0)
+    ctx.set_option("omega_host", 1)
+    assert ctx.get_option("omega_host") == 1
+    seed = oracle.derive_seed(12345, oracle.stream_id(1))
+    for mode, rows, cols in [(0, 1_000_000, 10), (2, 999, 37)]:
+        got = rcp.sketch_matrix(seed, mode, rows, cols, distribution=dist, dtype=dtype, ctx=ctx)
+        want = oracle.sketch_matrix(seed, mode, rows, cols, dist=dist, dtype=dtype)
+        assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("rows,cols", [(200, 20), (1000, 30), (5000, 70), (160000, 30)])
+def test_plu_basis_bitwise_random(rcp, oracle, rows, cols, dtype):
+    """FullPivLU (compress.hpp:47-58) on random panels: the same pivots and the same two-rounding
+    update x - m*u (no FMA contraction) as the oracle's -ffp-contract=off build: identical bits."""
+    rng = np.random.default_rng(rows + 7 * cols)
+    m = np.asfortranarray(rng.standard_normal((rows, cols)).astype(dtype))
+    assert np.array_equal(rcp.plu_basis(m), oracle.plu_basis(m))
+
+
+def test_plu_basis_bitwise_large_fp32(rcp, oracle):
+    """A 10^6 x 70 fp32 panel (C3's W size) through the grid LU: identical bits."""
+    rng = np.random.default_rng(70)
+    m = np.asfortranarray(rng.standard_normal((1_000_000, 70)).astype(np.float32))
+    assert np.array_equal(rcp.plu_basis(m), oracle.plu_basis(m))
+
+
+@pytest.mark.parametrize("rows,cols", [(100, 20), (1024, 70), (10000, 80), (48, 48)])
+def test_thin_qr_fp32_bitwise(rcp, oracle, rows, cols):
+    """fp32 thin_qr (compress.hpp:60-73): the Householder QR in the reference's float operation
+    order (fp64 dot products rounded once, separately rounded updates): identical bits."""
+    rng = np.random.default_rng(rows * cols)
+    m = np.asfortranarray(rng.standard_normal((rows, cols)).astype(np.float32))
+    q, rw = rcp.thin_qr(m)
+    qo, rwo = oracle.thin_qr(m)
+    assert rw == rwo
+    assert np.array_equal(q, qo)
+
+
 # --------------------------------------------------------- factorizations
 @pytest.mark.parametrize("rows,cols", [(200, 20), (1000, 30), (5000, 70)])
 def test_plu_basis_matches_fullpivlu(rcp, oracle, rows, cols):
