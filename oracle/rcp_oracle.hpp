@@ -1264,16 +1264,170 @@ std::pair<Kruskal<S>, FitTrace> als_solve(const Tensor<S>& t, const DecomposeCon
   return {std::move(model), trace};
 }
 
-// solve.hpp:381-398 (ALS only; bcd is out of scope)
+namespace detail {
+// solve.hpp:150-163: Kronecker chain of column r of every factor but `skip`,
+// highest mode first (Scalar products, rounded at every step)
+template <typename S>
+std::vector<S> kron_column_all_but(const std::vector<Matrix<S>>& factors, Index skip, Index r) {
+  std::vector<S> z(1, S(1));
+  for (Index m = Index(factors.size()) - 1; m >= 0; --m) {
+    if (m == skip) continue;
+    const Matrix<S>& f = factors[std::size_t(m)];
+    std::vector<S> next(z.size() * std::size_t(f.rows()));
+    for (std::size_t i = 0; i < z.size(); ++i)
+      for (Index c = 0; c < f.rows(); ++c) next[i * std::size_t(f.rows()) + std::size_t(c)] = z[i] * f(c, r);
+    z.swap(next);
+  }
+  return z;
+}
+
+// solve.hpp:165-175: weights(r) * outer product of column r (m(i, j) = A0(i, r) * (w_r * z_j))
+template <typename S>
+Tensor<S> component_tensor(const std::vector<Matrix<S>>& factors, const std::vector<S>& weights, Index r,
+                           const Shape& shape) {
+  const std::vector<S> z = kron_column_all_but(factors, 0, r);
+  const Matrix<S>& a0 = factors[0];
+  Matrix<S> m(a0.rows(), Index(z.size()));
+  for (Index j = 0; j < Index(z.size()); ++j) {
+    const S wz = weights[std::size_t(r)] * z[std::size_t(j)];
+    for (Index i = 0; i < a0.rows(); ++i) m(i, j) = a0(i, r) * wz;
+  }
+  return fold(m, 0, shape);
+}
+}  // namespace detail
+
+// solve.hpp:270-376: block coordinate descent over rank-one components (the
+// paper's solver for its tables). Scalar arithmetic as the reference except the
+// documented deviation: norms, dot products and matrix-vector products
+// accumulate in double and are rounded once to Scalar.
+template <typename S>
+std::pair<Kruskal<S>, FitTrace> bcd_solve(const Tensor<S>& t, const DecomposeConfig& cfg,
+                                          bool compute_relerr = true) {
+  detail::validate_solver_input(t, cfg);
+  const auto start = std::chrono::steady_clock::now();
+  const Index n = t.order();
+  const Index rank = cfg.rank;
+  const S norm_b2 = S(t.squared_norm());
+  constexpr int kComponentCap = 200;
+
+  std::vector<Matrix<S>> factors = init_factors(t, rank, cfg.seed, cfg.init);
+  for (auto& x : factors[0].v) x = S(0);
+  std::vector<S> weights(std::size_t(rank), S(0));
+  FitTrace trace;
+  int total = 0;
+
+  const auto update_component = [&](Index r, const Tensor<S>& y) -> bool {
+    const S norm_y2 = S(y.squared_norm());
+    if (norm_y2 == S(0)) {
+      weights[std::size_t(r)] = S(0);
+      if (col_norm(factors[0], r) == 0.0) {
+        for (Index i = 0; i < factors[0].rows(); ++i) factors[0](i, r) = S(0);
+        factors[0](0, r) = S(1);
+      }
+      return true;
+    }
+    std::vector<Matrix<S>> unf(static_cast<std::size_t>(n));
+    for (Index m = 0; m < n; ++m) unf[std::size_t(m)] = unfold(y, m);
+    S prev = S(0);
+    const int cap = std::min(kComponentCap, cfg.max_iter - total);
+    for (int j = 1; j <= cap; ++j) {
+      ++total;
+      S lambda_r = S(0);
+      S w_dot_c = S(0);
+      for (Index mode = 0; mode < n; ++mode) {
+        const std::vector<S> zv = detail::kron_column_all_but(factors, mode, r);
+        S sc = S(1);
+        for (Index m = 0; m < n; ++m) {
+          if (m == mode) continue;
+          const double c = col_norm(factors[std::size_t(m)], r);
+          sc *= S(c * c);
+        }
+        Matrix<S> z(Index(zv.size()), 1);
+        for (std::size_t i = 0; i < zv.size(); ++i) z.v[i] = zv[i];
+        const Matrix<S> w = gemm_nn(unf[std::size_t(mode)], z);
+        Matrix<S> col(w.rows(), 1);
+        for (Index i = 0; i < w.rows(); ++i) col(i, 0) = sc > S(0) ? w(i, 0) / sc : S(0);
+        const S nrm = S(col_norm(col, 0));
+        if (mode < n - 1) {
+          if (nrm > S(0))
+            for (Index i = 0; i < col.rows(); ++i) col(i, 0) /= nrm;
+        } else {
+          lambda_r = nrm;
+          if (nrm > S(0))
+            for (Index i = 0; i < col.rows(); ++i) col(i, 0) /= nrm;
+          double d = 0.0;
+          for (Index i = 0; i < col.rows(); ++i) d += double(col(i, 0)) * double(w(i, 0));
+          w_dot_c = S(d);
+        }
+        Matrix<S>& f = factors[std::size_t(mode)];
+        for (Index i = 0; i < f.rows(); ++i) f(i, r) = col(i, 0);
+      }
+      weights[std::size_t(r)] = lambda_r;
+      const S comp_fit = S(1) - (norm_y2 + lambda_r * lambda_r - S(2) * lambda_r * w_dot_c) / norm_y2;
+      if (!std::isfinite(double(comp_fit))) throw SolverError("bcd: fit became non-finite", total);
+      trace.entries.push_back({total, double(comp_fit), detail::elapsed_seconds(start)});
+      if (j >= 2 && std::abs(double(comp_fit - prev)) < cfg.tol) return true;
+      prev = comp_fit;
+    }
+    return false;
+  };
+
+  // deflation pass: component r against the residual of components 0..r-1
+  Tensor<S> residual = t;
+  for (Index r = 0; r < rank && total < cfg.max_iter; ++r) {
+    update_component(r, residual);
+    Kruskal<S> partial;
+    partial.weights.assign(weights.begin(), weights.begin() + (r + 1));
+    for (Index m = 0; m < n; ++m) {
+      const Matrix<S>& f = factors[std::size_t(m)];
+      Matrix<S> lc(f.rows(), r + 1);
+      for (Index c = 0; c <= r; ++c)
+        for (Index i = 0; i < f.rows(); ++i) lc(i, c) = f(i, c);
+      partial.factors.push_back(std::move(lc));
+    }
+    const Tensor<S> rec = reconstruct(partial);
+    for (Index i = 0; i < t.size(); ++i)
+      residual.values[std::size_t(i)] = t.values[std::size_t(i)] - rec.values[std::size_t(i)];
+  }
+  // refinement sweeps against leave-one-out residuals
+  S prev_overall = S(1) - S(residual.squared_norm()) / norm_b2;
+  while (total < cfg.max_iter) {
+    for (Index r = 0; r < rank && total < cfg.max_iter; ++r) {
+      const Tensor<S> c0 = detail::component_tensor(factors, weights, r, t.shape);
+      Tensor<S> loo = residual;
+      for (Index i = 0; i < t.size(); ++i) loo.values[std::size_t(i)] += c0.values[std::size_t(i)];
+      update_component(r, loo);
+      const Tensor<S> c1 = detail::component_tensor(factors, weights, r, t.shape);
+      for (Index i = 0; i < t.size(); ++i)
+        residual.values[std::size_t(i)] = loo.values[std::size_t(i)] - c1.values[std::size_t(i)];
+    }
+    const S overall = S(1) - S(residual.squared_norm()) / norm_b2;
+    if (!std::isfinite(double(overall))) throw SolverError("bcd: fit became non-finite", total);
+    if (std::abs(double(overall - prev_overall)) < cfg.tol) {
+      trace.converged = true;
+      break;
+    }
+    prev_overall = overall;
+  }
+  trace.iterations = total;
+  Kruskal<S> model{weights, std::move(factors)};
+  model = normalize(std::move(model));
+  if (compute_relerr) trace.final_relative_error = relative_error(t, model);
+  return {std::move(model), trace};
+}
+
+// solve.hpp:381-398
 template <typename S>
 std::pair<Kruskal<S>, FitTrace> decompose(const Tensor<S>& t, const DecomposeConfig& cfg) {
-  check(cfg.method == SolveMethod::als, "decompose: only the ALS solver is on this path");
-  if (!cfg.randomized) return als_solve(t, cfg);
+  const auto solve = [&](const Tensor<S>& x, bool relerr) {
+    return cfg.method == SolveMethod::als ? als_solve(x, cfg, relerr) : bcd_solve(x, cfg, relerr);
+  };
+  if (!cfg.randomized) return solve(t, true);
   CompressConfig cc = cfg.compress;
   if (cc.target_rank == 0) cc.target_rank = cfg.rank;
   check(cc.target_rank == cfg.rank, "decompose: compression target rank must equal the CP rank");
   const CompressionResult<S> reduced = compress(t, cc);
-  auto [small_model, trace] = als_solve(reduced.compressed, cfg, /*compute_relerr=*/false);
+  auto [small_model, trace] = solve(reduced.compressed, /*relerr=*/false);
   Kruskal<S> model = recover(small_model, reduced.bases);
   trace.final_relative_error = relative_error(t, model);
   return {std::move(model), trace};

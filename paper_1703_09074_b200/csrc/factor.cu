@@ -1415,6 +1415,177 @@ __global__ void __launch_bounds__(kFacThreads) householder_kernel(QrArgs<T> p) {
   }
 }
 
+// ------------------------------------------- Householder on one cluster
+// The faithful thin_qr (compress.hpp:60-73, Eigen's unblocked HouseholderQR in
+// the reference's Scalar arithmetic, operation for operation as
+// householder_kernel) for panels that fit the distributed shared memory of one
+// thread-block cluster: CTA r owns rows [r chunk, (r+1) chunk) of the I x n
+// panel (column-major in its smem); the per-column reductions (tail norm, the
+// n - k - 1 dot products, in fp64) are partial sums per CTA added in CTA order
+// through DSMEM. Two cluster barriers per reflector, one per Q column step,
+// instead of householder_kernel's grid barriers. Q (I x r, ld I) is built in
+// global memory, each CTA updating its own rows.
+constexpr int kHhThreads = 512;
+
+template <typename T>
+__global__ void __launch_bounds__(kHhThreads) householder_cluster_kernel(const T* __restrict__ A, T* __restrict__ Q,
+                                                                         int I, int n, int chunk,
+                                                                         int* rank_warning) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int CS = int(cl.num_blocks()), me = int(cl.block_rank());
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* part = reinterpret_cast<double*>(smem_raw);   // [2][kMaxPanelCols + 1] partial sums (double-buffered)
+  double* rowk = part + 2 * (kMaxPanelCols + 1);        // [2][kMaxPanelCols] row k (owner's copy)
+  T* tau = reinterpret_cast<T*>(rowk + 2 * kMaxPanelCols);  // [kMaxPanelCols]
+  T* diag = tau + kMaxPanelCols;                        // [kMaxPanelCols]
+  T* a = diag + kMaxPanelCols;                          // [n][chunk] own rows
+  __shared__ double red[32];
+  __shared__ double tmp[kMaxPanelCols];
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  const int r0 = me * chunk, rows = max(0, min(chunk, I - r0));
+  const int r = min(I, n);
+  for (int e = tid; e < chunk * n; e += nt) {
+    const int i = e % chunk, j = e / chunk;
+    a[e] = i < rows ? A[i64(r0 + i) + i64(j) * I] : T(0);
+  }
+  __syncthreads();
+  auto block_sum = [&](double v) {
+    v = warp_sum(v);
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (wid == 0) {
+      s = lane < nw ? red[lane] : 0.0;
+      s = warp_sum(s);
+    }
+    return s;  // valid in warp 0
+  };
+  for (int k = 0; k < r; ++k) {
+    const int buf = k & 1;
+    double* pb = part + buf * (kMaxPanelCols + 1);
+    const int ok = k / chunk, lk = k - ok * chunk;  // owner CTA / local row of row k
+    const int i0 = max(0, k + 1 - r0);              // first own row below k
+    // 1. tail squared norm of column k (fp64)
+    double acc = 0.0;
+    for (int i = i0 + tid; i < rows; i += nt) {
+      const double x = double(a[i + k * chunk]);
+      acc += x * x;
+    }
+    acc = block_sum(acc);
+    if (tid == 0) pb[kMaxPanelCols] = acc;
+    cl.sync();
+    double tsq = 0.0;
+    for (int q = 0; q < CS; ++q) tsq += *cl.map_shared_rank(pb + kMaxPanelCols, q);
+    const T tail_sq = T(tsq);
+    const T c0 = *cl.map_shared_rank(a + lk + k * chunk, ok);
+    T beta, t;
+    const bool trivial = !(tail_sq > Traits<T>::realmin);
+    if (trivial) {
+      t = T(0);
+      beta = c0;
+    } else {
+      beta = sqrt(add_rn(mul_rn(c0, c0), tail_sq));
+      if (c0 >= T(0)) beta = -beta;
+      t = (beta - c0) / beta;
+    }
+    const T denom = c0 - beta;
+    if (tid == 0) {
+      tau[k] = t;
+      diag[k] = beta;
+    }
+    // 2. essential vector of own tail rows
+    for (int i = i0 + tid; i < rows; i += nt) a[i + k * chunk] = trivial ? T(0) : a[i + k * chunk] / denom;
+    __syncthreads();
+    const int ncol = n - k - 1;
+    // 3. partial v^T A(:, j) (fp64) and the owner's row k
+    if (!trivial && ncol > 0) {
+      for (int jj = wid; jj < ncol; jj += nw) {
+        const int j = k + 1 + jj;
+        double s = 0.0;
+        for (int i = i0 + lane; i < rows; i += 32) s += double(a[i + k * chunk]) * double(a[i + j * chunk]);
+        s = warp_sum(s);
+        if (lane == 0) pb[jj] = s;
+      }
+      if (me == ok)
+        for (int jj = tid; jj < ncol; jj += nt) rowk[buf * kMaxPanelCols + jj] = double(a[lk + (k + 1 + jj) * chunk]);
+    }
+    cl.sync();
+    // 4. tmp_j = Scalar(v . A(:, j)) + A(k, j); rank-1 update of own rows
+    if (!trivial && ncol > 0) {
+      for (int jj = tid; jj < ncol; jj += nt) {
+        double sum = 0.0;
+        for (int q = 0; q < CS; ++q) sum += *cl.map_shared_rank(pb + jj, q);
+        tmp[jj] = double(add_rn(T(sum), T(*cl.map_shared_rank(rowk + buf * kMaxPanelCols + jj, ok))));
+      }
+      __syncthreads();
+      for (int e = tid; e < ncol * rows; e += nt) {
+        const int i = e % rows, jj = e / rows;
+        if (r0 + i < k) continue;
+        T& x = a[i + (k + 1 + jj) * chunk];
+        if (r0 + i == k)
+          x = sub_mul_rn(x, t, T(tmp[jj]));
+        else
+          x = sub_mul_rn(x, mul_rn(t, a[i + k * chunk]), T(tmp[jj]));
+      }
+    }
+    if (me == ok && tid == 0) a[lk + k * chunk] = beta;
+    __syncthreads();
+  }
+  if (me == 0 && tid == 0 && rank_warning != nullptr) {
+    T dmax = T(0), dmin = T(INFINITY);
+    for (int k = 0; k < r; ++k) {
+      const T d = fabs(diag[k]);
+      dmax = d > dmax ? d : dmax;
+      dmin = d < dmin ? d : dmin;
+    }
+    const T tol = T(I) * Traits<T>::eps * dmax;
+    *rank_warning = (dmax == T(0)) || (dmin <= tol);
+  }
+  // Q = H_0 ... H_{r-1} I(I, r): own rows, identity columns first
+  for (int e = tid; e < rows * r; e += nt) {
+    const int i = e % rows, j = e / rows;
+    Q[i64(r0 + i) + i64(j) * I] = (r0 + i == j) ? T(1) : T(0);
+  }
+  __syncthreads();
+  for (int k = r - 1; k >= 0; --k) {
+    const T t = tau[k];
+    if (t == T(0)) continue;  // identical on every CTA
+    const int buf = k & 1;
+    double* pb = part + buf * (kMaxPanelCols + 1);
+    const int ok = k / chunk;
+    const int i0 = max(0, k + 1 - r0);
+    const int ncol = r - k;  // columns j < k are untouched (exactly unchanged in Eigen too)
+    for (int jj = wid; jj < ncol; jj += nw) {
+      const int j = k + jj;
+      double s = 0.0;
+      for (int i = i0 + lane; i < rows; i += 32) s += double(a[i + k * chunk]) * double(Q[i64(r0 + i) + i64(j) * I]);
+      s = warp_sum(s);
+      if (lane == 0) pb[jj] = s;
+    }
+    if (me == ok)
+      for (int jj = tid; jj < ncol; jj += nt) rowk[buf * kMaxPanelCols + jj] = double(Q[i64(k) + i64(k + jj) * I]);
+    cl.sync();  // partials of this step; the other buffer is free (read before the previous barrier)
+    for (int jj = tid; jj < ncol; jj += nt) {
+      double sum = 0.0;
+      for (int q = 0; q < CS; ++q) sum += *cl.map_shared_rank(pb + jj, q);
+      tmp[jj] = double(add_rn(T(sum), T(*cl.map_shared_rank(rowk + buf * kMaxPanelCols + jj, ok))));
+    }
+    __syncthreads();
+    for (int e = tid; e < ncol * rows; e += nt) {
+      const int i = e % rows, jj = e / rows;
+      if (r0 + i < k) continue;
+      T& x = Q[i64(r0 + i) + i64(k + jj) * I];
+      if (r0 + i == k)
+        x = sub_mul_rn(x, t, T(tmp[jj]));
+      else
+        x = sub_mul_rn(x, mul_rn(t, a[i + k * chunk]), T(tmp[jj]));
+    }
+    __syncthreads();
+  }
+  cl.sync();  // no CTA exits while others may still read its shared memory
+}
+
 // -------------------------------------------------------- CholeskyQR2
 // One CTA; Y is I x n column-major (I >= n). work >= I*n doubles.
 // status: 0 = Q written, 1 = fall back to Householder.
@@ -2409,6 +2580,39 @@ int thin_qr(T* A, T* Q, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w, 
     count_launch();
     RCPG_LAUNCHED();
     skip = w.info + 2;  // the Householder kernel below runs only if CholeskyQR2 declined
+  }
+  // (fp64 keeps householder_kernel below: CholeskyQR2's hand-over to it must give the same bits)
+  if (!done && skip == nullptr && R == J && kolda_identity && (w.faithful_qr || path == "cluster_householder")) {
+    // one cluster, panel in distributed shared memory (the faithful Householder of the fp32 configs)
+    static const size_t hh_lim = enable_max_dyn_smem(householder_cluster_kernel<T>);
+    static const bool hh_np = [] {
+      return cudaFuncSetAttribute(householder_cluster_kernel<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+             cudaSuccess;
+    }();
+    const int max_cs = hh_np ? 16 : 8;
+    const size_t fixed = (2 * (kMaxPanelCols + 1) + 2 * kMaxPanelCols) * sizeof(double) + 2 * kMaxPanelCols * sizeof(T);
+    for (int cs = 1; cs <= max_cs; cs *= 2) {
+      const int chunk = int(ceil_div(J, i64(cs)));
+      if (cs < max_cs && chunk > 256) continue;  // ~256 rows per CTA keeps the per-step work short
+      const size_t smem = fixed + size_t(chunk) * n * sizeof(T);
+      if (smem > hh_lim - 1024) continue;
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(cs);
+      cfg.blockDim = dim3(kHhThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = cs;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      RCPG_CUDA(cudaLaunchKernelEx(&cfg, householder_cluster_kernel<T>, (const T*)A, Q, int(J), n, chunk,
+                                   rank_warning_dev));
+      count_launch();
+      return r;
+    }
   }
   init_row_keys(km, J, R, w.keys, st);
   const int maxc = max_coop_blocks(householder_kernel<T>, kFacThreads, 0);

@@ -581,7 +581,7 @@ void sketch_dmma(const double* X, ModeView v, const double* P, i64 cols, double*
   const int BN = pick_bn8(cols);
   const i64 nbt = ceil_div(v.R, kDBK);
   dim3 grid{unsigned(ceil_div(v.I, kDBM)), unsigned(splits), unsigned(ceil_div(cols, BN))};
-  const bool v16 = (v.R % 2 == 0);
+  const bool v16 = (v.R % 2 == 0) && reinterpret_cast<uintptr_t>(X) % 16 == 0 && reinterpret_cast<uintptr_t>(P) % 16 == 0;
 #define RCPG_SK(BNV)                                                                              \
   case BNV:                                                                                       \
     if (v16)                                                                                      \
@@ -603,7 +603,9 @@ void sketch_dmma(const double* X, ModeView v, const double* P, i64 cols, double*
 void project_dmma(const double* X, ModeView v, const double* Q, i64 ldq, i64 cols, double* O, cudaStream_t st) {
   if (project_tma_dispatch<double, double>(X, v, Q, ldq, cols, O, st)) return;
   const int BN = pick_bn8(cols);
-  const bool va = (v.R % 2 == 0), vb = (ldq % 2 == 0);
+  // 16-byte copies need 16-byte aligned rows: even strides and aligned bases (a slab's Q + lo may not be)
+  const bool va = (v.R % 2 == 0) && reinterpret_cast<uintptr_t>(X) % 16 == 0,
+             vb = (ldq % 2 == 0) && reinterpret_cast<uintptr_t>(Q) % 16 == 0;
   for (i64 a0 = 0; a0 < v.L; a0 += 65535) {
     const i64 na = std::min<i64>(65535, v.L - a0);
     dim3 grid{unsigned(ceil_div(v.R, kDBM)), unsigned(na), unsigned(ceil_div(cols, BN))};
