@@ -23,6 +23,7 @@
 
 #include "../../include/rcpg.h"
 #include "als.cuh"
+#include "bcd.cuh"
 #include "common.cuh"
 #include "factor.cuh"
 #include "passes.cuh"
@@ -94,6 +95,7 @@ struct rcpg_context {
   bool fp32_fast = false;
   DevBuf Q64;  // fp64 copy of a small basis (faithful fp32 passes)
   DevBuf B64;  // fp64 copy of the compressed tensor / KR panel (faithful fp32 ALS)
+  DevBuf bcd_res, bcd_loo;  // BCD residual / leave-one-out tensors
   // Omega source (rcpg_set_option "omega_host"): false = generated on the device
   // (CUDA libm, <= a few ulp from glibc), true = generated on the host with the
   // reference's own libm calls and uploaded (bit-identical)
@@ -1119,9 +1121,24 @@ AlsHandles<T> run_als(rcpg_context* c, const T* B, const i64* shape, int order, 
       woff += i64(init_work_doubles(int(shape[m])));
     }
     if (order > 1) init_factors_from_grams<T>(ib, order - 1, R, cfg.seed, cfg.init, c->st);
-    fill_ones<T>(h.weights, R, c->st);
+    if (cfg.method == RCPG_BCD)  // Vector::Zero(rank) (solve.hpp:281)
+      RCPG_CUDA(cudaMemsetAsync(h.weights, 0, size_t(R) * sizeof(T), c->st));
+    else
+      fill_ones<T>(h.weights, R, c->st);
   }
-  {
+  if (cfg.method == RCPG_BCD) {
+    // bcd_solve (solve.hpp:264-376): one cooperative launch
+    if (!bcd_supported(shape, order, R)) fail_after(c, dfr, "bcd: extents above the supported maximum (12288)");
+    ScopedPass sp(c, "bcd_iterations", 0.0);
+    i64 maxe = 1;
+    for (int m = 0; m < order; ++m) maxe = std::max(maxe, shape[m]);
+    const i64 part_elems = 2 * i64(sms) * (maxe + 1);
+    c->als_part.ensure(size_t(part_elems) * sizeof(double));
+    c->bcd_res.ensure(size_t(S) * sizeof(T));
+    c->bcd_loo.ensure(size_t(S) * sizeof(T));
+    bcd_solve<T>(B, c->bcd_res.as<T>(), c->bcd_loo.as<T>(), shape, order, h.fs, h.weights, cfg.tol, cfg.max_iter,
+                 h.tfit, h.tsec, h.state, c->als_part.as<double>(), part_elems, c->bar.as<GridBarrier>(), c->st);
+  } else {
     ScopedPass sp(c, "als_iterations", 0.0);
     const char* als_path = getenv("RCPG_ALS_PATH");  // A/B testing: loop | general
     const bool force_general = als_path != nullptr && std::strcmp(als_path, "general") == 0;
@@ -1293,7 +1310,7 @@ void finish_decompose(rcpg_context* c, const AlsHandles<T>& h, const FactorSet<T
 // solve.hpp:381-398
 template <typename T>
 void run_decompose(rcpg_context* c, const rcpg_tensor* t, const rcpg_decompose_config& cfg, rcpg_result* res) {
-  check_arg(cfg.method == RCPG_ALS, "decompose: only the ALS solver is on this path (bcd is out of scope)");
+  check_arg(cfg.method == RCPG_ALS || cfg.method == RCPG_BCD, "decompose: unknown solver method");
   Deferred dfr;
   check_arg(!(t->slab && !cfg.randomized), "decompose: sharded tensors are decomposed with randomized = true");
   if (!cfg.randomized) {
@@ -1464,7 +1481,7 @@ void rcpg_destroy(rcpg_context* c) {
                     &c->bar, &c->info, &c->part, &c->tau, &c->diag, &c->cqr, &c->als_f, &c->als_g, &c->als_w, &c->als_kr,
                     &c->als_work, &c->als_trace, &c->als_state, &c->weights, &c->small_tmp, &c->nrm, &c->als_part, &c->als_prof, &c->recov})
     b->release();
-  for (DevBuf* b : {&c->Q64, &c->B64}) b->release();
+  for (DevBuf* b : {&c->Q64, &c->B64, &c->bcd_res, &c->bcd_loo}) b->release();
   cudaStreamDestroy(c->st);
   if (c->pool) cudaMemPoolDestroy(c->pool);  // tensors still alive keep their blocks until freed
   delete c;

@@ -338,7 +338,8 @@ __global__ void __launch_bounds__(1024) plu_onchip_kernel(const T* __restrict__ 
                                                           i64 R, KoldaMap km, int W, int* info) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* a = reinterpret_cast<T*>(smem_raw);                   // [n][J]
-  int* phys = reinterpret_cast<int*>(a + i64(J) * n);     // [J] physical row of slot i
+  // [J] physical row of slot i; 8-byte aligned: it first holds one i64 per row (rbase below)
+  int* phys = reinterpret_cast<int*>((reinterpret_cast<uintptr_t>(a + i64(J) * n) + 7) & ~uintptr_t(7));
   int* rowat = phys + J;                                   // [J] slot at physical row p
   __shared__ int col_at[kMaxPanelCols];                    // storage column at physical column q
   __shared__ T red_v[32];
@@ -2431,7 +2432,7 @@ int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w
   }
   // one CTA, rows owned by threads, swaps bookkept
   static const size_t oc_lim = enable_max_dyn_smem(plu_onchip_kernel<T>);
-  const size_t oc_smem = size_t(J) * n * sizeof(T) + 2 * size_t(J) * sizeof(int);
+  const size_t oc_smem = size_t(J) * n * sizeof(T) + 8 + 2 * size_t(J) * sizeof(int);
   // A/B testing: RCPG_LU_PATH = rcluster | cluster | resident | coop starts the
   // chain (one CTA -> one cluster, swaps bookkept -> one cluster, Eigen's
   // physical swaps -> panel resident in the SMs -> grid) further down

@@ -377,3 +377,16 @@ def test_decompose_c2_parity(rcp, oracle):
     model, trace = rcp.decompose(x, g)
     ref = oracle.decompose(x, o)
     _check_fp64(model, trace, ref)
+
+
+def test_decompose_fp32_odd_panels(rcp, oracle):
+    """fp32 with odd panel sizes (mode-2 W is 81 x 9 = 729 floats): the on-chip LU keeps its
+    8-byte row-base scratch aligned behind an odd-length float panel."""
+    x, _ = oracle.random_lowrank([40, 32, 24], 4, 13, snr=4.0, noise_seed=13)
+    x = x.astype(np.float32)
+    g, o = cfgs(rcp, oracle, 4, 5, 2, 3, tol=1e-6, max_iter=300)
+    model, trace = rcp.decompose(x, g)
+    ref = oracle.decompose(x, o)
+    assert trace.iterations == ref.iterations
+    fit_g, fit_o = 1 - trace.final_relative_error ** 2, 1 - ref.final_relative_error ** 2
+    assert abs(fit_g - fit_o) <= 1e-6 * abs(fit_o)

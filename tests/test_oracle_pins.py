@@ -427,3 +427,46 @@ def test_probe_c1_known_values(oracle):
                                                                 seed=oracle.derive_seed(1, oracle.stream_id(1))))
     res = oracle.decompose(x, cfg)
     assert res.iterations == 6 and abs(res.final_relative_error - 0.0992737) < 5e-8
+
+
+# ------------------------------------------------------ BCD (solve.hpp:264-376)
+def check_factors_match(got_f, want_f, tol):  # test_solve.cpp:26-41
+    R = got_f[0].shape[1]
+    for r in range(R):
+        sign_product = 1.0
+        for g, w in zip(got_f, want_f):
+            s = 1.0 if g[:, r] @ w[:, r] >= 0 else -1.0
+            sign_product *= s
+            assert np.max(np.abs(g[:, r] - s * w[:, r])) <= tol
+        assert sign_product == 1.0
+
+
+def test_bcd_rank1_recovery(oracle):  # test_solve.cpp:188-195
+    t, (w, fs) = oracle.random_lowrank([12, 9, 11], 1, 3)
+    res = oracle.decompose(t, det_cfg(oracle, 1, method=1))
+    assert abs(res.weights[0] - w[0]) <= 1e-8 * abs(w[0])
+    check_factors_match(res.factors, fs, 1e-6)
+
+
+def test_bcd_orthogonal_rank2_in_weight_order(oracle):  # test_solve.cpp:197-217
+    rng = np.random.default_rng(5)
+    fs = [oracle.thin_qr(rng.standard_normal((e, 2)))[0] for e in (10, 12, 9)]
+    w, fs = oracle.normalize(np.array([3.0, 1.5]), fs)
+    t = oracle.reconstruct(w, fs)
+    res = oracle.decompose(t, det_cfg(oracle, 2, tol=1e-12, method=1))
+    assert res.final_relative_error <= 1e-6
+    assert np.allclose(res.weights, w, rtol=1e-5)
+    check_factors_match(res.factors, fs, 1e-5)
+
+
+def test_bcd_reports_nonconvergence(oracle):  # test_solve.cpp:219-229
+    clean, _ = oracle.random_lowrank([8, 8, 8], 3, 12)
+    t = oracle.add_noise(clean, 2.0, 1)
+    res = oracle.decompose(t, det_cfg(oracle, 3, tol=1e-300, method=1, max_iter=5))
+    assert not res.converged and res.iterations <= 5
+
+
+def test_bcd_rejects_invalid(oracle):  # test_solve.cpp:161-166
+    t, _ = oracle.random_lowrank([5, 5, 5], 2, 1)
+    with pytest.raises(oracle.OracleInvalidArgument):
+        oracle.decompose(t, det_cfg(oracle, 0, method=1))
