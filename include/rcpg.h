@@ -174,6 +174,18 @@ rcpg_status rcpg_tensor_upload_slab_mode(rcpg_context* ctx, rcpg_dtype dtype, in
 rcpg_status rcpg_relative_error(rcpg_context* ctx, const rcpg_tensor* t, int64_t rank, const void* weights,
                                 const void* factors, double* out);
 
+/* ---- bound validation (compress.hpp:148-164, diagnostics.hpp:36-86) ---- */
+/* projection_residual: ||t - t x_n Q_n Q_n^T ...||_F over the compressed modes of
+ * `c` (the result of rcpg_compress on t); fp64 accumulation. */
+rcpg_status rcpg_projection_residual(rcpg_context* ctx, const rcpg_tensor* t, const rcpg_compressed* c, double* out);
+/* theorem_bound: per-mode tail energies sum_{j >= k} sigma_j^2 of every unfolding
+ * (tail_energies[order]) and bound = sqrt(1 + k/(p-1)) sqrt(sum of tails);
+ * k >= 2, p >= 2, k < every extent <= 2048. (validate_bound = this plus `trials`
+ * rcpg_compress(q = 0) / rcpg_projection_residual calls with the trial seeds;
+ * see include/rcp_b200/rcp.hpp.) */
+rcpg_status rcpg_theorem_bound(rcpg_context* ctx, const rcpg_tensor* t, int64_t k, int64_t p, double* tail_energies,
+                               double* bound);
+
 /* ---- diagnostics (not on the reference API; used by tests/bench) -------- */
 /* Materializes Omega_n (rows x cols, column-major) exactly as compress.hpp:118-124
  * draws it, on the device, and copies it to host. */

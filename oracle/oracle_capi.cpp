@@ -300,6 +300,19 @@ int ro_projection_residual_d(int order, const std::int64_t* shape, const double*
   return projection_residual_impl<double>(order, shape, x, cfg, out);
 }
 
+// theorem_bound / validate_bound (diagnostics.hpp:36-86): tails[order], bound,
+// and (trials > 0) the mean projection residual of `trials` q = 0 compressions.
+int ro_validate_bound_d(int order, const std::int64_t* shape, const double* x, std::int64_t k, std::int64_t p,
+                        int trials, std::uint64_t seed, double* tails, double* bound, double* mean) {
+  return guarded([&] {
+    auto t = make_tensor(order, shape, x);
+    const BoundReport r = trials > 0 ? validate_bound_on(t, k, p, trials, seed) : theorem_bound(t, k, p);
+    for (int m = 0; m < order; ++m) tails[m] = r.tail_energies[std::size_t(m)];
+    *bound = r.bound;
+    *mean = r.empirical_mean;
+  });
+}
+
 // init_factors (solve.hpp:93-131): out = concatenated column-major I_n x R.
 int ro_init_factors_d(int order, const std::int64_t* shape, const double* x, std::int64_t rank,
                       std::uint64_t seed, int method, double* out) {

@@ -89,6 +89,7 @@ def lib():
             "ro_decompose_d": [I, V, V, V, V, V, V, V, V, V, V, V],
             "ro_decompose_f": [I, V, V, V, V, V, V, V, V, V, V, V],
             "ro_projection_residual_d": [I, V, V, V, V],
+            "ro_validate_bound_d": [I, V, V, L, L, I, U, V, V, V],
             "ro_init_factors_d": [I, V, V, L, U, I, V],
             "ro_normalize_d": [I, V, L, V, V, V, V],
             "ro_reconstruct_d": [I, V, L, V, V, V],
@@ -338,6 +339,18 @@ def projection_residual(x: np.ndarray, cfg: CompressConfig) -> float:
     out = C.c_double(0)
     _check(lib().ro_projection_residual_d(x.ndim, sp, _p(x, dp), C.byref(c), C.byref(out)))
     return out.value
+
+
+def theorem_bound(x: np.ndarray, k: int, p: int, trials: int = 0, seed: int = 0):
+    """theorem_bound (diagnostics.hpp:36-62) -> (tail_energies, bound); with trials > 0 also the
+    validate_bound (diagnostics.hpp:68-86) mean projection residual on this tensor."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    s, sp = _shape(x.shape)
+    tails = np.zeros(x.ndim)
+    b, m = C.c_double(0), C.c_double(0)
+    _check(lib().ro_validate_bound_d(x.ndim, sp, _p(x, dp), C.c_int64(k), C.c_int64(p), int(trials),
+                                     C.c_uint64(seed), _p(tails, dp), C.byref(b), C.byref(m)))
+    return (tails, b.value) if trials <= 0 else (tails, b.value, m.value)
 
 
 def decompose(x: np.ndarray, cfg: DecomposeConfig) -> Result:

@@ -1547,4 +1547,112 @@ Kruskal<S> synth_model(int kind, const Shape& shape, Index rank, std::uint64_t s
   return k;
 }
 
+
+// ---------------------------------------------------------- diagnostics.hpp
+// Singular values of an m x n matrix (one-sided Jacobi on the columns of A^T,
+// fp64): the restatement of Eigen::JacobiSVD's singularValues() that
+// theorem_bound uses (diagnostics.hpp:47-51) -- relatively accurate, so
+// noise-level trailing singular values are kept rather than deflated to 0.
+inline std::vector<double> singular_values(const Matrix<double>& a) {
+  const Index m = a.rows(), n = a.cols();
+  // work on the tall orientation: columns = the shorter side
+  const bool tr = m < n;
+  const Index rows = tr ? n : m, cols = tr ? m : n;
+  std::vector<double> u(std::size_t(rows) * std::size_t(cols));
+  for (Index j = 0; j < cols; ++j)
+    for (Index i = 0; i < rows; ++i) u[std::size_t(i + j * rows)] = tr ? a(j, i) : a(i, j);
+  auto col = [&](Index j) { return u.data() + std::size_t(j) * std::size_t(rows); };
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    bool rotated = false;
+    for (Index p = 0; p < cols - 1; ++p)
+      for (Index q = p + 1; q < cols; ++q) {
+        double alpha = 0.0, beta = 0.0, gamma = 0.0;
+        const double* up = col(p);
+        const double* uq = col(q);
+        for (Index i = 0; i < rows; ++i) {
+          alpha += up[i] * up[i];
+          beta += uq[i] * uq[i];
+          gamma += up[i] * uq[i];
+        }
+        if (gamma == 0.0 || std::abs(gamma) <= 1e-15 * std::sqrt(alpha * beta)) continue;
+        rotated = true;
+        const double zeta = (beta - alpha) / (2.0 * gamma);
+        const double t = (zeta >= 0 ? 1.0 : -1.0) / (std::abs(zeta) + std::sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / std::sqrt(1.0 + t * t), sn = c * t;
+        double* wp = col(p);
+        double* wq = col(q);
+        for (Index i = 0; i < rows; ++i) {
+          const double x = wp[i], y = wq[i];
+          wp[i] = c * x - sn * y;
+          wq[i] = sn * x + c * y;
+        }
+      }
+    if (!rotated) break;
+  }
+  std::vector<double> sv(static_cast<std::size_t>(cols));
+  for (Index j = 0; j < cols; ++j) {
+    double ss = 0.0;
+    const double* w = col(j);
+    for (Index i = 0; i < rows; ++i) ss += w[i] * w[i];
+    sv[std::size_t(j)] = std::sqrt(ss);
+  }
+  std::sort(sv.begin(), sv.end(), std::greater<double>());
+  return sv;
+}
+
+// diagnostics.hpp:23-31
+struct BoundReport {
+  std::vector<double> tail_energies;
+  double bound = 0.0;
+  double empirical_mean = std::numeric_limits<double>::quiet_NaN();
+  int trials = 0;
+  Index k = 0;
+  Index p = 0;
+};
+
+// diagnostics.hpp:36-62
+template <typename S>
+BoundReport theorem_bound(const Tensor<S>& t, Index k, Index p) {
+  check(k >= 2, "theorem_bound: k must be at least 2");
+  check(p >= 2, "theorem_bound: oversampling must be at least 2");
+  for (Index m = 0; m < t.order(); ++m)
+    check(k < t.extent(m), "theorem_bound: k must be smaller than every mode extent");
+  BoundReport report;
+  report.k = k;
+  report.p = p;
+  double total_tail = 0.0;
+  for (Index m = 0; m < t.order(); ++m) {
+    const Matrix<S> um = unfold(t, m);
+    Matrix<double> ud(um.rows(), um.cols());
+    for (std::size_t i = 0; i < um.v.size(); ++i) ud.v[i] = double(um.v[i]);
+    const std::vector<double> sv = singular_values(ud);
+    double tail = 0.0;
+    for (Index j = k; j < Index(sv.size()); ++j) tail += sv[std::size_t(j)] * sv[std::size_t(j)];
+    report.tail_energies.push_back(tail);
+    total_tail += tail;
+  }
+  report.bound = std::sqrt(1.0 + double(k) / double(p - 1)) * std::sqrt(total_tail);
+  return report;
+}
+
+// diagnostics.hpp:68-86 on a given tensor (validate_bound draws it with
+// random_lowrank<double>(shape, rank, seed) first; callers do that here)
+template <typename S>
+BoundReport validate_bound_on(const Tensor<S>& dense, Index k, Index p, int trials, std::uint64_t seed) {
+  check(trials >= 1, "validate_bound: need at least one trial");
+  BoundReport report = theorem_bound(dense, k, p);
+  report.trials = trials;
+  double sum = 0.0;
+  for (int trial = 0; trial < trials; ++trial) {
+    CompressConfig cfg;
+    cfg.target_rank = k;
+    cfg.oversampling = p;
+    cfg.power_iterations = 0;
+    cfg.seed = derive_seed(seed, stream_id(StreamDomain::trial, std::uint64_t(trial)));
+    sum += projection_residual(dense, compress(dense, cfg));
+  }
+  report.empirical_mean = sum / trials;
+  return report;
+}
+
 }  // namespace rcpo

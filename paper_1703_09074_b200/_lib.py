@@ -112,6 +112,8 @@ SIGNATURES = {
     "rcpg_synth": (_I32, [_V, C.c_int, _I32, _V, _I64, _V, _V, _D, _U64, C.POINTER(C.c_void_p)]),
     "rcpg_synchronize": (_I32, [_V]),
     "rcpg_set_option": (_I32, [_V, C.c_char_p, _I64]),
+    "rcpg_projection_residual": (_I32, [_V, _V, _V, C.POINTER(C.c_double)]),
+    "rcpg_theorem_bound": (_I32, [_V, _V, _I64, _I64, _V, C.POINTER(C.c_double)]),
     "rcpg_get_option": (_I32, [_V, C.c_char_p, C.POINTER(C.c_int64)]),
     "rcpg_bench_factor": (_I32, [_V, C.c_int, _I32, _I64, _I64, _I32, C.POINTER(C.c_double)]),
     "rcpg_event_record": (_I32, [_V, _I32]),

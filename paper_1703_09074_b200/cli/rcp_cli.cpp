@@ -6,7 +6,7 @@
 //
 //   rcp synth --shape 100,100,100 --rank 10 [--snr 10] [--seed S] --out x.dten
 //             [--truth t.kten] [--csv-export x.csv] [--dtype f64|f32]
-//   rcp decompose --in x.dten --rank R [--method als] [--deterministic]
+//   rcp decompose --in x.dten --rank R [--method als|bcd] [--deterministic]
 //             [--oversample P] [--power-iters Q] [--modes 1,2] [--tol T]
 //             [--max-iter N] [--seed S] --out m.kten [--trace fit.csv]
 //   rcp reconstruct --in m.kten --out x.dten [--csv-export x.csv]
@@ -14,7 +14,7 @@
 // Exit codes (main.cpp:289-311): 0 success (decompose: converged), 2 decompose
 // ran to max_iter without converging, 1 on any error (parse errors included).
 // Not carried over: `bound`, `bench` (diagnostics sweeps) and `--toy-video`
-// (demo generator); `--method bcd` reaches the library, which rejects it.
+// (demo generator).
 // --dtype is an extension: the fp32 configs are stored as dtype-1 files.
 #include <chrono>
 #include <cstdio>

@@ -1480,6 +1480,45 @@ void init_factors_from_grams(const InitBatch<T>& b, int count, int rank, u64 see
 
 size_t init_work_doubles(int n) { return 2 * size_t(n) * size_t(n | 1) + 4 * size_t(n) + 64; }
 
+namespace {
+// Tail energy of one Gram G = X_(m) X_(m)^T (n x n, fp64): the sum of its
+// n - k smallest eigenvalues (clamped at 0) = sum_{j >= k} sigma_j^2 of the
+// unfolding (diagnostics.hpp:47-58), one CTA per mode.
+__global__ void __launch_bounds__(kSmallThreads) gram_tail_kernel(TailBatch b, int k, double* out) {
+  const int q = blockIdx.x, n = b.n[q], tid = threadIdx.x, nt = blockDim.x;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const bool in_smem = n <= kEigSmemMax;
+  const int ld = n | 1;
+  double* work = b.work[q];
+  double* A = in_smem ? reinterpret_cast<double*>(smem_raw) : work;
+  double* V = A + i64(n) * ld;
+  double* ev = work + 2 * i64(n) * ld;
+  int* ord = reinterpret_cast<int*>(ev + n);
+  for (i64 e = tid; e < i64(n) * n; e += nt) A[(e % n) + (e / n) * ld] = b.G[q][e];
+  __syncthreads();
+  jacobi_eig(A, V, n, ld, ev, ord);
+  if (tid == 0) {
+    double t = 0.0;
+    for (int j = 0; j < n - k; ++j) t += ev[j] > 0.0 ? ev[j] : 0.0;  // ascending: the n - k smallest
+    out[q] = t;
+  }
+}
+}  // namespace
+
+void gram_tails(const TailBatch& b, int count, int k, double* out, cudaStream_t st) {
+  check_arg(count >= 1 && count <= kMaxOrder, "theorem_bound: mode count");
+  size_t smem = 0;
+  for (int q = 0; q < count; ++q) {
+    check_arg(b.n[q] <= 2 * kMaxRank * 8, "theorem_bound: extents up to 2048");
+    if (b.n[q] <= kEigSmemMax) smem = std::max(smem, 2 * size_t(b.n[q]) * size_t(b.n[q] | 1) * sizeof(double));
+  }
+  static const size_t lim = enable_max_dyn_smem(gram_tail_kernel);
+  (void)lim;
+  gram_tail_kernel<<<count, kSmallThreads, smem, st>>>(b, k, out);
+  count_launch();
+  RCPG_LAUNCHED();
+}
+
 template <typename T>
 void zero_factor(T* factor, i64 extent, int rank, T* gram_out, cudaStream_t st) {
   zero_factor_kernel<T><<<64, 256, 0, st>>>(factor, extent, rank, gram_out);

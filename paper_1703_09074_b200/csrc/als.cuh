@@ -56,6 +56,16 @@ template <typename T>
 void init_factors_from_grams(const InitBatch<T>& b, int count, int rank, u64 seed, int method, cudaStream_t st);
 // doubles of `work` one mode of extent n needs
 size_t init_work_doubles(int n);
+
+// theorem_bound (diagnostics.hpp:36-62): per mode q, the tail energy
+// sum_{j >= k} sigma_j^2 of the unfolding from the eigenvalues of its Gram
+// G[q] (n[q] x n[q], fp64, n <= 2048); work[q] >= init_work_doubles(n[q]).
+struct TailBatch {
+  const double* G[kMaxOrder];
+  int n[kMaxOrder];
+  double* work[kMaxOrder];
+};
+void gram_tails(const TailBatch& b, int count, int k, double* out, cudaStream_t st);
 template <typename T>
 void zero_factor(T* factor, i64 extent, int rank, T* gram_out, cudaStream_t st);
 

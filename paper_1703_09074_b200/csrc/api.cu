@@ -1769,6 +1769,177 @@ rcpg_status rcpg_tensor_upload_slab(rcpg_context* c, rcpg_dtype dtype, int32_t o
   return rcpg_tensor_upload_slab_mode(c, dtype, order, global_shape, order - 1, lo, hi, host_slab, out);
 }
 
+// ------------------------------------------------- bound validation
+}  // extern "C"
+
+namespace {
+
+template <typename T>
+__global__ void transpose_kernel(const T* __restrict__ Q, i64 I, i64 l, T* __restrict__ Qt) {
+  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < I * l; e += i64(gridDim.x) * blockDim.x) {
+    const i64 i = e % I, c = e / I;
+    Qt[c + i * l] = Q[e];
+  }
+}
+
+// per-block partials of sum (a - b)^2 in fp64
+template <typename T>
+__global__ void diff_sumsq_kernel(const T* __restrict__ a, const T* __restrict__ b, i64 n, double* part) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < n; e += i64(gridDim.x) * blockDim.x) {
+    const double d = double(a[e]) - double(b[e]);
+    acc += d * d;
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) s += red[w];
+    part[blockIdx.x] = s;
+  }
+}
+
+// projection_residual (compress.hpp:148-164): ||t - t x_n Q_n Q_n^T (compressed modes)||_F,
+// each product rounded to Scalar as the reference's Matrix<Scalar> products, the
+// residual accumulated in fp64.
+template <typename T>
+double run_projection_residual(rcpg_context* c, const rcpg_tensor* t, const rcpg_compressed* comp) {
+  const int order = t->order;
+  check_arg(int(comp->bases.size()) >= order && comp->order == order, "projection_residual: need one basis per mode");
+  for (int n = 0; n < order; ++n) {
+    const BasisRec& bs = comp->bases[n];
+    check_arg(bs.dim == t->shape[n], "projection_residual: basis extent mismatch");
+  }
+  const bool mixed = std::is_same<T, float>::value && !c->fp32_fast;
+  const T* cur = static_cast<const T*>(t->d);
+  int which = 0;
+  for (int n = 0; n < order; ++n) {
+    const BasisRec& bs = comp->bases[n];
+    if (bs.identity) continue;
+    const i64 I = t->shape[n], l = bs.cols;
+    const ModeView v = mode_view(t->shape, order, n);
+    const ModeView v2{v.L, l, v.R};
+    c->panelA.ensure(size_t(v.L) * l * v.R * sizeof(T));                 // B = Q^T P_(n)
+    c->Qy.ensure(size_t(I) * l * sizeof(T));                              // Q^T (l x I)
+    T* B = c->panelA.as<T>();
+    T* Qt = c->Qy.as<T>();
+    const T* Q = bs.q.as<T>();
+    transpose_kernel<T><<<grid_for(I * l), 256, 0, c->st>>>(Q, I, l, Qt);
+    count_launch();
+    DevBuf& dst = which == 0 ? c->work0 : c->work1;
+    dst.ensure(size_t(t->size) * sizeof(T));
+    if constexpr (std::is_same<T, float>::value) {
+      if (mixed) {
+        c->Q64.ensure(size_t(I) * l * sizeof(double));
+        c->B64.ensure(size_t(I) * l * sizeof(double));
+        widen_f32(Q, c->Q64.as<double>(), I * l, c->st);
+        widen_f32(Qt, c->B64.as<double>(), I * l, c->st);
+        project_mixed(cur, v, c->Q64.as<double>(), I, l, B, c->st);
+        project_mixed(B, v2, c->B64.as<double>(), l, I, dst.as<float>(), c->st);
+      }
+    }
+    if (!mixed) {
+      project<T>(cur, v, Q, I, l, B, c->st);
+      project<T>(B, v2, Qt, l, I, dst.as<T>(), c->st);
+    }
+    cur = dst.as<T>();
+    which ^= 1;
+  }
+  const int blocks = grid_for(t->size);
+  c->scratch.ensure(size_t(blocks) * sizeof(double));
+  diff_sumsq_kernel<T><<<blocks, 256, 0, c->st>>>(static_cast<const T*>(t->d), cur, t->size, c->scratch.as<double>());
+  count_launch();
+  RCPG_LAUNCHED();
+  std::vector<double> part(static_cast<size_t>(blocks));
+  RCPG_CUDA(cudaMemcpyAsync(part.data(), c->scratch.p, part.size() * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  RCPG_CUDA(cudaStreamSynchronize(c->st));
+  double s = 0.0;
+  for (double x : part) s += x;
+  return std::sqrt(s);
+}
+
+// theorem_bound (diagnostics.hpp:36-62): tail energies from the Gram of every
+// unfolding (fp64 products on the DMMA passes), bound = sqrt(1 + k / (p - 1)) sqrt(sum of tails)
+template <typename T>
+void run_theorem_bound(rcpg_context* c, const rcpg_tensor* t, i64 k, i64 p, double* tails, double* bound) {
+  check_arg(k >= 2, "theorem_bound: k must be at least 2");
+  check_arg(p >= 2, "theorem_bound: oversampling must be at least 2");
+  const int order = t->order;
+  for (int m = 0; m < order; ++m)
+    check_arg(k < t->shape[m], "theorem_bound: k must be smaller than every mode extent");
+  for (int m = 0; m < order; ++m)
+    check_arg(t->shape[m] <= 2048, "theorem_bound: extents up to 2048 (Gram eigenvalues on one SM)");
+  const int sms = device_caps().num_sms;
+  i64 gram_elems = 0, work_doubles = 0;
+  for (int m = 0; m < order; ++m) {
+    gram_elems += t->shape[m] * t->shape[m];
+    work_doubles += i64(init_work_doubles(int(t->shape[m])));
+  }
+  c->als_w.ensure(size_t(gram_elems) * sizeof(double));
+  c->als_work.ensure(size_t(work_doubles) * sizeof(double));
+  double* X64 = nullptr;
+  if (std::is_same<T, float>::value) {
+    c->B64.ensure(size_t(t->size) * sizeof(double));
+    X64 = c->B64.as<double>();
+    widen_f32(reinterpret_cast<const float*>(t->d), X64, t->size, c->st);
+  }
+  TailBatch tb{};
+  i64 goff = 0, woff = 0;
+  for (int m = 0; m < order; ++m) {
+    const ModeView v = mode_view(t->shape, order, m);
+    double* G = c->als_w.as<double>() + goff;
+    if (X64 != nullptr) {
+      const i64 scr = sketch_mixed_scratch_doubles(v, t->shape[m], sms);
+      c->scratch.ensure(size_t(scr) * sizeof(double));
+      sketch_mixed(reinterpret_cast<const float*>(t->d), v, X64, t->shape[m], G, c->scratch.as<double>(), scr, sms,
+                   c->st);
+    } else {
+      const i64 scr = sketch_scratch_elems<double>(v, t->shape[m], sms);
+      c->scratch.ensure(size_t(scr) * sizeof(double));
+      sketch<double>(static_cast<const double*>(t->d), v, static_cast<const double*>(t->d), t->shape[m], G,
+                     c->scratch.as<double>(), scr, sms, c->st);
+    }
+    tb.G[m] = G;
+    tb.n[m] = int(t->shape[m]);
+    tb.work[m] = c->als_work.as<double>() + woff;
+    goff += t->shape[m] * t->shape[m];
+    woff += i64(init_work_doubles(int(t->shape[m])));
+  }
+  gram_tails(tb, order, int(k), slots(c) + 16, c->st);
+  RCPG_CUDA(cudaMemcpyAsync(tails, slots(c) + 16, size_t(order) * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  RCPG_CUDA(cudaStreamSynchronize(c->st));
+  double total = 0.0;
+  for (int m = 0; m < order; ++m) total += tails[m];
+  *bound = std::sqrt(1.0 + double(k) / double(p - 1)) * std::sqrt(total);
+}
+
+}  // namespace
+
+extern "C" {
+
+rcpg_status rcpg_projection_residual(rcpg_context* c, const rcpg_tensor* t, const rcpg_compressed* comp, double* out) {
+  return guarded(c, [&] {
+    check_arg(t != nullptr && comp != nullptr && out != nullptr, "projection_residual: null argument");
+    check_arg(!t->slab, "projection_residual: sharded tensors are not supported");
+    check_arg(comp->dtype == t->dtype, "projection_residual: dtype mismatch");
+    *out = t->dtype == RCPG_F64 ? run_projection_residual<double>(c, t, comp) : run_projection_residual<float>(c, t, comp);
+  });
+}
+
+rcpg_status rcpg_theorem_bound(rcpg_context* c, const rcpg_tensor* t, int64_t k, int64_t p, double* tail_energies,
+                               double* bound) {
+  return guarded(c, [&] {
+    check_arg(t != nullptr && tail_energies != nullptr && bound != nullptr, "theorem_bound: null argument");
+    check_arg(!t->slab, "theorem_bound: sharded tensors are not supported");
+    if (t->dtype == RCPG_F64)
+      run_theorem_bound<double>(c, t, k, p, tail_energies, bound);
+    else
+      run_theorem_bound<float>(c, t, k, p, tail_energies, bound);
+  });
+}
+
 rcpg_status rcpg_relative_error(rcpg_context* c, const rcpg_tensor* t, int64_t rank, const void* weights,
                                 const void* factors, double* out) {
   return guarded(c, [&] {

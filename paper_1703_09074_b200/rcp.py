@@ -33,7 +33,7 @@ GAUSSIAN, UNIFORM = 0, 1          # rcp::RandomDistribution
 LU, QR = 0, 1                      # rcp::PowerStabilizer
 ALS, BCD = 0, 1                    # rcp::SolveMethod
 EIGENVECTORS, RANDOM = 0, 1        # rcp::InitMethod
-COMPRESS, INIT, FACTORS, NOISE = 1, 2, 3, 4  # rcp::StreamDomain
+COMPRESS, INIT, FACTORS, NOISE, PHASES, TRIAL = 1, 2, 3, 4, 5, 6  # rcp::StreamDomain (random.hpp:39-46)
 
 
 class SolverError(RuntimeError):
@@ -400,6 +400,75 @@ def compress(t, cfg: CompressConfig, ctx: Optional[Context] = None) -> Compressi
         finally:
             ctx.lib.rcpg_compressed_free(h)
         return CompressionResult(out, bases)
+    finally:
+        if tmp:
+            dt.free()
+
+
+def projection_residual(t, cfg: CompressConfig, ctx: Optional[Context] = None) -> float:
+    """projection_residual(t, compress(t, cfg)) (compress.hpp:148-164) on the GPU."""
+    ctx = ctx or default_context()
+    dt, tmp = _as_device(t, ctx)
+    try:
+        c, keep = cfg._c()
+        h = C.c_void_p()
+        ctx.check(ctx.lib.rcpg_compress(ctx.h, dt.h, C.byref(c), C.byref(h)))
+        try:
+            out = C.c_double()
+            ctx.check(ctx.lib.rcpg_projection_residual(ctx.h, dt.h, h, C.byref(out)))
+            return out.value
+        finally:
+            ctx.lib.rcpg_compressed_free(h)
+    finally:
+        if tmp:
+            dt.free()
+
+
+@dataclass
+class BoundReport:
+    """rcp::BoundReport (diagnostics.hpp:23-31)."""
+    tail_energies: List[float]
+    bound: float
+    empirical_mean: float = float("nan")
+    trials: int = 0
+    k: int = 0
+    p: int = 0
+
+
+def theorem_bound(t, k: int, p: int, ctx: Optional[Context] = None) -> BoundReport:
+    """theorem_bound (diagnostics.hpp:36-62) on the GPU: per-mode tail energies of every
+    unfolding (Gram eigenvalues, fp64) and sqrt(1 + k/(p-1)) sqrt(sum of tails)."""
+    ctx = ctx or default_context()
+    dt, tmp = _as_device(t, ctx)
+    try:
+        tails = np.zeros(len(dt.shape))
+        b = C.c_double()
+        ctx.check(ctx.lib.rcpg_theorem_bound(ctx.h, dt.h, int(k), int(p), tails.ctypes.data, C.byref(b)))
+        return BoundReport([float(x) for x in tails], b.value, k=int(k), p=int(p))
+    finally:
+        if tmp:
+            dt.free()
+
+
+def validate_bound(t, k: int, p: int, trials: int, seed: int, ctx: Optional[Context] = None) -> BoundReport:
+    """validate_bound (diagnostics.hpp:68-86) on a given tensor (the reference draws it with
+    random_lowrank<double>(shape, rank, seed)): the theorem bound and the mean projection
+    residual of `trials` single-pass compressions (q = 0) with seeds
+    derive_seed(seed, stream_id(trial, t))."""
+    if trials < 1:
+        raise ValueError("validate_bound: need at least one trial")
+    ctx = ctx or default_context()
+    dt, tmp = _as_device(t, ctx)
+    try:
+        rep = theorem_bound(dt, k, p, ctx=ctx)
+        total = 0.0
+        for trial in range(trials):
+            cfg = CompressConfig(target_rank=k, oversampling=p, power_iterations=0,
+                                 seed=derive_seed(seed, stream_id(TRIAL, trial)))
+            total += projection_residual(dt, cfg, ctx=ctx)
+        rep.trials = trials
+        rep.empirical_mean = total / trials
+        return rep
     finally:
         if tmp:
             dt.free()

@@ -470,3 +470,23 @@ def test_bcd_rejects_invalid(oracle):  # test_solve.cpp:161-166
     t, _ = oracle.random_lowrank([5, 5, 5], 2, 1)
     with pytest.raises(oracle.OracleInvalidArgument):
         oracle.decompose(t, det_cfg(oracle, 0, method=1))
+
+
+# ------------------------------------------------ diagnostics.hpp (bound)
+def test_theorem_bound_tails_are_svd_tails(oracle):  # diagnostics.hpp:36-62
+    x, _ = oracle.random_lowrank([12, 10, 9], 4, 2, snr=3.0, noise_seed=2)
+    tails, bound = oracle.theorem_bound(x, 3, 4)
+    for m in range(3):
+        sv = np.linalg.svd(oracle.unfold(x, m), compute_uv=False)
+        assert abs(tails[m] - np.sum(sv[3:] ** 2)) <= 1e-12 * np.sum(sv ** 2)
+    assert abs(bound - np.sqrt(1 + 3 / 3) * np.sqrt(tails.sum())) <= 1e-14 * bound
+    with pytest.raises(oracle.OracleInvalidArgument):
+        oracle.theorem_bound(x, 1, 4)
+    with pytest.raises(oracle.OracleInvalidArgument):
+        oracle.theorem_bound(x, 9, 4)
+
+
+def test_validate_bound_holds_below_rank(oracle):  # diagnostics.hpp:68-86 (acceptance criterion 4 shape)
+    x, _ = oracle.random_lowrank([15, 15, 15], 6, 8)
+    tails, bound, mean = oracle.theorem_bound(x, 3, 4, trials=10, seed=5)
+    assert 0 < mean <= bound

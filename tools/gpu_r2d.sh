@@ -1,2 +1,2 @@
 #!/bin/bash
-timeout 900 python -m pytest tests/test_gpu_bcd.py tests/test_gpu_parity.py -q -x 2>&1 | tail -15
+timeout 900 python -m pytest tests/test_gpu_bound.py tests/test_gpu_bcd.py -q -x 2>&1 | tail -25
