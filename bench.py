@@ -355,6 +355,23 @@ def cpu_baseline_single(cfg, x_host, c):
             "relerr": r["relerr"], "iterations": r["iterations"]}
 
 
+def lu_sweep_bytes(cfg) -> float:
+    """Algorithmic HBM traffic of the faithful complete-pivoting LUs of the W = X_(n)^T Q panels
+    (compress.hpp:127-132): at pivot k the trailing J x (l - k) panel is read
+    once to find the next pivot, sum_k J (l - k) b bytes per LU, q LUs per compressed mode."""
+    shape = list(cfg.shape)
+    b = np.dtype(cfg.dtype).itemsize
+    total = 0.0
+    for n in range(len(shape)):
+        l = min(cfg.rank + cfg.oversampling, shape[n])
+        if l >= shape[n]:
+            continue
+        J = float(np.prod(shape)) / shape[n]
+        total += cfg.power_iterations * J * b * l * (l + 1) / 2.0
+        shape[n] = l
+    return total
+
+
 def pass_roofline(pass_ms, pass_bytes, steps):
     peak, peak_kind = measured_peaks()
     sm_ms = sum(pass_ms.get(n, 0.0) for n in STREAMED_TIME)
@@ -539,7 +556,14 @@ def main():
             "relerr": trace.final_relative_error, "iterations": trace.iterations, "converged": trace.converged,
             "passes": passes,
         }
-        if cfg.dtype == np.float64 and sm_ms > 0:
+        lu_ms = pass_ms.get("stab_w", 0.0) / args.steps
+        if lu_ms > 0:
+            lb = lu_sweep_bytes(cfg)
+            line["lu_roofline"] = {"bound": "hbm", "achieved": lb / 1e9 / (lu_ms / 1e3), "peak": peak, "unit": "GB/s",
+                                   "frac": lb / 1e9 / (lu_ms / 1e3) / peak, "bytes_per_step": lb, "ms_per_step": lu_ms,
+                                   "kernel": "complete-pivoting LU of the W panels (stab_w; one trailing-panel "
+                                             "read per pivot)"}
+        if sm_ms > 0:  # fp64 data, and fp32 data in the faithful arithmetic, run the passes on DMMA
             tf = streamed_flops(cfg) * args.steps / (sm_ms / 1e3) / 1e12
             line["fp64_pipe"] = {"achieved": tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                                  "frac": tf / FP64_PEAK_TFLOPS,

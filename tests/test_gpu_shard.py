@@ -62,7 +62,8 @@ def _check_vs_single(got, want, tol):
 
 @pytest.mark.parametrize("shape,nranks,mode", [((40, 30, 20), 2, -1), ((40, 30, 21), 3, -1), ((12, 10, 14, 9), 2, -1),
                                                ((30, 24, 50), 4, -1), ((40, 30, 20), 2, 0), ((41, 30, 22), 3, 0),
-                                               ((14, 10, 12, 9), 2, 0), ((64, 20, 18), 4, 0)])
+                                               ((14, 10, 12, 9), 2, 0), ((64, 20, 18), 4, 0),
+                                               ((40, 30, 24), 8, -1), ((64, 20, 18), 8, 0)])
 def test_sharded_decompose_matches_single(rcp, oracle, shape, nranks, mode):
     x, _ = oracle.random_lowrank(list(shape), 4, 11, snr=3.0, noise_seed=11)
     cfg = _cfg(rcp, 4, 5, 2, 7)
