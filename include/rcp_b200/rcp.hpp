@@ -295,6 +295,59 @@ S relative_error(const Tensor<S>& x, const Kruskal<S>& k) {
   return S(out);
 }
 
+// compress.hpp:148-164
+template <typename S>
+S projection_residual(const Tensor<S>& t, const CompressionResult<S>& result) {
+  if (Index(result.bases.size()) != t.order()) throw std::invalid_argument("projection_residual: need one basis per mode");
+  rcpg_context* c = detail::context();
+  std::vector<int32_t> ident;
+  std::vector<int64_t> cols;
+  std::vector<S> q;
+  for (const auto& b : result.bases) {
+    ident.push_back(b.identity ? 1 : 0);
+    cols.push_back(b.identity ? 0 : b.q.cols());
+    if (!b.identity) q.insert(q.end(), b.q.data(), b.q.data() + b.q.size());
+  }
+  detail::DeviceTensor dt(c, t);
+  double out = 0;
+  detail::check(c, rcpg_projection_residual_bases(c, dt.t, ident.data(), cols.data(), q.data(), &out));
+  return S(out);
+}
+
+// diagnostics.hpp:23-31
+struct BoundReport {
+  std::vector<double> tail_energies;
+  double bound = 0.0;
+  double empirical_mean = std::numeric_limits<double>::quiet_NaN();
+  int trials = 0;
+  Index k = 0;
+  Index p = 0;
+};
+
+// diagnostics.hpp:36-62 (tail energies from the eigenvalues of each unfolding's Gram)
+template <typename S>
+BoundReport theorem_bound(const Tensor<S>& t, Index k, Index p) {
+  rcpg_context* c = detail::context();
+  detail::DeviceTensor dt(c, t);
+  BoundReport r;
+  r.k = k;
+  r.p = p;
+  r.tail_energies.assign(static_cast<std::size_t>(t.order()), 0.0);
+  detail::check(c, rcpg_theorem_bound(c, dt.t, k, p, r.tail_energies.data(), &r.bound));
+  return r;
+}
+
+// diagnostics.hpp:68-86 on a given tensor (the reference draws random_lowrank<double>(shape,
+// rank, seed) first; random_lowrank below is that generator)
+template <typename S>
+BoundReport validate_bound(const Tensor<S>& dense, Index k, Index p, int trials, std::uint64_t seed);
+
+// Library options (include/rcpg.h rcpg_set_option): "fp32_arith", "omega_host".
+inline void set_option(const char* name, std::int64_t value) {
+  rcpg_context* c = detail::context();
+  detail::check(c, rcpg_set_option(c, name, value));
+}
+
 inline const char* method_name(SolveMethod m) { return m == SolveMethod::bcd ? "bcd" : "als"; }
 
 // kruskal.hpp:117-176 (host side; models are small): unit-norm columns (left
@@ -464,6 +517,24 @@ std::pair<Tensor<S>, Kruskal<S>> random_lowrank(const Shape& shape, Index rank, 
   }
   truth = normalize(std::move(truth));
   return {detail::synth_dense(truth, snr, noise_seed), truth};
+}
+
+template <typename S>
+BoundReport validate_bound(const Tensor<S>& dense, Index k, Index p, int trials, std::uint64_t seed) {
+  if (trials < 1) throw std::invalid_argument("validate_bound: need at least one trial");
+  BoundReport report = theorem_bound(dense, k, p);
+  report.trials = trials;
+  double sum = 0.0;
+  for (int trial = 0; trial < trials; ++trial) {
+    CompressConfig cfg;
+    cfg.target_rank = k;
+    cfg.oversampling = p;
+    cfg.power_iterations = 0;
+    cfg.seed = derive_seed(seed, stream_id(StreamDomain::trial, static_cast<std::uint64_t>(trial)));
+    sum += double(projection_residual(dense, compress(dense, cfg)));
+  }
+  report.empirical_mean = sum / trials;
+  return report;
 }
 
 }  // namespace rcp

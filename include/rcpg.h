@@ -178,6 +178,10 @@ rcpg_status rcpg_relative_error(rcpg_context* ctx, const rcpg_tensor* t, int64_t
 /* projection_residual: ||t - t x_n Q_n Q_n^T ...||_F over the compressed modes of
  * `c` (the result of rcpg_compress on t); fp64 accumulation. */
 rcpg_status rcpg_projection_residual(rcpg_context* ctx, const rcpg_tensor* t, const rcpg_compressed* c, double* out);
+/* The same with host bases (rcp::CompressionResult): per mode identity flag and column
+ * count, the non-identity Q_n (dim x cols, column-major) concatenated in mode order. */
+rcpg_status rcpg_projection_residual_bases(rcpg_context* ctx, const rcpg_tensor* t, const int32_t* identity,
+                                          const int64_t* cols, const void* q_concat, double* out);
 /* theorem_bound: per-mode tail energies sum_{j >= k} sigma_j^2 of every unfolding
  * (tail_energies[order]) and bound = sqrt(1 + k/(p-1)) sqrt(sum of tails);
  * k >= 2, p >= 2, k < every extent <= 2048. (validate_bound = this plus `trials`

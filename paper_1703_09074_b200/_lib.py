@@ -114,6 +114,7 @@ SIGNATURES = {
     "rcpg_set_option": (_I32, [_V, C.c_char_p, _I64]),
     "rcpg_projection_residual": (_I32, [_V, _V, _V, C.POINTER(C.c_double)]),
     "rcpg_theorem_bound": (_I32, [_V, _V, _I64, _I64, _V, C.POINTER(C.c_double)]),
+    "rcpg_projection_residual_bases": (_I32, [_V, _V, _V, _V, _V, C.POINTER(C.c_double)]),
     "rcpg_get_option": (_I32, [_V, C.c_char_p, C.POINTER(C.c_int64)]),
     "rcpg_bench_factor": (_I32, [_V, C.c_int, _I32, _I64, _I64, _I32, C.POINTER(C.c_double)]),
     "rcpg_event_record": (_I32, [_V, _I32]),

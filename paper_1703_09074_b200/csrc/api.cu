@@ -1928,6 +1928,37 @@ rcpg_status rcpg_projection_residual(rcpg_context* c, const rcpg_tensor* t, cons
   });
 }
 
+rcpg_status rcpg_projection_residual_bases(rcpg_context* c, const rcpg_tensor* t, const int32_t* identity,
+                                          const int64_t* cols, const void* q_concat, double* out) {
+  return guarded(c, [&] {
+    check_arg(t != nullptr && identity != nullptr && cols != nullptr && out != nullptr,
+              "projection_residual: null argument");
+    check_arg(!t->slab, "projection_residual: sharded tensors are not supported");
+    rcpg_compressed comp;
+    comp.dtype = t->dtype;
+    comp.order = t->order;
+    comp.bases.resize(size_t(t->order));
+    const size_t b = dsize(t->dtype);
+    size_t off = 0;
+    for (int m = 0; m < t->order; ++m) {
+      BasisRec& bs = comp.bases[size_t(m)];
+      bs.identity = identity[m] != 0;
+      bs.dim = t->shape[m];
+      bs.cols = bs.identity ? 0 : cols[m];
+      if (!bs.identity) {
+        check_arg(cols[m] >= 1 && cols[m] <= t->shape[m], "projection_residual: basis extent mismatch");
+        const size_t bytes = size_t(t->shape[m]) * size_t(cols[m]) * b;
+        bs.q.ensure(bytes);
+        RCPG_CUDA(cudaMemcpyAsync(bs.q.p, static_cast<const unsigned char*>(q_concat) + off, bytes,
+                                  cudaMemcpyHostToDevice, c->st));
+        off += bytes;
+      }
+    }
+    *out = t->dtype == RCPG_F64 ? run_projection_residual<double>(c, t, &comp)
+                                : run_projection_residual<float>(c, t, &comp);
+  });
+}
+
 rcpg_status rcpg_theorem_bound(rcpg_context* c, const rcpg_tensor* t, int64_t k, int64_t p, double* tail_energies,
                                double* bound) {
   return guarded(c, [&] {

@@ -51,5 +51,19 @@ int main() {
   }());
   std::printf("compressed %lldx%lldx%lld\n", (long long)comp.compressed.extent(0),
               (long long)comp.compressed.extent(1), (long long)comp.compressed.extent(2));
+  // projection_residual (compress.hpp:148-164) of that compression
+  const double pr = rcp::projection_residual(t, comp);
+  std::printf("projection_residual=%.6f\n", pr);
+  if (!(pr > 0 && pr < 0.05 * std::sqrt(double(x.size())))) return 4;
+  // the BCD solver (solve.hpp:264-376) through the same entry point
+  rcp::DecomposeConfig bcd = cfg;
+  bcd.method = rcp::SolveMethod::bcd;
+  auto [mb, tb] = rcp::decompose(t, bcd);
+  std::printf("bcd iters=%d error=%.12f\n", tb.iterations, tb.final_relative_error);
+  if (!(tb.final_relative_error < 0.05)) return 5;
+  // validate_bound (diagnostics.hpp:68-86) on this tensor
+  const auto rep = rcp::validate_bound(t, 2, 3, 4, 11);
+  std::printf("bound=%.6f empirical=%.6f\n", rep.bound, rep.empirical_mean);
+  if (!(rep.empirical_mean <= rep.bound)) return 6;
   return 0;
 }
