@@ -119,6 +119,8 @@ def parse():
                     help="skip the scaling_config (C3) sub-record")
     ap.add_argument("--host-check", action="store_true",
                     help="launch / process-group / max-over-ranks plumbing only (no GPU work; CPU tests)")
+    ap.add_argument("--fast-fp32", action="store_true",
+                    help="fp32_arith = 1: 3xTF32 tcgen05 passes (not bit-faithful to the reference)")
     ap.add_argument("--omega-host", action="store_true",
                     help="Omega evaluated on the host and uploaded (bit-identical; slower)")
     return ap.parse_args()
@@ -372,6 +374,33 @@ def lu_sweep_bytes(cfg) -> float:
     return total
 
 
+def binding_roofline(cfg, pass_ms, pass_bytes, steps, fast_fp32=False, traffic=None):
+    """Roofline of the streamed passes against their binding roof.
+
+    The passes run on the FP64 tensor cores (DMMA) for fp64 data and, in the default faithful
+    fp32 arithmetic, for fp32 data too; at l = 30..80 their arithmetic intensity (2 l flops per
+    element) puts them above the DMMA ridge, so the binding roof is the FP64 tensor pipe
+    (bound "tensor", TFLOP/s); the fast 3xTF32 fp32 path (fp32_arith = 1) is HBM-bound.
+    Both fractions are reported; `frac` is the binding one."""
+    peak, peak_kind = measured_peaks()
+    sm_ms, achieved, _, _ = pass_roofline(pass_ms, pass_bytes, steps)
+    fl = streamed_flops(cfg)
+    by = sum(pass_bytes.get(n, 0.0) for n in STREAMED) / steps
+    hbm = {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak if peak else None,
+           "peak_source": peak_kind}
+    t_pipe, t_hbm = fl / (FP64_PEAK_TFLOPS * 1e12), by / (peak * 1e9)
+    if not fast_fp32 and t_pipe >= t_hbm and sm_ms > 0:
+        tf = fl * steps / (sm_ms / 1e3) / 1e12
+        return {"bound": "tensor", "achieved": tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": tf / FP64_PEAK_TFLOPS, "traffic": traffic,
+                "kernel": "streamed mode-n passes on the FP64 tensor cores (Omega + sketch / X^T Q / X Z / projection)",
+                "peak_source": "own DMMA microbenchmark (tools/microbench/fp64_peak.cu, 37.0 TFLOP/s); "
+                               "MEASURED_PEAKS.json has no FP64 entry",
+                "flops_per_step": fl, "hbm": hbm}
+    return dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=hbm["frac"], traffic=traffic,
+                kernel="streamed mode-n passes (Omega + sketch / X^T Q / X Z / projection)", peak_source=peak_kind)
+
+
 def pass_roofline(pass_ms, pass_bytes, steps):
     peak, peak_kind = measured_peaks()
     sm_ms = sum(pass_ms.get(n, 0.0) for n in STREAMED_TIME)
@@ -443,10 +472,7 @@ def scaling_record(args, dist, rcp, synthetic, ctx, world, rank, shard):
             "scaling": "strong" if shard else "weak",
             "parallelism": (shard_desc(cfg, world) if shard else "single GPU"),
             "gpu_launches": int(launches),
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak if peak else None,
-                         "kernel": "streamed mode-n passes (Omega + sketch / X^T Q / X Z / projection)",
-                         "peak_source": peak_kind},
+            "roofline": binding_roofline(cfg, pass_ms, pass_bytes, steps, fast_fp32=ctx.get_option("fp32_arith") == 1),
             "passes_ms": {n: pass_ms[n] / steps for n in pass_ms},
             "relerr": trace.final_relative_error, "iterations": trace.iterations}
 
@@ -481,6 +507,8 @@ def main():
     ctx = rcp.Context(local)
     if args.omega_host:
         ctx.set_option("omega_host", 1)
+    if args.fast_fp32:
+        ctx.set_option("fp32_arith", 1)
     # N > 1: one decomposition sharded in slabs along the slab mode, the
     # library's own NCCL communicator (id broadcast through torch.distributed)
     shard = (world > 1 and not args.replicas) or args.shard
@@ -546,12 +574,13 @@ def main():
                        "parallelism": (shard_desc(cfg, world) if shard
                                        else ("replicas" if world > 1 else "single GPU")),
                        "l2": "tensor larger than L2 (no flush needed)" if cfg.nbytes() > 126e6 else "L2-resident",
-                       "omega": "host-evaluated, uploaded" if args.omega_host else "device"},
+                       "omega": "host-evaluated, uploaded" if args.omega_host else "device",
+                       "fp32_arith": ("fast 3xTF32" if args.fast_fp32 else "faithful (fp64 products and sums)")
+                       if cfg.dtype == np.float32 else "fp64"},
             "gpu_launches": int(launches),
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak if peak else None, "traffic": profile_traffic(cfg.name),
-                         "kernel": "streamed mode-n passes (Omega + sketch / X^T Q / X Z / projection)",
-                         "peak_source": peak_kind},
+            "roofline": binding_roofline(cfg, pass_ms, pass_bytes, args.steps,
+                                         fast_fp32=ctx.get_option("fp32_arith") == 1,
+                                         traffic=profile_traffic(cfg.name)),
             "clocks": clk.summary(),
             "relerr": trace.final_relative_error, "iterations": trace.iterations, "converged": trace.converged,
             "passes": passes,
@@ -563,11 +592,6 @@ def main():
                                    "frac": lb / 1e9 / (lu_ms / 1e3) / peak, "bytes_per_step": lb, "ms_per_step": lu_ms,
                                    "kernel": "complete-pivoting LU of the W panels (stab_w; one trailing-panel "
                                              "read per pivot)"}
-        if sm_ms > 0:  # fp64 data, and fp32 data in the faithful arithmetic, run the passes on DMMA
-            tf = streamed_flops(cfg) * args.steps / (sm_ms / 1e3) / 1e12
-            line["fp64_pipe"] = {"achieved": tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                                 "frac": tf / FP64_PEAK_TFLOPS,
-                                 "peak_source": "tools/microbench/fp64_peak.cu (own measurement)"}
         if e2e:
             line["e2e"] = e2e
         if scaling:
