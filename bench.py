@@ -34,7 +34,9 @@ sys.path.insert(0, ROOT)
 
 STREAMED = ("sketch", "power_xtq", "power_xz", "project")
 # Omega is generated into a panel before the sketch (SURVEY.md 8(d) counts its bytes as 0):
-# its time is charged to the streamed passes
+# when generated in line ("omega") its time is charged to the streamed passes; by default
+# it is generated on a side stream concurrently with the input check ("omega_overlapped",
+# off the critical path, not charged)
 STREAMED_TIME = STREAMED + ("omega",)
 # FP64 DMMA / DFMA peak measured on this pool's B200 by tools/microbench/fp64_peak.cu
 # (not in MEASURED_PEAKS.json, which carries HBM and bf16 only)

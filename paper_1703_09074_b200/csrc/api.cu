@@ -101,6 +101,11 @@ struct rcpg_context {
   // reference's own libm calls and uploaded (bit-identical)
   bool omega_host = false;
   cudaMemPool_t pool = nullptr;  // private pool of the device tensors (rcpg_tensor_*)
+  // Omega of every compressed mode generated up front on a side stream, concurrently
+  // with the input check (it depends only on shapes and the seed)
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_omega[kMaxOrder] = {};
+  DevBuf omega_buf;
 };
 
 struct rcpg_tensor {
@@ -144,7 +149,7 @@ namespace {
 size_t dsize(int dtype) { return dtype == RCPG_F64 ? 8 : 4; }
 
 // --------------------------------------------------------------- timing
-void pass_begin(rcpg_context* c, const char* name, double bytes) {
+void pass_begin(rcpg_context* c, const char* name, double bytes, cudaStream_t st = nullptr) {
   if (!c->timing) return;
   if (c->pass_used == c->passes.size()) {
     PassRecord r;
@@ -155,11 +160,11 @@ void pass_begin(rcpg_context* c, const char* name, double bytes) {
   PassRecord& r = c->passes[c->pass_used];
   r.name = name;
   r.bytes = bytes;
-  RCPG_CUDA(cudaEventRecord(r.a, c->st));
+  RCPG_CUDA(cudaEventRecord(r.a, st ? st : c->st));
 }
-void pass_end(rcpg_context* c) noexcept {
+void pass_end(rcpg_context* c, cudaStream_t st = nullptr) noexcept {
   if (!c->timing || c->pass_used >= c->passes.size()) return;
-  if (cudaEventRecord(c->passes[c->pass_used].b, c->st) != cudaSuccess) (void)cudaGetLastError();
+  if (cudaEventRecord(c->passes[c->pass_used].b, st ? st : c->st) != cudaSuccess) (void)cudaGetLastError();
   ++c->pass_used;
 }
 
@@ -331,7 +336,8 @@ void finish_compress(rcpg_context* c, rcpg_compressed* out, const Deferred& dfr)
 // the new working tensor.
 template <typename T>
 const T* compress_mode_local(rcpg_context* c, const CompressCfg& cfg, int n, i64* shape, int order, const T* cur,
-                             int& which, BasisRec& basis, Deferred& dfr) {
+                             int& which, BasisRec& basis, Deferred& dfr, const void* pre_omega = nullptr,
+                             cudaEvent_t pre_ev = nullptr) {
   const int sms = device_caps().num_sms;
   const i64 extent = shape[n];
   const i64 l = std::min(cfg.target_rank + cfg.oversampling, extent);
@@ -370,13 +376,17 @@ const T* compress_mode_local(rcpg_context* c, const CompressCfg& cfg, int n, i64
       float* Zf = dst.as<float>();  // free until the projection
       double* Q64 = c->Q64.as<double>();
       double* scr = c->scratch.as<double>();
-      {
+      const double* Om = P64;
+      if (pre_omega != nullptr) {  // generated on the side stream (precompute_omega)
+        RCPG_CUDA(cudaStreamWaitEvent(c->st, pre_ev, 0));
+        Om = static_cast<const double*>(pre_omega);
+      } else {
         ScopedPass sp(c, "omega", 0.0);
         make_omega<double>(c, cfg.seed, n, km, v, l, cfg.distribution, P64, 2, c->st);
       }
       {
         ScopedPass sp(c, "sketch", (S + extent * l) * b);
-        sketch_mixed(cur, v, P64, l, Y, scr, scr64, sms, c->st);
+        sketch_mixed(cur, v, Om, l, Y, scr, scr64, sms, c->st);
       }
       i64 ycols = l;
       for (int it = 0; it < cfg.power_iterations; ++it) {
@@ -428,13 +438,17 @@ const T* compress_mode_local(rcpg_context* c, const CompressCfg& cfg, int n, i64
     }
   }
 
-  {
+  const T* Om = P;
+  if (pre_omega != nullptr) {
+    RCPG_CUDA(cudaStreamWaitEvent(c->st, pre_ev, 0));
+    Om = static_cast<const T*>(pre_omega);
+  } else {
     ScopedPass sp(c, "omega", 0.0);
     make_omega<T>(c, cfg.seed, n, km, v, l, cfg.distribution, P, sizeof(T) == 4 ? 0 : 1, c->st);
   }
   {
     ScopedPass sp(c, "sketch", (S + extent * l) * b);
-    sketch<T>(cur, v, P, l, Y, c->scratch.as<T>(), scr, sms, c->st);
+    sketch<T>(cur, v, Om, l, Y, c->scratch.as<T>(), scr, sms, c->st);
   }
   i64 ycols = l;
   for (int it = 0; it < cfg.power_iterations; ++it) {
@@ -503,6 +517,54 @@ const T* compress_mode_local(rcpg_context* c, const CompressCfg& cfg, int n, i64
 }
 
 
+// Omega_n of every mode that will be compressed, generated up front on the side
+// stream st2 (after all earlier work of the main stream), so it runs concurrently
+// with the input check: it depends only on the shapes and the seed. off[n] < 0:
+// mode n not planned (identity, or Omega from the host). Returns false when
+// nothing was launched (host Omega).
+template <typename T>
+bool precompute_omega(rcpg_context* c, const CompressCfg& cfg, const i64* shape0, int order,
+                      const std::set<i64>& selected, i64* off) {
+  for (int n = 0; n < order; ++n) off[n] = -1;
+  if (c->omega_host) return false;
+  const bool mixed = std::is_same<T, float>::value && !c->fp32_fast;
+  const size_t esz = mixed ? sizeof(double) : sizeof(T);
+  i64 shape[kMaxOrder];
+  for (int m = 0; m < order; ++m) shape[m] = shape0[m];
+  i64 total = 0;
+  struct Plan {
+    ModeView v;
+    KoldaMap km;
+    i64 l;
+  } plan[kMaxOrder];
+  for (int n = 0; n < order; ++n) {
+    const i64 l = std::min(cfg.target_rank + cfg.oversampling, shape[n]);
+    if (selected.count(n) == 0 || l >= shape[n] || l > kMaxPanelCols) continue;
+    plan[n] = Plan{mode_view(shape, order, n), mode_kolda(shape, order, n), l};
+    off[n] = total;
+    total += ceil_div(plan[n].v.L * plan[n].v.R * l * i64(esz), 256) * 256;  // 256-byte aligned panels
+    shape[n] = l;
+  }
+  if (total == 0) return false;
+  c->omega_buf.ensure(size_t(total));
+  RCPG_CUDA(cudaEventRecord(c->ev_start, c->st));
+  RCPG_CUDA(cudaStreamWaitEvent(c->st2, c->ev_start, 0));
+  pass_begin(c, "omega_overlapped", 0.0, c->st2);
+  for (int n = 0; n < order; ++n) {
+    if (off[n] < 0) continue;
+    unsigned char* dst = static_cast<unsigned char*>(c->omega_buf.p) + off[n];
+    if (mixed)
+      omega_panel_f32_as_f64(cfg.seed, n, plan[n].km, plan[n].v, plan[n].l, cfg.distribution,
+                             reinterpret_cast<double*>(dst), c->st2);
+    else
+      omega_panel<T>(cfg.seed, n, plan[n].km, plan[n].v, plan[n].l, cfg.distribution, reinterpret_cast<T*>(dst),
+                     c->st2);
+    RCPG_CUDA(cudaEventRecord(c->ev_omega[n], c->st2));
+  }
+  pass_end(c, c->st2);
+  return true;
+}
+
 // compress.hpp:86-146. With `sync_checks` false the input check is left in
 // the device slots (Deferred::compress_input) for the caller to raise.
 template <typename T>
@@ -513,22 +575,29 @@ void run_compress(rcpg_context* c, const rcpg_tensor* t, const CompressCfg& cfg,
   check_arg(cfg.power_iterations >= 0, "compress: power iteration count must be non-negative");
   const int order = t->order;
   const int sms = device_caps().num_sms;
+  std::set<i64> selected;
+  bool mode_error = false;
+  if (cfg.modes_present) {
+    for (i64 m : cfg.modes) {
+      if (!(m >= 0 && m < order)) {
+        mode_error = true;
+        continue;
+      }
+      selected.insert(m);
+    }
+  } else {
+    for (i64 m = 0; m < order; ++m) selected.insert(m);
+  }
+  i64 omega_off[kMaxOrder];
+  const bool pre = !mode_error && precompute_omega<T>(c, cfg, t->shape, order, selected, omega_off);
   {
     ScopedPass sp(c, "check_finite", double(t->size) * sizeof(T));
     c->scratch.ensure(size_t(sms) * 8 * sizeof(double) + 64);
     norm_and_finite<T>(static_cast<const T*>(t->d), t->size, slots(c) + kXSum, c->scratch.as<double>(), sms, c->st);
   }
   dfr.compress_input = true;
-
-  std::set<i64> selected;
-  if (cfg.modes_present) {
-    for (i64 m : cfg.modes) {
-      if (!(m >= 0 && m < order)) fail_after(c, dfr, "compress: mode index out of range");
-      selected.insert(m);
-    }
-  } else {
-    for (i64 m = 0; m < order; ++m) selected.insert(m);
-  }
+  // validation order (compress.hpp:89-97): the finite check comes before the mode range
+  if (mode_error) fail_after(c, dfr, "compress: mode index out of range");
 
   i64 shape[kMaxOrder];
   for (int m = 0; m < order; ++m) shape[m] = t->shape[m];
@@ -551,7 +620,10 @@ void run_compress(rcpg_context* c, const rcpg_tensor* t, const CompressCfg& cfg,
       basis.identity = true;
       continue;
     }
-    cur = compress_mode_local<T>(c, cfg, n, shape, order, cur, which, basis, dfr);
+    const bool have = pre && omega_off[n] >= 0;
+    cur = compress_mode_local<T>(c, cfg, n, shape, order, cur, which, basis, dfr,
+                                 have ? static_cast<unsigned char*>(c->omega_buf.p) + omega_off[n] : nullptr,
+                                 have ? c->ev_omega[n] : nullptr);
   }
   out->dtype = t->dtype;
   out->order = order;
@@ -1431,6 +1503,9 @@ rcpg_status rcpg_create(int device, rcpg_context** out) {
     if (device < 0 || device >= n) throw CudaFailure("rcpg_create: no such CUDA device", cudaErrorInvalidDevice);
     RCPG_CUDA(cudaSetDevice(device));
     RCPG_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    RCPG_CUDA(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+    RCPG_CUDA(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
+    for (auto& e : c->ev_omega) RCPG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     // uploaded tensors come from a private stream-ordered pool that keeps freed
     // blocks (per-call uploads reuse them); the device's default pool, which
     // other libraries in the host process share, is left untouched
@@ -1481,7 +1556,12 @@ void rcpg_destroy(rcpg_context* c) {
                     &c->bar, &c->info, &c->part, &c->tau, &c->diag, &c->cqr, &c->als_f, &c->als_g, &c->als_w, &c->als_kr,
                     &c->als_work, &c->als_trace, &c->als_state, &c->weights, &c->small_tmp, &c->nrm, &c->als_part, &c->als_prof, &c->recov})
     b->release();
-  for (DevBuf* b : {&c->Q64, &c->B64, &c->bcd_res, &c->bcd_loo}) b->release();
+  cudaStreamSynchronize(c->st2);
+  for (DevBuf* b : {&c->Q64, &c->B64, &c->bcd_res, &c->bcd_loo, &c->omega_buf}) b->release();
+  if (c->ev_start) cudaEventDestroy(c->ev_start);
+  for (auto& e : c->ev_omega)
+    if (e) cudaEventDestroy(e);
+  if (c->st2) cudaStreamDestroy(c->st2);
   cudaStreamDestroy(c->st);
   if (c->pool) cudaMemPoolDestroy(c->pool);  // tensors still alive keep their blocks until freed
   delete c;

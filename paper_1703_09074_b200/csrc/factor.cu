@@ -626,6 +626,13 @@ __device__ __forceinline__ unsigned long long lu_timer() {
 }
 
 constexpr int kLuThreads = 256;
+// minimum CTAs per SM of the grid LU: 3 caps it at 85 registers (3 x 256 threads
+// per SM): the read-latency-bound sweep gets 50% more bytes in flight. C4's LUs
+// 75.6 ms at 1 (255 registers allowed), 54.3 ms at the compiler's default (128
+// registers, 2 CTAs), 51.3 ms at 3 (tools/ab_r2.sh)
+#ifndef RCPG_LU_MINB
+#define RCPG_LU_MINB 3
+#endif
 
 // V consecutive panel rows per thread (16-byte loads/stores when V > 1): the
 // sweep is read-latency bound, so V multiplies the bytes each load keeps in
@@ -646,7 +653,7 @@ __device__ __forceinline__ void st_lv(T* p, const LuVec<T, V>& v) {
 }
 
 template <typename T, int V>
-__global__ void __launch_bounds__(kLuThreads) plu_coop_kernel(LuArgs<T> p) {
+__global__ void __launch_bounds__(kLuThreads, RCPG_LU_MINB) plu_coop_kernel(LuArgs<T> p) {
   __shared__ Cand<T> red[33];
   __shared__ int pcol_of[kMaxPanelCols], col_at[kMaxPanelCols];
   __shared__ T U[kMaxPanelCols], Uprev[kMaxPanelCols];
@@ -2594,7 +2601,11 @@ int thin_qr(T* A, T* Q, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w, 
     const size_t fixed = (2 * (kMaxPanelCols + 1) + 2 * kMaxPanelCols) * sizeof(double) + 2 * kMaxPanelCols * sizeof(T);
     for (int cs = 1; cs <= max_cs; cs *= 2) {
       const int chunk = int(ceil_div(J, i64(cs)));
-      if (cs < max_cs && chunk > 256) continue;  // ~256 rows per CTA keeps the per-step work short
+      static const int hh_rows = [] {  // rows per CTA targeted (A/B: RCPG_HH_ROWS)
+        const char* e = std::getenv("RCPG_HH_ROWS");
+        return e ? std::max(16, atoi(e)) : 64;
+      }();
+      if (cs < max_cs && chunk > hh_rows) continue;  // <= 64 rows per CTA: the largest cluster wins (1024 x 70: 16 CTAs 0.74 ms, 4 CTAs 1.45 ms)
       const size_t smem = fixed + size_t(chunk) * n * sizeof(T);
       if (smem > hh_lim - 1024) continue;
       cudaLaunchConfig_t cfg{};
