@@ -390,3 +390,35 @@ def test_decompose_fp32_odd_panels(rcp, oracle):
     assert trace.iterations == ref.iterations
     fit_g, fit_o = 1 - trace.final_relative_error ** 2, 1 - ref.final_relative_error ** 2
     assert abs(fit_g - fit_o) <= 1e-6 * abs(fit_o)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_decompose_graph_replay_identical(rcp, oracle, dtype):
+    """Repeated identical calls: the second is captured as a CUDA graph and later ones replay it.
+    Every call returns the same bits and counts the same kernel launches; a changed
+    configuration falls back to stream launches and still matches the oracle."""
+    x, _ = oracle.random_lowrank([40, 36, 30], 4, 7, snr=3.0, noise_seed=7)
+    x = x.astype(dtype)
+    ctx = rcp.Context(0)
+    X = rcp.DeviceTensor.upload(x, ctx=ctx)
+    g, o = cfgs(rcp, oracle, 4, 5, 2, 5, tol=1e-8 if dtype == np.float64 else 1e-6)
+    outs, launches = [], []
+    for _ in range(4):
+        l0 = ctx.kernel_launches()
+        outs.append(rcp.decompose(X, g, ctx=ctx))
+        launches.append(ctx.kernel_launches() - l0)
+    m0, t0 = outs[0]
+    for m, t in outs[1:]:
+        assert t.iterations == t0.iterations and t.final_relative_error == t0.final_relative_error
+        assert np.array_equal(m.weights, m0.weights)
+        for a, b in zip(m.factors, m0.factors):
+            assert np.array_equal(a, b)
+    assert len(set(launches)) == 1 and launches[0] > 10, launches
+    timings = ctx.pass_timings()
+    assert any(n == "sketch" and ms > 0 for n, ms, _ in timings)
+    ref = oracle.decompose(x, o)
+    assert t0.iterations == ref.iterations
+    g2, o2 = cfgs(rcp, oracle, 4, 5, 1, 5, tol=1e-8 if dtype == np.float64 else 1e-6)
+    m2, t2 = rcp.decompose(X, g2, ctx=ctx)
+    assert t2.iterations == oracle.decompose(x, o2).iterations
+    X.free()
