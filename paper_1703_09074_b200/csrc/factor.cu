@@ -2445,7 +2445,13 @@ int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w
   // physical swaps -> panel resident in the SMs -> grid) further down
   const char* lp = std::getenv("RCPG_LU_PATH");
   const std::string lpath = lp ? lp : "";
-  if (oc_smem <= oc_lim && J * i64(n) < (i64(1) << 31) && lpath.empty()) {
+  // from ~640 rows an 8-CTA cluster beats one CTA (C2's 900 x 30 W: 156 -> 110 us;
+  // its 400 x 30 samples stay faster on one CTA: 69 vs 90 us; tools/ab_r2b.sh)
+  static const i64 oc_rows = [] {
+    const char* e = std::getenv("RCPG_LU_ONCHIP_ROWS");
+    return e ? i64(atoll(e)) : i64(640);
+  }();
+  if (oc_smem <= oc_lim && J * i64(n) < (i64(1) << 31) && lpath.empty() && J < oc_rows) {
     // W row lanes (whole warps) x tpr column groups, at most 1024 threads
     const int W = int(std::min<i64>(1024, ceil_div(J, 32) * 32));
     const char* tp = std::getenv("RCPG_LU_TPR");
@@ -2474,7 +2480,8 @@ int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w
   const int max_cs = nonportable ? 16 : 8;
   int want_cs = 8;
   while (want_cs < max_cs && J > 128 * i64(want_cs)) want_cs *= 2;
-  const int min_cs = mcs ? std::max(1, atoi(mcs)) : 1;
+  // a panel the one-CTA kernel declined for size goes straight to the 8-CTA cluster
+  const int min_cs = mcs ? std::max(1, atoi(mcs)) : (J >= oc_rows && oc_smem <= oc_lim ? 8 : 1);
   for (int cs = 1; cs <= max_cs && lpath != "coop" && lpath != "resident"; cs *= 2) {
     if (cs < min_cs || (mcs == nullptr && cs > 1 && cs < want_cs)) continue;
     const int chunk = int(ceil_div(J, cs));
