@@ -6,6 +6,8 @@
 // fit, stopping test) runs in one CTA so a whole ALS iteration is a handful
 // of launches with no host round trip; each launch first checks the
 // device-side `done` flag so the host can enqueue iterations ahead.
+#include <cooperative_groups.h>
+
 #include <cfloat>
 #include <type_traits>
 
@@ -753,8 +755,20 @@ __device__ __forceinline__ void als_dmma(double (&c)[4], double a0, double a1, d
                : "d"(a0), "d"(a1), "d"(b0));
 }
 
-template <typename T, int BATCH>
+// CLUSTER: the grid is one thread-block cluster (<= 16 CTAs, small compressed
+// tensors such as C1 / C2): the hardware cluster barrier replaces the grid
+// barrier (release / acquire at cluster scope orders the global-memory partials
+// and factors exactly like grid_sync), ~2 us less per barrier, three per mode step.
+template <typename T, int BATCH, bool CLUSTER = false>
 __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p) {
+  auto gsync = [&]() {
+    if constexpr (CLUSTER) {
+      __threadfence();
+      cooperative_groups::this_cluster().sync();
+    } else {
+      grid_sync(p.bar);
+    }
+  };
   __shared__ int pidx[BATCH * kMaxOrder];
   __shared__ int sfoff[kMaxOrder], sext[kMaxOrder];
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -949,7 +963,7 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
         p.prof[23] += tp1 - ts;
         p.prof[24] = G;
       }
-      grid_sync(p.bar);
+      gsync();
       unsigned long long tp2 = 0;
       if (p.prof && g == 0 && tid == 0) tp2 = gtimer();
       // ---- reduction of the partials, spread over all CTAs (fixed CTA
@@ -983,7 +997,7 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
           if (on && l == 0) Wg[o] = s;
         }
       }
-      grid_sync(p.bar);
+      gsync();
       // ---- B: mode update on CTA 0
       if (g == 0) {
         double* W = sm;                   // I x R
@@ -1002,7 +1016,7 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
       unsigned long long tp3 = 0;
       if (p.prof && g == 0 && tid == 0) tp3 = gtimer();
       parity ^= 1;
-      grid_sync(p.bar);
+      gsync();
       if (p.prof && g == 0 && tid == 0) {
         const unsigned long long tp4 = gtimer();
         p.prof[0] += tp1 - tp0;
@@ -1605,13 +1619,53 @@ void als_loop(const T* B, const i64* shape, int order, const FactorSet<T>& fs, T
     G = std::max(G, 1);
     const bool split_ok = want_split && G >= 3 && (2 * i64(G) + 2) * maxout <= part_elems;
     a.pm = split_ok ? part + (2 * i64(G) + 1) * maxout : nullptr;
-    launch_coop(kern, G, kAlsThreads, smem, st, a);
+    return G;
   };
   const size_t s64 = als_loop_smem<T, 64>(shape, order, R);
-  if (s64 <= 180 * 1024)
-    run(als_loop_kernel<T, 64>, s64, 64);
+  const bool b64 = s64 <= 180 * 1024;
+  const size_t smem = b64 ? s64 : als_loop_smem<T, 32>(shape, order, R);
+  const int G = b64 ? run(als_loop_kernel<T, 64>, smem, 64) : run(als_loop_kernel<T, 32>, smem, 32);
+  // small grids run as one thread-block cluster (cluster barriers); RCPG_ALS_CLUSTER=0 (A/B) keeps the grid
+  static const bool cl_np = [] {
+    return cudaFuncSetAttribute(als_loop_kernel<T, 64, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+               cudaSuccess &&
+           cudaFuncSetAttribute(als_loop_kernel<T, 32, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+               cudaSuccess;
+  }();
+  static const bool cl_off = [] {
+    const char* e = std::getenv("RCPG_ALS_CLUSTER");
+    return e != nullptr && e[0] == '0';
+  }();
+  if (!cl_off && G >= 2 && G <= (cl_np ? 16 : 8)) {
+    auto kern = b64 ? als_loop_kernel<T, 64, true> : als_loop_kernel<T, 32, true>;
+    static const size_t l64c = enable_max_dyn_smem(als_loop_kernel<T, 64, true>);
+    static const size_t l32c = enable_max_dyn_smem(als_loop_kernel<T, 32, true>);
+    if (smem <= (b64 ? l64c : l32c)) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(G);
+      cfg.blockDim = dim3(kAlsThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = G;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) == cudaSuccess && nclusters >= 1) {
+        RCPG_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+        count_launch();
+        return;
+      }
+      (void)cudaGetLastError();
+    }
+  }
+  if (b64)
+    launch_coop(als_loop_kernel<T, 64>, G, kAlsThreads, smem, st, a);
   else
-    run(als_loop_kernel<T, 32>, als_loop_smem<T, 32>(shape, order, R), 32);
+    launch_coop(als_loop_kernel<T, 32>, G, kAlsThreads, smem, st, a);
 }
 
 template <typename T>
