@@ -12,10 +12,13 @@ and the model copied out inside the timed region.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
 
 Multi-GPU: one process per GPU (torchrun; `--gpus N` without torchrun re-launches
-itself under torch.distributed.run with N ranks). The tensor is sharded in slabs
-along the BASELINE slab mode (C5: mode 1, else the last) and decomposed collectively; value = the
-max over ranks of the device time. The same line carries `scaling_config`: C3
-(1024^3 fp32, BASELINE's sharded config) timed the same way at this N.
+itself under torch.distributed.run with N ranks). The configs BASELINE.json shards
+(C3 along mode 3, C4 along mode 4, C5 along mode 1) are split in slabs and decomposed
+collectively (strong scaling, value = the max over ranks of the
+device time). C1 / C2 are single-GPU configs in BASELINE.json: at N > 1 every rank
+decomposes its own tensor (replicas, weak scaling). The line carries
+`scaling_config` (C3) and `scaling_config_C5`, the sharded configs timed the same
+way at this N.
 """
 from __future__ import annotations
 
@@ -456,11 +459,15 @@ def make_tensor(rcp, synthetic, cfg, ctx, shard, world, rank):
     return X, slo, shi
 
 
-def scaling_record(args, dist, rcp, synthetic, ctx, world, rank, shard):
-    """scaling_config: C3 (1024^3 fp32 rank 50, BASELINE's config sharded along mode 3 at
-    1/2/4/8 GPUs) device-timed at this N, with its streamed-pass roofline."""
+SHARDED_CONFIGS = ("C3", "C4", "C5")  # BASELINE.json: sharded at 1/2/4/8 GPUs
+
+
+def scaling_record(args, dist, rcp, synthetic, ctx, world, rank, shard, name="C3"):
+    """scaling_config: a config BASELINE.json shards (C3 along mode 3, C5 along mode 1: the
+    largest sharded tensor of north_star's 1 -> 8 GPU target) device-timed at this N, with
+    its streamed-pass roofline."""
     from paper_1703_09074_b200.synthetic import CONFIGS
-    cfg = CONFIGS["C3"]
+    cfg = CONFIGS[name]
     X, _, _ = make_tensor(rcp, synthetic, cfg, ctx, shard, world, rank)
     c = configs(cfg, rcp)
     dcfg = rcp.DecomposeConfig(rank=c["rank"], tol=c["tol"], max_iter=c["max_iter"], seed=c["seed"],
@@ -513,8 +520,8 @@ def main():
         ctx.set_option("fp32_arith", 1)
     # N > 1: one decomposition sharded in slabs along the slab mode, the
     # library's own NCCL communicator (id broadcast through torch.distributed)
-    shard = (world > 1 and not args.replicas) or args.shard
-    if shard:
+    shard = (world > 1 and not args.replicas and args.config in SHARDED_CONFIGS) or args.shard
+    if world > 1 or args.shard:  # the sharded runs (this config or the scaling records) need the communicator
         uid = dist.broadcast_bytes(rcp.comm_unique_id() if rank == 0 else bytes(128))
         ctx.comm_init_nccl(world, rank, uid)
     X, slo, shi = make_tensor(rcp, synthetic, cfg, ctx, shard, world, rank)
@@ -557,9 +564,13 @@ def main():
         e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(d2h)}
     X.free()
 
-    scaling = None
-    if not args.no_scaling_config and args.config != "C3":
-        scaling = scaling_record(args, dist, rcp, synthetic, ctx, world, rank, shard)
+    scaling, scaling5 = None, None
+    if not args.no_scaling_config:
+        sh = world > 1 or args.shard
+        if args.config != "C3":
+            scaling = scaling_record(args, dist, rcp, synthetic, ctx, world, rank, sh, "C3")
+        if args.config != "C5":
+            scaling5 = scaling_record(args, dist, rcp, synthetic, ctx, world, rank, sh, "C5")
 
     if rank == 0:
         sm_ms, achieved, peak, peak_kind = pass_roofline(pass_ms, pass_bytes, args.steps)
@@ -598,6 +609,8 @@ def main():
             line["e2e"] = e2e
         if scaling:
             line["scaling_config"] = scaling
+        if scaling5:
+            line["scaling_config_C5"] = scaling5
         if world == 1 and not args.no_cpu_baseline:
             rec, ref = cpu_baseline(cfg, x_host, c)
             rec["single_thread"] = cpu_baseline_single(cfg, x_host, c)

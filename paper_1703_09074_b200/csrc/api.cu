@@ -1542,7 +1542,7 @@ void run_decompose(rcpg_context* c, const rcpg_tensor* t, const rcpg_decompose_c
   if (!c->graph_cache) c->graph_cache = std::make_shared<GraphCache>();
   GraphCache& g = *std::static_pointer_cast<GraphCache>(c->graph_cache);
   static const bool no_graph = std::getenv("RCPG_NO_GRAPH") != nullptr;
-  const bool graphable = !no_graph && !t->slab && !c->omega_host && c->comm == nullptr;
+  const bool graphable = !no_graph && !t->slab && !c->omega_host;
   const bool same = graphable && g.same(c, t, cfg) && g.gen == alloc_gen().load();
   if (same && g.ready) {  // replay
     c->pass_used = g.pass_used;
