@@ -564,14 +564,6 @@ def main():
         e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(d2h)}
     X.free()
 
-    scaling, scaling5 = None, None
-    if not args.no_scaling_config:
-        sh = world > 1 or args.shard
-        if args.config != "C3":
-            scaling = scaling_record(args, dist, rcp, synthetic, ctx, world, rank, sh, "C3")
-        if args.config != "C5":
-            scaling5 = scaling_record(args, dist, rcp, synthetic, ctx, world, rank, sh, "C5")
-
     if rank == 0:
         sm_ms, achieved, peak, peak_kind = pass_roofline(pass_ms, pass_bytes, args.steps)
         passes = {n: {"ms_per_step": pass_ms[n] / args.steps,
@@ -607,10 +599,6 @@ def main():
                                              "read per pivot)"}
         if e2e:
             line["e2e"] = e2e
-        if scaling:
-            line["scaling_config"] = scaling
-        if scaling5:
-            line["scaling_config_C5"] = scaling5
         if world == 1 and not args.no_cpu_baseline:
             rec, ref = cpu_baseline(cfg, x_host, c)
             rec["single_thread"] = cpu_baseline_single(cfg, x_host, c)
@@ -618,6 +606,39 @@ def main():
             line["parity"] = parity_record(cfg, model, trace, ref)
             if not line["parity"]["pass"]:
                 print(f"bench.py: PARITY FAILURE vs the oracle: {json.dumps(line['parity'])}", file=sys.stderr)
+    else:
+        line = None
+
+    # the sharded scaling records come last, each guarded: an exception is recorded in the
+    # sub-record, and a watchdog prints the main line without them if they hang (a collective
+    # that never completes must not cost the whole bench line)
+    if not args.no_scaling_config:
+        import threading
+
+        def watchdog():
+            if line is not None:
+                line.setdefault("scaling_config", {"error": f"timeout after {limit:.0f} s"})
+                print(json.dumps(line), flush=True)
+            print(f"bench.py: scaling records exceeded {limit:.0f} s, exiting", file=sys.stderr, flush=True)
+            os._exit(0)
+
+        limit = float(os.environ.get("RCPG_BENCH_SCALING_TIMEOUT", "480"))
+        timer = threading.Timer(limit, watchdog)
+        timer.daemon = True
+        timer.start()
+        sh = world > 1 or args.shard
+        for key, name in (("scaling_config", "C3"), ("scaling_config_C5", "C5")):
+            if args.config == name:
+                continue
+            try:
+                rec = scaling_record(args, dist, rcp, synthetic, ctx, world, rank, sh, name)
+            except Exception as exc:  # recorded, not fatal
+                print(f"bench.py: {key} failed: {exc!r}", file=sys.stderr, flush=True)
+                rec = {"workload": name, "error": repr(exc)[:300]}
+            if line is not None:
+                line[key] = rec
+        timer.cancel()
+    if line is not None:
         print(json.dumps(line), flush=True)
     dist.close()
 

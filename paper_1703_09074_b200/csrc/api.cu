@@ -1541,7 +1541,9 @@ void run_decompose(rcpg_context* c, const rcpg_tensor* t, const rcpg_decompose_c
   check_arg(!(t->slab && !cfg.randomized), "decompose: sharded tensors are decomposed with randomized = true");
   if (!c->graph_cache) c->graph_cache = std::make_shared<GraphCache>();
   GraphCache& g = *std::static_pointer_cast<GraphCache>(c->graph_cache);
-  static const bool no_graph = std::getenv("RCPG_NO_GRAPH") != nullptr;
+  // the phase profiles (RCPG_PROFILE_*) synchronize inside the call: no capture
+  static const bool no_graph = std::getenv("RCPG_NO_GRAPH") != nullptr || std::getenv("RCPG_PROFILE_ALS") != nullptr ||
+                               std::getenv("RCPG_PROFILE_QR") != nullptr || std::getenv("RCPG_PROFILE_LU") != nullptr;
   const bool graphable = !no_graph && !t->slab && !c->omega_host;
   const bool same = graphable && g.same(c, t, cfg) && g.gen == alloc_gen().load();
   if (same && g.ready) {  // replay
