@@ -345,50 +345,65 @@ __device__ void gj_inverse_regs(double* A, int R, int* ok, double* scratch) {
     for (int m = 0; m < KC; ++m) rowbuf[0][lane + 32 * m] = v[0][m];
   __syncthreads();
   int bad = 0;
-  int nxw = 1 % nw, nxq = 1 / nw;  // owner (warp, slot) of row k + 1
-  for (int k = 0; k < R; ++k) {
-    const double* rk = rowbuf[k & 1];
-    const double p = rk[k];
-    double rkj[KC];
+  // pivot k = q * nw + w: the slot q of the pivot row (and of the next one,
+  // q or q + 1) is a compile-time index, so v stays in registers (a runtime
+  // slot index made the compiler keep v on the stack: ~1.2 us per step)
 #pragma unroll
-    for (int m = 0; m < KC; ++m) rkj[m] = rk[lane + 32 * m];
-    const int mk = k >> 5, lk = k & 31;
-    double aik[KR];
+  for (int q0 = 0; q0 < KR; ++q0) {
+    for (int w = 0; w < nw; ++w) {
+      const int k = q0 * nw + w;
+      if (k >= R) break;
+      const double* rk = rowbuf[k & 1];
+      const double p = rk[k];
+      double rkj[KC];
 #pragma unroll
-    for (int q = 0; q < KR; ++q) {
-      double x = 0.0;
-#pragma unroll
-      for (int m = 0; m < KC; ++m)
-        if (m == mk) x = v[q][m];
-      aik[q] = __shfl_sync(0xffffffffu, x, lk);
-    }
-    bad |= !(p > 0.0);
-    const double ip = 1.0 / p;
-#pragma unroll
-    for (int m = 0; m < KC; ++m) {
-      const int j = lane + 32 * m;
-      const double akj = rkj[m] * ip;
+      for (int m = 0; m < KC; ++m) rkj[m] = rk[lane + 32 * m];
+      const int mk = k >> 5, lk = k & 31;
+      double aik[KR];
 #pragma unroll
       for (int q = 0; q < KR; ++q) {
-        const int i = wid + q * nw;
-        if (j != k)
-          v[q][m] = (i != k) ? v[q][m] - aik[q] * akj : akj;
-        else
-          v[q][m] = (i != k) ? -aik[q] * ip : ip;
+        double x = v[q][0];
+#pragma unroll
+        for (int m = 1; m < KC; ++m) x = (m == mk) ? v[q][m] : x;
+        aik[q] = __shfl_sync(0xffffffffu, x, lk);
       }
-    }
-    if (k + 1 < R && wid == nxw) {
+      bad |= !(p > 0.0);
+      const double ip = 1.0 / p;
+      // the general update on every entry (one FMA: v - aik akj), then the
+      // column-k entries (-aik / p, lane lk) and row k (akj, its pivot 1 / p)
+      // overwritten: the values of the branchy per-entry form, a quarter of
+      // the instructions
+      double akj[KC];
 #pragma unroll
-      for (int q = 0; q < KR; ++q)
-        if (q == nxq)
+      for (int m = 0; m < KC; ++m) akj[m] = rkj[m] * ip;
 #pragma unroll
-          for (int m = 0; m < KC; ++m) rowbuf[(k + 1) & 1][lane + 32 * m] = v[q][m];
+      for (int m = 0; m < KC; ++m)
+#pragma unroll
+        for (int q = 0; q < KR; ++q) v[q][m] = fma(-aik[q], akj[m], v[q][m]);
+      if (lane == lk)
+#pragma unroll
+        for (int m = 0; m < KC; ++m)
+          if (m == mk)
+#pragma unroll
+            for (int q = 0; q < KR; ++q) v[q][m] = -aik[q] * ip;
+      if (wid == w)
+#pragma unroll
+        for (int m = 0; m < KC; ++m) v[q0][m] = (lane + 32 * m == k) ? ip : akj[m];
+      // publish row k + 1: warp w + 1, slot q0 -- or warp 0, slot q0 + 1
+      if (k + 1 < R) {
+        double* dst = rowbuf[(k + 1) & 1];
+        if (w + 1 < nw) {
+          if (wid == w + 1)
+#pragma unroll
+            for (int m = 0; m < KC; ++m) dst[lane + 32 * m] = v[q0][m];
+        } else if (q0 + 1 < KR) {
+          if (wid == 0)
+#pragma unroll
+            for (int m = 0; m < KC; ++m) dst[lane + 32 * m] = v[q0 + 1 < KR ? q0 + 1 : q0][m];
+        }
+      }
+      __syncthreads();
     }
-    if (++nxw == nw) {
-      nxw = 0;
-      ++nxq;
-    }
-    __syncthreads();
   }
 #pragma unroll
   for (int q = 0; q < KR; ++q)
@@ -429,17 +444,40 @@ __device__ void als_mode_update(const FactorSet<T>& fs, int mode, const WT* W, T
   const int lane0 = tid & 31, wid0 = tid >> 5, nw0 = nt >> 5;
   double* Pm = A;
   if (part == 2) {
-    for (int e = tid; e < R2; e += nt) A[e] = ldcg(&pm_io[e]);
+    for (int e0 = tid; e0 < R2; e0 += 8 * nt) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = e0 + u * nt < R2 ? ldcg(&pm_io[e0 + u * nt]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (e0 + u * nt < R2) A[e0 + u * nt] = v[u];
+    }
     __syncthreads();
   } else {
   // 1. V = Hadamard of the other modes' Grams (solve.hpp:209-211): the
   // reference's Scalar product chain, v = 1, then v *= G_k for k ascending
-  for (int e = tid; e < R * R; e += nt) {
-    T v = T(1);
-    for (int k = 0; k < N; ++k)
-      if (k != mode) v = mul_rn(v, fs.gram[k][e]);
-    V[e] = double(v);
-    A[e] = V[e];
+  // (the Grams come from other CTAs in this launch: L2-coherent loads, the
+  // chunk's loads issued before any product)
+  for (int e0 = 0; e0 < R * R; e0 += 4 * nt) {
+    T gk[kMaxOrder][4];
+#pragma unroll
+    for (int k = 0; k < kMaxOrder; ++k)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + u * nt + tid;
+        gk[k][u] = (k < N && k != mode && e < R * R) ? ldcg(&fs.gram[k][e]) : T(1);
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * nt + tid;
+      if (e >= R * R) continue;
+      T v = T(1);
+#pragma unroll
+      for (int k = 0; k < kMaxOrder; ++k)
+        if (k < N && k != mode) v = mul_rn(v, gk[k][u]);
+      V[e] = double(v);
+      A[e] = V[e];
+    }
   }
   if (tid == 0) s_ok = 1;
   __syncthreads();
@@ -719,6 +757,7 @@ struct AlsLoopArgs {
   i64 part_stride;
   GridBarrier* bar;
   unsigned long long* prof;  // optional [8] ns per phase (CTA 0): A, bar1, B, bar2
+  int grid_update;           // split mode: mode update spread over the grid (als_update_grid)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -753,6 +792,225 @@ __device__ __forceinline__ void als_dmma(double (&c)[4], double a0, double a1, d
   asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
                : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
                : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// The mode update of the loop kernel spread over the whole grid (split mode:
+// pinv(V) is already in pm). Every output keeps the operation order of
+// als_mode_update, so the factors and Grams carry the same bits:
+//  B1  CTA g owns rows i = g, g + G, ...: W(i, :) reduced from the GA MTTKRP
+//      partials in a fixed order and rounded to Scalar (solve.hpp:212-213);
+//      F(i, :) = W(i, :) pinv(V), the k-ascending chain, rounded to Scalar.
+//  --  grid sync
+//  B2  every CTA: the R column norms from F (warp per column, lanes striding
+//      the rows: identical in every CTA), the weights (last mode); its own rows
+//      normalized into the factor; the 4 x 4 Gram blocks spread over the grid,
+//      one i-ascending chain per entry (solve.hpp:215-230).
+//  --  grid sync
+//  B3  last mode: CTA 0 the fit and the stopping test (solve.hpp:232-254),
+//      then a grid sync so every CTA reads the same `done`.
+// CTA 0's mode update used to serialize B1-B3 on one SM (C5: 45 us per mode step).
+template <typename T, typename Sync>
+__device__ void als_update_grid(const FactorSet<T>& fs, int mode, const double* part0, i64 pstride, int GA,
+                                double* wbuf, double* fraw, const double* pm, T* weights, double tol, int max_iter,
+                                double* trace_fit, double* trace_sec, AlsState* st, double* sm, Sync gsync,
+                                unsigned long long* prof = nullptr) {
+  const int tid = threadIdx.x, nt = blockDim.x, G = gridDim.x, g = blockIdx.x;
+  const int R = fs.rank, N = fs.order, I = int(fs.extent[mode]);
+  const bool stamp = prof != nullptr && g == 0 && tid == 0;
+  unsigned long long ts = 0;
+  if (stamp) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
+  auto mark = [&](int slot) {
+    if (stamp) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      prof[slot] += t - ts;
+      ts = t;
+    }
+  };
+  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  double* wrow = sm;             // [R] this row of W (Scalar-rounded)
+  double* nr = wrow + R;         // [R] column norms (Scalar-rounded)
+  double* spm = nr + R;          // [R][R] pinv(V), staged (one L2 round trip, not R)
+  double* sfr = spm + R * R;     // [I][R] F before normalization, staged
+  double* fn = sfr + I * R;      // [R][I | 1] normalized factor (Gram / fit CTAs); B1's subset sums
+  // ---- B1 (partials row-major: partial q's row i is R contiguous doubles)
+  const int nsub = nt / R > 0 ? nt / R : 1;  // partial subsets, summed in order
+  const int rr = tid % R, sb = tid / R;
+  double* red = fn;                          // [nsub][R] subset sums (fn is free here)
+  if (g < I) {  // transposed: thread r reads pinv(V)(k, r) at k R + r; 8 loads in flight per thread
+    for (int e0 = tid; e0 < R * R; e0 += 8 * nt) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = e0 + u * nt < R * R ? ldcg(pm + e0 + u * nt) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * nt;
+        if (e < R * R) spm[(e % R) * R + e / R] = v[u];
+      }
+    }
+  }
+  for (int i = g; i < I; i += G) {
+    if (sb < nsub) {
+      const double* src = part0 + i64(i) * R + rr;
+      double s = 0.0;
+      for (int q0 = sb; q0 < GA; q0 += 16 * nsub) {
+        double v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int q = q0 + nsub * u;
+          v[u] = q < GA ? ldcg(src + i64(q) * pstride) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) s += v[u];
+      }
+      red[sb * R + rr] = s;
+    }
+    __syncthreads();
+    for (int r = tid; r < R; r += nt) {
+      double s = 0.0;
+      for (int b = 0; b < nsub; ++b) s += red[b * R + r];
+      const double w = double(T(s));
+      wrow[r] = w;
+      wbuf[i + i64(r) * I] = w;
+    }
+    __syncthreads();
+    for (int r = tid; r < R; r += nt) {
+      double acc = 0.0;
+      for (int k = 0; k < R; ++k) acc += wrow[k] * spm[k * R + r];
+      fraw[i + i64(r) * I] = double(T(acc));
+    }
+    __syncthreads();
+  }
+  mark(25);
+  gsync();
+  mark(26);
+  // ---- B2
+  for (int e0 = tid; e0 < I * R; e0 += 8 * nt) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = e0 + u * nt < I * R ? ldcg(&fraw[e0 + u * nt]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (e0 + u * nt < I * R) sfr[e0 + u * nt] = v[u];
+  }
+  __syncthreads();
+  for (int r = wid; r < R; r += nw) {
+    double s = 0.0;
+    for (int i = lane; i < I; i += 32) {
+      const double f = sfr[i + r * I];
+      s += f * f;
+    }
+    s = warp_sum(s);
+    if (lane == 0) {
+      const T nrm = T(sqrt(s));
+      nr[r] = double(nrm);
+      if (g == 0 && mode == N - 1) weights[r] = nrm;
+    }
+  }
+  __syncthreads();
+  for (int i = g; i < I; i += G)
+    for (int r = tid; r < R; r += nt) {
+      const T nrm = T(nr[r]);
+      const T f = T(sfr[i + r * I]);
+      fs.f[mode][i + i64(r) * I] = nrm > T(0) ? f / nrm : f;
+    }
+  // Gram entries (a <= b) in CTA-contiguous ranges: a warp shares b and walks
+  // consecutive a (odd leading dimension: conflict-free), one i-ascending
+  // chain per entry -- the per-entry chain of the 4 x 4 register tiles of
+  // als_mode_update, so the same bits
+  const int ldn = I | 1;
+  const int E = R * (R + 1) / 2, gcta = (E + nt - 1) / nt;
+  const bool last = mode == N - 1;
+  if (g < gcta || (last && g == 0)) {
+    for (int e = tid; e < I * R; e += nt) {
+      const int i = e % I, r = e / I;
+      const T nrm = T(nr[r]);
+      const T f = T(sfr[e]);
+      fn[i + r * ldn] = double(nrm > T(0) ? f / nrm : f);
+    }
+    __syncthreads();
+    const int e = g * nt + tid;
+    if (g < gcta && e < E) {
+      int b = int((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+      while (b * (b + 1) / 2 > e) --b;
+      while ((b + 1) * (b + 2) / 2 <= e) ++b;
+      const int a = e - b * (b + 1) / 2;
+      const double* fa = fn + a * ldn;
+      const double* fb = fn + b * ldn;
+      double acc = 0.0;
+      for (int i = 0; i < I; ++i) acc += fa[i] * fb[i];
+      const T gv = T(acc);
+      fs.gram[mode][a + b * R] = gv;
+      fs.gram[mode][b + a * R] = gv;
+    }
+  }
+  mark(27);
+  gsync();
+  mark(28);
+  if (!last) return;
+  // ---- B3
+  if (g == 0) {
+    const int R2 = R * R;
+    double m2 = 0.0;
+    for (int e0 = 0; e0 < R2; e0 += 4 * nt) {  // every Gram load of the chunk in flight first
+      T gk[kMaxOrder][4];
+#pragma unroll
+      for (int k = 0; k < kMaxOrder; ++k)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = e0 + u * nt + tid;
+          gk[k][u] = (k < N && e < R2) ? ldcg(&fs.gram[k][e]) : T(1);
+        }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + u * nt + tid;
+        if (e >= R2) continue;
+        T gv = T(1);
+#pragma unroll
+        for (int k = 0; k < kMaxOrder; ++k)
+          if (k < N) gv = mul_rn(gv, gk[k][u]);
+        m2 += nr[e % R] * double(gv) * nr[e / R];
+      }
+    }
+    m2 = block_reduce_sum(m2);
+    double xi = 0.0;
+    for (int e0 = tid; e0 < I * R; e0 += 8 * nt) {
+      double wv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) wv[u] = e0 + u * nt < I * R ? ldcg(&wbuf[e0 + u * nt]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * nt;
+        if (e < I * R) xi += wv[u] * fn[(e % I) + (e / I) * ldn] * nr[e / I];
+      }
+    }
+    xi = block_reduce_sum(xi);
+    if (tid == 0) {
+      const double model2 = m2 > 0.0 ? m2 : 0.0;
+      const double nx2 = st->nx2;
+      const double fit_now = 1.0 - (nx2 + model2 - 2.0 * xi) / nx2;
+      const int it = st->it;
+      if (!isfinite(fit_now)) {
+        st->error_it = it;
+        st->done = 1;
+      } else {
+        unsigned long long now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        trace_fit[it - 1] = fit_now;
+        trace_sec[it - 1] = double(now - st->t0) * 1e-9;
+        if (it >= 2 && fabs(fit_now - st->prev_fit) < tol) {
+          st->converged = 1;
+          st->done = 1;
+        }
+        st->prev_fit = fit_now;
+        if (it >= max_iter) st->done = 1;
+        st->it = it + 1;
+      }
+    }
+  }
+  mark(29);
+  gsync();
+  mark(30);
 }
 
 // CLUSTER: the grid is one thread-block cluster (<= 16 CTAs, small compressed
@@ -831,11 +1089,15 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
           const int nk = sext[k] * R;
           const T* src = p.fs.f[k];
           const int ek = sext[k];
-          for (int e = tid; e < nk; e += nt) {  // transpose: a warp then reads one row's ranks
-            const int row = e / R, r = e % R;
-            fsm[sfoff[k] + e] = src[row + r * ek];
+          // transpose (a warp then reads one row's ranks) with every element's
+          // copy in flight at once: one L2 round trip, not one per element
+          for (int e = tid; e < nk; e += nt) {
+            const int row = e / R, r = e - (e / R) * R;
+            als_cp_elem(&fsm[sfoff[k] + e], &src[row + r * ek], true);
           }
         }
+        als_cp_commit();
+        als_cp_wait<0>();
         __syncthreads();
       }
       // gather: thread tid always handles position pp = tid % BATCH
@@ -953,7 +1215,8 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int i = ib + (q >> 1) * 8, r = rb + (q & 1);
-            if (i < I && r < R) pt[i + i64(r) * I] = acc[t][q];
+            // the grid update reads each row's R outputs of one partial together
+            if (i < I && r < R) pt[p.grid_update && split ? i64(i) * R + r : i + i64(r) * I] = acc[t][q];
           }
         }
       }
@@ -966,6 +1229,23 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
       gsync();
       unsigned long long tp2 = 0;
       if (p.prof && g == 0 && tid == 0) tp2 = gtimer();
+      if (split && p.grid_update) {
+        const double* pp0 = p.part + i64(parity) * G * p.part_stride;
+        double* Wg = p.part + 2 * i64(G) * p.part_stride;
+        double* fraw = p.part + (2 * i64(G) + 2) * p.part_stride;
+        FactorSet<T> fs = p.fs;
+        als_update_grid<T>(fs, m, pp0, p.part_stride, GA, Wg, fraw, p.pm, p.weights, p.tol, p.max_iter, p.trace_fit,
+                           p.trace_sec, p.st, sm, gsync, p.prof);
+        parity ^= 1;
+        if (p.prof && g == 0 && tid == 0) {
+          const unsigned long long tp4 = gtimer();
+          p.prof[0] += tp1 - tp0;
+          p.prof[1] += tp2 - tp1;
+          p.prof[2] += tp4 - tp2;
+          p.prof[4] += 1;
+        }
+        continue;
+      }
       // ---- reduction of the partials, spread over all CTAs (fixed CTA
       //      order per output: deterministic), into Wg after the partials
       double* Wg = p.part + 2 * i64(G) * p.part_stride;
@@ -1173,7 +1453,15 @@ __global__ void small_gemm_kernel(const T* Q, i64 dim, i64 l, const T* A, int ra
 
 // ------------------------------------------------------------ reductions
 template <typename T>
-__global__ void __launch_bounds__(256) norm_finite_kernel(const T* __restrict__ x, i64 n, double* part) {
+__global__ void __launch_bounds__(256) norm_finite_kernel(const T* __restrict__ x, i64 n, double* part,
+                                                          const double* cond = nullptr) {
+  if (cond != nullptr && *cond == 0.0) {  // the caller proved the input finite (sum not needed)
+    if (threadIdx.x == 0) {
+      part[2 * blockIdx.x] = 0.0;
+      part[2 * blockIdx.x + 1] = 0.0;
+    }
+    return;
+  }
   // 16-byte loads, four in flight per thread (a streaming reduction needs many
   // bytes in flight per SM to reach HBM bandwidth); scalar head/tail
   using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
@@ -1602,7 +1890,12 @@ void als_loop(const T* B, const i64* shape, int order, const FactorSet<T>& fs, T
     maxout = std::max(maxout, shape[m] * R);
   }
   AlsLoopArgs<T> a{B, make_shape(shape, order), fs, weights, tol, max_iter, trace_fit, trace_sec, state, part,
-                   nullptr, maxout, bar, prof};
+                   nullptr, maxout, bar, prof, 1};
+  static const bool grid_upd = [] {  // RCPG_ALS_GRIDUPD=0: CTA 0 does the mode update (A/B hook)
+    const char* e = std::getenv("RCPG_ALS_GRIDUPD");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  a.grid_update = grid_upd && R >= 8 ? 1 : 0;  // (B1's subset sums fit the smem layout from R = 8)
   // 64-position batches when they fit: half the per-batch latency chains
   static const size_t lim64 = enable_max_dyn_smem(als_loop_kernel<T, 64>);
   static const size_t lim32 = enable_max_dyn_smem(als_loop_kernel<T, 32>);
@@ -1615,9 +1908,10 @@ void als_loop(const T* B, const i64* shape, int order, const FactorSet<T>& fs, T
     const char* sp = std::getenv("RCPG_ALS_SPLIT");
     const bool want_split = !(sp != nullptr && sp[0] == '0') && i64(R) * R <= maxout;
     int G = int(std::max<i64>(1, std::min<i64>(ceil_div(maxJ, batch) + (want_split ? 1 : 0), maxc)));
-    G = int(std::min<i64>(G, part_elems / (2 * maxout) - 2));  // + slots for the reduced W and pinv(V)
+    // + slots for the reduced W, pinv(V) and the grid update's unnormalized factor
+    G = int(std::min<i64>(G, part_elems / (2 * maxout) - 2));
     G = std::max(G, 1);
-    const bool split_ok = want_split && G >= 3 && (2 * i64(G) + 2) * maxout <= part_elems;
+    const bool split_ok = want_split && G >= 3 && (2 * i64(G) + 3) * maxout <= part_elems;
     a.pm = split_ok ? part + (2 * i64(G) + 1) * maxout : nullptr;
     return G;
   };
@@ -1701,10 +1995,29 @@ void small_gemm(const T* Q, i64 dim, i64 l, const T* A, int rank, T* out, cudaSt
   RCPG_LAUNCHED();
 }
 
+// flag (zeroed here) += 1 per CTA that saw a non-finite entry of y
 template <typename T>
-void norm_and_finite(const T* x, i64 n, double* out2, double* scratch, int num_sms, cudaStream_t st) {
+__global__ void nonfinite_flag_kernel(const T* __restrict__ y, i64 n, double* flag) {
+  bool bad = false;
+  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < n; e += i64(gridDim.x) * blockDim.x)
+    bad |= !isfinite(double(y[e]));
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicAdd(flag, 1.0);
+}
+
+template <typename T>
+void nonfinite_flag(const T* y, i64 n, double* flag, cudaStream_t st) {
+  RCPG_CUDA(cudaMemsetAsync(flag, 0, sizeof(double), st));
+  const int blocks = int(std::max<i64>(1, std::min<i64>(ceil_div(n, 256 * 8), 296)));
+  nonfinite_flag_kernel<T><<<blocks, 256, 0, st>>>(y, n, flag);
+  count_launch();
+  RCPG_LAUNCHED();
+}
+
+template <typename T>
+void norm_and_finite(const T* x, i64 n, double* out2, double* scratch, int num_sms, cudaStream_t st,
+                     const double* cond) {
   const int blocks = int(std::max<i64>(1, std::min<i64>(ceil_div(n, 256), i64(num_sms) * 4)));
-  norm_finite_kernel<T><<<blocks, 256, 0, st>>>(x, n, scratch);
+  norm_finite_kernel<T><<<blocks, 256, 0, st>>>(x, n, scratch, cond);
   sum_pairs_kernel<<<1, 256, 0, st>>>(scratch, blocks, out2);
   count_launch(2);
   RCPG_LAUNCHED();
@@ -1818,7 +2131,8 @@ void synth_tensor(const i64* shape, int order, int rank, const double* w_dev, co
   template void als_loop<T>(const T*, const i64*, int, const FactorSet<T>&, T*, double, int, double*, double*, \
                             AlsState*, double*, i64, GridBarrier*, cudaStream_t, unsigned long long*);                                \
   template void small_gemm<T>(const T*, i64, i64, const T*, int, T*, cudaStream_t);                           \
-  template void norm_and_finite<T>(const T*, i64, double*, double*, int, cudaStream_t);                       \
+  template void norm_and_finite<T>(const T*, i64, double*, double*, int, cudaStream_t, const double*);       \
+  template void nonfinite_flag<T>(const T*, i64, double*, cudaStream_t);                                      \
   template void residual_norms<T>(const T*, const i64*, int, const FactorSet<T>&, const T*, double*, double*, \
                                   int, cudaStream_t);                                                         \
   template void synth_tensor<T>(const i64*, int, int, const double*, const double* const*, double, u64, T*,   \

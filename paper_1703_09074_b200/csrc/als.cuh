@@ -99,7 +99,10 @@ void small_gemm(const T* Q, i64 dim, i64 l, const T* A, int rank, T* out, cudaSt
 // Sum of squares (double) and count of non-finite entries of a device array.
 template <typename T>
 void norm_and_finite(const T* x, i64 n, double* out2 /* [2]: sumsq, nonfinite */, double* scratch,
-                     int num_sms, cudaStream_t st);
+                     int num_sms, cudaStream_t st, const double* cond = nullptr);
+// flag <- count of CTAs that saw a non-finite entry of y (zeroed first)
+template <typename T>
+void nonfinite_flag(const T* y, i64 n, double* flag, cudaStream_t st);
 
 // ||X - model||^2 and ||X||^2 (double), streamed over X (relative_error,
 // kruskal.hpp:187-194, accumulated in double). out2 = {resid2, x2}.

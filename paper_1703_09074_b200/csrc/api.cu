@@ -87,7 +87,7 @@ struct rcpg_context {
   std::string err;
   int err_it = -1;
   // workspace
-  DevBuf panelA, panelB, work0, work1, Y, Qy, scratch, keys, cands, bar, info, part, tau, diag, cqr;
+  DevBuf panelA, panelB, work0, work1, Y, Qy, scratch, keys, cands, bar, info, part, tau, diag, cqr, lu_ctr;
   DevBuf als_f, als_g, als_w, als_kr, als_work, als_trace, als_state, weights, small_tmp, nrm, als_part, als_prof,
       recov;
   std::vector<PassRecord> passes;
@@ -238,10 +238,12 @@ FactorWork factor_work(rcpg_context* c, i64 rows) {
   c->part.ensure((2 * size_t(maxb) + 1) * (kMaxPanelCols + 1) * sizeof(double));
   c->tau.ensure(kMaxPanelCols * sizeof(double));
   c->diag.ensure(kMaxPanelCols * sizeof(double));
+  c->lu_ctr.ensure((kMaxPanelCols + 1) * sizeof(unsigned));
   FactorWork w;
   w.keys = c->keys.as<i64>();
   w.cands = c->cands.p;
   w.bar = c->bar.as<GridBarrier>();
+  w.ctr = c->lu_ctr.as<unsigned>();
   w.info = c->info.as<int>();
   w.part = c->part.as<double>();
   w.rowk = w.part + 2 * size_t(maxb) * (kMaxPanelCols + 1);
@@ -266,7 +268,7 @@ void read_doubles(rcpg_context* c, const double* d, double* h, int n) {
 // Device check slots (c->nrm): written by kernels, read back once at the end
 // of a call so the whole decomposition is enqueued without host syncs.
 constexpr int kSlotCount = 512;
-enum Slot { kXSum = 0, kXBad = 1, kBSum = 2, kBBad = 3, kResid = 4, kResX = 5, kRankWarn = 8 /* 8 ints */ };
+enum Slot { kXSum = 0, kXBad = 1, kBSum = 2, kBBad = 3, kResid = 4, kResX = 5, kYBad = 6, kRankWarn = 8 /* 8 ints */ };
 double* slots(rcpg_context* c) { return c->nrm.as<double>(); }
 int* rank_warn_slot(rcpg_context* c, int mode) { return reinterpret_cast<int*>(slots(c) + kRankWarn) + mode; }
 const double* read_slots(rcpg_context* c) {
@@ -353,6 +355,33 @@ int stabilize_small(rcpg_context* c, int stab, T* Y, i64 I, int n, T* out) {
   return thin_qr<T>(Y, out, I, I, n, km, w, nullptr, c->st);
 }
 
+// stab(W) of the big J x l panel (compress.hpp:127-132); RCPG_PROFILE_LU prints
+// the LU kernel's per-step phase times (synchronizes: not for timed runs)
+template <typename T>
+int stabilize_big(rcpg_context* c, int stab, T* W, T* Z, i64 J, i64 R, int n, const KoldaMap& km) {
+  FactorWork w = factor_work_t<T>(c, J);
+  static const bool lu_prof = getenv("RCPG_PROFILE_LU") != nullptr;
+  if (lu_prof) {
+    c->als_prof.ensure(16 * sizeof(unsigned long long));
+    RCPG_CUDA(cudaMemsetAsync(c->als_prof.p, 0, 16 * sizeof(unsigned long long), c->st));
+    w.prof = c->als_prof.as<unsigned long long>();
+  }
+  int rz;
+  if (stab == RCPG_STAB_LU)
+    rz = plu_basis<T>(W, Z, J, R, n, km, w, c->st);
+  else
+    rz = thin_qr<T>(W, Z, J, R, n, km, w, nullptr, c->st);
+  if (lu_prof) {
+    unsigned long long h[5];
+    RCPG_CUDA(cudaMemcpyAsync(h, w.prof, sizeof(h), cudaMemcpyDeviceToHost, c->st));
+    RCPG_CUDA(cudaStreamSynchronize(c->st));
+    if (h[3] && h[3] < 100000)
+      fprintf(stderr, "[rcpg lu] J=%lld n=%d steps=%llu  reduce+book %.2f  update %.2f  cand+barrier %.2f us/step\n",
+              (long long)J, n, h[3], h[0] / 1e3 / h[3], h[1] / 1e3 / h[3], h[2] / 1e3 / h[3]);
+  }
+  return rz;
+}
+
 void finish_compress(rcpg_context* c, rcpg_compressed* out, const Deferred& dfr);
 
 // One compressed mode (compress.hpp:110-141) on an unsharded working tensor
@@ -362,8 +391,20 @@ void finish_compress(rcpg_context* c, rcpg_compressed* out, const Deferred& dfr)
 template <typename T>
 const T* compress_mode_local(rcpg_context* c, const CompressCfg& cfg, int n, i64* shape, int order, const T* cur,
                              int& which, BasisRec& basis, Deferred& dfr, const void* pre_omega = nullptr,
-                             cudaEvent_t pre_ev = nullptr) {
+                             cudaEvent_t pre_ev = nullptr, const T* xcheck = nullptr, i64 xsize = 0) {
   const int sms = device_caps().num_sms;
+  // The input check folded into the first sketch (compress.hpp:93): a non-finite
+  // entry of X makes its whole row of Y = X_(n) Omega non-finite (Inf * w is
+  // +-Inf or NaN for every w), so a finite Y proves a finite X. Only a
+  // non-finite Y (bad input, or fp64 overflow from huge finite input) runs the
+  // counting pass over X, which then decides -- one full read of X saved.
+  auto check_after_sketch = [&](const T* Yv, i64 ny) {
+    if (xcheck == nullptr) return;
+    ScopedPass sp(c, "check_finite", 0.0);
+    nonfinite_flag<T>(Yv, ny, slots(c) + kYBad, c->st);
+    c->scratch.ensure(size_t(sms) * 8 * sizeof(double) + 64);
+    norm_and_finite<T>(xcheck, xsize, slots(c) + kXSum, c->scratch.as<double>(), sms, c->st, slots(c) + kYBad);
+  };
   const i64 extent = shape[n];
   const i64 l = std::min(cfg.target_rank + cfg.oversampling, extent);
   if (l > kMaxPanelCols) fail_after(c, dfr, "compress: sketch width k + p above the supported maximum (256)");
@@ -413,6 +454,7 @@ const T* compress_mode_local(rcpg_context* c, const CompressCfg& cfg, int n, i64
         ScopedPass sp(c, "sketch", (S + extent * l) * b);
         sketch_mixed(cur, v, Om, l, Y, scr, scr64, sms, c->st);
       }
+      check_after_sketch(Y, extent * l);
       i64 ycols = l;
       for (int it = 0; it < cfg.power_iterations; ++it) {
         int rq;
@@ -428,11 +470,7 @@ const T* compress_mode_local(rcpg_context* c, const CompressCfg& cfg, int n, i64
         int rz;
         {
           ScopedPass sp(c, "stab_w", 2.0 * J * rq * b);
-          FactorWork w = factor_work_t<T>(c, J);
-          if (cfg.stabilizer == RCPG_STAB_LU)
-            rz = plu_basis<T>(Wf, Zf, J, v.R, rq, km, w, c->st);
-          else
-            rz = thin_qr<T>(Wf, Zf, J, v.R, rq, km, w, nullptr, c->st);
+          rz = stabilize_big<T>(c, cfg.stabilizer, Wf, Zf, J, v.R, rq, km);
         }
         {
           ScopedPass sp(c, "power_xz", (S + J * rz + extent * rz) * b);
@@ -475,6 +513,7 @@ const T* compress_mode_local(rcpg_context* c, const CompressCfg& cfg, int n, i64
     ScopedPass sp(c, "sketch", (S + extent * l) * b);
     sketch<T>(cur, v, Om, l, Y, c->scratch.as<T>(), scr, sms, c->st);
   }
+  check_after_sketch(Y, extent * l);
   i64 ycols = l;
   for (int it = 0; it < cfg.power_iterations; ++it) {
     int rq;
@@ -489,25 +528,7 @@ const T* compress_mode_local(rcpg_context* c, const CompressCfg& cfg, int n, i64
     int rz;
     {
       ScopedPass sp(c, "stab_w", 2.0 * J * rq * b);
-      FactorWork w = factor_work_t<T>(c, J);
-      const bool lu_prof = getenv("RCPG_PROFILE_LU") != nullptr;
-      if (lu_prof) {
-        c->als_prof.ensure(16 * sizeof(unsigned long long));
-        RCPG_CUDA(cudaMemsetAsync(c->als_prof.p, 0, 16 * sizeof(unsigned long long), c->st));
-        w.prof = c->als_prof.as<unsigned long long>();
-      }
-      if (cfg.stabilizer == RCPG_STAB_LU)
-        rz = plu_basis<T>(P, Zp, J, v.R, rq, km, w, c->st);
-      else
-        rz = thin_qr<T>(P, Zp, J, v.R, rq, km, w, nullptr, c->st);
-      if (lu_prof) {
-        unsigned long long h[4];
-        RCPG_CUDA(cudaMemcpyAsync(h, w.prof, sizeof(h), cudaMemcpyDeviceToHost, c->st));
-        RCPG_CUDA(cudaStreamSynchronize(c->st));
-        if (h[3])
-          fprintf(stderr, "[rcpg lu] J=%lld n=%d steps=%llu  reduce+book %.2f  update %.2f  cand+barrier %.2f us/step\n",
-                  (long long)J, rq, h[3], h[0] / 1e3 / h[3], h[1] / 1e3 / h[3], h[2] / 1e3 / h[3]);
-      }
+      rz = stabilize_big<T>(c, cfg.stabilizer, P, Zp, J, v.R, rq, km);
     }
     {
       ScopedPass sp(c, "power_xz", (S + J * rz + extent * rz) * b);
@@ -616,10 +637,20 @@ void run_compress(rcpg_context* c, const rcpg_tensor* t, const CompressCfg& cfg,
   }
   i64 omega_off[kMaxOrder];
   const bool pre = !mode_error && precompute_omega<T>(c, cfg, t->shape, order, selected, omega_off);
-  {
+  // the first compressed mode's sketch checks the input (check_after_sketch);
+  // without one (no mode compressed, a mode error) the counting pass runs here
+  int first_mode = -1;
+  for (int n = 0; n < order && !mode_error; ++n)
+    if (selected.count(n) && std::min(cfg.target_rank + cfg.oversampling, t->shape[n]) < t->shape[n]) {
+      first_mode = n;
+      break;
+    }
+  static const bool eager_check = getenv("RCPG_EAGER_CHECK") != nullptr;  // A/B hook
+  if (first_mode < 0 || eager_check) {
     ScopedPass sp(c, "check_finite", double(t->size) * sizeof(T));
     c->scratch.ensure(size_t(sms) * 8 * sizeof(double) + 64);
     norm_and_finite<T>(static_cast<const T*>(t->d), t->size, slots(c) + kXSum, c->scratch.as<double>(), sms, c->st);
+    first_mode = -1;
   }
   dfr.compress_input = true;
   // validation order (compress.hpp:89-97): the finite check comes before the mode range
@@ -649,7 +680,8 @@ void run_compress(rcpg_context* c, const rcpg_tensor* t, const CompressCfg& cfg,
     const bool have = pre && omega_off[n] >= 0;
     cur = compress_mode_local<T>(c, cfg, n, shape, order, cur, which, basis, dfr,
                                  have ? static_cast<unsigned char*>(c->omega_buf.p) + omega_off[n] : nullptr,
-                                 have ? c->ev_omega[n] : nullptr);
+                                 have ? c->ev_omega[n] : nullptr,
+                                 n == first_mode ? static_cast<const T*>(t->d) : nullptr, t->size);
   }
   if (pre) RCPG_CUDA(cudaStreamWaitEvent(c->st, c->ev_join, 0));  // all side-stream work joined
   out->dtype = t->dtype;
@@ -1267,6 +1299,9 @@ AlsHandles<T> run_als(rcpg_context* c, const T* B, const i64* shape, int order, 
         fprintf(stderr, "[rcpg als] modes=%llu  A %.2f us  bar1 %.2f us  B %.2f us  bar2 %.2f us (per mode step)\n",
                 hp[4], hp[0] / 1e3 / double(hp[4]), hp[1] / 1e3 / double(hp[4]), hp[2] / 1e3 / double(hp[4]),
                 hp[3] / 1e3 / double(hp[4]));
+        fprintf(stderr, "[rcpg als grid] B1 %.2f sync %.2f B2 %.2f sync %.2f fit %.2f sync %.2f us (per mode step)\n",
+                hp[25] / 1e3 / double(hp[4]), hp[26] / 1e3 / double(hp[4]), hp[27] / 1e3 / double(hp[4]),
+                hp[28] / 1e3 / double(hp[4]), hp[29] / 1e3 / double(hp[4]), hp[30] / 1e3 / double(hp[4]));
         const char* nm[] = {"reduceW", "GJ", "pinv-check", "F=W*Pm", "norms", "gram", "fit"};
         const int sl[] = {14, 8, 9, 10, 11, 12, 13};
         fprintf(stderr, "[rcpg als B]");
@@ -1732,7 +1767,7 @@ void rcpg_destroy(rcpg_context* c) {
                     &c->sh_fac})
     b->release();
   for (DevBuf* b : {&c->panelA, &c->panelB, &c->work0, &c->work1, &c->Y, &c->Qy, &c->scratch, &c->keys, &c->cands,
-                    &c->bar, &c->info, &c->part, &c->tau, &c->diag, &c->cqr, &c->als_f, &c->als_g, &c->als_w, &c->als_kr,
+                    &c->bar, &c->info, &c->part, &c->tau, &c->diag, &c->cqr, &c->lu_ctr, &c->als_f, &c->als_g, &c->als_w, &c->als_kr,
                     &c->als_work, &c->als_trace, &c->als_state, &c->weights, &c->small_tmp, &c->nrm, &c->als_part, &c->als_prof, &c->recov})
     b->release();
   cudaStreamSynchronize(c->st2);

@@ -120,20 +120,21 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   return v;
 }
 
+// Flip-bit arrival (the scheme of cooperative_groups' grid sync): CTA 0 adds
+// 2^31 - (G - 1), every other CTA adds 1, so the last arrival flips bit 31 and
+// the low bits return to their value before the barrier (no reset, any G).
+// Waiters spin on the flip: one L2 round trip after the last arrival instead
+// of the arrive / reset / generation-bump chain (three dependent atomics).
 __device__ inline void grid_sync(GridBarrier* b) {
   __syncthreads();
-  if (gridDim.x * gridDim.y * gridDim.z == 1) return;
+  const unsigned nblocks = gridDim.x * gridDim.y * gridDim.z;
+  if (nblocks == 1) return;
   if (threadIdx.x == 0) {
-    const unsigned nblocks = gridDim.x * gridDim.y * gridDim.z;
-    const unsigned g = ld_acquire_u32(&b->gen);
+    const bool master = (blockIdx.x | blockIdx.y | blockIdx.z) == 0;
+    const unsigned inc = master ? 0x80000000u - (nblocks - 1) : 1u;
     __threadfence();
-    const unsigned arrived = atomicAdd(&b->count, 1u);
-    if (arrived == nblocks - 1) {
-      atomicExch(&b->count, 0u);
-      __threadfence();
-      atomicAdd(&b->gen, 1u);
-    } else {
-      while (ld_acquire_u32(&b->gen) == g) __nanosleep(20);
+    const unsigned old = atomicAdd(&b->count, inc);
+    while (((old ^ ld_acquire_u32(&b->count)) & 0x80000000u) == 0) {
     }
     __threadfence();
   }

@@ -617,6 +617,8 @@ struct LuArgs {
   int* info;   // [1] nonzero pivots
   unsigned long long* prof;  // optional [8]: ns in reduce / bookkeeping / update / barrier (CTA 0)
   int delay;   // 1: store the panel after odd pivots only (see plu_coop_kernel)
+  unsigned* ctr;  // [n] per-step chunk counters (zeroed before the launch)
+  int chunk_groups;  // row groups (blockDim * V rows) per dynamically scheduled chunk; 0 = static split
 };
 
 __device__ __forceinline__ unsigned long long lu_timer() {
@@ -662,6 +664,7 @@ __global__ void __launch_bounds__(kLuThreads, RCPG_LU_MINB) plu_coop_kernel(LuAr
   __shared__ i64 ov_pos[kMaxPanelCols], ov_row[kMaxPanelCols];
   __shared__ int n_ov;
   __shared__ i64 s_u;
+  __shared__ unsigned s_chunk[2];
 
   const int G = gridDim.x;
   const i64 chunk = ceil_div(p.J, i64(G) * V) * V;
@@ -747,10 +750,12 @@ __global__ void __launch_bounds__(kLuThreads, RCPG_LU_MINB) plu_coop_kernel(LuAr
     __syncthreads();
     const T piv = U[cs];
     const i64 u = s_u;
-    if (threadIdx.x == 0) {
-      if (ss >= r0 && ss < r1) p.phys[ss] = k;
-      if (u != ss && u >= r0 && u < r1) p.phys[u] = pr;
+    if (threadIdx.x == 0 && blockIdx.x == 0) {  // read in later steps (after a grid barrier)
+      p.phys[ss] = k;
+      if (u != ss) p.phys[u] = pr;
     }
+    const bool dyn = p.chunk_groups > 0;
+    if (threadIdx.x == 0) s_chunk[0] = dyn ? atomicAdd(&p.ctr[k], 1u) : unsigned(blockIdx.x);
     __syncthreads();
     unsigned long long t_b = 0;
     if (prof) {
@@ -763,7 +768,25 @@ __global__ void __launch_bounds__(kLuThreads, RCPG_LU_MINB) plu_coop_kernel(LuAr
     const bool more = (k + 1 < p.r);
     const int cprev = s_cprev;
     const T pivprev = s_pivprev;
-    for (i64 s0 = r0 + i64(threadIdx.x) * V; s0 < r1; s0 += i64(blockDim.x) * V) {
+    // Snake order: odd pivots walk each thread's row groups backwards, so a step
+    // starts on the rows the previous step touched last -- still in L2 (up to
+    // ~100 MB of the trailing panel per step; all of it once it fits). The
+    // candidates are order-independent (total order), so the bits do not change.
+    // Rows are handed out in chunks from a per-step counter (the static split left
+    // every step waiting ~25% on the slowest CTA: the SMs do not get equal shares
+    // of HBM); the next chunk is claimed while this one is swept.
+    // With fewer than two chunks per CTA the static split (one range per CTA) is
+    // better balanced (chunk_groups = 0).
+    const i64 grp = i64(blockDim.x) * V;
+    const i64 csz = dyn ? grp * p.chunk_groups : chunk;
+    const i64 nchunks = dyn ? ceil_div(p.J, csz) : i64(G);
+    for (int ci = 0;; ++ci) {
+      const i64 c0 = s_chunk[ci & 1];
+      if (c0 >= nchunks) break;
+      if (threadIdx.x == 0) s_chunk[(ci + 1) & 1] = dyn ? atomicAdd(&p.ctr[k], 1u) : unsigned(nchunks);
+      const i64 cb = (dyn && (k & 1) ? nchunks - 1 - c0 : c0) * csz;
+      const i64 cend = cb + csz < p.J ? cb + csz : p.J;
+      for (i64 s0 = cb + i64(threadIdx.x) * V; s0 < cend; s0 += grp) {
       i64 ba, bz;
       if (unit) {
         ba = s0;
@@ -779,7 +802,10 @@ __global__ void __launch_bounds__(kLuThreads, RCPG_LU_MINB) plu_coop_kernel(LuAr
       // are independent loads: one memory round trip, not two
       i64 ps[V];
 #pragma unroll
-      for (int e = 0; e < V; ++e) ps[e] = p.phys[s0 + e];
+      for (int e = 0; e < V; ++e) {
+        const i64 se = s0 + e;
+        ps[e] = se == ss ? i64(k) : (se == u ? pr : p.phys[se]);
+      }
       const LuVec<T, V> pcv = ld_lv<T, V>(p.A + ba + cs * R);
       LuVec<T, V> pvv;
       if (pend) pvv = ld_lv<T, V>(p.A + ba + cprev * R);
@@ -854,6 +880,8 @@ __global__ void __launch_bounds__(kLuThreads, RCPG_LU_MINB) plu_coop_kernel(LuAr
             if (better(cd, best)) best = cd;
           }
       }
+      }
+      __syncthreads();  // s_chunk[(ci + 1) & 1] visible; s_chunk[ci & 1] free
     }
     unsigned long long t_c = 0;
     if (prof) {
@@ -1435,6 +1463,20 @@ __global__ void __launch_bounds__(kFacThreads) householder_kernel(QrArgs<T> p) {
 // global memory, each CTA updating its own rows.
 constexpr int kHhThreads = 512;
 
+// sum_{q < CS} (value at p in CTA q of the cluster), in rank order, with every
+// DSMEM load issued before the first add (a dependent chain of remote loads
+// cost ~1.5 us per reduction at 16 CTAs)
+__device__ __forceinline__ double cluster_ordered_sum(cooperative_groups::cluster_group& cl, double* p, int CS) {
+  double v[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) v[q] = q < CS ? *cl.map_shared_rank(p, q) : 0.0;
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < 16; ++q)
+    if (q < CS) s += v[q];
+  return s;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kHhThreads) householder_cluster_kernel(const T* __restrict__ A, T* __restrict__ Q,
                                                                          int I, int n, int chunk,
@@ -1483,8 +1525,7 @@ __global__ void __launch_bounds__(kHhThreads) householder_cluster_kernel(const T
     acc = block_sum(acc);
     if (tid == 0) pb[kMaxPanelCols] = acc;
     cl.sync();
-    double tsq = 0.0;
-    for (int q = 0; q < CS; ++q) tsq += *cl.map_shared_rank(pb + kMaxPanelCols, q);
+    const double tsq = cluster_ordered_sum(cl, pb + kMaxPanelCols, CS);
     const T tail_sq = T(tsq);
     const T c0 = *cl.map_shared_rank(a + lk + k * chunk, ok);
     T beta, t;
@@ -1522,8 +1563,7 @@ __global__ void __launch_bounds__(kHhThreads) householder_cluster_kernel(const T
     // 4. tmp_j = Scalar(v . A(:, j)) + A(k, j); rank-1 update of own rows
     if (!trivial && ncol > 0) {
       for (int jj = tid; jj < ncol; jj += nt) {
-        double sum = 0.0;
-        for (int q = 0; q < CS; ++q) sum += *cl.map_shared_rank(pb + jj, q);
+        const double sum = cluster_ordered_sum(cl, pb + jj, CS);
         tmp[jj] = double(add_rn(T(sum), T(*cl.map_shared_rank(rowk + buf * kMaxPanelCols + jj, ok))));
       }
       __syncthreads();
@@ -1575,8 +1615,7 @@ __global__ void __launch_bounds__(kHhThreads) householder_cluster_kernel(const T
       for (int jj = tid; jj < ncol; jj += nt) rowk[buf * kMaxPanelCols + jj] = double(Q[i64(k) + i64(k + jj) * I]);
     cl.sync();  // partials of this step; the other buffer is free (read before the previous barrier)
     for (int jj = tid; jj < ncol; jj += nt) {
-      double sum = 0.0;
-      for (int q = 0; q < CS; ++q) sum += *cl.map_shared_rank(pb + jj, q);
+      const double sum = cluster_ordered_sum(cl, pb + jj, CS);
       tmp[jj] = double(add_rn(T(sum), T(*cl.map_shared_rank(rowk + buf * kMaxPanelCols + jj, ok))));
     }
     __syncthreads();
@@ -2512,12 +2551,17 @@ int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w
   // panel resident in the SMs (grid of up to one CTA per SM, one grid barrier per pivot)
   if (lpath != "coop" && plu_resident<T>(A, Z, J, R, n, r, km, w, st)) return r;
   init_row_keys(km, J, R, w.keys, st);
+  // chunks of 1 row group (blockDim * V rows) per claim; 2 on panels of 4M+ rows
+  // (fewer claims on the one counter)
   LuArgs<T> a{A, Z, J, R, n, r, w.keys, km, reinterpret_cast<Cand<T>*>(w.cands), w.bar, w.info, w.prof,
-              std::getenv("RCPG_LU_NODELAY") == nullptr ? 1 : 0};
+              std::getenv("RCPG_LU_NODELAY") == nullptr ? 1 : 0, w.ctr, 0};
+  RCPG_CUDA(cudaMemsetAsync(w.ctr, 0, size_t(n + 1) * sizeof(unsigned), st));
   // about one group of V panel rows per thread; the per-step work is latency bound
   auto run = [&](auto kern, int V) {
     const int maxc = max_coop_blocks(kern, kLuThreads, 0);
     const int G = int(std::max<i64>(1, std::min<i64>({ceil_div(J, i64(kLuThreads) * V), i64(maxc), i64(w.max_blocks)})));
+    const i64 cgr = J >= (i64(1) << 22) ? 2 : 1;
+    a.chunk_groups = ceil_div(J, i64(kLuThreads) * V * cgr) >= 2 * i64(G) ? int(cgr) : 0;
     launch_coop(kern, G, kLuThreads, 0, st, a);
   };
   constexpr int VV = 16 / int(sizeof(T));

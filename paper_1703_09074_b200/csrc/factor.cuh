@@ -24,6 +24,7 @@ struct FactorWork {
   unsigned long long* prof = nullptr;  // optional phase timers (RCPG_PROFILE_LU)
   double* rowk = nullptr;     // [kMaxPanelCols] Householder: row k before its update
   bool faithful_qr = false;   // thin_qr: always the faithful Householder (no CholeskyQR2)
+  unsigned* ctr = nullptr;    // [kMaxPanelCols + 1] grid LU per-step chunk counters
 };
 
 size_t factor_cand_bytes();
