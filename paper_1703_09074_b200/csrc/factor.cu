@@ -1265,340 +1265,6 @@ __global__ void __launch_bounds__(lu_res_max_threads(RC, RPT), 1) plu_resident_k
   if constexpr (CL) cg::this_cluster().sync();  // keep this CTA's smem alive for remote readers
 }
 
-// Resident LU with tagged candidate slots (the non-cluster grids): per pivot
-// two block barriers and no grid barrier.
-//  1. warp reduce of the candidates; each warp's winning lane stages its row's
-//     register columns; B1; warp 0 picks the CTA's best, writes its key and row
-//     to slot (k & 1, b) and releases tag = k + 1 (after a fence).
-//  2. warps 0..4 poll the G slots (one per lane, acquire) -- the wait on the
-//     slowest CTA and the key loads in one round trip -- reduce, and the warp
-//     winner's row is fetched; B2; every thread picks the winner of <= 5.
-//  3. bookkeeping without a barrier: the column maps are double-buffered by
-//     step parity (this step's swap applied on the fly, the next buffer written
-//     by warp 0), and each row's physical position is kept by its owner (the
-//     row at physical position k moves to the pivot's position).
-//  4. the update of plu_resident_kernel (same keys, arithmetic and results).
-// Slot reuse is safe: CTA X overwrites slot (k & 1) at step k + 2 only after
-// seeing every CTA's tag k + 2, published after that CTA's reads of step k.
-template <typename T>
-struct LuTagArgs {
-  LuResArgs<T> b;
-  unsigned* tags;  // [2][G]
-};
-
-template <typename T, int RC, int RPT>
-__global__ void __launch_bounds__(lu_res_max_threads(RC, RPT), 1) plu_resident_tag_kernel(LuTagArgs<T> pa) {
-  const LuResArgs<T>& p = pa.b;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int tid = threadIdx.x, nt = blockDim.x, G = gridDim.x, b = blockIdx.x;
-  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
-  const int n = p.n, ns = p.ns, ldl = p.chunk;
-  const i64 R = p.R;
-  const i64 r0 = i64(b) * p.chunk;
-  const int rows = int(max(i64(0), min(i64(p.chunk), p.J - r0)));
-  T* a = reinterpret_cast<T*>(smem_raw);                                             // [ns][ldl]
-  i64* physl = reinterpret_cast<i64*>(smem_raw + ((size_t(ns) * ldl * sizeof(T) + 15) & ~size_t(15)));  // [ldl]
-  __shared__ int colb[2][kMaxPanelCols], pcolb[2][kMaxPanelCols];  // storage col at physical q / physical of storage c
-  __shared__ Cand<T> wc[32];                                         // warp bests (B1)
-  __shared__ Cand<T> pw[kResKeyLoads];                               // poll-warp winners (B2)
-  __shared__ int wlr[32];                                            // local row of each warp best (-1: none)
-  __shared__ __align__(16) T wreg[32][RC > 0 ? RC : 1];              // the warp best's register columns
-  __shared__ __align__(16) T wrow[kResKeyLoads][kMaxPanelCols];      // rows of the poll-warp winners
-  __shared__ int s_k0;
-  const Cand<T> none{T(-1), 0x7fffffff, 0, 0x7fffffffffffffffll, 0};
-  unsigned* tags = pa.tags;
-  T rg[RPT][RC > 0 ? RC : 1];
-  for (int c = tid; c < n; c += nt) {
-    colb[0][c] = c;
-    pcolb[0][c] = c;
-  }
-  if (tid == 0) s_k0 = p.r;
-  if (tid < 2) tags[tid * G + b] = 0u;
-  Cand<T> best = none;
-  i64 psr[RPT];
-#pragma unroll
-  for (int i = 0; i < RPT; ++i) {
-    const int lr = tid + i * nt;
-    psr[i] = 0;
-    if (lr >= rows) continue;
-    const i64 s = r0 + lr;
-    const i64 ba = row_base(s, R, p.J, n);
-    const i64 ps = p.keys[s];
-    physl[lr] = ps;
-    psr[i] = ps;
-    T rv = T(-1);
-    int rq = 0;
-    for (int c = 0; c < ns; ++c) {
-      const T x = p.A[ba + c * R];
-      a[c * ldl + lr] = x;
-      if (fabs(x) > rv) {
-        rv = fabs(x);
-        rq = c;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < RC; ++j) {
-      const T x = ns + j < n ? p.A[ba + (ns + j) * R] : T(0);
-      rg[i][j] = x;
-      if (ns + j < n && fabs(x) > rv) {
-        rv = fabs(x);
-        rq = ns + j;
-      }
-    }
-    const Cand<T> cd{rv, rq, rq, ps, s};
-    if (better(cd, best)) best = cd;
-  }
-  grid_sync(p.bar);  // the tags are cleared everywhere before the first publish
-  const bool prof = p.prof != nullptr && b == 0 && tid == 0;
-  unsigned long long t0 = prof ? lu_timer() : 0, t1 = 0;
-  auto stamp = [&](int slot) {
-    if (prof) {
-      t1 = lu_timer();
-      p.prof[slot] += t1 - t0;
-      t0 = t1;
-    }
-  };
-  for (int k = 0; k < p.r; ++k) {
-    const int par = k & 1;
-    const int* col_prev = colb[par];
-    const int* pcol_prev = pcolb[par];
-    // ---- 1. warp best (lane index carried), register columns staged, CTA best, publish
-    {
-      Cand<T> x = best;
-      int xl = lane;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const Cand<T> y = shfl_cand(x, o);
-        const int yl = __shfl_xor_sync(0xffffffffu, xl, o);
-        if (better(y, x)) {
-          x = y;
-          xl = yl;
-        }
-      }
-      if (lane == 0) {
-        wc[wid] = x;
-        wlr[wid] = (x.v > T(0) && x.s >= r0 && x.s < r0 + rows) ? int(x.s - r0) : -1;
-      }
-      if (RC > 0 && lane == xl && x.v > T(0) && x.s >= r0 && x.s < r0 + rows) {
-        const int lr = int(x.s - r0), ii = lr / nt;
-#pragma unroll
-        for (int i = 0; i < RPT; ++i)
-          if (i == ii)
-#pragma unroll
-            for (int j = 0; j < RC; ++j) wreg[wid][j] = rg[i][j];
-      }
-    }
-    __syncthreads();  // B1
-    if (wid == 0) {
-      Cand<T> x = lane < nw ? wc[lane] : none;
-      int xw = lane;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const Cand<T> y = shfl_cand(x, o);
-        const int yw = __shfl_xor_sync(0xffffffffu, xw, o);
-        if (better(y, x)) {
-          x = y;
-          xw = yw;
-        }
-      }
-      const int lr = wlr[xw];
-      T* dst = p.pubr + (i64(par) * G + b) * n;
-      if (lr >= 0)
-        for (int c = lane; c < n; c += 32) dst[c] = c < ns ? a[c * ldl + lr] : wreg[xw][(c - ns) & (RC > 0 ? RC - 1 : 0)];
-      if (lane == 0) p.pubk[par * G + b] = x;
-      __threadfence();
-      __syncwarp();
-      if (lane == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(tags + par * G + b), "r"(unsigned(k + 1)) : "memory");
-    }
-    stamp(0);
-    // ---- 2. every CTA's candidate: poll the tags, reduce, fetch the warp winner's row
-    if (wid < kResKeyLoads) {
-      const int q = wid * 32 + lane;
-      Cand<T> x = none;
-      int xq = q;
-      if (q < G) {
-        const unsigned want = unsigned(k + 1);
-        while (ld_acquire_u32(tags + par * G + q) != want) {
-        }
-        x = load_cand_cg(p.pubk + par * G + q);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const Cand<T> y = shfl_cand(x, o);
-        const int yq = __shfl_xor_sync(0xffffffffu, xq, o);
-        if (better(y, x)) {
-          x = y;
-          xq = yq;
-        }
-      }
-      if (x.v > T(0)) {
-        const T* src = p.pubr + (i64(par) * G + xq) * n;
-        for (int c = lane; c < n; c += 32) wrow[wid][c] = ldcg(src + c);
-      }
-      if (lane == 0) pw[wid] = x;
-    }
-    __syncthreads();  // B2
-    stamp(1);
-    Cand<T> g = pw[0];
-    int gw = 0;
-    for (int q = 1; q < kResKeyLoads && 32 * q < G; ++q)
-      if (better(pw[q], g)) {
-        g = pw[q];
-        gw = q;
-      }
-    if (!(g.v > T(0))) {  // exactly-zero corner (FullPivLU early stop), uniform
-      if (tid == 0) s_k0 = k;
-      break;
-    }
-    const T* U = wrow[gw];
-    const i64 ss = g.s, pr = g.prow;
-    const int cs = g.c, pc = g.pcol;
-    const int colk = col_prev[k];  // storage column at physical k before the swap
-    // next step's column maps (this step's swap applied); readers of the other
-    // buffer finished before B1 of this step
-    if (wid == 0)
-      for (int c = lane; c < n; c += 32) {
-        colb[par ^ 1][c] = c == k ? cs : (c == pc ? colk : col_prev[c]);
-        pcolb[par ^ 1][c] = c == cs ? k : (c == colk ? pc : pcol_prev[c]);
-      }
-    const T piv = U[cs];
-    const bool more = k + 1 < p.r;
-    stamp(2);
-    // ---- 3. update own rows, next candidates
-    best = none;
-    bool act[RPT];
-    T m[RPT], rv[RPT];
-    int rq[RPT], rcol[RPT];
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      const int lr = tid + i * nt;
-      act[i] = false;
-      m[i] = T(0);
-      rv[i] = T(-1);
-      rq[i] = 0x7fffffff;
-      rcol[i] = 0;
-      if (lr >= rows) continue;
-      // physical positions: the pivot row goes to k, the row at k to the pivot's
-      const i64 s = r0 + lr;
-      if (s == ss)
-        psr[i] = k;
-      else if (psr[i] == k)
-        psr[i] = pr;
-      if (psr[i] <= k) continue;  // pivoted (the pivot row itself has ps == k)
-      act[i] = true;
-      T pcv;
-      if (cs < ns) {
-        pcv = a[cs * ldl + lr];
-      } else {
-        pcv = T(0);
-#pragma unroll
-        for (int j = 0; j < RC; ++j)
-          if (cs == ns + j) pcv = rg[i][j];
-      }
-      m[i] = pcv / piv;
-      if (cs < ns) {
-        a[cs * ldl + lr] = m[i];
-      } else {
-#pragma unroll
-        for (int j = 0; j < RC; ++j)
-          if (cs == ns + j) rg[i][j] = m[i];
-      }
-    }
-    if (more) {
-      constexpr int NB = RC * RPT >= 8 ? 4 : 8;
-      for (int q0 = k + 1; q0 < n; q0 += NB) {
-        int cc[NB];
-        T uc[NB];
-#pragma unroll
-        for (int u = 0; u < NB; ++u) {
-          const int q = q0 + u;
-          cc[u] = q < n ? (q == pc ? colk : col_prev[q]) : ns;
-          uc[u] = cc[u] < ns ? U[cc[u]] : T(0);
-        }
-#pragma unroll
-        for (int i = 0; i < RPT; ++i) {
-          if (!act[i]) continue;
-          const int lr = tid + i * nt;
-          T xv[NB];
-#pragma unroll
-          for (int u = 0; u < NB; ++u)
-            if (cc[u] < ns) xv[u] = a[cc[u] * ldl + lr];
-#pragma unroll
-          for (int u = 0; u < NB; ++u)
-            if (cc[u] < ns) {
-              const T x = sub_mul_rn(xv[u], m[i], uc[u]);
-              a[cc[u] * ldl + lr] = x;
-              if (fabs(x) > rv[i]) {  // columns in physical order: first maximum
-                rv[i] = fabs(x);
-                rq[i] = q0 + u;
-                rcol[i] = cc[u];
-              }
-            }
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < RPT; ++i) {
-        if (!act[i]) continue;
-#pragma unroll
-        for (int j = 0; j < RC; ++j) {
-          const int c = ns + j;
-          if (c >= n) continue;
-          const int q = c == cs ? k : (c == colk ? pc : pcol_prev[c]);
-          if (q <= k) continue;
-          const T x = sub_mul_rn(rg[i][j], m[i], U[c]);
-          rg[i][j] = x;
-          const T ax = fabs(x);
-          if (ax > rv[i] || (ax == rv[i] && q < rq[i])) {
-            rv[i] = ax;
-            rq[i] = q;
-            rcol[i] = c;
-          }
-        }
-        const Cand<T> cd{rv[i], rq[i], rcol[i], psr[i], r0 + tid + i * nt};
-        if (better(cd, best)) best = cd;
-      }
-    }
-    stamp(3);
-    if (prof) p.prof[4] += 1;
-  }
-  __syncthreads();
-  const int k0 = s_k0;
-  // physical positions and column maps after the last executed step
-  const int fin = k0 & 1;
-#pragma unroll
-  for (int i = 0; i < RPT; ++i) {
-    const int lr = tid + i * nt;
-    if (lr < rows) physl[lr] = psr[i];
-  }
-  __syncthreads();
-  // P^{-1} L for own rows (as plu_resident_kernel)
-#pragma unroll
-  for (int i = 0; i < RPT; ++i) {
-    const int lr = tid + i * nt;
-    if (lr >= rows) continue;
-    const i64 s = r0 + lr;
-    const i64 pp = physl[lr];
-    const i64 bz = row_base(s, R, p.J, p.r);
-    for (int j = 0; j < p.r; ++j) {
-      T v = T(0);
-      if (pp == j) {
-        v = T(1);
-      } else if (j < pp && j < k0) {
-        const int c = colb[fin][j];
-        if (c < ns) {
-          v = a[c * ldl + lr];
-        } else {
-#pragma unroll
-          for (int jj = 0; jj < RC; ++jj)
-            if (c == ns + jj) v = rg[i][jj];
-        }
-      }
-      p.Z[bz + j * R] = v;
-    }
-  }
-  if (b == 0 && tid == 0) *p.info = k0;
-}
-
 // ---------------------------------------------------------- Householder
 template <typename T>
 struct QrArgs {
@@ -2706,11 +2372,6 @@ bool plu_resident(T* A, T* Z, i64 J, i64 R, int n, int r, const KoldaMap& km, Fa
     int rc, rpt;
     K k;
   };
-  using KT = void (*)(LuTagArgs<T>);
-  static const bool tagged = std::getenv("RCPG_LU_BARRIER") == nullptr;  // A/B: grid-barrier kernel
-  static const KT tk[] = {plu_resident_tag_kernel<T, 0, 1>, plu_resident_tag_kernel<T, 4, 1>,
-                          plu_resident_tag_kernel<T, 8, 1>, plu_resident_tag_kernel<T, 0, 2>,
-                          plu_resident_tag_kernel<T, 4, 2>, plu_resident_tag_kernel<T, 8, 2>};
   static const V vars[] = {{0, 1, plu_resident_kernel<T, 0, 1, false>}, {4, 1, plu_resident_kernel<T, 4, 1, false>},
                            {8, 1, plu_resident_kernel<T, 8, 1, false>}, {0, 2, plu_resident_kernel<T, 0, 2, false>},
                            {4, 2, plu_resident_kernel<T, 4, 2, false>}, {8, 2, plu_resident_kernel<T, 8, 2, false>}};
@@ -2720,10 +2381,9 @@ bool plu_resident(T* A, T* Z, i64 J, i64 R, int n, int r, const KoldaMap& km, Fa
   } lim = [] {
     Lim l{};
     for (int i = 0; i < 6; ++i) {
-      const void* kp = tagged ? reinterpret_cast<const void*>(tk[i]) : reinterpret_cast<const void*>(vars[i].k);
-      l.smem[i] = tagged ? enable_max_dyn_smem(tk[i]) : enable_max_dyn_smem(vars[i].k);
+      l.smem[i] = enable_max_dyn_smem(vars[i].k);
       cudaFuncAttributes fa{};
-      RCPG_CUDA(cudaFuncGetAttributes(&fa, kp));
+      RCPG_CUDA(cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(vars[i].k)));
       l.regs[i] = fa.numRegs;
     }
     return l;
@@ -2750,12 +2410,7 @@ bool plu_resident(T* A, T* Z, i64 J, i64 R, int n, int r, const KoldaMap& km, Fa
         init_row_keys(km, J, R, w.keys, st);
         LuResArgs<T> a{A, Z, J, R, n, r, ns, chunk, w.keys, km, reinterpret_cast<Cand<T>*>(w.cands),
                        reinterpret_cast<T*>(w.part), w.bar, w.info, w.prof};
-        if (tagged) {  // tags after the 2 x G candidate slots
-          LuTagArgs<T> ta{a, reinterpret_cast<unsigned*>(static_cast<char*>(w.cands) + 2 * size_t(G) * sizeof(Cand<T>))};
-          launch_coop(tk[i], int(G), nt, smem, st, ta);
-        } else {
-          launch_coop(vars[i].k, int(G), nt, smem, st, a);
-        }
+        launch_coop(vars[i].k, int(G), nt, smem, st, a);
         RCPG_LAUNCHED();
         if (w.prof) {
           unsigned long long h[8];
