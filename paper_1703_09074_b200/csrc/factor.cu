@@ -452,11 +452,14 @@ __global__ void __launch_bounds__(1024) plu_onchip_kernel(const T* __restrict__ 
       if (!more) continue;
       T rv = T(-1);
       int rq = 0;
+      // 32-bit offsets from per-row / pivot-row base pointers (J * n < 2^31 on
+      // this path): no 64-bit address arithmetic per entry
+      T* __restrict__ ai = a + i;
 #pragma unroll 4
       for (int q = k + 1 + g; q < n; q += tpr) {
-        const i64 co = i64(col_at[q]) * J;
-        const T x = sub_mul_rn(a[i + co], m, up[co]);
-        a[i + co] = x;
+        const int co = col_at[q] * J;
+        const T x = sub_mul_rn(ai[co], m, up[co]);
+        ai[co] = x;
         if (fabs(x) > rv) {
           rv = fabs(x);
           rq = q;
