@@ -1164,17 +1164,44 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
         }
         __syncthreads();
         if (kr_p0 < kr_ps) {
-          for (int pp = kr_p0; pp < BATCH; pp += kr_ps) {
-            double v = 0.0;
-            if (pp < np) {
-              const int* po = pidx + pp * kMaxOrder;
-              T prod = T(1);
+          // four positions at a time: their index and factor loads issued
+          // before the products (the per-position chain of dependent shared
+          // loads was the longest stall of the MTTKRP); the same product order
+          // (fp32 only: in the fp64 kernels the extra registers spill, C2 0.43 -> 0.46 ms)
+          if (sizeof(T) == 4 && N <= 4) {
+            for (int pp0 = kr_p0; pp0 < BATCH; pp0 += 4 * kr_ps) {
+              T f[4][3];
 #pragma unroll
-              for (int j = 0; j < kMaxOrder - 1; ++j)
-                if (j < N - 1) prod *= fsm[po[j] + kr_r];
-              v = double(prod);
+              for (int u = 0; u < 4; ++u) {
+                const int pp = pp0 + u * kr_ps;
+                const int* po = pidx + (pp < np ? pp : 0) * kMaxOrder;
+#pragma unroll
+                for (int j = 0; j < 3; ++j) f[u][j] = j < N - 1 ? fsm[po[j] + kr_r] : T(1);
+              }
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int pp = pp0 + u * kr_ps;
+                if (pp >= BATCH) break;
+                T prod = T(1);
+#pragma unroll
+                for (int j = 0; j < 3; ++j)
+                  if (j < N - 1) prod *= f[u][j];
+                kc[pp * ldR + kr_r] = pp < np ? double(prod) : 0.0;
+              }
             }
-            kc[pp * ldR + kr_r] = v;
+          } else {
+            for (int pp = kr_p0; pp < BATCH; pp += kr_ps) {
+              double v = 0.0;
+              if (pp < np) {
+                const int* po = pidx + pp * kMaxOrder;
+                T prod = T(1);
+#pragma unroll
+                for (int j = 0; j < kMaxOrder - 1; ++j)
+                  if (j < N - 1) prod *= fsm[po[j] + kr_r];
+                v = double(prod);
+              }
+              kc[pp * ldR + kr_r] = v;
+            }
           }
         }
         stampa(18);
@@ -1183,6 +1210,7 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
           const int pp = tid % BATCH;
           const T* src = fibT + buf * BATCH * int(I) + pp * int(I);
           double* dst = fibD + pp * ldI;
+#pragma unroll 4
           for (int i = tid / BATCH; i < int(I); i += nt / BATCH) dst[i] = double(src[i]);
         }
         __syncthreads();

@@ -131,7 +131,7 @@ __device__ Cand<T> block_best(Cand<T> x, Cand<T>* scratch) {
 // memory (physical row/column swaps, first maximum in column-major order).
 // The pivot key is (|a|, column-major index) so one 64-bit value and one
 // 32-bit index move per shuffle.
-constexpr int kSmemLuThreads = 256;
+constexpr int kSmemLuThreads = 256;  // 512 from 128 rows per CTA (plu_basis)
 
 template <typename T>
 __device__ __forceinline__ void key_better(T& v, int& idx, T ov, int oidx) {
@@ -165,8 +165,8 @@ __device__ void block_argmax(T& v, int& idx, T* sv, int* si) {
 // physical rows [r*chunk, (r+1)*chunk). Row swaps move rows between CTAs
 // through DSMEM, column swaps are local, so the elimination is Eigen's,
 // operation for operation. Two cluster barriers per pivot.
-template <typename T, bool CLUSTER>
-__global__ void __launch_bounds__(kSmemLuThreads) plu_cluster_kernel(const T* __restrict__ A, T* __restrict__ Z,
+template <typename T, bool CLUSTER, int NT = kSmemLuThreads>
+__global__ void __launch_bounds__(NT) plu_cluster_kernel(const T* __restrict__ A, T* __restrict__ Z,
                                                                      int J, int n, int chunk, i64 R, KoldaMap km,
                                                                      int* info) {
   namespace cg = cooperative_groups;
@@ -638,6 +638,12 @@ constexpr int kLuThreads = 256;
 #ifndef RCPG_LU_MINB
 #define RCPG_LU_MINB 3
 #endif
+// Column batch per load round; a software-pipelined variant (the next batch's
+// loads issued before this batch's update: B = 4 / 8, 2 or 3 CTAs per SM) was
+// 12-23% slower on every C3-C5 panel (tools/gpu_s3r.sh), not kept.
+#ifndef RCPG_LU_B
+#define RCPG_LU_B 8
+#endif
 
 // V consecutive panel rows per thread (16-byte loads/stores when V > 1): the
 // sweep is read-latency bound, so V multiplies the bytes each load keeps in
@@ -799,7 +805,7 @@ __global__ void __launch_bounds__(kLuThreads, RCPG_LU_MINB) plu_coop_kernel(LuAr
         ba = aa * p.n * R + bb;
         bz = aa * p.r * R + bb;
       }
-      constexpr int B = 8;  // vector loads in flight per thread
+      constexpr int B = RCPG_LU_B;  // vector loads in flight per thread
       LuVec<T, V> v[B];
       // the rows' physical positions, pivot-column values and the first chunk
       // are independent loads: one memory round trip, not two
@@ -2520,10 +2526,13 @@ int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w
   if (lpath == "rcluster" && plu_resident_cluster<T>(A, Z, J, R, n, r, km, w, st)) return r;
   // on-chip paths: one CTA, or one cluster of up to 16 CTAs
   static const size_t lu_lim1 = enable_max_dyn_smem(plu_cluster_kernel<T, false>);
-  static const size_t lu_lim = enable_max_dyn_smem(plu_cluster_kernel<T, true>);
+  static const size_t lu_lim = std::min(enable_max_dyn_smem(plu_cluster_kernel<T, true>),
+                                        enable_max_dyn_smem(plu_cluster_kernel<T, true, 512>));
   static const bool nonportable = [] {
     return cudaFuncSetAttribute(plu_cluster_kernel<T, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
-           cudaSuccess;
+               cudaSuccess &&
+           cudaFuncSetAttribute(plu_cluster_kernel<T, true, 512>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+               cudaSuccess;
   }();
   // When the panel needs a cluster, ~128 rows per CTA (at least 8 CTAs) beat the
   // smallest cluster that fits: 1024 x 70 fp32 (C3's samples) 403 us on 2 CTAs, 290
@@ -2547,9 +2556,12 @@ int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w
       RCPG_LAUNCHED();
       return r;
     }
+    // 512 threads from 128 rows per CTA (12000 x 30 f64 on 16 CTAs 180 -> 161 us,
+    // 10000 x 80 f32 649 -> 534 us), 256 below (900 x 30: 95 vs 98 us); tools/gpu_s3q.sh
+    const bool wide = chunk >= 128;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(cs);
-    cfg.blockDim = dim3(kSmemLuThreads);
+    cfg.blockDim = dim3(wide ? 512 : kSmemLuThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -2559,7 +2571,11 @@ int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    RCPG_CUDA(cudaLaunchKernelEx(&cfg, plu_cluster_kernel<T, true>, (const T*)A, Z, int(J), n, chunk, R, km, w.info));
+    if (wide)
+      RCPG_CUDA(cudaLaunchKernelEx(&cfg, plu_cluster_kernel<T, true, 512>, (const T*)A, Z, int(J), n, chunk, R, km,
+                                   w.info));
+    else
+      RCPG_CUDA(cudaLaunchKernelEx(&cfg, plu_cluster_kernel<T, true>, (const T*)A, Z, int(J), n, chunk, R, km, w.info));
     count_launch();
     return r;
   }
