@@ -417,7 +417,7 @@ const T* compress_mode_local(rcpg_context* c, const CompressCfg& cfg, int n, i64
   c->panelB.ensure(size_t(J) * l * sizeof(T));
   c->Y.ensure(size_t(extent) * l * sizeof(T));
   c->Qy.ensure(size_t(extent) * l * sizeof(T));
-  const i64 scr = sketch_scratch_elems<T>(v, l, sms);
+  const i64 scr = std::max(sketch_scratch_elems<T>(v, l, sms), project_scratch_elems<T>(v, l, sms));
   c->scratch.ensure(size_t(scr) * sizeof(T));
   T* P = c->panelA.as<T>();
   T* Zp = c->panelB.as<T>();
@@ -523,7 +523,7 @@ const T* compress_mode_local(rcpg_context* c, const CompressCfg& cfg, int n, i64
     }
     {
       ScopedPass sp(c, "power_xtq", (S + J * rq) * b);
-      project<T>(cur, v, Qy, extent, rq, P, c->st);
+      project<T>(cur, v, Qy, extent, rq, P, c->st, c->scratch.as<T>(), i64(c->scratch.bytes / sizeof(T)));
     }
     int rz;
     {
@@ -555,7 +555,8 @@ const T* compress_mode_local(rcpg_context* c, const CompressCfg& cfg, int n, i64
   dst.ensure(size_t(v.L) * l * v.R * sizeof(T));
   {
     ScopedPass sp(c, "project", (S + l * J) * b);
-    project<T>(cur, v, basis.q.as<T>(), extent, l, dst.as<T>(), c->st);
+    project<T>(cur, v, basis.q.as<T>(), extent, l, dst.as<T>(), c->st, c->scratch.as<T>(),
+               i64(c->scratch.bytes / sizeof(T)));
   }
   which ^= 1;
   shape[n] = l;

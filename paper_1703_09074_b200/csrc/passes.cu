@@ -299,10 +299,43 @@ void sketch(const T* X, ModeView v, const T* P, i64 cols, T* Y, T* scratch, i64 
 }
 
 namespace {
+// split-K factor of a last-mode projection: ~4 CTAs per SM, at least 2 K tiles each
+template <typename T>
+i64 project_last_splits(ModeView v, i64 cols, int num_sms, i64& tps) {
+  constexpr int BM = TileCfg<T>::BM, BK = TileCfg<T>::BK;
+  const i64 mt = ceil_div(v.L, BM), nt = ceil_div(cols, pick_bn(cols)), kt = ceil_div(v.I, BK);
+  const i64 want = std::min<i64>(ceil_div(i64(4) * num_sms, mt * nt), kt / 2);
+  if (v.R != 1 || want < 2) {
+    tps = 0;
+    return 1;
+  }
+  tps = ceil_div(kt, want);
+  return ceil_div(kt, tps);
+}
+
 template <typename T, int BN>
-void project_bn(const T* X, ModeView v, const T* Q, i64 ldq, i64 cols, T* O, cudaStream_t st) {
+void project_bn(const T* X, ModeView v, const T* Q, i64 ldq, i64 cols, T* O, cudaStream_t st, T* scratch,
+                i64 scratch_elems) {
   constexpr int BM = TileCfg<T>::BM, BK = TileCfg<T>::BK;
   const i64 nt = ceil_div(cols, BN), kt = ceil_div(v.I, BK);
+  if (v.R == 1 && scratch != nullptr) {
+    // a small output (C2's last mode: 900 x 30 from 15 CTAs) splits K and sums
+    // the partials in a fixed order (reduce_partials): 26 -> ~8 us
+    i64 tps = 0;
+    const i64 splits = project_last_splits<T>(v, cols, device_caps().num_sms, tps);
+    if (splits > 1 && splits * v.L * cols <= scratch_elems) {
+      dim3 grid{unsigned(ceil_div(v.L, BM)), unsigned(splits), unsigned(nt)};
+      ProjectLastLoader<T, BM, BN, BK> ld{X, Q, v.L, v.I, cols, ldq, kt, nullptr, tps};
+      ProjectLastPartEpilogue<T, BM, BN> ep{scratch, v.L, cols};
+      launch_tile_gemm<T, BM, BN, BK, false>(grid, ld, ep, st);
+      const i64 n = v.L * cols;
+      reduce_partials_kernel<T, T><<<unsigned(ceil_div(n, 32)), 32 * kRedChunks, 0, st>>>(scratch, splits, n, O,
+                                                                                         nullptr);
+      count_launch();
+      RCPG_LAUNCHED();
+      return;
+    }
+  }
   if (v.R > 1) {
     // batch over a in chunks of 65535 (gridDim.y limit)
     for (i64 a0 = 0; a0 < v.L; a0 += 65535) {
@@ -323,7 +356,15 @@ void project_bn(const T* X, ModeView v, const T* Q, i64 ldq, i64 cols, T* O, cud
 }  // namespace
 
 template <typename T>
-void project(const T* X, ModeView v, const T* Q, i64 ldq, i64 cols, T* O, cudaStream_t st) {
+i64 project_scratch_elems(ModeView v, i64 cols, int num_sms) {
+  i64 tps = 0;
+  const i64 splits = project_last_splits<T>(v, cols, num_sms, tps);
+  return splits > 1 ? splits * v.L * cols : 0;
+}
+
+template <typename T>
+void project(const T* X, ModeView v, const T* Q, i64 ldq, i64 cols, T* O, cudaStream_t st, T* scratch,
+             i64 scratch_elems) {
   if constexpr (std::is_same<T, double>::value) {
     if (v.R > 1) {
       project_dmma(X, v, Q, ldq, cols, O, st);
@@ -336,11 +377,11 @@ void project(const T* X, ModeView v, const T* Q, i64 ldq, i64 cols, T* O, cudaSt
     }
   }
   switch (pick_bn(cols)) {
-    case 16: project_bn<T, 16>(X, v, Q, ldq, cols, O, st); break;
-    case 32: project_bn<T, 32>(X, v, Q, ldq, cols, O, st); break;
-    case 48: project_bn<T, 48>(X, v, Q, ldq, cols, O, st); break;
-    case 64: project_bn<T, 64>(X, v, Q, ldq, cols, O, st); break;
-    default: project_bn<T, 80>(X, v, Q, ldq, cols, O, st); break;
+    case 16: project_bn<T, 16>(X, v, Q, ldq, cols, O, st, scratch, scratch_elems); break;
+    case 32: project_bn<T, 32>(X, v, Q, ldq, cols, O, st, scratch, scratch_elems); break;
+    case 48: project_bn<T, 48>(X, v, Q, ldq, cols, O, st, scratch, scratch_elems); break;
+    case 64: project_bn<T, 64>(X, v, Q, ldq, cols, O, st, scratch, scratch_elems); break;
+    default: project_bn<T, 80>(X, v, Q, ldq, cols, O, st, scratch, scratch_elems); break;
   }
 }
 
@@ -440,7 +481,8 @@ void omega_panel_f32_as_f64(u64 seed, i64 mode, const KoldaMap& km, ModeView v, 
 #define RCPG_INST(T)                                                                                     \
   template i64 sketch_scratch_elems<T>(ModeView, i64, int);                                              \
   template void sketch<T>(const T*, ModeView, const T*, i64, T*, T*, i64, int, cudaStream_t, const int*);             \
-  template void project<T>(const T*, ModeView, const T*, i64, i64, T*, cudaStream_t);                    \
+  template void project<T>(const T*, ModeView, const T*, i64, i64, T*, cudaStream_t, T*, i64);           \
+  template i64 project_scratch_elems<T>(ModeView, i64, int);                                                \
   template void omega_panel<T>(u64, i64, const KoldaMap&, ModeView, i64, int, T*, cudaStream_t, i64);
 RCPG_INST(float)
 RCPG_INST(double)

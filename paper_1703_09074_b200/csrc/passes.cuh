@@ -236,12 +236,13 @@ struct ProjectLastLoader {
   const TP* Q;
   i64 L, I, cols, ldq, ktiles;
   const int* skip = nullptr;
+  i64 tps = 0;  // > 0: split-K, blockIdx.y takes K tiles [y tps, (y + 1) tps)
   struct Tile {
     i64 i0;
   };
   __device__ void range(i64& t0, i64& t1) const {
-    t0 = 0;
-    t1 = ktiles;
+    t0 = tps > 0 ? blockIdx.y * tps : 0;
+    t1 = tps > 0 && t0 + tps < ktiles ? t0 + tps : ktiles;
   }
   __device__ Tile tile(i64 t) const { return {t * BK}; }
   __device__ T a(const Tile& tl, int k, int m) const {
@@ -251,6 +252,17 @@ struct ProjectLastLoader {
   __device__ T b(const Tile& tl, int k, int n) const {
     const i64 c = i64(blockIdx.z) * BN + n, i = tl.i0 + k;
     return (c < cols && i < I) ? T(Q[i + c * ldq]) : T(0);
+  }
+};
+
+// split-K partial of the last-mode projection: part[y][a * cols + c]
+template <typename T, int BM, int BN>
+struct ProjectLastPartEpilogue {
+  T* part;
+  i64 L, cols;
+  __device__ void operator()(int m, int n, T v) const {
+    const i64 a = i64(blockIdx.x) * BM + m, c = i64(blockIdx.z) * BN + n;
+    if (a < L && c < cols) part[(i64(blockIdx.y) * L + a) * cols + c] = v;
   }
 };
 
@@ -275,8 +287,13 @@ void sketch(const T* X, ModeView v, const T* P, i64 cols, T* Y, T* scratch, i64 
             int num_sms, cudaStream_t st, const int* skip = nullptr);
 template <typename T>
 i64 sketch_scratch_elems(ModeView v, i64 cols, int num_sms);
+// scratch (optional): split-K partials of a last-mode view (R == 1), when the
+// plain grid would be small (project_scratch_elems doubles)
 template <typename T>
-void project(const T* X, ModeView v, const T* Q, i64 ldq, i64 cols, T* O, cudaStream_t st);
+void project(const T* X, ModeView v, const T* Q, i64 ldq, i64 cols, T* O, cudaStream_t st, T* scratch = nullptr,
+             i64 scratch_elems = 0);
+template <typename T>
+i64 project_scratch_elems(ModeView v, i64 cols, int num_sms);
 
 // 128-byte CUtensorMap (opaque here) for an fp64 (d0, d1, d2) view, box {16, b1, 1}, 128B swizzle.
 void tensor_map_f64_3d(void* out, const double* base, i64 d0, i64 d1, i64 d2, int b1, i64 pitch = 0);
