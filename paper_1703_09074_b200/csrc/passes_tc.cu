@@ -405,7 +405,11 @@ constexpr i64 kMaxCoord = (i64(1) << 31) - 1;
 // are zero on both sides (zero coef, TMA zero fill), so they add nothing.
 constexpr int kResMaxOrder = 8;
 constexpr int kRBM = 128, kRBN = 64;
-constexpr int kResThreads = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 coef + epilogue
+// warp 0 TMA, warp 1 MMA, warps 2-9 coef + epilogue: two warps per TMEM lane
+// quadrant, each taking one 32-column box of an item (with four epilogue warps,
+// one per scheduler, the epilogue had no latency hiding: C5 3.2 TB/s)
+constexpr int kResThreads = 320;
+constexpr int kResEpi = kResThreads - 64;  // epilogue threads (mbarrier arrival counts)
 
 struct ResArgs {
   i64 P, E;
@@ -464,19 +468,19 @@ __global__ void __launch_bounds__(kResThreads, 1)
   if (threadIdx.x == 0) {
     for (int b = 0; b < SX; ++b) {
       mbar_init(&fullx[b], 1);
-      mbar_init(&emptyx[b], 128);
+      mbar_init(&emptyx[b], kResEpi);
     }
     for (int b = 0; b < SB; ++b) {
       mbar_init(&fullb[b], 1);
       mbar_init(&emptyb[b], 1);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&afull[b], 128);
+      mbar_init(&afull[b], kResEpi);
       mbar_init(&aempty[b], 1);
     }
     for (int b = 0; b < NA; ++b) {
       mbar_init(&accf[b], 1);
-      mbar_init(&acce[b], 128);
+      mbar_init(&acce[b], kResEpi);
     }
     fence_mbar_init();
     tma_prefetch_desc(&tmX);
@@ -541,7 +545,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
     }
   } else {
     // ------------------------------------- coef rows + residual epilogue
-    const int qd = warp & 3;
+    const int qd = warp & 3, gq = (warp - 2) >> 2;  // lane quadrant, column half
     const int m = qd * 32 + lane;
     const uint32_t my_lanes = tmem + tmem_lane(qd);
     double acc_r = 0.0, acc_x = 0.0;
@@ -564,6 +568,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
       fence_after_sync();
 #pragma unroll
       for (int h = 0; h < KP / 32; ++h) {
+        if ((h & 1) != gq) continue;  // the two warps of a quadrant split the coef columns
         float hi[32], lo[32];
 #pragma unroll
         for (int rr = 0; rr < 32; ++rr) {
@@ -604,8 +609,9 @@ __global__ void __launch_bounds__(kResThreads, 1)
         const uint32_t taddr = my_lanes + G::DCOL + uint32_t(pb) * kRBN;
         // 32 accumulator columns per TMEM load, one wait per load (not per 8 columns);
         // the X reads of the 32-column box are issued before the wait
-#pragma unroll
-        for (int c32 = 0; c32 < kRBN; c32 += 32) {
+        static_assert(kRBN == 64, "one 32-column box per epilogue warp group");
+        {
+          const int c32 = 32 * gq;
           uint32_t xr[32];
           tmem_ld32_nw(taddr + c32, xr);
           const unsigned char* box = xs + (c32 >> 5) * (kRBM * 128) + m * 128;
@@ -650,8 +656,13 @@ __global__ void __launch_bounds__(kResThreads, 1)
   fence_before_sync();
   __syncthreads();
   if (threadIdx.x == 0) {
-    p.part[2 * blockIdx.x] = ((red[0][0] + red[0][1]) + red[0][2]) + red[0][3];
-    p.part[2 * blockIdx.x + 1] = ((red[1][0] + red[1][1]) + red[1][2]) + red[1][3];
+    double r0 = 0.0, r1 = 0.0;
+    for (int q = 0; q < 8; ++q) {
+      r0 += red[0][q];
+      r1 += red[1][q];
+    }
+    p.part[2 * blockIdx.x] = r0;
+    p.part[2 * blockIdx.x + 1] = r1;
   }
   if (warp == 1) {
     fence_after_sync();
