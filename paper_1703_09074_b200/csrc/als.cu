@@ -1691,36 +1691,51 @@ __global__ void __launch_bounds__(256) residual_dmma_kernel(const double* __rest
     const bool ok0 = row0 < prefix, ok1 = row1 < prefix;
     const double* x0 = X + row0 * L;
     const double* x1 = X + row1 * L;
-#pragma unroll 4
-    for (int nt = nh; nt < NT8; nt += 2) {
-      const int c = nt * 8 + 2 * t;
-      double x00 = 0.0, x01 = 0.0, x10 = 0.0, x11 = 0.0;
-      if (v16 && c + 1 < L) {
-        if (ok0) {
-          const double2 v = *reinterpret_cast<const double2*>(x0 + c);
-          x00 = v.x;
-          x01 = v.y;
-        }
-        if (ok1) {
-          const double2 v = *reinterpret_cast<const double2*>(x1 + c);
-          x10 = v.x;
-          x11 = v.y;
-        }
-      } else {
-        if (ok0 && c < L) x00 = x0[c];
-        if (ok0 && c + 1 < L) x01 = x0[c + 1];
-        if (ok1 && c < L) x10 = x1[c];
-        if (ok1 && c + 1 < L) x11 = x1[c + 1];
-      }
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    // X of kPf tiles loaded before their MMAs: with the loads interleaved with the
+    // (volatile asm) MMAs one HBM latency was exposed per tile (C2: 2.2 TB/s)
+    constexpr int kPf = 8;
+    for (int nb = nh; nb < NT8; nb += 2 * kPf) {
+      double xv[kPf][4];
 #pragma unroll
-      for (int s = 0; s < KS; ++s) als_dmma(acc, a0[s], a1[s], Bs[(nt * 8 + g) * ldb + 4 * s + t]);
-      // acc: (row g, col c), (g, c + 1), (g + 8, c), (g + 8, c + 1); padding is zero on both sides
-      const double d00 = x00 - acc[0], d01 = x01 - acc[1], d10 = x10 - acc[2], d11 = x11 - acc[3];
-      const bool c0 = c < L, c1 = c + 1 < L;
-      acc_r += (ok0 && c0 ? d00 * d00 : 0.0) + (ok0 && c1 ? d01 * d01 : 0.0) + (ok1 && c0 ? d10 * d10 : 0.0) +
-               (ok1 && c1 ? d11 * d11 : 0.0);
-      acc_x += (x00 * x00 + x01 * x01) + (x10 * x10 + x11 * x11);
+      for (int u = 0; u < kPf; ++u) {
+        const int nt = nb + 2 * u;
+        const int c = nt * 8 + 2 * t;
+        xv[u][0] = xv[u][1] = xv[u][2] = xv[u][3] = 0.0;
+        if (nt >= NT8) continue;
+        if (v16 && c + 1 < L) {
+          if (ok0) {
+            const double2 v = __ldcs(reinterpret_cast<const double2*>(x0 + c));
+            xv[u][0] = v.x;
+            xv[u][1] = v.y;
+          }
+          if (ok1) {
+            const double2 v = __ldcs(reinterpret_cast<const double2*>(x1 + c));
+            xv[u][2] = v.x;
+            xv[u][3] = v.y;
+          }
+        } else {
+          if (ok0 && c < L) xv[u][0] = x0[c];
+          if (ok0 && c + 1 < L) xv[u][1] = x0[c + 1];
+          if (ok1 && c < L) xv[u][2] = x1[c];
+          if (ok1 && c + 1 < L) xv[u][3] = x1[c + 1];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kPf; ++u) {
+        const int nt = nb + 2 * u;
+        if (nt >= NT8) break;
+        const int c = nt * 8 + 2 * t;
+        const double x00 = xv[u][0], x01 = xv[u][1], x10 = xv[u][2], x11 = xv[u][3];
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int s = 0; s < KS; ++s) als_dmma(acc, a0[s], a1[s], Bs[(nt * 8 + g) * ldb + 4 * s + t]);
+        // acc: (row g, col c), (g, c + 1), (g + 8, c), (g + 8, c + 1); padding is zero on both sides
+        const double d00 = x00 - acc[0], d01 = x01 - acc[1], d10 = x10 - acc[2], d11 = x11 - acc[3];
+        const bool c0 = c < L, c1 = c + 1 < L;
+        acc_r += (ok0 && c0 ? d00 * d00 : 0.0) + (ok0 && c1 ? d01 * d01 : 0.0) + (ok1 && c0 ? d10 * d10 : 0.0) +
+                 (ok1 && c1 ? d11 * d11 : 0.0);
+        acc_x += (x00 * x00 + x01 * x01) + (x10 * x10 + x11 * x11);
+      }
     }
   }
   acc_r = block_reduce_sum(acc_r);
