@@ -976,10 +976,9 @@ __global__ void __launch_bounds__(lu_res_max_threads(RC, RPT), 1) plu_resident_k
   __shared__ int pcol_of[kMaxPanelCols], col_at[kMaxPanelCols];
   __shared__ T U[kMaxPanelCols];
   __shared__ i64 ov_pos[kMaxPanelCols], ov_row[kMaxPanelCols];
-  __shared__ int n_ov, s_w, red_w[kResKeyLoads];
+  __shared__ int n_ov, red_w[kResKeyLoads];
   __shared__ i64 kinv[kMaxPanelCols];  // Kolda row at physical position k (before any swap)
   __shared__ Cand<T> red[33];
-  __shared__ Cand<T> s_g;
   __shared__ Cand<T> cpub[CL ? 2 : 1];                       // CL: this CTA's candidate per parity
   __shared__ __align__(16) T rpub[CL ? 2 : 1][CL ? kMaxPanelCols : 1];  // CL: its row
   const Cand<T> none{T(-1), 0x7fffffff, 0, 0x7fffffffffffffffll, 0};
@@ -1090,19 +1089,14 @@ __global__ void __launch_bounds__(lu_res_max_threads(RC, RPT), 1) plu_resident_k
       }
     }
     __syncthreads();
-    if (tid == 0) {
-      Cand<T> g = red[0];
-      int gw = red_w[0];
-      for (int q = 1; q < kResKeyLoads && 32 * q < G; ++q)
-        if (better(red[q], g)) {
-          g = red[q];
-          gw = red_w[q];
-        }
-      s_g = g;
-      s_w = gw;
-    }
-    __syncthreads();
-    const Cand<T> g = s_g;
+    // every thread reduces the <= 5 warp winners itself (no second barrier)
+    Cand<T> g = red[0];
+    int gwin = red_w[0];
+    for (int q = 1; q < kResKeyLoads && 32 * q < G; ++q)
+      if (better(red[q], g)) {
+        g = red[q];
+        gwin = red_w[q];
+      }
     if (!(g.v > T(0))) {  // exactly-zero corner (FullPivLU early stop)
       k0 = k;
       break;
@@ -1110,10 +1104,10 @@ __global__ void __launch_bounds__(lu_res_max_threads(RC, RPT), 1) plu_resident_k
     const i64 ss = g.s, pr = g.prow;
     const int cs = g.c, pc = g.pcol;
     if constexpr (CL) {
-      const T* src = cg::this_cluster().map_shared_rank(&rpub[par & (CL ? 1 : 0)][0], s_w);
+      const T* src = cg::this_cluster().map_shared_rank(&rpub[par & (CL ? 1 : 0)][0], gwin);
       for (int c = tid; c < n; c += nt) U[c] = src[c];
     } else {
-      const T* src = p.pubr + (i64(par) * G + s_w) * n;
+      const T* src = p.pubr + (i64(par) * G + gwin) * n;
       for (int c = tid; c < n; c += nt) U[c] = ldcg(src + c);
     }
     if (tid == 0) {
