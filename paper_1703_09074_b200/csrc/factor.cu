@@ -7,19 +7,19 @@
 //                                   convention) + householderQ() * I + rank warning
 // Parity needs the reference's *basis*, not only its span.
 //
-//  * plu_smem_kernel: one CTA, panel resident in shared memory, rows and
-//    columns physically swapped exactly like FullPivLU (small I x l sample
-//    matrices Y).
-//  * plu_coop_kernel: cooperative persistent kernel over an HBM/L2 panel
-//    (the big J x l panel W = X_(n)^T Q): every CTA owns a block of rows and
-//    tracks each row's physical (Kolda) position for the column-major
-//    first-maximum tie-breaking; one grid barrier per elimination step.
-//  * cqr2_kernel: CholeskyQR2 in double followed by the Householder sign
-//    reconstruction (the LU of Q_top - S that picks each column's sign the
-//    way beta = -sign(c0)||x|| does), which yields Eigen's Householder Q up
-//    to O(eps * cond(Y)). A device-side status flag hands ill-conditioned
-//    or rank-deficient inputs to householder_kernel, a faithful
-//    right-looking Householder QR (same cooperative structure as the LU).
+// FullPivLU, by panel size (plu_basis picks the first that fits):
+//  * plu_onchip_kernel: one CTA, rows owned by threads, swaps bookkept (the
+//    I x l samples Y and small W);
+//  * plu_cluster_kernel: one thread-block cluster of 8-16 CTAs, rows in DSMEM,
+//    Eigen's physical row / column swaps (W up to ~3.5 MB);
+//  * plu_resident_kernel: the panel resident in the SMs (one CTA per SM, smem +
+//    register columns), one grid barrier per pivot (W up to ~40 MB);
+//  * plu_coop_kernel: cooperative grid over an HBM/L2 panel, rows handed out in
+//    chunks per step, delayed write-back (C3-C5's big W);
+//  * plu_basis_dist: the row-sharded panel of the multi-GPU path.
+// thin_qr: cqr2_* (CholeskyQR2 in double + the Householder sign
+// reconstruction, fp64), householder_cluster_kernel / householder_kernel (the
+// faithful Householder order: fp32, or when CholeskyQR2 declines).
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -483,125 +483,6 @@ __global__ void __launch_bounds__(1024) plu_onchip_kernel(const T* __restrict__ 
     }
     for (int j = 0; j < r; ++j)
       Z[base + j * R] = (p == j) ? T(1) : (j < p && j < k0 ? a[i + i64(col_at[j]) * J] : T(0));
-  }
-  if (tid == 0) *info = k0;
-}
-
-// FullPivLU with ONE barrier per pivot: the panel is double-buffered in
-// shared memory and every step rewrites it from the previous buffer with the
-// row swap (k <-> br) and column swap (k <-> bc) applied as an index remap,
-// the multipliers formed and the trailing update done in the same pass; the
-// next pivot's candidates come out of that pass (warp-reduced, then reduced
-// redundantly by every thread after the barrier). Same operations as
-// FullPivLU; the multiplier uses a * (1 / pivot) (an ulp from a / pivot).
-constexpr int kPpThreads = 256;
-
-template <typename T>
-__global__ void __launch_bounds__(kPpThreads) plu_pp_kernel(const T* __restrict__ A, T* __restrict__ Z, int I, int n,
-                                                            i64 R, KoldaMap km, int* info) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* b0 = reinterpret_cast<T*>(smem_raw);
-  T* b1 = b0 + i64(I) * n;
-  int* q0 = reinterpret_cast<int*>(b1 + i64(I) * n);
-  int* q1 = q0 + I;
-  __shared__ T cv[2][kPpThreads / 32];
-  __shared__ int ci[2][kPpThreads / 32];
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
-  const int r = I < n ? I : n;
-  const bool ident = (R == i64(I)) && km.n_low == 0 && km.n_high == 1;
-  T* cur = b0;
-  T* nxt = b1;
-  int* pc = q0;
-  int* pn = q1;
-  // load (physical row order) and step-0 candidates
-  T bv = T(-1);
-  int bi = 0x7fffffff;
-  if (ident) {
-    for (int j = wid; j < n; j += nw)
-      for (int i = lane; i < I; i += 32) {
-        const T x = A[i + i64(j) * I];
-        cur[i + j * I] = x;
-        key_better(bv, bi, T(fabs(x)), j * I + i);
-      }
-  } else {
-    for (int i = tid; i < I; i += nt) {
-      const i64 srow = kolda_inverse(km, i, R);
-      const i64 aa = srow / R, bb = srow - aa * R;
-      const i64 base = aa * n * R + bb;
-      for (int j = 0; j < n; ++j) cur[i + j * I] = A[base + j * R];
-    }
-    __syncthreads();
-    for (int j = wid; j < n; j += nw)
-      for (int i = lane; i < I; i += 32) key_better(bv, bi, T(fabs(cur[i + j * I])), j * I + i);
-  }
-  for (int i = tid; i < I; i += nt) pc[i] = i;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) key_better(bv, bi, __shfl_xor_sync(0xffffffffu, bv, o), __shfl_xor_sync(0xffffffffu, bi, o));
-  if (lane == 0) {
-    cv[0][wid] = bv;
-    ci[0][wid] = bi;
-  }
-  __syncthreads();
-  int k0 = r;
-  for (int k = 0; k < r; ++k) {
-    const int par = k & 1;
-    T gv = T(-1);
-    int gi = 0x7fffffff;
-    for (int w = 0; w < nw; ++w) key_better(gv, gi, cv[par][w], ci[par][w]);
-    if (!(gv > T(0))) {
-      k0 = k;
-      break;
-    }
-    const int br = gi % I, bc = gi / I;
-    const T rp = T(1) / cur[br + bc * I];
-    const bool upd = (k < r - 1);
-    bv = T(-1);
-    bi = 0x7fffffff;
-    for (int j = wid; j < n; j += nw) {
-      const int tj = (j == k) ? bc : (j == bc ? k : j);
-      const T u = cur[br + tj * I];  // pivot row (physical br -> k)
-      for (int i = lane; i < I; i += 32) {
-        const int si = (i == k) ? br : (i == br ? k : i);
-        T x = cur[si + tj * I];
-        if (i > k) {
-          const T m = cur[si + bc * I] * rp;  // multiplier of row i
-          if (j == k) {
-            x = m;
-          } else if (j > k && upd) {
-            x = sub_mul_rn(x, m, u);
-            key_better(bv, bi, T(fabs(x)), j * I + i);
-          }
-        }
-        nxt[i + j * I] = x;
-      }
-    }
-    for (int i = tid; i < I; i += nt) pn[i] = pc[(i == k) ? br : (i == br ? k : i)];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) key_better(bv, bi, __shfl_xor_sync(0xffffffffu, bv, o), __shfl_xor_sync(0xffffffffu, bi, o));
-    if (lane == 0) {
-      cv[par ^ 1][wid] = bv;
-      ci[par ^ 1][wid] = bi;
-    }
-    __syncthreads();
-    T* t = cur;
-    cur = nxt;
-    nxt = t;
-    int* tq = pc;
-    pc = pn;
-    pn = tq;
-  }
-  // P^{-1} L
-  if (ident) {
-    for (int j = wid; j < r; j += nw)
-      for (int p = lane; p < I; p += 32) Z[pc[p] + i64(j) * I] = (p == j) ? T(1) : (p > j ? cur[p + j * I] : T(0));
-  } else {
-    for (int p = tid; p < I; p += nt) {
-      const i64 srow = kolda_inverse(km, pc[p], R);
-      const i64 aa = srow / R, bb = srow - aa * R;
-      const i64 base = aa * r * R + bb;
-      for (int j = 0; j < r; ++j) Z[base + j * R] = (p == j) ? T(1) : (p > j ? cur[p + j * I] : T(0));
-    }
   }
   if (tid == 0) *info = k0;
 }
@@ -2482,15 +2363,6 @@ template <typename T>
 int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w, cudaStream_t st) {
   check_arg(n <= kMaxPanelCols, "plu_basis: panel wider than supported");
   const int r = int(std::min<i64>(J, n));
-  // one CTA with a double-buffered panel: one barrier per pivot
-  static const size_t pp_lim = enable_max_dyn_smem(plu_pp_kernel<T>);
-  const size_t pp_smem = 2 * size_t(J) * n * sizeof(T) + 2 * size_t(J) * sizeof(int);
-  if (false && pp_smem <= pp_lim) {  // slower than the swap kernel on B200 (latency bound); kept for reference
-    plu_pp_kernel<T><<<1, kPpThreads, pp_smem, st>>>(A, Z, int(J), n, R, km, w.info);
-    count_launch();
-    RCPG_LAUNCHED();
-    return r;
-  }
   // one CTA, rows owned by threads, swaps bookkept
   static const size_t oc_lim = enable_max_dyn_smem(plu_onchip_kernel<T>);
   const size_t oc_smem = size_t(J) * n * sizeof(T) + 8 + 2 * size_t(J) * sizeof(int);
