@@ -2380,8 +2380,10 @@ int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w
   if (oc_smem <= oc_lim && J * i64(n) < (i64(1) << 31) && lpath.empty() && J < oc_rows) {
     // W row lanes (whole warps) x tpr column groups, at most 1024 threads
     const int W = int(std::min<i64>(1024, ceil_div(J, 32) * 32));
+    // column groups per row for short panels: 128 x 48 f32 (C4's samples) 100 -> 76 us
+    // with 4, no gain from 400 rows up (tools/gpu_s3ac.sh); RCPG_LU_TPR overrides
     const char* tp = std::getenv("RCPG_LU_TPR");
-    const int tpr = tp ? std::max(1, std::min(atoi(tp), 1024 / W)) : 1;
+    const int tpr = tp ? std::max(1, std::min(atoi(tp), 1024 / W)) : (J <= 256 ? std::min(4, 1024 / W) : 1);
     plu_onchip_kernel<T><<<1, W * tpr, oc_smem, st>>>(A, Z, int(J), n, R, km, W, w.info);
     count_launch();
     RCPG_LAUNCHED();
