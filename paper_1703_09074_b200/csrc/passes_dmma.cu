@@ -423,7 +423,8 @@ int pick_bn8(i64 cols) {
   if (cols <= 32) return 32;
   if (cols <= 48) return 48;
   if (cols <= 64) return 64;
-  return 80;
+  if (cols <= 72) return 72;  // TMA kernels only (C3's l = 70: 80 wasted 12% of the MMAs);
+  return 80;                  // the cp.async kernels run 72 as 80
 }
 
 template <int BN, bool V>
@@ -469,6 +470,7 @@ int tma_per_sm(int bn) {
     case 32: return tma_ctas_per_sm<32, TX>();
     case 48: return tma_ctas_per_sm<48, TX>();
     case 64: return tma_ctas_per_sm<64, TX>();
+    case 72: return tma_ctas_per_sm<72, TX>();
     default: return tma_ctas_per_sm<80, TX>();
   }
 }
@@ -551,6 +553,7 @@ bool sketch_tma_dispatch(const TX* X, ModeView v, const double* P, i64 cols, dou
     case 32: launch_sketch_tma<32, TX>(X, v, P, cols, tps, total, splits, part, skip, st); break;
     case 48: launch_sketch_tma<48, TX>(X, v, P, cols, tps, total, splits, part, skip, st); break;
     case 64: launch_sketch_tma<64, TX>(X, v, P, cols, tps, total, splits, part, skip, st); break;
+    case 72: launch_sketch_tma<72, TX>(X, v, P, cols, tps, total, splits, part, skip, st); break;
     default: launch_sketch_tma<80, TX>(X, v, P, cols, tps, total, splits, part, skip, st); break;
   }
   return true;
@@ -585,6 +588,7 @@ bool project_tma_dispatch(const TX* X, ModeView v, const double* Q, i64 ldq, i64
     case 32: launch_project_tma<32, TX, TO>(X, v, Q, ldq, cols, O, st); break;
     case 48: launch_project_tma<48, TX, TO>(X, v, Q, ldq, cols, O, st); break;
     case 64: launch_project_tma<64, TX, TO>(X, v, Q, ldq, cols, O, st); break;
+    case 72: launch_project_tma<72, TX, TO>(X, v, Q, ldq, cols, O, st); break;
     default: launch_project_tma<80, TX, TO>(X, v, Q, ldq, cols, O, st); break;
   }
   return true;
