@@ -248,6 +248,53 @@ std::pair<Kruskal<S>, FitTrace> decompose(const Tensor<S>& t, const DecomposeCon
   return {std::move(model), trace};
 }
 
+// solve.hpp:183-262: CP-ALS on t itself (no compression)
+template <typename S>
+std::pair<Kruskal<S>, FitTrace> als_solve(const Tensor<S>& t, const DecomposeConfig& cfg) {
+  DecomposeConfig d = cfg;
+  d.randomized = false;
+  d.method = SolveMethod::als;
+  return decompose(t, d);
+}
+
+// kruskal.hpp:198-220: A_n = Q_n A~_n (identity modes copied), then normalize
+template <typename S>
+Kruskal<S> recover(const Kruskal<S>& k, const std::vector<ModeBasis<S>>& bases) {
+  rcpg_context* c = detail::context();
+  const int32_t order = int32_t(k.order());
+  if (Index(bases.size()) != k.order()) throw std::invalid_argument("recover: need exactly one basis per mode");
+  std::vector<int64_t> sext, dims, cols;
+  std::vector<int32_t> ident;
+  std::vector<S> f, q;
+  for (Index m = 0; m < k.order(); ++m) {
+    const auto& fm = k.factors[std::size_t(m)];
+    const auto& b = bases[std::size_t(m)];
+    sext.push_back(fm.rows());
+    f.insert(f.end(), fm.data(), fm.data() + fm.size());
+    ident.push_back(b.identity ? 1 : 0);
+    dims.push_back(b.identity ? b.dim : b.q.rows());
+    cols.push_back(b.identity ? 0 : b.q.cols());
+    if (!b.identity) q.insert(q.end(), b.q.data(), b.q.data() + b.q.size());
+  }
+  if (q.empty()) q.push_back(S(0));
+  const Index R = k.rank();
+  Index big = 0;
+  for (int64_t d : dims) big += d;
+  std::vector<S> ow(static_cast<std::size_t>(R)), of(static_cast<std::size_t>(big * R));
+  detail::check(c, rcpg_recover(c, detail::dtype<S>(), order, R, sext.data(), k.weights.data(), f.data(),
+                                ident.data(), dims.data(), cols.data(), q.data(), ow.data(), of.data()));
+  Kruskal<S> out;
+  out.weights = ow;
+  Index off = 0;
+  for (int64_t d : dims) {
+    Matrix<S> mtx(d, R);
+    for (Index i = 0; i < d * R; ++i) mtx.data()[i] = of[std::size_t(off + i)];
+    off += d * R;
+    out.factors.push_back(std::move(mtx));
+  }
+  return out;
+}
+
 // compress.hpp:86-146
 template <typename S>
 CompressionResult<S> compress(const Tensor<S>& t, const CompressConfig& cfg) {

@@ -174,6 +174,26 @@ rcpg_status rcpg_tensor_upload_slab_mode(rcpg_context* ctx, rcpg_dtype dtype, in
 rcpg_status rcpg_relative_error(rcpg_context* ctx, const rcpg_tensor* t, int64_t rank, const void* weights,
                                 const void* factors, double* out);
 
+/* recover (kruskal.hpp:198-220): the full-space model of a model fitted on the
+ * compressed tensor. Inputs: order, rank R, the compressed extents, the small
+ * model (weights [R], factors column-major concatenated, extent_m x R each) and
+ * the bases as rcpg_projection_residual_bases takes them plus their row counts
+ * `dims` (identity: the factor is copied, dims[m] must equal its extent; else
+ * Q_m is dims[m] x cols[m] with cols[m] = the compressed extent). A_m = Q_m A~_m,
+ * then normalize (kruskal.hpp:117-176). Outputs: weights [R] and the factors
+ * (dims[m] x R, concatenated). Errors as the reference: INVALID_ARGUMENT with
+ * "recover: ..." messages. */
+rcpg_status rcpg_recover(rcpg_context* ctx, rcpg_dtype dtype, int32_t order, int64_t rank,
+                         const int64_t* small_extents, const void* weights, const void* factors,
+                         const int32_t* identity, const int64_t* dims, const int64_t* cols, const void* q_concat,
+                         void* out_weights, void* out_factors);
+
+/* als_solve (solve.hpp:183-262): CP-ALS on the tensor itself (no compression;
+ * cfg->method and cfg->randomized are ignored), with the fit trace and the
+ * final relative error of the returned model. */
+rcpg_status rcpg_als_solve(rcpg_context* ctx, const rcpg_tensor* t, const rcpg_decompose_config* cfg,
+                           rcpg_result* res);
+
 /* ---- bound validation (compress.hpp:148-164, diagnostics.hpp:36-86) ---- */
 /* projection_residual: ||t - t x_n Q_n Q_n^T ...||_F over the compressed modes of
  * `c` (the result of rcpg_compress on t); fp64 accumulation. */

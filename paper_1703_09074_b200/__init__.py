@@ -7,7 +7,8 @@ reference's C++ API on top of its C ABI (include/rcpg.h).
 from .rcp import (  # noqa: F401
     ALS, BCD, COMPRESS, EIGENVECTORS, FACTORS, GAUSSIAN, INIT, LU, NOISE, QR, RANDOM, UNIFORM,
     CompressConfig, CompressionResult, Context, CudaError, DecomposeConfig, DeviceTensor, FitTrace, Kruskal,
-    ModeBasis, SolverError, compress, decompose, default_context, derive_seed, plu_basis, relative_error,
+    ModeBasis, SolverError, als_solve, compress, decompose, default_context, derive_seed, plu_basis, recover,
+    relative_error,
     sketch_matrix, stream_id, stream_pass, thin_qr, comm_unique_id, comm_init_loopback, slab_range,
     BoundReport, projection_residual, theorem_bound, validate_bound, TRIAL,
 )
@@ -15,6 +16,6 @@ from ._lib import LIB_PATH, build  # noqa: F401
 
 __all__ = [
     "CompressConfig", "DecomposeConfig", "Kruskal", "FitTrace", "SolverError", "ModeBasis", "CompressionResult",
-    "compress", "decompose", "relative_error", "sketch_matrix", "stream_pass", "comm_unique_id", "comm_init_loopback", "slab_range", "plu_basis", "thin_qr", "DeviceTensor", "Context",
+    "compress", "decompose", "als_solve", "recover", "relative_error", "sketch_matrix", "stream_pass", "comm_unique_id", "comm_init_loopback", "slab_range", "plu_basis", "thin_qr", "DeviceTensor", "Context",
     "BoundReport", "projection_residual", "theorem_bound", "validate_bound",
 ]

@@ -93,6 +93,8 @@ SIGNATURES = {
     "rcpg_decompose": (_I32, [_V, _V, C.POINTER(DecomposeConfigC), C.POINTER(ResultC)]),
     "rcpg_decompose_host": (_I32, [_V, C.c_int, _I32, _V, _V, C.POINTER(DecomposeConfigC), C.POINTER(ResultC)]),
     "rcpg_relative_error": (_I32, [_V, _V, _I64, _V, _V, C.POINTER(C.c_double)]),
+    "rcpg_recover": (_I32, [_V, C.c_int, _I32, _I64, _V, _V, _V, _V, _V, _V, _V, _V, _V]),
+    "rcpg_als_solve": (_I32, [_V, _V, C.POINTER(DecomposeConfigC), C.POINTER(ResultC)]),
     "rcpg_sketch_matrix": (_I32, [_V, C.c_int, _U64, _I64, _I64, _I64, _I32, _V]),
     "rcpg_comm_unique_id": (_I32, [_V]),
     "rcpg_comm_init_nccl": (_I32, [_V, C.c_int32, C.c_int32, _V]),

@@ -1691,6 +1691,61 @@ void validate_tensor_args(int dtype, int order, const int64_t* shape) {
 }  // namespace
 
 // ===================================================================== ABI
+// kruskal.hpp:198-220 on the device: A_m = Q_m A~_m (identity modes copied), then
+// normalize (the recover step of run_decompose, on host inputs)
+template <typename T>
+void run_recover(rcpg_context* c, int order, i64 R, const i64* sext, const void* weights, const void* factors,
+                 const int32_t* identity, const i64* dims, const i64* cols, const void* q_concat, void* out_w,
+                 void* out_f) {
+  check_arg(order >= 1 && order <= kMaxOrder, "recover: need exactly one basis per mode");
+  check_arg(R >= 1 && R <= kMaxRank, "recover: rank out of range");
+  i64 small_sum = 0, big_sum = 0, qsz = 0;
+  for (int m = 0; m < order; ++m) {
+    check_arg(sext[m] >= 1, "recover: factor extents must be positive");
+    if (identity[m] != 0) {
+      check_arg(dims[m] == sext[m], "recover: identity basis extent mismatch");
+    } else {
+      check_arg(cols[m] == sext[m], "recover: basis columns must match the compressed extent");
+      check_arg(dims[m] >= 1, "recover: basis extents must be positive");
+      qsz += dims[m] * cols[m];
+    }
+    small_sum += sext[m];
+    big_sum += dims[m];
+  }
+  DevBuf small, big, qb, tmp;
+  small.ensure(size_t(small_sum * R + R) * sizeof(T));
+  big.ensure(size_t(big_sum * R) * sizeof(T));
+  qb.ensure(size_t(std::max<i64>(qsz, 1)) * sizeof(T));
+  tmp.ensure(size_t(big_sum * R + R) * sizeof(T));
+  T* wdev = small.as<T>() + small_sum * R;
+  RCPG_CUDA(cudaMemcpyAsync(small.p, factors, size_t(small_sum * R) * sizeof(T), cudaMemcpyHostToDevice, c->st));
+  RCPG_CUDA(cudaMemcpyAsync(wdev, weights, size_t(R) * sizeof(T), cudaMemcpyHostToDevice, c->st));
+  if (qsz > 0)
+    RCPG_CUDA(cudaMemcpyAsync(qb.p, q_concat, size_t(qsz) * sizeof(T), cudaMemcpyHostToDevice, c->st));
+  FactorSet<T> fs{};
+  fs.order = order;
+  fs.rank = int(R);
+  i64 so = 0, bo = 0, qo = 0;
+  for (int m = 0; m < order; ++m) {
+    T* dst = big.as<T>() + bo;
+    const T* src = small.as<T>() + so;
+    if (identity[m] != 0) {
+      RCPG_CUDA(cudaMemcpyAsync(dst, src, size_t(sext[m] * R) * sizeof(T), cudaMemcpyDeviceToDevice, c->st));
+    } else {
+      small_gemm<T>(qb.as<T>() + qo, dims[m], cols[m], src, int(R), dst, c->st);
+      qo += dims[m] * cols[m];
+    }
+    fs.f[m] = dst;
+    fs.extent[m] = dims[m];
+    so += sext[m] * R;
+    bo += dims[m] * R;
+  }
+  normalize_model<T>(fs, wdev, tmp.as<T>(), c->st);
+  RCPG_CUDA(cudaMemcpyAsync(out_w, wdev, size_t(R) * sizeof(T), cudaMemcpyDeviceToHost, c->st));
+  RCPG_CUDA(cudaMemcpyAsync(out_f, big.p, size_t(big_sum * R) * sizeof(T), cudaMemcpyDeviceToHost, c->st));
+  RCPG_CUDA(cudaStreamSynchronize(c->st));
+}
+
 extern "C" {
 
 const char* rcpg_version(void) { return "rcpg 0.1 (sm_100a)"; }
@@ -2254,6 +2309,32 @@ rcpg_status rcpg_projection_residual_bases(rcpg_context* c, const rcpg_tensor* t
     *out = t->dtype == RCPG_F64 ? run_projection_residual<double>(c, t, &comp)
                                 : run_projection_residual<float>(c, t, &comp);
   });
+}
+
+
+rcpg_status rcpg_recover(rcpg_context* c, rcpg_dtype dtype, int32_t order, int64_t rank, const int64_t* small_extents,
+                         const void* weights, const void* factors, const int32_t* identity, const int64_t* dims,
+                         const int64_t* cols, const void* q_concat, void* out_weights, void* out_factors) {
+  return guarded(c, [&] {
+    check_arg(small_extents != nullptr && weights != nullptr && factors != nullptr && identity != nullptr &&
+                  dims != nullptr && cols != nullptr && out_weights != nullptr && out_factors != nullptr,
+              "recover: null argument");
+    check_arg(dtype == RCPG_F32 || dtype == RCPG_F64, "recover: unsupported dtype");
+    if (dtype == RCPG_F64)
+      run_recover<double>(c, order, rank, small_extents, weights, factors, identity, dims, cols, q_concat,
+                          out_weights, out_factors);
+    else
+      run_recover<float>(c, order, rank, small_extents, weights, factors, identity, dims, cols, q_concat,
+                         out_weights, out_factors);
+  });
+}
+
+rcpg_status rcpg_als_solve(rcpg_context* c, const rcpg_tensor* t, const rcpg_decompose_config* cfg, rcpg_result* res) {
+  if (cfg == nullptr) return rcpg_decompose(c, t, cfg, res);
+  rcpg_decompose_config d = *cfg;  // solve.hpp:183: the ALS on t itself
+  d.randomized = 0;
+  d.method = RCPG_ALS;
+  return rcpg_decompose(c, t, &d, res);
 }
 
 rcpg_status rcpg_theorem_bound(rcpg_context* c, const rcpg_tensor* t, int64_t k, int64_t p, double* tail_energies,

@@ -513,6 +513,81 @@ def decompose(t, cfg: DecomposeConfig, ctx: Optional[Context] = None) -> Tuple[K
             dt.free()
 
 
+def als_solve(t, cfg: DecomposeConfig, ctx: Optional[Context] = None) -> Tuple[Kruskal, FitTrace]:
+    """rcp::als_solve (solve.hpp:183-262): CP-ALS on the tensor itself, no compression
+    (cfg.method and cfg.randomized are ignored), on the GPU."""
+    import copy
+    d = copy.copy(cfg)
+    d.randomized = False
+    d.method = ALS
+    ctx = ctx or default_context()
+    dt, tmp = _as_device(t, ctx)
+    try:
+        c, keep = d._c()
+        R = max(int(d.rank), 1)
+        cap = max(int(d.max_iter), 1)
+        w = np.zeros(R, dtype=dt.dtype)
+        f = np.zeros(sum(dt.global_shape) * R, dtype=dt.dtype)
+        ti = np.zeros(cap, dtype=np.int32)
+        tf = np.zeros(cap, dtype=np.float64)
+        ts = np.zeros(cap, dtype=np.float64)
+        res = _L.ResultC()
+        res.weights = w.ctypes.data
+        res.factors = f.ctypes.data
+        res.trace_iteration = ti.ctypes.data_as(C.POINTER(C.c_int32))
+        res.trace_fit = tf.ctypes.data_as(C.POINTER(C.c_double))
+        res.trace_seconds = ts.ctypes.data_as(C.POINTER(C.c_double))
+        res.trace_capacity = cap
+        ctx.check(ctx.lib.rcpg_als_solve(ctx.h, dt.h, C.byref(c), C.byref(res)))
+        facs, off = [], 0
+        for e in dt.global_shape:
+            facs.append(f[off:off + e * R].reshape((e, R), order="F").copy(order="F"))
+            off += e * R
+        n = int(res.iterations)
+        trace = FitTrace(
+            entries=[FitTrace.Entry(int(ti[i]), float(tf[i]), float(ts[i])) for i in range(min(n, cap))],
+            final_relative_error=float(res.final_relative_error),
+            iterations=n,
+            converged=bool(res.converged),
+        )
+        return Kruskal(w, facs), trace
+    finally:
+        if tmp:
+            dt.free()
+
+
+def recover(model: Kruskal, bases, ctx: Optional[Context] = None) -> Kruskal:
+    """rcp::recover (kruskal.hpp:198-220) on the GPU: A_n = Q_n A~_n for every
+    non-identity basis (identity modes copied), then normalize (kruskal.hpp:117-176).
+    `bases` is a list of ModeBasis (CompressionResult.bases)."""
+    ctx = ctx or default_context()
+    w = np.ascontiguousarray(model.weights)
+    dtype = w.dtype
+    if dtype not in (np.float32, np.float64):
+        raise TypeError("recover: float32 or float64 models")
+    R = int(w.size)
+    order = len(model.factors)
+    if len(bases) != order:
+        raise ValueError("recover: need exactly one basis per mode")
+    sext = np.array([f.shape[0] for f in model.factors], dtype=np.int64)
+    f = np.concatenate([np.asarray(x, dtype=dtype).reshape(-1, order="F") for x in model.factors])
+    ident = np.array([1 if b.identity else 0 for b in bases], dtype=np.int32)
+    dims = np.array([int(b.dim) for b in bases], dtype=np.int64)
+    cols = np.array([0 if b.identity else int(np.asarray(b.q).shape[1]) for b in bases], dtype=np.int64)
+    qs = [np.asarray(b.q, dtype=dtype).reshape(-1, order="F") for b in bases if not b.identity]
+    q = np.concatenate(qs) if qs else np.zeros(1, dtype=dtype)
+    ow = np.zeros(R, dtype=dtype)
+    of = np.zeros(int(dims.sum()) * R, dtype=dtype)
+    ctx.check(ctx.lib.rcpg_recover(ctx.h, _dtype_code(dtype), order, R, sext.ctypes.data, w.ctypes.data,
+                                   f.ctypes.data, ident.ctypes.data, dims.ctypes.data, cols.ctypes.data,
+                                   q.ctypes.data, ow.ctypes.data, of.ctypes.data))
+    facs, off = [], 0
+    for e in dims:
+        facs.append(of[off:off + e * R].reshape((e, R), order="F").copy(order="F"))
+        off += int(e) * R
+    return Kruskal(ow, facs)
+
+
 def relative_error(t, model: Kruskal, ctx: Optional[Context] = None) -> float:
     """rcp::relative_error (kruskal.hpp:187-194) on the GPU (double accumulation)."""
     ctx = ctx or default_context()

@@ -61,6 +61,22 @@ int main() {
   auto [mb, tb] = rcp::decompose(t, bcd);
   std::printf("bcd iters=%d error=%.12f\n", tb.iterations, tb.final_relative_error);
   if (!(tb.final_relative_error < 0.05)) return 5;
+  // als_solve (solve.hpp:183-262): the uncompressed ALS equals decompose(randomized=false)
+  auto [ma, ta] = rcp::als_solve(t, cfg);
+  rcp::DecomposeConfig plain = cfg;
+  plain.randomized = false;
+  plain.method = rcp::SolveMethod::als;
+  auto [mp, tp] = rcp::decompose(t, plain);
+  std::printf("als_solve iters=%d error=%.12f\n", ta.iterations, ta.final_relative_error);
+  if (ta.iterations != tp.iterations || ta.final_relative_error != tp.final_relative_error) return 7;
+  // recover (kruskal.hpp:198-220) of a solve on the compressed tensor through the compress bases
+  rcp::DecomposeConfig small = plain;
+  small.rank = 3;
+  auto [mc, tc] = rcp::decompose(comp.compressed, small);
+  auto full = rcp::recover(mc, comp.bases);
+  const double rerr = rcp::relative_error(t, full);
+  std::printf("recover rows=%lld error=%.6f\n", (long long)full.factors[0].rows(), rerr);
+  if (full.factors[0].rows() != t.extent(0) || !(rerr < 0.05)) return 8;
   // validate_bound (diagnostics.hpp:68-86) on this tensor
   const auto rep = rcp::validate_bound(t, 2, 3, 4, 11);
   std::printf("bound=%.6f empirical=%.6f\n", rep.bound, rep.empirical_mean);
