@@ -8,6 +8,8 @@
 // Parity needs the reference's *basis*, not only its span.
 //
 // FullPivLU, by panel size (plu_basis picks the first that fits):
+//  * plu_reg_kernel: rows in registers on one CTA or a cluster of up to 16,
+//    integer-pipe pivot search (fp64 panels of <= 32 columns up to 12288 rows);
 //  * plu_onchip_kernel: one CTA, rows owned by threads, swaps bookkept (the
 //    I x l samples Y and small W);
 //  * plu_cluster_kernel: one thread-block cluster of 8-16 CTAs, rows in DSMEM,
@@ -27,6 +29,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include "factor.cuh"
 #include "runtime.cuh"
@@ -486,6 +489,432 @@ __global__ void __launch_bounds__(1024) plu_onchip_kernel(const T* __restrict__ 
   }
   if (tid == 0) *info = k0;
 }
+
+// FullPivLU with the panel in registers: thread t of CTA q (of a cluster of CS
+// CTAs) owns Kolda rows (q*RPT + j)*NT + t, j < RPT, as NC register columns in
+// storage order. Columns are bookkept (col_at / pcol_of in shared memory, every
+// CTA an identical copy), rows too (phys per row in a register): no data moves
+// per pivot. The multiplier of step k is stored straight to Z (column k of
+// P^{-1} L), so a column that has been eliminated, and a row that has been
+// pivoted, no longer holds anything that is read: the rank-1 update runs over
+// all NC columns of every row without a branch or a select, and the candidate
+// search masks eliminated columns out.
+//
+// Candidate search on the integer pipe: for |y| >= 0 the IEEE bit pattern is
+// monotone, so each row keeps the max of (high word of |y|) & mask[c] (two ALU
+// ops per entry, no fp64 compares); a warp reduces those with redux.sync, and
+// only the row(s) that reach the warp's maximum are resolved exactly -- staged
+// in shared memory, one column per lane: the low word, then the physical
+// column among equal values (Eigen's first maximum in column-major order),
+// then the physical row. One barrier (a cluster barrier on a cluster), warp 0
+// picks the winner among all warps (DSMEM) and stages (u, mask) per column,
+// one block barrier, then the multipliers (the pivot column found by a switch:
+// register arrays take compile-time indices only) and the update. Same picks,
+// same operations, same bits as plu_onchip_kernel / Eigen (x - m*u rounded
+// twice, m = x / pivot). Requires finite panels (compress checks its input).
+template <typename T>
+struct __align__(16) LuUpk {
+  T u;            // pivot row entry (storage column c)
+  unsigned mask;  // 0x7fffffff while column c is not eliminated, else 0
+  int pcol;       // physical column of storage column c after this pivot's swap
+};
+
+template <typename T, int NC, int RPT>
+constexpr int lu_reg_max_threads() {
+  // registers: the rows plus ~40 for the rest; at most 1024 threads
+  constexpr int need = NC * RPT * int(sizeof(T)) / 4 + 40;
+  constexpr int t = (65536 / need) / 32 * 32;
+  return t > 1024 ? 1024 : t;
+}
+
+// high word of |y| (the whole pattern for float) and the low word (0 for float)
+template <typename T>
+__device__ __forceinline__ unsigned lu_hi(T y) {
+  if constexpr (sizeof(T) == 8)
+    return unsigned(__double2hiint(y));
+  else
+    return __float_as_uint(y);
+}
+template <typename T>
+__device__ __forceinline__ unsigned lu_lo(T y) {
+  if constexpr (sizeof(T) == 8)
+    return unsigned(__double2loint(y));
+  else
+    return 0u;
+}
+
+#ifdef RCPG_LU_REG_PROF
+__device__ unsigned long long g_lu_reg_prof[8];
+#define LU_REG_STAMP(i)                  \
+  do {                                   \
+    if (tid == 0 && me == 0) {           \
+      const long long t_ = clock64();    \
+      prof_acc[i] += t_ - prof_t;        \
+      prof_t = t_;                       \
+    }                                    \
+  } while (0)
+#else
+#define LU_REG_STAMP(i) \
+  do {                  \
+  } while (0)
+#endif
+
+#define RCPG_LU_CASE(C)                                 \
+  case C:                                               \
+    if constexpr (C < NC) {                             \
+      _Pragma("unroll") for (int j = 0; j < RPT; ++j) { \
+        m[j] = x[j][C] / piv;                           \
+      }                                                 \
+    }                                                   \
+    break;
+
+template <typename T, int NC, int RPT, bool CL>
+__global__ void __launch_bounds__(lu_reg_max_threads<T, NC, RPT>(), 1)
+    plu_reg_kernel(const T* __restrict__ A, T* __restrict__ Z, int J, int n, i64 R, KoldaMap km, int* info) {
+  namespace cg = cooperative_groups;
+  constexpr int kMaxW = lu_reg_max_threads<T, NC, RPT>() / 32;
+  constexpr int kCPL = (NC + 31) / 32;  // columns per lane in the exact resolution
+  __shared__ T wrow[2][kMaxW][NC];      // each warp's best row, by pivot parity
+  __shared__ T wtmp[kMaxW][NC];         // a tied row being resolved
+  __shared__ unsigned wkh[2][kMaxW], wkl[2][kMaxW];
+  __shared__ int wki[2][kMaxW];
+  __shared__ LuUpk<T> upk[NC];
+  __shared__ int col_at[NC], pcol_of[NC];
+  __shared__ T s_piv;
+  __shared__ int s_pr, s_cs, s_stop;
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, wid = tid >> 5, NW = NT >> 5;
+  const int me = CL ? int(cg::this_cluster().block_rank()) : 0;
+  const int CS = CL ? int(cg::this_cluster().num_blocks()) : 1;
+  const int r = J < n ? J : n;
+  const bool ident = (R == i64(J)) && km.n_low == 0 && km.n_high == 1;
+  for (int c = tid; c < NC; c += NT) {
+    col_at[c] = c;
+    pcol_of[c] = c;
+    upk[c].mask = c < n ? 0x7fffffffu : 0u;
+    upk[c].pcol = c;
+  }
+  T x[RPT][NC];
+  int ph[RPT];    // physical row (-1: padding)
+  i64 ob[RPT];    // Z offset of the row
+  unsigned mh[RPT];  // max over live columns of the high word of |x|
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const int slot = (me * RPT + j) * NT + tid;
+    ph[j] = slot < J ? slot : -1;
+    i64 base = slot;
+    ob[j] = slot;
+    if (!ident && slot < J) {
+      const i64 srow = kolda_inverse(km, slot, R);
+      const i64 aa = srow / R, bb = srow - aa * R;
+      base = aa * n * R + bb;
+      ob[j] = aa * r * R + bb;
+    }
+    mh[j] = 0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      x[j][c] = (slot < J && c < n) ? A[base + c * R] : T(0);
+      mh[j] = max(mh[j], lu_hi(x[j][c]) & 0x7fffffffu);
+    }
+  }
+  __syncthreads();
+  int k0 = r;
+#ifdef RCPG_LU_REG_PROF
+  long long prof_t = clock64(), prof_acc[6] = {0, 0, 0, 0, 0, 0};
+#endif
+  for (int k = 0; k < r; ++k) {
+    const int par = k & 1;
+    LU_REG_STAMP(0);
+    // ---- warp: the rows at the warp's largest high word, resolved exactly
+    unsigned mt = 0;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j)
+      if (ph[j] >= k) mt = max(mt, mh[j]);  // live rows (phys >= k before this pivot)
+    const unsigned hmax = __reduce_max_sync(0xffffffffu, mt);
+    unsigned wl = 0;
+    int wi = 0x7fffffff;
+    {  // (hmax == 0 with live rows: a zero or subnormal corner; every live row is resolved)
+      unsigned pend = 0;  // my rows at hmax
+#pragma unroll
+      for (int j = 0; j < RPT; ++j)
+        if (ph[j] >= k && mh[j] == hmax) pend |= 1u << j;
+      bool first = true;
+      for (unsigned bal = __ballot_sync(0xffffffffu, pend != 0); bal; bal = __ballot_sync(0xffffffffu, pend != 0)) {
+        const int src = __ffs(bal) - 1;
+        T* dst = first ? &wrow[par][wid][0] : &wtmp[wid][0];
+        int prow = 0;
+        if (lane == src) {
+          const int j = __ffs(pend) - 1;
+          pend &= pend - 1;
+#pragma unroll
+          for (int jj = 0; jj < RPT; ++jj)
+            if (jj == j) {
+              prow = ph[jj];
+#pragma unroll
+              for (int c = 0; c < NC; ++c) dst[c] = x[jj][c];
+            }
+        }
+        prow = __shfl_sync(0xffffffffu, prow, src);
+        __syncwarp();
+        unsigned l = 0;
+        int pc = 0x7fffffff;
+#pragma unroll
+        for (int q = 0; q < kCPL; ++q) {
+          const int c = lane + 32 * q;
+          if (c < NC) {
+            const T v = dst[c];
+            const LuUpk<T>& e = upk[c];
+            if ((lu_hi(v) & e.mask) == hmax) {
+              const unsigned lo = lu_lo(v);
+              if (lo > l || (lo == l && e.pcol < pc)) {
+                l = lo;
+                pc = e.pcol;
+              }
+            }
+          }
+        }
+        const unsigned L = __reduce_max_sync(0xffffffffu, l);
+        const int P = int(__reduce_min_sync(0xffffffffu, unsigned(l == L ? pc : 0x7fffffff)));
+        const int I = (P << 16) | prow;
+        if (first || L > wl || (L == wl && I < wi)) {
+          if (!first) {  // a better tie: it becomes the staged row
+#pragma unroll
+            for (int q = 0; q < kCPL; ++q) {
+              const int c = lane + 32 * q;
+              if (c < NC) wrow[par][wid][c] = wtmp[wid][c];
+            }
+          }
+          wl = L;
+          wi = I;
+        }
+        first = false;
+        __syncwarp();
+      }
+    }
+    if (lane == 0) {
+      wkh[par][wid] = hmax;
+      wkl[par][wid] = wl;
+      wki[par][wid] = wi;
+    }
+    LU_REG_STAMP(1);
+    if constexpr (CL)
+      cg::this_cluster().sync();
+    else
+      __syncthreads();
+    LU_REG_STAMP(2);
+    // ---- warp 0: the winner over the cluster's warps, bookkeeping, staging
+    if (wid == 0) {
+      unsigned gh = 0, gl = 0;
+      int gi = 0x7fffffff, ge = 0;
+      for (int e = lane; e < CS * NW; e += 32) {
+        const int q = e / NW, w = e - q * NW;
+        unsigned oh, ol;
+        int oi;
+        if constexpr (CL) {
+          oh = *cg::this_cluster().map_shared_rank(&wkh[par][w], q);
+          ol = *cg::this_cluster().map_shared_rank(&wkl[par][w], q);
+          oi = *cg::this_cluster().map_shared_rank(&wki[par][w], q);
+        } else {
+          oh = wkh[par][w];
+          ol = wkl[par][w];
+          oi = wki[par][w];
+        }
+        if (oh > gh || (oh == gh && (ol > gl || (ol == gl && oi < gi)))) {
+          gh = oh;
+          gl = ol;
+          gi = oi;
+          ge = e;
+        }
+      }
+      const unsigned H = __reduce_max_sync(0xffffffffu, gh);
+      const unsigned Lw = __reduce_max_sync(0xffffffffu, gh == H ? gl : 0u);
+      const int I = int(__reduce_min_sync(0xffffffffu, unsigned(gh == H && gl == Lw ? gi : 0x7fffffff)));
+      const unsigned who = __ballot_sync(0xffffffffu, gh == H && gl == Lw && gi == I);
+      const int E = __shfl_sync(0xffffffffu, ge, __ffs(who) - 1);
+      const bool stop = H == 0 && Lw == 0;  // the largest remaining |a| is 0
+      if (lane == 0) {
+        s_stop = stop;
+        if (!stop) {
+          const int pc = I >> 16, pr = I & 0xffff;
+          const int cs = col_at[pc], ck = col_at[k];
+          col_at[pc] = ck;
+          col_at[k] = cs;
+          pcol_of[cs] = k;
+          pcol_of[ck] = pc;
+          s_pr = pr;
+          s_cs = cs;
+        }
+      }
+      __syncwarp();
+      if (!stop) {
+        const int q = E / NW, w = E - q * NW;
+        const T* src = &wrow[par][w][0];
+        if constexpr (CL) src = cg::this_cluster().map_shared_rank(src, q);
+        const int cs = s_cs;
+        for (int c = lane; c < NC; c += 32) {
+          const T u = src[c];
+          upk[c].u = u;
+          upk[c].pcol = pcol_of[c];
+          if (c == cs) {
+            upk[c].mask = 0u;
+            s_piv = u;
+          }
+        }
+      }
+    }
+    LU_REG_STAMP(3);
+    __syncthreads();
+    LU_REG_STAMP(4);
+    if (s_stop) {
+      k0 = k;
+      break;
+    }
+    const int pr = s_pr, cs = s_cs;
+    const T piv = s_piv;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const int p = ph[j];
+      ph[j] = p == pr ? k : (p == k ? pr : p);
+    }
+    T m[RPT];
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) m[j] = T(0);
+    switch (cs) {
+      RCPG_LU_CASE(0)
+      RCPG_LU_CASE(1)
+      RCPG_LU_CASE(2)
+      RCPG_LU_CASE(3)
+      RCPG_LU_CASE(4)
+      RCPG_LU_CASE(5)
+      RCPG_LU_CASE(6)
+      RCPG_LU_CASE(7)
+      RCPG_LU_CASE(8)
+      RCPG_LU_CASE(9)
+      RCPG_LU_CASE(10)
+      RCPG_LU_CASE(11)
+      RCPG_LU_CASE(12)
+      RCPG_LU_CASE(13)
+      RCPG_LU_CASE(14)
+      RCPG_LU_CASE(15)
+      RCPG_LU_CASE(16)
+      RCPG_LU_CASE(17)
+      RCPG_LU_CASE(18)
+      RCPG_LU_CASE(19)
+      RCPG_LU_CASE(20)
+      RCPG_LU_CASE(21)
+      RCPG_LU_CASE(22)
+      RCPG_LU_CASE(23)
+      RCPG_LU_CASE(24)
+      RCPG_LU_CASE(25)
+      RCPG_LU_CASE(26)
+      RCPG_LU_CASE(27)
+      RCPG_LU_CASE(28)
+      RCPG_LU_CASE(29)
+      RCPG_LU_CASE(30)
+      RCPG_LU_CASE(31)
+      RCPG_LU_CASE(32)
+      RCPG_LU_CASE(33)
+      RCPG_LU_CASE(34)
+      RCPG_LU_CASE(35)
+      RCPG_LU_CASE(36)
+      RCPG_LU_CASE(37)
+      RCPG_LU_CASE(38)
+      RCPG_LU_CASE(39)
+      RCPG_LU_CASE(40)
+      RCPG_LU_CASE(41)
+      RCPG_LU_CASE(42)
+      RCPG_LU_CASE(43)
+      RCPG_LU_CASE(44)
+      RCPG_LU_CASE(45)
+      RCPG_LU_CASE(46)
+      RCPG_LU_CASE(47)
+      RCPG_LU_CASE(48)
+      RCPG_LU_CASE(49)
+      RCPG_LU_CASE(50)
+      RCPG_LU_CASE(51)
+      RCPG_LU_CASE(52)
+      RCPG_LU_CASE(53)
+      RCPG_LU_CASE(54)
+      RCPG_LU_CASE(55)
+      RCPG_LU_CASE(56)
+      RCPG_LU_CASE(57)
+      RCPG_LU_CASE(58)
+      RCPG_LU_CASE(59)
+      RCPG_LU_CASE(60)
+      RCPG_LU_CASE(61)
+      RCPG_LU_CASE(62)
+      RCPG_LU_CASE(63)
+      RCPG_LU_CASE(64)
+      RCPG_LU_CASE(65)
+      RCPG_LU_CASE(66)
+      RCPG_LU_CASE(67)
+      RCPG_LU_CASE(68)
+      RCPG_LU_CASE(69)
+      RCPG_LU_CASE(70)
+      RCPG_LU_CASE(71)
+      RCPG_LU_CASE(72)
+      RCPG_LU_CASE(73)
+      RCPG_LU_CASE(74)
+      RCPG_LU_CASE(75)
+      RCPG_LU_CASE(76)
+      RCPG_LU_CASE(77)
+      RCPG_LU_CASE(78)
+      RCPG_LU_CASE(79)
+      RCPG_LU_CASE(80)
+      RCPG_LU_CASE(81)
+      RCPG_LU_CASE(82)
+      RCPG_LU_CASE(83)
+      RCPG_LU_CASE(84)
+      RCPG_LU_CASE(85)
+      RCPG_LU_CASE(86)
+      RCPG_LU_CASE(87)
+      RCPG_LU_CASE(88)
+      RCPG_LU_CASE(89)
+      RCPG_LU_CASE(90)
+      RCPG_LU_CASE(91)
+      RCPG_LU_CASE(92)
+      RCPG_LU_CASE(93)
+      RCPG_LU_CASE(94)
+      RCPG_LU_CASE(95)
+      default:
+        break;
+    }
+#pragma unroll
+    for (int j = 0; j < RPT; ++j)
+      if (ph[j] > k) Z[ob[j] + i64(k) * R] = m[j];  // column k of P^{-1} L
+    LU_REG_STAMP(5);
+    if (k + 1 < r) {
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) mh[j] = 0;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const LuUpk<T> e = upk[c];
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+          const T y = sub_mul_rn(x[j][c], m[j], e.u);
+          x[j][c] = y;
+          mh[j] = max(mh[j], lu_hi(y) & e.mask);
+        }
+      }
+    }
+  }
+#ifdef RCPG_LU_REG_PROF
+  if (tid == 0 && me == 0) {
+    for (int i = 0; i < 6; ++i) g_lu_reg_prof[i] = prof_acc[i];
+    g_lu_reg_prof[6] = k0;
+  }
+#endif
+  // the rest of P^{-1} L: the unit entry at p, zeros right of it (and from an
+  // early stop on); the multipliers left of min(p, k0) were stored per step
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const int p = ph[j];
+    if (p < 0) continue;
+    for (int jj = min(p, k0); jj < r; ++jj) Z[ob[j] + i64(jj) * R] = jj == p ? T(1) : T(0);
+  }
+  if (me == 0 && tid == 0) *info = k0;
+  if constexpr (CL) cg::this_cluster().sync();  // remote readers done before exit
+}
+#undef RCPG_LU_CASE
 
 // -------------------------------------------------- LU, cooperative grid
 template <typename T>
@@ -2359,6 +2788,93 @@ bool plu_resident_cluster(T* A, T* Z, i64 J, i64 R, int n, int r, const KoldaMap
   return false;
 }
 
+// Launch plu_reg_kernel<T, NC, RPT, CL> on the smallest CTA count (1, or a
+// cluster of 2..16) whose threads hold the panel with RPT rows each.
+template <typename T, int NC, int RPT>
+bool plu_reg_try(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w, cudaStream_t st, int force_cs) {
+  constexpr int maxt = lu_reg_max_threads<T, NC, RPT>();
+  static const bool nonportable = [] {
+    return cudaFuncSetAttribute(plu_reg_kernel<T, NC, RPT, true>, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                                1) == cudaSuccess;
+  }();
+  const int max_cs = nonportable ? 16 : 8;
+  for (int cs = 1; cs <= max_cs; cs *= 2) {
+    if (force_cs > 0 && cs != force_cs) continue;
+    const i64 per = ceil_div(J, i64(cs) * RPT);
+    if (per > maxt) continue;
+    const int nt = int(std::max<i64>(32, ceil_div(per, 32) * 32));
+    if (cs == 1) {
+      plu_reg_kernel<T, NC, RPT, false><<<1, nt, 0, st>>>(A, Z, int(J), n, R, km, w.info);
+    } else {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(cs);
+      cfg.blockDim = dim3(nt);
+      cfg.dynamicSmemBytes = 0;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = cs;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      RCPG_CUDA(cudaLaunchKernelEx(&cfg, plu_reg_kernel<T, NC, RPT, true>, (const T*)A, Z, int(J), n, R, km,
+                                   w.info));
+    }
+    count_launch();
+    RCPG_LAUNCHED();
+#ifdef RCPG_LU_REG_PROF
+    unsigned long long h[8];
+    RCPG_CUDA(cudaMemcpyFromSymbolAsync(h, g_lu_reg_prof, sizeof(h), 0, cudaMemcpyDeviceToHost, st));
+    RCPG_CUDA(cudaStreamSynchronize(st));
+    const double kk = double(h[6] ? h[6] : 1);
+    fprintf(stderr, "[lu reg] J=%lld n=%d cs=%d nt=%d rpt=%d cycles/pivot: update %.0f  reduce+stage %.0f  bar1 %.0f  pick %.0f  bar2 %.0f  mult %.0f\n",
+            (long long)J, n, cs, nt, RPT, h[0] / kk, h[1] / kk, h[2] / kk, h[3] / kk, h[4] / kk, h[5] / kk);
+#endif
+    return true;
+  }
+  return false;
+}
+
+// The register-resident LU for panels it holds (n <= 32 for double; 48 / 80
+// for float), one row per thread first, two when one row per thread needs more
+// than 16 CTAs. RCPG_LU_REG=0 disables it, RCPG_LU_REG_RPT / _CS force a shape,
+// RCPG_LU_PATH=reg takes it for every panel it holds (parity tests).
+template <typename T>
+bool plu_reg(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w, cudaStream_t st, bool all) {
+  static const int env_mode = [] {
+    const char* e = std::getenv("RCPG_LU_REG");
+    return e ? atoi(e) : 1;
+  }();
+  const int mode = all ? 2 : env_mode;
+  static const int force_rpt = [] {
+    const char* e = std::getenv("RCPG_LU_REG_RPT");
+    return e ? atoi(e) : 0;
+  }();
+  static const int force_cs = [] {
+    const char* e = std::getenv("RCPG_LU_REG_CS");
+    return e ? atoi(e) : 0;
+  }();
+  if (mode == 0 || J >= 65536) return false;  // row index in the low 16 bits of the pivot key
+  auto go = [&](auto nc_tag) {
+    constexpr int NC = decltype(nc_tag)::value;
+    if (force_rpt != 2 && plu_reg_try<T, NC, 1>(A, Z, J, R, n, km, w, st, force_cs)) return true;
+    if (force_rpt != 1 && plu_reg_try<T, NC, 2>(A, Z, J, R, n, km, w, st, force_cs)) return true;
+    return false;
+  };
+  // where it beats the one-CTA / cluster kernels (tools/gpu_s4c.sh): fp64 up to
+  // 32 columns (12000 x 30 161 -> 136 us, 400 x 30 70 -> 67); fp32 only for the
+  // 48-column panels of 1024+ rows (3072 x 48 178 -> 162 us), the 70-80 column
+  // ones lose (1024 x 70 241 -> 299). RCPG_LU_REG=2 takes every panel it holds.
+  if constexpr (sizeof(T) == 8) {
+    if (n <= 32) return go(std::integral_constant<int, 32>{});
+  } else {
+    if (n <= 48 && (J >= 1024 || mode == 2)) return go(std::integral_constant<int, 48>{});
+    if (n <= 80 && mode == 2) return go(std::integral_constant<int, 80>{});
+  }
+  return false;
+}
+
 template <typename T>
 int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w, cudaStream_t st) {
   check_arg(n <= kMaxPanelCols, "plu_basis: panel wider than supported");
@@ -2366,9 +2882,10 @@ int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w
   // one CTA, rows owned by threads, swaps bookkept
   static const size_t oc_lim = enable_max_dyn_smem(plu_onchip_kernel<T>);
   const size_t oc_smem = size_t(J) * n * sizeof(T) + 8 + 2 * size_t(J) * sizeof(int);
-  // A/B testing: RCPG_LU_PATH = rcluster | cluster | resident | coop starts the
-  // chain (one CTA -> one cluster, swaps bookkept -> one cluster, Eigen's
-  // physical swaps -> panel resident in the SMs -> grid) further down
+  // A/B testing: RCPG_LU_PATH = reg | onchip | rcluster | cluster | resident |
+  // coop starts the chain (rows in registers -> one CTA -> one cluster, swaps
+  // bookkept -> one cluster, Eigen's physical swaps -> panel resident in the
+  // SMs -> grid) further down
   const char* lp = std::getenv("RCPG_LU_PATH");
   const std::string lpath = lp ? lp : "";
   // from ~640 rows an 8-CTA cluster beats one CTA (C2's 900 x 30 W: 156 -> 110 us;
@@ -2377,7 +2894,8 @@ int plu_basis(T* A, T* Z, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w
     const char* e = std::getenv("RCPG_LU_ONCHIP_ROWS");
     return e ? i64(atoll(e)) : i64(640);
   }();
-  if (oc_smem <= oc_lim && J * i64(n) < (i64(1) << 31) && lpath.empty() && J < oc_rows) {
+  if ((lpath.empty() || lpath == "reg") && plu_reg<T>(A, Z, J, R, n, km, w, st, lpath == "reg")) return r;
+  if (oc_smem <= oc_lim && J * i64(n) < (i64(1) << 31) && (lpath.empty() || lpath == "onchip") && J < oc_rows) {
     // W row lanes (whole warps) x tpr column groups, at most 1024 threads
     const int W = int(std::min<i64>(1024, ceil_div(J, 32) * 32));
     // column groups per row for short panels: 128 x 48 f32 (C4's samples) 100 -> 76 us

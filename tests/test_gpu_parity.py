@@ -136,9 +136,11 @@ def test_plu_basis_rank_deficient_and_ties(rcp, oracle):
                                          (1024, 48, np.float32), (128, 48, np.float32), (12000, 30, np.float64),
                                          (20000, 70, np.float32), (160000, 30, np.float64), (50000, 48, np.float32),
                                          (416, 32, np.float64), (33, 32, np.float64), (410, 31, np.float32),
-                                         (20, 30, np.float64)])
+                                         (20, 30, np.float64), (10000, 80, np.float32), (4900, 70, np.float32),
+                                         (1000, 80, np.float32), (3072, 48, np.float32), (7000, 17, np.float64)])
 def test_plu_basis_paths_agree_bitwise(rcp, oracle, rows, cols, dt, monkeypatch):
-    """Every LU path -- one CTA (rows owned by threads, swaps bookkept), one cluster with the
+    """Every LU path -- rows in registers (one CTA or a cluster, the default for panels it holds),
+    one CTA (rows owned by threads in smem, swaps bookkept), one cluster with the
     panel resident and swaps bookkept (DSMEM exchange), one cluster with Eigen's physical swaps,
     panel resident in the SMs (smem + register columns, one grid barrier per pivot), grid over
     HBM (delayed write-back) -- makes the same pivots with the same arithmetic in the same
@@ -155,7 +157,8 @@ def test_plu_basis_paths_agree_bitwise(rcp, oracle, rows, cols, dt, monkeypatch)
         return rcp.plu_basis(x)
 
     got, tie = run(m, ""), run(t, "")
-    paths = ["resident", "coop"] + (["cluster", "rcluster"] if rows * cols * m.itemsize <= 3_000_000 else [])
+    paths = ["resident", "coop"] + (["reg", "onchip", "cluster", "rcluster"] if rows * cols * m.itemsize <= 3_000_000
+                                    else [])
     for path in paths:
         assert np.array_equal(run(m, path), got), path
         assert np.array_equal(run(t, path), tie), path
