@@ -75,6 +75,31 @@ __device__ double block_reduce_sum(double v) {
   return block_sum(v, scratch);
 }
 
+// Jacobi rotation (c, s) that annihilates a_pq: tan(phi) = t, the smaller root
+// of t^2 + 2 theta t - 1 = 0 with theta = (a_qq - a_pp) / (2 a_pq) (the
+// oracle's symmetric Jacobi), in half-angle form so the chain of long-latency
+// fp64 operations is two reciprocal square roots instead of two square roots
+// and three divisions: with d = a_qq - a_pp, b = 2 a_pq, h = sqrt(d^2 + b^2):
+// c^2 = (1 + |d| / h) / 2 and 2 s c = sign(theta) |b| / h. The round waits
+// on this chain, so its latency is the Jacobi's critical path.
+__device__ __forceinline__ void jacobi_rotation(double app, double aqq, double apq, double& c, double& s) {
+  const double d = aqq - app, b = 2.0 * apq;
+  const double h2 = d * d + b * b;
+  if (h2 > 1e-290 && h2 < 1e290) {
+    const double r = rsqrt(h2);  // 1 / h
+    const double c2 = fma(0.5 * fabs(d), r, 0.5);
+    const double ic = rsqrt(c2);
+    const bool pos = d == 0.0 || ((d > 0.0) == (b > 0.0));  // theta >= 0
+    c = c2 * ic;
+    s = (pos ? 0.5 : -0.5) * fabs(b) * r * ic;
+  } else {  // d^2 + b^2 under- or overflows: the scale-free form
+    const double theta = d / b;
+    const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+    c = 1.0 / sqrt(t * t + 1.0);
+    s = t * c;
+  }
+}
+
 // Parallel cyclic Jacobi (round-robin pairs) on a symmetric n x n matrix in
 // global memory A (destroyed; diagonal -> eigenvalues), V <- eigenvectors.
 // On exit evals[0..n) ascending, order[0..n) the column of V for each.
@@ -96,6 +121,8 @@ __device__ void jacobi_eig(double* A, double* V, int n, int ld, double* evals, i
   __syncthreads();
   const int m = n + (n & 1);  // players (one dummy when n is odd)
   const int npairs = m / 2;
+  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  const int nwp = npairs < nw ? npairs : nw;  // warps that own a pair
   for (int sweep = 0; sweep < 60; ++sweep) {
     double off = 0.0, dg = 0.0;
     for (int e = tid; e < n * n; e += nt) {
@@ -110,67 +137,78 @@ __device__ void jacobi_eig(double* A, double* V, int n, int ld, double* evals, i
     if (tid == 0) s_stop = (off <= 1e-30 * dg) || off == 0.0;
     __syncthreads();
     if (s_stop) break;
-    for (int round = 0; round < m - 1; ++round) {
-      for (int q = tid; q < npairs; q += nt) {
-        int i, j;
-        if (q == 0) {
-          i = m - 1;
-          j = round % (m - 1);
-        } else {
-          i = (round + q) % (m - 1);
-          j = (round + m - 1 - q) % (m - 1);
-        }
-        if (i > j) {
-          const int t = i;
-          i = j;
-          j = t;
-        }
-        double c = 1.0, s = 0.0;
-        if (j < n) {
-          const double apq = A[i + j * ld];
-          if (apq != 0.0) {
-            const double app = A[i + i * ld], aqq = A[j + j * ld];
-            const double theta = (aqq - app) / (2.0 * apq);
-            const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-            c = 1.0 / sqrt(t * t + 1.0);
-            s = t * c;
+    // One round = m / 2 disjoint rotations. The warp that owns pair q computes
+    // its rotation itself (no staging barrier) from columns i, j, which no other
+    // warp touches before the barrier, and rotates those columns; after the
+    // barrier it rotates rows i, j of A and columns i, j of V. Only the warps that own a pair take part (named barrier 1);
+    // the others wait at the sweep's closing barrier.
+    if (wid < nwp) {
+      for (int round = 0; round < m - 1; ++round) {
+        // lane u computes the rotation of this warp's u-th pair (all of the
+        // warp's pairs in one pass; at most 32 of them for n <= 2048)
+        int pi = 0, pj = n;
+        double pc = 1.0, ps = 0.0;
+        {
+          const int q = wid + lane * nwp;
+          if (q < npairs) {
+            int i, j;
+            if (q == 0) {
+              i = m - 1;
+              j = round;
+            } else {
+              i = round + q;
+              if (i >= m - 1) i -= m - 1;
+              j = round + m - 1 - q;
+              if (j >= m - 1) j -= m - 1;
+            }
+            if (i > j) {
+              const int t = i;
+              i = j;
+              j = t;
+            }
+            pi = i;
+            pj = j;
+            if (j < n) {
+              const double apq = A[i + j * ld];
+              if (apq != 0.0) jacobi_rotation(A[i + i * ld], A[j + j * ld], apq, pc, ps);
+            }
+            pp[q] = i;
+            pq[q] = j;
+            cs_c[q] = pc;
+            cs_s[q] = ps;
           }
         }
-        pp[q] = i;
-        pq[q] = j;
-        cs_c[q] = c;
-        cs_s[q] = s;
-      }
-      __syncthreads();
-      const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
-      // columns: A <- A J
-      for (int q = wid; q < npairs; q += nw) {
-        const int i = pp[q], j = pq[q];
-        if (j >= n) continue;
-        const double c = cs_c[q], s = cs_s[q];
-        for (int k = lane; k < n; k += 32) {
-          const double akp = A[k + i * ld], akq = A[k + j * ld];
-          A[k + i * ld] = c * akp - s * akq;
-          A[k + j * ld] = s * akp + c * akq;
+        __syncwarp();  // every rotation is formed before a lane overwrites its entries
+        // columns: A <- A J
+        for (int u = 0; wid + u * nwp < npairs; ++u) {
+          const int i = __shfl_sync(0xffffffffu, pi, u), j = __shfl_sync(0xffffffffu, pj, u);
+          const double c = __shfl_sync(0xffffffffu, pc, u), s = __shfl_sync(0xffffffffu, ps, u);
+          if (j >= n) continue;
+          for (int k = lane; k < n; k += 32) {
+            const double akp = A[k + i * ld], akq = A[k + j * ld];
+            A[k + i * ld] = c * akp - s * akq;
+            A[k + j * ld] = s * akp + c * akq;
+          }
         }
-      }
-      __syncthreads();
-      // rows: A <- J^T A, and V <- V J
-      for (int q = wid; q < npairs; q += nw) {
-        const int i = pp[q], j = pq[q];
-        if (j >= n) continue;
-        const double c = cs_c[q], s = cs_s[q];
-        for (int k = lane; k < n; k += 32) {
-          const double apk = A[i + k * ld], aqk = A[j + k * ld];
-          A[i + k * ld] = c * apk - s * aqk;
-          A[j + k * ld] = s * apk + c * aqk;
-          const double vkp = V[k + i * ld], vkq = V[k + j * ld];
-          V[k + i * ld] = c * vkp - s * vkq;
-          V[k + j * ld] = s * vkp + c * vkq;
+        asm volatile("bar.sync 1, %0;" ::"r"(nwp * 32) : "memory");
+        // rows: A <- J^T A, and V <- V J
+        for (int q = wid; q < npairs; q += nwp) {
+          const int i = pp[q], j = pq[q];
+          if (j >= n) continue;
+          const double c = cs_c[q], s = cs_s[q];
+          for (int k = lane; k < n; k += 32) {
+            const double apk = A[i + k * ld], aqk = A[j + k * ld];
+            A[i + k * ld] = c * apk - s * aqk;
+            A[j + k * ld] = s * apk + c * aqk;
+            const double vkp = V[k + i * ld], vkq = V[k + j * ld];
+            V[k + i * ld] = c * vkp - s * vkq;
+            V[k + j * ld] = s * vkp + c * vkq;
+          }
         }
+        asm volatile("bar.sync 1, %0;" ::"r"(nwp * 32) : "memory");
       }
-      __syncthreads();
     }
+    __syncthreads();
   }
   // ascending, stable by index
   for (int i = tid; i < n; i += nt) {
