@@ -100,7 +100,7 @@ struct rcpg_context {
   rcpg_compressed* dcomp = nullptr;
   // ranks of a sharded decomposition; null = unsharded
   std::unique_ptr<rcpg::Comm> comm;
-  DevBuf dl_phys, dl_cand_loc, dl_cand_all, dl_U, dl_state, sh_send, sh_recv, sh_fac;
+  DevBuf dl_phys, dl_cand_loc, dl_cand_all, dl_U, dl_state, sh_send, sh_recv, sh_fac, sh_full_w, sh_full_z;
   // fp32 arithmetic (rcpg_set_option "fp32_arith"): false = fp64 products and
   // sums with the reference's Scalar roundings (faithful, default); true = the
   // 3xTF32 tcgen05 passes and CholeskyQR2 (fast, ~1e-7 relative per pass)
@@ -830,8 +830,6 @@ void run_compress_sharded(rcpg_context* c, const rcpg_tensor* t, const CompressC
   } else {
     for (i64 m = 0; m < order; ++m) selected.insert(m);
   }
-  check_arg(cfg.stabilizer == RCPG_STAB_LU || cfg.power_iterations == 0,
-            "compress: sharded tensors use the LU stabilizer (the distributed QR stabilizer is not implemented)");
 
   i64 lsh[kMaxOrder], gsh[kMaxOrder];
   for (int m = 0; m < order; ++m) {
@@ -1001,7 +999,37 @@ void run_compress_sharded(rcpg_context* c, const rcpg_tensor* t, const CompressC
           // W (in Zp) -> Z; for the fp64 passes Z is then widened into P64 (P's memory)
           dst.ensure(size_t(J) * l * sizeof(T));
           T* Zt = mixed ? dst.as<T>() : P;
-          rz = plu_basis_dist<T>(Zp, Zt, J, v.R, rq, Jg, km, smap, comm, w, st);
+          if (cfg.stabilizer == RCPG_STAB_LU) {
+            rz = plu_basis_dist<T>(Zp, Zt, J, v.R, rq, Jg, km, smap, comm, w, st);
+          } else {
+            // QR stabilizer (compress.hpp:60-70 on the row-sharded W): the row
+            // blocks are all-gathered into the unsharded panel, thin_qr runs
+            // replicated (the same bits on every rank, like the slab mode's
+            // factorizations) and each rank keeps its own rows. In the panel
+            // layout (a, c, b) with b = (middle modes, slab index) a rank's rows
+            // are [prefix][slab][1] with prefix = L * cols * middle.
+            const i64 El = lsh[sm_], Es = gsh[sm_];
+            const i64 pre = (El > 0 ? J / El : Jg / Es) * rq, stride = pre * sl.maxext();
+            c->sh_send.ensure(size_t(std::max<i64>(stride, 1)) * sizeof(T));
+            c->sh_recv.ensure(size_t(std::max<i64>(stride, 1)) * size_t(comm.size) * sizeof(T));
+            if (J > 0)
+              RCPG_CUDA(cudaMemcpyAsync(c->sh_send.p, Zp, size_t(J) * rq * sizeof(T), cudaMemcpyDeviceToDevice, st));
+            comm.allgather(c->sh_send.p, c->sh_recv.p, size_t(stride) * sizeof(T), st);
+            c->sh_full_w.ensure(size_t(Jg) * rq * sizeof(T));
+            c->sh_full_z.ensure(size_t(Jg) * rq * sizeof(T));
+            slab_assemble_kernel<T><<<grid_for(Jg * rq), 256, 0, st>>>(c->sh_recv.as<T>(), stride, sl, pre, Es, 1,
+                                                                       c->sh_full_w.as<T>());
+            count_launch();
+            RCPG_LAUNCHED();
+            FactorWork fw = factor_work_t<T>(c, Jg);
+            rz = thin_qr<T>(c->sh_full_w.as<T>(), c->sh_full_z.as<T>(), Jg, vg.R, rq, smap.kmg, fw, nullptr, st);
+            if (J > 0) {
+              slab_extract_kernel<T><<<grid_for(J * rz), 256, 0, st>>>(c->sh_full_z.as<T>(), (J / El) * rz, Es, lo,
+                                                                        El, 1, Zt);
+              count_launch();
+              RCPG_LAUNCHED();
+            }
+          }
           if (mixed) widen_f32(reinterpret_cast<const float*>(Zt), P64, J * rz, st);
         }
         {
@@ -1076,7 +1104,11 @@ void run_compress_sharded(rcpg_context* c, const rcpg_tensor* t, const CompressC
         FactorWork w = factor_work_t<T>(c, J);
         dst.ensure(size_t(J) * l * sizeof(T));
         T* Zt = mixed ? dst.as<T>() : P;
-        rz = plu_basis<T>(Zp, Zt, J, v.R, rq, km, w, st);  // replicated (same bits on every rank)
+        // replicated (same bits on every rank)
+        if (cfg.stabilizer == RCPG_STAB_LU)
+          rz = plu_basis<T>(Zp, Zt, J, v.R, rq, km, w, st);
+        else
+          rz = thin_qr<T>(Zp, Zt, J, v.R, rq, km, w, nullptr, st);
         if (mixed) widen_f32(reinterpret_cast<const float*>(Zt), P64, J * rz, st);
       }
       {

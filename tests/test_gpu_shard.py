@@ -124,6 +124,36 @@ def test_sharded_fp32(rcp, oracle, mode, fast):
             assert tr.iterations == want[1].iterations
 
 
+@pytest.mark.parametrize("shape,nranks,mode", [((40, 30, 20), 2, -1), ((40, 30, 21), 3, -1), ((12, 10, 14, 9), 2, -1),
+                                               ((40, 30, 20), 2, 0), ((30, 24, 50), 4, -1)])
+def test_sharded_qr_stabilizer(rcp, oracle, shape, nranks, mode):
+    """stabilizer = QR (compress.hpp:60-70): the row-sharded W of the modes before a last-mode slab is
+    all-gathered, factored replicated and re-split; everything else factors replicated panels."""
+    x, _ = oracle.random_lowrank(list(shape), 4, 21, snr=3.0, noise_seed=21)
+    cfg = _cfg(rcp, 4, 5, 2, 9)
+    cfg.compress.stabilizer = rcp.QR
+    want = rcp.decompose(x, cfg)
+    got = _run_ranks(rcp, x, nranks, lambda t, c: rcp.decompose(t, cfg, ctx=c), mode=mode)
+    for g in got:
+        _check_vs_single(g, want, 1e-8)
+    for g in got[1:]:
+        for a, b in zip(g[0].factors, got[0][0].factors):
+            assert np.array_equal(a, b)
+
+
+def test_sharded_qr_stabilizer_fp32(rcp, oracle):
+    x, _ = oracle.random_lowrank([64, 48, 40], 5, 13, snr=4.0, noise_seed=13)
+    x = x.astype(np.float32)
+    cfg = _cfg(rcp, 5, 5, 2, 3, tol=1e-5, max_iter=300)
+    cfg.compress.stabilizer = rcp.QR
+    want = rcp.decompose(x, cfg)
+    got = _run_ranks(rcp, x, 2, lambda t, c: rcp.decompose(t, cfg, ctx=c), mode=-1)
+    for m, tr in got:
+        fit_g, fit_w = 1 - tr.final_relative_error ** 2, 1 - want[1].final_relative_error ** 2
+        assert abs(fit_g - fit_w) <= 1e-6 * abs(fit_w)
+        assert tr.iterations == want[1].iterations
+
+
 def test_sharded_rejects_unsupported(rcp, oracle):
     x, _ = oracle.random_lowrank([20, 18, 16], 3, 1, snr=3.0, noise_seed=1)
     det = rcp.DecomposeConfig(rank=3, randomized=False, tol=1e-8, max_iter=50)

@@ -1,6 +1,6 @@
 #!/bin/bash
-# session 5: ncu source-level captures of C2's latency kernels (ALS loop, init, residual, reg LU)
-O=gpurun_out/s5b; mkdir -p $O; T=/tmp/s5b; mkdir -p $T
+# ncu source-level captures of C2's latency kernels (ALS loop, init, residual, reg LU)
+O=gpurun_out/ncu_c2; mkdir -p $O; T=/tmp/ncu_c2; mkdir -p $T
 cap() {  # name config kernel-regex
   timeout 600 ncu --set full --import-source on --clock-control none -k regex:$3 -s 0 -c 1 -o $T/$1 \
     python tools/profile_step.py --config $2 --warmup 0 > $O/ncu_$1.log 2>&1
