@@ -499,6 +499,14 @@ i64 sketch_dmma_splits_t(ModeView v, i64 cols, int num_sms, i64& tps, i64& total
   i64 want = std::max<i64>(1, (waves * slots) / (mt * nt));
   want = std::max<i64>(1, std::min<i64>(want, 65535));
   i64 best_tps = std::max<i64>(1, ceil_div(total, want));
+  // small views (C2's mode 1: 750 K-tiles over 7 m-tiles): a two-wave plan gives
+  // every CTA ~5 K-tiles, mostly pipeline fill, and doubles the partials; one
+  // wave of CTAs twice as long is shorter
+  static const int short_tps = getenv("RCPG_SKETCH_SHORT_TPS") ? atoi(getenv("RCPG_SKETCH_SHORT_TPS")) : 16;
+  if (best_tps < short_tps) {
+    want = std::max<i64>(1, std::min<i64>(slots / (mt * nt), 65535));
+    best_tps = std::max<i64>(1, ceil_div(total, want));
+  }
   double best_fill = -1.0;
   {  // keep the 2-wave plan when its last wave is already >= 90% full or its CTAs
      // are short (more splits only add partial traffic: C2's X Z 0.42 -> 0.44 ms)

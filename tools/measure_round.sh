@@ -1,7 +1,7 @@
 #!/bin/bash
-# Final round-2 measurements (session 3): tests, bench lines C1-C5 (+ cpu_baseline / parity),
+# Round measurements: tests, bench lines C1-C5 (+ cpu_baseline / parity),
 # the reference arm, ncu launch lists and full captures (exported to CSV on the box).
-TAG=${1:-r2s3}
+TAG=${1:-r02s5}
 O=gpurun_out/$TAG; mkdir -p $O; T=/tmp/$TAG; mkdir -p $T
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt
 timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
@@ -27,3 +27,11 @@ cap C4_coop_lu C4 plu_coop
 cap C5_residual_tc C5 residual_tc
 cap C5_als C5 als_loop
 ls -la $O
+cap C2_als C2 als_loop
+cap C2_init C2 init_from_gram
+cap C2_residual C2 residual_dmma
+cap C2_reglu C2 plu_reg
+for n in C2_sketch C3_sketch_f32 C2_resident_lu C4_coop_lu C5_residual_tc C5_als C2_als C2_init C2_residual C2_reglu; do
+  python tools/ncu_src_top.py $O/ncu_${n}_source.csv.gz 40 > $O/ncu_${n}_source_top.txt 2>/dev/null
+done
+for c in C2 C3; do python tools/launch_summary.py $O/ncu_launches_$c.csv > $O/ncu_launches_${c}_summary.txt 2>/dev/null; done
