@@ -1056,7 +1056,7 @@ __device__ void als_update_grid(const FactorSet<T>& fs, int mode, const double* 
 // barrier (release / acquire at cluster scope orders the global-memory partials
 // and factors exactly like grid_sync), ~2 us less per barrier, three per mode step.
 template <typename T, int BATCH, bool CLUSTER = false>
-__global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p) {
+__global__ void __launch_bounds__(kAlsThreads, CLUSTER ? 1 : 2) als_loop_kernel(AlsLoopArgs<T> p) {
   auto gsync = [&]() {
     if constexpr (CLUSTER) {
       __threadfence();
@@ -1111,6 +1111,19 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
       double* fibD = sm + als_fib_doubles<T, BATCH>(I);           // [BATCH][ldI], converted once
       double* kc = fibD + BATCH * ldI;                 // [BATCH][ldR]
       T* fsm = reinterpret_cast<T*>(kc + BATCH * ldR); // other modes' factors, row-major (rank fastest)
+      // gather: thread tid always handles position pp = tid % BATCH
+      auto gather = [&](i64 pb, int buf) {
+        const int pp = tid % BATCH;
+        const bool ok = pb + pp < j1;
+        const unsigned s_ = unsigned(ok ? pb + pp : pb);
+        const unsigned a = s_ / unsigned(Rr), b = s_ - a * unsigned(Rr);
+        const T* src = p.B + i64(a) * I * Rr + b;
+        T* dst = fibT + buf * BATCH * int(I) + pp * int(I);
+        for (int i = tid / BATCH; i < int(I); i += nt / BATCH) als_cp_elem(dst + i, src + i64(i) * Rr, ok);
+        als_cp_commit();
+      };
+      // the first batch's fibers are in flight while the factors are staged
+      if (j0 < j1) gather(j0, 0);
       {
         __syncthreads();
         if (tid == 0) {
@@ -1138,17 +1151,6 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
         als_cp_wait<0>();
         __syncthreads();
       }
-      // gather: thread tid always handles position pp = tid % BATCH
-      auto gather = [&](i64 pb, int buf) {
-        const int pp = tid % BATCH;
-        const bool ok = pb + pp < j1;
-        const unsigned s_ = unsigned(ok ? pb + pp : pb);
-        const unsigned a = s_ / unsigned(Rr), b = s_ - a * unsigned(Rr);
-        const T* src = p.B + i64(a) * I * Rr + b;
-        T* dst = fibT + buf * BATCH * int(I) + pp * int(I);
-        for (int i = tid / BATCH; i < int(I); i += nt / BATCH) als_cp_elem(dst + i, src + i64(i) * Rr, ok);
-        als_cp_commit();
-      };
       const bool stampA = p.prof != nullptr && g == 0 && tid == 0;
       unsigned long long ts = stampA ? gtimer() : 0;
       if (stampA) p.prof[22] += ts - tp0;
@@ -1173,7 +1175,6 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
       // Khatri-Rao rows: thread -> (column kr_r, first position kr_p0), stride kr_ps
       const int kr_ps = nt / R, kr_r = tid % R, kr_p0 = tid / R;
       __syncthreads();
-      if (j0 < j1) gather(j0, 0);
       stampa(16);
       int buf = 0;
       for (i64 pb = j0; pb < j1; pb += BATCH, buf ^= 1) {
@@ -1206,7 +1207,7 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
           // before the products (the per-position chain of dependent shared
           // loads was the longest stall of the MTTKRP); the same product order
           // (fp32 only: in the fp64 kernels the extra registers spill, C2 0.43 -> 0.46 ms)
-          if (sizeof(T) == 4 && N <= 4) {
+          if ((sizeof(T) == 4 || CLUSTER) && N <= 4) {  // (one-cluster variant: registers to spare)
             for (int pp0 = kr_p0; pp0 < BATCH; pp0 += 4 * kr_ps) {
               T f[4][3];
 #pragma unroll
@@ -1254,16 +1255,40 @@ __global__ void __launch_bounds__(kAlsThreads) als_loop_kernel(AlsLoopArgs<T> p)
         __syncthreads();
         stampa(19);
         const double* fb = fibD;
-#pragma unroll 2
-        for (int ks = 0; ks < BATCH / 4; ++ks) {
-          const int pp = 4 * ks + tq;
-          const double* frow = fb + pp * ldI;
-          const double* krow = kc + pp * ldR;
+        if (CLUSTER && NTILE <= nwarp) {
+          // (one-cluster variant only: one CTA per SM, registers to spare; the grid
+          // variant keeps 128 registers for two CTAs per SM)
+          // at most one tile per warp (small compressed tensors: C1 / C2): one
+          // accumulator would be a chain of BATCH / 4 dependent DMMAs (3.8 us per
+          // batch at C2); four interleaved chains, summed pairwise per batch
+          if (wrp < NTILE) {
+            const int i0 = toff[0] & 0xffff, r0 = toff[0] >> 16;
+            double a4[4][4];
 #pragma unroll
-          for (int t = 0; t < kAlsTiles; ++t) {
-            if (wrp + t * nwarp < NTILE) {  // zero padding beyond I and R (see above)
-              const int i0 = toff[t] & 0xffff, r0 = toff[t] >> 16;
-              als_dmma(acc[t], frow[i0], frow[i0 + 8], krow[r0]);
+            for (int u = 0; u < 4; ++u) a4[u][0] = a4[u][1] = a4[u][2] = a4[u][3] = 0.0;
+#pragma unroll 2
+            for (int ks4 = 0; ks4 < BATCH / 16; ++ks4) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int pp = 4 * (4 * ks4 + u) + tq;
+                als_dmma(a4[u], fb[pp * ldI + i0], fb[pp * ldI + i0 + 8], kc[pp * ldR + r0]);
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[0][q] += (a4[0][q] + a4[1][q]) + (a4[2][q] + a4[3][q]);
+          }
+        } else {
+#pragma unroll 2
+          for (int ks = 0; ks < BATCH / 4; ++ks) {
+            const int pp = 4 * ks + tq;
+            const double* frow = fb + pp * ldI;
+            const double* krow = kc + pp * ldR;
+#pragma unroll
+            for (int t = 0; t < kAlsTiles; ++t) {
+              if (wrp + t * nwarp < NTILE) {  // zero padding beyond I and R (see above)
+                const int i0 = toff[t] & 0xffff, r0 = toff[t] >> 16;
+                als_dmma(acc[t], frow[i0], frow[i0 + 8], krow[r0]);
+              }
             }
           }
         }
@@ -1991,6 +2016,8 @@ void als_loop(const T* B, const i64* shape, int order, const FactorSet<T>& fs, T
     int G = int(std::max<i64>(1, std::min<i64>(ceil_div(maxJ, batch) + (want_split ? 1 : 0), maxc)));
     // + slots for the reduced W, pinv(V) and the grid update's unnormalized factor
     G = int(std::min<i64>(G, part_elems / (2 * maxout) - 2));
+    static const int g_cap = std::getenv("RCPG_ALS_MAXG") ? atoi(std::getenv("RCPG_ALS_MAXG")) : 0;  // A/B hook
+    if (g_cap > 0) G = std::min(G, g_cap);
     G = std::max(G, 1);
     const bool split_ok = want_split && G >= 3 && (2 * i64(G) + 3) * maxout <= part_elems;
     a.pm = split_ok ? part + (2 * i64(G) + 1) * maxout : nullptr;
