@@ -414,9 +414,13 @@ def pass_roofline(pass_ms, pass_bytes, steps):
     return sm_ms, achieved, peak, peak_kind
 
 
+PROFILED = {}  # instrumented step time of the last timed_decompositions call
+
+
 def timed_decompositions(rcp, ctx, X, dcfg, steps, warmup, dist):
     """W untimed + K timed decompositions on the device; device time per step (max over ranks),
     per-pass times of the timed steps, launches, the last model."""
+    ctx.set_option("pass_timing", 0)  # the library default: no instrumentation in the timed region
     for _ in range(warmup):
         model, trace = rcp.decompose(X, dcfg, ctx=ctx)
     ctx.synchronize()
@@ -428,11 +432,25 @@ def timed_decompositions(rcp, ctx, X, dcfg, steps, warmup, dist):
         model, trace = rcp.decompose(X, dcfg, ctx=ctx)
     ctx.event_record(1)
     total_ms = ctx.event_elapsed_ms(0, 1)
-    for name, ms, by in ctx.pass_timings():  # last timed step
-        pass_ms[name] = pass_ms.get(name, 0.0) + ms * steps
-        pass_bytes[name] = pass_bytes.get(name, 0.0) + by * steps
     ctx.synchronize()
     launches = ctx.kernel_launches() - l0
+    dist.barrier()
+    # Per-pass times (the roofline's kernel durations): the same steps again with the library's
+    # per-pass CUDA events on. The ~60 event records cost 0.3 ms per decomposition (C2), so they
+    # stay out of `value`; PROFILED["ms_per_step"] is the instrumented step time.
+    ctx.set_option("pass_timing", 1)
+    for _ in range(min(warmup, 2) + 1):  # (the option change drops the captured graph: call, capture, replay)
+        rcp.decompose(X, dcfg, ctx=ctx)
+    ctx.synchronize()
+    ctx.event_record(4)
+    for _ in range(steps):
+        rcp.decompose(X, dcfg, ctx=ctx)
+    ctx.event_record(5)
+    PROFILED["ms_per_step"] = ctx.event_elapsed_ms(4, 5) / steps
+    for name, ms, by in ctx.pass_timings():  # last profiled step
+        pass_ms[name] = pass_ms.get(name, 0.0) + ms * steps
+        pass_bytes[name] = pass_bytes.get(name, 0.0) + by * steps
+    ctx.set_option("pass_timing", 0)
     dist.barrier()
     return dist.max(total_ms / steps), pass_ms, pass_bytes, launches, model, trace
 
@@ -531,6 +549,7 @@ def main():
     with ClockSampler(local) as clk:
         ms_step, pass_ms, pass_bytes, launches, model, trace = timed_decompositions(
             rcp, ctx, X, dcfg, args.steps, args.warmup, dist)
+        profiled_ms = PROFILED.get("ms_per_step")
 
     # e2e through the C ABI with host buffers (pinned), copies inside the timed region
     e2e = None
@@ -581,7 +600,11 @@ def main():
                        "l2": "tensor larger than L2 (no flush needed)" if cfg.nbytes() > 126e6 else "L2-resident",
                        "omega": "host-evaluated, uploaded" if args.omega_host else "device",
                        "fp32_arith": ("fast 3xTF32" if args.fast_fp32 else "faithful (fp64 products and sums)")
-                       if cfg.dtype == np.float32 else "fp64"},
+                       if cfg.dtype == np.float32 else "fp64",
+                       "pass_events": "off in the timed region (library default); `passes`, `roofline` and "
+                                      "`lu_roofline` from the same number of further steps with the per-pass CUDA "
+                                      "events on (profiled_ms_per_step)"},
+            "profiled_ms_per_step": profiled_ms,
             "gpu_launches": int(launches),
             "roofline": binding_roofline(cfg, pass_ms, pass_bytes, args.steps,
                                          fast_fp32=ctx.get_option("fp32_arith") == 1,

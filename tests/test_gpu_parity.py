@@ -403,6 +403,7 @@ def test_decompose_graph_replay_identical(rcp, oracle, dtype):
     x, _ = oracle.random_lowrank([40, 36, 30], 4, 7, snr=3.0, noise_seed=7)
     x = x.astype(dtype)
     ctx = rcp.Context(0)
+    ctx.set_option("pass_timing", 1)  # the per-pass events ride in the graph as record nodes
     X = rcp.DeviceTensor.upload(x, ctx=ctx)
     g, o = cfgs(rcp, oracle, 4, 5, 2, 5, tol=1e-8 if dtype == np.float64 else 1e-6)
     outs, launches = [], []

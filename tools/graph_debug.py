@@ -7,6 +7,7 @@ import paper_1703_09074_b200 as rcp
 import pyoracle as oracle
 x, _ = oracle.random_lowrank([40, 36, 30], 4, 7, snr=3.0, noise_seed=7)
 ctx = rcp.Context(0)
+ctx.set_option("pass_timing", 1)
 X = rcp.DeviceTensor.upload(x, ctx=ctx)
 cs = oracle.derive_seed(5, oracle.stream_id(1))
 g = rcp.DecomposeConfig(rank=4, tol=1e-8, max_iter=200, seed=5,

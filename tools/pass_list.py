@@ -20,6 +20,7 @@ ap.add_argument("--filter", default="")
 args = ap.parse_args()
 cfg = synthetic.CONFIGS[args.config]
 ctx = rcp.Context(0)
+ctx.set_option("pass_timing", 1)
 w, f = synthetic.model(cfg.kind, cfg.shape, cfg.rank, cfg.seed)
 X = rcp.DeviceTensor.synth(cfg.shape, w, f, cfg.snr, cfg.seed, dtype=cfg.dtype, ctx=ctx)
 cs = rcp.derive_seed(cfg.seed, rcp.stream_id(rcp.COMPRESS))
