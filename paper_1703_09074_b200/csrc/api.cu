@@ -1647,6 +1647,24 @@ void run_decompose(rcpg_context* c, const rcpg_tensor* t, const rcpg_decompose_c
     else if (e == cudaSuccess)
       e = cudaErrorStreamCaptureInvalidated;
     if (e == cudaSuccess) {
+      if (std::getenv("RCPG_GRAPH_DUMP") != nullptr) {  // node census of the captured decomposition
+        size_t nn = 0;
+        cudaGraphGetNodes(graph, nullptr, &nn);
+        std::vector<cudaGraphNode_t> nodes(nn);
+        cudaGraphGetNodes(graph, nodes.data(), &nn);
+        int cnt[16] = {};
+        for (size_t i = 0; i < nn; ++i) {
+          cudaGraphNodeType ty;
+          if (cudaGraphNodeGetType(nodes[i], &ty) == cudaSuccess && int(ty) < 16) ++cnt[int(ty)];
+        }
+        fprintf(stderr, "[rcpg graph] %zu nodes: kernel %d memcpy %d memset %d host %d empty %d wait-event %d record-event %d other %d\n",
+                nn, cnt[cudaGraphNodeTypeKernel], cnt[cudaGraphNodeTypeMemcpy], cnt[cudaGraphNodeTypeMemset],
+                cnt[cudaGraphNodeTypeHost], cnt[cudaGraphNodeTypeEmpty], cnt[cudaGraphNodeTypeWaitEvent],
+                cnt[cudaGraphNodeTypeEventRecord],
+                int(nn) - cnt[cudaGraphNodeTypeKernel] - cnt[cudaGraphNodeTypeMemcpy] - cnt[cudaGraphNodeTypeMemset] -
+                    cnt[cudaGraphNodeTypeHost] - cnt[cudaGraphNodeTypeEmpty] - cnt[cudaGraphNodeTypeWaitEvent] -
+                    cnt[cudaGraphNodeTypeEventRecord]);
+      }
       g.graph = graph;
       g.ready = true;
       g.dfr = dfr;
