@@ -2088,9 +2088,69 @@ void als_start(AlsState* state, double* nx2_src, cudaStream_t st) {
   RCPG_LAUNCHED();
 }
 
+// als_start + zero_factor + the initial weights in one launch (three dependent
+// 3 us kernels before): state reset and t0, factor 0 = zeros (solve.hpp:98) with
+// its Gram, weights = wval (ones for ALS, solve.hpp:190; zeros for BCD, :281).
+template <typename T>
+__global__ void als_prepare_kernel(AlsState* st, const double* nx2, T* F, i64 n, int R, T* gram, T* weights, T wval) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    st->it = 1;
+    st->done = 0;
+    st->converged = 0;
+    st->error_it = -1;
+    st->pivots_fallback = 0;
+    st->prev_fit = 0.0;
+    st->nx2 = nx2[0];
+    st->t0 = now;
+  }
+  if (blockIdx.x == 0)
+    for (int j = threadIdx.x; j < R; j += blockDim.x) weights[j] = wval;
+  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < n * R; e += i64(gridDim.x) * blockDim.x) F[e] = T(0);
+  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < i64(R) * R; e += i64(gridDim.x) * blockDim.x)
+    gram[e] = T(0);
+}
+
+template <typename T>
+void als_prepare(AlsState* state, double* nx2_src, T* factor0, i64 extent0, int rank, T* gram0, T* weights, T wval,
+                 cudaStream_t st) {
+  als_prepare_kernel<T><<<64, 256, 0, st>>>(state, nx2_src, factor0, extent0, rank, gram0, weights, wval);
+  count_launch();
+  RCPG_LAUNCHED();
+}
+
 template <typename T>
 void normalize_model(const FactorSet<T>& fs, T* weights, T* tmp, cudaStream_t st) {
   normalize_kernel<T><<<1, kSmallThreads, 0, st>>>(fs, weights, tmp);
+  count_launch();
+  RCPG_LAUNCHED();
+}
+
+// recover's A_n = Q_n A~_n of every non-identity mode in one launch
+// (blockIdx.y = entry; the per-output sums are small_gemm_kernel's)
+template <typename T>
+__global__ void small_gemm_batch_kernel(SmallGemmBatch<T> b, int rank) {
+  const int q = blockIdx.y;
+  const T* Q = b.Q[q];
+  const T* A = b.A[q];
+  T* out = b.out[q];
+  const i64 dim = b.dim[q], l = b.l[q];
+  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < dim * rank; e += i64(gridDim.x) * blockDim.x) {
+    const i64 i = e % dim, r = e / dim;
+    double s = 0.0;
+    for (i64 c = 0; c < l; ++c) s += double(Q[i + c * dim]) * double(A[c + r * l]);
+    out[e] = T(s);
+  }
+}
+
+template <typename T>
+void small_gemm_batch(const SmallGemmBatch<T>& b, int count, int rank, cudaStream_t st) {
+  if (count <= 0) return;
+  i64 most = 1;
+  for (int q = 0; q < count; ++q) most = std::max(most, b.dim[q] * rank);
+  const int blocks = int(std::max<i64>(1, std::min<i64>(ceil_div(most, 256), 148 * 8)));
+  small_gemm_batch_kernel<T><<<dim3(unsigned(blocks), unsigned(count)), 256, 0, st>>>(b, rank);
   count_launch();
   RCPG_LAUNCHED();
 }
@@ -2238,7 +2298,9 @@ void synth_tensor(const i64* shape, int order, int rank, const double* w_dev, co
   template bool als_loop_supported<T>(const i64*, int, int);                                                  \
   template void als_loop<T>(const T*, const i64*, int, const FactorSet<T>&, T*, double, int, double*, double*, \
                             AlsState*, double*, i64, GridBarrier*, cudaStream_t, unsigned long long*);                                \
-  template void small_gemm<T>(const T*, i64, i64, const T*, int, T*, cudaStream_t);                           \
+  template void small_gemm<T>(const T*, i64, i64, const T*, int, T*, cudaStream_t); \
+  template void als_prepare<T>(AlsState*, double*, T*, i64, int, T*, T*, T, cudaStream_t); \
+  template void small_gemm_batch<T>(const SmallGemmBatch<T>&, int, int, cudaStream_t);                           \
   template void norm_and_finite<T>(const T*, i64, double*, double*, int, cudaStream_t, const double*);       \
   template void nonfinite_flag<T>(const T*, i64, double*, cudaStream_t);                                      \
   template void residual_norms<T>(const T*, const i64*, int, const FactorSet<T>&, const T*, double*, double*, \

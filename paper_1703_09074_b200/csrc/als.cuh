@@ -77,6 +77,9 @@ void als_update(const FactorSet<T>& fs, int mode, const T* W, T* weights, double
 
 void als_start(AlsState* state, double* nx2_src, cudaStream_t st);
 template <typename T>
+void als_prepare(AlsState* state, double* nx2_src, T* factor0, i64 extent0, int rank, T* gram0, T* weights, T wval,
+                 cudaStream_t st);
+template <typename T>
 void fill_ones(T* p, int n, cudaStream_t st);
 
 // The whole ALS iteration loop as one cooperative kernel (when the mode
@@ -95,6 +98,15 @@ void normalize_model(const FactorSet<T>& fs, T* weights, T* tmp, cudaStream_t st
 // out = Q (dim x l) * A (l x rank), column-major (recover, kruskal.hpp:198-220).
 template <typename T>
 void small_gemm(const T* Q, i64 dim, i64 l, const T* A, int rank, T* out, cudaStream_t st);
+template <typename T>
+struct SmallGemmBatch {
+  const T* Q[kMaxOrder];
+  const T* A[kMaxOrder];
+  T* out[kMaxOrder];
+  i64 dim[kMaxOrder], l[kMaxOrder];
+};
+template <typename T>
+void small_gemm_batch(const SmallGemmBatch<T>& b, int count, int rank, cudaStream_t st);
 
 // Sum of squares (double) and count of non-finite entries of a device array.
 template <typename T>

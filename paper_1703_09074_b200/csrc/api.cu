@@ -1238,10 +1238,11 @@ AlsHandles<T> run_als(rcpg_context* c, const T* B, const i64* shape, int order, 
   h.tsec = h.tfit + cfg.max_iter;
   h.max_iter = cfg.max_iter;
 
-  als_start(h.state, slots(c) + kBSum, c->st);
   {
     ScopedPass sp(c, "als_init", 0.0);
-    zero_factor<T>(h.fs.f[0], shape[0], R, h.fs.gram[0], c->st);
+    // state reset, factor 0 = zeros, weights = ones (ALS) / zeros (BCD, Vector::Zero(rank), solve.hpp:281)
+    als_prepare<T>(h.state, slots(c) + kBSum, h.fs.f[0], shape[0], R, h.fs.gram[0], h.weights,
+                   cfg.method == RCPG_BCD ? T(0) : T(1), c->st);
     // every Gram first (each a slice of als_w), then all eigenproblems in one launch
     i64 gram_elems = 0, work_doubles = 0;
     for (int m = 1; m < order; ++m) {
@@ -1287,10 +1288,6 @@ AlsHandles<T> run_als(rcpg_context* c, const T* B, const i64* shape, int order, 
       woff += i64(init_work_doubles(int(shape[m])));
     }
     if (order > 1) init_factors_from_grams<T>(ib, order - 1, R, cfg.seed, cfg.init, c->st);
-    if (cfg.method == RCPG_BCD)  // Vector::Zero(rank) (solve.hpp:281)
-      RCPG_CUDA(cudaMemsetAsync(h.weights, 0, size_t(R) * sizeof(T), c->st));
-    else
-      fill_ones<T>(h.weights, R, c->st);
   }
   if (cfg.method == RCPG_BCD) {
     // bcd_solve (solve.hpp:264-376): one cooperative launch
@@ -1509,6 +1506,8 @@ void enqueue_decompose(rcpg_context* c, const rcpg_tensor* t, const rcpg_decompo
   {
     ScopedPass sp(c, "recover", 0.0);
     i64 off = 0;
+    SmallGemmBatch<T> gb{};
+    int ngb = 0;
     for (int m = 0; m < t->order; ++m) {
       T* dst = c->recov.as<T>() + off;
       const BasisRec& b = comp.bases[m];
@@ -1517,12 +1516,18 @@ void enqueue_decompose(rcpg_context* c, const rcpg_tensor* t, const rcpg_decompo
         RCPG_CUDA(cudaMemcpyAsync(dst, h.fs.f[m], sizeof(T) * h.fs.extent[m] * R, cudaMemcpyDeviceToDevice, c->st));
       } else {
         if (b.cols != h.fs.extent[m]) fail_after(c, dfr, "recover: basis columns must match the compressed extent");
-        small_gemm<T>(b.q.as<T>(), b.dim, b.cols, h.fs.f[m], R, dst, c->st);
+        gb.Q[ngb] = b.q.as<T>();
+        gb.A[ngb] = h.fs.f[m];
+        gb.out[ngb] = dst;
+        gb.dim[ngb] = b.dim;
+        gb.l[ngb] = b.cols;
+        ++ngb;
       }
       big.f[m] = dst;
       big.extent[m] = t->gshape(m);
       off += t->gshape(m) * R;
     }
+    small_gemm_batch<T>(gb, ngb, R, c->st);  // every non-identity mode in one launch
     c->small_tmp.ensure(size_t(sum_ext * R + R) * sizeof(T));
     normalize_model<T>(big, h.weights, c->small_tmp.as<T>(), c->st);
   }

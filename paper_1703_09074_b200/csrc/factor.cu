@@ -1585,7 +1585,7 @@ struct QrArgs {
   T* Q;        // output panel J x r
   i64 J, R;
   int n, r;
-  const i64* krow;  // [J] Kolda row index
+  i64* krow;        // [J] Kolda row index (filled by the kernel: every CTA reads only its own rows)
   KoldaMap km;
   double* part;     // [2][G][kMaxPanelCols + 1]
   T* tau;           // [r]
@@ -1609,6 +1609,13 @@ __global__ void __launch_bounds__(kFacThreads) householder_kernel(QrArgs<T> p) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const i64 R = p.R;
   int phase = 0;
+  // row keys of this CTA's rows (no separate launch: the kernel is a skipped
+  // fallback after CholeskyQR2 in the common case)
+  for (i64 s = r0 + threadIdx.x; s < r1; s += blockDim.x) {
+    const i64 a = s / R, b = s - a * R;
+    p.krow[s] = kolda_index(p.km, a, b);
+  }
+  __syncthreads();
 
   for (int k = 0; k < p.r; ++k) {
     const i64 sk = kolda_inverse(p.km, k, p.R);
@@ -3094,7 +3101,6 @@ int thin_qr(T* A, T* Q, i64 J, i64 R, int n, const KoldaMap& km, FactorWork& w, 
       return r;
     }
   }
-  init_row_keys(km, J, R, w.keys, st);
   const int maxc = max_coop_blocks(householder_kernel<T>, kFacThreads, 0);
   const int G = std::min(pick_grid(J, n, maxc), w.max_blocks);
   QrArgs<T> a{A,     Q,      J, R, n, r, w.keys, km, w.part, reinterpret_cast<T*>(w.tau), reinterpret_cast<T*>(w.diag),
