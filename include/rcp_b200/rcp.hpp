@@ -389,7 +389,7 @@ BoundReport theorem_bound(const Tensor<S>& t, Index k, Index p) {
 template <typename S>
 BoundReport validate_bound(const Tensor<S>& dense, Index k, Index p, int trials, std::uint64_t seed);
 
-// Library options (include/rcpg.h rcpg_set_option): "fp32_arith", "omega_host".
+// Library options (include/rcpg.h rcpg_set_option): "fp32_arith", "omega_host", "pass_timing".
 inline void set_option(const char* name, std::int64_t value) {
   rcpg_context* c = detail::context();
   detail::check(c, rcpg_set_option(c, name, value));

@@ -203,7 +203,8 @@ class Context:
     # options (include/rcpg.h rcpg_set_option) ---------------------------
     def set_option(self, name: str, value: int) -> None:
         """"fp32_arith": 0 faithful fp64 arithmetic (default) / 1 fast 3xTF32;
-        "omega_host": 0 device Omega (default) / 1 host-evaluated, uploaded (bit-identical)."""
+        "omega_host": 0 device Omega (default) / 1 host-evaluated, uploaded (bit-identical);
+        "pass_timing": 0 no per-pass events (default) / 1 events on, read with pass_timings()."""
         self.check(self.lib.rcpg_set_option(self.h, name.encode(), int(value)))
 
     def get_option(self, name: str) -> int:
