@@ -418,7 +418,7 @@ __global__ void omega_pairs_kernel(u64 s0, KoldaMap km, i64 J, i64 R, i64 cols, 
     const i64 j = kolda_index(km, a, b);
     T* d1 = P + a * cols * R + b;
     T* d2 = P + a2 * cols * R + b2;
-    for (i64 c = 0; c < cols; ++c) {
+    for (i64 c = blockIdx.y; c < cols; c += gridDim.y) {  // column groups: small panels spread over the SMs
       double cs, sn;
       normal_pair(s0, (u64(c) * u64(Jg) + u64(j)) >> 1, cs, sn);
       d1[c * R] = T(TV(cs));
@@ -455,7 +455,12 @@ void omega_panel_impl(u64 seed, i64 mode, const KoldaMap& km, ModeView v, i64 co
                      !(km.n_low == 0 && km.n_high == 1 && km.high_last_off % 2 != 0);
   if (pairs) {
     const int blocks = int(std::max<i64>(1, std::min<i64>(ceil_div(J / 2, 256), 148 * 16)));
-    omega_pairs_kernel<T, TV><<<blocks, 256, 0, st>>>(s0, km, J, v.R, cols, P, Jg, sig, Ef);
+    // a thread evaluates its row pair's columns one after the other (a chain of
+    // fp64 log / sincos): panels with few rows get column groups in grid.y until
+    // ~8 CTAs per SM are in flight (C2 mode 0: 313 x 4 CTAs instead of 313)
+    const int ygroups = int(std::max<i64>(1, std::min<i64>(cols, ceil_div(i64(148) * 8, i64(blocks)))));
+    omega_pairs_kernel<T, TV><<<dim3(unsigned(blocks), unsigned(ygroups)), 256, 0, st>>>(s0, km, J, v.R, cols, P, Jg,
+                                                                                       sig, Ef);
     count_launch();
     RCPG_LAUNCHED();
     return;
