@@ -290,8 +290,10 @@ struct Deferred {
   bool als_input = false;       // solve.hpp:139-141
   bool relerr = false;          // kruskal.hpp:190-191
 };
-void raise_deferred(rcpg_context* c, const Deferred& d) {
-  const double* h = read_slots(c);
+// the deferred checks on slots already read back (one D2H + sync per call site)
+void check_deferred(const double* h, const Deferred& d);
+void raise_deferred(rcpg_context* c, const Deferred& d) { check_deferred(read_slots(c), d); }
+void check_deferred(const double* h, const Deferred& d) {
   if (d.compress_input) check_arg(h[kXBad] == 0.0, "compress: input values must be finite");
   if (d.als_input) {
     if (h[kBBad] != 0.0) throw SolverFailure("solve: input values are not finite", 0);
@@ -1489,12 +1491,12 @@ void finish_decompose(rcpg_context* c, const AlsHandles<T>& h, const FactorSet<T
   const AlsState& hs = *reinterpret_cast<const AlsState*>(hb + o_state);
   const double* fit = reinterpret_cast<const double*>(hb + o_fit);
   const double* sec = reinterpret_cast<const double*>(hb + o_sec);
-  raise_deferred(c, Deferred{dfr.compress_input, dfr.als_input, false});  // syncs the stream
+  const double* hsl = read_slots(c);  // syncs the stream: the slots and the staging buffer are complete
+  check_deferred(hsl, Deferred{dfr.compress_input, dfr.als_input, false});
   if (hs.error_it > 0) throw SolverFailure("als: fit became non-finite", hs.error_it);
-  raise_deferred(c, Deferred{false, false, dfr.relerr});
+  check_deferred(hsl, Deferred{false, false, dfr.relerr});
   if (res->weights) std::memcpy(res->weights, hb + o_w, sizeof(T) * size_t(R));
   if (res->factors) std::memcpy(res->factors, hb + o_f, sizeof(T) * size_t(fel));
-  const double* hsl = c->hslots;
   const int iters = hs.it - 1;
   const int n = std::min(iters, cap);
   for (int i = 0; i < n; ++i) {

@@ -484,11 +484,11 @@ def decompose(t, cfg: DecomposeConfig, ctx: Optional[Context] = None) -> Tuple[K
         c, keep = cfg._c()
         R = max(int(cfg.rank), 1)
         cap = max(int(cfg.max_iter), 1)
-        w = np.zeros(R, dtype=dt.dtype)
-        f = np.zeros(sum(dt.global_shape) * R, dtype=dt.dtype)
-        ti = np.zeros(cap, dtype=np.int32)
-        tf = np.zeros(cap, dtype=np.float64)
-        ts = np.zeros(cap, dtype=np.float64)
+        w = np.empty(R, dtype=dt.dtype)  # (every entry read below is written by the call)
+        f = np.empty(sum(dt.global_shape) * R, dtype=dt.dtype)
+        ti = np.empty(cap, dtype=np.int32)
+        tf = np.empty(cap, dtype=np.float64)
+        ts = np.empty(cap, dtype=np.float64)
         res = _L.ResultC()
         res.weights = w.ctypes.data
         res.factors = f.ctypes.data
