@@ -1935,8 +1935,22 @@ void rcpg_destroy(rcpg_context* c) {
 const char* rcpg_last_error(const rcpg_context* c) { return c ? c->err.c_str() : "no context"; }
 int32_t rcpg_last_error_iteration(const rcpg_context* c) { return c ? c->err_it : -1; }
 
+namespace {
+// sync = false: the copy is only enqueued (rcpg_decompose_host: the decomposition
+// follows on the same stream and the call synchronizes at its end, so the host
+// buffer stays valid for the copy and the GPU never waits on a host round trip)
+rcpg_status tensor_upload_impl(rcpg_context* c, rcpg_dtype dtype, int32_t order, const int64_t* shape,
+                               const void* host, rcpg_tensor** out, bool sync);
+}  // namespace
+
 rcpg_status rcpg_tensor_upload(rcpg_context* c, rcpg_dtype dtype, int32_t order, const int64_t* shape,
                                const void* host, rcpg_tensor** out) {
+  return tensor_upload_impl(c, dtype, order, shape, host, out, true);
+}
+
+namespace {
+rcpg_status tensor_upload_impl(rcpg_context* c, rcpg_dtype dtype, int32_t order, const int64_t* shape,
+                               const void* host, rcpg_tensor** out, bool sync) {
   return guarded(c, [&] {
     validate_tensor_args(dtype, order, shape);
     auto t = std::make_unique<rcpg_tensor>();
@@ -1959,10 +1973,11 @@ rcpg_status rcpg_tensor_upload(rcpg_context* c, rcpg_dtype dtype, int32_t order,
     }
     t->owned = true;
     RCPG_CUDA(cudaMemcpyAsync(t->d, host, bytes, cudaMemcpyHostToDevice, c->st));
-    RCPG_CUDA(cudaStreamSynchronize(c->st));
+    if (sync) RCPG_CUDA(cudaStreamSynchronize(c->st));
     *out = t.release();
   });
 }
+}  // namespace
 
 rcpg_status rcpg_tensor_wrap_device(rcpg_context* c, rcpg_dtype dtype, int32_t order, const int64_t* shape,
                                     void* device_ptr, rcpg_tensor** out) {
@@ -2073,9 +2088,11 @@ rcpg_status rcpg_decompose(rcpg_context* c, const rcpg_tensor* t, const rcpg_dec
 rcpg_status rcpg_decompose_host(rcpg_context* c, rcpg_dtype dtype, int32_t order, const int64_t* shape,
                                 const void* host, const rcpg_decompose_config* cfg, rcpg_result* res) {
   rcpg_tensor* t = nullptr;
-  rcpg_status s = rcpg_tensor_upload(c, dtype, order, shape, host, &t);
+  rcpg_status s = tensor_upload_impl(c, dtype, order, shape, host, &t, /*sync=*/false);
   if (s != RCPG_OK) return s;
   s = rcpg_decompose(c, t, cfg, res);
+  // an early error return may leave the copy in flight: the host buffer is the caller's again on return
+  if (s != RCPG_OK) cudaStreamSynchronize(c->st);
   rcpg_tensor_free(t);
   return s;
 }

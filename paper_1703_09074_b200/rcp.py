@@ -368,6 +368,15 @@ def slab_range(extent: int, nranks: int, rank: int) -> Tuple[int, int]:
     return lo.value, hi.value
 
 
+class _HostTensor:
+    """A host array handed to rcpg_decompose_host (shape / dtype views like DeviceTensor's)."""
+
+    def __init__(self, x: np.ndarray):
+        self.x = x
+        self.dtype = x.dtype
+        self.global_shape = tuple(int(e) for e in x.shape)
+
+
 def _as_device(x, ctx):
     if isinstance(x, DeviceTensor):
         return x, False
@@ -479,7 +488,13 @@ def decompose(t, cfg: DecomposeConfig, ctx: Optional[Context] = None) -> Tuple[K
     """rcp::decompose (solve.hpp:381-398) on the GPU. `t` is a numpy array
     (copied to HBM inside the call) or a DeviceTensor already in HBM."""
     ctx = ctx or default_context()
-    dt, tmp = _as_device(t, ctx)
+    if not isinstance(t, DeviceTensor):
+        # host tensor: rcpg_decompose_host (the upload is enqueued in front of the decomposition,
+        # one synchronization at the end of the call)
+        x = np.ascontiguousarray(np.asarray(t))
+        dt, tmp = _HostTensor(x), False
+    else:
+        dt, tmp = t, False
     try:
         c, keep = cfg._c()
         R = max(int(cfg.rank), 1)
@@ -496,7 +511,12 @@ def decompose(t, cfg: DecomposeConfig, ctx: Optional[Context] = None) -> Tuple[K
         res.trace_fit = tf.ctypes.data_as(C.POINTER(C.c_double))
         res.trace_seconds = ts.ctypes.data_as(C.POINTER(C.c_double))
         res.trace_capacity = cap
-        ctx.check(ctx.lib.rcpg_decompose(ctx.h, dt.h, C.byref(c), C.byref(res)))
+        if isinstance(dt, _HostTensor):
+            shape = np.asarray(dt.x.shape, dtype=np.int64)
+            ctx.check(ctx.lib.rcpg_decompose_host(ctx.h, _dtype_code(dt.dtype), dt.x.ndim, shape.ctypes.data,
+                                                  dt.x.ctypes.data, C.byref(c), C.byref(res)))
+        else:
+            ctx.check(ctx.lib.rcpg_decompose(ctx.h, dt.h, C.byref(c), C.byref(res)))
         facs, off = [], 0
         for e in dt.global_shape:
             facs.append(f[off:off + e * R].reshape((e, R), order="F").copy(order="F"))
