@@ -229,8 +229,8 @@ std::pair<Kruskal<S>, FitTrace> decompose(const Tensor<S>& t, const DecomposeCon
   res.trace_fit = fit.data();
   res.trace_seconds = sec.data();
   res.trace_capacity = cap;
-  detail::DeviceTensor dt(c, t);
-  detail::check(c, rcpg_decompose(c, dt.t, &d, &res));
+  // the upload is enqueued in front of the decomposition (one synchronization, at the end of the call)
+  detail::check(c, rcpg_decompose_host(c, detail::dtype<S>(), int32_t(t.order()), t.shape().data(), t.data(), &d, &res));
   Kruskal<S> model;
   model.weights = w;
   Index off = 0;
